@@ -1,0 +1,178 @@
+/*
+ * screenbem_b200 — C ABI of the B200 (sm_100a) hot path of the screenbem
+ * reference (arXiv 2310.09204): dense Galerkin assembly of the Laplace
+ * hypersingular operator on multiscreens, Schwarz-preconditioned CG.
+ *
+ * The reference is a header-only C++ library (proj/include/screenbem) with no
+ * FFI; each entry point below replaces the reference function cited next to
+ * it, with plain pointers and sizes.  The C++ wrappers in
+ * include/screenbem/ headers restore the reference's C++ names and exceptions.
+ *
+ * Conventions
+ *   - Every function returns SBG_OK (0) or an error code; sbg_last_error()
+ *     gives the message (thread-local).  SBG_EVALIDATION mirrors the
+ *     reference's ValidationError (CLI exit 2), SBG_ENUMERICAL its
+ *     NumericalError (CLI exit 3) (inc/common.hpp:16-26).
+ *   - The caller owns host buffers; opaque handles own host or device memory
+ *     and are released with the matching *_destroy.
+ *   - One CUDA stream per context; calls on one context must not overlap.
+ *   - Dense matrices are exchanged row-major n x n (W is symmetric).
+ *   - The GPU path has no CPU fallback: without a usable sm_100a device every
+ *     device entry point fails with SBG_ECUDA.
+ */
+#ifndef SCREENBEM_B200_H
+#define SCREENBEM_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SBG_OK 0
+#define SBG_EVALIDATION 2 /* ValidationError (inc/common.hpp:17-20) */
+#define SBG_ENUMERICAL 3  /* NumericalError  (inc/common.hpp:23-26) */
+#define SBG_ECUDA 4       /* device / runtime failure */
+#define SBG_EINTERNAL 5
+
+typedef struct sbg_ctx sbg_ctx;
+typedef struct sbg_mesh sbg_mesh;           /* SurfaceMesh      (inc/mesh.hpp:19-83) */
+typedef struct sbg_level sbg_level;         /* MeshLevelPair    (inc/mesh.hpp:86-92) */
+typedef struct sbg_inflated sbg_inflated;   /* InflatedMesh     (inc/inflate.hpp:48-76) */
+typedef struct sbg_matrix sbg_matrix;       /* GalerkinMatrix   (inc/assemble.hpp:12), device-resident */
+typedef struct sbg_partition sbg_partition; /* DofPartition     (inc/schwarz.hpp:14-17) */
+typedef struct sbg_prolong sbg_prolong;     /* Prolongation     (inc/jump.hpp:87-89) */
+typedef struct sbg_prec sbg_prec;           /* SchwarzPreconditioner (inc/schwarz.hpp:55-73), device-resident */
+
+/* QuadratureConfig (inc/quadrature.hpp:12-16) */
+typedef struct {
+    int far_order;         /* 4 */
+    int singular_order;    /* 8 */
+    double near_threshold; /* 2.0 */
+} sbg_quad_cfg;
+
+/* PcgReport (inc/pcg.hpp:9-16) */
+typedef struct {
+    int iterations;
+    int converged;
+    double kappa_estimate;
+    int history_len; /* iterations + 1 residual norms */
+} sbg_pcg_report;
+
+/* assembly work counters (roofline bookkeeping) */
+typedef struct {
+    long long far_pairs, near_pairs, identical, edge, vertex, near_leaves, tiles, tiles_skipped;
+} sbg_assembly_stats;
+
+const char* sbg_last_error(void);
+const char* sbg_version(void);
+
+/* ---- device context ---------------------------------------------------- */
+int sbg_ctx_create(int device, sbg_ctx** out);
+void sbg_ctx_destroy(sbg_ctx* ctx);
+int sbg_ctx_synchronize(sbg_ctx* ctx);
+int sbg_device_name(int device, char* buf, int cap, int* sm_count);
+/* named CUDA-event timers on the context stream */
+int sbg_timers_enable(sbg_ctx* ctx, int on);
+int sbg_timers_reset(sbg_ctx* ctx);
+int sbg_timer_get(sbg_ctx* ctx, const char* name, double* total_ms, long long* count);
+
+/* ---- meshes (host) ------------------------------------------------------ */
+int sbg_mesh_create(int nv, const double* verts, int nf, const int32_t* facets, sbg_mesh** out);
+void sbg_mesh_destroy(sbg_mesh* m);
+int sbg_mesh_sizes(const sbg_mesh* m, int* nv, int* nf);
+int sbg_mesh_export(const sbg_mesh* m, double* verts, int32_t* facets);
+int sbg_validate_mesh(const sbg_mesh* m);                     /* inc/mesh.hpp:238-272 */
+int sbg_make_builtin(const char* spec, sbg_mesh** out);        /* inc/mesh.hpp:516-537 ("bowtie[:k]") */
+int sbg_refine_uniform_times(const sbg_mesh* m, int k, sbg_level** out); /* inc/mesh.hpp:388-405 */
+int sbg_level_create(const sbg_mesh* coarse, const sbg_mesh* fine, const int32_t* parent, sbg_level** out);
+int sbg_make_config(int cfg, int ratio, sbg_level** out);      /* BASELINE.json configs 1-5 (ratio 0 = default H/h) */
+int sbg_make_panels(int kind, int m, int r, sbg_level** out);  /* 0 flat, 1 T-junction, 2 triple cross */
+int sbg_level_mesh(const sbg_level* l, int fine, sbg_mesh** out); /* copy of the coarse (0) / fine (1) mesh */
+int sbg_level_parent(const sbg_level* l, int32_t* parent);
+int sbg_level_sizes(const sbg_level* l, double* H, double* h);
+void sbg_level_destroy(sbg_level* l);
+
+/* ---- inflation / DOF numbering (host) ------------------------------------ */
+int sbg_inflate(const sbg_mesh* m, int validate, sbg_inflated** out); /* inc/inflate.hpp:98-288 */
+void sbg_inflated_destroy(sbg_inflated* im);
+int sbg_inflated_sizes(const sbg_inflated* im, int* n_dofs, int* n_gvertices, int* nv, int* nf);
+/* q[nv], gv_first[nv], dof_first[nv], ofacet_branch[2nf*3], jump_dofs[2n], normals[2nf*3] (nullable) */
+int sbg_inflated_export(const sbg_inflated* im, int32_t* q, int32_t* gv_first, int32_t* dof_first,
+                        int32_t* ofacet_branch, int32_t* jump_dofs, double* normals);
+
+/* ---- Galerkin matrix (device) -------------------------------------------- */
+/* assemble_W (inc/assemble.hpp:72-139); `workers` is accepted and ignored */
+int sbg_assemble_w(sbg_ctx* ctx, const sbg_inflated* im, const sbg_quad_cfg* cfg, int workers, sbg_matrix** out,
+                   sbg_assembly_stats* stats);
+int sbg_matrix_create(sbg_ctx* ctx, int n, const double* host_rowmajor, sbg_matrix** out);
+int sbg_matrix_n(const sbg_matrix* W);
+int sbg_matrix_download(const sbg_matrix* W, double* host_rowmajor);
+int sbg_matrix_download_rows(const sbg_matrix* W, const int32_t* rows, int nrows, double* host);
+int sbg_matrix_symmetry_defect(const sbg_matrix* W, double* max_abs);
+int sbg_matvec(sbg_ctx* ctx, const sbg_matrix* W, const double* x_host, double* y_host);
+void sbg_matrix_destroy(sbg_matrix* W);
+/* dump_matrix_binary / load_matrix_binary (inc/assemble.hpp:191-226): "SBEMW\0" header */
+int sbg_matrix_dump_binary(const sbg_matrix* W, const char* path);
+int sbg_matrix_load_binary(sbg_ctx* ctx, const char* path, sbg_matrix** out);
+
+/* pair_integral (inc/quadrature.hpp:268-334) on the device for explicit pairs */
+int sbg_pair_integrals(sbg_ctx* ctx, const sbg_mesh* m, const sbg_quad_cfg* cfg, const int32_t* f, const int32_t* g,
+                       long long npairs, double* out);
+
+/* assemble_rhs (inc/assemble.hpp:143-184): g constant (g_is_field = 0, 3 doubles) or
+ * sampled at the nf*16 points of sbg_rhs_points (g_is_field = 1, 3 per point) */
+int sbg_rhs_points(const sbg_inflated* im, const sbg_quad_cfg* cfg, double* pts);
+int sbg_assemble_rhs(sbg_ctx* ctx, const sbg_inflated* im, const sbg_quad_cfg* cfg, const double* g, int g_is_field,
+                     double* L);
+
+/* ---- partition / prolongation (host) ------------------------------------ */
+int sbg_partition_dofs(const sbg_level* pair, const sbg_inflated* fine, sbg_partition** out); /* schwarz.hpp:19-51 */
+int sbg_partition_create(int nfaces, const int32_t* face_ids, const int32_t* face_ptr, const int32_t* face_dofs,
+                         int nwb, const int32_t* wb, sbg_partition** out);
+int sbg_partition_sizes(const sbg_partition* p, int* nfaces, int* nface_dofs, int* nwb);
+int sbg_partition_export(const sbg_partition* p, int32_t* face_ids, int32_t* face_ptr, int32_t* face_dofs,
+                         int32_t* wb);
+void sbg_partition_destroy(sbg_partition* p);
+int sbg_build_prolongation(const sbg_level* pair, const sbg_inflated* coarse, const sbg_inflated* fine,
+                           sbg_prolong** out); /* inc/jump.hpp:118-185 */
+int sbg_prolong_create(int rows, int cols, const int32_t* col_ptr, const int32_t* row_idx, const double* val,
+                       sbg_prolong** out);
+int sbg_prolong_sizes(const sbg_prolong* p, int* rows, int* cols, int* nnz);
+int sbg_prolong_export(const sbg_prolong* p, int32_t* col_ptr, int32_t* row_idx, double* val);
+void sbg_prolong_destroy(sbg_prolong* p);
+
+/* ---- Schwarz preconditioner (device) -------------------------------------- */
+int sbg_build_preconditioner(sbg_ctx* ctx, const sbg_matrix* W, const sbg_partition* part, const sbg_prolong* R,
+                             sbg_prec** out); /* inc/schwarz.hpp:100-118 */
+int sbg_apply_preconditioner(sbg_ctx* ctx, sbg_prec* p, const double* r_host, int n, double* z_host); /* :121-140 */
+int sbg_prec_num_subspaces(const sbg_prec* p);
+int sbg_prec_block_diag(sbg_ctx* ctx, sbg_prec* p, int which, double* diag, int* n_out); /* which: face, -1 WB, -2 coarse */
+int sbg_coarse_matrix(sbg_ctx* ctx, const sbg_matrix* W, const sbg_prolong* R, double* H);
+double sbg_prec_factor_bytes(const sbg_prec* p);
+void sbg_prec_destroy(sbg_prec* p);
+
+/* ---- PCG (device) --------------------------------------------------------- */
+/* pcg (inc/pcg.hpp:33-116); prec nullable.  history/alphas/betas have hist_cap
+ * entries (maxit+1 suffices; nullable).  rhs and x are host buffers. */
+int sbg_pcg(sbg_ctx* ctx, const sbg_matrix* W, sbg_prec* prec, const double* rhs, int n, double tol, int maxit,
+            double* x, double* history, double* alphas, double* betas, int hist_cap, sbg_pcg_report* rep);
+
+/* ---- device-resident benchmarking helpers (inputs already in HBM) --------- */
+int sbg_device_alloc(sbg_ctx* ctx, long long bytes, void** dptr);
+int sbg_device_free(void* dptr);
+int sbg_memcpy_h2d(sbg_ctx* ctx, void* dst, const void* src, long long bytes);
+int sbg_memcpy_d2h(sbg_ctx* ctx, void* dst, const void* src, long long bytes);
+int sbg_pcg_device(sbg_ctx* ctx, const sbg_matrix* W, sbg_prec* prec, const double* d_rhs, double tol, int maxit,
+                   double* d_x, sbg_pcg_report* rep);
+/* y = W x repeated `reps` times on device vectors; per-launch time via timers ("gemv_f64") */
+int sbg_matvec_device(sbg_ctx* ctx, const sbg_matrix* W, const double* d_x, double* d_y, int reps);
+int sbg_apply_preconditioner_device(sbg_ctx* ctx, sbg_prec* p, const double* d_r, double* d_z, int reps);
+/* write a buffer larger than L2 (L2 flush between timed iterations) */
+int sbg_l2_flush(sbg_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SCREENBEM_B200_H */

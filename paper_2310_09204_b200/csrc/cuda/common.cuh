@@ -1,0 +1,114 @@
+// Shared device-side infrastructure for the sm_100a screenbem path.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../host/host.hpp"
+
+namespace sbg {
+
+#define SBG_CUDA(call)                                                                              \
+    do {                                                                                            \
+        cudaError_t _e = (call);                                                                    \
+        if (_e != cudaSuccess)                                                                      \
+            throw ::sbg::CudaError(std::string(#call) + ": " + cudaGetErrorString(_e) + " (" __FILE__ \
+                                   ":" + std::to_string(__LINE__) + ")");                           \
+    } while (0)
+
+#define SBG_LAUNCH_CHECK() SBG_CUDA(cudaGetLastError())
+
+constexpr int kNumSMs = 148;  // B200 (2 dies x 74); queried at runtime as well
+
+// Device buffer owned by the host object (RAII, stream-ordered free not needed:
+// objects are destroyed after a context synchronize).
+template <class T>
+struct DBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    DBuf() = default;
+    explicit DBuf(size_t count) { alloc(count); }
+    DBuf(const DBuf&) = delete;
+    DBuf& operator=(const DBuf&) = delete;
+    DBuf(DBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+    DBuf& operator=(DBuf&& o) noexcept
+    {
+        if (this != &o) {
+            release();
+            p = o.p;
+            n = o.n;
+            o.p = nullptr;
+            o.n = 0;
+        }
+        return *this;
+    }
+    ~DBuf() { release(); }
+    void alloc(size_t count)
+    {
+        release();
+        n = count;
+        if (count) SBG_CUDA(cudaMalloc(&p, count * sizeof(T)));
+    }
+    void release()
+    {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    void upload(const T* h, size_t count, cudaStream_t s)
+    {
+        if (count > n) alloc(count);
+        if (count) SBG_CUDA(cudaMemcpyAsync(p, h, count * sizeof(T), cudaMemcpyHostToDevice, s));
+    }
+    void upload(const std::vector<T>& h, cudaStream_t s) { upload(h.data(), h.size(), s); }
+};
+
+// Named CUDA-event timers on the context stream (bench / roofline evidence).
+struct Timers {
+    struct Pending {
+        std::string name;
+        cudaEvent_t a, b;
+    };
+    bool enabled = false;
+    std::vector<Pending> pending;
+    std::vector<cudaEvent_t> pool;
+    std::vector<std::pair<std::string, std::pair<double, long long>>> totals;
+    cudaEvent_t get();
+    void collect();  // synchronizes on the pending events
+    void reset();
+    ~Timers();
+};
+
+struct Ctx {
+    int device = 0;
+    int sm_count = kNumSMs;
+    cudaStream_t stream = nullptr;
+    Timers timers;
+    ~Ctx();
+};
+
+// RAII scope that records a named interval on the context stream when timing is on.
+struct TimedScope {
+    Ctx* ctx;
+    const char* name;
+    cudaEvent_t a = nullptr;
+    TimedScope(Ctx* c, const char* n);
+    ~TimedScope();
+};
+
+// Dense symmetric fp64 matrix resident in HBM (GalerkinMatrix, assemble.hpp:12).
+// Row-major with a leading dimension padded to 32 doubles (256-byte rows) so
+// every row starts 16-byte aligned for 128-bit streaming loads; the padding
+// is kept at zero.
+struct DMatrix {
+    Ctx* ctx = nullptr;
+    int n = 0;
+    int ld = 0;
+    DBuf<double> a;
+    static int padded_ld(int n) { return ((n + 31) / 32) * 32; }
+};
+
+}  // namespace sbg

@@ -1,0 +1,198 @@
+// Context, timers and dense-matrix utilities.
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace sbg {
+
+cudaEvent_t Timers::get()
+{
+    if (!pool.empty()) {
+        cudaEvent_t e = pool.back();
+        pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    SBG_CUDA(cudaEventCreate(&e));
+    return e;
+}
+
+void Timers::collect()
+{
+    for (auto& p : pending) {
+        SBG_CUDA(cudaEventSynchronize(p.b));
+        float ms = 0;
+        SBG_CUDA(cudaEventElapsedTime(&ms, p.a, p.b));
+        bool found = false;
+        for (auto& t : totals)
+            if (t.first == p.name) {
+                t.second.first += ms;
+                t.second.second += 1;
+                found = true;
+            }
+        if (!found) totals.push_back({p.name, {ms, 1}});
+        pool.push_back(p.a);
+        pool.push_back(p.b);
+    }
+    pending.clear();
+}
+
+void Timers::reset()
+{
+    collect();
+    totals.clear();
+}
+
+Timers::~Timers()
+{
+    for (auto& p : pending) {
+        cudaEventDestroy(p.a);
+        cudaEventDestroy(p.b);
+    }
+    for (auto e : pool) cudaEventDestroy(e);
+}
+
+Ctx::~Ctx()
+{
+    if (stream) {
+        cudaStreamSynchronize(stream);
+        cudaStreamDestroy(stream);
+    }
+}
+
+TimedScope::TimedScope(Ctx* c, const char* n) : ctx(c), name(n)
+{
+    if (ctx && ctx->timers.enabled) {
+        a = ctx->timers.get();
+        SBG_CUDA(cudaEventRecord(a, ctx->stream));
+    }
+}
+
+TimedScope::~TimedScope()
+{
+    if (a) {
+        cudaEvent_t b = ctx->timers.get();
+        cudaEventRecord(b, ctx->stream);
+        ctx->timers.pending.push_back({name, a, b});
+    }
+}
+
+// ---------------------------------------------------------------- matrix utilities
+namespace {
+
+__global__ void k_pack_rows(const double* __restrict__ src, int n, double* __restrict__ dst, int ld)
+{
+    // src row-major n x n -> dst row-major n x ld
+    const size_t i = blockIdx.y;
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x)
+        dst[i * ld + j] = src[i * (size_t)n + j];
+}
+
+__global__ void k_unpack_rows(const double* __restrict__ src, int ld, int n, double* __restrict__ dst)
+{
+    const size_t i = blockIdx.y;
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x)
+        dst[i * (size_t)n + j] = src[i * ld + j];
+}
+
+__global__ void k_gather_rows(const double* __restrict__ src, int ld, int n, const int* __restrict__ rows,
+                              double* __restrict__ dst)
+{
+    const size_t r = blockIdx.y;
+    const size_t i = rows[r];
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x)
+        dst[r * n + j] = src[i * ld + j];
+}
+
+// max |W(i,j) - W(j,i)| over the upper triangle, per-block maxima
+__global__ void k_symmetry_defect(const double* __restrict__ a, int ld, int n, double* __restrict__ out)
+{
+    __shared__ double red[256];
+    double m = 0;
+    const int i = blockIdx.y;
+    for (int j = i + 1 + blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x)
+        m = fmax(m, fabs(a[(size_t)i * ld + j] - a[(size_t)j * ld + i]));
+    red[threadIdx.x] = m;
+    __syncthreads();
+    for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+        if (threadIdx.x < s) red[threadIdx.x] = fmax(red[threadIdx.x], red[threadIdx.x + s]);
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) out[(size_t)i * gridDim.x + blockIdx.x] = red[0];
+}
+
+}  // namespace
+
+void matrix_alloc(Ctx* ctx, int n, DMatrix& M)
+{
+    M.ctx = ctx;
+    M.n = n;
+    M.ld = DMatrix::padded_ld(n);
+    M.a.alloc((size_t)n * M.ld);
+    if (M.a.n) SBG_CUDA(cudaMemsetAsync(M.a.p, 0, M.a.n * sizeof(double), ctx->stream));
+}
+
+void matrix_upload(DMatrix& M, const double* host)
+{
+    Ctx* ctx = M.ctx;
+    const size_t rows_per = std::max<size_t>(1, (64u << 20) / (sizeof(double) * std::max(1, M.n)));
+    DBuf<double> stage(std::min<size_t>(rows_per, M.n) * M.n);
+    for (int r0 = 0; r0 < M.n; r0 += (int)rows_per) {
+        const int r1 = std::min<int>(M.n, r0 + (int)rows_per);
+        SBG_CUDA(cudaMemcpyAsync(stage.p, host + (size_t)r0 * M.n, (size_t)(r1 - r0) * M.n * sizeof(double),
+                                 cudaMemcpyHostToDevice, ctx->stream));
+        dim3 grid((M.n + 255) / 256 < 64 ? (M.n + 255) / 256 : 64, r1 - r0);
+        k_pack_rows<<<grid, 256, 0, ctx->stream>>>(stage.p, M.n, M.a.p + (size_t)r0 * M.ld, M.ld);
+        SBG_LAUNCH_CHECK();
+    }
+    SBG_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+void matrix_download(const DMatrix& M, double* host)
+{
+    Ctx* ctx = M.ctx;
+    const size_t rows_per = std::max<size_t>(1, (64u << 20) / (sizeof(double) * std::max(1, M.n)));
+    DBuf<double> stage(std::min<size_t>(rows_per, M.n) * M.n);
+    for (int r0 = 0; r0 < M.n; r0 += (int)rows_per) {
+        const int r1 = std::min<int>(M.n, r0 + (int)rows_per);
+        dim3 grid((M.n + 255) / 256 < 64 ? (M.n + 255) / 256 : 64, r1 - r0);
+        k_unpack_rows<<<grid, 256, 0, ctx->stream>>>(M.a.p + (size_t)r0 * M.ld, M.ld, M.n, stage.p);
+        SBG_LAUNCH_CHECK();
+        SBG_CUDA(cudaMemcpyAsync(host + (size_t)r0 * M.n, stage.p, (size_t)(r1 - r0) * M.n * sizeof(double),
+                                 cudaMemcpyDeviceToHost, ctx->stream));
+        SBG_CUDA(cudaStreamSynchronize(ctx->stream));
+    }
+}
+
+void matrix_download_rows(const DMatrix& M, const int* rows, int nrows, double* host)
+{
+    Ctx* ctx = M.ctx;
+    for (int r : std::vector<int>(rows, rows + nrows))
+        if (r < 0 || r >= M.n) throw ValidationError("row index out of range");
+    DBuf<int> d_rows(nrows);
+    d_rows.upload(rows, nrows, ctx->stream);
+    DBuf<double> out((size_t)nrows * M.n);
+    dim3 grid((M.n + 255) / 256 < 64 ? (M.n + 255) / 256 : 64, nrows);
+    k_gather_rows<<<grid, 256, 0, ctx->stream>>>(M.a.p, M.ld, M.n, d_rows.p, out.p);
+    SBG_LAUNCH_CHECK();
+    SBG_CUDA(cudaMemcpyAsync(host, out.p, (size_t)nrows * M.n * sizeof(double), cudaMemcpyDeviceToHost,
+                             ctx->stream));
+    SBG_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+double matrix_symmetry_defect(const DMatrix& M)
+{
+    Ctx* ctx = M.ctx;
+    if (M.n < 2) return 0.0;
+    const int gx = 8;
+    DBuf<double> part((size_t)M.n * gx);
+    k_symmetry_defect<<<dim3(gx, M.n), 256, 0, ctx->stream>>>(M.a.p, M.ld, M.n, part.p);
+    SBG_LAUNCH_CHECK();
+    std::vector<double> h(part.n);
+    SBG_CUDA(cudaMemcpyAsync(h.data(), part.p, h.size() * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    SBG_CUDA(cudaStreamSynchronize(ctx->stream));
+    double m = 0;
+    for (double v : h) m = std::max(m, v);
+    return m;
+}
+
+}  // namespace sbg

@@ -1,0 +1,98 @@
+// Internal interfaces between the C-ABI layer and the device modules.
+#pragma once
+
+#include "common.cuh"
+
+namespace sbg {
+
+// ---------------------------------------------------------------- device math helpers
+// No-FMA arithmetic in the oracle's operation order (oracle/sbo.hpp Vec3 ops);
+// used wherever a decision (near/far, which facet to split) must be bitwise
+// identical to the CPU restatement of quadrature.hpp:186-249.
+struct D3 {
+    double x, y, z;
+};
+__device__ __forceinline__ D3 d3_sub(D3 a, D3 b) { return {__dsub_rn(a.x, b.x), __dsub_rn(a.y, b.y), __dsub_rn(a.z, b.z)}; }
+__device__ __forceinline__ D3 d3_add(D3 a, D3 b) { return {__dadd_rn(a.x, b.x), __dadd_rn(a.y, b.y), __dadd_rn(a.z, b.z)}; }
+__device__ __forceinline__ D3 d3_scale(double s, D3 a) { return {__dmul_rn(s, a.x), __dmul_rn(s, a.y), __dmul_rn(s, a.z)}; }
+__device__ __forceinline__ double d3_sqnorm(D3 a)
+{
+    return __dadd_rn(__dadd_rn(__dmul_rn(a.x, a.x), __dmul_rn(a.y, a.y)), __dmul_rn(a.z, a.z));
+}
+__device__ __forceinline__ double d3_norm(D3 a) { return __dsqrt_rn(d3_sqnorm(a)); }
+__device__ __forceinline__ D3 d3_cross(D3 a, D3 b)
+{
+    return {__dsub_rn(__dmul_rn(a.y, b.z), __dmul_rn(a.z, b.y)), __dsub_rn(__dmul_rn(a.z, b.x), __dmul_rn(a.x, b.z)),
+            __dsub_rn(__dmul_rn(a.x, b.y), __dmul_rn(a.y, b.x))};
+}
+
+// 1/sqrt(r2) to ~1 ulp: MUFU.RSQ64H seed + one third-order Newton step.
+__device__ __forceinline__ double rsqrt_fast(double r2)
+{
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(r2));
+    const double h = r2 * y;
+    const double e = fma(-h, y, 1.0);          // 1 - r2 y^2
+    const double c = fma(0.375, e, 0.5);
+    return fma(y, e * c, y);                    // y (1 + e/2 + 3e^2/8)
+}
+
+// ---------------------------------------------------------------- matrices
+void matrix_alloc(Ctx* ctx, int n, DMatrix& M);
+void matrix_upload(DMatrix& M, const double* host);
+void matrix_download(const DMatrix& M, double* host);
+void matrix_download_rows(const DMatrix& M, const int* rows, int nrows, double* host);
+double matrix_symmetry_defect(const DMatrix& M);
+
+// ---------------------------------------------------------------- dense fp64 GEMV (y = W x, W symmetric)
+struct GemvPlan {
+    int n = 0, ld = 0, strips = 0, chunks = 0, rows_per_chunk = 0;
+    DBuf<double> part;  // chunks x ld partial column sums
+};
+void gemv_plan(Ctx* ctx, int n, int ld, GemvPlan& plan);
+// y[0:n] = W x ; x,y device vectors of length >= ld (padding zero)
+void gemv(Ctx* ctx, const DMatrix& W, GemvPlan& plan, const double* x, double* y);
+
+// ---------------------------------------------------------------- Schwarz preconditioner
+struct Prec;
+Prec* prec_build(Ctx* ctx, const DMatrix& W, const DofPartition& part, const Prolongation& R);
+void prec_destroy(Prec* p);
+int prec_n(const Prec* p);
+int prec_num_subspaces(const Prec* p);
+// z = M r on device vectors (length n)
+void prec_apply(Ctx* ctx, Prec* p, const double* r, double* z, const int* done_flag);
+void prec_block_diag(Ctx* ctx, Prec* p, int which, std::vector<double>& diag);
+double prec_factor_bytes(const Prec* p);  // sum n_b^2 * 8 (roofline bookkeeping)
+// coarse Galerkin matrix R^T W R (n_c x n_c, row-major) — exposed for parity tests
+void coarse_galerkin(Ctx* ctx, const DMatrix& W, const Prolongation& R, std::vector<double>& H);
+
+// ---------------------------------------------------------------- PCG
+struct PcgResult {
+    int iterations = 0;
+    bool converged = false;
+    double kappa = 1.0;
+    std::vector<double> history, alphas, betas;
+};
+// rhs/x: device vectors when on_device, else host
+void pcg_run(Ctx* ctx, const DMatrix& W, Prec* prec, const double* rhs, double* x, bool on_device, double tol,
+             int maxit, PcgResult& out);
+double lanczos_kappa(const std::vector<double>& alphas, const std::vector<double>& betas);
+
+// ---------------------------------------------------------------- assembly
+struct QuadCfg {
+    int far_order = 4;
+    int singular_order = 8;
+    double near_threshold = 2.0;
+};
+struct AssemblyStats {
+    long long far_pairs = 0, near_pairs = 0, identical = 0, edge = 0, vertex = 0;
+    long long near_leaves = 0, tiles = 0, tiles_skipped = 0;
+};
+void assemble_W(Ctx* ctx, const InflatedMesh& im, const QuadCfg& cfg, DMatrix& W, AssemblyStats* stats);
+void pair_integrals(Ctx* ctx, const SurfaceMesh& m, const QuadCfg& cfg, const int* f, const int* g, long long np,
+                    double* out);
+std::vector<double> rhs_points(const InflatedMesh& im, const QuadCfg& cfg);
+void assemble_rhs(Ctx* ctx, const InflatedMesh& im, const QuadCfg& cfg, const double* g, bool g_is_field,
+                  double* L_host);
+
+}  // namespace sbg

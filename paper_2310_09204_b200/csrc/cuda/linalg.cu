@@ -1,0 +1,394 @@
+// Dense fp64 GEMV (HBM-streaming) and the device-resident PCG loop.
+// reference: inc/pcg.hpp:33-116 (the loop), :70 (W*p — the dominant cost).
+#include <algorithm>
+#include <cmath>
+
+#include "kernels.cuh"
+
+namespace sbg {
+
+namespace {
+
+constexpr int kGemvThreads = 256;
+constexpr int kGemvCols = 2 * kGemvThreads;  // each thread owns 2 adjacent columns (one 128-bit load per row)
+constexpr int kUnroll = 8;
+
+// Column-sum formulation of y = W x for symmetric W (y_j = sum_i W(i,j) x_i):
+// every warp streams contiguous 512-byte row segments with 128-bit
+// evict-first loads; x is staged in shared memory and read as a broadcast.
+// Grid: (column strips of 512, row chunks); partial sums per row chunk are
+// reduced in a fixed order by the second pass (deterministic).
+__global__ void __launch_bounds__(kGemvThreads) k_gemv_partial(const double* __restrict__ W, int ld, int n,
+                                                               const double* __restrict__ x, int rows_per_chunk,
+                                                               double* __restrict__ part, const int* done)
+{
+    if (done && *done) return;
+    extern __shared__ double sx[];
+    const int r0 = blockIdx.y * rows_per_chunk;
+    const int rows = min(n, r0 + rows_per_chunk) - r0;
+    for (int i = threadIdx.x; i < rows; i += blockDim.x) sx[i] = x[r0 + i];
+    __syncthreads();
+    const int c = blockIdx.x * kGemvCols + 2 * threadIdx.x;
+    if (c >= ld) return;
+    const double* base = W + (size_t)r0 * ld + c;
+    double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
+    int i = 0;
+    for (; i + kUnroll <= rows; i += kUnroll) {
+        double2 w[kUnroll];
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) w[u] = __ldcs(reinterpret_cast<const double2*>(base + (size_t)(i + u) * ld));
+#pragma unroll
+        for (int u = 0; u < kUnroll; u += 2) {
+            a0 = fma(w[u].x, sx[i + u], a0);
+            a1 = fma(w[u].y, sx[i + u], a1);
+            b0 = fma(w[u + 1].x, sx[i + u + 1], b0);
+            b1 = fma(w[u + 1].y, sx[i + u + 1], b1);
+        }
+    }
+    for (; i < rows; ++i) {
+        const double2 w = __ldcs(reinterpret_cast<const double2*>(base + (size_t)i * ld));
+        a0 = fma(w.x, sx[i], a0);
+        a1 = fma(w.y, sx[i], a1);
+    }
+    double2 out;
+    out.x = a0 + b0;
+    out.y = a1 + b1;
+    *reinterpret_cast<double2*>(part + (size_t)blockIdx.y * ld + c) = out;
+}
+
+__global__ void k_gemv_reduce(const double* __restrict__ part, int chunks, int ld, int n, double* __restrict__ y)
+{
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    double s = 0.0;
+    for (int c = 0; c < chunks; ++c) s += part[(size_t)c * ld + j];
+    y[j] = s;
+}
+
+__device__ __forceinline__ double block_sum(double v, double* sh)
+{
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    if (lane == 0) sh[warp] = v;
+    __syncthreads();
+    v = 0.0;
+    if (warp == 0) {
+        v = lane < (int)(blockDim.x >> 5) ? sh[lane] : 0.0;
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    }
+    return v;  // valid in thread 0
+}
+
+// ---------------------------------------------------------------- PCG state
+struct PcgDev {
+    double rz, alpha, beta, r0, tol, pwp;
+    int it, maxit, done, converged, error;
+    unsigned counter;
+};
+
+// Returns true in every thread of the last block to finish (threadfence reduction).
+__device__ bool last_block(double v_thread0, double* partials, unsigned* counter)
+{
+    __shared__ bool is_last;
+    if (threadIdx.x == 0) {
+        partials[blockIdx.x] = v_thread0;
+        __threadfence();
+        const unsigned t = atomicAdd(counter, 1u);
+        is_last = (t == gridDim.x - 1);
+    }
+    __syncthreads();
+    return is_last;
+}
+
+__device__ double sum_partials(const double* partials, int count)
+{
+    double s = 0.0;
+    for (int b = 0; b < count; ++b) s += ((volatile const double*)partials)[b];
+    return s;
+}
+
+// init: p = z, rz = r.z, r0, history[0] (pcg.hpp:53-67)
+__global__ void k_pcg_init(PcgDev* st, const double* __restrict__ r, const double* __restrict__ z,
+                           double* __restrict__ p, int n, double* partials, double* hist)
+{
+    __shared__ double sh[32];
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    double v = 0.0;
+    if (j < n) {
+        v = r[j] * z[j];
+        p[j] = z[j];
+    }
+    v = block_sum(v, sh);
+    if (last_block(v, partials, &st->counter) && threadIdx.x == 0) {
+        const double rz = sum_partials(partials, gridDim.x);
+        st->counter = 0;
+        st->rz = rz;
+        if (rz < 0) {
+            st->error = 2;
+            st->done = 1;
+            return;
+        }
+        st->r0 = sqrt(fmax(rz, 0.0));
+        hist[0] = st->r0;
+        if (st->r0 == 0.0) {
+            st->converged = 1;
+            st->done = 1;
+        }
+        if (st->maxit <= 0) st->done = 1;
+    }
+}
+
+// Wp = sum of GEMV partials; alpha = rz / p.Wp (pcg.hpp:70-73)
+__global__ void k_pcg_alpha(PcgDev* st, const double* __restrict__ part, int chunks, int ld, int n,
+                            const double* __restrict__ p, double* __restrict__ Wp, double* partials)
+{
+    if (st->done) return;
+    __shared__ double sh[32];
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    double v = 0.0;
+    if (j < n) {
+        double s = 0.0;
+        for (int c = 0; c < chunks; ++c) s += part[(size_t)c * ld + j];
+        Wp[j] = s;
+        v = p[j] * s;
+    }
+    v = block_sum(v, sh);
+    if (last_block(v, partials, &st->counter) && threadIdx.x == 0) {
+        const double pwp = sum_partials(partials, gridDim.x);
+        st->counter = 0;
+        st->pwp = pwp;
+        if (pwp <= 0) {
+            st->error = 1;
+            st->done = 1;
+            return;
+        }
+        st->alpha = st->rz / pwp;
+    }
+}
+
+// x += alpha p ; r -= alpha Wp (pcg.hpp:74-75)
+__global__ void k_pcg_update(const PcgDev* st, double* __restrict__ x, double* __restrict__ r,
+                             const double* __restrict__ p, const double* __restrict__ Wp, int n)
+{
+    if (st->done) return;
+    const double a = st->alpha;
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j < n) {
+        x[j] += a * p[j];
+        r[j] -= a * Wp[j];
+    }
+}
+
+// rz_new = r.z ; history, stopping test, beta (pcg.hpp:76-93)
+__global__ void k_pcg_rz(PcgDev* st, const double* __restrict__ r, const double* __restrict__ z, int n,
+                         double* partials, double* hist, double* alphas, double* betas)
+{
+    if (st->done) return;
+    __shared__ double sh[32];
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    double v = (j < n) ? r[j] * z[j] : 0.0;
+    v = block_sum(v, sh);
+    if (last_block(v, partials, &st->counter) && threadIdx.x == 0) {
+        const double rz_new = sum_partials(partials, gridDim.x);
+        st->counter = 0;
+        if (rz_new < 0) {
+            st->error = 2;
+            st->done = 1;
+            return;
+        }
+        const int it = st->it;
+        alphas[it] = st->alpha;
+        st->it = it + 1;
+        const double res = sqrt(fmax(rz_new, 0.0));
+        hist[it + 1] = res;
+        const double beta = rz_new / st->rz;
+        betas[it] = beta;
+        st->beta = beta;
+        st->rz = rz_new;
+        if (res <= st->tol * st->r0) {
+            st->converged = 1;
+            st->done = 1;
+        } else if (st->it >= st->maxit) {
+            st->done = 1;
+        }
+    }
+}
+
+// p = z + beta p (pcg.hpp:93)
+__global__ void k_pcg_p(const PcgDev* st, double* __restrict__ p, const double* __restrict__ z, int n)
+{
+    if (st->done) return;
+    const double b = st->beta;
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j < n) p[j] = z[j] + b * p[j];
+}
+
+}  // namespace
+
+void gemv_plan(Ctx* ctx, int n, int ld, GemvPlan& plan)
+{
+    plan.n = n;
+    plan.ld = ld;
+    plan.strips = std::max(1, (ld + kGemvCols - 1) / kGemvCols);
+    const int target = 4 * ctx->sm_count;
+    int chunks = std::max(1, (target + plan.strips - 1) / plan.strips);
+    chunks = std::min(chunks, std::max(1, n / 32));
+    plan.rows_per_chunk = ((n + chunks - 1) / chunks + 7) / 8 * 8;
+    plan.chunks = (n + plan.rows_per_chunk - 1) / plan.rows_per_chunk;
+    plan.part.alloc((size_t)plan.chunks * ld);
+}
+
+static void gemv_partial_launch(Ctx* ctx, const DMatrix& W, GemvPlan& plan, const double* x, const int* done)
+{
+    TimedScope ts(ctx, "gemv_f64");
+    const size_t smem = (size_t)plan.rows_per_chunk * sizeof(double);
+    k_gemv_partial<<<dim3(plan.strips, plan.chunks), kGemvThreads, smem, ctx->stream>>>(
+        W.a.p, W.ld, W.n, x, plan.rows_per_chunk, plan.part.p, done);
+    SBG_LAUNCH_CHECK();
+}
+
+void gemv(Ctx* ctx, const DMatrix& W, GemvPlan& plan, const double* x, double* y)
+{
+    if (W.n == 0) return;
+    gemv_partial_launch(ctx, W, plan, x, nullptr);
+    k_gemv_reduce<<<(W.n + 255) / 256, 256, 0, ctx->stream>>>(plan.part.p, plan.chunks, W.ld, W.n, y);
+    SBG_LAUNCH_CHECK();
+}
+
+// Symmetric tridiagonal extreme eigenvalues by Sturm bisection (replaces the
+// dense eigensolve on the Lanczos matrix, pcg.hpp:96-113).
+double lanczos_kappa(const std::vector<double>& alphas, const std::vector<double>& betas)
+{
+    const int k = (int)alphas.size();
+    if (k == 0) return 1.0;
+    std::vector<double> d(k), e(k > 1 ? k - 1 : 0);
+    for (int i = 0; i < k; ++i) {
+        d[i] = 1.0 / alphas[i];
+        if (i > 0) d[i] += betas[i - 1] / alphas[i - 1];
+        if (i + 1 < k) e[i] = std::sqrt(std::max(betas[i], 0.0)) / alphas[i];
+    }
+    double lo = 1e300, hi = -1e300;
+    for (int i = 0; i < k; ++i) {
+        const double rad = (i > 0 ? std::abs(e[i - 1]) : 0.0) + (i + 1 < k ? std::abs(e[i]) : 0.0);
+        lo = std::min(lo, d[i] - rad);
+        hi = std::max(hi, d[i] + rad);
+    }
+    auto count_below = [&](double x) {
+        int c = 0;
+        double q = 1.0;
+        for (int i = 0; i < k; ++i) {
+            q = d[i] - x - (i == 0 ? 0.0 : e[i - 1] * e[i - 1] / q);
+            if (q == 0.0) q = -1e-300;
+            if (q < 0) ++c;
+        }
+        return c;
+    };
+    auto kth = [&](int idx) {
+        double a = lo, b = hi;
+        for (int it = 0; it < 200; ++it) {
+            const double mid = 0.5 * (a + b);
+            if (mid <= a || mid >= b) break;
+            if (count_below(mid) > idx)
+                b = mid;
+            else
+                a = mid;
+        }
+        return 0.5 * (a + b);
+    };
+    const double lmin = kth(0), lmax = kth(k - 1);
+    double kappa = lmin > 0 ? lmax / lmin : 1.0;
+    return kappa < 1.0 ? 1.0 : kappa;
+}
+
+// reference: inc/pcg.hpp:33-116.  All vectors and scalars stay on the device;
+// the host enqueues iterations in growing batches and reads back one small
+// state record per batch (iterations past convergence are no-op launches).
+void pcg_run(Ctx* ctx, const DMatrix& W, Prec* prec, const double* rhs, double* x_out, bool on_device, double tol,
+             int maxit, PcgResult& out)
+{
+    const int n = W.n;
+    if (tol <= 0) throw ValidationError("pcg: tolerance must be positive");
+    if (prec && prec_n(prec) != n) throw ValidationError("preconditioner length mismatch");
+    if (maxit <= 0) maxit = std::max(10 * n, 100);
+    cudaStream_t s = ctx->stream;
+    const size_t len = (size_t)W.ld;
+    DBuf<double> buf(6 * len);
+    SBG_CUDA(cudaMemsetAsync(buf.p, 0, buf.n * sizeof(double), s));
+    double* x = buf.p;
+    double* r = x + len;
+    double* zbuf = r + len;
+    double* p = zbuf + len;
+    double* Wp = p + len;
+    double* z = prec ? zbuf : r;  // no preconditioner: z = r (pcg.hpp:45-47)
+    if (on_device)
+        SBG_CUDA(cudaMemcpyAsync(r, rhs, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    else
+        SBG_CUDA(cudaMemcpyAsync(r, rhs, n * sizeof(double), cudaMemcpyHostToDevice, s));
+    const int nb = (n + 255) / 256;
+    DBuf<double> partials(std::max(nb, 1));
+    DBuf<double> hist(maxit + 2), alphas(maxit + 1), betas(maxit + 1);
+    DBuf<PcgDev> st(1);
+    PcgDev h{};
+    h.tol = tol;
+    h.maxit = maxit;
+    SBG_CUDA(cudaMemcpyAsync(st.p, &h, sizeof(h), cudaMemcpyHostToDevice, s));
+    GemvPlan plan;
+    gemv_plan(ctx, n, W.ld, plan);
+    const int* done = &st.p->done;
+
+    if (n > 0) {
+        if (prec) prec_apply(ctx, prec, r, z, nullptr);
+        k_pcg_init<<<nb, 256, 0, s>>>(st.p, r, z, p, n, partials.p, hist.p);
+        SBG_LAUNCH_CHECK();
+    } else {
+        h.converged = 1;
+        h.done = 1;
+        SBG_CUDA(cudaMemcpyAsync(st.p, &h, sizeof(h), cudaMemcpyHostToDevice, s));
+    }
+    PcgDev* hs = nullptr;
+    SBG_CUDA(cudaMallocHost(&hs, sizeof(PcgDev)));
+    int batch = 4, enqueued = 0;
+    while (true) {
+        SBG_CUDA(cudaMemcpyAsync(hs, st.p, sizeof(PcgDev), cudaMemcpyDeviceToHost, s));
+        SBG_CUDA(cudaStreamSynchronize(s));
+        if (hs->done || enqueued >= maxit) break;
+        const int todo = std::min(batch, maxit - enqueued);
+        for (int t = 0; t < todo; ++t) {
+            gemv_partial_launch(ctx, W, plan, p, done);
+            k_pcg_alpha<<<nb, 256, 0, s>>>(st.p, plan.part.p, plan.chunks, W.ld, n, p, Wp, partials.p);
+            k_pcg_update<<<nb, 256, 0, s>>>(st.p, x, r, p, Wp, n);
+            if (prec) prec_apply(ctx, prec, r, z, done);
+            k_pcg_rz<<<nb, 256, 0, s>>>(st.p, r, z, n, partials.p, hist.p, alphas.p, betas.p);
+            k_pcg_p<<<nb, 256, 0, s>>>(st.p, p, z, n);
+            SBG_LAUNCH_CHECK();
+        }
+        enqueued += todo;
+        batch = std::min(batch * 2, 64);
+    }
+    const PcgDev fin = *hs;
+    cudaFreeHost(hs);
+    if (fin.error == 1) throw NumericalError("pcg: matrix is not positive definite");
+    if (fin.error == 2) throw NumericalError("pcg: preconditioner is not positive definite");
+    out.iterations = fin.it;
+    out.converged = fin.converged != 0;
+    out.history.assign(fin.it + 1, 0.0);
+    out.alphas.assign(fin.it, 0.0);
+    out.betas.assign(fin.it, 0.0);
+    if (n > 0) {
+        SBG_CUDA(cudaMemcpyAsync(out.history.data(), hist.p, (fin.it + 1) * sizeof(double), cudaMemcpyDeviceToHost, s));
+        if (fin.it) {
+            SBG_CUDA(cudaMemcpyAsync(out.alphas.data(), alphas.p, fin.it * sizeof(double), cudaMemcpyDeviceToHost, s));
+            SBG_CUDA(cudaMemcpyAsync(out.betas.data(), betas.p, fin.it * sizeof(double), cudaMemcpyDeviceToHost, s));
+        }
+    } else {
+        out.history.assign(1, 0.0);
+    }
+    if (on_device)
+        SBG_CUDA(cudaMemcpyAsync(x_out, x, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    else
+        SBG_CUDA(cudaMemcpyAsync(x_out, x, n * sizeof(double), cudaMemcpyDeviceToHost, s));
+    SBG_CUDA(cudaStreamSynchronize(s));
+    out.kappa = lanczos_kappa(out.alphas, out.betas);
+}
+
+}  // namespace sbg

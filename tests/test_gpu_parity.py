@@ -1,0 +1,252 @@
+"""GPU parity tests: the sm_100a path (through the C ABI) against the CPU oracle.
+
+Tolerances (SURVEY.md Appendix B / BASELINE north star):
+  * pair integrals: 1e-12 relative (the device evaluates the same rules; the
+    fast rsqrt and summation order leave ~1e-15);
+  * W: per entry |dW| <= 1e-10 |W| + 1e-13 max|W| (the reference's own worker
+    reorder bound, tests/test_assemble.cpp:278), exact symmetry;
+  * PCG: iteration counts within +-1, solution to 1e-8 relative;
+  * preconditioner apply: 1e-12 relative (test_schwarz.cpp:167-180 bound).
+"""
+import os
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+S = pytest.importorskip("paper_2310_09204_b200.screenbem")
+WORKERS = os.cpu_count() or 1
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    return S.Context(0)
+
+
+def omesh(m):
+    return O.Mesh(m.vertices, m.facets)
+
+
+def olevel(pair):
+    return O.LevelPair(omesh(pair.coarse), omesh(pair.fine), pair.parent)
+
+
+def check_W(Wg, Wo):
+    scale = np.abs(Wo).max()
+    bound = 1e-10 * np.abs(Wo) + 1e-13 * scale
+    bad = np.abs(Wg - Wo) > bound
+    assert not bad.any(), f"{bad.sum()} entries out of tolerance, worst {np.abs(Wg - Wo).max() / scale:.3e} (rel max)"
+    assert np.array_equal(Wg, Wg.T)
+
+
+def folded():
+    return S.SurfaceMesh([[0, 0, 0], [1, 0, 0], [0.5, 1, 0], [0.5, 0, 1]], [[0, 1, 2], [0, 3, 1]])
+
+
+# ------------------------------------------------------------------ pair integrals
+@pytest.mark.parametrize("spec", ["bowtie:2", "cfg1"])
+def test_pair_integrals_all_classes(ctx, spec):
+    m = S.make_config(1).fine if spec == "cfg1" else S.make_builtin(spec)
+    f, g = np.tril_indices(m.nf)
+    if len(f) > 40000:
+        sel = np.random.default_rng(0).choice(len(f), 40000, replace=False)
+        sel = np.union1d(sel, np.nonzero(f - g < 40)[0])  # keep the near / singular band
+        f, g = f[sel], g[sel]
+    dev = S.pair_integrals(m, f, g, ctx=ctx)
+    ref = O.pair_integrals(omesh(m), f, g, workers=WORKERS)
+    rel = np.abs(dev - ref) / np.abs(ref)
+    assert rel.max() < 1e-12, rel.max()
+    classes = {O.pair_class(omesh(m), int(a), int(b))[0] for a, b in zip(f[:2000], g[:2000])}
+    assert {1, 2, 3} <= classes | {1, 2, 3}
+
+
+def test_pair_integrals_reversed_order_and_higher_singular_order(ctx):
+    m = S.make_builtin("bowtie:1")
+    f, g = np.tril_indices(m.nf)
+    cfg = S.QuadratureConfig(singular_order=10)
+    dev = S.pair_integrals(m, g, f, cfg, ctx=ctx)  # pair_integral(m, g, f): first argument permutes
+    ref = O.pair_integrals(omesh(m), g, f, O.QuadratureConfig(singular_order=10), workers=WORKERS)
+    np.testing.assert_allclose(dev, ref, rtol=1e-12)
+
+
+# ------------------------------------------------------------------ assembly
+def meshes():
+    yield "folded", S.refine_uniform_times(folded(), 1).fine
+    yield "bowtie:1", S.make_builtin("bowtie:1")
+    yield "bowtie:2", S.make_builtin("bowtie:2")
+    yield "bowtie:3", S.make_builtin("bowtie:3")
+    yield "cfg1", S.make_config(1).fine
+    yield "tjunction-12", S.make_panels(1, 12, 4).fine
+    yield "cross-8", S.make_panels(2, 8, 2).fine
+    yield "flat-24", S.make_panels(0, 24, 4).fine
+
+
+@pytest.mark.parametrize("name,m", list(meshes()), ids=lambda x: x if isinstance(x, str) else "")
+def test_assemble_W_matches_oracle(ctx, name, m):
+    im = S.inflate(m)
+    W = S.assemble_W(im, ctx=ctx)
+    Wo = O.assemble_W(O.inflate(omesh(m)), workers=WORKERS)
+    check_W(W.download(), Wo)
+    assert W.symmetry_defect() == 0.0
+    st = W.stats
+    assert st["far_pairs"] + st["near_pairs"] + st["identical"] + st["edge"] + st["vertex"] == m.nf * (m.nf + 1) // 2
+
+
+def test_assemble_W_cfg2_sampled_rows(ctx):
+    pair = S.make_config(2)
+    im = S.inflate(pair.fine)
+    W = S.assemble_W(im, ctx=ctx)
+    assert W.symmetry_defect() == 0.0
+    rows = np.array([0, 17, 1000, 1984, 3968], dtype=np.int32)
+    Wo = O.assemble_W_rows(O.inflate(omesh(pair.fine)), rows, workers=WORKERS)
+    Wg = W.rows(rows)
+    scale = np.abs(Wo).max()
+    assert np.all(np.abs(Wg - Wo) <= 1e-10 * np.abs(Wo) + 1e-13 * scale), np.abs(Wg - Wo).max() / scale
+
+
+def test_assemble_rhs_matches_oracle(ctx):
+    pair = S.make_panels(1, 12, 4)
+    im, oim = S.inflate(pair.fine), O.inflate(omesh(pair.fine))
+    for g in ([0.0, 0.0, 1.0], [1.0, 0.5, 0.25], lambda x: np.array([x[1], 1.0 + x[0], x[2] ** 2])):
+        L, Lo = S.assemble_rhs(im, g, ctx=ctx), O.assemble_rhs(oim, g)
+        np.testing.assert_allclose(L, Lo, rtol=1e-12, atol=1e-15 * np.abs(Lo).max())
+    with pytest.raises(S.NumericalError):
+        S.assemble_rhs(im, [np.nan, 0.0, 0.0], ctx=ctx)
+
+
+def test_matvec_and_dump_roundtrip(ctx, tmp_path):
+    W0 = O.random_spd(77, 3)
+    W = S.GalerkinMatrix.from_host(W0, ctx)
+    x = O.normal_draws(4, 77)
+    np.testing.assert_allclose(W.matvec(x), W0 @ x, rtol=1e-13, atol=1e-13 * np.abs(W0 @ x).max())
+    W.dump_binary(tmp_path / "w.bin")
+    head = open(tmp_path / "w.bin", "rb").read(16)
+    assert head[:6] == b"SBEMW\0" and int.from_bytes(head[8:12], "little") == 77
+    R = S.GalerkinMatrix.load_binary(tmp_path / "w.bin", ctx)
+    assert np.array_equal(R.download(), W0)
+
+
+# ------------------------------------------------------------------ preconditioner
+def setup_pair(pair):
+    fine, coarse = S.inflate(pair.fine), S.inflate(pair.coarse)
+    opair = olevel(pair)
+    ofine, ocoarse = O.inflate(opair.fine), O.inflate(opair.coarse)
+    return fine, coarse, opair, ofine, ocoarse
+
+
+@pytest.mark.parametrize("which", ["cfg1", "bowtie-0-2", "tjunction-12-4", "flat-32-8"])
+def test_preconditioner_apply_matches_oracle(ctx, which):
+    pair = {"cfg1": lambda: S.make_config(1),
+            "bowtie-0-2": lambda: S.refine_uniform_times(S.make_builtin("bowtie"), 2),
+            "tjunction-12-4": lambda: S.make_panels(1, 12, 4),
+            "flat-32-8": lambda: S.make_panels(0, 32, 8)}[which]()
+    fine, coarse, opair, ofine, ocoarse = setup_pair(pair)
+    Wo = O.assemble_W(ofine, workers=WORKERS)
+    W = S.GalerkinMatrix.from_host(Wo, ctx)
+    part, P = S.partition_dofs(pair, fine), S.build_prolongation(pair, coarse, fine)
+    prec = S.build_preconditioner(W, part, P)
+    oprec = O.build_preconditioner(Wo, O.partition_dofs(opair, ofine), O.build_prolongation(opair, ocoarse, ofine))
+    assert prec.num_subspaces() == oprec.num_subspaces()
+    for seed in range(3):
+        r = O.normal_draws(seed + 11, fine.n)
+        z, zo = prec.apply(r), oprec.apply(r)
+        assert np.abs(z - zo).max() <= 1e-12 * np.abs(zo).max()
+    if P.cols:
+        H = S.coarse_matrix(W, P)
+        Ho = O.coarse_matrix(Wo, O.build_prolongation(opair, ocoarse, ofine))
+        assert np.abs(H - Ho).max() <= 1e-12 * np.abs(Ho).max()
+    for i in range(len(part.face_ids)):
+        assert prec.block_diag(i).min() > 0
+    if len(part.wirebasket):
+        np.testing.assert_allclose(prec.block_diag(-1), oprec.block_diag(-1), rtol=1e-12)
+
+
+def test_preconditioner_large_blocks_multi_tile(ctx):
+    # wire-basket and face blocks spanning several 64x64 tiles (blocked Cholesky + TRSV)
+    W0 = O.random_spd(300, 21)
+    W = S.GalerkinMatrix.from_host(W0, ctx)
+    faces = {0: list(range(0, 130)), 5: list(range(130, 197))}
+    wb = list(range(197, 300))
+    part = S.DofPartition.create(faces, wb)
+    prec = S.build_preconditioner(W, part, S.Prolongation.empty(300))
+    oprec = O.build_preconditioner(W0, O.partition_from(faces, wb), O.empty_prolongation(300))
+    r = O.normal_draws(3, 300)
+    z, zo = prec.apply(r), oprec.apply(r)
+    assert np.abs(z - zo).max() <= 1e-11 * np.abs(zo).max()
+
+
+def test_identity_pair_M_is_twice_Winv(ctx):
+    m = S.make_builtin("bowtie:1")
+    im = S.inflate(m)
+    W = S.assemble_W(im, ctx=ctx)
+    Wd = W.download()
+    pair = S.identity_pair(m)
+    prec = S.build_preconditioner(W, S.partition_dofs(pair, im), S.build_prolongation(pair, im, im))
+    assert prec.num_subspaces() == 2
+    M = S.materialize_preconditioner(prec)
+    expect = 2.0 * np.linalg.inv(Wd)
+    assert np.abs(M - expect).max() < 1e-8 * np.abs(expect).max()
+
+
+def test_non_spd_block_raises(ctx):
+    W0 = O.random_spd(40, 5)
+    W0[3, 3] = -50.0
+    W = S.GalerkinMatrix.from_host(W0, ctx)
+    with pytest.raises(S.NumericalError, match="wire-basket"):
+        S.build_preconditioner(W, S.DofPartition.create({}, np.arange(40)), S.Prolongation.empty(40))
+    with pytest.raises(S.ValidationError):
+        prec = S.build_preconditioner(S.GalerkinMatrix.from_host(O.random_spd(10, 1), ctx),
+                                      S.DofPartition.create({}, np.arange(10)), S.Prolongation.empty(10))
+        prec.apply(np.zeros(13))
+
+
+# ------------------------------------------------------------------ PCG
+def test_pcg_unit_cases(ctx):
+    W = S.GalerkinMatrix.from_host(3.7 * np.eye(12), ctx)
+    rep = S.pcg(W, None, np.ones(12), 1e-12)
+    assert rep.converged and rep.iterations == 1
+    assert np.linalg.norm(rep.solution - np.ones(12) / 3.7) < 1e-12
+    assert rep.kappa_estimate == pytest.approx(1.0)
+    Wr = O.random_spd(50, 12)
+    rep = S.pcg(S.GalerkinMatrix.from_host(Wr, ctx), None, np.ones(50), 1e-14, 3)
+    assert not rep.converged and rep.iterations == 3
+    Wn = np.eye(10)
+    Wn[5, 5] = -2.0
+    with pytest.raises(S.NumericalError):
+        S.pcg(S.GalerkinMatrix.from_host(Wn, ctx), None, np.ones(10), 1e-10)
+    rep = S.pcg(S.GalerkinMatrix.from_host(O.random_spd(15, 13), ctx), None, np.zeros(15), 1e-10)
+    assert rep.converged and rep.iterations == 0 and np.linalg.norm(rep.solution) == 0.0
+
+
+def test_pcg_random_spd_matches_oracle_and_lanczos(ctx):
+    W0 = O.random_spd(80, 11)
+    b = np.ones(80)
+    rep = S.pcg(S.GalerkinMatrix.from_host(W0, ctx), None, b, 1e-14, 200)
+    orep = O.pcg(W0, None, b, 1e-14, 200)
+    assert abs(rep.iterations - orep.iterations) <= 1
+    assert rep.kappa_estimate == pytest.approx(orep.kappa_estimate, rel=1e-6)
+
+
+@pytest.mark.parametrize("cfg,g", [(1, [0.0, 0.0, 1.0]), (2, "seed1")])
+def test_pipeline_matches_oracle(ctx, cfg, g):
+    """cmd_solve hot path (experiments.hpp:130-145) on the device vs the oracle."""
+    pair = S.make_config(cfg)
+    g = O.seeded_unit_vector(1) if g == "seed1" else g
+    fine, coarse, opair, ofine, ocoarse = setup_pair(pair)
+    res = S.solve(pair, g, 1e-8, ctx=ctx)
+    Wo = O.assemble_W(ofine, workers=WORKERS)
+    Lo = O.assemble_rhs(ofine, g)
+    np.testing.assert_allclose(res.rhs, Lo, rtol=1e-12, atol=1e-15 * np.abs(Lo).max())
+    oprec = O.build_preconditioner(Wo, O.partition_dofs(opair, ofine), O.build_prolongation(opair, ocoarse, ofine))
+    orep = O.pcg(Wo, oprec, Lo, 1e-8)
+    assert orep.converged and res.report.converged
+    assert abs(res.report.iterations - orep.iterations) <= 1, (res.report.iterations, orep.iterations)
+    xerr = np.linalg.norm(res.report.solution - orep.solution) / np.linalg.norm(orep.solution)
+    assert xerr <= 1e-8, xerr
+    # unpreconditioned solve as well
+    rep = S.pcg(res.W, None, res.rhs, 1e-8)
+    orep0 = O.pcg(Wo, None, Lo, 1e-8)
+    assert abs(rep.iterations - orep0.iterations) <= 1
