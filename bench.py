@@ -1,0 +1,344 @@
+"""Benchmark of the B200 screenbem hot path (driver contract).
+
+A step is one pass of the hot path over the config's synthetic mesh: assemble_W,
+assemble_rhs, build_preconditioner and PCG to 1e-8 (inc/experiments.hpp:130-145).
+  value : assembly triangle-pairs/s (nf(nf+1)/2 per assembly) with the mesh-derived
+          data resident in HBM (AssemblyPlan built before the timed region),
+          device time from CUDA events, max over ranks, x N ranks (replicas);
+  e2e   : the same metric through the public assemble_W call (host mesh in, host W
+          out: plan build + H2D + kernels + D2H of the n x n matrix), the drop-in for
+          the reference's assemble_W (inc/assemble.hpp:72-139);
+  extras: PCG iterations/s, matvec GB/s (HBM roofline), preconditioner applies/s,
+          time-to-solution, per-phase device times.
+--impl reference runs the CPU restatement of the reference's assemble_W
+(oracle/, all host threads, run_partitioned semantics) on a bounded sample.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "assembly tri-pairs/s; PCG iters/s & matvec GB/s vs HBM peak (fp64, 1 B200)"
+UNIT = "tri-pairs/s"
+CFG_NAMES = {1: "flat 16x16 (512 tri), H/h 8", 2: "flat 64x64 (8192 tri), H/h 16",
+             3: "T-junction 3x48x48 (13824 tri), H/h 12", 4: "triple cross 3x64x64 (24576 tri), H/h 8",
+             5: "flat 160x160 (51200 tri)"}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--ratio", type=int, default=0, help="H/h for config 5 (default 8)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU sample length")
+    return ap.parse_args()
+
+
+def dist_env():
+    return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), int(
+        os.environ.get("LOCAL_RANK", "0"))
+
+
+# --------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device, self.rows, self.proc = device, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = sorted(float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit())
+        mx = max((float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()), default=None)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].lower() == "active"})
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+# --------------------------------------------------------------------------- CPU restatement (oracle)
+def cpu_assembly_sample(cfg: int, ratio: int, target_s: float):
+    """Reference assemble_W restated in oracle/ (CPU, all host threads, contiguous
+    pair ranges + per-worker dense partials as in inc/assemble.hpp:91-133) on the
+    last rows of the reference's pair ordering (rows ff cover all partners g <= ff)."""
+    from oracle import oracle as O
+    from paper_2310_09204_b200 import screenbem as S
+    pair = S.make_config(cfg, ratio)
+    m = O.Mesh(pair.fine.vertices, pair.fine.facets)
+    im = O.inflate(m, validate=False)
+    nf = m.nf
+    workers = os.cpu_count() or 1
+    n = im.n
+    # per-worker dense partials are n^2 doubles (assemble.hpp:92-96): cap workers by RAM
+    try:
+        ram = os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_PHYS_PAGES")
+        workers = max(1, min(workers, int(0.5 * ram // max(8 * n * n, 1))))
+    except Exception:
+        pass
+    total = nf * (nf + 1) // 2
+
+    def run_rows(k):
+        lo = total - sum(nf - i for i in range(k))  # last k rows ff = nf-k .. nf-1
+        t0 = time.perf_counter()
+        O.assemble_W(im, workers=workers, pair_range=(lo, total))
+        return total - lo, time.perf_counter() - t0
+
+    # calibrate the per-row cost net of the fixed per-call cost (zeroing the
+    # per-worker n x n partials and their ordered sum), then take a sample of
+    # about target_s seconds
+    k1, k2 = max(1, workers), 4 * max(1, workers)
+    _, t1 = run_rows(k1)
+    _, t2 = run_rows(k2)
+    per_row = max((t2 - t1) / (k2 - k1), 1e-6)
+    k = max(k2, min(nf, int(target_s / per_row)))
+    pairs, t = run_rows(k)
+    return {"value": pairs / t, "unit": UNIT, "cores": workers, "kind": "port",
+            "sample": f"oracle assemble_W on the last {k} pair rows ({pairs} of {total} pairs) of config {cfg}, "
+                      f"{t:.1f} s", "seconds": t, "pairs": pairs}
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    cfg = args.config
+    samples = []
+    for i in range(args.warmup + args.steps):
+        r = cpu_assembly_sample(cfg, args.ratio, max(2.0, args.cpu_seconds / 2))
+        if i >= args.warmup:
+            samples.append(r)
+    v = sum(s["pairs"] for s in samples) / sum(s["seconds"] for s in samples)
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(s["seconds"] for s in samples) / len(samples),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"config {cfg}: {CFG_NAMES[cfg]}", "sample": samples[-1]["sample"]},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": samples[-1]["cores"], "kind": "port",
+                             "sample": samples[-1]["sample"]},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------- ours
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+def run_ours(args):
+    import numpy as np
+
+    from paper_2310_09204_b200 import screenbem as S
+    rank, world, local = dist_env()
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    ctx = S.Context(local)
+    ctx.timers(True)
+    cfg = args.config
+    ratio = args.ratio if args.ratio else (8 if cfg == 5 else 0)
+    pair = S.make_config(cfg, ratio)
+    fine = S.inflate(pair.fine, validate=cfg <= 3)
+    coarse = S.inflate(pair.coarse)
+    part = S.partition_dofs(pair, fine)
+    P = S.build_prolongation(pair, coarse, fine)
+    g = S.config_g(cfg)
+    nf, n = pair.fine.nf, fine.n
+    npairs = nf * (nf + 1) // 2
+    plan = S.AssemblyPlan(fine, ctx=ctx)
+
+    def step(W):
+        W = plan.run(W)
+        L = S.assemble_rhs(fine, g, ctx=ctx)
+        prec = S.build_preconditioner(W, part, P)
+        rep = S.pcg(W, prec, L, 1e-8)
+        return W, prec, rep
+
+    W = None
+    for _ in range(args.warmup):
+        ctx.l2_flush()
+        W, prec, rep = step(W)
+    ctx.synchronize()
+    ctx.reset_timers()
+    launches0 = S.launch_count()
+    iters = []
+    if dist:
+        dist.barrier()
+    with ClockSampler(local) as clocks:
+        for _ in range(args.steps):
+            ctx.l2_flush()
+            ctx.begin("step")
+            W, prec, rep = step(W)
+            ctx.end()
+            iters.append(rep.iterations)
+        ctx.synchronize()
+    launches = S.launch_count() - launches0
+    tm = {k: ctx.timer(k) for k in ("step", "assemble_W", "far_tiles", "near", "near_leaves", "sauter", "classify",
+                                     "local_scatter", "mirror", "cholesky", "coarse_galerkin", "pcg", "gemv_f64",
+                                     "precond_apply")}
+    ms = {k: (v[0] / v[1] if v[1] else 0.0) for k, v in tm.items()}
+    t_asm = ms["assemble_W"] * 1e-3
+    step_ms = ms["step"]
+    if dist:
+        import torch
+        t = torch.tensor([t_asm, step_ms], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_asm, step_ms = float(t[0]), float(t[1])
+    value = world * npairs / t_asm
+    stats = W.stats
+    # ---- dominant-kernel roofline (FP64 pipe): SURVEY.md §8d 20 flop per tensor-rule evaluation
+    fp64_peak = S.fp64_peak_tflops(ctx)
+    far_ms = tm["far_tiles"][0] / max(tm["far_tiles"][1], 1)
+    near_ms = tm["near_leaves"][0] / max(tm["near_leaves"][1], 1)
+    far_flop = 20.0 * 256 * stats["far_pairs"]
+    near_flop = 20.0 * 1296 * stats["near_leaves"]
+    dom = ("far_tiles", far_flop, far_ms) if far_ms >= near_ms else ("near_leaves", near_flop, near_ms)
+    achieved = dom[1] / (dom[2] * 1e-3) / 1e12 if dom[2] > 0 else 0.0
+    # ---- matvec (HBM) and preconditioner applies, L2 flushed between launches
+    ctx.reset_timers()
+    import ctypes as C
+    dx = C.c_void_p()
+    dy = C.c_void_p()
+    ldp = (n + 31) // 32 * 32
+    S._check(S.lib().sbg_device_alloc(ctx.h, 8 * ldp, C.byref(dx)))
+    S._check(S.lib().sbg_device_alloc(ctx.h, 8 * ldp, C.byref(dy)))
+    xh = np.random.default_rng(0).standard_normal(n)
+    S._check(S.lib().sbg_memcpy_h2d(ctx.h, dx, xh.ctypes.data_as(C.c_void_p), 8 * n))
+    for _ in range(3):
+        S._check(S.lib().sbg_matvec_device(ctx.h, W.h, dx, dy, 1))
+    ctx.reset_timers()
+    reps = 20
+    for _ in range(reps):
+        ctx.l2_flush()
+        S._check(S.lib().sbg_matvec_device(ctx.h, W.h, dx, dy, 1))
+        S._check(S.lib().sbg_apply_preconditioner_device(ctx.h, prec.h, dx, dy, 1))
+    gm, gc = ctx.timer("gemv_f64")
+    am, ac = ctx.timer("precond_apply")
+    S.lib().sbg_device_free(dx)
+    S.lib().sbg_device_free(dy)
+    matvec_s = gm / gc * 1e-3
+    matvec_bytes = 8.0 * n * n + 16.0 * n
+    matvec_gbs = matvec_bytes / matvec_s / 1e9
+    peaks = load_peaks()
+    hbm_peak = peaks.get("hbm_gbs") or 6650.0
+    # ---- e2e: public assemble_W with host mesh in, host W out
+    e2e_times = []
+    h2d = 8 * 3 * pair.fine.nv + 4 * 3 * nf
+    for _ in range(1 + min(args.steps, 2)):
+        ctx.reset_timers()
+        t0 = time.perf_counter()
+        ctx.begin("e2e")
+        mesh = S.SurfaceMesh(pair.fine.vertices, pair.fine.facets)
+        im2 = S.inflate(mesh, validate=False)
+        W2 = S.assemble_W(im2, ctx=ctx)
+        Wh = W2.download()
+        ctx.end()
+        ctx.synchronize()
+        e2e_times.append(ctx.timer("e2e")[0] * 1e-3)
+        del W2, Wh
+    e2e_t = min(e2e_times[1:]) if len(e2e_times) > 1 else e2e_times[0]
+    if dist:
+        import torch
+        t = torch.tensor([e2e_t], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_t = float(t[0])
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_assembly_sample(cfg, ratio, args.cpu_seconds)
+            cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        except Exception as e:  # pragma: no cover
+            cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "port", "sample": f"failed: {e}"}
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"config {cfg}: {CFG_NAMES[cfg]}" + (f", H/h {ratio}" if cfg == 5 else ""),
+                       "triangles": nf, "dofs": n, "tri_pairs": npairs, "parallelism": f"replicas x{world}",
+                       "l2": "flushed (256 MiB write) before every timed step and every matvec/apply launch",
+                       "pcg_tol": 1e-8},
+            "roofline": {"bound": "fp64", "kernel": dom[0], "achieved": achieved, "peak": fp64_peak,
+                         "unit": "TFLOP/s", "frac": achieved / fp64_peak if fp64_peak else None, "traffic": None,
+                         "peak_source": "DFMA loop measured by bench.py on this GPU (MEASURED_PEAKS.json has no fp64)",
+                         "flop_convention": "20 flop per tensor-rule kernel evaluation (SURVEY.md §8d)"},
+            "roofline_matvec": {"bound": "hbm", "kernel": "gemv_f64", "achieved": matvec_gbs, "peak": hbm_peak,
+                                "unit": "GB/s", "frac": matvec_gbs / hbm_peak, "traffic": None,
+                                "bytes_per_launch": matvec_bytes, "us_per_launch": matvec_s * 1e6,
+                                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks.get("hbm_gbs") else "fallback"},
+            "pcg": {"iterations": iters[-1], "iters_per_s": iters[-1] / (ms["pcg"] * 1e-3) if ms["pcg"] else None,
+                    "ms": ms["pcg"], "kappa_lanczos": rep.kappa_estimate,
+                    "precond_applies_per_s": 1e3 / (am / ac) if ac else None, "precond_apply_us": 1e3 * am / ac if ac else None,
+                    "precond_factor_bytes": prec.factor_bytes()},
+            "time_to_solution_ms": step_ms,
+            "phases_ms": {k: round(v, 4) for k, v in ms.items()},
+            "assembly_stats": stats,
+            "e2e": {"value": world * npairs / e2e_t, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": 8 * n * n, "ms": e2e_t * 1e3,
+                    "what": "S.assemble_W(host mesh) + W.download(): plan build, H2D, kernels, D2H of W"},
+            "gpu_launches": launches,
+            "clocks": clocks.summary(),
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

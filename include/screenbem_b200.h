@@ -43,6 +43,7 @@ typedef struct sbg_matrix sbg_matrix;       /* GalerkinMatrix   (inc/assemble.hp
 typedef struct sbg_partition sbg_partition; /* DofPartition     (inc/schwarz.hpp:14-17) */
 typedef struct sbg_prolong sbg_prolong;     /* Prolongation     (inc/jump.hpp:87-89) */
 typedef struct sbg_prec sbg_prec;           /* SchwarzPreconditioner (inc/schwarz.hpp:55-73), device-resident */
+typedef struct sbg_aplan sbg_aplan;         /* assembly plan: mesh-derived device data of assemble_W */
 
 /* QuadratureConfig (inc/quadrature.hpp:12-16) */
 typedef struct {
@@ -76,6 +77,11 @@ int sbg_device_name(int device, char* buf, int cap, int* sm_count);
 int sbg_timers_enable(sbg_ctx* ctx, int on);
 int sbg_timers_reset(sbg_ctx* ctx);
 int sbg_timer_get(sbg_ctx* ctx, const char* name, double* total_ms, long long* count);
+/* user intervals on the same timer set (CUDA events on the context stream) */
+int sbg_timer_begin(sbg_ctx* ctx, const char* name);
+int sbg_timer_end(sbg_ctx* ctx);
+/* kernels launched by this library so far (all contexts) */
+long long sbg_launch_count(void);
 
 /* ---- meshes (host) ------------------------------------------------------ */
 int sbg_mesh_create(int nv, const double* verts, int nf, const int32_t* facets, sbg_mesh** out);
@@ -88,6 +94,9 @@ int sbg_refine_uniform_times(const sbg_mesh* m, int k, sbg_level** out); /* inc/
 int sbg_level_create(const sbg_mesh* coarse, const sbg_mesh* fine, const int32_t* parent, sbg_level** out);
 int sbg_make_config(int cfg, int ratio, sbg_level** out);      /* BASELINE.json configs 1-5 (ratio 0 = default H/h) */
 int sbg_make_panels(int kind, int m, int r, sbg_level** out);  /* 0 flat, 1 T-junction, 2 triple cross */
+/* Neumann field g of a BASELINE config: constant, or for cfg 2 / 4 the unit vector of three
+ * std::normal_distribution<double> draws from std::mt19937(seed 1 / 7) (tests/test_pcg.cpp:14-15) */
+int sbg_config_g(int cfg, double* g3);
 int sbg_level_mesh(const sbg_level* l, int fine, sbg_mesh** out); /* copy of the coarse (0) / fine (1) mesh */
 int sbg_level_parent(const sbg_level* l, int32_t* parent);
 int sbg_level_sizes(const sbg_level* l, double* H, double* h);
@@ -105,6 +114,12 @@ int sbg_inflated_export(const sbg_inflated* im, int32_t* q, int32_t* gv_first, i
 /* assemble_W (inc/assemble.hpp:72-139); `workers` is accepted and ignored */
 int sbg_assemble_w(sbg_ctx* ctx, const sbg_inflated* im, const sbg_quad_cfg* cfg, int workers, sbg_matrix** out,
                    sbg_assembly_stats* stats);
+/* the same split in two: host preparation of one mesh (facet blocks, curl lists,
+ * singular lists, rules, uploaded once) and the device-only assembly, which
+ * (re)fills *W (allocated on first use) */
+int sbg_assembly_plan_create(sbg_ctx* ctx, const sbg_inflated* im, const sbg_quad_cfg* cfg, sbg_aplan** out);
+int sbg_assembly_run(sbg_aplan* plan, sbg_matrix** W, sbg_assembly_stats* stats);
+void sbg_assembly_plan_destroy(sbg_aplan* plan);
 int sbg_matrix_create(sbg_ctx* ctx, int n, const double* host_rowmajor, sbg_matrix** out);
 int sbg_matrix_n(const sbg_matrix* W);
 int sbg_matrix_download(const sbg_matrix* W, double* host_rowmajor);
@@ -170,6 +185,8 @@ int sbg_matvec_device(sbg_ctx* ctx, const sbg_matrix* W, const double* d_x, doub
 int sbg_apply_preconditioner_device(sbg_ctx* ctx, sbg_prec* p, const double* d_r, double* d_z, int reps);
 /* write a buffer larger than L2 (L2 flush between timed iterations) */
 int sbg_l2_flush(sbg_ctx* ctx);
+/* measured DFMA throughput of this device (TFLOP/s), the FP64 roofline denominator */
+int sbg_fp64_peak(sbg_ctx* ctx, double* tflops);
 
 #ifdef __cplusplus
 }

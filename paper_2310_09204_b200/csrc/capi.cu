@@ -1,5 +1,7 @@
 // C ABI (include/screenbem_b200.h) over the host layer and the device modules.
 #include <cstring>
+#include <memory>
+#include <random>
 #include <fstream>
 
 #include "../../include/screenbem_b200.h"
@@ -32,6 +34,18 @@ struct sbg_prec {
     Prec* P = nullptr;
     ~sbg_prec() { prec_destroy(P); }
 };
+struct sbg_aplan {
+    AssemblyPlan* P = nullptr;
+    Ctx* ctx = nullptr;
+    ~sbg_aplan() { assembly_plan_destroy(P); }
+};
+namespace {
+struct UserScope {
+    std::string name;
+    std::unique_ptr<TimedScope> ts;
+};
+thread_local std::vector<std::unique_ptr<UserScope>> g_user_scopes;
+}  // namespace
 
 namespace {
 thread_local std::string g_err;
@@ -150,6 +164,26 @@ int sbg_timer_get(sbg_ctx* ctx, const char* name, double* total_ms, long long* c
     });
 }
 
+int sbg_timer_begin(sbg_ctx* ctx, const char* name)
+{
+    return guard([&] {
+        auto u = std::make_unique<UserScope>();
+        u->name = name;
+        u->ts = std::make_unique<TimedScope>(&ctx->c, u->name.c_str());
+        g_user_scopes.push_back(std::move(u));
+    });
+}
+int sbg_timer_end(sbg_ctx* ctx)
+{
+    return guard([&] {
+        (void)ctx;
+        if (g_user_scopes.empty()) throw ValidationError("sbg_timer_end without sbg_timer_begin");
+        g_user_scopes.back()->ts.reset();
+        g_user_scopes.pop_back();
+    });
+}
+long long sbg_launch_count(void) { return launch_count(); }
+
 // ---------------------------------------------------------------- meshes
 int sbg_mesh_create(int nv, const double* verts, int nf, const int32_t* facets, sbg_mesh** out)
 {
@@ -241,6 +275,29 @@ int sbg_make_panels(int kind, int m, int r, sbg_level** out)
             throw;
         }
         *out = l;
+    });
+}
+int sbg_config_g(int cfg, double* g)
+{
+    return guard([&] {
+        if (cfg == 2 || cfg == 4) {
+            std::mt19937 rng(cfg == 2 ? 1u : 7u);
+            std::normal_distribution<double> dist;
+            double v[3];
+            for (double& x : v) x = dist(rng);
+            const double nrm = std::sqrt((v[0] * v[0] + v[1] * v[1]) + v[2] * v[2]);
+            for (int k = 0; k < 3; ++k) g[k] = v[k] / nrm;
+        } else if (cfg == 3) {
+            g[0] = 1.0;
+            g[1] = 0.5;
+            g[2] = 0.25;
+        } else if (cfg == 1 || cfg == 5) {
+            g[0] = 0.0;
+            g[1] = 0.0;
+            g[2] = 1.0;
+        } else {
+            throw ValidationError("unknown BASELINE config " + std::to_string(cfg));
+        }
     });
 }
 int sbg_level_mesh(const sbg_level* l, int fine, sbg_mesh** out)
@@ -340,6 +397,50 @@ int sbg_assemble_w(sbg_ctx* ctx, const sbg_inflated* im, const sbg_quad_cfg* cfg
         *out = W;
     });
 }
+int sbg_assembly_plan_create(sbg_ctx* ctx, const sbg_inflated* im, const sbg_quad_cfg* cfg, sbg_aplan** out)
+{
+    return guard([&] {
+        auto* p = new sbg_aplan;
+        p->ctx = &ctx->c;
+        try {
+            p->P = assembly_plan_create(&ctx->c, im->im, qcfg(cfg));
+        } catch (...) {
+            delete p;
+            throw;
+        }
+        *out = p;
+    });
+}
+int sbg_assembly_run(sbg_aplan* plan, sbg_matrix** W, sbg_assembly_stats* stats)
+{
+    return guard([&] {
+        need(W, "W");
+        const bool fresh = *W == nullptr;
+        if (fresh) *W = new sbg_matrix;
+        try {
+            AssemblyStats st;
+            assembly_run(plan->P, (*W)->M, &st);
+            SBG_CUDA(cudaStreamSynchronize(plan->ctx->stream));
+            if (stats) {
+                stats->far_pairs = st.far_pairs;
+                stats->near_pairs = st.near_pairs;
+                stats->identical = st.identical;
+                stats->edge = st.edge;
+                stats->vertex = st.vertex;
+                stats->near_leaves = st.near_leaves;
+                stats->tiles = st.tiles;
+                stats->tiles_skipped = st.tiles_skipped;
+            }
+        } catch (...) {
+            if (fresh) {
+                delete *W;
+                *W = nullptr;
+            }
+            throw;
+        }
+    });
+}
+void sbg_assembly_plan_destroy(sbg_aplan* plan) { delete plan; }
 int sbg_matrix_create(sbg_ctx* ctx, int n, const double* host, sbg_matrix** out)
 {
     return guard([&] {
@@ -678,6 +779,10 @@ int sbg_apply_preconditioner_device(sbg_ctx* ctx, sbg_prec* p, const double* d_r
         for (int i = 0; i < reps; ++i) prec_apply(&ctx->c, p->P, d_r, d_z, nullptr);
         SBG_CUDA(cudaStreamSynchronize(ctx->c.stream));
     });
+}
+int sbg_fp64_peak(sbg_ctx* ctx, double* tflops)
+{
+    return guard([&] { *tflops = fp64_peak_tflops(&ctx->c); });
 }
 int sbg_l2_flush(sbg_ctx* ctx)
 {

@@ -33,7 +33,6 @@ constexpr int NF = 16;          // far rule points (far_order 4)
 constexpr int NN = 36;          // near rule points (far_order + 2 = 6)
 constexpr int SAUTER_THREADS = 128;
 constexpr int SAUTER_STAGE = 1024;  // rule points staged per smem pass
-constexpr int NEAR_WARPS = 8;
 
 __constant__ double c_far_u[NF], c_far_v[NF], c_far_w[NF];
 __constant__ double c_near_u[NN], c_near_v[NN], c_near_w[NN];
@@ -276,11 +275,15 @@ __global__ void k_classify_near(const TileInfo* __restrict__ tiles, GeoPtrs G, c
 }
 
 // ---------------------------------------------------------------- near pairs (recursion)
-struct NearFrame {
-    double t[9], s[9], kids[36];
-    int split_t, next, expanded, pad;
-};
-
+// The split4 recursion of triangle_pair_disjoint (quadrature.hpp:231-249) is
+// run in three phases:
+//   N1/N3  one thread per pair walks the recursion depth-first in the
+//          reference's child order with no-FMA classification (bitwise the
+//          oracle's decisions), first counting, then writing its leaves as
+//          18-bit path codes (depth | per level: split side, child index);
+//   N4     leaves are evaluated two per warp (one per half-warp, a 9x9 block
+//          of the 36x36 rule per lane) after replaying the path from the root;
+//   N5     one thread per pair sums its leaves in depth-first order.
 __device__ __forceinline__ double tri_diam(const double* t)
 {
     const D3 a = {t[0], t[1], t[2]}, b = {t[3], t[4], t[5]}, c = {t[6], t[7], t[8]};
@@ -298,169 +301,239 @@ __device__ __forceinline__ double tri_area(const double* t)
     const D3 a = {t[0], t[1], t[2]}, b = {t[3], t[4], t[5]}, c = {t[6], t[7], t[8]};
     return __dmul_rn(0.5, d3_norm(d3_cross(d3_sub(b, a), d3_sub(c, a))));
 }
-// split4 children {v0,m01,m02},{m01,v1,m12},{m02,m12,v2},{m01,m12,m02} (quadrature.hpp:222-229)
-__device__ __forceinline__ void split4(const double* t, double* kids)
+// child k of split4 (quadrature.hpp:222-229): {v0,m01,m02},{m01,v1,m12},{m02,m12,v2},{m01,m12,m02}
+__device__ __forceinline__ void split4_child(const double* t, int k, double* out)
 {
-    double m01[3], m12[3], m02[3];
+#pragma unroll
     for (int c = 0; c < 3; ++c) {
-        m01[c] = __dmul_rn(0.5, __dadd_rn(t[c], t[3 + c]));
-        m12[c] = __dmul_rn(0.5, __dadd_rn(t[3 + c], t[6 + c]));
-        m02[c] = __dmul_rn(0.5, __dadd_rn(t[c], t[6 + c]));
-    }
-    for (int c = 0; c < 3; ++c) {
-        kids[0 * 9 + 0 + c] = t[c];
-        kids[0 * 9 + 3 + c] = m01[c];
-        kids[0 * 9 + 6 + c] = m02[c];
-        kids[1 * 9 + 0 + c] = m01[c];
-        kids[1 * 9 + 3 + c] = t[3 + c];
-        kids[1 * 9 + 6 + c] = m12[c];
-        kids[2 * 9 + 0 + c] = m02[c];
-        kids[2 * 9 + 3 + c] = m12[c];
-        kids[2 * 9 + 6 + c] = t[6 + c];
-        kids[3 * 9 + 0 + c] = m01[c];
-        kids[3 * 9 + 3 + c] = m12[c];
-        kids[3 * 9 + 6 + c] = m02[c];
+        const double v0 = t[c], v1 = t[3 + c], v2 = t[6 + c];
+        const double m01 = __dmul_rn(0.5, __dadd_rn(v0, v1));
+        const double m12 = __dmul_rn(0.5, __dadd_rn(v1, v2));
+        const double m02 = __dmul_rn(0.5, __dadd_rn(v0, v2));
+        double a, b, d;
+        if (k == 0) {
+            a = v0; b = m01; d = m02;
+        } else if (k == 1) {
+            a = m01; b = v1; d = m12;
+        } else if (k == 2) {
+            a = m02; b = m12; d = v2;
+        } else {
+            a = m01; b = m12; d = m02;
+        }
+        out[c] = a;
+        out[3 + c] = b;
+        out[6 + c] = d;
     }
 }
 
-// Evaluate the 36x36 rule on up to two leaves: half-warp h takes leaf h; each
-// lane owns a 9x9 block (i in [9*ia, 9*ia+9), j in [9*jb, 9*jb+9)).
-__device__ __forceinline__ double near_leaf_eval(const double* leaf /* 2 x 19 */, int nleaves, int lane)
+// Depth-first walk of one pair; returns the number of leaves and, when
+// codes != nullptr, writes their path codes in visiting order.
+__device__ int near_walk(const double* root_t, const double* root_s, double thr, unsigned* codes)
 {
-    const int h = lane >> 4;
-    if (h >= nleaves) return 0.0;
-    const double* L = leaf + 19 * h;
-    const double* t = L;
-    const double* s = L + 9;
-    const double scale = L[18];
-    const int l16 = lane & 15, ia = l16 >> 2, jb = l16 & 3;
-    const double e1x = s[3] - s[0], e1y = s[4] - s[1], e1z = s[5] - s[2];
-    const double e2x = s[6] - s[0], e2y = s[7] - s[1], e2z = s[8] - s[2];
-    double yx[9], yy[9], yz[9], wj[9];
-#pragma unroll
+    double T[6][9], Sv[6][9];
+    int child[6], side[6];
     for (int q = 0; q < 9; ++q) {
-        const int j = 9 * jb + q;
-        const double u = c_near_u[j], v = c_near_v[j];
-        yx[q] = fma(v, e2x, fma(u, e1x, s[0]));
-        yy[q] = fma(v, e2y, fma(u, e1y, s[1]));
-        yz[q] = fma(v, e2z, fma(u, e1z, s[2]));
-        wj[q] = c_near_w[j];
+        T[0][q] = root_t[q];
+        Sv[0][q] = root_s[q];
     }
-    const double f1x = t[3] - t[0], f1y = t[4] - t[1], f1z = t[5] - t[2];
-    const double f2x = t[6] - t[0], f2y = t[7] - t[1], f2z = t[8] - t[2];
-    double acc = 0.0;
-#pragma unroll 1
-    for (int p = 0; p < 9; ++p) {
-        const int i = 9 * ia + p;
-        const double u = c_near_u[i], v = c_near_v[i];
-        const double xx = fma(v, f2x, fma(u, f1x, t[0]));
-        const double xy = fma(v, f2y, fma(u, f1y, t[1]));
-        const double xz = fma(v, f2z, fma(u, f1z, t[2]));
-        double in = 0.0;
-#pragma unroll
-        for (int q = 0; q < 9; ++q) {
-            const double dx = xx - yx[q], dy = xy - yy[q], dz = xz - yz[q];
-            in = fma(wj[q], rsqrt_fast(fma(dx, dx, fma(dy, dy, dz * dz))), in);
+    int d = 0, count = 0;
+    while (true) {
+        // visit node d
+        bool leaf = d >= 5;
+        int split_t = 0;
+        if (!leaf) {
+            const double dt = tri_diam(T[d]), ds = tri_diam(Sv[d]);
+            D3 ct, cs;
+            double rt, rs;
+            tri_centroid_rad(T[d], ct, rt);
+            tri_centroid_rad(Sv[d], cs, rs);
+            const double dist = fmax(0.0, __dsub_rn(__dsub_rn(d3_norm(d3_sub(ct, cs)), rt), rs));
+            leaf = dist >= __dmul_rn(thr, fmax(dt, ds));
+            split_t = dt >= ds ? 1 : 0;
         }
-        acc = fma(c_near_w[i], in, acc);
+        if (leaf) {
+            if (codes) {
+                unsigned code = (unsigned)d;
+                for (int l = 0; l < d; ++l) code |= (unsigned)(side[l] | (child[l] << 1)) << (3 + 3 * l);
+                codes[count] = code;
+            }
+            ++count;
+            // advance to the next sibling (or pop)
+            bool done = true;
+            while (d > 0) {
+                const int p = d - 1;
+                if (++child[p] < 4) {
+                    if (side[p]) {
+                        split4_child(T[p], child[p], T[d]);
+                        for (int q = 0; q < 9; ++q) Sv[d][q] = Sv[p][q];
+                    } else {
+                        split4_child(Sv[p], child[p], Sv[d]);
+                        for (int q = 0; q < 9; ++q) T[d][q] = T[p][q];
+                    }
+                    done = false;
+                    break;
+                }
+                --d;
+            }
+            if (done) break;
+        } else {
+            side[d] = split_t;
+            child[d] = 0;
+            if (split_t) {
+                split4_child(T[d], 0, T[d + 1]);
+                for (int q = 0; q < 9; ++q) Sv[d + 1][q] = Sv[d][q];
+            } else {
+                split4_child(Sv[d], 0, Sv[d + 1]);
+                for (int q = 0; q < 9; ++q) T[d + 1][q] = T[d][q];
+            }
+            ++d;
+        }
     }
-    return acc * scale;
+    return count;
 }
 
-// One warp per near pair (dynamic scheduling).  The recursion of
-// triangle_pair_disjoint (quadrature.hpp:231-249) is walked iteratively with a
-// per-warp frame stack in shared memory; all lanes take the same branches.
-__global__ void __launch_bounds__(NEAR_WARPS * 32)
-    k_near_pairs(const int2* __restrict__ pairs, long long npairs, const double* __restrict__ GV, double thr,
-                 double* __restrict__ out, unsigned long long* __restrict__ next, double inv_pi,
-                 unsigned long long* __restrict__ leaf_count)
+__global__ void k_near_count(const int2* __restrict__ pairs, const unsigned long long* __restrict__ np_dev,
+                             long long cap, const double* __restrict__ GV, double thr, long long* __restrict__ nleaf)
 {
-    __shared__ NearFrame frames[NEAR_WARPS][6];
-    __shared__ double leafbuf[NEAR_WARPS][2 * 19];
-    __shared__ long long cur[NEAR_WARPS];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    NearFrame* F = frames[warp];
-    double* LB = leafbuf[warp];
-    unsigned long long leaves_total = 0;
-    while (true) {
-        if (lane == 0) cur[warp] = (long long)atomicAdd(next, 1ull);
-        __syncwarp();
-        const long long pi = cur[warp];
-        if (pi >= npairs) break;
-        const int2 pr = pairs[pi];  // (t, s) = (larger index, smaller index)
-        if (lane == 0) {
-            for (int k = 0; k < 9; ++k) {
-                F[0].t[k] = GV[9 * pr.x + k];
-                F[0].s[k] = GV[9 * pr.y + k];
-            }
-            F[0].expanded = 0;
-        }
-        __syncwarp();
-        int depth = 0, nleaf = 0;
-        double acc = 0.0;
-        while (depth >= 0) {
-            NearFrame& fr = F[depth];
-            if (!fr.expanded) {
-                const double dt = tri_diam(fr.t), ds = tri_diam(fr.s);
-                D3 ct, cs;
-                double rt, rs;
-                tri_centroid_rad(fr.t, ct, rt);
-                tri_centroid_rad(fr.s, cs, rs);
-                const double dist = fmax(0.0, __dsub_rn(__dsub_rn(d3_norm(d3_sub(ct, cs)), rt), rs));
-                const bool leaf = dist >= __dmul_rn(thr, fmax(dt, ds)) || depth >= 5;
-                if (leaf) {
-                    const double sc = __dmul_rn(tri_area(fr.t), tri_area(fr.s));
-                    if (lane == 0) {
-                        for (int k = 0; k < 9; ++k) {
-                            LB[19 * nleaf + k] = fr.t[k];
-                            LB[19 * nleaf + 9 + k] = fr.s[k];
-                        }
-                        LB[19 * nleaf + 18] = sc;
-                    }
-                    __syncwarp();
-                    ++nleaf;
-                    ++leaves_total;
-                    if (nleaf == 2) {
-                        acc += near_leaf_eval(LB, 2, lane);
-                        nleaf = 0;
-                        __syncwarp();
-                    }
-                    --depth;
-                    continue;
-                }
-                const int split_t = dt >= ds ? 1 : 0;
-                if (lane == 0) {
-                    split4(split_t ? fr.t : fr.s, fr.kids);
-                    fr.split_t = split_t;
-                    fr.next = 0;
-                    fr.expanded = 1;
-                }
-                __syncwarp();
-            }
-            if (fr.next == 4) {
-                --depth;
-                continue;
-            }
-            const int k = fr.next;
-            __syncwarp();
-            if (lane == 0) {
-                fr.next = k + 1;
-                NearFrame& ch = F[depth + 1];
-                for (int q = 0; q < 9; ++q) {
-                    ch.t[q] = fr.split_t ? fr.kids[9 * k + q] : fr.t[q];
-                    ch.s[q] = fr.split_t ? fr.s[q] : fr.kids[9 * k + q];
-                }
-                ch.expanded = 0;
-            }
-            __syncwarp();
-            ++depth;
-        }
-        if (nleaf) acc += near_leaf_eval(LB, nleaf, lane);
-        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if (lane == 0) out[pi] = acc * inv_pi;
-        __syncwarp();
+    const long long np = min((long long)*np_dev, cap);
+    for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < np; p += (long long)gridDim.x * blockDim.x) {
+        const int2 pr = pairs[p];
+        nleaf[p] = near_walk(GV + 9 * pr.x, GV + 9 * pr.y, thr, nullptr);
     }
-    if (leaf_count && lane == 0) atomicAdd(leaf_count, leaves_total);
+}
+
+__global__ void k_near_fill(const int2* __restrict__ pairs, const unsigned long long* __restrict__ np_dev,
+                            long long cap, const double* __restrict__ GV, double thr,
+                            const long long* __restrict__ off, unsigned* __restrict__ codes, int* __restrict__ owner)
+{
+    const long long np = min((long long)*np_dev, cap);
+    for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < np; p += (long long)gridDim.x * blockDim.x) {
+        const int2 pr = pairs[p];
+        const long long o = off[p];
+        const int c = near_walk(GV + 9 * pr.x, GV + 9 * pr.y, thr, codes + o);
+        for (int k = 0; k < c; ++k) owner[o + k] = (int)p;
+    }
+}
+
+// exclusive scan of per-pair leaf counts (single CTA, chunked; counts are small)
+__global__ void k_scan_exclusive(const long long* __restrict__ in, const unsigned long long* __restrict__ np_dev,
+                                 long long cap, long long* __restrict__ out, long long* __restrict__ total)
+{
+    __shared__ long long part[1024];
+    __shared__ long long carry;
+    const long long n = min((long long)*np_dev, cap);
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    const int T = blockDim.x;
+    for (long long base = 0; base < n; base += (long long)T * 8) {
+        long long v[8], s = 0;
+        for (int k = 0; k < 8; ++k) {
+            const long long i = base + (long long)threadIdx.x * 8 + k;
+            v[k] = i < n ? in[i] : 0;
+            s += v[k];
+        }
+        part[threadIdx.x] = s;
+        __syncthreads();
+        for (int o = 1; o < T; o <<= 1) {
+            const long long add = threadIdx.x >= o ? part[threadIdx.x - o] : 0;
+            __syncthreads();
+            part[threadIdx.x] += add;
+            __syncthreads();
+        }
+        long long run = carry + part[threadIdx.x] - s;
+        for (int k = 0; k < 8; ++k) {
+            const long long i = base + (long long)threadIdx.x * 8 + k;
+            if (i < n) out[i] = run;
+            run += v[k];
+        }
+        __syncthreads();
+        if (threadIdx.x == T - 1) carry += part[T - 1];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *total = carry;
+}
+
+// N4: two leaves per warp; lane (ia, jb) of each half-warp owns i in [9ia, 9ia+9), j in [9jb, 9jb+9)
+__global__ void __launch_bounds__(256) k_near_leaves(const unsigned* __restrict__ codes, const int* __restrict__ owner,
+                                                     long long nleaves, const int2* __restrict__ pairs,
+                                                     const double* __restrict__ GV, double* __restrict__ leaf_val)
+{
+    const int lane = threadIdx.x & 31;
+    const int h = lane >> 4, l16 = lane & 15, ia = l16 >> 2, jb = l16 & 3;
+    const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
+    for (long long w = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); 2 * w < nleaves; w += warps) {
+        const long long q = 2 * w + h;
+        const bool active = q < nleaves;
+        double acc = 0.0, scale = 0.0;
+        if (active) {
+            const unsigned code = codes[q];
+            const int2 pr = pairs[owner[q]];
+            double t[9], s[9], tmp[9];
+            for (int c = 0; c < 9; ++c) {
+                t[c] = GV[9 * pr.x + c];
+                s[c] = GV[9 * pr.y + c];
+            }
+            const int depth = code & 7;
+            for (int lv = 0; lv < depth; ++lv) {
+                const unsigned e = (code >> (3 + 3 * lv)) & 7;
+                if (e & 1) {
+                    split4_child(t, (int)(e >> 1), tmp);
+                    for (int c = 0; c < 9; ++c) t[c] = tmp[c];
+                } else {
+                    split4_child(s, (int)(e >> 1), tmp);
+                    for (int c = 0; c < 9; ++c) s[c] = tmp[c];
+                }
+            }
+            scale = tri_area(t) * tri_area(s);
+            const double e1x = s[3] - s[0], e1y = s[4] - s[1], e1z = s[5] - s[2];
+            const double e2x = s[6] - s[0], e2y = s[7] - s[1], e2z = s[8] - s[2];
+            double yx[9], yy[9], yz[9];
+#pragma unroll
+            for (int k = 0; k < 9; ++k) {
+                const int j = 9 * jb + k;
+                yx[k] = fma(c_near_v[j], e2x, fma(c_near_u[j], e1x, s[0]));
+                yy[k] = fma(c_near_v[j], e2y, fma(c_near_u[j], e1y, s[1]));
+                yz[k] = fma(c_near_v[j], e2z, fma(c_near_u[j], e1z, s[2]));
+            }
+            const double f1x = t[3] - t[0], f1y = t[4] - t[1], f1z = t[5] - t[2];
+            const double f2x = t[6] - t[0], f2y = t[7] - t[1], f2z = t[8] - t[2];
+#pragma unroll 1
+            for (int p = 0; p < 9; ++p) {
+                const int i = 9 * ia + p;
+                const double xx = fma(c_near_v[i], f2x, fma(c_near_u[i], f1x, t[0]));
+                const double xy = fma(c_near_v[i], f2y, fma(c_near_u[i], f1y, t[1]));
+                const double xz = fma(c_near_v[i], f2z, fma(c_near_u[i], f1z, t[2]));
+                double in0 = 0.0, in1 = 0.0;
+#pragma unroll
+                for (int k = 0; k < 9; ++k) {
+                    const double dx = xx - yx[k], dy = xy - yy[k], dz = xz - yz[k];
+                    const double r = rsqrt_fast(fma(dx, dx, fma(dy, dy, dz * dz)));
+                    if (k & 1)
+                        in1 = fma(c_near_w[9 * jb + k], r, in1);
+                    else
+                        in0 = fma(c_near_w[9 * jb + k], r, in0);
+                }
+                acc = fma(c_near_w[i], in0 + in1, acc);
+            }
+        }
+        // reduce over the 16 lanes of each half-warp
+        for (int o = 8; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (active && l16 == 0) leaf_val[q] = acc * scale;
+    }
+}
+
+// N5: I = sum of the pair's leaves (visiting order) / pi
+__global__ void k_near_reduce(const long long* __restrict__ off, const long long* __restrict__ nleaf,
+                              const unsigned long long* __restrict__ np_dev, long long cap,
+                              const double* __restrict__ leaf_val, double inv_pi, double* __restrict__ out)
+{
+    const long long np = min((long long)*np_dev, cap);
+    for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < np; p += (long long)gridDim.x * blockDim.x) {
+        double s = 0.0;
+        const long long o = off[p];
+        for (long long k = 0; k < nleaf[p]; ++k) s += leaf_val[o + k];
+        out[p] = s * inv_pi;
+    }
 }
 
 // ---------------------------------------------------------------- Sauter (singular) pairs
@@ -674,7 +747,7 @@ void upload_geometry(Ctx* ctx, const SurfaceMesh& m, DeviceGeometry& G)
     G.vid.alloc(3 * (size_t)nf);
     if (nf)
         k_facet_geometry<<<(nf + 127) / 128, 128, 0, s>>>(G.X.p, G.F.p, nf, G.v.p, G.c.p, G.rad.p, G.diam.p, G.area.p,
-                                                          G.vid.p);
+                                                          G.vid.p); ::sbg::count_launch();
     SBG_LAUNCH_CHECK();
 }
 
@@ -760,240 +833,341 @@ void run_sauter(Ctx* ctx, const DBuf<double>& X, const std::vector<int>& pv, con
     {
         TimedScope ts(ctx, "sauter");
         k_sauter_partial<<<dim3(pblocks, nchunks), SAUTER_THREADS, 0, s>>>(d_pv.p, np, X.p, R.r[cls].p, npts, chunk,
-                                                                          part.p);
-        k_sauter_finish<<<(np + 127) / 128, 128, 0, s>>>(part.p, np, nchunks, d_pv.p, X.p, out_dev);
+                                                                          part.p); ::sbg::count_launch();
+        k_sauter_finish<<<(np + 127) / 128, 128, 0, s>>>(part.p, np, nchunks, d_pv.p, X.p, out_dev); ::sbg::count_launch();
         SBG_LAUNCH_CHECK();
     }
     SBG_CUDA(cudaStreamSynchronize(s));
 }
 
-void run_near(Ctx* ctx, const DBuf<double>& GV, const int2* pairs, long long np, double thr, double* out_dev,
-              long long* leaves)
+struct NearWork {
+    DBuf<long long> nleaf, off, total;
+    DBuf<unsigned> codes;
+    DBuf<int> owner;
+    DBuf<double> leaf_val;
+};
+
+// near-pair integrals for the device list pairs[0:*np_dev] (capacity cap); returns the leaf count
+long long run_near(Ctx* ctx, const double* GV, const int2* pairs, const unsigned long long* np_dev, long long cap,
+                   double thr, double* out, NearWork& NW)
 {
-    if (np == 0) return;
+    if (cap <= 0) return 0;
     cudaStream_t s = ctx->stream;
-    DBuf<unsigned long long> ctr(2);
-    SBG_CUDA(cudaMemsetAsync(ctr.p, 0, 2 * sizeof(unsigned long long), s));
-    const int grid = std::min<long long>((np + NEAR_WARPS - 1) / NEAR_WARPS, 4LL * ctx->sm_count);
+    TimedScope ts(ctx, "near");
+    if ((long long)NW.nleaf.n < cap) {
+        NW.nleaf.alloc(cap);
+        NW.off.alloc(cap);
+    }
+    if (!NW.total.n) NW.total.alloc(1);
+    const int thr_blk = 128;
+    const int grid = (int)std::min<long long>((cap + thr_blk - 1) / thr_blk, 8LL * ctx->sm_count);
+    k_near_count<<<grid, thr_blk, 0, s>>>(pairs, np_dev, cap, GV, thr, NW.nleaf.p);
+    count_launch();
+    k_scan_exclusive<<<1, 1024, 0, s>>>(NW.nleaf.p, np_dev, cap, NW.off.p, NW.total.p);
+    count_launch();
+    SBG_LAUNCH_CHECK();
+    long long total = 0;
+    SBG_CUDA(cudaMemcpyAsync(&total, NW.total.p, sizeof(total), cudaMemcpyDeviceToHost, s));
+    SBG_CUDA(cudaStreamSynchronize(s));
+    if (total == 0) return 0;
+    if ((long long)NW.codes.n < total) {
+        NW.codes.alloc(total);
+        NW.owner.alloc(total);
+        NW.leaf_val.alloc(total);
+    }
+    k_near_fill<<<grid, thr_blk, 0, s>>>(pairs, np_dev, cap, GV, thr, NW.off.p, NW.codes.p, NW.owner.p);
+    count_launch();
     {
-        TimedScope ts(ctx, "near");
-        k_near_pairs<<<grid, NEAR_WARPS * 32, 0, s>>>(pairs, np, GV.p, thr, out_dev, ctr.p, 1.0 / M_PI, ctr.p + 1);
-        SBG_LAUNCH_CHECK();
+        TimedScope tl(ctx, "near_leaves");
+        const long long warps = (total + 1) / 2;
+        const int lgrid = (int)std::min<long long>((warps + 7) / 8, 64LL * ctx->sm_count);
+        k_near_leaves<<<lgrid, 256, 0, s>>>(NW.codes.p, NW.owner.p, total, pairs, GV, NW.leaf_val.p);
+        count_launch();
     }
-    if (leaves) {
-        unsigned long long h = 0;
-        SBG_CUDA(cudaMemcpyAsync(&h, ctr.p + 1, sizeof(h), cudaMemcpyDeviceToHost, s));
-        SBG_CUDA(cudaStreamSynchronize(s));
-        *leaves = (long long)h;
-    }
+    k_near_reduce<<<grid, thr_blk, 0, s>>>(NW.off.p, NW.nleaf.p, np_dev, cap, NW.leaf_val.p, 1.0 / M_PI, out);
+    count_launch();
+    SBG_LAUNCH_CHECK();
+    return total;
 }
 
 }  // namespace
 
-// reference: inc/assemble.hpp:72-139
-void assemble_W(Ctx* ctx, const InflatedMesh& im, const QuadCfg& cfg, DMatrix& W, AssemblyStats* stats)
-{
-    cudaStream_t s = ctx->stream;
-    const SurfaceMesh& m = im.base;
-    const int nf = m.num_facets(), n = im.num_jump_dofs();
-    matrix_alloc(ctx, n, W);
-    if (nf == 0 || n == 0) return;
-    upload_rules(ctx, cfg);
+// ---------------------------------------------------------------- assembly plan
+// Host-side preparation of one mesh (facet blocks, curl lists, tile list,
+// singular lists, rules), uploaded once; assembly_run only launches kernels.
+struct AssemblyPlan {
+    Ctx* ctx = nullptr;
+    QuadCfg cfg;
+    int nf = 0, n = 0;
     DeviceGeometry G;
-    upload_geometry(ctx, m, G);
-    const double thr = cfg.near_threshold;
+    DBuf<int> uptr, udof;
+    DBuf<double> uval;
+    DBuf<int> bfac, dof_ptr, dofs, ent_ptr;
+    DBuf<double4> ents;
+    DBuf<TileInfo> tiles, cand;
+    long long ntiles = 0, ncand = 0;
+    // local pairs: singular classes (vertex, edge, identical) then the near list
+    long long nsing = 0, cls_off[4] = {0, 0, 0, 0}, cls_cnt[4] = {0, 0, 0, 0};
+    DBuf<int> pv[4];
+    DBuf<double> spart[4];
+    int schunks[4] = {0, 0, 0, 0}, schunk[4] = {0, 0, 0, 0};
+    SauterRulesDev SR;
+    long long near_cap = 0;
+    DBuf<int2> loc_pairs;
+    DBuf<double> loc_I;
+    DBuf<unsigned long long> near_cnt;
+    NearWork NW;
+};
 
-    // curl lists (per facet CSR) for the per-pair scatter
-    const FacetCurls U = facet_curls(im);
-    DBuf<int> d_uptr, d_udof;
-    DBuf<double> d_uval;
-    d_uptr.upload(U.ptr, s);
-    d_udof.upload(U.dof, s);
-    d_uval.upload(U.u, s);
-
-    // ---- Morton-ordered facet blocks
-    std::vector<int> perm(nf);
-    {
+AssemblyPlan* assembly_plan_create(Ctx* ctx, const InflatedMesh& im, const QuadCfg& cfg)
+{
+    auto* P = new AssemblyPlan;
+    try {
+        cudaStream_t s = ctx->stream;
+        const SurfaceMesh& m = im.base;
+        const int nf = m.num_facets();
+        P->ctx = ctx;
+        P->cfg = cfg;
+        P->nf = nf;
+        P->n = im.num_jump_dofs();
+        if (nf == 0 || P->n == 0) return P;
+        upload_rules(ctx, cfg);
+        upload_geometry(ctx, m, P->G);
+        const FacetCurls U = facet_curls(im);
+        P->uptr.upload(U.ptr, s);
+        P->udof.upload(U.dof, s);
+        P->uval.upload(U.u, s);
+        // ---- Morton-ordered facet blocks
+        std::vector<Vec3> cen(nf);
         double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
-        std::vector<Vec3> c(nf);
+        double rmax = 0, dmax = 0;
         for (int f = 0; f < nf; ++f) {
-            c[f] = m.facet_centroid(f);
-            const double xyz[3] = {c[f].x, c[f].y, c[f].z};
+            cen[f] = m.facet_centroid(f);
+            const double xyz[3] = {cen[f].x, cen[f].y, cen[f].z};
             for (int d = 0; d < 3; ++d) {
                 lo[d] = std::min(lo[d], xyz[d]);
                 hi[d] = std::max(hi[d], xyz[d]);
             }
+            for (int k = 0; k < 3; ++k) rmax = std::max(rmax, norm(m.vertices[m.facets[f][k]] - cen[f]));
+            dmax = std::max(dmax, m.facet_diameter(f));
         }
         const double span = std::max({hi[0] - lo[0], hi[1] - lo[1], hi[2] - lo[2], 1e-300});
         std::vector<std::uint64_t> key(nf);
         for (int f = 0; f < nf; ++f) {
-            const double xyz[3] = {c[f].x, c[f].y, c[f].z};
+            const double xyz[3] = {cen[f].x, cen[f].y, cen[f].z};
             std::uint64_t q[3];
             for (int d = 0; d < 3; ++d) q[d] = (std::uint64_t)((xyz[d] - lo[d]) / span * 2097151.0);
             key[f] = spread3(q[0]) | (spread3(q[1]) << 1) | (spread3(q[2]) << 2);
         }
+        std::vector<int> perm(nf);
         std::iota(perm.begin(), perm.end(), 0);
         std::stable_sort(perm.begin(), perm.end(), [&](int a, int b) { return key[a] < key[b]; });
-    }
-    const int nblk = (nf + BS - 1) / BS;
-    std::vector<int> bfac((size_t)nblk * BS, -1);
-    for (int k = 0; k < nf; ++k) bfac[k] = perm[k];
-    // per-block dof lists and per-dof entry lists (facet_local, U)
-    std::vector<int> dof_ptr{0}, dofs, ent_ptr;
-    std::vector<double4> ents;
-    std::vector<double> bcx(nblk), bcy(nblk), bcz(nblk), brad(nblk);
-    double rmax = 0, dmax = 0;
-    for (int f = 0; f < nf; ++f) {
-        rmax = std::max(rmax, [&] {
-            const Vec3 cc = m.facet_centroid(f);
-            double r = 0;
-            for (int k = 0; k < 3; ++k) r = std::max(r, norm(m.vertices[m.facets[f][k]] - cc));
-            return r;
-        }());
-        dmax = std::max(dmax, m.facet_diameter(f));
-    }
-    int max_dofs = 0;
-    struct DE {
-        int dof, l, p;
-    };
-    std::vector<DE> dl;
-    for (int b = 0; b < nblk; ++b) {
-        dl.clear();
-        Vec3 cs;
-        int cnt = 0;
-        for (int l = 0; l < BS; ++l) {
-            const int f = bfac[b * BS + l];
-            if (f < 0) continue;
-            cs = cs + m.facet_centroid(f);
-            ++cnt;
-            for (int p = U.ptr[f]; p < U.ptr[f + 1]; ++p) dl.push_back({U.dof[p], l, p});
-        }
-        const Vec3 cc = cs / (double)cnt;
-        double R = 0;
-        for (int l = 0; l < BS; ++l) {
-            const int f = bfac[b * BS + l];
-            if (f >= 0) R = std::max(R, norm(m.facet_centroid(f) - cc));
-        }
-        bcx[b] = cc.x;
-        bcy[b] = cc.y;
-        bcz[b] = cc.z;
-        brad[b] = R;
-        std::sort(dl.begin(), dl.end(), [](const DE& x, const DE& y) { return x.dof != y.dof ? x.dof < y.dof : x.l < y.l; });
-        int nd = 0;
-        for (size_t i = 0; i < dl.size(); ++i) {
-            if (i == 0 || dl[i].dof != dl[i - 1].dof) {
-                dofs.push_back(dl[i].dof);
-                ent_ptr.push_back((int)ents.size());
-                ++nd;
+        const int nblk = (nf + BS - 1) / BS;
+        std::vector<int> bfac((size_t)nblk * BS, -1);
+        for (int k = 0; k < nf; ++k) bfac[k] = perm[k];
+        std::vector<int> dof_ptr{0}, dofs, ent_ptr;
+        std::vector<double4> ents;
+        std::vector<double> bcx(nblk), bcy(nblk), bcz(nblk), brad(nblk);
+        struct DE {
+            int dof, l, p;
+        };
+        std::vector<DE> dl;
+        for (int b = 0; b < nblk; ++b) {
+            dl.clear();
+            Vec3 cs;
+            int cnt = 0;
+            for (int l = 0; l < BS; ++l) {
+                const int f = bfac[b * BS + l];
+                if (f < 0) continue;
+                cs = cs + cen[f];
+                ++cnt;
+                for (int p = U.ptr[f]; p < U.ptr[f + 1]; ++p) dl.push_back({U.dof[p], l, p});
             }
-            const int p = dl[i].p;
-            ents.push_back(make_double4(U.u[3 * p], U.u[3 * p + 1], U.u[3 * p + 2], (double)dl[i].l));
+            const Vec3 cc = cs / (double)cnt;
+            double R = 0;
+            for (int l = 0; l < BS; ++l) {
+                const int f = bfac[b * BS + l];
+                if (f >= 0) R = std::max(R, norm(cen[f] - cc));
+            }
+            bcx[b] = cc.x;
+            bcy[b] = cc.y;
+            bcz[b] = cc.z;
+            brad[b] = R;
+            std::sort(dl.begin(), dl.end(),
+                      [](const DE& x, const DE& y) { return x.dof != y.dof ? x.dof < y.dof : x.l < y.l; });
+            for (size_t i = 0; i < dl.size(); ++i) {
+                if (i == 0 || dl[i].dof != dl[i - 1].dof) {
+                    dofs.push_back(dl[i].dof);
+                    ent_ptr.push_back((int)ents.size());
+                }
+                const int p = dl[i].p;
+                ents.push_back(make_double4(U.u[3 * p], U.u[3 * p + 1], U.u[3 * p + 2], (double)dl[i].l));
+            }
+            dof_ptr.push_back((int)dofs.size());
         }
-        dof_ptr.push_back((int)dofs.size());
-        max_dofs = std::max(max_dofs, nd);
+        ent_ptr.push_back((int)ents.size());
+        // ---- tiles (fb >= gb); certainly-far tiles skip per-pair classification
+        const double thr = cfg.near_threshold;
+        std::vector<TileInfo> tiles, cand;
+        tiles.reserve((size_t)nblk * (nblk + 1) / 2);
+        const double margin = 1e-9 * std::max(1.0, dmax);
+        for (int fb = 0; fb < nblk; ++fb)
+            for (int gb = 0; gb <= fb; ++gb) {
+                const double dx = bcx[fb] - bcx[gb], dy = bcy[fb] - bcy[gb], dz = bcz[fb] - bcz[gb];
+                // any pair: dist_estimate >= D - R_f - R_g - 2 rmax >= thr * dmax (and no shared vertex)
+                const double lower = std::sqrt(dx * dx + dy * dy + dz * dz) - brad[fb] - brad[gb] - 2.0 * rmax;
+                const bool certain =
+                    fb != gb && lower > margin && lower >= std::max(0.0, thr) * dmax * (1.0 + 1e-9) + margin;
+                tiles.push_back({fb, gb, certain ? 1 : 0, 0});
+                if (!certain) cand.push_back({fb, gb, 0, 0});
+            }
+        P->bfac.upload(bfac, s);
+        P->dof_ptr.upload(dof_ptr, s);
+        P->dofs.upload(dofs, s);
+        P->ent_ptr.upload(ent_ptr, s);
+        P->ents.upload(ents, s);
+        P->tiles.upload(tiles, s);
+        P->cand.upload(cand, s);
+        P->ntiles = (long long)tiles.size();
+        P->ncand = (long long)cand.size();
+        // ---- singular lists (host adjacency, deterministic order) and Sauter workspaces
+        SingularLists S;
+        singular_pairs(m, S);
+        upload_sauter(ctx, cfg, P->SR);
+        P->near_cap = std::max<long long>(1024, 64LL * nf);
+        long long off = 0;
+        for (int cls = 1; cls <= 3; ++cls) {
+            P->cls_off[cls] = off;
+            P->cls_cnt[cls] = (long long)S.pairs[cls].size();
+            off += P->cls_cnt[cls];
+        }
+        P->nsing = off;
+        P->loc_pairs.alloc(P->nsing + P->near_cap);
+        P->loc_I.alloc(P->nsing + P->near_cap);
+        for (int cls = 1; cls <= 3; ++cls) {
+            const long long np = P->cls_cnt[cls];
+            if (!np) continue;
+            SBG_CUDA(cudaMemcpyAsync(P->loc_pairs.p + P->cls_off[cls], S.pairs[cls].data(), np * sizeof(int2),
+                                     cudaMemcpyHostToDevice, s));
+            P->pv[cls].upload(S.pv[cls], s);
+            const int npts = P->SR.npts[cls];
+            const int pblocks = (int)((np + SAUTER_THREADS - 1) / SAUTER_THREADS);
+            int nchunks = std::max(1, std::min((4 * ctx->sm_count + pblocks - 1) / pblocks, (npts + 999) / 1000));
+            const int chunk = (npts + nchunks - 1) / nchunks;
+            P->schunk[cls] = chunk;
+            P->schunks[cls] = (npts + chunk - 1) / chunk;
+            P->spart[cls].alloc((size_t)P->schunks[cls] * np);
+        }
+        P->near_cnt.alloc(1);
+        SBG_CUDA(cudaStreamSynchronize(s));
+    } catch (...) {
+        delete P;
+        throw;
     }
-    ent_ptr.push_back((int)ents.size());
-    // ---- tiles (fb >= gb); certainly-far tiles skip per-pair classification
-    std::vector<TileInfo> tiles, cand;
-    tiles.reserve((size_t)nblk * (nblk + 1) / 2);
-    const double margin = 1e-9 * std::max(1.0, dmax);
-    for (int fb = 0; fb < nblk; ++fb)
-        for (int gb = 0; gb <= fb; ++gb) {
-            const double dx = bcx[fb] - bcx[gb], dy = bcy[fb] - bcy[gb], dz = bcz[fb] - bcz[gb];
-            const double D = std::sqrt(dx * dx + dy * dy + dz * dz);
-            // any pair: dist_estimate >= D - R_f - R_g - 2 rmax >= thr * dmax (and no shared vertex)
-            const double lower = D - brad[fb] - brad[gb] - 2.0 * rmax;
-            const bool certain = fb != gb && lower > margin && lower >= std::max(0.0, thr) * dmax * (1.0 + 1e-9) + margin;
-            tiles.push_back({fb, gb, certain ? 1 : 0, 0});
-            if (!certain) cand.push_back({fb, gb, 0, 0});
-        }
-    DBuf<int> d_bfac, d_dof_ptr, d_dofs, d_ent_ptr;
-    DBuf<double4> d_ents;
-    d_bfac.upload(bfac, s);
-    d_dof_ptr.upload(dof_ptr, s);
-    d_dofs.upload(dofs, s);
-    d_ent_ptr.upload(ent_ptr, s);
-    d_ents.upload(ents, s);
-    BlockPtrs BP{d_bfac.p, d_dof_ptr.p, d_dofs.p, d_ent_ptr.p, d_ents.p};
-    // dof_ptr indexes ent_ptr by global block-dof position: ent_ptr has one entry per block-dof + 1
-    DBuf<TileInfo> d_tiles, d_cand;
-    d_tiles.upload(tiles, s);
-    d_cand.upload(cand, s);
+    return P;
+}
 
-    // ---- near list
-    unsigned long long cap = std::max<unsigned long long>(1024, 64ULL * nf);
-    DBuf<int2> d_near;
-    DBuf<unsigned long long> d_cnt(1);
+void assembly_plan_destroy(AssemblyPlan* P) { delete P; }
+
+// reference: inc/assemble.hpp:72-139 (device kernels only; the plan holds the mesh data)
+void assembly_run(AssemblyPlan* P, DMatrix& W, AssemblyStats* stats)
+{
+    Ctx* ctx = P->ctx;
+    cudaStream_t s = ctx->stream;
+    TimedScope total(ctx, "assemble_W");
+    if (W.n != P->n || !W.a.p) matrix_alloc(ctx, P->n, W);
+    else SBG_CUDA(cudaMemsetAsync(W.a.p, 0, W.a.n * sizeof(double), s));
+    if (P->nf == 0 || P->n == 0) return;
+    upload_rules(ctx, P->cfg);
+    const double thr = P->cfg.near_threshold;
+    // near list (classification of the non-certainly-far tiles)
+    long long leaves = 0;
     unsigned long long nnear = 0;
     for (int attempt = 0; attempt < 2; ++attempt) {
-        d_near.alloc(cap);
-        SBG_CUDA(cudaMemsetAsync(d_cnt.p, 0, sizeof(unsigned long long), s));
-        if (!cand.empty()) {
+        SBG_CUDA(cudaMemsetAsync(P->near_cnt.p, 0, sizeof(unsigned long long), s));
+        if (P->ncand) {
             TimedScope ts(ctx, "classify");
-            k_classify_near<<<(int)cand.size(), 256, 0, s>>>(d_cand.p, G.ptrs(), d_bfac.p, thr, d_near.p, cap, d_cnt.p);
+            k_classify_near<<<(int)P->ncand, 256, 0, s>>>(P->cand.p, P->G.ptrs(), P->bfac.p, thr,
+                                                          P->loc_pairs.p + P->nsing, P->near_cap, P->near_cnt.p);
+            count_launch();
             SBG_LAUNCH_CHECK();
         }
-        SBG_CUDA(cudaMemcpyAsync(&nnear, d_cnt.p, sizeof(nnear), cudaMemcpyDeviceToHost, s));
+        leaves = run_near(ctx, P->G.v.p, P->loc_pairs.p + P->nsing, P->near_cnt.p, P->near_cap, thr,
+                          P->loc_I.p + P->nsing, P->NW);
+        SBG_CUDA(cudaMemcpyAsync(&nnear, P->near_cnt.p, sizeof(nnear), cudaMemcpyDeviceToHost, s));
         SBG_CUDA(cudaStreamSynchronize(s));
-        if (nnear <= cap) break;
-        cap = nnear;
+        if ((long long)nnear <= P->near_cap) break;
+        // near list overflow: grow and redo
+        P->near_cap = (long long)nnear + 1024;
+        DBuf<int2> np2(P->nsing + P->near_cap);
+        DBuf<double> ni2(P->nsing + P->near_cap);
+        if (P->nsing) {
+            SBG_CUDA(cudaMemcpyAsync(np2.p, P->loc_pairs.p, P->nsing * sizeof(int2), cudaMemcpyDeviceToDevice, s));
+        }
+        P->loc_pairs = std::move(np2);
+        P->loc_I = std::move(ni2);
     }
-
-    // ---- singular lists (host adjacency, deterministic order)
-    SingularLists S;
-    singular_pairs(m, S);
-    SauterRulesDev SR;
-    upload_sauter(ctx, cfg, SR);
-
-    // local pairs: [vertex | edge | identical | near] with their integrals
-    const long long nloc_sing = (long long)S.pairs[1].size() + S.pairs[2].size() + S.pairs[3].size();
-    const long long nloc = nloc_sing + (long long)nnear;
-    DBuf<int2> d_loc_pairs(std::max<long long>(nloc, 1));
-    DBuf<double> d_loc_I(std::max<long long>(nloc, 1));
-    long long off = 0;
+    // singular pairs (Sauter rules)
     for (int cls = 1; cls <= 3; ++cls) {
-        const long long np = (long long)S.pairs[cls].size();
+        const long long np = P->cls_cnt[cls];
         if (!np) continue;
-        SBG_CUDA(cudaMemcpyAsync(d_loc_pairs.p + off, S.pairs[cls].data(), np * sizeof(int2), cudaMemcpyHostToDevice, s));
-        run_sauter(ctx, G.X, S.pv[cls], SR, cls, d_loc_I.p + off);
-        off += np;
-    }
-    if (nnear) {
-        SBG_CUDA(cudaMemcpyAsync(d_loc_pairs.p + off, d_near.p, nnear * sizeof(int2), cudaMemcpyDeviceToDevice, s));
-        long long leaves = 0;
-        run_near(ctx, G.v, d_loc_pairs.p + off, (long long)nnear, thr, d_loc_I.p + off, stats ? &leaves : nullptr);
-        if (stats) stats->near_leaves = leaves;
-    }
-    // ---- far tiles
-    {
-        TimedScope ts(ctx, "far_tiles");
-        k_far_tiles<<<(int)tiles.size(), FAR_THREADS, 0, s>>>(d_tiles.p, G.ptrs(), BP, thr, W.a.p, W.ld, 1.0 / M_PI);
+        TimedScope ts(ctx, "sauter");
+        const int pblocks = (int)((np + SAUTER_THREADS - 1) / SAUTER_THREADS);
+        k_sauter_partial<<<dim3(pblocks, P->schunks[cls]), SAUTER_THREADS, 0, s>>>(
+            P->pv[cls].p, (int)np, P->G.X.p, P->SR.r[cls].p, P->SR.npts[cls], P->schunk[cls], P->spart[cls].p);
+        count_launch();
+        k_sauter_finish<<<(int)((np + 127) / 128), 128, 0, s>>>(P->spart[cls].p, (int)np, P->schunks[cls],
+                                                                 P->pv[cls].p, P->G.X.p, P->loc_I.p + P->cls_off[cls]);
+        count_launch();
         SBG_LAUNCH_CHECK();
     }
-    // ---- per-pair scatter of near + singular integrals
+    // far tiles
+    {
+        TimedScope ts(ctx, "far_tiles");
+        BlockPtrs BP{P->bfac.p, P->dof_ptr.p, P->dofs.p, P->ent_ptr.p, P->ents.p};
+        k_far_tiles<<<(int)P->ntiles, FAR_THREADS, 0, s>>>(P->tiles.p, P->G.ptrs(), BP, thr, W.a.p, W.ld, 1.0 / M_PI);
+        count_launch();
+        SBG_LAUNCH_CHECK();
+    }
+    // per-pair scatter of singular + near integrals
+    const long long nloc = P->nsing + (long long)nnear;
     if (nloc) {
         TimedScope ts(ctx, "local_scatter");
-        k_local_scatter<<<(int)((nloc + 127) / 128), 128, 0, s>>>(d_loc_pairs.p, d_loc_I.p, nloc, d_uptr.p, d_udof.p,
-                                                                  d_uval.p, W.a.p, W.ld);
+        k_local_scatter<<<(int)((nloc + 127) / 128), 128, 0, s>>>(P->loc_pairs.p, P->loc_I.p, nloc, P->uptr.p,
+                                                                  P->udof.p, P->uval.p, W.a.p, W.ld);
+        count_launch();
         SBG_LAUNCH_CHECK();
     }
     {
         TimedScope ts(ctx, "mirror");
-        const int nt = (n + 31) / 32;
-        k_mirror<<<dim3(nt, nt), dim3(32, 8), 0, s>>>(W.a.p, n, W.ld);
+        const int nt = (P->n + 31) / 32;
+        k_mirror<<<dim3(nt, nt), dim3(32, 8), 0, s>>>(W.a.p, P->n, W.ld);
+        count_launch();
         SBG_LAUNCH_CHECK();
     }
-    SBG_CUDA(cudaStreamSynchronize(s));
-    (void)max_dofs;
     if (stats) {
-        stats->identical = (long long)S.pairs[3].size();
-        stats->edge = (long long)S.pairs[2].size();
-        stats->vertex = (long long)S.pairs[1].size();
+        stats->identical = P->cls_cnt[3];
+        stats->edge = P->cls_cnt[2];
+        stats->vertex = P->cls_cnt[1];
         stats->near_pairs = (long long)nnear;
-        stats->far_pairs = (long long)nf * (nf + 1) / 2 - nloc;
-        stats->tiles = (long long)tiles.size();
-        stats->tiles_skipped = (long long)(tiles.size() - cand.size());
+        stats->near_leaves = leaves;
+        stats->far_pairs = (long long)P->nf * (P->nf + 1) / 2 - nloc;
+        stats->tiles = P->ntiles;
+        stats->tiles_skipped = P->ntiles - P->ncand;
     }
+}
+
+void assemble_W(Ctx* ctx, const InflatedMesh& im, const QuadCfg& cfg, DMatrix& W, AssemblyStats* stats)
+{
+    AssemblyPlan* P = assembly_plan_create(ctx, im, cfg);
+    try {
+        assembly_run(P, W, stats);
+        SBG_CUDA(cudaStreamSynchronize(ctx->stream));
+    } catch (...) {
+        delete P;
+        throw;
+    }
+    delete P;
 }
 
 namespace {
@@ -1011,7 +1185,7 @@ __global__ void k_far_pair_list(GeoPtrs G, const int2* __restrict__ pairs, long 
 }
 void far_pair_list(Ctx* ctx, const GeoPtrs& G, const int2* pairs, long long np, double* out)
 {
-    k_far_pair_list<<<(int)((np + 127) / 128), 128, 0, ctx->stream>>>(G, pairs, np, out, 1.0 / M_PI);
+    k_far_pair_list<<<(int)((np + 127) / 128), 128, 0, ctx->stream>>>(G, pairs, np, out, 1.0 / M_PI); ::sbg::count_launch();
     SBG_LAUNCH_CHECK();
 }
 
@@ -1096,7 +1270,11 @@ void pair_integrals(Ctx* ctx, const SurfaceMesh& m, const QuadCfg& cfg, const in
         DBuf<int2> d_p;
         d_p.upload(nearp, s);
         DBuf<double> o(nearp.size());
-        run_near(ctx, G.v, d_p.p, (long long)nearp.size(), cfg.near_threshold, o.p, nullptr);
+        DBuf<unsigned long long> cnt(1);
+        const unsigned long long hn = nearp.size();
+        SBG_CUDA(cudaMemcpyAsync(cnt.p, &hn, sizeof(hn), cudaMemcpyHostToDevice, s));
+        NearWork NW;
+        run_near(ctx, G.v.p, d_p.p, cnt.p, (long long)nearp.size(), cfg.near_threshold, o.p, NW);
         fetch(o.p, idx[0]);
     }
     if (!farp.empty()) {
@@ -1174,7 +1352,7 @@ void assemble_rhs(Ctx* ctx, const InflatedMesh& im, const QuadCfg& cfg, const do
     SBG_CUDA(cudaMemsetAsync(d_L.p, 0, d_L.n * sizeof(double), s));
     if (nf)
         k_rhs<<<(nf * NF + 127) / 128, 128, 0, s>>>(nf, G.v.p, d_on.p, d_g.p, g_is_field ? 1 : 0, d_sptr.p, d_sdof.p,
-                                                    d_ssgn.p, d_L.p);
+                                                    d_ssgn.p, d_L.p); ::sbg::count_launch();
     SBG_LAUNCH_CHECK();
     if (n) SBG_CUDA(cudaMemcpyAsync(L_host, d_L.p, n * sizeof(double), cudaMemcpyDeviceToHost, s));
     SBG_CUDA(cudaStreamSynchronize(s));

@@ -23,6 +23,10 @@ namespace sbg {
 
 constexpr int kNumSMs = 148;  // B200 (2 dies x 74); queried at runtime as well
 
+// Number of kernels this library has launched (bench evidence: gpu_launches).
+void count_launch();
+long long launch_count();
+
 // Device buffer owned by the host object (RAII, stream-ordered free not needed:
 // objects are destroyed after a context synchronize).
 template <class T>

@@ -1,8 +1,16 @@
 // Context, timers and dense-matrix utilities.
 #include "common.cuh"
+#include <atomic>
+
 #include "kernels.cuh"
 
 namespace sbg {
+
+namespace {
+std::atomic<long long> g_launches{0};
+}
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+long long launch_count() { return g_launches.load(); }
 
 cudaEvent_t Timers::get()
 {
@@ -141,7 +149,7 @@ void matrix_upload(DMatrix& M, const double* host)
         SBG_CUDA(cudaMemcpyAsync(stage.p, host + (size_t)r0 * M.n, (size_t)(r1 - r0) * M.n * sizeof(double),
                                  cudaMemcpyHostToDevice, ctx->stream));
         dim3 grid((M.n + 255) / 256 < 64 ? (M.n + 255) / 256 : 64, r1 - r0);
-        k_pack_rows<<<grid, 256, 0, ctx->stream>>>(stage.p, M.n, M.a.p + (size_t)r0 * M.ld, M.ld);
+        k_pack_rows<<<grid, 256, 0, ctx->stream>>>(stage.p, M.n, M.a.p + (size_t)r0 * M.ld, M.ld); ::sbg::count_launch();
         SBG_LAUNCH_CHECK();
     }
     SBG_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -155,7 +163,7 @@ void matrix_download(const DMatrix& M, double* host)
     for (int r0 = 0; r0 < M.n; r0 += (int)rows_per) {
         const int r1 = std::min<int>(M.n, r0 + (int)rows_per);
         dim3 grid((M.n + 255) / 256 < 64 ? (M.n + 255) / 256 : 64, r1 - r0);
-        k_unpack_rows<<<grid, 256, 0, ctx->stream>>>(M.a.p + (size_t)r0 * M.ld, M.ld, M.n, stage.p);
+        k_unpack_rows<<<grid, 256, 0, ctx->stream>>>(M.a.p + (size_t)r0 * M.ld, M.ld, M.n, stage.p); ::sbg::count_launch();
         SBG_LAUNCH_CHECK();
         SBG_CUDA(cudaMemcpyAsync(host + (size_t)r0 * M.n, stage.p, (size_t)(r1 - r0) * M.n * sizeof(double),
                                  cudaMemcpyDeviceToHost, ctx->stream));
@@ -172,7 +180,7 @@ void matrix_download_rows(const DMatrix& M, const int* rows, int nrows, double* 
     d_rows.upload(rows, nrows, ctx->stream);
     DBuf<double> out((size_t)nrows * M.n);
     dim3 grid((M.n + 255) / 256 < 64 ? (M.n + 255) / 256 : 64, nrows);
-    k_gather_rows<<<grid, 256, 0, ctx->stream>>>(M.a.p, M.ld, M.n, d_rows.p, out.p);
+    k_gather_rows<<<grid, 256, 0, ctx->stream>>>(M.a.p, M.ld, M.n, d_rows.p, out.p); ::sbg::count_launch();
     SBG_LAUNCH_CHECK();
     SBG_CUDA(cudaMemcpyAsync(host, out.p, (size_t)nrows * M.n * sizeof(double), cudaMemcpyDeviceToHost,
                              ctx->stream));
@@ -185,7 +193,7 @@ double matrix_symmetry_defect(const DMatrix& M)
     if (M.n < 2) return 0.0;
     const int gx = 8;
     DBuf<double> part((size_t)M.n * gx);
-    k_symmetry_defect<<<dim3(gx, M.n), 256, 0, ctx->stream>>>(M.a.p, M.ld, M.n, part.p);
+    k_symmetry_defect<<<dim3(gx, M.n), 256, 0, ctx->stream>>>(M.a.p, M.ld, M.n, part.p); ::sbg::count_launch();
     SBG_LAUNCH_CHECK();
     std::vector<double> h(part.n);
     SBG_CUDA(cudaMemcpyAsync(h.data(), part.p, h.size() * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
@@ -195,4 +203,45 @@ double matrix_symmetry_defect(const DMatrix& M)
     return m;
 }
 
+}  // namespace sbg
+
+// ---------------------------------------------------------------- FP64 peak probe
+namespace sbg {
+namespace {
+__global__ void k_dfma_peak(double* out, int iters)
+{
+    double a0 = threadIdx.x * 1e-9, a1 = a0 + 1e-9, a2 = a0 + 2e-9, a3 = a0 + 3e-9;
+    double a4 = a0 + 4e-9, a5 = a0 + 5e-9, a6 = a0 + 6e-9, a7 = a0 + 7e-9;
+    const double b = 0.999999999, c = 1e-12;
+    for (int i = 0; i < iters; ++i) {
+        a0 = fma(a0, b, c); a1 = fma(a1, b, c); a2 = fma(a2, b, c); a3 = fma(a3, b, c);
+        a4 = fma(a4, b, c); a5 = fma(a5, b, c); a6 = fma(a6, b, c); a7 = fma(a7, b, c);
+    }
+    const double s = ((a0 + a1) + (a2 + a3)) + ((a4 + a5) + (a6 + a7));
+    if (s == 12345.678) out[0] = s;
+}
+}  // namespace
+
+// measured DFMA throughput (TFLOP/s, 2 flop per FMA) over a ~50 ms launch
+double fp64_peak_tflops(Ctx* ctx)
+{
+    DBuf<double> out(1);
+    const int blocks = ctx->sm_count * 8, threads = 256, iters = 1 << 14;
+    cudaEvent_t a, b;
+    SBG_CUDA(cudaEventCreate(&a));
+    SBG_CUDA(cudaEventCreate(&b));
+    k_dfma_peak<<<blocks, threads, 0, ctx->stream>>>(out.p, 1024);  // warm-up
+    count_launch();
+    SBG_CUDA(cudaEventRecord(a, ctx->stream));
+    k_dfma_peak<<<blocks, threads, 0, ctx->stream>>>(out.p, iters);
+    count_launch();
+    SBG_CUDA(cudaEventRecord(b, ctx->stream));
+    SBG_CUDA(cudaEventSynchronize(b));
+    float ms = 0;
+    SBG_CUDA(cudaEventElapsedTime(&ms, a, b));
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    const double flops = 2.0 * 8.0 * (double)iters * blocks * threads;
+    return flops / (ms * 1e-3) / 1e12;
+}
 }  // namespace sbg

@@ -37,6 +37,8 @@ __device__ __forceinline__ double rsqrt_fast(double r2)
     return fma(y, e * c, y);                    // y (1 + e/2 + 3e^2/8)
 }
 
+double fp64_peak_tflops(Ctx* ctx);
+
 // ---------------------------------------------------------------- matrices
 void matrix_alloc(Ctx* ctx, int n, DMatrix& M);
 void matrix_upload(DMatrix& M, const double* host);
@@ -88,6 +90,10 @@ struct AssemblyStats {
     long long far_pairs = 0, near_pairs = 0, identical = 0, edge = 0, vertex = 0;
     long long near_leaves = 0, tiles = 0, tiles_skipped = 0;
 };
+struct AssemblyPlan;
+AssemblyPlan* assembly_plan_create(Ctx* ctx, const InflatedMesh& im, const QuadCfg& cfg);
+void assembly_plan_destroy(AssemblyPlan* p);
+void assembly_run(AssemblyPlan* p, DMatrix& W, AssemblyStats* stats);
 void assemble_W(Ctx* ctx, const InflatedMesh& im, const QuadCfg& cfg, DMatrix& W, AssemblyStats* stats);
 void pair_integrals(Ctx* ctx, const SurfaceMesh& m, const QuadCfg& cfg, const int* f, const int* g, long long np,
                     double* out);

@@ -243,7 +243,7 @@ static void gemv_partial_launch(Ctx* ctx, const DMatrix& W, GemvPlan& plan, cons
     TimedScope ts(ctx, "gemv_f64");
     const size_t smem = (size_t)plan.rows_per_chunk * sizeof(double);
     k_gemv_partial<<<dim3(plan.strips, plan.chunks), kGemvThreads, smem, ctx->stream>>>(
-        W.a.p, W.ld, W.n, x, plan.rows_per_chunk, plan.part.p, done);
+        W.a.p, W.ld, W.n, x, plan.rows_per_chunk, plan.part.p, done); ::sbg::count_launch();
     SBG_LAUNCH_CHECK();
 }
 
@@ -251,7 +251,7 @@ void gemv(Ctx* ctx, const DMatrix& W, GemvPlan& plan, const double* x, double* y
 {
     if (W.n == 0) return;
     gemv_partial_launch(ctx, W, plan, x, nullptr);
-    k_gemv_reduce<<<(W.n + 255) / 256, 256, 0, ctx->stream>>>(plan.part.p, plan.chunks, W.ld, W.n, y);
+    k_gemv_reduce<<<(W.n + 255) / 256, 256, 0, ctx->stream>>>(plan.part.p, plan.chunks, W.ld, W.n, y); ::sbg::count_launch();
     SBG_LAUNCH_CHECK();
 }
 
@@ -310,6 +310,7 @@ void pcg_run(Ctx* ctx, const DMatrix& W, Prec* prec, const double* rhs, double* 
     if (tol <= 0) throw ValidationError("pcg: tolerance must be positive");
     if (prec && prec_n(prec) != n) throw ValidationError("preconditioner length mismatch");
     if (maxit <= 0) maxit = std::max(10 * n, 100);
+    TimedScope tpcg(ctx, "pcg");
     cudaStream_t s = ctx->stream;
     const size_t len = (size_t)W.ld;
     DBuf<double> buf(6 * len);
@@ -338,7 +339,7 @@ void pcg_run(Ctx* ctx, const DMatrix& W, Prec* prec, const double* rhs, double* 
 
     if (n > 0) {
         if (prec) prec_apply(ctx, prec, r, z, nullptr);
-        k_pcg_init<<<nb, 256, 0, s>>>(st.p, r, z, p, n, partials.p, hist.p);
+        k_pcg_init<<<nb, 256, 0, s>>>(st.p, r, z, p, n, partials.p, hist.p); ::sbg::count_launch();
         SBG_LAUNCH_CHECK();
     } else {
         h.converged = 1;
@@ -355,11 +356,11 @@ void pcg_run(Ctx* ctx, const DMatrix& W, Prec* prec, const double* rhs, double* 
         const int todo = std::min(batch, maxit - enqueued);
         for (int t = 0; t < todo; ++t) {
             gemv_partial_launch(ctx, W, plan, p, done);
-            k_pcg_alpha<<<nb, 256, 0, s>>>(st.p, plan.part.p, plan.chunks, W.ld, n, p, Wp, partials.p);
-            k_pcg_update<<<nb, 256, 0, s>>>(st.p, x, r, p, Wp, n);
+            k_pcg_alpha<<<nb, 256, 0, s>>>(st.p, plan.part.p, plan.chunks, W.ld, n, p, Wp, partials.p); ::sbg::count_launch();
+            k_pcg_update<<<nb, 256, 0, s>>>(st.p, x, r, p, Wp, n); ::sbg::count_launch();
             if (prec) prec_apply(ctx, prec, r, z, done);
-            k_pcg_rz<<<nb, 256, 0, s>>>(st.p, r, z, n, partials.p, hist.p, alphas.p, betas.p);
-            k_pcg_p<<<nb, 256, 0, s>>>(st.p, p, z, n);
+            k_pcg_rz<<<nb, 256, 0, s>>>(st.p, r, z, n, partials.p, hist.p, alphas.p, betas.p); ::sbg::count_launch();
+            k_pcg_p<<<nb, 256, 0, s>>>(st.p, p, z, n); ::sbg::count_launch();
             SBG_LAUNCH_CHECK();
         }
         enqueued += todo;

@@ -430,7 +430,7 @@ Prec* prec_build(Ctx* ctx, const DMatrix& W, const DofPartition& part, const Pro
             DBuf<int> d_bptr, d_bdofs;
             d_bptr.upload(bptr, s);
             d_bdofs.upload(bdofs, s);
-            k_gather_blocks<<<dim3(ngather, 64), 128, 0, s>>>(W.a.p, W.ld, d_bptr.p, d_bdofs.p, P->d_Loff.p, P->L.p);
+            k_gather_blocks<<<dim3(ngather, 64), 128, 0, s>>>(W.a.p, W.ld, d_bptr.p, d_bdofs.p, P->d_Loff.p, P->L.p); ::sbg::count_launch();
             SBG_LAUNCH_CHECK();
             SBG_CUDA(cudaStreamSynchronize(s));
         }
@@ -458,9 +458,9 @@ Prec* prec_build(Ctx* ctx, const DMatrix& W, const DofPartition& part, const Pro
             DBuf<double> WR((size_t)n * P->nc);
             TimedScope ts(ctx, "coarse_galerkin");
             k_coarse_WR<<<std::min(n, 8 * ctx->sm_count), 128, 0, s>>>(W.a.p, W.ld, n, P->Rc_ptr.p, P->Rc_row.p,
-                                                                      P->Rc_val.p, P->nc, WR.p);
+                                                                      P->Rc_val.p, P->nc, WR.p); ::sbg::count_launch();
             k_coarse_H<<<P->nc, 128, 0, s>>>(WR.p, P->Rc_ptr.p, P->Rc_row.p, P->Rc_val.p, P->nc,
-                                             P->L.p + P->h_Loff[P->coarse_block]);
+                                             P->L.p + P->h_Loff[P->coarse_block]); ::sbg::count_launch();
             SBG_LAUNCH_CHECK();
             SBG_CUDA(cudaStreamSynchronize(s));
         }
@@ -491,18 +491,18 @@ Prec* prec_build(Ctx* ctx, const DMatrix& W, const DofPartition& part, const Pro
                 }
                 d_pot.upload(pot, s);
                 k_potrf<<<(int)pot.size(), 256, smem_potrf, s>>>(k, d_pot.p, P->d_nb.p, P->d_Loff.p, P->d_Doff.p,
-                                                                 P->L.p, P->D.p, fail.p);
+                                                                 P->L.p, P->D.p, fail.p); ::sbg::count_launch();
                 SBG_LAUNCH_CHECK();
                 if (!trsm.empty()) {
                     d_trsm.upload(trsm, s);
                     k_tile_gemm<<<(int)trsm.size(), 128, smem_gemm, s>>>(k, 0, d_trsm.p, P->d_nb.p, P->d_Loff.p,
-                                                                          P->d_Doff.p, P->L.p, P->D.p);
+                                                                          P->d_Doff.p, P->L.p, P->D.p); ::sbg::count_launch();
                     SBG_LAUNCH_CHECK();
                 }
                 if (!upd.empty()) {
                     d_upd.upload(upd, s);
                     k_tile_gemm<<<(int)upd.size(), 128, smem_gemm, s>>>(k, 1, d_upd.p, P->d_nb.p, P->d_Loff.p,
-                                                                         P->d_Doff.p, P->L.p, P->D.p);
+                                                                         P->d_Doff.p, P->L.p, P->D.p); ::sbg::count_launch();
                     SBG_LAUNCH_CHECK();
                 }
                 // host task vectors are reused next step: wait for the async uploads
@@ -561,24 +561,24 @@ void prec_apply(Ctx* ctx, Prec* P, const double* r, double* z, const int* done)
     if (n == 0) return;
     const int nb = (n + 255) / 256;
     double* loc_c = P->coarse_block >= 0 ? P->loc.p + P->h_loc[P->coarse_block] : nullptr;
-    k_prec_gather<<<nb, 256, 0, s>>>(r, n, P->pos.p, P->loc.p, done);
+    k_prec_gather<<<nb, 256, 0, s>>>(r, n, P->pos.p, P->loc.p, done); ::sbg::count_launch();
     if (P->nc > 0)
         k_prec_restrict<<<(P->nc + 127) / 128, 128, 0, s>>>(r, P->Rc_ptr.p, P->Rc_row.p, P->Rc_val.p, P->nc, loc_c,
-                                                            done);
+                                                            done); ::sbg::count_launch();
     for (int k = 0; k < P->Tmax; ++k) {
         const int cnt = P->fwd_off[k + 1] - P->fwd_off[k];
         if (cnt)
             k_trsv_fwd<<<cnt, 256, 0, s>>>(k, P->fwd_tasks.p + P->fwd_off[k], P->d_nb.p, P->d_loc.p, P->d_Loff.p,
-                                           P->d_Doff.p, P->L.p, P->D.p, P->loc.p, done);
+                                           P->d_Doff.p, P->L.p, P->D.p, P->loc.p, done); ::sbg::count_launch();
     }
     for (int st = 0; st < P->Tmax; ++st) {
         const int cnt = P->bwd_off[st + 1] - P->bwd_off[st];
         if (cnt)
             k_trsv_bwd<<<cnt, 256, 0, s>>>(st, P->bwd_tasks.p + P->bwd_off[st], P->d_nb.p, P->d_T.p, P->d_loc.p,
-                                           P->d_Loff.p, P->d_Doff.p, P->L.p, P->D.p, P->loc.p, done);
+                                           P->d_Loff.p, P->d_Doff.p, P->L.p, P->D.p, P->loc.p, done); ::sbg::count_launch();
     }
     k_prec_scatter<<<nb, 256, 0, s>>>(P->loc.p, P->pos.p, n, P->nc > 0 ? P->Rr_ptr.p : nullptr, P->Rr_col.p,
-                                      P->Rr_val.p, loc_c, z, done);
+                                      P->Rr_val.p, loc_c, z, done); ::sbg::count_launch();
     SBG_LAUNCH_CHECK();
 }
 
@@ -613,8 +613,8 @@ void coarse_galerkin(Ctx* ctx, const DMatrix& W, const Prolongation& R, std::vec
     cp.upload(R.col_ptr, s);
     cr.upload(R.row_idx, s);
     cv.upload(R.val, s);
-    k_coarse_WR<<<std::min(n, 8 * ctx->sm_count), 128, 0, s>>>(W.a.p, W.ld, n, cp.p, cr.p, cv.p, nc, WR.p);
-    k_coarse_H<<<nc, 128, 0, s>>>(WR.p, cp.p, cr.p, cv.p, nc, dH.p);
+    k_coarse_WR<<<std::min(n, 8 * ctx->sm_count), 128, 0, s>>>(W.a.p, W.ld, n, cp.p, cr.p, cv.p, nc, WR.p); ::sbg::count_launch();
+    k_coarse_H<<<nc, 128, 0, s>>>(WR.p, cp.p, cr.p, cv.p, nc, dH.p); ::sbg::count_launch();
     SBG_LAUNCH_CHECK();
     SBG_CUDA(cudaMemcpyAsync(H.data(), dH.p, H.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
     SBG_CUDA(cudaStreamSynchronize(s));

@@ -60,6 +60,12 @@ SIGNATURES = {
     "sbg_timers_enable": (C.c_int, [vp, C.c_int]),
     "sbg_timers_reset": (C.c_int, [vp]),
     "sbg_timer_get": (C.c_int, [vp, C.c_char_p, C.POINTER(C.c_double), C.POINTER(C.c_longlong)]),
+    "sbg_timer_begin": (C.c_int, [vp, C.c_char_p]),
+    "sbg_timer_end": (C.c_int, [vp]),
+    "sbg_launch_count": (C.c_longlong, []),
+    "sbg_assembly_plan_create": (C.c_int, [vp, vp, C.POINTER(QuadCfgC), C.POINTER(vp)]),
+    "sbg_assembly_run": (C.c_int, [vp, C.POINTER(vp), C.POINTER(AssemblyStatsC)]),
+    "sbg_assembly_plan_destroy": (None, [vp]),
     "sbg_mesh_create": (C.c_int, [C.c_int, f64p, C.c_int, i32p, C.POINTER(vp)]),
     "sbg_mesh_destroy": (None, [vp]),
     "sbg_mesh_sizes": (C.c_int, [vp, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
@@ -118,6 +124,8 @@ SIGNATURES = {
     "sbg_matvec_device": (C.c_int, [vp, vp, vp, vp, C.c_int]),
     "sbg_apply_preconditioner_device": (C.c_int, [vp, vp, vp, vp, C.c_int]),
     "sbg_l2_flush": (C.c_int, [vp]),
+    "sbg_fp64_peak": (C.c_int, [vp, C.POINTER(C.c_double)]),
+    "sbg_config_g": (C.c_int, [C.c_int, f64p]),
 }
 
 _lib = None
@@ -191,6 +199,32 @@ class Context(_Handle):
 
     def l2_flush(self):
         _check(lib().sbg_l2_flush(self.h))
+
+    def begin(self, name: str):
+        _check(lib().sbg_timer_begin(self.h, name.encode()))
+
+    def end(self):
+        _check(lib().sbg_timer_end(self.h))
+
+
+def fp64_peak_tflops(ctx: "Context" = None) -> float:
+    """Measured DFMA throughput of the device (TFLOP/s)."""
+    ctx = ctx or default_context()
+    t = C.c_double()
+    _check(lib().sbg_fp64_peak(ctx.h, C.byref(t)))
+    return t.value
+
+
+def config_g(cfg: int):
+    """Neumann field g of a BASELINE config (seeded std::mt19937 draws for cfg 2 and 4)."""
+    g = np.zeros(3)
+    _check(lib().sbg_config_g(cfg, g))
+    return g
+
+
+def launch_count() -> int:
+    """Kernels launched by libscreenbem_b200 so far (all contexts)."""
+    return lib().sbg_launch_count()
 
 
 _default_ctx = None
@@ -413,6 +447,33 @@ def assemble_W(im: InflatedMesh, cfg: QuadratureConfig = None, workers: int = 1,
     _check(lib().sbg_assemble_w(ctx.h, im.h, C.byref(c), workers, C.byref(h), C.byref(st)))
     stats = {n: getattr(st, n) for n, _ in AssemblyStatsC._fields_}
     return GalerkinMatrix(h, ctx, stats)
+
+
+class AssemblyPlan(_Handle):
+    """Mesh-derived device data of assemble_W, built once (host preparation);
+    run() is the device-only assembly into a resident GalerkinMatrix."""
+    _destroy = "sbg_assembly_plan_destroy"
+
+    def __init__(self, im: InflatedMesh, cfg: QuadratureConfig = None, ctx: Context = None):
+        self.ctx = ctx or default_context()
+        cfg = cfg or QuadratureConfig()
+        c = cfg.c()
+        h = vp()
+        _check(lib().sbg_assembly_plan_create(self.ctx.h, im.h, C.byref(c), C.byref(h)))
+        super().__init__(h)
+        self.n, self.nf = im.n, im.base.nf
+        self._W = None
+
+    def run(self, W: GalerkinMatrix = None) -> GalerkinMatrix:
+        st = AssemblyStatsC()
+        hw = vp(W.h if W is not None else None)
+        _check(lib().sbg_assembly_run(self.h, C.byref(hw), C.byref(st)))
+        stats = {n: getattr(st, n) for n, _ in AssemblyStatsC._fields_}
+        if W is None:
+            W = GalerkinMatrix(hw, self.ctx, stats)
+        else:
+            W.stats = stats
+        return W
 
 
 def pair_integrals(m: SurfaceMesh, f, g, cfg: QuadratureConfig = None, ctx: Context = None):
