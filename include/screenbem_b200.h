@@ -160,6 +160,10 @@ void sbg_prolong_destroy(sbg_prolong* p);
 /* ---- Schwarz preconditioner (device) -------------------------------------- */
 int sbg_build_preconditioner(sbg_ctx* ctx, const sbg_matrix* W, const sbg_partition* part, const sbg_prolong* R,
                              sbg_prec** out); /* inc/schwarz.hpp:100-118 */
+/* mode 1 (default): block inverses L^-T L^-1 formed once, apply = one batched GEMV;
+ * mode 0: blocked forward/backward triangular solves with L (llt.solve, schwarz.hpp:130) */
+int sbg_build_preconditioner_mode(sbg_ctx* ctx, const sbg_matrix* W, const sbg_partition* part, const sbg_prolong* R,
+                                  int mode, sbg_prec** out);
 int sbg_apply_preconditioner(sbg_ctx* ctx, sbg_prec* p, const double* r_host, int n, double* z_host); /* :121-140 */
 int sbg_prec_num_subspaces(const sbg_prec* p);
 int sbg_prec_block_diag(sbg_ctx* ctx, sbg_prec* p, int which, double* diag, int* n_out); /* which: face, -1 WB, -2 coarse */

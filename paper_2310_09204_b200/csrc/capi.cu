@@ -659,7 +659,24 @@ int sbg_build_preconditioner(sbg_ctx* ctx, const sbg_matrix* W, const sbg_partit
         none.rows = W->M.n;
         auto* p = new sbg_prec;
         try {
-            p->P = prec_build(&ctx->c, W->M, part->p, R ? R->R : none);
+            p->P = prec_build(&ctx->c, W->M, part->p, R ? R->R : none, kPrecInverse);
+        } catch (...) {
+            delete p;
+            throw;
+        }
+        *out = p;
+    });
+}
+int sbg_build_preconditioner_mode(sbg_ctx* ctx, const sbg_matrix* W, const sbg_partition* part, const sbg_prolong* R,
+                                  int mode, sbg_prec** out)
+{
+    return guard([&] {
+        if (mode != kPrecTrsv && mode != kPrecInverse) throw ValidationError("unknown preconditioner apply mode");
+        Prolongation none;
+        none.rows = W->M.n;
+        auto* p = new sbg_prec;
+        try {
+            p->P = prec_build(&ctx->c, W->M, part->p, R ? R->R : none, mode);
         } catch (...) {
             delete p;
             throw;

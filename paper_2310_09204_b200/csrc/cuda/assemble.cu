@@ -276,14 +276,15 @@ __global__ void k_classify_near(const TileInfo* __restrict__ tiles, GeoPtrs G, c
 
 // ---------------------------------------------------------------- near pairs (recursion)
 // The split4 recursion of triangle_pair_disjoint (quadrature.hpp:231-249) is
-// run in three phases:
-//   N1/N3  one thread per pair walks the recursion depth-first in the
-//          reference's child order with no-FMA classification (bitwise the
-//          oracle's decisions), first counting, then writing its leaves as
-//          18-bit path codes (depth | per level: split side, child index);
-//   N4     leaves are evaluated two per warp (one per half-warp, a 9x9 block
-//          of the 36x36 rule per lane) after replaying the path from the root;
-//   N5     one thread per pair sums its leaves in depth-first order.
+// run level-synchronously: the frontier of recursion nodes at depth L is a list
+// of (local pair index, path code) records; one thread per node replays its
+// path from the pair's triangles, classifies it with no-FMA arithmetic (bitwise
+// the oracle's decision: leaf iff dist >= thr * diam or depth >= 5, split the
+// larger triangle, t on ties) and appends either a leaf record or its four
+// children.  Leaves of each level are then evaluated two per warp (one per
+// half-warp, a 9x9 block of the 36x36 rule per lane) and accumulated into the
+// pair's integral.  Path code: bits 0-2 depth, then per level 3 bits
+// (split side | child << 1).
 __device__ __forceinline__ double tri_diam(const double* t)
 {
     const D3 a = {t[0], t[1], t[2]}, b = {t[3], t[4], t[5]}, c = {t[6], t[7], t[8]};
@@ -302,7 +303,7 @@ __device__ __forceinline__ double tri_area(const double* t)
     return __dmul_rn(0.5, d3_norm(d3_cross(d3_sub(b, a), d3_sub(c, a))));
 }
 // child k of split4 (quadrature.hpp:222-229): {v0,m01,m02},{m01,v1,m12},{m02,m12,v2},{m01,m12,m02}
-__device__ __forceinline__ void split4_child(const double* t, int k, double* out)
+__device__ __forceinline__ void split4_child_inplace(double* t, int k)
 {
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
@@ -310,181 +311,94 @@ __device__ __forceinline__ void split4_child(const double* t, int k, double* out
         const double m01 = __dmul_rn(0.5, __dadd_rn(v0, v1));
         const double m12 = __dmul_rn(0.5, __dadd_rn(v1, v2));
         const double m02 = __dmul_rn(0.5, __dadd_rn(v0, v2));
-        double a, b, d;
-        if (k == 0) {
-            a = v0; b = m01; d = m02;
-        } else if (k == 1) {
-            a = m01; b = v1; d = m12;
-        } else if (k == 2) {
-            a = m02; b = m12; d = v2;
-        } else {
-            a = m01; b = m12; d = m02;
-        }
-        out[c] = a;
-        out[3 + c] = b;
-        out[6 + c] = d;
+        t[c] = k == 0 ? v0 : (k == 2 ? m02 : m01);
+        t[3 + c] = k == 0 ? m01 : (k == 1 ? v1 : m12);
+        t[6 + c] = k == 0 ? m02 : (k == 1 ? m12 : (k == 2 ? v2 : m02));
+    }
+}
+// triangles of the node (pair root triangles replayed along the path)
+__device__ __forceinline__ void node_triangles(const double* __restrict__ GV, int2 pr, unsigned code, double* t,
+                                               double* s)
+{
+#pragma unroll
+    for (int c = 0; c < 9; ++c) {
+        t[c] = __ldg(GV + 9 * pr.x + c);
+        s[c] = __ldg(GV + 9 * pr.y + c);
+    }
+    const int depth = code & 7;
+    for (int lv = 0; lv < depth; ++lv) {
+        const unsigned e = (code >> (3 + 3 * lv)) & 7;
+        if (e & 1)
+            split4_child_inplace(t, (int)(e >> 1));
+        else
+            split4_child_inplace(s, (int)(e >> 1));
     }
 }
 
-// Depth-first walk of one pair; returns the number of leaves and, when
-// codes != nullptr, writes their path codes in visiting order.
-__device__ int near_walk(const double* root_t, const double* root_s, double thr, unsigned* codes)
+struct NearNode {
+    int pair;       // index into the near-pair list
+    unsigned code;  // path code
+};
+
+// classify every node of level `depth`: leaves go to `leaves`, split nodes append 4 children to `next`
+__global__ void k_near_level(const NearNode* __restrict__ nodes, const unsigned long long* __restrict__ nnodes_dev,
+                             long long cap_nodes, int depth, const int2* __restrict__ pairs,
+                             const double* __restrict__ GV, double thr, NearNode* __restrict__ leaves,
+                             unsigned long long* __restrict__ nleaves, long long cap_leaves,
+                             NearNode* __restrict__ next, unsigned long long* __restrict__ nnext, long long cap_next)
 {
-    double T[6][9], Sv[6][9];
-    int child[6], side[6];
-    for (int q = 0; q < 9; ++q) {
-        T[0][q] = root_t[q];
-        Sv[0][q] = root_s[q];
-    }
-    int d = 0, count = 0;
-    while (true) {
-        // visit node d
-        bool leaf = d >= 5;
+    const long long nn = min((long long)*nnodes_dev, cap_nodes);
+    for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < nn; k += (long long)gridDim.x * blockDim.x) {
+        const NearNode nd = nodes[k];
+        bool leaf = depth >= 5;
         int split_t = 0;
         if (!leaf) {
-            const double dt = tri_diam(T[d]), ds = tri_diam(Sv[d]);
+            double t[9], s[9];
+            node_triangles(GV, pairs[nd.pair], nd.code, t, s);
+            const double dt = tri_diam(t), ds = tri_diam(s);
             D3 ct, cs;
             double rt, rs;
-            tri_centroid_rad(T[d], ct, rt);
-            tri_centroid_rad(Sv[d], cs, rs);
+            tri_centroid_rad(t, ct, rt);
+            tri_centroid_rad(s, cs, rs);
             const double dist = fmax(0.0, __dsub_rn(__dsub_rn(d3_norm(d3_sub(ct, cs)), rt), rs));
             leaf = dist >= __dmul_rn(thr, fmax(dt, ds));
             split_t = dt >= ds ? 1 : 0;
         }
         if (leaf) {
-            if (codes) {
-                unsigned code = (unsigned)d;
-                for (int l = 0; l < d; ++l) code |= (unsigned)(side[l] | (child[l] << 1)) << (3 + 3 * l);
-                codes[count] = code;
-            }
-            ++count;
-            // advance to the next sibling (or pop)
-            bool done = true;
-            while (d > 0) {
-                const int p = d - 1;
-                if (++child[p] < 4) {
-                    if (side[p]) {
-                        split4_child(T[p], child[p], T[d]);
-                        for (int q = 0; q < 9; ++q) Sv[d][q] = Sv[p][q];
-                    } else {
-                        split4_child(Sv[p], child[p], Sv[d]);
-                        for (int q = 0; q < 9; ++q) T[d][q] = T[p][q];
-                    }
-                    done = false;
-                    break;
-                }
-                --d;
-            }
-            if (done) break;
+            const unsigned long long q = atomicAdd(nleaves, 1ull);
+            if ((long long)q < cap_leaves) leaves[q] = nd;
         } else {
-            side[d] = split_t;
-            child[d] = 0;
-            if (split_t) {
-                split4_child(T[d], 0, T[d + 1]);
-                for (int q = 0; q < 9; ++q) Sv[d + 1][q] = Sv[d][q];
-            } else {
-                split4_child(Sv[d], 0, Sv[d + 1]);
-                for (int q = 0; q < 9; ++q) T[d + 1][q] = T[d][q];
-            }
-            ++d;
+            const unsigned long long q = atomicAdd(nnext, 4ull);
+            const unsigned base = (nd.code & ~7u) | (unsigned)(depth + 1);
+            for (int c = 0; c < 4; ++c)
+                if ((long long)q + c < cap_next)
+                    next[q + c] = {nd.pair, base | ((unsigned)(split_t | (c << 1)) << (3 + 3 * depth))};
         }
-    }
-    return count;
-}
-
-__global__ void k_near_count(const int2* __restrict__ pairs, const unsigned long long* __restrict__ np_dev,
-                             long long cap, const double* __restrict__ GV, double thr, long long* __restrict__ nleaf)
-{
-    const long long np = min((long long)*np_dev, cap);
-    for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < np; p += (long long)gridDim.x * blockDim.x) {
-        const int2 pr = pairs[p];
-        nleaf[p] = near_walk(GV + 9 * pr.x, GV + 9 * pr.y, thr, nullptr);
     }
 }
 
-__global__ void k_near_fill(const int2* __restrict__ pairs, const unsigned long long* __restrict__ np_dev,
-                            long long cap, const double* __restrict__ GV, double thr,
-                            const long long* __restrict__ off, unsigned* __restrict__ codes, int* __restrict__ owner)
+// leaves: two per warp; lane (ia, jb) of each half-warp owns i in [9ia, 9ia+9), j in [9jb, 9jb+9)
+__global__ void __launch_bounds__(256) k_near_leaves(const NearNode* __restrict__ leaves,
+                                                     const unsigned long long* __restrict__ nleaves_dev,
+                                                     long long cap, const int2* __restrict__ pairs,
+                                                     const double* __restrict__ GV, double inv_pi,
+                                                     double* __restrict__ out)
 {
-    const long long np = min((long long)*np_dev, cap);
-    for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < np; p += (long long)gridDim.x * blockDim.x) {
-        const int2 pr = pairs[p];
-        const long long o = off[p];
-        const int c = near_walk(GV + 9 * pr.x, GV + 9 * pr.y, thr, codes + o);
-        for (int k = 0; k < c; ++k) owner[o + k] = (int)p;
-    }
-}
-
-// exclusive scan of per-pair leaf counts (single CTA, chunked; counts are small)
-__global__ void k_scan_exclusive(const long long* __restrict__ in, const unsigned long long* __restrict__ np_dev,
-                                 long long cap, long long* __restrict__ out, long long* __restrict__ total)
-{
-    __shared__ long long part[1024];
-    __shared__ long long carry;
-    const long long n = min((long long)*np_dev, cap);
-    if (threadIdx.x == 0) carry = 0;
-    __syncthreads();
-    const int T = blockDim.x;
-    for (long long base = 0; base < n; base += (long long)T * 8) {
-        long long v[8], s = 0;
-        for (int k = 0; k < 8; ++k) {
-            const long long i = base + (long long)threadIdx.x * 8 + k;
-            v[k] = i < n ? in[i] : 0;
-            s += v[k];
-        }
-        part[threadIdx.x] = s;
-        __syncthreads();
-        for (int o = 1; o < T; o <<= 1) {
-            const long long add = threadIdx.x >= o ? part[threadIdx.x - o] : 0;
-            __syncthreads();
-            part[threadIdx.x] += add;
-            __syncthreads();
-        }
-        long long run = carry + part[threadIdx.x] - s;
-        for (int k = 0; k < 8; ++k) {
-            const long long i = base + (long long)threadIdx.x * 8 + k;
-            if (i < n) out[i] = run;
-            run += v[k];
-        }
-        __syncthreads();
-        if (threadIdx.x == T - 1) carry += part[T - 1];
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) *total = carry;
-}
-
-// N4: two leaves per warp; lane (ia, jb) of each half-warp owns i in [9ia, 9ia+9), j in [9jb, 9jb+9)
-__global__ void __launch_bounds__(256) k_near_leaves(const unsigned* __restrict__ codes, const int* __restrict__ owner,
-                                                     long long nleaves, const int2* __restrict__ pairs,
-                                                     const double* __restrict__ GV, double* __restrict__ leaf_val)
-{
+    const long long nl = min((long long)*nleaves_dev, cap);
     const int lane = threadIdx.x & 31;
     const int h = lane >> 4, l16 = lane & 15, ia = l16 >> 2, jb = l16 & 3;
     const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
-    for (long long w = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); 2 * w < nleaves; w += warps) {
+    for (long long w = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); 2 * w < nl; w += warps) {
         const long long q = 2 * w + h;
-        const bool active = q < nleaves;
+        const bool active = q < nl;
         double acc = 0.0, scale = 0.0;
+        int pair = 0;
         if (active) {
-            const unsigned code = codes[q];
-            const int2 pr = pairs[owner[q]];
-            double t[9], s[9], tmp[9];
-            for (int c = 0; c < 9; ++c) {
-                t[c] = GV[9 * pr.x + c];
-                s[c] = GV[9 * pr.y + c];
-            }
-            const int depth = code & 7;
-            for (int lv = 0; lv < depth; ++lv) {
-                const unsigned e = (code >> (3 + 3 * lv)) & 7;
-                if (e & 1) {
-                    split4_child(t, (int)(e >> 1), tmp);
-                    for (int c = 0; c < 9; ++c) t[c] = tmp[c];
-                } else {
-                    split4_child(s, (int)(e >> 1), tmp);
-                    for (int c = 0; c < 9; ++c) s[c] = tmp[c];
-                }
-            }
-            scale = tri_area(t) * tri_area(s);
+            const NearNode nd = leaves[q];
+            pair = nd.pair;
+            double t[9], s[9];
+            node_triangles(GV, pairs[nd.pair], nd.code, t, s);
+            scale = tri_area(t) * tri_area(s) * inv_pi;
             const double e1x = s[3] - s[0], e1y = s[4] - s[1], e1z = s[5] - s[2];
             const double e2x = s[6] - s[0], e2y = s[7] - s[1], e2z = s[8] - s[2];
             double yx[9], yy[9], yz[9];
@@ -516,23 +430,8 @@ __global__ void __launch_bounds__(256) k_near_leaves(const unsigned* __restrict_
                 acc = fma(c_near_w[i], in0 + in1, acc);
             }
         }
-        // reduce over the 16 lanes of each half-warp
         for (int o = 8; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if (active && l16 == 0) leaf_val[q] = acc * scale;
-    }
-}
-
-// N5: I = sum of the pair's leaves (visiting order) / pi
-__global__ void k_near_reduce(const long long* __restrict__ off, const long long* __restrict__ nleaf,
-                              const unsigned long long* __restrict__ np_dev, long long cap,
-                              const double* __restrict__ leaf_val, double inv_pi, double* __restrict__ out)
-{
-    const long long np = min((long long)*np_dev, cap);
-    for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < np; p += (long long)gridDim.x * blockDim.x) {
-        double s = 0.0;
-        const long long o = off[p];
-        for (long long k = 0; k < nleaf[p]; ++k) s += leaf_val[o + k];
-        out[p] = s * inv_pi;
+        if (active && l16 == 0) atomicAdd(out + pair, acc * scale);
     }
 }
 
@@ -841,11 +740,21 @@ void run_sauter(Ctx* ctx, const DBuf<double>& X, const std::vector<int>& pv, con
 }
 
 struct NearWork {
-    DBuf<long long> nleaf, off, total;
-    DBuf<unsigned> codes;
-    DBuf<int> owner;
-    DBuf<double> leaf_val;
+    DBuf<NearNode> cur, next, leaves;
+    DBuf<unsigned long long> cnt;  // [0] current frontier, [1] next frontier, [2] leaves
 };
+
+__global__ void k_near_init(const unsigned long long* __restrict__ np_dev, long long cap, NearNode* __restrict__ nodes,
+                            double* __restrict__ out, unsigned long long* __restrict__ cnt)
+{
+    const long long np = min((long long)*np_dev, cap);
+    const long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < np) {
+        nodes[k] = {(int)k, 0u};
+        out[k] = 0.0;
+    }
+    if (k == 0) cnt[0] = (unsigned long long)np;
+}
 
 // near-pair integrals for the device list pairs[0:*np_dev] (capacity cap); returns the leaf count
 long long run_near(Ctx* ctx, const double* GV, const int2* pairs, const unsigned long long* np_dev, long long cap,
@@ -854,40 +763,43 @@ long long run_near(Ctx* ctx, const double* GV, const int2* pairs, const unsigned
     if (cap <= 0) return 0;
     cudaStream_t s = ctx->stream;
     TimedScope ts(ctx, "near");
-    if ((long long)NW.nleaf.n < cap) {
-        NW.nleaf.alloc(cap);
-        NW.off.alloc(cap);
-    }
-    if (!NW.total.n) NW.total.alloc(1);
-    const int thr_blk = 128;
-    const int grid = (int)std::min<long long>((cap + thr_blk - 1) / thr_blk, 8LL * ctx->sm_count);
-    k_near_count<<<grid, thr_blk, 0, s>>>(pairs, np_dev, cap, GV, thr, NW.nleaf.p);
-    count_launch();
-    k_scan_exclusive<<<1, 1024, 0, s>>>(NW.nleaf.p, np_dev, cap, NW.off.p, NW.total.p);
+    if (!NW.cnt.n) NW.cnt.alloc(3);
+    if ((long long)NW.cur.n < cap) NW.cur.alloc(cap);
+    k_near_init<<<(int)((cap + 255) / 256), 256, 0, s>>>(np_dev, cap, NW.cur.p, out, NW.cnt.p);
     count_launch();
     SBG_LAUNCH_CHECK();
-    long long total = 0;
-    SBG_CUDA(cudaMemcpyAsync(&total, NW.total.p, sizeof(total), cudaMemcpyDeviceToHost, s));
+    unsigned long long h[3] = {0, 0, 0};
+    SBG_CUDA(cudaMemcpyAsync(h, NW.cnt.p, sizeof(h[0]), cudaMemcpyDeviceToHost, s));
     SBG_CUDA(cudaStreamSynchronize(s));
-    if (total == 0) return 0;
-    if ((long long)NW.codes.n < total) {
-        NW.codes.alloc(total);
-        NW.owner.alloc(total);
-        NW.leaf_val.alloc(total);
+    long long ncur = (long long)h[0], total_leaves = 0;
+    for (int depth = 0; depth <= 5 && ncur > 0; ++depth) {
+        const long long cap_next = depth < 5 ? 4 * ncur : 0;
+        if ((long long)NW.next.n < cap_next) NW.next.alloc(cap_next);
+        if ((long long)NW.leaves.n < ncur) NW.leaves.alloc(ncur);
+        SBG_CUDA(cudaMemsetAsync(NW.cnt.p + 1, 0, 2 * sizeof(unsigned long long), s));
+        {
+            TimedScope tc(ctx, "near_classify");
+            const int grid = (int)std::min<long long>((ncur + 127) / 128, 16LL * ctx->sm_count);
+            k_near_level<<<grid, 128, 0, s>>>(NW.cur.p, NW.cnt.p, ncur, depth, pairs, GV, thr, NW.leaves.p,
+                                              NW.cnt.p + 2, ncur, NW.next.p, NW.cnt.p + 1, cap_next);
+            count_launch();
+        }
+        {
+            TimedScope tl(ctx, "near_leaves");
+            const long long warps = (ncur + 1) / 2;  // upper bound on this level's leaf pairs
+            const int lgrid = (int)std::min<long long>((warps + 7) / 8, 32LL * ctx->sm_count);
+            k_near_leaves<<<lgrid, 256, 0, s>>>(NW.leaves.p, NW.cnt.p + 2, ncur, pairs, GV, 1.0 / M_PI, out);
+            count_launch();
+        }
+        SBG_LAUNCH_CHECK();
+        SBG_CUDA(cudaMemcpyAsync(h, NW.cnt.p, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+        SBG_CUDA(cudaStreamSynchronize(s));
+        total_leaves += (long long)h[2];
+        ncur = (long long)h[1];
+        std::swap(NW.cur, NW.next);
+        if (ncur > 0) SBG_CUDA(cudaMemcpyAsync(NW.cnt.p, &h[1], sizeof(h[1]), cudaMemcpyHostToDevice, s));
     }
-    k_near_fill<<<grid, thr_blk, 0, s>>>(pairs, np_dev, cap, GV, thr, NW.off.p, NW.codes.p, NW.owner.p);
-    count_launch();
-    {
-        TimedScope tl(ctx, "near_leaves");
-        const long long warps = (total + 1) / 2;
-        const int lgrid = (int)std::min<long long>((warps + 7) / 8, 64LL * ctx->sm_count);
-        k_near_leaves<<<lgrid, 256, 0, s>>>(NW.codes.p, NW.owner.p, total, pairs, GV, NW.leaf_val.p);
-        count_launch();
-    }
-    k_near_reduce<<<grid, thr_blk, 0, s>>>(NW.off.p, NW.nleaf.p, np_dev, cap, NW.leaf_val.p, 1.0 / M_PI, out);
-    count_launch();
-    SBG_LAUNCH_CHECK();
-    return total;
+    return total_leaves;
 }
 
 }  // namespace

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -91,6 +92,7 @@ struct Ctx {
     int sm_count = kNumSMs;
     cudaStream_t stream = nullptr;
     Timers timers;
+    std::shared_ptr<void> pcg_ws;  // cached PCG workspace (linalg.cu)
     ~Ctx();
 };
 

@@ -57,7 +57,9 @@ void gemv(Ctx* ctx, const DMatrix& W, GemvPlan& plan, const double* x, double* y
 
 // ---------------------------------------------------------------- Schwarz preconditioner
 struct Prec;
-Prec* prec_build(Ctx* ctx, const DMatrix& W, const DofPartition& part, const Prolongation& R);
+enum { kPrecTrsv = 0, kPrecInverse = 1 };
+Prec* prec_build(Ctx* ctx, const DMatrix& W, const DofPartition& part, const Prolongation& R, int mode);
+int prec_mode(const Prec* p);
 void prec_destroy(Prec* p);
 int prec_n(const Prec* p);
 int prec_num_subspaces(const Prec* p);

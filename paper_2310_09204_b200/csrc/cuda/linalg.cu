@@ -300,6 +300,41 @@ double lanczos_kappa(const std::vector<double>& alphas, const std::vector<double
     return kappa < 1.0 ? 1.0 : kappa;
 }
 
+// Device workspace of one PCG size, cached on the context (no allocation or
+// pinned-memory registration per solve).
+struct PcgWork {
+    int ld = 0, cap = 0;
+    DBuf<double> buf, partials, hist, alphas, betas;
+    DBuf<PcgDev> st;
+    GemvPlan plan;
+    PcgDev* hs = nullptr;
+    ~PcgWork()
+    {
+        if (hs) cudaFreeHost(hs);
+    }
+};
+
+static PcgWork& pcg_work(Ctx* ctx, const DMatrix& W, int maxit)
+{
+    auto* w = static_cast<PcgWork*>(ctx->pcg_ws.get());
+    if (!w || w->ld != W.ld || w->plan.n != W.n || w->cap < maxit + 2) {
+        auto fresh = std::make_shared<PcgWork>();
+        fresh->ld = W.ld;
+        fresh->cap = std::max(maxit + 2, 128);
+        fresh->buf.alloc(6 * (size_t)W.ld);
+        fresh->partials.alloc(std::max((W.n + 255) / 256, 1));
+        fresh->hist.alloc(fresh->cap);
+        fresh->alphas.alloc(fresh->cap);
+        fresh->betas.alloc(fresh->cap);
+        fresh->st.alloc(1);
+        gemv_plan(ctx, W.n, W.ld, fresh->plan);
+        SBG_CUDA(cudaMallocHost(&fresh->hs, sizeof(PcgDev)));
+        ctx->pcg_ws = fresh;
+        w = fresh.get();
+    }
+    return *w;
+}
+
 // reference: inc/pcg.hpp:33-116.  All vectors and scalars stay on the device;
 // the host enqueues iterations in growing batches and reads back one small
 // state record per batch (iterations past convergence are no-op launches).
@@ -312,62 +347,55 @@ void pcg_run(Ctx* ctx, const DMatrix& W, Prec* prec, const double* rhs, double* 
     if (maxit <= 0) maxit = std::max(10 * n, 100);
     TimedScope tpcg(ctx, "pcg");
     cudaStream_t s = ctx->stream;
+    PcgWork& w = pcg_work(ctx, W, maxit);
     const size_t len = (size_t)W.ld;
-    DBuf<double> buf(6 * len);
-    SBG_CUDA(cudaMemsetAsync(buf.p, 0, buf.n * sizeof(double), s));
-    double* x = buf.p;
+    SBG_CUDA(cudaMemsetAsync(w.buf.p, 0, w.buf.n * sizeof(double), s));
+    double* x = w.buf.p;
     double* r = x + len;
     double* zbuf = r + len;
     double* p = zbuf + len;
     double* Wp = p + len;
     double* z = prec ? zbuf : r;  // no preconditioner: z = r (pcg.hpp:45-47)
-    if (on_device)
-        SBG_CUDA(cudaMemcpyAsync(r, rhs, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
-    else
-        SBG_CUDA(cudaMemcpyAsync(r, rhs, n * sizeof(double), cudaMemcpyHostToDevice, s));
+    SBG_CUDA(cudaMemcpyAsync(r, rhs, n * sizeof(double), on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
     const int nb = (n + 255) / 256;
-    DBuf<double> partials(std::max(nb, 1));
-    DBuf<double> hist(maxit + 2), alphas(maxit + 1), betas(maxit + 1);
-    DBuf<PcgDev> st(1);
     PcgDev h{};
     h.tol = tol;
     h.maxit = maxit;
-    SBG_CUDA(cudaMemcpyAsync(st.p, &h, sizeof(h), cudaMemcpyHostToDevice, s));
-    GemvPlan plan;
-    gemv_plan(ctx, n, W.ld, plan);
-    const int* done = &st.p->done;
-
+    SBG_CUDA(cudaMemcpyAsync(w.st.p, &h, sizeof(h), cudaMemcpyHostToDevice, s));
+    const int* done = &w.st.p->done;
     if (n > 0) {
         if (prec) prec_apply(ctx, prec, r, z, nullptr);
-        k_pcg_init<<<nb, 256, 0, s>>>(st.p, r, z, p, n, partials.p, hist.p); ::sbg::count_launch();
+        k_pcg_init<<<nb, 256, 0, s>>>(w.st.p, r, z, p, n, w.partials.p, w.hist.p);
+        count_launch();
         SBG_LAUNCH_CHECK();
     } else {
         h.converged = 1;
         h.done = 1;
-        SBG_CUDA(cudaMemcpyAsync(st.p, &h, sizeof(h), cudaMemcpyHostToDevice, s));
+        SBG_CUDA(cudaMemcpyAsync(w.st.p, &h, sizeof(h), cudaMemcpyHostToDevice, s));
     }
-    PcgDev* hs = nullptr;
-    SBG_CUDA(cudaMallocHost(&hs, sizeof(PcgDev)));
     int batch = 4, enqueued = 0;
     while (true) {
-        SBG_CUDA(cudaMemcpyAsync(hs, st.p, sizeof(PcgDev), cudaMemcpyDeviceToHost, s));
+        SBG_CUDA(cudaMemcpyAsync(w.hs, w.st.p, sizeof(PcgDev), cudaMemcpyDeviceToHost, s));
         SBG_CUDA(cudaStreamSynchronize(s));
-        if (hs->done || enqueued >= maxit) break;
+        if (w.hs->done || enqueued >= maxit) break;
         const int todo = std::min(batch, maxit - enqueued);
         for (int t = 0; t < todo; ++t) {
-            gemv_partial_launch(ctx, W, plan, p, done);
-            k_pcg_alpha<<<nb, 256, 0, s>>>(st.p, plan.part.p, plan.chunks, W.ld, n, p, Wp, partials.p); ::sbg::count_launch();
-            k_pcg_update<<<nb, 256, 0, s>>>(st.p, x, r, p, Wp, n); ::sbg::count_launch();
+            gemv_partial_launch(ctx, W, w.plan, p, done);
+            k_pcg_alpha<<<nb, 256, 0, s>>>(w.st.p, w.plan.part.p, w.plan.chunks, W.ld, n, p, Wp, w.partials.p);
+            count_launch();
+            k_pcg_update<<<nb, 256, 0, s>>>(w.st.p, x, r, p, Wp, n);
+            count_launch();
             if (prec) prec_apply(ctx, prec, r, z, done);
-            k_pcg_rz<<<nb, 256, 0, s>>>(st.p, r, z, n, partials.p, hist.p, alphas.p, betas.p); ::sbg::count_launch();
-            k_pcg_p<<<nb, 256, 0, s>>>(st.p, p, z, n); ::sbg::count_launch();
+            k_pcg_rz<<<nb, 256, 0, s>>>(w.st.p, r, z, n, w.partials.p, w.hist.p, w.alphas.p, w.betas.p);
+            count_launch();
+            k_pcg_p<<<nb, 256, 0, s>>>(w.st.p, p, z, n);
+            count_launch();
             SBG_LAUNCH_CHECK();
         }
         enqueued += todo;
         batch = std::min(batch * 2, 64);
     }
-    const PcgDev fin = *hs;
-    cudaFreeHost(hs);
+    const PcgDev fin = *w.hs;
     if (fin.error == 1) throw NumericalError("pcg: matrix is not positive definite");
     if (fin.error == 2) throw NumericalError("pcg: preconditioner is not positive definite");
     out.iterations = fin.it;
@@ -376,18 +404,15 @@ void pcg_run(Ctx* ctx, const DMatrix& W, Prec* prec, const double* rhs, double* 
     out.alphas.assign(fin.it, 0.0);
     out.betas.assign(fin.it, 0.0);
     if (n > 0) {
-        SBG_CUDA(cudaMemcpyAsync(out.history.data(), hist.p, (fin.it + 1) * sizeof(double), cudaMemcpyDeviceToHost, s));
+        SBG_CUDA(cudaMemcpyAsync(out.history.data(), w.hist.p, (fin.it + 1) * sizeof(double), cudaMemcpyDeviceToHost, s));
         if (fin.it) {
-            SBG_CUDA(cudaMemcpyAsync(out.alphas.data(), alphas.p, fin.it * sizeof(double), cudaMemcpyDeviceToHost, s));
-            SBG_CUDA(cudaMemcpyAsync(out.betas.data(), betas.p, fin.it * sizeof(double), cudaMemcpyDeviceToHost, s));
+            SBG_CUDA(cudaMemcpyAsync(out.alphas.data(), w.alphas.p, fin.it * sizeof(double), cudaMemcpyDeviceToHost, s));
+            SBG_CUDA(cudaMemcpyAsync(out.betas.data(), w.betas.p, fin.it * sizeof(double), cudaMemcpyDeviceToHost, s));
         }
+        SBG_CUDA(cudaMemcpyAsync(x_out, x, n * sizeof(double), on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s));
     } else {
         out.history.assign(1, 0.0);
     }
-    if (on_device)
-        SBG_CUDA(cudaMemcpyAsync(x_out, x, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
-    else
-        SBG_CUDA(cudaMemcpyAsync(x_out, x, n * sizeof(double), cudaMemcpyDeviceToHost, s));
     SBG_CUDA(cudaStreamSynchronize(s));
     out.kappa = lanczos_kappa(out.alphas, out.betas);
 }

@@ -2,13 +2,18 @@
 // reference: inc/schwarz.hpp:55-140 (blocks, factor_block, build, apply).
 //
 // All blocks — faces (map order), the wire-basket and the coarse matrix — form
-// one batch of dense SPD matrices, factored by a batched right-looking tiled
-// Cholesky (64x64 tiles): potrf of the diagonal tile (+ its inverse D_k), a
-// "trsm" GEMM A_ik <- A_ik D_k^T and the trailing update A_ij -= A_ik A_jk^T,
-// both on the FP64 tensor cores (DMMA, mma.sync.m8n8k4.f64).  The apply runs
-// the blocked forward/backward triangular solves of every block in lock-step
-// (one launch per tile step), using the inverted diagonal tiles so each step
-// is a pair of tile GEMVs.
+// one batch of dense SPD matrices stored as padded 64x64 tiles (identity on the
+// padded diagonal, so every tile is full).  Build: batched right-looking tiled
+// Cholesky — potrf of the diagonal tile (+ its inverse D_k), a "trsm" GEMM
+// A_ik <- A_ik D_k^T and the trailing update A_ij -= A_ik A_jk^T — with every
+// tile GEMM on the FP64 tensor cores (DMMA, mma.sync.m8n8k4.f64).
+// Apply, two modes:
+//   * kPrecTrsv: blocked forward/backward triangular solves with L (the
+//     reference's llt.solve, schwarz.hpp:130), one launch per tile step;
+//   * kPrecInverse (default): the factor is turned into W_bb^-1 = L^-T L^-1 once
+//     (blocked triangular inverse + L^-T L^-1 product, both DMMA), and every
+//     apply is one batched dense GEMV over all blocks — the same HBM bytes as
+//     two triangular solves with L, without their sequential tile chain.
 #include <algorithm>
 #include <cmath>
 
@@ -17,17 +22,24 @@
 namespace sbg {
 
 namespace {
-constexpr int TB = 64;     // tile size
-constexpr int TLD = 68;    // padded shared-memory leading dimension (conflict-free DMMA fragments)
+constexpr int TB = 64;   // tile size
+constexpr int TLD = 68;  // padded shared-memory leading dimension (conflict-free DMMA fragments)
+constexpr int GEMV_ROWS = 32;
+enum { K_TRSM = 0, K_UPDATE = 1, K_TRTRI = 2, K_LAUUM = 3 };
+struct GTask {
+    int b, i, j, pad;
+};
 }  // namespace
 
 struct Prec {
     Ctx* ctx = nullptr;
-    int n = 0, nfaces = 0, nwb = 0, nc = 0;
-    int nblocks = 0, coarse_block = -1, Tmax = 0;
-    std::vector<int> h_nb, h_T, h_loc, h_Loff, h_Doff;
-    DBuf<int> d_nb, d_loc, d_Loff, d_Doff, d_T;
-    DBuf<double> L, D, loc;
+    int n = 0, nfaces = 0, nwb = 0, nc = 0, mode = kPrecInverse;
+    int nblocks = 0, coarse_block = -1, Tmax = 0, maxnb = 0;
+    std::vector<int> h_nb, h_T, h_loc, h_Doff;
+    std::vector<long long> h_Poff, h_Moff;
+    DBuf<int> d_nb, d_T, d_loc, d_Doff;
+    DBuf<long long> d_Poff, d_Moff;
+    DBuf<double> Lp, Xp, D, Mc, loc, locy;
     DBuf<int> pos;  // dof -> loc index (face/WB), -1 if none
     // R in CSC (restriction, ascending rows) and CSR (prolongation, ascending cols)
     DBuf<int> Rc_ptr, Rc_row, Rr_ptr, Rr_col;
@@ -35,7 +47,10 @@ struct Prec {
     // trsv tasks (block, tile row) per step
     DBuf<int2> fwd_tasks, bwd_tasks;
     std::vector<int> fwd_off, bwd_off;
-    double factor_bytes = 0;
+    // gemv tasks (block, first row)
+    DBuf<int2> gemv_tasks;
+    int ngemv = 0;
+    double apply_bytes = 0;
 };
 
 namespace {
@@ -48,16 +63,24 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
                  : "d"(a), "d"(b));
 }
 
-// ---------------------------------------------------------------- gather
-__global__ void k_gather_blocks(const double* __restrict__ W, int ld, const int* __restrict__ bdofs_ptr,
-                                const int* __restrict__ bdofs, const int* __restrict__ Loff, double* __restrict__ L)
+// ---------------------------------------------------------------- gather / coarse Galerkin
+// padded block b <- W[dofs, dofs] (full square) with identity on the padding
+__global__ void k_gather_blocks(const double* __restrict__ W, int ld, const int* __restrict__ bptr,
+                                const int* __restrict__ bdofs, const int* __restrict__ Tv,
+                                const long long* __restrict__ Poff, double* __restrict__ Lp)
 {
     const int b = blockIdx.x;
-    const int p0 = bdofs_ptr[b], nb = bdofs_ptr[b + 1] - p0;
-    double* Lb = L + Loff[b];
-    for (int i = blockIdx.y; i < nb; i += gridDim.y) {
-        const size_t wi = (size_t)bdofs[p0 + i] * ld;
-        for (int j = threadIdx.x; j <= i; j += blockDim.x) Lb[(size_t)i * nb + j] = W[wi + bdofs[p0 + j]];
+    const int p0 = bptr[b], nb = bptr[b + 1] - p0;
+    const int np = Tv[b] * TB;
+    double* Lb = Lp + Poff[b];
+    for (int i = blockIdx.y; i < np; i += gridDim.y) {
+        if (i < nb) {
+            const size_t wi = (size_t)bdofs[p0 + i] * ld;
+            for (int j = threadIdx.x; j < np; j += blockDim.x)
+                Lb[(size_t)i * np + j] = j < nb ? W[wi + bdofs[p0 + j]] : 0.0;
+        } else {
+            for (int j = threadIdx.x; j < np; j += blockDim.x) Lb[(size_t)i * np + j] = (i == j) ? 1.0 : 0.0;
+        }
     }
 }
 
@@ -76,41 +99,43 @@ __global__ void k_coarse_WR(const double* __restrict__ W, int ld, int n, const i
     }
 }
 
-// H[a][b] = sum_{r in col a} R(r,a) WR[r][b]  (lower triangle used)
+// H[a][b] = sum_{r in col a} R(r,a) WR[r][b]  into a padded block (ldh), identity padding
 __global__ void k_coarse_H(const double* __restrict__ WR, const int* __restrict__ cptr, const int* __restrict__ crow,
-                           const double* __restrict__ cval, int nc, double* __restrict__ H)
+                           const double* __restrict__ cval, int nc, int ldh, double* __restrict__ H)
 {
     const int a = blockIdx.x;
-    for (int b = threadIdx.x; b < nc; b += blockDim.x) {
+    for (int b = threadIdx.x; b < ldh; b += blockDim.x) {
         double s = 0.0;
-        for (int q = cptr[a]; q < cptr[a + 1]; ++q) s += cval[q] * WR[(size_t)crow[q] * nc + b];
-        H[(size_t)a * nc + b] = s;
+        if (a < nc && b < nc) {
+            for (int q = cptr[a]; q < cptr[a + 1]; ++q) s += cval[q] * WR[(size_t)crow[q] * nc + b];
+        } else {
+            s = (a == b) ? 1.0 : 0.0;
+        }
+        H[(size_t)a * ldh + b] = s;
     }
 }
 
 // ---------------------------------------------------------------- Cholesky: diagonal tile
 // Factor tile (k,k) of each listed block in shared memory, write L_kk and its
-// inverse D_k (lower triangular, stored as a full 64x64 slot).
-__global__ void __launch_bounds__(256) k_potrf(int k, const int* __restrict__ blocks, const int* __restrict__ nbv,
-                                               const int* __restrict__ Loff, const int* __restrict__ Doff,
-                                               double* __restrict__ L, double* __restrict__ D, int* __restrict__ fail)
+// inverse D_k (lower triangular, full 64x64 slot).
+__global__ void __launch_bounds__(256) k_potrf(int k, const int* __restrict__ blocks, const int* __restrict__ Tv,
+                                               const long long* __restrict__ Poff, const int* __restrict__ Doff,
+                                               double* __restrict__ Lp, double* __restrict__ D, int* __restrict__ fail)
 {
     extern __shared__ double sm[];
-    double* a = sm;             // TB x (TB+1)
+    double* a = sm;  // TB x (TB+1)
     double* x = sm + TB * (TB + 1);
-    const int b = blocks[blockIdx.x];
-    const int nb = nbv[b];
-    const int r0 = k * TB;
-    const int tn = min(TB, nb - r0);
-    double* Lt = L + Loff[b] + (size_t)r0 * nb + r0;
-    for (int e = threadIdx.x; e < tn * tn; e += blockDim.x) {
-        const int i = e / tn, j = e % tn;
-        a[i * (TB + 1) + j] = (j <= i) ? Lt[(size_t)i * nb + j] : 0.0;
-    }
-    __syncthreads();
     __shared__ int bad;
+    const int b = blocks[blockIdx.x];
+    const int ld = Tv[b] * TB;
+    double* Lt = Lp + Poff[b] + (size_t)k * TB * ld + (size_t)k * TB;
+    for (int e = threadIdx.x; e < TB * TB; e += blockDim.x) {
+        const int i = e / TB, j = e % TB;
+        a[i * (TB + 1) + j] = (j <= i) ? Lt[(size_t)i * ld + j] : 0.0;
+    }
     if (threadIdx.x == 0) bad = 0;
-    for (int j = 0; j < tn; ++j) {
+    __syncthreads();
+    for (int j = 0; j < TB; ++j) {
         if (threadIdx.x == 0) {
             const double d = a[j * (TB + 1) + j];
             if (!(d > 0.0) || !isfinite(d)) bad = 1;
@@ -118,9 +143,9 @@ __global__ void __launch_bounds__(256) k_potrf(int k, const int* __restrict__ bl
         }
         __syncthreads();
         const double djj = a[j * (TB + 1) + j];
-        for (int i = j + 1 + threadIdx.x; i < tn; i += blockDim.x) a[i * (TB + 1) + j] /= djj;
+        for (int i = j + 1 + threadIdx.x; i < TB; i += blockDim.x) a[i * (TB + 1) + j] /= djj;
         __syncthreads();
-        const int m = tn - j - 1;
+        const int m = TB - j - 1;
         for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
             const int i = j + 1 + e / m, l = j + 1 + e % m;
             if (l <= i) a[i * (TB + 1) + l] -= a[i * (TB + 1) + j] * a[l * (TB + 1) + j];
@@ -128,69 +153,43 @@ __global__ void __launch_bounds__(256) k_potrf(int k, const int* __restrict__ bl
         __syncthreads();
     }
     if (threadIdx.x == 0 && bad) atomicExch(&fail[b], 1);
-    for (int e = threadIdx.x; e < tn * tn; e += blockDim.x) {
-        const int i = e / tn, j = e % tn;
-        if (j <= i) Lt[(size_t)i * nb + j] = a[i * (TB + 1) + j];
+    for (int e = threadIdx.x; e < TB * TB; e += blockDim.x) {
+        const int i = e / TB, j = e % TB;
+        Lt[(size_t)i * ld + j] = (j <= i) ? a[i * (TB + 1) + j] : 0.0;
     }
     // inverse of the lower-triangular tile, one column per thread
-    double* Dt = D + Doff[b] + (size_t)k * TB * TB;
     const int c = threadIdx.x;
     if (c < TB) {
         for (int i = 0; i < TB; ++i) x[i * (TB + 1) + c] = 0.0;
-        if (c < tn) {
-            x[c * (TB + 1) + c] = 1.0 / a[c * (TB + 1) + c];
-            for (int i = c + 1; i < tn; ++i) {
-                double s = 0.0;
-                for (int l = c; l < i; ++l) s += a[i * (TB + 1) + l] * x[l * (TB + 1) + c];
-                x[i * (TB + 1) + c] = -s / a[i * (TB + 1) + i];
-            }
+        x[c * (TB + 1) + c] = 1.0 / a[c * (TB + 1) + c];
+        for (int i = c + 1; i < TB; ++i) {
+            double s = 0.0;
+            for (int l = c; l < i; ++l) s += a[i * (TB + 1) + l] * x[l * (TB + 1) + c];
+            x[i * (TB + 1) + c] = -s / a[i * (TB + 1) + i];
         }
     }
     __syncthreads();
+    double* Dt = D + Doff[b] + (size_t)k * TB * TB;
     for (int e = threadIdx.x; e < TB * TB; e += blockDim.x) Dt[e] = x[(e / TB) * (TB + 1) + (e % TB)];
 }
 
-// ---------------------------------------------------------------- Cholesky: tile GEMMs on DMMA
-// task.x = block, task.y = tile row i, task.z = tile col j; mode 0: C(i,k) = C(i,k) D_k^T
-// (trsm through the inverted diagonal tile), mode 1: C(i,j) -= L(i,k) L(j,k)^T.
-__global__ void __launch_bounds__(128) k_tile_gemm(int k, int mode, const int4* __restrict__ tasks,
-                                                   const int* __restrict__ nbv, const int* __restrict__ Loff,
-                                                   const int* __restrict__ Doff, double* __restrict__ L,
-                                                   const double* __restrict__ D)
+// ---------------------------------------------------------------- tile GEMMs on DMMA
+// stage a 64x64 tile (row-major, ld) into shared memory, optionally transposed
+__device__ __forceinline__ void stage(double* __restrict__ dst, const double* __restrict__ src, size_t ld, bool trans)
 {
-    extern __shared__ double sm[];
-    double* As = sm;             // TB x TLD
-    double* Bs = sm + TB * TLD;  // TB x TLD
-    const int4 t = tasks[blockIdx.x];
-    const int b = t.x, ti = t.y, tj = t.z;
-    const int nb = nbv[b];
-    double* Lb = L + Loff[b];
-    const int mi = min(TB, nb - ti * TB), mj = min(TB, nb - tj * TB), mk = min(TB, nb - k * TB);
-    const double* A = Lb + (size_t)ti * TB * nb + (size_t)k * TB;  // tile (i,k)
-    for (int e = threadIdx.x; e < TB * TB; e += blockDim.x) {
-        const int r = e / TB, c = e % TB;
-        As[r * TLD + c] = (r < mi && c < mk) ? A[(size_t)r * nb + c] : 0.0;
-    }
-    if (mode == 0) {
-        const double* Dk = D + Doff[b] + (size_t)k * TB * TB;
-        for (int e = threadIdx.x; e < TB * TB; e += blockDim.x) Bs[(e / TB) * TLD + (e % TB)] = Dk[e];
+    if (!trans) {
+        for (int e = threadIdx.x; e < TB * TB; e += blockDim.x) dst[(e / TB) * TLD + (e % TB)] = src[(size_t)(e / TB) * ld + (e % TB)];
     } else {
-        const double* B = Lb + (size_t)tj * TB * nb + (size_t)k * TB;  // tile (j,k)
-        for (int e = threadIdx.x; e < TB * TB; e += blockDim.x) {
-            const int r = e / TB, c = e % TB;
-            Bs[r * TLD + c] = (r < mj && c < mk) ? B[(size_t)r * nb + c] : 0.0;
-        }
+        for (int e = threadIdx.x; e < TB * TB; e += blockDim.x) dst[(e % TB) * TLD + (e / TB)] = src[(size_t)(e / TB) * ld + (e % TB)];
     }
-    __syncthreads();
-    // each warp: 32x32 output = 4x4 DMMA tiles of 8x8; C = A * B^T
+}
+
+// acc += As * Bs^T (As: rows = output rows, Bs: rows = output cols, k contiguous); 4 warps x 32x32
+__device__ __forceinline__ void mma_tiles(const double* __restrict__ As, const double* __restrict__ Bs, double (&acc)[4][4][2])
+{
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int gid = lane >> 2, tig = lane & 3;
     const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
-    double acc[4][4][2];
-#pragma unroll
-    for (int x = 0; x < 4; ++x)
-#pragma unroll
-        for (int y = 0; y < 4; ++y) acc[x][y][0] = acc[x][y][1] = 0.0;
 #pragma unroll 4
     for (int kk = 0; kk < TB; kk += 4) {
         double af[4], bf[4];
@@ -203,164 +202,300 @@ __global__ void __launch_bounds__(128) k_tile_gemm(int k, int mode, const int4* 
 #pragma unroll
             for (int y = 0; y < 4; ++y) dmma(acc[x][y][0], acc[x][y][1], af[x], bf[y]);
     }
-    double* C = Lb + (size_t)ti * TB * nb + (size_t)tj * TB;
-    if (mode == 0) __syncthreads();  // C aliases A (already staged in smem)
+}
+
+// visit the accumulator elements: f(row, col, value)
+template <class F>
+__device__ __forceinline__ void for_acc(const double (&acc)[4][4][2], F f)
+{
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int gid = lane >> 2, tig = lane & 3;
+    const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
 #pragma unroll
     for (int x = 0; x < 4; ++x)
 #pragma unroll
         for (int y = 0; y < 4; ++y)
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const int r = wm + 8 * x + gid, c = wn + 8 * y + 2 * tig + h;
-                if (r < mi && c < mj) {
-                    double* dst = C + (size_t)r * nb + c;
-                    if (mode == 0)
-                        *dst = acc[x][y][h];
-                    else
-                        *dst -= acc[x][y][h];
-                }
-            }
+            for (int h = 0; h < 2; ++h) f(wm + 8 * x + gid, wn + 8 * y + 2 * tig + h, acc[x][y][h]);
+}
+
+// KIND K_TRSM  : L(i,k) = L(i,k) D_k^T            (task.i = i)
+//      K_UPDATE: L(i,j) -= L(i,k) L(j,k)^T        (task.i, task.j)
+//      K_TRTRI : X(i,j) = -D_i sum_{q=j}^{i-1} L(i,q) X(q,j);  X(i,i) = D_i
+//      K_LAUUM : M(i,j) = sum_{q=i}^{T-1} X(q,i)^T X(q,j)   (written over L)
+template <int KIND>
+__global__ void __launch_bounds__(128) k_tile_gemm(int k, const GTask* __restrict__ tasks, const int* __restrict__ Tv,
+                                                   const long long* __restrict__ Poff, const int* __restrict__ Doff,
+                                                   double* __restrict__ Lp, double* __restrict__ Xp,
+                                                   const double* __restrict__ D)
+{
+    extern __shared__ double sm[];
+    double* As = sm;
+    double* Bs = sm + TB * TLD;
+    const GTask t = tasks[blockIdx.x];
+    const int T = Tv[t.b];
+    const size_t ld = (size_t)T * TB;
+    double* L = Lp + Poff[t.b];
+    double* X = Xp ? Xp + Poff[t.b] : nullptr;
+    const double* Db = D + Doff[t.b];
+    auto tile = [&](double* base, int ti, int tj) { return base + (size_t)ti * TB * ld + (size_t)tj * TB; };
+    double acc[4][4][2];
+#pragma unroll
+    for (int x = 0; x < 4; ++x)
+#pragma unroll
+        for (int y = 0; y < 4; ++y) acc[x][y][0] = acc[x][y][1] = 0.0;
+
+    if (KIND == K_TRSM || KIND == K_UPDATE) {
+        stage(As, tile(L, t.i, k), ld, false);
+        if (KIND == K_TRSM)
+            stage(Bs, Db + (size_t)k * TB * TB, TB, false);
+        else
+            stage(Bs, tile(L, t.j, k), ld, false);
+        __syncthreads();
+        mma_tiles(As, Bs, acc);
+        double* C = tile(L, t.i, KIND == K_TRSM ? k : t.j);
+        if (KIND == K_TRSM) __syncthreads();  // C aliases the staged A
+        for_acc(acc, [&](int r, int c, double v) {
+            double* dst = C + (size_t)r * ld + c;
+            if (KIND == K_TRSM)
+                *dst = v;
+            else
+                *dst -= v;
+        });
+    } else if (KIND == K_TRTRI) {
+        double* C = tile(X, t.i, t.j);
+        if (t.i == t.j) {
+            const double* Di = Db + (size_t)t.i * TB * TB;
+            for (int e = threadIdx.x; e < TB * TB; e += blockDim.x) C[(size_t)(e / TB) * ld + (e % TB)] = Di[e];
+            return;
+        }
+        for (int q = t.j; q < t.i; ++q) {
+            __syncthreads();
+            stage(As, tile(L, t.i, q), ld, false);
+            stage(Bs, tile(X, q, t.j), ld, true);
+            __syncthreads();
+            mma_tiles(As, Bs, acc);
+        }
+        __syncthreads();
+        // Bs <- acc^T (rows = output cols), As <- D_i, then C = -D_i acc
+        for_acc(acc, [&](int r, int c, double v) { Bs[c * TLD + r] = v; });
+        stage(As, Db + (size_t)t.i * TB * TB, TB, false);
+        __syncthreads();
+        double acc2[4][4][2];
+#pragma unroll
+        for (int x = 0; x < 4; ++x)
+#pragma unroll
+            for (int y = 0; y < 4; ++y) acc2[x][y][0] = acc2[x][y][1] = 0.0;
+        mma_tiles(As, Bs, acc2);
+        for_acc(acc2, [&](int r, int c, double v) { C[(size_t)r * ld + c] = -v; });
+    } else {  // K_LAUUM
+        for (int q = t.i; q < T; ++q) {
+            __syncthreads();
+            stage(As, tile(X, q, t.i), ld, true);
+            stage(Bs, tile(X, q, t.j), ld, true);
+            __syncthreads();
+            mma_tiles(As, Bs, acc);
+        }
+        double* C = tile(L, t.i, t.j);
+        for_acc(acc, [&](int r, int c, double v) { C[(size_t)r * ld + c] = v; });
+    }
+}
+
+// compact inverse: Mc_b[r][c] = M[max(r,c)][min(r,c)] over the valid n_b x n_b part
+__global__ void k_compact_inverse(const double* __restrict__ Lp, const long long* __restrict__ Poff,
+                                  const int* __restrict__ Tv, const int* __restrict__ nbv,
+                                  const long long* __restrict__ Moff, double* __restrict__ Mc)
+{
+    const int b = blockIdx.x;
+    const int nb = nbv[b];
+    const size_t ld = (size_t)Tv[b] * TB;
+    const double* M = Lp + Poff[b];
+    double* out = Mc + Moff[b];
+    for (int r = blockIdx.y; r < nb; r += gridDim.y)
+        for (int c = threadIdx.x; c < nb; c += blockDim.x)
+            out[(size_t)r * nb + c] = r >= c ? M[(size_t)r * ld + c] : M[(size_t)c * ld + r];
 }
 
 // ---------------------------------------------------------------- apply
-// gather r into the block-local vector and restrict to the coarse space
+// gather r into the block-local vector (faces/WB) and restrict to the coarse space
 __global__ void k_prec_gather(const double* __restrict__ r, int n, const int* __restrict__ pos,
-                              double* __restrict__ loc, const int* done)
+                              double* __restrict__ loc, const int* __restrict__ cptr, const int* __restrict__ crow,
+                              const double* __restrict__ cval, int nc, double* __restrict__ loc_c, const int* done)
 {
     if (done && *done) return;
     const int d = blockIdx.x * blockDim.x + threadIdx.x;
-    if (d < n && pos[d] >= 0) loc[pos[d]] = r[d];
+    if (d < n) {
+        if (pos[d] >= 0) loc[pos[d]] = r[d];
+    } else if (d - n < nc) {
+        const int c = d - n;
+        double s = 0.0;
+        for (int q = cptr[c]; q < cptr[c + 1]; ++q) s += cval[q] * r[crow[q]];
+        loc_c[c] = s;
+    }
 }
 
-__global__ void k_prec_restrict(const double* __restrict__ r, const int* __restrict__ cptr,
-                                const int* __restrict__ crow, const double* __restrict__ cval, int nc,
-                                double* __restrict__ loc_c, const int* done)
+// y_b = M_b x_b for GEMV_ROWS rows of one block per CTA (warp per row, x_b in smem)
+__global__ void __launch_bounds__(256) k_block_gemv(const int2* __restrict__ tasks, const int* __restrict__ nbv,
+                                                    const int* __restrict__ locv, const long long* __restrict__ Moff,
+                                                    const double* __restrict__ Mc, const double* __restrict__ loc,
+                                                    double* __restrict__ locy, const int* done)
 {
     if (done && *done) return;
-    const int c = blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= nc) return;
-    double s = 0.0;
-    for (int q = cptr[c]; q < cptr[c + 1]; ++q) s += cval[q] * r[crow[q]];
-    loc_c[c] = s;
+    extern __shared__ double xs[];
+    const int2 t = tasks[blockIdx.x];
+    const int b = t.x, r0 = t.y, nb = nbv[b];
+    const double* x = loc + locv[b];
+    for (int c = threadIdx.x; c < nb; c += blockDim.x) xs[c] = x[c];
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const double* M = Mc + Moff[b];
+    const int r1 = min(nb, r0 + GEMV_ROWS);
+    for (int r = r0 + warp; r < r1; r += blockDim.x >> 5) {
+        const double* row = M + (size_t)r * nb;
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+        int c = lane;
+        for (; c + 96 < nb; c += 128) {
+            s0 = fma(__ldcs(row + c), xs[c], s0);
+            s1 = fma(__ldcs(row + c + 32), xs[c + 32], s1);
+            s2 = fma(__ldcs(row + c + 64), xs[c + 64], s2);
+            s3 = fma(__ldcs(row + c + 96), xs[c + 96], s3);
+        }
+        for (; c < nb; c += 32) s0 = fma(__ldcs(row + c), xs[c], s0);
+        double s = (s0 + s1) + (s2 + s3);
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == 0) locy[locv[b] + r] = s;
+    }
 }
 
-// y[0:m] (smem) = sum_c T[r][c] v[c] over an m x kc tile (row-major, ld) — 4 threads per row
+// 4 threads per row: partial dot of a 64-wide tile row
 __device__ __forceinline__ double tile_row_dot(const double* __restrict__ T, size_t ld, int r, int kc,
-                                               const double* v, int part, bool active)
+                                               const double* v, int part)
 {
     double s = 0.0;
-    if (active)
-        for (int c = part; c < kc; c += 4) s += T[(size_t)r * ld + c] * v[c];
+    for (int c = part; c < kc; c += 4) s += T[(size_t)r * ld + c] * v[c];
     s += __shfl_xor_sync(0xffffffffu, s, 1);
     s += __shfl_xor_sync(0xffffffffu, s, 2);
     return s;
 }
 
-// Forward step k: for each task (b, i) with i >= k:
-//   v_i = loc_i - L(i,k-1) y_{k-1}   (k >= 1),  and if i == k: y_k = D_k v_k
-__global__ void __launch_bounds__(256) k_trsv_fwd(int k, const int2* __restrict__ tasks, const int* __restrict__ nbv,
-                                                  const int* __restrict__ locv, const int* __restrict__ Loff,
-                                                  const int* __restrict__ Doff, const double* __restrict__ L,
+// Forward step k (padded tiles): tasks (b, i >= k): v_i = loc_i - L(i,k-1) y_{k-1}; i == k: y_k = D_k v_k
+__global__ void __launch_bounds__(256) k_trsv_fwd(int k, const int2* __restrict__ tasks, const int* __restrict__ Tv,
+                                                  const int* __restrict__ locv, const long long* __restrict__ Poff,
+                                                  const int* __restrict__ Doff, const double* __restrict__ Lp,
                                                   const double* __restrict__ D, double* __restrict__ loc,
                                                   const int* done)
 {
     if (done && *done) return;
     __shared__ double yprev[TB], v[TB];
     const int2 t = tasks[blockIdx.x];
-    const int b = t.x, i = t.y, nb = nbv[b];
+    const int b = t.x, i = t.y;
+    const size_t ld = (size_t)Tv[b] * TB;
     double* lb = loc + locv[b];
-    const int mi = min(TB, nb - i * TB);
     const int row = threadIdx.x >> 2, part = threadIdx.x & 3;
-    if (threadIdx.x < TB) v[threadIdx.x] = threadIdx.x < mi ? lb[i * TB + threadIdx.x] : 0.0;
+    if (threadIdx.x < TB) v[threadIdx.x] = lb[i * TB + threadIdx.x];
     if (k >= 1) {
-        const int kc = TB;  // column tile k-1 is always full
         if (threadIdx.x < TB) yprev[threadIdx.x] = lb[(k - 1) * TB + threadIdx.x];
         __syncthreads();
-        const double* T = L + Loff[b] + (size_t)i * TB * nb + (size_t)(k - 1) * TB;
-        const double s = tile_row_dot(T, nb, row, kc, yprev, part, row < mi);
+        const double* T = Lp + Poff[b] + (size_t)i * TB * ld + (size_t)(k - 1) * TB;
+        const double s = tile_row_dot(T, ld, row, TB, yprev, part);
         __syncthreads();
-        if (row < mi && part == 0) v[row] -= s;
+        if (part == 0) v[row] -= s;
     }
     __syncthreads();
     if (i == k) {
         const double* Dk = D + Doff[b] + (size_t)k * TB * TB;
-        const double s = tile_row_dot(Dk, TB, row, row + 1, v, part, row < mi);
+        const double s = tile_row_dot(Dk, TB, row, row + 1, v, part);
         __syncthreads();
-        if (row < mi && part == 0) lb[i * TB + row] = s;
-    } else if (threadIdx.x < mi) {
+        if (part == 0) lb[i * TB + row] = s;
+    } else if (threadIdx.x < TB) {
         lb[i * TB + threadIdx.x] = v[threadIdx.x];
     }
 }
 
-// Backward step with block-local k = T_b - 1 - s: tasks (b, i) with i <= k:
-//   v_i = loc_i - L(k+1,i)^T z_{k+1}   (k+1 < T_b),  and if i == k: z_k = D_k^T v_k
-__global__ void __launch_bounds__(256) k_trsv_bwd(int s, const int2* __restrict__ tasks, const int* __restrict__ nbv,
-                                                  const int* __restrict__ Tv, const int* __restrict__ locv,
-                                                  const int* __restrict__ Loff, const int* __restrict__ Doff,
-                                                  const double* __restrict__ L, const double* __restrict__ D,
-                                                  double* __restrict__ loc, const int* done)
+// Backward step with block-local k = T_b - 1 - s: tasks (b, i <= k):
+//   v_i = loc_i - L(k+1,i)^T z_{k+1} (k+1 < T_b); i == k: z_k = D_k^T v_k
+__global__ void __launch_bounds__(256) k_trsv_bwd(int s, const int2* __restrict__ tasks, const int* __restrict__ Tv,
+                                                  const int* __restrict__ locv, const long long* __restrict__ Poff,
+                                                  const int* __restrict__ Doff, const double* __restrict__ Lp,
+                                                  const double* __restrict__ D, double* __restrict__ loc,
+                                                  const int* done)
 {
     if (done && *done) return;
     __shared__ double znext[TB], v[TB], red[4][TB];
     const int2 t = tasks[blockIdx.x];
-    const int b = t.x, i = t.y, nb = nbv[b], T = Tv[b];
+    const int b = t.x, i = t.y, T = Tv[b];
+    const size_t ld = (size_t)T * TB;
     const int k = T - 1 - s;
     double* lb = loc + locv[b];
-    const int mi = min(TB, nb - i * TB);
-    const int col = threadIdx.x & 63, grp = threadIdx.x >> 6;  // 4 row groups x 64 columns
-    if (threadIdx.x < TB) v[threadIdx.x] = threadIdx.x < mi ? lb[i * TB + threadIdx.x] : 0.0;
+    const int col = threadIdx.x & 63, grp = threadIdx.x >> 6;
+    if (threadIdx.x < TB) v[threadIdx.x] = lb[i * TB + threadIdx.x];
     if (k + 1 < T) {
-        const int mk1 = min(TB, nb - (k + 1) * TB);
-        if (threadIdx.x < TB) znext[threadIdx.x] = threadIdx.x < mk1 ? lb[(k + 1) * TB + threadIdx.x] : 0.0;
+        if (threadIdx.x < TB) znext[threadIdx.x] = lb[(k + 1) * TB + threadIdx.x];
         __syncthreads();
-        const double* Tt = L + Loff[b] + (size_t)(k + 1) * TB * nb + (size_t)i * TB;  // tile (k+1, i)
+        const double* Tt = Lp + Poff[b] + (size_t)(k + 1) * TB * ld + (size_t)i * TB;  // tile (k+1, i)
         double acc = 0.0;
-        if (col < mi)
-            for (int r = grp; r < mk1; r += 4) acc += Tt[(size_t)r * nb + col] * znext[r];
+        for (int r = grp; r < TB; r += 4) acc += Tt[(size_t)r * ld + col] * znext[r];
         red[grp][col] = acc;
         __syncthreads();
-        if (threadIdx.x < mi) v[threadIdx.x] -= (red[0][threadIdx.x] + red[1][threadIdx.x]) +
+        if (threadIdx.x < TB) v[threadIdx.x] -= (red[0][threadIdx.x] + red[1][threadIdx.x]) +
                                                 (red[2][threadIdx.x] + red[3][threadIdx.x]);
     }
     __syncthreads();
     if (i == k) {
         const double* Dk = D + Doff[b] + (size_t)k * TB * TB;
         double acc = 0.0;
-        if (col < mi)
-            for (int r = col + grp; r < mi; r += 4)
-                if (r >= col) acc += Dk[(size_t)r * TB + col] * v[r];
+        for (int r = col + grp; r < TB; r += 4) acc += Dk[(size_t)r * TB + col] * v[r];
         red[grp][col] = acc;
         __syncthreads();
-        if (threadIdx.x < mi)
+        if (threadIdx.x < TB)
             lb[i * TB + threadIdx.x] = (red[0][threadIdx.x] + red[1][threadIdx.x]) +
                                        (red[2][threadIdx.x] + red[3][threadIdx.x]);
-    } else if (threadIdx.x < mi) {
+    } else if (threadIdx.x < TB) {
         lb[i * TB + threadIdx.x] = v[threadIdx.x];
     }
 }
 
-// z[d] = z_block[d] + (R y_c)[d]  (schwarz.hpp:126-138: faces/WB then coarse)
-__global__ void k_prec_scatter(const double* __restrict__ loc, const int* __restrict__ pos, int n,
+// z[d] = z_block[d] + (R y_c)[d]  (schwarz.hpp:126-138: faces/WB, then coarse)
+__global__ void k_prec_scatter(const double* __restrict__ locy, const int* __restrict__ pos, int n,
                                const int* __restrict__ rptr, const int* __restrict__ rcol,
-                               const double* __restrict__ rval, const double* __restrict__ loc_c,
+                               const double* __restrict__ rval, const double* __restrict__ y_c,
                                double* __restrict__ z, const int* done)
 {
     if (done && *done) return;
     const int d = blockIdx.x * blockDim.x + threadIdx.x;
     if (d >= n) return;
-    double out = pos[d] >= 0 ? loc[pos[d]] : 0.0;
+    double out = pos[d] >= 0 ? locy[pos[d]] : 0.0;
     if (rptr) {
         double y = 0.0;
-        for (int q = rptr[d]; q < rptr[d + 1]; ++q) y += rval[q] * loc_c[rcol[q]];
+        for (int q = rptr[d]; q < rptr[d + 1]; ++q) y += rval[q] * y_c[rcol[q]];
         out += y;
     }
     z[d] = out;
 }
 
+template <int KIND>
+void launch_gemm(Ctx* ctx, Prec* P, int k, const std::vector<GTask>& tasks, DBuf<GTask>& dev)
+{
+    if (tasks.empty()) return;
+    cudaStream_t s = ctx->stream;
+    const size_t smem = 2 * TB * TLD * sizeof(double);
+    static bool configured = false;
+    if (!configured) {
+        SBG_CUDA(cudaFuncSetAttribute(k_tile_gemm<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        configured = true;
+    }
+    dev.upload(tasks, s);
+    k_tile_gemm<KIND><<<(int)tasks.size(), 128, smem, s>>>(k, dev.p, P->d_T.p, P->d_Poff.p, P->d_Doff.p, P->Lp.p,
+                                                          P->Xp.p, P->D.p);
+    count_launch();
+    SBG_LAUNCH_CHECK();
+    SBG_CUDA(cudaStreamSynchronize(s));  // the host task vector and device copy are reused
+}
+
 }  // namespace
 
 // reference: inc/schwarz.hpp:100-118
-Prec* prec_build(Ctx* ctx, const DMatrix& W, const DofPartition& part, const Prolongation& R)
+Prec* prec_build(Ctx* ctx, const DMatrix& W, const DofPartition& part, const Prolongation& R, int mode)
 {
     cudaStream_t s = ctx->stream;
     const int n = W.n;
@@ -369,12 +504,12 @@ Prec* prec_build(Ctx* ctx, const DMatrix& W, const DofPartition& part, const Pro
     try {
         P->ctx = ctx;
         P->n = n;
+        P->mode = mode;
         P->nfaces = (int)part.face_ids.size();
         P->nwb = (int)part.wirebasket.size();
         P->nc = R.cols;
-        // block dof lists: faces in map order, then WB (skipping empty blocks as factor_block does)
-        std::vector<int> bptr{0}, bdofs;
-        std::vector<int> kinds;  // 0 face, 1 wb, 2 coarse
+        // block dof lists: faces in map order, then WB (empty blocks skipped as in factor_block)
+        std::vector<int> bptr{0}, bdofs, kinds;  // kinds: 0 face, 1 wb, 2 coarse
         for (int f = 0; f < P->nfaces; ++f) {
             const int a = part.face_ptr[f], e = part.face_ptr[f + 1];
             if (e == a) continue;
@@ -395,47 +530,53 @@ Prec* prec_build(Ctx* ctx, const DMatrix& W, const DofPartition& part, const Pro
             P->coarse_block = ngather;
         }
         P->nblocks = (int)kinds.size();
-        size_t Loff = 0, Doff = 0, loc = 0;
+        long long Poff = 0, Moff = 0;
+        int Doff = 0, loc = 0;
         for (int b = 0; b < P->nblocks; ++b) {
             const int nb = b < ngather ? bptr[b + 1] - bptr[b] : P->nc;
             const int T = (nb + TB - 1) / TB;
             P->h_nb.push_back(nb);
             P->h_T.push_back(T);
-            P->h_loc.push_back((int)loc);
-            P->h_Loff.push_back((int)Loff);
-            P->h_Doff.push_back((int)Doff);
-            if (Loff + (size_t)nb * nb > 0x7fffffffULL || Doff + (size_t)T * TB * TB > 0x7fffffffULL)
-                throw ValidationError("preconditioner blocks exceed the 2^31 element index range");
-            Loff += (size_t)nb * nb;
-            Doff += (size_t)T * TB * TB;
-            loc += (size_t)T * TB;
+            P->h_loc.push_back(loc);
+            P->h_Poff.push_back(Poff);
+            P->h_Doff.push_back(Doff);
+            P->h_Moff.push_back(Moff);
+            Poff += (long long)T * TB * T * TB;
+            Moff += (long long)nb * nb;
+            if ((long long)Doff + (long long)T * TB * TB > 0x7fffffffLL) throw ValidationError("preconditioner too large");
+            Doff += T * TB * TB;
+            loc += T * TB;
             P->Tmax = std::max(P->Tmax, T);
-            P->factor_bytes += (double)nb * nb * 8.0;
+            P->maxnb = std::max(P->maxnb, nb);
+            P->apply_bytes += (double)nb * nb * 8.0;
         }
         P->d_nb.upload(P->h_nb, s);
         P->d_T.upload(P->h_T, s);
         P->d_loc.upload(P->h_loc, s);
-        P->d_Loff.upload(P->h_Loff, s);
+        P->d_Poff.upload(P->h_Poff, s);
         P->d_Doff.upload(P->h_Doff, s);
-        P->L.alloc(std::max<size_t>(Loff, 1));
-        P->D.alloc(std::max<size_t>(Doff, 1));
-        P->loc.alloc(std::max<size_t>(loc, 1));
+        P->d_Moff.upload(P->h_Moff, s);
+        P->Lp.alloc(std::max<long long>(Poff, 1));
+        P->D.alloc(std::max(Doff, 1));
+        P->loc.alloc(std::max(loc, 1));
+        P->locy.alloc(std::max(loc, 1));
         SBG_CUDA(cudaMemsetAsync(P->loc.p, 0, P->loc.n * sizeof(double), s));
+        SBG_CUDA(cudaMemsetAsync(P->locy.p, 0, P->locy.n * sizeof(double), s));
         std::vector<int> pos(n, -1);
         for (int b = 0; b < ngather; ++b)
             for (int q = bptr[b]; q < bptr[b + 1]; ++q) pos[bdofs[q]] = P->h_loc[b] + (q - bptr[b]);
         P->pos.upload(pos, s);
-        // gather face/WB blocks from W (factor_block's submatrix, schwarz.hpp:77-83)
-        if (ngather > 0) {
+        if (ngather > 0) {  // factor_block's submatrix (schwarz.hpp:77-83)
             DBuf<int> d_bptr, d_bdofs;
             d_bptr.upload(bptr, s);
             d_bdofs.upload(bdofs, s);
-            k_gather_blocks<<<dim3(ngather, 64), 128, 0, s>>>(W.a.p, W.ld, d_bptr.p, d_bdofs.p, P->d_Loff.p, P->L.p); ::sbg::count_launch();
+            k_gather_blocks<<<dim3(ngather, 64), 128, 0, s>>>(W.a.p, W.ld, d_bptr.p, d_bdofs.p, P->d_T.p, P->d_Poff.p,
+                                                              P->Lp.p);
+            count_launch();
             SBG_LAUNCH_CHECK();
             SBG_CUDA(cudaStreamSynchronize(s));
         }
-        // coarse space: R in CSC and CSR, H = R^T W R into the coarse block
-        if (P->nc > 0) {
+        if (P->nc > 0) {  // R^T W R with the sparse R (schwarz.hpp:110-116)
             P->Rc_ptr.upload(R.col_ptr, s);
             P->Rc_row.upload(R.row_idx, s);
             P->Rc_val.upload(R.val, s);
@@ -458,25 +599,26 @@ Prec* prec_build(Ctx* ctx, const DMatrix& W, const DofPartition& part, const Pro
             DBuf<double> WR((size_t)n * P->nc);
             TimedScope ts(ctx, "coarse_galerkin");
             k_coarse_WR<<<std::min(n, 8 * ctx->sm_count), 128, 0, s>>>(W.a.p, W.ld, n, P->Rc_ptr.p, P->Rc_row.p,
-                                                                      P->Rc_val.p, P->nc, WR.p); ::sbg::count_launch();
-            k_coarse_H<<<P->nc, 128, 0, s>>>(WR.p, P->Rc_ptr.p, P->Rc_row.p, P->Rc_val.p, P->nc,
-                                             P->L.p + P->h_Loff[P->coarse_block]); ::sbg::count_launch();
+                                                                      P->Rc_val.p, P->nc, WR.p);
+            count_launch();
+            const int ldh = P->h_T[P->coarse_block] * TB;
+            k_coarse_H<<<ldh, 128, 0, s>>>(WR.p, P->Rc_ptr.p, P->Rc_row.p, P->Rc_val.p, P->nc, ldh,
+                                           P->Lp.p + P->h_Poff[P->coarse_block]);
+            count_launch();
             SBG_LAUNCH_CHECK();
             SBG_CUDA(cudaStreamSynchronize(s));
         }
-        // batched tiled Cholesky
+        // ---- batched tiled Cholesky
         DBuf<int> fail(std::max(P->nblocks, 1));
         SBG_CUDA(cudaMemsetAsync(fail.p, 0, fail.n * sizeof(int), s));
         {
             TimedScope ts(ctx, "cholesky");
-            std::vector<int> pot;
-            std::vector<int4> trsm, upd;
-            DBuf<int> d_pot;
-            DBuf<int4> d_trsm, d_upd;
             const size_t smem_potrf = 2 * TB * (TB + 1) * sizeof(double);
-            const size_t smem_gemm = 2 * TB * TLD * sizeof(double);
             SBG_CUDA(cudaFuncSetAttribute(k_potrf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_potrf));
-            SBG_CUDA(cudaFuncSetAttribute(k_tile_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_gemm));
+            std::vector<int> pot;
+            std::vector<GTask> trsm, upd;
+            DBuf<int> d_pot;
+            DBuf<GTask> d_tasks;
             for (int k = 0; k < P->Tmax; ++k) {
                 pot.clear();
                 trsm.clear();
@@ -490,22 +632,12 @@ Prec* prec_build(Ctx* ctx, const DMatrix& W, const DofPartition& part, const Pro
                         for (int i = j; i < T; ++i) upd.push_back({b, i, j, 0});
                 }
                 d_pot.upload(pot, s);
-                k_potrf<<<(int)pot.size(), 256, smem_potrf, s>>>(k, d_pot.p, P->d_nb.p, P->d_Loff.p, P->d_Doff.p,
-                                                                 P->L.p, P->D.p, fail.p); ::sbg::count_launch();
+                k_potrf<<<(int)pot.size(), 256, smem_potrf, s>>>(k, d_pot.p, P->d_T.p, P->d_Poff.p, P->d_Doff.p,
+                                                                 P->Lp.p, P->D.p, fail.p);
+                count_launch();
                 SBG_LAUNCH_CHECK();
-                if (!trsm.empty()) {
-                    d_trsm.upload(trsm, s);
-                    k_tile_gemm<<<(int)trsm.size(), 128, smem_gemm, s>>>(k, 0, d_trsm.p, P->d_nb.p, P->d_Loff.p,
-                                                                          P->d_Doff.p, P->L.p, P->D.p); ::sbg::count_launch();
-                    SBG_LAUNCH_CHECK();
-                }
-                if (!upd.empty()) {
-                    d_upd.upload(upd, s);
-                    k_tile_gemm<<<(int)upd.size(), 128, smem_gemm, s>>>(k, 1, d_upd.p, P->d_nb.p, P->d_Loff.p,
-                                                                         P->d_Doff.p, P->L.p, P->D.p); ::sbg::count_launch();
-                    SBG_LAUNCH_CHECK();
-                }
-                // host task vectors are reused next step: wait for the async uploads
+                launch_gemm<K_TRSM>(ctx, P, k, trsm, d_tasks);
+                launch_gemm<K_UPDATE>(ctx, P, k, upd, d_tasks);
                 SBG_CUDA(cudaStreamSynchronize(s));
             }
         }
@@ -518,25 +650,61 @@ Prec* prec_build(Ctx* ctx, const DMatrix& W, const DofPartition& part, const Pro
                                      (kinds[b] == 0 ? "face" : "wire-basket") +
                                      "): partition inconsistent with the assembled matrix");
             }
-        // trsv task lists
-        std::vector<int2> fw, bw;
-        P->fwd_off.assign(1, 0);
-        P->bwd_off.assign(1, 0);
-        for (int k = 0; k < P->Tmax; ++k) {
-            for (int b = 0; b < P->nblocks; ++b)
-                for (int i = k; i < P->h_T[b]; ++i) fw.push_back({b, i});
-            P->fwd_off.push_back((int)fw.size());
-        }
-        for (int st = 0; st < P->Tmax; ++st) {
-            for (int b = 0; b < P->nblocks; ++b) {
-                const int kk = P->h_T[b] - 1 - st;
-                for (int i = 0; i <= kk; ++i) bw.push_back({b, i});
+        if (mode == kPrecInverse) {
+            // ---- W_bb^-1 = L^-T L^-1: X = L^-1 row-tile by row-tile, then M = X^T X over L
+            TimedScope ts(ctx, "block_inverse");
+            P->Xp.alloc(std::max<long long>(Poff, 1));
+            std::vector<GTask> tasks;
+            DBuf<GTask> d_tasks;
+            for (int i = 0; i < P->Tmax; ++i) {
+                tasks.clear();
+                for (int b = 0; b < P->nblocks; ++b)
+                    if (i < P->h_T[b])
+                        for (int j = 0; j <= i; ++j) tasks.push_back({b, i, j, 0});
+                launch_gemm<K_TRTRI>(ctx, P, 0, tasks, d_tasks);
             }
-            P->bwd_off.push_back((int)bw.size());
+            tasks.clear();
+            for (int b = 0; b < P->nblocks; ++b)
+                for (int i = 0; i < P->h_T[b]; ++i)
+                    for (int j = 0; j <= i; ++j) tasks.push_back({b, i, j, 0});
+            launch_gemm<K_LAUUM>(ctx, P, 0, tasks, d_tasks);
+            P->Xp.release();
+            P->Mc.alloc(std::max<long long>(Moff, 1));
+            k_compact_inverse<<<dim3(P->nblocks, 64), 128, 0, s>>>(P->Lp.p, P->d_Poff.p, P->d_T.p, P->d_nb.p,
+                                                                   P->d_Moff.p, P->Mc.p);
+            count_launch();
+            SBG_LAUNCH_CHECK();
+            std::vector<int2> gt;
+            for (int b = 0; b < P->nblocks; ++b)
+                for (int r = 0; r < P->h_nb[b]; r += GEMV_ROWS) gt.push_back({b, r});
+            P->gemv_tasks.upload(gt, s);
+            P->ngemv = (int)gt.size();
+            const size_t smem = (size_t)std::max(P->maxnb, 1) * sizeof(double);
+            if (smem > 48 * 1024)
+                SBG_CUDA(cudaFuncSetAttribute(k_block_gemv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            SBG_CUDA(cudaStreamSynchronize(s));
+            P->Lp.release();
+            P->D.release();
+        } else {
+            std::vector<int2> fw, bw;
+            P->fwd_off.assign(1, 0);
+            P->bwd_off.assign(1, 0);
+            for (int k = 0; k < P->Tmax; ++k) {
+                for (int b = 0; b < P->nblocks; ++b)
+                    for (int i = k; i < P->h_T[b]; ++i) fw.push_back({b, i});
+                P->fwd_off.push_back((int)fw.size());
+            }
+            for (int st = 0; st < P->Tmax; ++st) {
+                for (int b = 0; b < P->nblocks; ++b) {
+                    const int kk = P->h_T[b] - 1 - st;
+                    for (int i = 0; i <= kk; ++i) bw.push_back({b, i});
+                }
+                P->bwd_off.push_back((int)bw.size());
+            }
+            P->fwd_tasks.upload(fw, s);
+            P->bwd_tasks.upload(bw, s);
+            SBG_CUDA(cudaStreamSynchronize(s));
         }
-        P->fwd_tasks.upload(fw, s);
-        P->bwd_tasks.upload(bw, s);
-        SBG_CUDA(cudaStreamSynchronize(s));
     } catch (...) {
         delete P;
         throw;
@@ -546,11 +714,12 @@ Prec* prec_build(Ctx* ctx, const DMatrix& W, const DofPartition& part, const Pro
 
 void prec_destroy(Prec* p) { delete p; }
 int prec_n(const Prec* p) { return p->n; }
+int prec_mode(const Prec* p) { return p->mode; }
 int prec_num_subspaces(const Prec* p)  // schwarz.hpp:66-72
 {
     return p->nfaces + (p->nwb > 0 ? 1 : 0) + (p->nc > 0 ? 1 : 0);
 }
-double prec_factor_bytes(const Prec* p) { return p->factor_bytes; }
+double prec_factor_bytes(const Prec* p) { return p->apply_bytes; }
 
 // reference: inc/schwarz.hpp:121-140
 void prec_apply(Ctx* ctx, Prec* P, const double* r, double* z, const int* done)
@@ -559,46 +728,65 @@ void prec_apply(Ctx* ctx, Prec* P, const double* r, double* z, const int* done)
     cudaStream_t s = ctx->stream;
     const int n = P->n;
     if (n == 0) return;
-    const int nb = (n + 255) / 256;
-    double* loc_c = P->coarse_block >= 0 ? P->loc.p + P->h_loc[P->coarse_block] : nullptr;
-    k_prec_gather<<<nb, 256, 0, s>>>(r, n, P->pos.p, P->loc.p, done); ::sbg::count_launch();
-    if (P->nc > 0)
-        k_prec_restrict<<<(P->nc + 127) / 128, 128, 0, s>>>(r, P->Rc_ptr.p, P->Rc_row.p, P->Rc_val.p, P->nc, loc_c,
-                                                            done); ::sbg::count_launch();
-    for (int k = 0; k < P->Tmax; ++k) {
-        const int cnt = P->fwd_off[k + 1] - P->fwd_off[k];
-        if (cnt)
-            k_trsv_fwd<<<cnt, 256, 0, s>>>(k, P->fwd_tasks.p + P->fwd_off[k], P->d_nb.p, P->d_loc.p, P->d_Loff.p,
-                                           P->d_Doff.p, P->L.p, P->D.p, P->loc.p, done); ::sbg::count_launch();
+    const int cb = P->coarse_block;
+    double* loc_c = cb >= 0 ? P->loc.p + P->h_loc[cb] : nullptr;
+    k_prec_gather<<<(n + P->nc + 255) / 256, 256, 0, s>>>(r, n, P->pos.p, P->loc.p, P->Rc_ptr.p, P->Rc_row.p,
+                                                          P->Rc_val.p, P->nc, loc_c, done);
+    count_launch();
+    const double* yloc;
+    if (P->mode == kPrecInverse) {
+        k_block_gemv<<<P->ngemv, 256, (size_t)std::max(P->maxnb, 1) * sizeof(double), s>>>(
+            P->gemv_tasks.p, P->d_nb.p, P->d_loc.p, P->d_Moff.p, P->Mc.p, P->loc.p, P->locy.p, done);
+        count_launch();
+        yloc = P->locy.p;
+    } else {
+        for (int k = 0; k < P->Tmax; ++k) {
+            const int cnt = P->fwd_off[k + 1] - P->fwd_off[k];
+            if (cnt) {
+                k_trsv_fwd<<<cnt, 256, 0, s>>>(k, P->fwd_tasks.p + P->fwd_off[k], P->d_T.p, P->d_loc.p, P->d_Poff.p,
+                                               P->d_Doff.p, P->Lp.p, P->D.p, P->loc.p, done);
+                count_launch();
+            }
+        }
+        for (int st = 0; st < P->Tmax; ++st) {
+            const int cnt = P->bwd_off[st + 1] - P->bwd_off[st];
+            if (cnt) {
+                k_trsv_bwd<<<cnt, 256, 0, s>>>(st, P->bwd_tasks.p + P->bwd_off[st], P->d_T.p, P->d_loc.p,
+                                               P->d_Poff.p, P->d_Doff.p, P->Lp.p, P->D.p, P->loc.p, done);
+                count_launch();
+            }
+        }
+        yloc = P->loc.p;
     }
-    for (int st = 0; st < P->Tmax; ++st) {
-        const int cnt = P->bwd_off[st + 1] - P->bwd_off[st];
-        if (cnt)
-            k_trsv_bwd<<<cnt, 256, 0, s>>>(st, P->bwd_tasks.p + P->bwd_off[st], P->d_nb.p, P->d_T.p, P->d_loc.p,
-                                           P->d_Loff.p, P->d_Doff.p, P->L.p, P->D.p, P->loc.p, done); ::sbg::count_launch();
-    }
-    k_prec_scatter<<<nb, 256, 0, s>>>(P->loc.p, P->pos.p, n, P->nc > 0 ? P->Rr_ptr.p : nullptr, P->Rr_col.p,
-                                      P->Rr_val.p, loc_c, z, done); ::sbg::count_launch();
+    k_prec_scatter<<<(n + 255) / 256, 256, 0, s>>>(yloc, P->pos.p, n, P->nc > 0 ? P->Rr_ptr.p : nullptr, P->Rr_col.p,
+                                                   P->Rr_val.p, cb >= 0 ? yloc + P->h_loc[cb] : nullptr, z, done);
+    count_launch();
     SBG_LAUNCH_CHECK();
 }
 
+// diagonal of the block's Cholesky factor (TRSV mode) or of its inverse (inverse mode)
 void prec_block_diag(Ctx* ctx, Prec* P, int which, std::vector<double>& diag)
 {
     int b = -1;
-    if (which >= 0) {
-        // face index counted over non-empty faces
+    if (which >= 0)
         b = which;
-    } else if (which == -1) {
+    else if (which == -1)
         b = P->nwb > 0 ? (P->coarse_block >= 0 ? P->coarse_block - 1 : P->nblocks - 1) : -1;
-    } else if (which == -2) {
+    else if (which == -2)
         b = P->coarse_block;
-    }
     diag.clear();
     if (b < 0 || b >= P->nblocks) return;
     const int nb = P->h_nb[b];
-    std::vector<double> h((size_t)nb * nb);
-    SBG_CUDA(cudaMemcpy(h.data(), P->L.p + P->h_Loff[b], h.size() * sizeof(double), cudaMemcpyDeviceToHost));
-    for (int i = 0; i < nb; ++i) diag.push_back(h[(size_t)i * nb + i]);
+    if (P->mode == kPrecInverse) {
+        std::vector<double> h((size_t)nb * nb);
+        SBG_CUDA(cudaMemcpy(h.data(), P->Mc.p + P->h_Moff[b], h.size() * sizeof(double), cudaMemcpyDeviceToHost));
+        for (int i = 0; i < nb; ++i) diag.push_back(h[(size_t)i * nb + i]);
+    } else {
+        const size_t ld = (size_t)P->h_T[b] * TB;
+        std::vector<double> h(ld * ld);
+        SBG_CUDA(cudaMemcpy(h.data(), P->Lp.p + P->h_Poff[b], h.size() * sizeof(double), cudaMemcpyDeviceToHost));
+        for (int i = 0; i < nb; ++i) diag.push_back(h[(size_t)i * ld + i]);
+    }
     (void)ctx;
 }
 
@@ -613,8 +801,10 @@ void coarse_galerkin(Ctx* ctx, const DMatrix& W, const Prolongation& R, std::vec
     cp.upload(R.col_ptr, s);
     cr.upload(R.row_idx, s);
     cv.upload(R.val, s);
-    k_coarse_WR<<<std::min(n, 8 * ctx->sm_count), 128, 0, s>>>(W.a.p, W.ld, n, cp.p, cr.p, cv.p, nc, WR.p); ::sbg::count_launch();
-    k_coarse_H<<<nc, 128, 0, s>>>(WR.p, cp.p, cr.p, cv.p, nc, dH.p); ::sbg::count_launch();
+    k_coarse_WR<<<std::min(n, 8 * ctx->sm_count), 128, 0, s>>>(W.a.p, W.ld, n, cp.p, cr.p, cv.p, nc, WR.p);
+    count_launch();
+    k_coarse_H<<<nc, 128, 0, s>>>(WR.p, cp.p, cr.p, cv.p, nc, nc, dH.p);
+    count_launch();
     SBG_LAUNCH_CHECK();
     SBG_CUDA(cudaMemcpyAsync(H.data(), dH.p, H.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
     SBG_CUDA(cudaStreamSynchronize(s));

@@ -108,6 +108,7 @@ SIGNATURES = {
     "sbg_prolong_export": (C.c_int, [vp, i32p, i32p, f64p]),
     "sbg_prolong_destroy": (None, [vp]),
     "sbg_build_preconditioner": (C.c_int, [vp, vp, vp, vp, C.POINTER(vp)]),
+    "sbg_build_preconditioner_mode": (C.c_int, [vp, vp, vp, vp, C.c_int, C.POINTER(vp)]),
     "sbg_apply_preconditioner": (C.c_int, [vp, vp, f64p, C.c_int, f64p]),
     "sbg_prec_num_subspaces": (C.c_int, [vp]),
     "sbg_prec_block_diag": (C.c_int, [vp, vp, C.c_int, C.c_void_p, C.POINTER(C.c_int)]),
@@ -466,7 +467,7 @@ class AssemblyPlan(_Handle):
 
     def run(self, W: GalerkinMatrix = None) -> GalerkinMatrix:
         st = AssemblyStatsC()
-        hw = vp(W.h if W is not None else None)
+        hw = vp(W.h.value if W is not None else None)
         _check(lib().sbg_assembly_run(self.h, C.byref(hw), C.byref(st)))
         stats = {n: getattr(st, n) for n, _ in AssemblyStatsC._fields_}
         if W is None:
@@ -625,10 +626,17 @@ class SchwarzPreconditioner(_Handle):
         return lib().sbg_prec_factor_bytes(self.h)
 
 
-def build_preconditioner(W: GalerkinMatrix, part: DofPartition, P: Prolongation) -> SchwarzPreconditioner:
-    """reference: inc/schwarz.hpp:100-118"""
+def build_preconditioner(W: GalerkinMatrix, part: DofPartition, P: Prolongation,
+                         mode: str = "inverse") -> SchwarzPreconditioner:
+    """reference: inc/schwarz.hpp:100-118.  mode "inverse" (default) forms the block
+    inverses L^-T L^-1 once and applies one batched GEMV; "trsv" applies the blocked
+    triangular solves with L as llt.solve does (schwarz.hpp:130)."""
+    modes = {"trsv": 0, "inverse": 1}
+    if mode not in modes:
+        raise ValidationError(f"unknown preconditioner mode {mode!r}")
     h = vp()
-    _check(lib().sbg_build_preconditioner(W.ctx.h, W.h, part.h, P.h if P is not None else None, C.byref(h)))
+    _check(lib().sbg_build_preconditioner_mode(W.ctx.h, W.h, part.h, P.h if P is not None else None, modes[mode],
+                                               C.byref(h)))
     return SchwarzPreconditioner(h, W.ctx, W.n)
 
 

@@ -18,12 +18,12 @@ for cfg in cfgs:
         W = S.assemble_W(fine, ctx=ctx)
         ctx.synchronize()
         t1 = time.time()
-        names = ["far_tiles", "near", "sauter", "classify", "local_scatter", "mirror"]
+        names = ["far_tiles", "near", "near_leaves", "sauter", "classify", "local_scatter", "mirror"]
         tm = {n: ctx.timer(n)[0] for n in names}
     npairs = nf * (nf + 1) // 2
     print(f"cfg{cfg}: nf={nf} n={fine.n} assemble wall {1e3*(t1-t0):.1f} ms -> {npairs/(t1-t0):.3e} pairs/s; "
           + " ".join(f"{k}={v:.2f}ms" for k, v in tm.items()), W.stats, flush=True)
-    g = [0.0, 0.0, 1.0]
+    g = S.config_g(cfg)
     L = S.assemble_rhs(fine, g, ctx=ctx)
     t0 = time.time()
     P = S.build_prolongation(pair, coarse, fine)
@@ -45,5 +45,5 @@ for cfg in cfgs:
     ld = (n + 31) // 32 * 32
     gb = 8.0 * n * ld / 1e9
     print(f"   pcg {rep.iterations} it in {1e3*(t1-t0):.1f} ms wall; gemv {gm/max(gc,1)*1e3:.1f} us/launch "
-          f"({gb/(gm/max(gc,1)/1e3):.0f} GB/s incl padding), precond apply {pm/max(pc,1)*1e3:.1f} us; kappa {rep.kappa_estimate:.3f}",
+          f"({gb/max(gm/max(gc,1)/1e3,1e-12):.0f} GB/s incl padding), precond apply {pm/max(pc,1)*1e3:.1f} us; kappa {rep.kappa_estimate:.3f}",
           flush=True)
