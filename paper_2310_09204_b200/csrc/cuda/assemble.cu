@@ -185,60 +185,131 @@ __device__ void tile_contract_flush(const double* __restrict__ It, int fb, int g
     }
 }
 
-__global__ void __launch_bounds__(FAR_THREADS, 1)
+// Far pairs with the distance expansion |x-y|^2 = |x|^2 + |y|^2 - 2 x.y in
+// tile-local coordinates (origin o = first vertex of the tile's first f-facet):
+// per evaluation DADD + 3 DFMA instead of 3 DADD + DMUL + 2 DFMA.  Far pairs
+// satisfy dist >= 2 diam, so (|x|^2+|y|^2)/|x-y|^2 stays O(10) inside a tile and
+// ~1 between distant tiles: the rounding stays at the 1e-15 level.
+struct XPts {
+    double m2x[8], m2y[8], m2z[8], x2[8];  // -2x, -2y, -2z, |x|^2 for 8 rule points
+};
+
+__device__ __forceinline__ void far_xpoints(const double* t, const double* o, int half, XPts& X)
+{
+    const double e1x = t[3] - t[0], e1y = t[4] - t[1], e1z = t[5] - t[2];
+    const double e2x = t[6] - t[0], e2y = t[7] - t[1], e2z = t[8] - t[2];
+    const double bx = t[0] - o[0], by = t[1] - o[1], bz = t[2] - o[2];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        const int i = 8 * half + q;
+        const double x = fma(c_far_v[i], e2x, fma(c_far_u[i], e1x, bx));
+        const double y = fma(c_far_v[i], e2y, fma(c_far_u[i], e1y, by));
+        const double z = fma(c_far_v[i], e2z, fma(c_far_u[i], e1z, bz));
+        X.m2x[q] = -2.0 * x;
+        X.m2y[q] = -2.0 * y;
+        X.m2z[q] = -2.0 * z;
+        X.x2[q] = fma(x, x, fma(y, y, z * z));
+    }
+}
+
+__device__ __forceinline__ double4 far_ypoint(const double* s, const double* o, int j)
+{
+    const double y0 = fma(c_far_v[j], s[6] - s[0], fma(c_far_u[j], s[3] - s[0], s[0] - o[0]));
+    const double y1 = fma(c_far_v[j], s[7] - s[1], fma(c_far_u[j], s[4] - s[1], s[1] - o[1]));
+    const double y2 = fma(c_far_v[j], s[8] - s[2], fma(c_far_u[j], s[5] - s[2], s[2] - o[2]));
+    return make_double4(y0, y1, y2, fma(y0, y0, fma(y1, y1, y2 * y2)));
+}
+
+// sum_j w_j sum_{q in half} w_{8 half + q} / |x_q - y_j|
+__device__ __forceinline__ double far_half_sum(const XPts& X, const double4* __restrict__ Y, int half)
+{
+    double acc = 0.0;
+#pragma unroll 1
+    for (int j = 0; j < NF; ++j) {
+        const double4 y = Y[j];
+        double in0 = 0.0, in1 = 0.0;
+#pragma unroll
+        for (int q = 0; q < 8; q += 2) {
+            const double ra = fma(X.m2x[q], y.x, fma(X.m2y[q], y.y, fma(X.m2z[q], y.z, X.x2[q] + y.w)));
+            const double rb = fma(X.m2x[q + 1], y.x, fma(X.m2y[q + 1], y.y, fma(X.m2z[q + 1], y.z, X.x2[q + 1] + y.w)));
+            in0 = fma(c_far_w[8 * half + q], rsqrt_fast(ra), in0);
+            in1 = fma(c_far_w[8 * half + q + 1], rsqrt_fast(rb), in1);
+        }
+        acc = fma(c_far_w[j], in0 + in1, acc);
+    }
+    return acc;
+}
+
+constexpr size_t FAR_SMEM = (size_t)BS * (BS + 1) * 8 + (size_t)BS * NF * 32 + (size_t)BS * 6 * 8 + (size_t)BS * 4 * 4;
+
+__global__ void __launch_bounds__(FAR_THREADS, 2)
     k_far_tiles(const TileInfo* __restrict__ tiles, GeoPtrs G, BlockPtrs B, double thr, double* __restrict__ W,
                 int ld, double inv_pi)
 {
-    __shared__ double It[BS * (BS + 1)];
-    __shared__ double gv[BS * 9];
-    __shared__ double gcr[BS * 5];  // cx, cy, cz, rad, diam
-    __shared__ double garea[BS];
-    __shared__ int gid[BS], gvid[BS * 3];
+    extern __shared__ __align__(16) unsigned char far_smem[];
+    double4* Ys = reinterpret_cast<double4*>(far_smem);                 // BS x 16 y-points (y, |y|^2)
+    double* It = reinterpret_cast<double*>(Ys + BS * NF);               // BS x (BS+1)
+    double* gcr = It + BS * (BS + 1);                                   // cx, cy, cz, rad, diam, area
+    int* gid = reinterpret_cast<int*>(gcr + BS * 6);
+    int* gvid = gid + BS;
+    __shared__ double o[3];
     const TileInfo T = tiles[blockIdx.x];
     const bool diag = T.fb == T.gb;
+    if (threadIdx.x < 3) o[threadIdx.x] = G.v[9 * B.facets[T.fb * BS] + threadIdx.x];
     for (int e = threadIdx.x; e < BS; e += blockDim.x) {
         const int g = B.facets[T.gb * BS + e];
         gid[e] = g;
         if (g >= 0) {
-            for (int k = 0; k < 9; ++k) gv[e * 9 + k] = G.v[9 * g + k];
-            gcr[e * 5] = G.c[3 * g];
-            gcr[e * 5 + 1] = G.c[3 * g + 1];
-            gcr[e * 5 + 2] = G.c[3 * g + 2];
-            gcr[e * 5 + 3] = G.rad[g];
-            gcr[e * 5 + 4] = G.diam[g];
-            garea[e] = G.area[g];
+            gcr[e * 6] = G.c[3 * g];
+            gcr[e * 6 + 1] = G.c[3 * g + 1];
+            gcr[e * 6 + 2] = G.c[3 * g + 2];
+            gcr[e * 6 + 3] = G.rad[g];
+            gcr[e * 6 + 4] = G.diam[g];
+            gcr[e * 6 + 5] = G.area[g];
             for (int k = 0; k < 3; ++k) gvid[e * 3 + k] = G.vid[3 * g + k];
         }
     }
     for (int e = threadIdx.x; e < BS * (BS + 1); e += blockDim.x) It[e] = 0.0;
     __syncthreads();
+    for (int e = threadIdx.x; e < BS * NF; e += blockDim.x) {
+        const int g = gid[e / NF];
+        Ys[e] = g >= 0 ? far_ypoint(G.v + 9 * g, o, e % NF) : make_double4(0, 0, 0, 1);
+    }
+    __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int fl = (warp & 1) * 32 + lane;
     const int f = B.facets[T.fb * BS + fl];
     if (f >= 0) {
-        double t[9];
-        for (int k = 0; k < 9; ++k) t[k] = G.v[9 * f + k];
-        const D3 cf = {G.c[3 * f], G.c[3 * f + 1], G.c[3 * f + 2]};
-        const double rf = G.rad[f], df = G.diam[f], af = G.area[f];
-        int fv[3] = {G.vid[3 * f], G.vid[3 * f + 1], G.vid[3 * f + 2]};
-        FarPts P;
-        far_points(t, P);
-        for (int gl = warp >> 1; gl < BS; gl += FAR_THREADS / 64) {
-            const int g = gid[gl];
-            if (g < 0 || (diag && gl >= fl)) continue;
-            bool far = true;
-            if (!T.certain_far) {
-                if (shared_count(fv, gvid + 3 * gl) > 0) {
-                    far = false;
-                } else {
-                    const D3 cg = {gcr[gl * 5], gcr[gl * 5 + 1], gcr[gl * 5 + 2]};
-                    far = (f > g) ? far_test(cf, rf, df, cg, gcr[gl * 5 + 3], gcr[gl * 5 + 4], thr)
-                                  : far_test(cg, gcr[gl * 5 + 3], gcr[gl * 5 + 4], cf, rf, df, thr);
+        // classification: far mask over this warp's 16 g-facets (bit m <-> gl = warp/2 + 4m)
+        unsigned mask = 0;
+        {
+            const D3 cf = {G.c[3 * f], G.c[3 * f + 1], G.c[3 * f + 2]};
+            const double rf = G.rad[f], df = G.diam[f];
+            const int fv[3] = {G.vid[3 * f], G.vid[3 * f + 1], G.vid[3 * f + 2]};
+            for (int m = 0, gl = warp >> 1; gl < BS; gl += FAR_THREADS / 64, ++m) {
+                const int g = gid[gl];
+                if (g < 0 || (diag && gl >= fl)) continue;
+                bool far = true;
+                if (!T.certain_far) {
+                    if (shared_count(fv, gvid + 3 * gl) > 0) {
+                        far = false;
+                    } else {
+                        const D3 cg = {gcr[gl * 6], gcr[gl * 6 + 1], gcr[gl * 6 + 2]};
+                        far = (f > g) ? far_test(cf, rf, df, cg, gcr[gl * 6 + 3], gcr[gl * 6 + 4], thr)
+                                      : far_test(cg, gcr[gl * 6 + 3], gcr[gl * 6 + 4], cf, rf, df, thr);
+                    }
                 }
+                if (far) mask |= 1u << m;
             }
-            if (!far) continue;
-            const double acc = far_sum(P, gv + 9 * gl);
-            It[fl * (BS + 1) + gl] = acc * af * garea[gl] * inv_pi;
+        }
+        const double sf = G.area[f] * inv_pi;
+        for (int half = 0; half < 2; ++half) {
+            XPts X;
+            far_xpoints(G.v + 9 * f, o, half, X);
+            for (int m = 0, gl = warp >> 1; gl < BS; gl += FAR_THREADS / 64, ++m) {
+                if (!(mask >> m & 1)) continue;
+                It[fl * (BS + 1) + gl] += far_half_sum(X, Ys + gl * NF, half) * sf * gcr[gl * 6 + 5];
+            }
         }
     }
     __syncthreads();
@@ -377,19 +448,19 @@ __global__ void k_near_level(const NearNode* __restrict__ nodes, const unsigned 
     }
 }
 
-// leaves: two per warp; lane (ia, jb) of each half-warp owns i in [9ia, 9ia+9), j in [9jb, 9jb+9)
-__global__ void __launch_bounds__(256) k_near_leaves(const NearNode* __restrict__ leaves,
-                                                     const unsigned long long* __restrict__ nleaves_dev,
-                                                     long long cap, const int2* __restrict__ pairs,
-                                                     const double* __restrict__ GV, double inv_pi,
-                                                     double* __restrict__ out)
+// leaves: four per warp; lane (ia, jb) of each 8-lane group owns i in [18ia, 18ia+18), j in [9jb, 9jb+9)
+__global__ void __launch_bounds__(256, 2) k_near_leaves(const NearNode* __restrict__ leaves,
+                                                        const unsigned long long* __restrict__ nleaves_dev,
+                                                        long long cap, const int2* __restrict__ pairs,
+                                                        const double* __restrict__ GV, double inv_pi,
+                                                        double* __restrict__ out)
 {
     const long long nl = min((long long)*nleaves_dev, cap);
     const int lane = threadIdx.x & 31;
-    const int h = lane >> 4, l16 = lane & 15, ia = l16 >> 2, jb = l16 & 3;
+    const int h = lane >> 3, l8 = lane & 7, ia = l8 >> 2, jb = l8 & 3;
     const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
-    for (long long w = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); 2 * w < nl; w += warps) {
-        const long long q = 2 * w + h;
+    for (long long w = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); 4 * w < nl; w += warps) {
+        const long long q = 4 * w + h;
         const bool active = q < nl;
         double acc = 0.0, scale = 0.0;
         int pair = 0;
@@ -412,8 +483,8 @@ __global__ void __launch_bounds__(256) k_near_leaves(const NearNode* __restrict_
             const double f1x = t[3] - t[0], f1y = t[4] - t[1], f1z = t[5] - t[2];
             const double f2x = t[6] - t[0], f2y = t[7] - t[1], f2z = t[8] - t[2];
 #pragma unroll 1
-            for (int p = 0; p < 9; ++p) {
-                const int i = 9 * ia + p;
+            for (int p = 0; p < 18; ++p) {
+                const int i = 18 * ia + p;
                 const double xx = fma(c_near_v[i], f2x, fma(c_near_u[i], f1x, t[0]));
                 const double xy = fma(c_near_v[i], f2y, fma(c_near_u[i], f1y, t[1]));
                 const double xz = fma(c_near_v[i], f2z, fma(c_near_u[i], f1z, t[2]));
@@ -430,8 +501,8 @@ __global__ void __launch_bounds__(256) k_near_leaves(const NearNode* __restrict_
                 acc = fma(c_near_w[i], in0 + in1, acc);
             }
         }
-        for (int o = 8; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if (active && l16 == 0) atomicAdd(out + pair, acc * scale);
+        for (int o = 4; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (active && l8 == 0) atomicAdd(out + pair, acc * scale);
     }
 }
 
@@ -786,7 +857,7 @@ long long run_near(Ctx* ctx, const double* GV, const int2* pairs, const unsigned
         }
         {
             TimedScope tl(ctx, "near_leaves");
-            const long long warps = (ncur + 1) / 2;  // upper bound on this level's leaf pairs
+            const long long warps = (ncur + 3) / 4;  // upper bound on this level's leaf quads
             const int lgrid = (int)std::min<long long>((warps + 7) / 8, 32LL * ctx->sm_count);
             k_near_leaves<<<lgrid, 256, 0, s>>>(NW.leaves.p, NW.cnt.p + 2, ncur, pairs, GV, 1.0 / M_PI, out);
             count_launch();
@@ -1037,7 +1108,13 @@ void assembly_run(AssemblyPlan* P, DMatrix& W, AssemblyStats* stats)
     {
         TimedScope ts(ctx, "far_tiles");
         BlockPtrs BP{P->bfac.p, P->dof_ptr.p, P->dofs.p, P->ent_ptr.p, P->ents.p};
-        k_far_tiles<<<(int)P->ntiles, FAR_THREADS, 0, s>>>(P->tiles.p, P->G.ptrs(), BP, thr, W.a.p, W.ld, 1.0 / M_PI);
+        static bool attr = false;
+        if (!attr) {
+            SBG_CUDA(cudaFuncSetAttribute(k_far_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FAR_SMEM));
+            attr = true;
+        }
+        k_far_tiles<<<(int)P->ntiles, FAR_THREADS, FAR_SMEM, s>>>(P->tiles.p, P->G.ptrs(), BP, thr, W.a.p, W.ld,
+                                                                  1.0 / M_PI);
         count_launch();
         SBG_LAUNCH_CHECK();
     }
@@ -1089,11 +1166,17 @@ __global__ void k_far_pair_list(GeoPtrs G, const int2* __restrict__ pairs, long 
     const long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= np) return;
     const int f = pairs[k].x, g = pairs[k].y;
-    double t[9];
-    for (int q = 0; q < 9; ++q) t[q] = G.v[9 * f + q];
-    FarPts P;
-    far_points(t, P);
-    out[k] = far_sum(P, G.v + 9 * g) * G.area[f] * G.area[g] * inv_pi;
+    const double* t = G.v + 9 * f;
+    const double* sv = G.v + 9 * g;
+    double4 Y[NF];
+    for (int j = 0; j < NF; ++j) Y[j] = far_ypoint(sv, t, j);
+    double acc = 0.0;
+    for (int half = 0; half < 2; ++half) {
+        XPts X;
+        far_xpoints(t, t, half, X);
+        acc += far_half_sum(X, Y, half) * (G.area[f] * inv_pi) * G.area[g];
+    }
+    out[k] = acc;
 }
 void far_pair_list(Ctx* ctx, const GeoPtrs& G, const int2* pairs, long long np, double* out)
 {

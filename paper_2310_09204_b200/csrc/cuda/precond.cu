@@ -317,21 +317,26 @@ __global__ void k_compact_inverse(const double* __restrict__ Lp, const long long
 }
 
 // ---------------------------------------------------------------- apply
-// gather r into the block-local vector (faces/WB) and restrict to the coarse space
+// gather r into the block-local vector (faces/WB) and restrict to the coarse space:
+// blocks [0, dof_blocks) gather one dof per thread, the rest one coarse column per warp
 __global__ void k_prec_gather(const double* __restrict__ r, int n, const int* __restrict__ pos,
                               double* __restrict__ loc, const int* __restrict__ cptr, const int* __restrict__ crow,
-                              const double* __restrict__ cval, int nc, double* __restrict__ loc_c, const int* done)
+                              const double* __restrict__ cval, int nc, double* __restrict__ loc_c, int dof_blocks,
+                              const int* done)
 {
     if (done && *done) return;
-    const int d = blockIdx.x * blockDim.x + threadIdx.x;
-    if (d < n) {
-        if (pos[d] >= 0) loc[pos[d]] = r[d];
-    } else if (d - n < nc) {
-        const int c = d - n;
-        double s = 0.0;
-        for (int q = cptr[c]; q < cptr[c + 1]; ++q) s += cval[q] * r[crow[q]];
-        loc_c[c] = s;
+    if ((int)blockIdx.x < dof_blocks) {
+        const int d = blockIdx.x * blockDim.x + threadIdx.x;
+        if (d < n && pos[d] >= 0) loc[pos[d]] = r[d];
+        return;
     }
+    const int c = ((int)blockIdx.x - dof_blocks) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (c >= nc) return;
+    double s = 0.0;
+    for (int q = cptr[c] + lane; q < cptr[c + 1]; q += 32) s += cval[q] * r[crow[q]];
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) loc_c[c] = s;
 }
 
 // y_b = M_b x_b for GEMV_ROWS rows of one block per CTA (warp per row, x_b in smem)
@@ -730,8 +735,9 @@ void prec_apply(Ctx* ctx, Prec* P, const double* r, double* z, const int* done)
     if (n == 0) return;
     const int cb = P->coarse_block;
     double* loc_c = cb >= 0 ? P->loc.p + P->h_loc[cb] : nullptr;
-    k_prec_gather<<<(n + P->nc + 255) / 256, 256, 0, s>>>(r, n, P->pos.p, P->loc.p, P->Rc_ptr.p, P->Rc_row.p,
-                                                          P->Rc_val.p, P->nc, loc_c, done);
+    const int dof_blocks = (n + 255) / 256;
+    k_prec_gather<<<dof_blocks + (P->nc + 7) / 8, 256, 0, s>>>(r, n, P->pos.p, P->loc.p, P->Rc_ptr.p, P->Rc_row.p,
+                                                               P->Rc_val.p, P->nc, loc_c, dof_blocks, done);
     count_launch();
     const double* yloc;
     if (P->mode == kPrecInverse) {
