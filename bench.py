@@ -220,8 +220,8 @@ def run_ours(args):
         ctx.synchronize()
     launches = S.launch_count() - launches0
     tm = {k: ctx.timer(k) for k in ("step", "assemble_W", "far_tiles", "near", "near_leaves", "sauter", "classify",
-                                     "local_scatter", "mirror", "cholesky", "coarse_galerkin", "pcg", "gemv_f64",
-                                     "precond_apply")}
+                                     "local_scatter", "mirror", "near_classify", "build_preconditioner", "cholesky",
+                                     "block_inverse", "coarse_galerkin", "pcg", "gemv_f64", "precond_apply")}
     ms = {k: (v[0] / v[1] if v[1] else 0.0) for k, v in tm.items()}
     t_asm = ms["assemble_W"] * 1e-3
     step_ms = ms["step"]

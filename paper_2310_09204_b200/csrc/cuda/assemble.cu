@@ -95,51 +95,6 @@ __device__ __forceinline__ int shared_count(const int* a, const int* b)
     return s;
 }
 
-// ---------------------------------------------------------------- far rule
-struct FarPts {
-    double x[NF], y[NF], z[NF];
-};
-
-__device__ __forceinline__ void far_points(const double* t, FarPts& P)
-{
-    const double e1x = t[3] - t[0], e1y = t[4] - t[1], e1z = t[5] - t[2];
-    const double e2x = t[6] - t[0], e2y = t[7] - t[1], e2z = t[8] - t[2];
-#pragma unroll
-    for (int i = 0; i < NF; ++i) {
-        P.x[i] = fma(c_far_v[i], e2x, fma(c_far_u[i], e1x, t[0]));
-        P.y[i] = fma(c_far_v[i], e2y, fma(c_far_u[i], e1y, t[1]));
-        P.z[i] = fma(c_far_v[i], e2z, fma(c_far_u[i], e1z, t[2]));
-    }
-}
-
-// sum_ij w_i w_j / |x_i - y_j| for the 16x16 tensor rule (triangle_pair_rule,
-// quadrature.hpp:208-220, without the 4 A A' / (4 pi) factor)
-__device__ __forceinline__ double far_sum(const FarPts& P, const double* s)
-{
-    const double e1x = s[3] - s[0], e1y = s[4] - s[1], e1z = s[5] - s[2];
-    const double e2x = s[6] - s[0], e2y = s[7] - s[1], e2z = s[8] - s[2];
-    double acc = 0.0;
-#pragma unroll 1
-    for (int j = 0; j < NF; ++j) {
-        const double u = c_far_u[j], v = c_far_v[j];
-        const double yx = fma(v, e2x, fma(u, e1x, s[0]));
-        const double yy = fma(v, e2y, fma(u, e1y, s[1]));
-        const double yz = fma(v, e2z, fma(u, e1z, s[2]));
-        double in0 = 0.0, in1 = 0.0;
-#pragma unroll
-        for (int i = 0; i < NF; i += 2) {
-            const double ax = P.x[i] - yx, ay = P.y[i] - yy, az = P.z[i] - yz;
-            const double bx = P.x[i + 1] - yx, by = P.y[i + 1] - yy, bz = P.z[i + 1] - yz;
-            const double ra = fma(ax, ax, fma(ay, ay, az * az));
-            const double rb = fma(bx, bx, fma(by, by, bz * bz));
-            in0 = fma(c_far_w[i], rsqrt_fast(ra), in0);
-            in1 = fma(c_far_w[i + 1], rsqrt_fast(rb), in1);
-        }
-        acc = fma(c_far_w[j], in0 + in1, acc);
-    }
-    return acc;
-}
-
 // ---------------------------------------------------------------- far tiles
 struct BlockPtrs {
     const int* facets;    // nblk * BS original facet ids (-1 padding)
@@ -223,21 +178,30 @@ __device__ __forceinline__ double4 far_ypoint(const double* s, const double* o, 
 // sum_j w_j sum_{q in half} w_{8 half + q} / |x_q - y_j|
 __device__ __forceinline__ double far_half_sum(const XPts& X, const double4* __restrict__ Y, int half)
 {
-    double acc = 0.0;
+    // two y-points per step: 16 independent rsqrt chains in flight (the kernel is
+    // bound by fixed-latency dependency waits otherwise)
+    double acc0 = 0.0, acc1 = 0.0;
 #pragma unroll 1
-    for (int j = 0; j < NF; ++j) {
-        const double4 y = Y[j];
-        double in0 = 0.0, in1 = 0.0;
+    for (int j = 0; j < NF; j += 2) {
+        const double4 ya = Y[j], yb = Y[j + 1];
+        double r2[16];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            r2[q] = fma(X.m2x[q], ya.x, fma(X.m2y[q], ya.y, fma(X.m2z[q], ya.z, X.x2[q] + ya.w)));
+            r2[8 + q] = fma(X.m2x[q], yb.x, fma(X.m2y[q], yb.y, fma(X.m2z[q], yb.z, X.x2[q] + yb.w)));
+        }
+        double ia0 = 0.0, ia1 = 0.0, ib0 = 0.0, ib1 = 0.0;
 #pragma unroll
         for (int q = 0; q < 8; q += 2) {
-            const double ra = fma(X.m2x[q], y.x, fma(X.m2y[q], y.y, fma(X.m2z[q], y.z, X.x2[q] + y.w)));
-            const double rb = fma(X.m2x[q + 1], y.x, fma(X.m2y[q + 1], y.y, fma(X.m2z[q + 1], y.z, X.x2[q + 1] + y.w)));
-            in0 = fma(c_far_w[8 * half + q], rsqrt_fast(ra), in0);
-            in1 = fma(c_far_w[8 * half + q + 1], rsqrt_fast(rb), in1);
+            ia0 = fma(c_far_w[8 * half + q], rsqrt_fast(r2[q]), ia0);
+            ib0 = fma(c_far_w[8 * half + q], rsqrt_fast(r2[8 + q]), ib0);
+            ia1 = fma(c_far_w[8 * half + q + 1], rsqrt_fast(r2[q + 1]), ia1);
+            ib1 = fma(c_far_w[8 * half + q + 1], rsqrt_fast(r2[9 + q]), ib1);
         }
-        acc = fma(c_far_w[j], in0 + in1, acc);
+        acc0 = fma(c_far_w[j], ia0 + ia1, acc0);
+        acc1 = fma(c_far_w[j + 1], ib0 + ib1, acc1);
     }
-    return acc;
+    return acc0 + acc1;
 }
 
 constexpr size_t FAR_SMEM = (size_t)BS * (BS + 1) * 8 + (size_t)BS * NF * 32 + (size_t)BS * 6 * 8 + (size_t)BS * 4 * 4;
@@ -482,23 +446,28 @@ __global__ void __launch_bounds__(256, 2) k_near_leaves(const NearNode* __restri
             }
             const double f1x = t[3] - t[0], f1y = t[4] - t[1], f1z = t[5] - t[2];
             const double f2x = t[6] - t[0], f2y = t[7] - t[1], f2z = t[8] - t[2];
+            // two x-points per step: 18 independent rsqrt chains in flight
 #pragma unroll 1
-            for (int p = 0; p < 18; ++p) {
+            for (int p = 0; p < 18; p += 2) {
                 const int i = 18 * ia + p;
-                const double xx = fma(c_near_v[i], f2x, fma(c_near_u[i], f1x, t[0]));
-                const double xy = fma(c_near_v[i], f2y, fma(c_near_u[i], f1y, t[1]));
-                const double xz = fma(c_near_v[i], f2z, fma(c_near_u[i], f1z, t[2]));
-                double in0 = 0.0, in1 = 0.0;
+                const double xa = fma(c_near_v[i], f2x, fma(c_near_u[i], f1x, t[0]));
+                const double ya = fma(c_near_v[i], f2y, fma(c_near_u[i], f1y, t[1]));
+                const double za = fma(c_near_v[i], f2z, fma(c_near_u[i], f1z, t[2]));
+                const double xb = fma(c_near_v[i + 1], f2x, fma(c_near_u[i + 1], f1x, t[0]));
+                const double yb = fma(c_near_v[i + 1], f2y, fma(c_near_u[i + 1], f1y, t[1]));
+                const double zb = fma(c_near_v[i + 1], f2z, fma(c_near_u[i + 1], f1z, t[2]));
+                double ina = 0.0, inb = 0.0;
 #pragma unroll
                 for (int k = 0; k < 9; ++k) {
-                    const double dx = xx - yx[k], dy = xy - yy[k], dz = xz - yz[k];
-                    const double r = rsqrt_fast(fma(dx, dx, fma(dy, dy, dz * dz)));
-                    if (k & 1)
-                        in1 = fma(c_near_w[9 * jb + k], r, in1);
-                    else
-                        in0 = fma(c_near_w[9 * jb + k], r, in0);
+                    const double dxa = xa - yx[k], dya = ya - yy[k], dza = za - yz[k];
+                    const double dxb = xb - yx[k], dyb = yb - yy[k], dzb = zb - yz[k];
+                    const double ra = rsqrt_fast(fma(dxa, dxa, fma(dya, dya, dza * dza)));
+                    const double rb = rsqrt_fast(fma(dxb, dxb, fma(dyb, dyb, dzb * dzb)));
+                    ina = fma(c_near_w[9 * jb + k], ra, ina);
+                    inb = fma(c_near_w[9 * jb + k], rb, inb);
                 }
-                acc = fma(c_near_w[i], in0 + in1, acc);
+                acc = fma(c_near_w[i], ina, acc);
+                acc = fma(c_near_w[i + 1], inb, acc);
             }
         }
         for (int o = 4; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);

@@ -35,9 +35,9 @@ struct Prec {
     Ctx* ctx = nullptr;
     int n = 0, nfaces = 0, nwb = 0, nc = 0, mode = kPrecInverse;
     int nblocks = 0, coarse_block = -1, Tmax = 0, maxnb = 0;
-    std::vector<int> h_nb, h_T, h_loc, h_Doff;
+    std::vector<int> h_nb, h_T, h_loc, h_Doff, h_ldm;
     std::vector<long long> h_Poff, h_Moff;
-    DBuf<int> d_nb, d_T, d_loc, d_Doff;
+    DBuf<int> d_nb, d_T, d_loc, d_Doff, d_ldm;
     DBuf<long long> d_Poff, d_Moff;
     DBuf<double> Lp, Xp, D, Mc, loc, locy;
     DBuf<int> pos;  // dof -> loc index (face/WB), -1 if none
@@ -301,19 +301,20 @@ __global__ void __launch_bounds__(128) k_tile_gemm(int k, const GTask* __restric
     }
 }
 
-// compact inverse: Mc_b[r][c] = M[max(r,c)][min(r,c)] over the valid n_b x n_b part
+// compact inverse: Mc_b[r][c] = M[max(r,c)][min(r,c)] over the valid n_b x n_b part,
+// rows padded with zeros to ldm_b (a multiple of 4) so every row is 32-byte aligned
 __global__ void k_compact_inverse(const double* __restrict__ Lp, const long long* __restrict__ Poff,
-                                  const int* __restrict__ Tv, const int* __restrict__ nbv,
+                                  const int* __restrict__ Tv, const int* __restrict__ nbv, const int* __restrict__ ldmv,
                                   const long long* __restrict__ Moff, double* __restrict__ Mc)
 {
     const int b = blockIdx.x;
-    const int nb = nbv[b];
+    const int nb = nbv[b], ldm = ldmv[b];
     const size_t ld = (size_t)Tv[b] * TB;
     const double* M = Lp + Poff[b];
     double* out = Mc + Moff[b];
     for (int r = blockIdx.y; r < nb; r += gridDim.y)
-        for (int c = threadIdx.x; c < nb; c += blockDim.x)
-            out[(size_t)r * nb + c] = r >= c ? M[(size_t)r * ld + c] : M[(size_t)c * ld + r];
+        for (int c = threadIdx.x; c < ldm; c += blockDim.x)
+            out[(size_t)r * ldm + c] = c >= nb ? 0.0 : (r >= c ? M[(size_t)r * ld + c] : M[(size_t)c * ld + r]);
 }
 
 // ---------------------------------------------------------------- apply
@@ -339,33 +340,43 @@ __global__ void k_prec_gather(const double* __restrict__ r, int n, const int* __
     if (lane == 0) loc_c[c] = s;
 }
 
-// y_b = M_b x_b for GEMV_ROWS rows of one block per CTA (warp per row, x_b in smem)
+// y_b = M_b x_b for GEMV_ROWS rows of one block per CTA: warp per row, 128-bit
+// streaming loads (4 in flight per lane), x_b staged in shared memory
 __global__ void __launch_bounds__(256) k_block_gemv(const int2* __restrict__ tasks, const int* __restrict__ nbv,
-                                                    const int* __restrict__ locv, const long long* __restrict__ Moff,
-                                                    const double* __restrict__ Mc, const double* __restrict__ loc,
-                                                    double* __restrict__ locy, const int* done)
+                                                    const int* __restrict__ ldmv, const int* __restrict__ locv,
+                                                    const long long* __restrict__ Moff, const double* __restrict__ Mc,
+                                                    const double* __restrict__ loc, double* __restrict__ locy,
+                                                    const int* done)
 {
     if (done && *done) return;
     extern __shared__ double xs[];
     const int2 t = tasks[blockIdx.x];
-    const int b = t.x, r0 = t.y, nb = nbv[b];
+    const int b = t.x, r0 = t.y, nb = nbv[b], ldm = ldmv[b];
     const double* x = loc + locv[b];
-    for (int c = threadIdx.x; c < nb; c += blockDim.x) xs[c] = x[c];
+    for (int c = threadIdx.x; c < ldm; c += blockDim.x) xs[c] = c < nb ? x[c] : 0.0;
     __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const double* M = Mc + Moff[b];
     const int r1 = min(nb, r0 + GEMV_ROWS);
+    const double2* xs2 = reinterpret_cast<const double2*>(xs);
+    const int half = ldm >> 1;  // double2 per row
     for (int r = r0 + warp; r < r1; r += blockDim.x >> 5) {
-        const double* row = M + (size_t)r * nb;
+        const double2* row = reinterpret_cast<const double2*>(M + (size_t)r * ldm);
         double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
         int c = lane;
-        for (; c + 96 < nb; c += 128) {
-            s0 = fma(__ldcs(row + c), xs[c], s0);
-            s1 = fma(__ldcs(row + c + 32), xs[c + 32], s1);
-            s2 = fma(__ldcs(row + c + 64), xs[c + 64], s2);
-            s3 = fma(__ldcs(row + c + 96), xs[c + 96], s3);
+        for (; c + 96 < half; c += 128) {
+            const double2 a = __ldcs(row + c), bq = __ldcs(row + c + 32), cq = __ldcs(row + c + 64), dq = __ldcs(row + c + 96);
+            const double2 xa = xs2[c], xb = xs2[c + 32], xc = xs2[c + 64], xd = xs2[c + 96];
+            s0 = fma(a.x, xa.x, fma(a.y, xa.y, s0));
+            s1 = fma(bq.x, xb.x, fma(bq.y, xb.y, s1));
+            s2 = fma(cq.x, xc.x, fma(cq.y, xc.y, s2));
+            s3 = fma(dq.x, xd.x, fma(dq.y, xd.y, s3));
         }
-        for (; c < nb; c += 32) s0 = fma(__ldcs(row + c), xs[c], s0);
+        for (; c < half; c += 32) {
+            const double2 a = __ldcs(row + c);
+            const double2 xa = xs2[c];
+            s0 = fma(a.x, xa.x, fma(a.y, xa.y, s0));
+        }
         double s = (s0 + s1) + (s2 + s3);
         for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
         if (lane == 0) locy[locv[b] + r] = s;
@@ -505,6 +516,7 @@ Prec* prec_build(Ctx* ctx, const DMatrix& W, const DofPartition& part, const Pro
     cudaStream_t s = ctx->stream;
     const int n = W.n;
     if (R.cols > 0 && R.rows != n) throw ValidationError("prolongation row count does not match the matrix");
+    TimedScope tbuild(ctx, "build_preconditioner");
     auto* P = new Prec;
     try {
         P->ctx = ctx;
@@ -546,13 +558,15 @@ Prec* prec_build(Ctx* ctx, const DMatrix& W, const DofPartition& part, const Pro
             P->h_Poff.push_back(Poff);
             P->h_Doff.push_back(Doff);
             P->h_Moff.push_back(Moff);
+            const int ldm = (nb + 3) / 4 * 4;
+            P->h_ldm.push_back(ldm);
             Poff += (long long)T * TB * T * TB;
-            Moff += (long long)nb * nb;
+            Moff += (long long)nb * ldm;
             if ((long long)Doff + (long long)T * TB * TB > 0x7fffffffLL) throw ValidationError("preconditioner too large");
             Doff += T * TB * TB;
             loc += T * TB;
             P->Tmax = std::max(P->Tmax, T);
-            P->maxnb = std::max(P->maxnb, nb);
+            P->maxnb = std::max(P->maxnb, ldm);
             P->apply_bytes += (double)nb * nb * 8.0;
         }
         P->d_nb.upload(P->h_nb, s);
@@ -561,6 +575,7 @@ Prec* prec_build(Ctx* ctx, const DMatrix& W, const DofPartition& part, const Pro
         P->d_Poff.upload(P->h_Poff, s);
         P->d_Doff.upload(P->h_Doff, s);
         P->d_Moff.upload(P->h_Moff, s);
+        P->d_ldm.upload(P->h_ldm, s);
         P->Lp.alloc(std::max<long long>(Poff, 1));
         P->D.alloc(std::max(Doff, 1));
         P->loc.alloc(std::max(loc, 1));
@@ -676,7 +691,7 @@ Prec* prec_build(Ctx* ctx, const DMatrix& W, const DofPartition& part, const Pro
             P->Xp.release();
             P->Mc.alloc(std::max<long long>(Moff, 1));
             k_compact_inverse<<<dim3(P->nblocks, 64), 128, 0, s>>>(P->Lp.p, P->d_Poff.p, P->d_T.p, P->d_nb.p,
-                                                                   P->d_Moff.p, P->Mc.p);
+                                                                   P->d_ldm.p, P->d_Moff.p, P->Mc.p);
             count_launch();
             SBG_LAUNCH_CHECK();
             std::vector<int2> gt;
@@ -742,7 +757,7 @@ void prec_apply(Ctx* ctx, Prec* P, const double* r, double* z, const int* done)
     const double* yloc;
     if (P->mode == kPrecInverse) {
         k_block_gemv<<<P->ngemv, 256, (size_t)std::max(P->maxnb, 1) * sizeof(double), s>>>(
-            P->gemv_tasks.p, P->d_nb.p, P->d_loc.p, P->d_Moff.p, P->Mc.p, P->loc.p, P->locy.p, done);
+            P->gemv_tasks.p, P->d_nb.p, P->d_ldm.p, P->d_loc.p, P->d_Moff.p, P->Mc.p, P->loc.p, P->locy.p, done);
         count_launch();
         yloc = P->locy.p;
     } else {
@@ -784,9 +799,10 @@ void prec_block_diag(Ctx* ctx, Prec* P, int which, std::vector<double>& diag)
     if (b < 0 || b >= P->nblocks) return;
     const int nb = P->h_nb[b];
     if (P->mode == kPrecInverse) {
-        std::vector<double> h((size_t)nb * nb);
+        const int ldm = P->h_ldm[b];
+        std::vector<double> h((size_t)nb * ldm);
         SBG_CUDA(cudaMemcpy(h.data(), P->Mc.p + P->h_Moff[b], h.size() * sizeof(double), cudaMemcpyDeviceToHost));
-        for (int i = 0; i < nb; ++i) diag.push_back(h[(size_t)i * nb + i]);
+        for (int i = 0; i < nb; ++i) diag.push_back(h[(size_t)i * ldm + i]);
     } else {
         const size_t ld = (size_t)P->h_T[b] * TB;
         std::vector<double> h(ld * ld);
