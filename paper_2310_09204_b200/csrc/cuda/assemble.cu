@@ -142,21 +142,24 @@ __device__ void tile_contract_flush(const double* __restrict__ It, int fb, int g
 
 // Far pairs with the distance expansion |x-y|^2 = |x|^2 + |y|^2 - 2 x.y in
 // tile-local coordinates (origin o = first vertex of the tile's first f-facet):
-// per evaluation DADD + 3 DFMA instead of 3 DADD + DMUL + 2 DFMA.  Far pairs
+// per evaluation DADD + 3 DFMA instead of 3 DADD + DMUL + 2 DFMA.  Each lane keeps
+// 4 of its facet's 16 rule points in registers per pass (3 CTAs of 256 per SM).  Far pairs
 // satisfy dist >= 2 diam, so (|x|^2+|y|^2)/|x-y|^2 stays O(10) inside a tile and
 // ~1 between distant tiles: the rounding stays at the 1e-15 level.
+constexpr int FAR_PASS = 4;            // rule points of f held in registers per pass
+constexpr int FAR_NPASS = NF / FAR_PASS;
 struct XPts {
-    double m2x[8], m2y[8], m2z[8], x2[8];  // -2x, -2y, -2z, |x|^2 for 8 rule points
+    double m2x[FAR_PASS], m2y[FAR_PASS], m2z[FAR_PASS], x2[FAR_PASS];  // -2x, -2y, -2z, |x|^2
 };
 
-__device__ __forceinline__ void far_xpoints(const double* t, const double* o, int half, XPts& X)
+__device__ __forceinline__ void far_xpoints(const double* t, const double* o, int pass, XPts& X)
 {
     const double e1x = t[3] - t[0], e1y = t[4] - t[1], e1z = t[5] - t[2];
     const double e2x = t[6] - t[0], e2y = t[7] - t[1], e2z = t[8] - t[2];
     const double bx = t[0] - o[0], by = t[1] - o[1], bz = t[2] - o[2];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-        const int i = 8 * half + q;
+    for (int q = 0; q < FAR_PASS; ++q) {
+        const int i = FAR_PASS * pass + q;
         const double x = fma(c_far_v[i], e2x, fma(c_far_u[i], e1x, bx));
         const double y = fma(c_far_v[i], e2y, fma(c_far_u[i], e1y, by));
         const double z = fma(c_far_v[i], e2z, fma(c_far_u[i], e1z, bz));
@@ -175,38 +178,29 @@ __device__ __forceinline__ double4 far_ypoint(const double* s, const double* o, 
     return make_double4(y0, y1, y2, fma(y0, y0, fma(y1, y1, y2 * y2)));
 }
 
-// sum_j w_j sum_{q in half} w_{8 half + q} / |x_q - y_j|
-__device__ __forceinline__ double far_half_sum(const XPts& X, const double4* __restrict__ Y, int half)
+// sum_j w_j sum_{q in pass} w_{4 pass + q} / |x_q - y_j|  (16 y-points x 4 x-points)
+__device__ __forceinline__ double far_pass_sum(const XPts& X, const double4* __restrict__ Y, int pass)
 {
-    // two y-points per step: 16 independent rsqrt chains in flight (the kernel is
-    // bound by fixed-latency dependency waits otherwise)
-    double acc0 = 0.0, acc1 = 0.0;
-#pragma unroll 1
-    for (int j = 0; j < NF; j += 2) {
-        const double4 ya = Y[j], yb = Y[j + 1];
-        double r2[16];
+    double acc = 0.0;
+#pragma unroll 2
+    for (int j = 0; j < NF; ++j) {
+        const double4 y = Y[j];
+        double in0 = 0.0, in1 = 0.0;
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-            r2[q] = fma(X.m2x[q], ya.x, fma(X.m2y[q], ya.y, fma(X.m2z[q], ya.z, X.x2[q] + ya.w)));
-            r2[8 + q] = fma(X.m2x[q], yb.x, fma(X.m2y[q], yb.y, fma(X.m2z[q], yb.z, X.x2[q] + yb.w)));
+        for (int q = 0; q < FAR_PASS; q += 2) {
+            const double ra = fma(X.m2x[q], y.x, fma(X.m2y[q], y.y, fma(X.m2z[q], y.z, X.x2[q] + y.w)));
+            const double rb = fma(X.m2x[q + 1], y.x, fma(X.m2y[q + 1], y.y, fma(X.m2z[q + 1], y.z, X.x2[q + 1] + y.w)));
+            in0 = fma(c_far_w[FAR_PASS * pass + q], rsqrt_fast(ra), in0);
+            in1 = fma(c_far_w[FAR_PASS * pass + q + 1], rsqrt_fast(rb), in1);
         }
-        double ia0 = 0.0, ia1 = 0.0, ib0 = 0.0, ib1 = 0.0;
-#pragma unroll
-        for (int q = 0; q < 8; q += 2) {
-            ia0 = fma(c_far_w[8 * half + q], rsqrt_fast(r2[q]), ia0);
-            ib0 = fma(c_far_w[8 * half + q], rsqrt_fast(r2[8 + q]), ib0);
-            ia1 = fma(c_far_w[8 * half + q + 1], rsqrt_fast(r2[q + 1]), ia1);
-            ib1 = fma(c_far_w[8 * half + q + 1], rsqrt_fast(r2[9 + q]), ib1);
-        }
-        acc0 = fma(c_far_w[j], ia0 + ia1, acc0);
-        acc1 = fma(c_far_w[j + 1], ib0 + ib1, acc1);
+        acc = fma(c_far_w[j], in0 + in1, acc);
     }
-    return acc0 + acc1;
+    return acc;
 }
 
 constexpr size_t FAR_SMEM = (size_t)BS * (BS + 1) * 8 + (size_t)BS * NF * 32 + (size_t)BS * 6 * 8 + (size_t)BS * 4 * 4;
 
-__global__ void __launch_bounds__(FAR_THREADS, 2)
+__global__ void __launch_bounds__(FAR_THREADS, 3)
     k_far_tiles(const TileInfo* __restrict__ tiles, GeoPtrs G, BlockPtrs B, double thr, double* __restrict__ W,
                 int ld, double inv_pi)
 {
@@ -267,12 +261,12 @@ __global__ void __launch_bounds__(FAR_THREADS, 2)
             }
         }
         const double sf = G.area[f] * inv_pi;
-        for (int half = 0; half < 2; ++half) {
+        for (int pass = 0; pass < FAR_NPASS; ++pass) {
             XPts X;
-            far_xpoints(G.v + 9 * f, o, half, X);
+            far_xpoints(G.v + 9 * f, o, pass, X);
             for (int m = 0, gl = warp >> 1; gl < BS; gl += FAR_THREADS / 64, ++m) {
                 if (!(mask >> m & 1)) continue;
-                It[fl * (BS + 1) + gl] += far_half_sum(X, Ys + gl * NF, half) * sf * gcr[gl * 6 + 5];
+                It[fl * (BS + 1) + gl] += far_pass_sum(X, Ys + gl * NF, pass) * sf * gcr[gl * 6 + 5];
             }
         }
     }
@@ -1140,10 +1134,10 @@ __global__ void k_far_pair_list(GeoPtrs G, const int2* __restrict__ pairs, long 
     double4 Y[NF];
     for (int j = 0; j < NF; ++j) Y[j] = far_ypoint(sv, t, j);
     double acc = 0.0;
-    for (int half = 0; half < 2; ++half) {
+    for (int pass = 0; pass < FAR_NPASS; ++pass) {
         XPts X;
-        far_xpoints(t, t, half, X);
-        acc += far_half_sum(X, Y, half) * (G.area[f] * inv_pi) * G.area[g];
+        far_xpoints(t, t, pass, X);
+        acc += far_pass_sum(X, Y, pass) * (G.area[f] * inv_pi) * G.area[g];
     }
     out[k] = acc;
 }

@@ -24,8 +24,8 @@ namespace sbg {
 namespace {
 constexpr int TB = 64;   // tile size
 constexpr int TLD = 68;  // padded shared-memory leading dimension (conflict-free DMMA fragments)
-constexpr int GEMV_ROWS = 32;
-enum { K_TRSM = 0, K_UPDATE = 1, K_TRTRI = 2, K_LAUUM = 3 };
+constexpr int GEMV_ROWS = 8;  // one row per warp
+enum { K_TRSM = 0, K_UPDATE = 1, K_XDIAG = 2, K_LAUUM = 3, K_XUPD = 4 };
 struct GTask {
     int b, i, j, pad;
 };
@@ -221,7 +221,9 @@ __device__ __forceinline__ void for_acc(const double (&acc)[4][4][2], F f)
 
 // KIND K_TRSM  : L(i,k) = L(i,k) D_k^T            (task.i = i)
 //      K_UPDATE: L(i,j) -= L(i,k) L(j,k)^T        (task.i, task.j)
-//      K_TRTRI : X(i,j) = -D_i sum_{q=j}^{i-1} L(i,q) X(q,j);  X(i,i) = D_i
+//      K_XDIAG : X(i,j) = -D_i S(i,j) (S accumulated in X), X(i,i) = D_i   (step k = i)
+//      K_XUPD  : X(i',j) += L(i',k) X(k,j)  for i' > k >= j          (step k)
+//                (right-looking blocked L^-1: X(i,j) = -D_i sum_{q=j}^{i-1} L(i,q) X(q,j))
 //      K_LAUUM : M(i,j) = sum_{q=i}^{T-1} X(q,i)^T X(q,j)   (written over L)
 template <int KIND>
 __global__ void __launch_bounds__(128) k_tile_gemm(int k, const GTask* __restrict__ tasks, const int* __restrict__ Tv,
@@ -262,32 +264,25 @@ __global__ void __launch_bounds__(128) k_tile_gemm(int k, const GTask* __restric
             else
                 *dst -= v;
         });
-    } else if (KIND == K_TRTRI) {
+    } else if (KIND == K_XDIAG) {
         double* C = tile(X, t.i, t.j);
         if (t.i == t.j) {
             const double* Di = Db + (size_t)t.i * TB * TB;
             for (int e = threadIdx.x; e < TB * TB; e += blockDim.x) C[(size_t)(e / TB) * ld + (e % TB)] = Di[e];
             return;
         }
-        for (int q = t.j; q < t.i; ++q) {
-            __syncthreads();
-            stage(As, tile(L, t.i, q), ld, false);
-            stage(Bs, tile(X, q, t.j), ld, true);
-            __syncthreads();
-            mma_tiles(As, Bs, acc);
-        }
-        __syncthreads();
-        // Bs <- acc^T (rows = output cols), As <- D_i, then C = -D_i acc
-        for_acc(acc, [&](int r, int c, double v) { Bs[c * TLD + r] = v; });
         stage(As, Db + (size_t)t.i * TB * TB, TB, false);
+        stage(Bs, C, ld, true);
         __syncthreads();
-        double acc2[4][4][2];
-#pragma unroll
-        for (int x = 0; x < 4; ++x)
-#pragma unroll
-            for (int y = 0; y < 4; ++y) acc2[x][y][0] = acc2[x][y][1] = 0.0;
-        mma_tiles(As, Bs, acc2);
-        for_acc(acc2, [&](int r, int c, double v) { C[(size_t)r * ld + c] = -v; });
+        mma_tiles(As, Bs, acc);
+        for_acc(acc, [&](int r, int c, double v) { C[(size_t)r * ld + c] = -v; });
+    } else if (KIND == K_XUPD) {
+        stage(As, tile(L, t.i, k), ld, false);
+        stage(Bs, tile(X, k, t.j), ld, true);
+        __syncthreads();
+        mma_tiles(As, Bs, acc);
+        double* C = tile(X, t.i, t.j);
+        for_acc(acc, [&](int r, int c, double v) { C[(size_t)r * ld + c] += v; });
     } else {  // K_LAUUM
         for (int q = t.i; q < T; ++q) {
             __syncthreads();
@@ -340,8 +335,8 @@ __global__ void k_prec_gather(const double* __restrict__ r, int n, const int* __
     if (lane == 0) loc_c[c] = s;
 }
 
-// y_b = M_b x_b for GEMV_ROWS rows of one block per CTA: warp per row, 128-bit
-// streaming loads (4 in flight per lane), x_b staged in shared memory
+// y_b = M_b x_b: one row per warp, 8 rows per CTA; 128-bit streaming loads of M
+// (8 in flight per lane), x_b through the L1 (it is re-read by every row of the block)
 __global__ void __launch_bounds__(256) k_block_gemv(const int2* __restrict__ tasks, const int* __restrict__ nbv,
                                                     const int* __restrict__ ldmv, const int* __restrict__ locv,
                                                     const long long* __restrict__ Moff, const double* __restrict__ Mc,
@@ -349,38 +344,33 @@ __global__ void __launch_bounds__(256) k_block_gemv(const int2* __restrict__ tas
                                                     const int* done)
 {
     if (done && *done) return;
-    extern __shared__ double xs[];
     const int2 t = tasks[blockIdx.x];
-    const int b = t.x, r0 = t.y, nb = nbv[b], ldm = ldmv[b];
-    const double* x = loc + locv[b];
-    for (int c = threadIdx.x; c < ldm; c += blockDim.x) xs[c] = c < nb ? x[c] : 0.0;
-    __syncthreads();
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const double* M = Mc + Moff[b];
-    const int r1 = min(nb, r0 + GEMV_ROWS);
-    const double2* xs2 = reinterpret_cast<const double2*>(xs);
-    const int half = ldm >> 1;  // double2 per row
-    for (int r = r0 + warp; r < r1; r += blockDim.x >> 5) {
-        const double2* row = reinterpret_cast<const double2*>(M + (size_t)r * ldm);
-        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-        int c = lane;
-        for (; c + 96 < half; c += 128) {
-            const double2 a = __ldcs(row + c), bq = __ldcs(row + c + 32), cq = __ldcs(row + c + 64), dq = __ldcs(row + c + 96);
-            const double2 xa = xs2[c], xb = xs2[c + 32], xc = xs2[c + 64], xd = xs2[c + 96];
-            s0 = fma(a.x, xa.x, fma(a.y, xa.y, s0));
-            s1 = fma(bq.x, xb.x, fma(bq.y, xb.y, s1));
-            s2 = fma(cq.x, xc.x, fma(cq.y, xc.y, s2));
-            s3 = fma(dq.x, xd.x, fma(dq.y, xd.y, s3));
+    const int b = t.x, nb = nbv[b], ldm = ldmv[b];
+    const int r = t.y + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+    if (r >= nb) return;
+    const double2* x2 = reinterpret_cast<const double2*>(loc + locv[b]);  // loc rows are 64-padded (zeros)
+    const double2* row = reinterpret_cast<const double2*>(Mc + Moff[b] + (size_t)r * ldm);
+    const int half = ldm >> 1;
+    double s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    int c = lane;
+    for (; c + 7 * 32 < half; c += 8 * 32) {
+        double2 a[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) a[u] = __ldcs(row + c + 32 * u);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const double2 xv = __ldg(x2 + c + 32 * u);
+            s[u] = fma(a[u].x, xv.x, fma(a[u].y, xv.y, s[u]));
         }
-        for (; c < half; c += 32) {
-            const double2 a = __ldcs(row + c);
-            const double2 xa = xs2[c];
-            s0 = fma(a.x, xa.x, fma(a.y, xa.y, s0));
-        }
-        double s = (s0 + s1) + (s2 + s3);
-        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-        if (lane == 0) locy[locv[b] + r] = s;
     }
+    for (; c < half; c += 32) {
+        const double2 a = __ldcs(row + c);
+        const double2 xv = __ldg(x2 + c);
+        s[0] = fma(a.x, xv.x, fma(a.y, xv.y, s[0]));
+    }
+    double v = ((s[0] + s[1]) + (s[2] + s[3])) + ((s[4] + s[5]) + (s[6] + s[7]));
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) locy[locv[b] + r] = v;
 }
 
 // 4 threads per row: partial dot of a 64-wide tile row
@@ -490,23 +480,28 @@ __global__ void k_prec_scatter(const double* __restrict__ locy, const int* __res
 }
 
 template <int KIND>
-void launch_gemm(Ctx* ctx, Prec* P, int k, const std::vector<GTask>& tasks, DBuf<GTask>& dev)
+void launch_gemm(Ctx* ctx, Prec* P, int k, const GTask* dev_tasks, int count)
 {
-    if (tasks.empty()) return;
-    cudaStream_t s = ctx->stream;
+    if (count <= 0) return;
     const size_t smem = 2 * TB * TLD * sizeof(double);
     static bool configured = false;
     if (!configured) {
         SBG_CUDA(cudaFuncSetAttribute(k_tile_gemm<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         configured = true;
     }
-    dev.upload(tasks, s);
-    k_tile_gemm<KIND><<<(int)tasks.size(), 128, smem, s>>>(k, dev.p, P->d_T.p, P->d_Poff.p, P->d_Doff.p, P->Lp.p,
-                                                          P->Xp.p, P->D.p);
+    k_tile_gemm<KIND><<<count, 128, smem, ctx->stream>>>(k, dev_tasks, P->d_T.p, P->d_Poff.p, P->d_Doff.p, P->Lp.p,
+                                                        P->Xp.p, P->D.p);
     count_launch();
     SBG_LAUNCH_CHECK();
-    SBG_CUDA(cudaStreamSynchronize(s));  // the host task vector and device copy are reused
 }
+
+// per-step task lists, built on the host once and uploaded in one copy
+struct StepTasks {
+    std::vector<GTask> all;
+    std::vector<int> off{0};
+    void close() { off.push_back((int)all.size()); }
+    int count(int st) const { return off[st + 1] - off[st]; }
+};
 
 }  // namespace
 
@@ -628,38 +623,43 @@ Prec* prec_build(Ctx* ctx, const DMatrix& W, const DofPartition& part, const Pro
             SBG_LAUNCH_CHECK();
             SBG_CUDA(cudaStreamSynchronize(s));
         }
-        // ---- batched tiled Cholesky
+        // ---- batched tiled Cholesky: per step k, potrf of tile (k,k), trsm of column k, trailing update
         DBuf<int> fail(std::max(P->nblocks, 1));
         SBG_CUDA(cudaMemsetAsync(fail.p, 0, fail.n * sizeof(int), s));
         {
             TimedScope ts(ctx, "cholesky");
             const size_t smem_potrf = 2 * TB * (TB + 1) * sizeof(double);
             SBG_CUDA(cudaFuncSetAttribute(k_potrf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_potrf));
-            std::vector<int> pot;
-            std::vector<GTask> trsm, upd;
-            DBuf<int> d_pot;
-            DBuf<GTask> d_tasks;
+            std::vector<int> pot, pot_off{0};
+            StepTasks trsm, upd;
             for (int k = 0; k < P->Tmax; ++k) {
-                pot.clear();
-                trsm.clear();
-                upd.clear();
                 for (int b = 0; b < P->nblocks; ++b) {
                     const int T = P->h_T[b];
                     if (T <= k) continue;
                     pot.push_back(b);
-                    for (int i = k + 1; i < T; ++i) trsm.push_back({b, i, k, 0});
+                    for (int i = k + 1; i < T; ++i) trsm.all.push_back({b, i, k, 0});
                     for (int j = k + 1; j < T; ++j)
-                        for (int i = j; i < T; ++i) upd.push_back({b, i, j, 0});
+                        for (int i = j; i < T; ++i) upd.all.push_back({b, i, j, 0});
                 }
-                d_pot.upload(pot, s);
-                k_potrf<<<(int)pot.size(), 256, smem_potrf, s>>>(k, d_pot.p, P->d_T.p, P->d_Poff.p, P->d_Doff.p,
-                                                                 P->Lp.p, P->D.p, fail.p);
+                pot_off.push_back((int)pot.size());
+                trsm.close();
+                upd.close();
+            }
+            DBuf<int> d_pot;
+            DBuf<GTask> d_trsm, d_upd;
+            d_pot.upload(pot, s);
+            d_trsm.upload(trsm.all, s);
+            d_upd.upload(upd.all, s);
+            for (int k = 0; k < P->Tmax; ++k) {
+                k_potrf<<<pot_off[k + 1] - pot_off[k], 256, smem_potrf, s>>>(k, d_pot.p + pot_off[k], P->d_T.p,
+                                                                             P->d_Poff.p, P->d_Doff.p, P->Lp.p,
+                                                                             P->D.p, fail.p);
                 count_launch();
                 SBG_LAUNCH_CHECK();
-                launch_gemm<K_TRSM>(ctx, P, k, trsm, d_tasks);
-                launch_gemm<K_UPDATE>(ctx, P, k, upd, d_tasks);
-                SBG_CUDA(cudaStreamSynchronize(s));
+                launch_gemm<K_TRSM>(ctx, P, k, d_trsm.p + trsm.off[k], trsm.count(k));
+                launch_gemm<K_UPDATE>(ctx, P, k, d_upd.p + upd.off[k], upd.count(k));
             }
+            SBG_CUDA(cudaStreamSynchronize(s));
         }
         std::vector<int> hfail(fail.n);
         SBG_CUDA(cudaMemcpy(hfail.data(), fail.p, hfail.size() * sizeof(int), cudaMemcpyDeviceToHost));
@@ -671,23 +671,36 @@ Prec* prec_build(Ctx* ctx, const DMatrix& W, const DofPartition& part, const Pro
                                      "): partition inconsistent with the assembled matrix");
             }
         if (mode == kPrecInverse) {
-            // ---- W_bb^-1 = L^-T L^-1: X = L^-1 row-tile by row-tile, then M = X^T X over L
+            // ---- W_bb^-1 = L^-T L^-1: X = L^-1 (right-looking, one-stage tile tasks), then M = X^T X over L
             TimedScope ts(ctx, "block_inverse");
             P->Xp.alloc(std::max<long long>(Poff, 1));
-            std::vector<GTask> tasks;
-            DBuf<GTask> d_tasks;
-            for (int i = 0; i < P->Tmax; ++i) {
-                tasks.clear();
-                for (int b = 0; b < P->nblocks; ++b)
-                    if (i < P->h_T[b])
-                        for (int j = 0; j <= i; ++j) tasks.push_back({b, i, j, 0});
-                launch_gemm<K_TRTRI>(ctx, P, 0, tasks, d_tasks);
+            SBG_CUDA(cudaMemsetAsync(P->Xp.p, 0, P->Xp.n * sizeof(double), s));
+            StepTasks xd, xu;
+            std::vector<GTask> la;
+            for (int k = 0; k < P->Tmax; ++k) {
+                for (int b = 0; b < P->nblocks; ++b) {
+                    const int T = P->h_T[b];
+                    if (T <= k) continue;
+                    for (int j = 0; j <= k; ++j) xd.all.push_back({b, k, j, 0});
+                    for (int i = k + 1; i < T; ++i)
+                        for (int j = 0; j <= k; ++j) xu.all.push_back({b, i, j, 0});
+                }
+                xd.close();
+                xu.close();
             }
-            tasks.clear();
             for (int b = 0; b < P->nblocks; ++b)
                 for (int i = 0; i < P->h_T[b]; ++i)
-                    for (int j = 0; j <= i; ++j) tasks.push_back({b, i, j, 0});
-            launch_gemm<K_LAUUM>(ctx, P, 0, tasks, d_tasks);
+                    for (int j = 0; j <= i; ++j) la.push_back({b, i, j, 0});
+            DBuf<GTask> d_xd, d_xu, d_la;
+            d_xd.upload(xd.all, s);
+            d_xu.upload(xu.all, s);
+            d_la.upload(la, s);
+            for (int k = 0; k < P->Tmax; ++k) {
+                launch_gemm<K_XDIAG>(ctx, P, k, d_xd.p + xd.off[k], xd.count(k));
+                launch_gemm<K_XUPD>(ctx, P, k, d_xu.p + xu.off[k], xu.count(k));
+            }
+            launch_gemm<K_LAUUM>(ctx, P, 0, d_la.p, (int)la.size());
+            SBG_CUDA(cudaStreamSynchronize(s));
             P->Xp.release();
             P->Mc.alloc(std::max<long long>(Moff, 1));
             k_compact_inverse<<<dim3(P->nblocks, 64), 128, 0, s>>>(P->Lp.p, P->d_Poff.p, P->d_T.p, P->d_nb.p,
@@ -699,9 +712,6 @@ Prec* prec_build(Ctx* ctx, const DMatrix& W, const DofPartition& part, const Pro
                 for (int r = 0; r < P->h_nb[b]; r += GEMV_ROWS) gt.push_back({b, r});
             P->gemv_tasks.upload(gt, s);
             P->ngemv = (int)gt.size();
-            const size_t smem = (size_t)std::max(P->maxnb, 1) * sizeof(double);
-            if (smem > 48 * 1024)
-                SBG_CUDA(cudaFuncSetAttribute(k_block_gemv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
             SBG_CUDA(cudaStreamSynchronize(s));
             P->Lp.release();
             P->D.release();
@@ -756,7 +766,7 @@ void prec_apply(Ctx* ctx, Prec* P, const double* r, double* z, const int* done)
     count_launch();
     const double* yloc;
     if (P->mode == kPrecInverse) {
-        k_block_gemv<<<P->ngemv, 256, (size_t)std::max(P->maxnb, 1) * sizeof(double), s>>>(
+        k_block_gemv<<<P->ngemv, 256, 0, s>>>(
             P->gemv_tasks.p, P->d_nb.p, P->d_ldm.p, P->d_loc.p, P->d_Moff.p, P->Mc.p, P->loc.p, P->locy.p, done);
         count_launch();
         yloc = P->locy.p;
