@@ -1,0 +1,280 @@
+// screenbem/gpu.hpp — C++ drop-in for the hot path of the screenbem reference
+// (proj/include/screenbem), backed by libscreenbem_b200.so (include/screenbem_b200.h).
+//
+// Names and error behaviour follow the reference: ValidationError (CLI exit 2)
+// and NumericalError (CLI exit 3) are thrown exactly where the reference throws
+// them (inc/common.hpp:16-26).  A caller of the reference replaces
+//
+//     #include "screenbem/experiments.hpp"          // Eigen-based, CPU
+//     GalerkinMatrix W = assemble_W(im, quad, threads);
+//     SchwarzPreconditioner P = build_preconditioner(W, part, R);
+//     PcgReport rep = pcg(W, &P, L, tol);
+//
+// with
+//
+//     #include "screenbem/gpu.hpp"
+//     namespace sb = screenbem::gpu;
+//     sb::Context ctx;                                 // one B200, one stream
+//     sb::InflatedMesh im = sb::inflate(mesh);
+//     sb::GalerkinMatrix W = sb::assemble_W(ctx, im);  // device-resident, .download() for dumps
+//     sb::SchwarzPreconditioner P = sb::build_preconditioner(ctx, W, sb::partition_dofs(pair, im),
+//                                                            sb::build_prolongation(pair, coarse, im));
+//     sb::PcgReport rep = sb::pcg(ctx, W, &P, L, tol);
+//
+// Host arrays are std::vector<double> (row-major for matrices) instead of Eigen types.
+#pragma once
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "../screenbem_b200.h"
+
+namespace screenbem {
+
+class ValidationError : public std::runtime_error {  // reference: inc/common.hpp:17-20
+public:
+    explicit ValidationError(const std::string& m) : std::runtime_error(m) {}
+};
+class NumericalError : public std::runtime_error {  // reference: inc/common.hpp:23-26
+public:
+    explicit NumericalError(const std::string& m) : std::runtime_error(m) {}
+};
+class CudaError : public std::runtime_error {
+public:
+    explicit CudaError(const std::string& m) : std::runtime_error(m) {}
+};
+
+namespace gpu {
+
+inline void check(int rc)
+{
+    if (rc == SBG_OK) return;
+    const std::string msg = sbg_last_error();
+    if (rc == SBG_EVALIDATION) throw ValidationError(msg);
+    if (rc == SBG_ENUMERICAL) throw NumericalError(msg);
+    if (rc == SBG_ECUDA) throw CudaError(msg);
+    throw std::runtime_error(msg);
+}
+
+template <class T, void (*Destroy)(T*)>
+class Handle {
+public:
+    Handle() = default;
+    explicit Handle(T* p) : p_(p) {}
+    Handle(const Handle&) = delete;
+    Handle& operator=(const Handle&) = delete;
+    Handle(Handle&& o) noexcept : p_(std::exchange(o.p_, nullptr)) {}
+    Handle& operator=(Handle&& o) noexcept
+    {
+        if (this != &o) {
+            reset();
+            p_ = std::exchange(o.p_, nullptr);
+        }
+        return *this;
+    }
+    ~Handle() { reset(); }
+    T* get() const { return p_; }
+    void reset()
+    {
+        if (p_) Destroy(p_);
+        p_ = nullptr;
+    }
+
+private:
+    T* p_ = nullptr;
+};
+
+struct QuadratureConfig {  // reference: inc/quadrature.hpp:12-16
+    int far_order = 4;
+    int singular_order = 8;
+    double near_threshold = 2.0;
+    sbg_quad_cfg c() const { return {far_order, singular_order, near_threshold}; }
+};
+
+class Context : public Handle<sbg_ctx, sbg_ctx_destroy> {
+public:
+    explicit Context(int device = 0)
+    {
+        sbg_ctx* p = nullptr;
+        check(sbg_ctx_create(device, &p));
+        *this = Context(p);
+    }
+    void synchronize() { check(sbg_ctx_synchronize(get())); }
+
+private:
+    explicit Context(sbg_ctx* p) : Handle(p) {}
+};
+
+// reference: inc/mesh.hpp:19-83 (3-D triangles), vertices xyz-interleaved
+class SurfaceMesh : public Handle<sbg_mesh, sbg_mesh_destroy> {
+public:
+    SurfaceMesh() = default;
+    SurfaceMesh(const std::vector<double>& verts, const std::vector<int32_t>& facets)
+    {
+        sbg_mesh* p = nullptr;
+        check(sbg_mesh_create((int)(verts.size() / 3), verts.data(), (int)(facets.size() / 3), facets.data(), &p));
+        *this = SurfaceMesh(p);
+    }
+    explicit SurfaceMesh(sbg_mesh* p) : Handle(p) {}
+};
+
+inline SurfaceMesh make_builtin(const std::string& spec)  // inc/mesh.hpp:516-537
+{
+    sbg_mesh* p = nullptr;
+    check(sbg_make_builtin(spec.c_str(), &p));
+    return SurfaceMesh(p);
+}
+inline void validate_mesh(const SurfaceMesh& m) { check(sbg_validate_mesh(m.get())); }  // inc/mesh.hpp:238-272
+
+class MeshLevelPair : public Handle<sbg_level, sbg_level_destroy> {  // inc/mesh.hpp:86-92
+public:
+    explicit MeshLevelPair(sbg_level* p) : Handle(p) {}
+    SurfaceMesh coarse() const { return mesh(0); }
+    SurfaceMesh fine() const { return mesh(1); }
+
+private:
+    SurfaceMesh mesh(int which) const
+    {
+        sbg_mesh* p = nullptr;
+        check(sbg_level_mesh(get(), which, &p));
+        return SurfaceMesh(p);
+    }
+};
+inline MeshLevelPair refine_uniform_times(const SurfaceMesh& m, int k)  // inc/mesh.hpp:388-405
+{
+    sbg_level* p = nullptr;
+    check(sbg_refine_uniform_times(m.get(), k, &p));
+    return MeshLevelPair(p);
+}
+inline MeshLevelPair make_config(int cfg, int ratio = 0)
+{
+    sbg_level* p = nullptr;
+    check(sbg_make_config(cfg, ratio, &p));
+    return MeshLevelPair(p);
+}
+
+class InflatedMesh : public Handle<sbg_inflated, sbg_inflated_destroy> {  // inc/inflate.hpp:48-76
+public:
+    explicit InflatedMesh(sbg_inflated* p) : Handle(p) {}
+    int num_jump_dofs() const
+    {
+        int n, ng, nv, nf;
+        check(sbg_inflated_sizes(get(), &n, &ng, &nv, &nf));
+        return n;
+    }
+};
+inline InflatedMesh inflate(const SurfaceMesh& m)  // inc/inflate.hpp:98-288
+{
+    sbg_inflated* p = nullptr;
+    check(sbg_inflate(m.get(), 1, &p));
+    return InflatedMesh(p);
+}
+
+class GalerkinMatrix : public Handle<sbg_matrix, sbg_matrix_destroy> {  // inc/assemble.hpp:12
+public:
+    explicit GalerkinMatrix(sbg_matrix* p) : Handle(p) {}
+    int rows() const { return sbg_matrix_n(get()); }
+    std::vector<double> download() const  // row-major n x n
+    {
+        std::vector<double> h((size_t)rows() * rows());
+        check(sbg_matrix_download(get(), h.data()));
+        return h;
+    }
+};
+// reference: inc/assemble.hpp:72-139 (`workers` is accepted and ignored on the GPU)
+inline GalerkinMatrix assemble_W(Context& ctx, const InflatedMesh& im, const QuadratureConfig& cfg = {},
+                                 int workers = 1)
+{
+    const sbg_quad_cfg c = cfg.c();
+    sbg_matrix* p = nullptr;
+    check(sbg_assemble_w(ctx.get(), im.get(), &c, workers, &p, nullptr));
+    return GalerkinMatrix(p);
+}
+// reference: inc/assemble.hpp:143-184 with a constant field g
+inline std::vector<double> assemble_rhs(Context& ctx, const InflatedMesh& im, const double g[3],
+                                        const QuadratureConfig& cfg = {})
+{
+    const sbg_quad_cfg c = cfg.c();
+    std::vector<double> L(im.num_jump_dofs());
+    check(sbg_assemble_rhs(ctx.get(), im.get(), &c, g, 0, L.data()));
+    return L;
+}
+// reference: inc/assemble.hpp:191-226
+inline void dump_matrix_binary(const GalerkinMatrix& W, const std::string& path)
+{
+    check(sbg_matrix_dump_binary(W.get(), path.c_str()));
+}
+
+class DofPartition : public Handle<sbg_partition, sbg_partition_destroy> {  // inc/schwarz.hpp:14-17
+public:
+    explicit DofPartition(sbg_partition* p) : Handle(p) {}
+};
+inline DofPartition partition_dofs(const MeshLevelPair& pair, const InflatedMesh& fine)  // schwarz.hpp:19-51
+{
+    sbg_partition* p = nullptr;
+    check(sbg_partition_dofs(pair.get(), fine.get(), &p));
+    return DofPartition(p);
+}
+class Prolongation : public Handle<sbg_prolong, sbg_prolong_destroy> {  // inc/jump.hpp:87-89
+public:
+    explicit Prolongation(sbg_prolong* p) : Handle(p) {}
+};
+inline Prolongation build_prolongation(const MeshLevelPair& pair, const InflatedMesh& coarse,
+                                       const InflatedMesh& fine)  // inc/jump.hpp:118-185
+{
+    sbg_prolong* p = nullptr;
+    check(sbg_build_prolongation(pair.get(), coarse.get(), fine.get(), &p));
+    return Prolongation(p);
+}
+
+class SchwarzPreconditioner : public Handle<sbg_prec, sbg_prec_destroy> {  // inc/schwarz.hpp:55-73
+public:
+    explicit SchwarzPreconditioner(sbg_prec* p) : Handle(p) {}
+    int num_subspaces() const { return sbg_prec_num_subspaces(get()); }
+};
+inline SchwarzPreconditioner build_preconditioner(Context& ctx, const GalerkinMatrix& W, const DofPartition& part,
+                                                  const Prolongation& R)  // inc/schwarz.hpp:100-118
+{
+    sbg_prec* p = nullptr;
+    check(sbg_build_preconditioner(ctx.get(), W.get(), part.get(), R.get(), &p));
+    return SchwarzPreconditioner(p);
+}
+inline std::vector<double> apply_preconditioner(Context& ctx, const SchwarzPreconditioner& P,
+                                                const std::vector<double>& r)  // inc/schwarz.hpp:121-140
+{
+    std::vector<double> z(r.size());
+    check(sbg_apply_preconditioner(ctx.get(), P.get(), r.data(), (int)r.size(), z.data()));
+    return z;
+}
+
+struct PcgReport {  // reference: inc/pcg.hpp:9-16
+    std::vector<double> solution;
+    int iterations = 0;
+    bool converged = false;
+    std::vector<double> residual_history;
+    double kappa_estimate = 1.0;
+};
+// reference: inc/pcg.hpp:33-116 (prec nullable)
+inline PcgReport pcg(Context& ctx, const GalerkinMatrix& W, const SchwarzPreconditioner* prec,
+                     const std::vector<double>& rhs, double tol = 1e-8, int maxit = 0)
+{
+    const int n = (int)rhs.size();
+    const int cap = (maxit > 0 ? maxit : std::max(10 * n, 100)) + 2;
+    PcgReport rep;
+    rep.solution.assign(n, 0.0);
+    rep.residual_history.assign(cap, 0.0);
+    sbg_pcg_report r{};
+    check(sbg_pcg(ctx.get(), W.get(), prec ? prec->get() : nullptr, rhs.data(), n, tol, maxit, rep.solution.data(),
+                  rep.residual_history.data(), nullptr, nullptr, cap, &r));
+    rep.iterations = r.iterations;
+    rep.converged = r.converged != 0;
+    rep.kappa_estimate = r.kappa_estimate;
+    rep.residual_history.resize(r.history_len);
+    return rep;
+}
+
+}  // namespace gpu
+}  // namespace screenbem

@@ -428,40 +428,40 @@ __global__ void __launch_bounds__(256, 2) k_near_leaves(const NearNode* __restri
             double t[9], s[9];
             node_triangles(GV, pairs[nd.pair], nd.code, t, s);
             scale = tri_area(t) * tri_area(s) * inv_pi;
+            // leaf-local origin t0: |x-y|^2 = |x|^2 + |y|^2 - 2 x.y (leaves satisfy dist >= 2 diam
+            // except at the forced depth 5, so the expansion loses at most a few bits)
             const double e1x = s[3] - s[0], e1y = s[4] - s[1], e1z = s[5] - s[2];
             const double e2x = s[6] - s[0], e2y = s[7] - s[1], e2z = s[8] - s[2];
-            double yx[9], yy[9], yz[9];
+            const double bx = s[0] - t[0], by = s[1] - t[1], bz = s[2] - t[2];
+            double yx[9], yy[9], yz[9], y2[9];
 #pragma unroll
             for (int k = 0; k < 9; ++k) {
                 const int j = 9 * jb + k;
-                yx[k] = fma(c_near_v[j], e2x, fma(c_near_u[j], e1x, s[0]));
-                yy[k] = fma(c_near_v[j], e2y, fma(c_near_u[j], e1y, s[1]));
-                yz[k] = fma(c_near_v[j], e2z, fma(c_near_u[j], e1z, s[2]));
+                yx[k] = fma(c_near_v[j], e2x, fma(c_near_u[j], e1x, bx));
+                yy[k] = fma(c_near_v[j], e2y, fma(c_near_u[j], e1y, by));
+                yz[k] = fma(c_near_v[j], e2z, fma(c_near_u[j], e1z, bz));
+                y2[k] = fma(yx[k], yx[k], fma(yy[k], yy[k], yz[k] * yz[k]));
             }
             const double f1x = t[3] - t[0], f1y = t[4] - t[1], f1z = t[5] - t[2];
             const double f2x = t[6] - t[0], f2y = t[7] - t[1], f2z = t[8] - t[2];
-            // two x-points per step: 18 independent rsqrt chains in flight
 #pragma unroll 1
-            for (int p = 0; p < 18; p += 2) {
+            for (int p = 0; p < 18; ++p) {
                 const int i = 18 * ia + p;
-                const double xa = fma(c_near_v[i], f2x, fma(c_near_u[i], f1x, t[0]));
-                const double ya = fma(c_near_v[i], f2y, fma(c_near_u[i], f1y, t[1]));
-                const double za = fma(c_near_v[i], f2z, fma(c_near_u[i], f1z, t[2]));
-                const double xb = fma(c_near_v[i + 1], f2x, fma(c_near_u[i + 1], f1x, t[0]));
-                const double yb = fma(c_near_v[i + 1], f2y, fma(c_near_u[i + 1], f1y, t[1]));
-                const double zb = fma(c_near_v[i + 1], f2z, fma(c_near_u[i + 1], f1z, t[2]));
-                double ina = 0.0, inb = 0.0;
+                const double xx = fma(c_near_v[i], f2x, c_near_u[i] * f1x);
+                const double xy = fma(c_near_v[i], f2y, c_near_u[i] * f1y);
+                const double xz = fma(c_near_v[i], f2z, c_near_u[i] * f1z);
+                const double x2 = fma(xx, xx, fma(xy, xy, xz * xz));
+                const double mx = -2.0 * xx, my = -2.0 * xy, mz = -2.0 * xz;
+                double in0 = 0.0, in1 = 0.0;
 #pragma unroll
                 for (int k = 0; k < 9; ++k) {
-                    const double dxa = xa - yx[k], dya = ya - yy[k], dza = za - yz[k];
-                    const double dxb = xb - yx[k], dyb = yb - yy[k], dzb = zb - yz[k];
-                    const double ra = rsqrt_fast(fma(dxa, dxa, fma(dya, dya, dza * dza)));
-                    const double rb = rsqrt_fast(fma(dxb, dxb, fma(dyb, dyb, dzb * dzb)));
-                    ina = fma(c_near_w[9 * jb + k], ra, ina);
-                    inb = fma(c_near_w[9 * jb + k], rb, inb);
+                    const double r2 = fma(mx, yx[k], fma(my, yy[k], fma(mz, yz[k], x2 + y2[k])));
+                    if (k & 1)
+                        in1 = fma(c_near_w[9 * jb + k], rsqrt_fast(r2), in1);
+                    else
+                        in0 = fma(c_near_w[9 * jb + k], rsqrt_fast(r2), in0);
                 }
-                acc = fma(c_near_w[i], ina, acc);
-                acc = fma(c_near_w[i + 1], inb, acc);
+                acc = fma(c_near_w[i], in0 + in1, acc);
             }
         }
         for (int o = 4; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
@@ -867,6 +867,7 @@ struct AssemblyPlan {
 
 AssemblyPlan* assembly_plan_create(Ctx* ctx, const InflatedMesh& im, const QuadCfg& cfg)
 {
+    HostScope hs_all(ctx, "plan_total");
     auto* P = new AssemblyPlan;
     try {
         cudaStream_t s = ctx->stream;
@@ -879,6 +880,7 @@ AssemblyPlan* assembly_plan_create(Ctx* ctx, const InflatedMesh& im, const QuadC
         if (nf == 0 || P->n == 0) return P;
         upload_rules(ctx, cfg);
         upload_geometry(ctx, m, P->G);
+        HostScope hs1(ctx, "plan_curls");
         const FacetCurls U = facet_curls(im);
         P->uptr.upload(U.ptr, s);
         P->udof.upload(U.dof, s);
@@ -952,6 +954,7 @@ AssemblyPlan* assembly_plan_create(Ctx* ctx, const InflatedMesh& im, const QuadC
             dof_ptr.push_back((int)dofs.size());
         }
         ent_ptr.push_back((int)ents.size());
+        HostScope hs2(ctx, "plan_tiles");
         // ---- tiles (fb >= gb); certainly-far tiles skip per-pair classification
         const double thr = cfg.near_threshold;
         std::vector<TileInfo> tiles, cand;
@@ -976,6 +979,7 @@ AssemblyPlan* assembly_plan_create(Ctx* ctx, const InflatedMesh& im, const QuadC
         P->cand.upload(cand, s);
         P->ntiles = (long long)tiles.size();
         P->ncand = (long long)cand.size();
+        HostScope hs3(ctx, "plan_singular");
         // ---- singular lists (host adjacency, deterministic order) and Sauter workspaces
         SingularLists S;
         singular_pairs(m, S);

@@ -84,6 +84,7 @@ struct Timers {
     cudaEvent_t get();
     void collect();  // synchronizes on the pending events
     void reset();
+    void add(const std::string& name, double ms);  // host-side interval
     ~Timers();
 };
 
@@ -94,6 +95,15 @@ struct Ctx {
     Timers timers;
     std::shared_ptr<void> pcg_ws;  // cached PCG workspace (linalg.cu)
     ~Ctx();
+};
+
+// RAII wall-clock scope for host-side work (recorded only when timing is on).
+struct HostScope {
+    Ctx* ctx;
+    const char* name;
+    double t0;
+    HostScope(Ctx* c, const char* n);
+    ~HostScope();
 };
 
 // RAII scope that records a named interval on the context stream when timing is on.

@@ -1,6 +1,7 @@
 // Context, timers and dense-matrix utilities.
 #include "common.cuh"
 #include <atomic>
+#include <chrono>
 
 #include "kernels.cuh"
 
@@ -48,6 +49,29 @@ void Timers::reset()
 {
     collect();
     totals.clear();
+}
+
+void Timers::add(const std::string& name, double ms)
+{
+    for (auto& t : totals)
+        if (t.first == name) {
+            t.second.first += ms;
+            t.second.second += 1;
+            return;
+        }
+    totals.push_back({name, {ms, 1}});
+}
+
+static double now_ms()
+{
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+HostScope::HostScope(Ctx* c, const char* n) : ctx(c), name(n), t0(now_ms()) {}
+
+HostScope::~HostScope()
+{
+    if (ctx && ctx->timers.enabled) ctx->timers.add(name, now_ms() - t0);
 }
 
 Timers::~Timers()

@@ -1,0 +1,37 @@
+// The reference's cmd_solve hot path (inc/experiments.hpp:130-145) written against
+// the C++ drop-in header screenbem/gpu.hpp.  Built and run by tests/test_cpp_dropin.py.
+//   g++ -std=c++17 -I include tools/cpp_dropin_example.cpp -L paper_2310_09204_b200/_lib -lscreenbem_b200
+#include <cstdio>
+
+#include "screenbem/gpu.hpp"
+
+namespace sb = screenbem::gpu;
+
+int main(int argc, char** argv)
+{
+    const int cfg = argc > 1 ? std::atoi(argv[1]) : 1;
+    try {
+        sb::Context ctx(0);
+        sb::MeshLevelPair pair = sb::make_config(cfg);
+        sb::InflatedMesh fine = sb::inflate(pair.fine());
+        sb::InflatedMesh coarse = sb::inflate(pair.coarse());
+        sb::GalerkinMatrix W = sb::assemble_W(ctx, fine);
+        const double g[3] = {0.0, 0.0, 1.0};
+        const std::vector<double> L = sb::assemble_rhs(ctx, fine, g);
+        sb::SchwarzPreconditioner P =
+            sb::build_preconditioner(ctx, W, sb::partition_dofs(pair, fine), sb::build_prolongation(pair, coarse, fine));
+        const sb::PcgReport rep = sb::pcg(ctx, W, &P, L, 1e-8);
+        std::printf("dofs %d iterations %d converged %d kappa %.4f\n", W.rows(), rep.iterations, (int)rep.converged,
+                    rep.kappa_estimate);
+        return rep.converged ? 0 : 3;
+    } catch (const screenbem::ValidationError& e) {
+        std::fprintf(stderr, "validation error: %s\n", e.what());
+        return 2;
+    } catch (const screenbem::NumericalError& e) {
+        std::fprintf(stderr, "numerical error: %s\n", e.what());
+        return 3;
+    } catch (const std::exception& e) {
+        std::fprintf(stderr, "error: %s\n", e.what());
+        return 4;
+    }
+}
