@@ -192,6 +192,7 @@ def run_ours(args):
     nf, n = pair.fine.nf, fine.n
     npairs = nf * (nf + 1) // 2
     plan = S.AssemblyPlan(fine, ctx=ctx)
+    plan_ms = {k: round(ctx.timer(k)[0], 3) for k in ("plan_total", "plan_curls", "plan_tiles", "plan_singular")}
 
     def step(W):
         W = plan.run(W)
@@ -318,6 +319,7 @@ def run_ours(args):
                     "precond_factor_bytes": prec.factor_bytes()},
             "time_to_solution_ms": step_ms,
             "phases_ms": {k: round(v, 4) for k, v in ms.items()},
+            "plan_build_ms_host": plan_ms,
             "assembly_stats": stats,
             "e2e": {"value": world * npairs / e2e_t, "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": 8 * n * n, "ms": e2e_t * 1e3,
