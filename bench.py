@@ -51,6 +51,17 @@ def dist_env():
         os.environ.get("LOCAL_RANK", "0"))
 
 
+def reduce_max(values, dist=None, device="cpu"):
+    """Element-wise max over ranks (the timing contract: max over ranks of device times).
+    NCCL on the GPU box (device cuda:LOCAL_RANK), gloo on CPU (tests/test_distributed.py)."""
+    if dist is None:
+        return list(values)
+    import torch
+    t = torch.tensor(list(values), dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return [float(v) for v in t]
+
+
 # --------------------------------------------------------------------------- clocks
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
@@ -226,11 +237,7 @@ def run_ours(args):
     ms = {k: (v[0] / v[1] if v[1] else 0.0) for k, v in tm.items()}
     t_asm = ms["assemble_W"] * 1e-3
     step_ms = ms["step"]
-    if dist:
-        import torch
-        t = torch.tensor([t_asm, step_ms], dtype=torch.float64, device=f"cuda:{local}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        t_asm, step_ms = float(t[0]), float(t[1])
+    t_asm, step_ms = reduce_max([t_asm, step_ms], dist, f"cuda:{local}")
     value = world * npairs / t_asm
     stats = W.stats
     # ---- dominant-kernel roofline (FP64 pipe): SURVEY.md §8d 20 flop per tensor-rule evaluation
@@ -284,11 +291,7 @@ def run_ours(args):
         e2e_times.append(ctx.timer("e2e")[0] * 1e-3)
         del W2, Wh
     e2e_t = min(e2e_times[1:]) if len(e2e_times) > 1 else e2e_times[0]
-    if dist:
-        import torch
-        t = torch.tensor([e2e_t], dtype=torch.float64, device=f"cuda:{local}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_t = float(t[0])
+    e2e_t = reduce_max([e2e_t], dist, f"cuda:{local}")[0]
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:

@@ -111,7 +111,7 @@ double time_kernel(K kern, int blocks, int threads, int iters, double* out)
     return ms * 1e-3;
 }
 
-int main()
+int main1()
 {
     double* d;
     cudaMalloc(&d, 64);
@@ -134,5 +134,68 @@ int main()
     printf("mixed 4 DMMA + 16 DFMA per iter: %.2f TFLOP/s total (%.3f ms; DFMA-only equiv %.3f ms, DMMA-only equiv %.3f ms)\n",
            fl3 / t3 / 1e12, t3 * 1e3, 2.0 * 16 * (double)iters * blocks * threads / (fl1 / t1) * 1e3,
            2.0 * 256 * 4 * (double)iters * blocks * (threads / 32) / (fl2 / t2) * 1e3);
+    return 0;
+}
+
+// ---- MUFU.RSQ64H throughput and alternative seeds (appended experiments)
+__global__ void k_mufu64(double* out, int iters)
+{
+    double a[8];
+    for (int q = 0; q < 8; ++q) a[q] = 1.0 + threadIdx.x * 1e-6 + q;
+    for (int i = 0; i < iters; ++i)
+#pragma unroll
+        for (int q = 0; q < 8; ++q) a[q] = rsq_seed(a[q]) + 1.0;
+    double s = 0;
+    for (int q = 0; q < 8; ++q) s += a[q];
+    if (s == 1.2345) out[0] = s;
+}
+__global__ void k_mufu32cvt(double* out, int iters)
+{
+    double a[8];
+    for (int q = 0; q < 8; ++q) a[q] = 1.0 + threadIdx.x * 1e-6 + q;
+    for (int i = 0; i < iters; ++i)
+#pragma unroll
+        for (int q = 0; q < 8; ++q) a[q] = (double)rsqrtf((float)a[q]) + 1.0;
+    double s = 0;
+    for (int q = 0; q < 8; ++q) s += a[q];
+    if (s == 1.2345) out[0] = s;
+}
+// full evaluation as in the far kernel: 4 FP64 for r2 + refined rsqrt + accumulate
+__global__ void k_eval(double* out, int iters)
+{
+    double acc[8], x[8];
+    for (int q = 0; q < 8; ++q) {
+        acc[q] = 0;
+        x[q] = 1.0 + threadIdx.x * 1e-6 + q;
+    }
+    const double y = 0.3, w = 0.7;
+    for (int i = 0; i < iters; ++i)
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const double r2 = fma(x[q], y, fma(x[q], y, fma(x[q], y, x[q] + 2.0)));
+            acc[q] = fma(w, rsq3(r2), acc[q]);
+        }
+    double s = 0;
+    for (int q = 0; q < 8; ++q) s += acc[q];
+    if (s == 1.2345) out[0] = s;
+}
+int main2()
+{
+    double* d;
+    cudaMalloc(&d, 64);
+    const int blocks = 148 * 8, threads = 256, iters = 2048;
+    const double n = 8.0 * iters * blocks * threads;
+    double t = time_kernel(k_mufu64, blocks, threads, iters, d);
+    printf("MUFU.RSQ64H (+DADD): %.2f /clk/SM at 1.965 GHz\n", n / t / 148 / 1.965e9);
+    t = time_kernel(k_mufu32cvt, blocks, threads, iters, d);
+    printf("F2F+MUFU.RSQ+F2F (+DADD): %.2f /clk/SM\n", n / t / 148 / 1.965e9);
+    t = time_kernel(k_eval, blocks, threads, iters, d);
+    printf("full eval (10 FP64 + MUFU): %.2f evals/clk/SM (FP64 bound would be 6.4)\n", n / t / 148 / 1.965e9);
+    return 0;
+}
+int main()
+{
+    main1();
+    main2();
     return 0;
 }
