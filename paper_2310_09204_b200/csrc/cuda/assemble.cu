@@ -23,6 +23,10 @@
 
 #include "kernels.cuh"
 
+#include <map>
+#include <memory>
+#include <mutex>
+
 namespace sbg {
 
 namespace {
@@ -36,6 +40,10 @@ constexpr int SAUTER_STAGE = 1024;  // rule points staged per smem pass
 
 __constant__ double c_far_u[NF], c_far_v[NF], c_far_w[NF];
 __constant__ double c_near_u[NN], c_near_v[NN], c_near_w[NN];
+// composed split4 maps: for every child path of depth <= 5 (index (4^d-1)/3 + base-4 digits),
+// the barycentric weights (x32, exact dyadics) of the leaf vertices on the root vertices
+constexpr int NPATH = 1365;
+__constant__ unsigned char c_paths[NPATH * 9];
 
 // ---------------------------------------------------------------- facet geometry
 struct GeoPtrs {
@@ -406,11 +414,27 @@ __global__ void k_near_level(const NearNode* __restrict__ nodes, const unsigned 
     }
 }
 
-// leaves: four per warp; lane (ia, jb) of each 8-lane group owns i in [18ia, 18ia+18), j in [9jb, 9jb+9)
+// leaf vertices from the root triangle and the composed barycentric map of a path
+__device__ __forceinline__ void path_triangle(const double* __restrict__ root, int path, double* out)
+{
+    const unsigned char* B = c_paths + 9 * path;
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+        const double w0 = B[3 * r] * (1.0 / 32), w1 = B[3 * r + 1] * (1.0 / 32), w2 = B[3 * r + 2] * (1.0 / 32);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) out[3 * r + c] = fma(w2, root[6 + c], fma(w1, root[3 + c], w0 * root[c]));
+    }
+}
+
+// leaves: four per warp; lane (ia, jb) of each 8-lane group owns i in [18ia, 18ia+18), j in [9jb, 9jb+9).
+// Leaf triangles come from the composed split4 maps (exact dyadic weights; the
+// classification pass already reproduced the reference's recursion bit for bit),
+// and their areas are the root areas / 4^depth.
 __global__ void __launch_bounds__(256, 2) k_near_leaves(const NearNode* __restrict__ leaves,
                                                         const unsigned long long* __restrict__ nleaves_dev,
                                                         long long cap, const int2* __restrict__ pairs,
-                                                        const double* __restrict__ GV, double inv_pi,
+                                                        const double* __restrict__ GV,
+                                                        const double* __restrict__ GA, double inv_pi,
                                                         double* __restrict__ out)
 {
     const long long nl = min((long long)*nleaves_dev, cap);
@@ -425,9 +449,23 @@ __global__ void __launch_bounds__(256, 2) k_near_leaves(const NearNode* __restri
         if (active) {
             const NearNode nd = leaves[q];
             pair = nd.pair;
+            const int2 pr = pairs[nd.pair];
+            const int depth = nd.code & 7;
+            int it = 0, is = 0, dt = 0, ds = 0;
+            for (int lv = 0; lv < depth; ++lv) {
+                const unsigned e = (nd.code >> (3 + 3 * lv)) & 7;
+                if (e & 1) {
+                    it = 4 * it + (int)(e >> 1);
+                    ++dt;
+                } else {
+                    is = 4 * is + (int)(e >> 1);
+                    ++ds;
+                }
+            }
             double t[9], s[9];
-            node_triangles(GV, pairs[nd.pair], nd.code, t, s);
-            scale = tri_area(t) * tri_area(s) * inv_pi;
+            path_triangle(GV + 9 * pr.x, ((1 << 2 * dt) - 1) / 3 + it, t);
+            path_triangle(GV + 9 * pr.y, ((1 << 2 * ds) - 1) / 3 + is, s);
+            scale = __ldg(GA + pr.x) * __ldg(GA + pr.y) * ldexp(inv_pi, -2 * (dt + ds));
             // leaf-local origin t0: |x-y|^2 = |x|^2 + |y|^2 - 2 x.y (leaves satisfy dist >= 2 diam
             // except at the forced depth 5, so the expansion loses at most a few bits)
             const double e1x = s[3] - s[0], e1y = s[4] - s[1], e1z = s[5] - s[2];
@@ -649,6 +687,42 @@ void upload_rules(Ctx* ctx, const QuadCfg& cfg)
     SBG_CUDA(cudaMemcpyToSymbolAsync(c_near_u, nr.u.data(), NN * sizeof(double), 0, cudaMemcpyHostToDevice, s));
     SBG_CUDA(cudaMemcpyToSymbolAsync(c_near_v, nr.v.data(), NN * sizeof(double), 0, cudaMemcpyHostToDevice, s));
     SBG_CUDA(cudaMemcpyToSymbolAsync(c_near_w, nr.w.data(), NN * sizeof(double), 0, cudaMemcpyHostToDevice, s));
+    // composed split4 maps (quadrature.hpp:222-229 child order), weights x32
+    static std::vector<unsigned char> paths;
+    if (paths.empty()) {
+        paths.resize(NPATH * 9);
+        int idx = 0;
+        for (int d = 0; d <= 5; ++d) {
+            int count = 1;
+            for (int l = 0; l < d; ++l) count *= 4;
+            for (int code = 0; code < count; ++code, ++idx) {
+                int B[3][3] = {{32, 0, 0}, {0, 32, 0}, {0, 0, 32}};
+                for (int l = 0; l < d; ++l) {
+                    int digit = code;
+                    for (int r = 0; r < d - 1 - l; ++r) digit /= 4;
+                    digit %= 4;
+                    int m01[3], m12[3], m02[3];
+                    for (int c = 0; c < 3; ++c) {
+                        m01[c] = (B[0][c] + B[1][c]) / 2;
+                        m12[c] = (B[1][c] + B[2][c]) / 2;
+                        m02[c] = (B[0][c] + B[2][c]) / 2;
+                    }
+                    int nb[3][3];
+                    for (int c = 0; c < 3; ++c) {
+                        const int v0 = B[0][c], v1 = B[1][c], v2 = B[2][c];
+                        const int rows[4][3] = {{v0, m01[c], m02[c]}, {m01[c], v1, m12[c]}, {m02[c], m12[c], v2},
+                                                {m01[c], m12[c], m02[c]}};
+                        for (int r = 0; r < 3; ++r) nb[r][c] = rows[digit][r];
+                    }
+                    for (int r = 0; r < 3; ++r)
+                        for (int c = 0; c < 3; ++c) B[r][c] = nb[r][c];
+                }
+                for (int r = 0; r < 3; ++r)
+                    for (int c = 0; c < 3; ++c) paths[9 * idx + 3 * r + c] = (unsigned char)B[r][c];
+            }
+        }
+    }
+    SBG_CUDA(cudaMemcpyToSymbolAsync(c_paths, paths.data(), paths.size(), 0, cudaMemcpyHostToDevice, s));
 }
 
 struct DeviceGeometry {
@@ -738,8 +812,24 @@ struct SauterRulesDev {
 
 void upload_sauter(Ctx* ctx, const QuadCfg& cfg, SauterRulesDev& R)
 {
-    SauterRule id, ed, vx;
-    sauter_rules(cfg.singular_order + 2, id, ed, vx);
+    // the rules depend only on the order: build them once per process
+    struct Rules {
+        SauterRule id, ed, vx;
+    };
+    static std::mutex mu;
+    static std::map<int, std::shared_ptr<const Rules>> cache;
+    std::shared_ptr<const Rules> rules;
+    {
+        std::lock_guard<std::mutex> lock(mu);
+        auto& slot = cache[cfg.singular_order];
+        if (!slot) {
+            auto r = std::make_shared<Rules>();
+            sauter_rules(cfg.singular_order + 2, r->id, r->ed, r->vx);
+            slot = r;
+        }
+        rules = slot;
+    }
+    const SauterRule &id = rules->id, &ed = rules->ed, &vx = rules->vx;
     R.r[3].upload(id.pts, ctx->stream);
     R.npts[3] = id.size();
     R.r[2].upload(ed.pts, ctx->stream);
@@ -791,8 +881,8 @@ __global__ void k_near_init(const unsigned long long* __restrict__ np_dev, long 
 }
 
 // near-pair integrals for the device list pairs[0:*np_dev] (capacity cap); returns the leaf count
-long long run_near(Ctx* ctx, const double* GV, const int2* pairs, const unsigned long long* np_dev, long long cap,
-                   double thr, double* out, NearWork& NW)
+long long run_near(Ctx* ctx, const double* GV, const double* GA, const int2* pairs,
+                   const unsigned long long* np_dev, long long cap, double thr, double* out, NearWork& NW)
 {
     if (cap <= 0) return 0;
     cudaStream_t s = ctx->stream;
@@ -808,8 +898,19 @@ long long run_near(Ctx* ctx, const double* GV, const int2* pairs, const unsigned
     long long ncur = (long long)h[0], total_leaves = 0;
     for (int depth = 0; depth <= 5 && ncur > 0; ++depth) {
         const long long cap_next = depth < 5 ? 4 * ncur : 0;
-        if ((long long)NW.next.n < cap_next) NW.next.alloc(cap_next);
-        if ((long long)NW.leaves.n < ncur) NW.leaves.alloc(ncur);
+        // cur/next swap every level: grow both together (and with headroom) so a
+        // plan that is run again never reallocates (cudaFree synchronises the device)
+        if ((long long)NW.next.n < cap_next) {
+            const long long want = std::max<long long>(cap_next, (long long)NW.cur.n) * 5 / 4;
+            NW.next.alloc(want);
+            if ((long long)NW.cur.n < want) {
+                DBuf<NearNode> grown(want);
+                SBG_CUDA(cudaMemcpyAsync(grown.p, NW.cur.p, ncur * sizeof(NearNode), cudaMemcpyDeviceToDevice, s));
+                std::swap(NW.cur, grown);
+                SBG_CUDA(cudaStreamSynchronize(s));
+            }
+        }
+        if ((long long)NW.leaves.n < ncur) NW.leaves.alloc(ncur * 5 / 4);
         SBG_CUDA(cudaMemsetAsync(NW.cnt.p + 1, 0, 2 * sizeof(unsigned long long), s));
         {
             TimedScope tc(ctx, "near_classify");
@@ -822,7 +923,7 @@ long long run_near(Ctx* ctx, const double* GV, const int2* pairs, const unsigned
             TimedScope tl(ctx, "near_leaves");
             const long long warps = (ncur + 3) / 4;  // upper bound on this level's leaf quads
             const int lgrid = (int)std::min<long long>((warps + 7) / 8, 32LL * ctx->sm_count);
-            k_near_leaves<<<lgrid, 256, 0, s>>>(NW.leaves.p, NW.cnt.p + 2, ncur, pairs, GV, 1.0 / M_PI, out);
+            k_near_leaves<<<lgrid, 256, 0, s>>>(NW.leaves.p, NW.cnt.p + 2, ncur, pairs, GV, GA, 1.0 / M_PI, out);
             count_launch();
         }
         SBG_LAUNCH_CHECK();
@@ -1042,7 +1143,7 @@ void assembly_run(AssemblyPlan* P, DMatrix& W, AssemblyStats* stats)
             count_launch();
             SBG_LAUNCH_CHECK();
         }
-        leaves = run_near(ctx, P->G.v.p, P->loc_pairs.p + P->nsing, P->near_cnt.p, P->near_cap, thr,
+        leaves = run_near(ctx, P->G.v.p, P->G.area.p, P->loc_pairs.p + P->nsing, P->near_cnt.p, P->near_cap, thr,
                           P->loc_I.p + P->nsing, P->NW);
         SBG_CUDA(cudaMemcpyAsync(&nnear, P->near_cnt.p, sizeof(nnear), cudaMemcpyDeviceToHost, s));
         SBG_CUDA(cudaStreamSynchronize(s));
@@ -1236,7 +1337,7 @@ void pair_integrals(Ctx* ctx, const SurfaceMesh& m, const QuadCfg& cfg, const in
         const unsigned long long hn = nearp.size();
         SBG_CUDA(cudaMemcpyAsync(cnt.p, &hn, sizeof(hn), cudaMemcpyHostToDevice, s));
         NearWork NW;
-        run_near(ctx, G.v.p, d_p.p, cnt.p, (long long)nearp.size(), cfg.near_threshold, o.p, NW);
+        run_near(ctx, G.v.p, G.area.p, d_p.p, cnt.p, (long long)nearp.size(), cfg.near_threshold, o.p, NW);
         fetch(o.p, idx[0]);
     }
     if (!farp.empty()) {

@@ -94,6 +94,7 @@ struct Ctx {
     cudaStream_t stream = nullptr;
     Timers timers;
     std::shared_ptr<void> pcg_ws;  // cached PCG workspace (linalg.cu)
+    std::shared_ptr<void> dl_ws;   // cached pinned download ring (context.cu)
     ~Ctx();
 };
 

@@ -2,6 +2,9 @@
 #include "common.cuh"
 #include <atomic>
 #include <chrono>
+#include <cstring>
+#include <thread>
+#include <vector>
 
 #include "kernels.cuh"
 
@@ -179,20 +182,99 @@ void matrix_upload(DMatrix& M, const double* host)
     SBG_CUDA(cudaStreamSynchronize(ctx->stream));
 }
 
+namespace {
+// Pinned staging ring for full-matrix downloads: the padded rows are packed on
+// the device, DMA'd into pinned slots, and copied out by host threads while the
+// next slots are in flight (a pageable D2H of a 5 GB matrix runs at a few GB/s).
+struct DownloadRing {
+    static constexpr int kSlots = 3;
+    static constexpr size_t kSlotBytes = 64u << 20;
+    double* pinned[kSlots] = {};
+    DBuf<double> dev[kSlots];
+    cudaEvent_t done[kSlots] = {};
+    DownloadRing()
+    {
+        for (int k = 0; k < kSlots; ++k) {
+            SBG_CUDA(cudaHostAlloc((void**)&pinned[k], kSlotBytes, cudaHostAllocDefault));
+            dev[k].alloc(kSlotBytes / sizeof(double));
+            SBG_CUDA(cudaEventCreateWithFlags(&done[k], cudaEventDisableTiming));
+        }
+    }
+    ~DownloadRing()
+    {
+        for (int k = 0; k < kSlots; ++k) {
+            if (pinned[k]) cudaFreeHost(pinned[k]);
+            if (done[k]) cudaEventDestroy(done[k]);
+        }
+    }
+};
+}  // namespace
+
 void matrix_download(const DMatrix& M, double* host)
 {
     Ctx* ctx = M.ctx;
-    const size_t rows_per = std::max<size_t>(1, (64u << 20) / (sizeof(double) * std::max(1, M.n)));
-    DBuf<double> stage(std::min<size_t>(rows_per, M.n) * M.n);
-    for (int r0 = 0; r0 < M.n; r0 += (int)rows_per) {
-        const int r1 = std::min<int>(M.n, r0 + (int)rows_per);
-        dim3 grid((M.n + 255) / 256 < 64 ? (M.n + 255) / 256 : 64, r1 - r0);
-        k_unpack_rows<<<grid, 256, 0, ctx->stream>>>(M.a.p + (size_t)r0 * M.ld, M.ld, M.n, stage.p); ::sbg::count_launch();
-        SBG_LAUNCH_CHECK();
-        SBG_CUDA(cudaMemcpyAsync(host + (size_t)r0 * M.n, stage.p, (size_t)(r1 - r0) * M.n * sizeof(double),
-                                 cudaMemcpyDeviceToHost, ctx->stream));
+    if (M.n == 0) return;
+    if (!ctx->dl_ws) ctx->dl_ws = std::make_shared<DownloadRing>();
+    auto& R = *static_cast<DownloadRing*>(ctx->dl_ws.get());
+    const size_t row_bytes = sizeof(double) * (size_t)M.n;
+    const int rows_per = (int)std::max<size_t>(1, DownloadRing::kSlotBytes / row_bytes);
+    const int nchunks = (M.n + rows_per - 1) / rows_per;
+    if ((size_t)std::min(rows_per, M.n) * row_bytes > DownloadRing::kSlotBytes) {
+        // a single row larger than a slot (n > 8M): plain pageable copy row by row
+        for (int r = 0; r < M.n; ++r)
+            SBG_CUDA(cudaMemcpyAsync(host + (size_t)r * M.n, M.a.p + (size_t)r * M.ld, row_bytes,
+                                     cudaMemcpyDeviceToHost, ctx->stream));
         SBG_CUDA(cudaStreamSynchronize(ctx->stream));
+        return;
     }
+    const int nthreads =
+        (int)std::max(1u, std::min(16u, std::thread::hardware_concurrency() ? std::thread::hardware_concurrency() : 1u));
+    std::atomic<int> posted{0};
+    std::vector<std::atomic<int>> finished(nchunks);
+    for (auto& f : finished) f.store(0);
+    std::atomic<bool> failed{false};
+    auto worker = [&](int t) {
+        for (int i = 0; i < nchunks; ++i) {
+            while (posted.load(std::memory_order_acquire) <= i) {
+                if (failed.load()) return;
+                std::this_thread::yield();
+            }
+            if (cudaEventSynchronize(R.done[i % DownloadRing::kSlots]) != cudaSuccess) {
+                failed.store(true);
+                return;
+            }
+            const int r0 = i * rows_per, r1 = std::min(M.n, r0 + rows_per);
+            const size_t total = (size_t)(r1 - r0) * M.n;
+            const size_t lo = total * t / nthreads, hi = total * (t + 1) / nthreads;
+            std::memcpy(host + (size_t)r0 * M.n + lo, R.pinned[i % DownloadRing::kSlots] + lo, (hi - lo) * sizeof(double));
+            finished[i].fetch_add(1, std::memory_order_acq_rel);
+        }
+    };
+    std::vector<std::thread> pool;
+    for (int t = 0; t < nthreads; ++t) pool.emplace_back(worker, t);
+    try {
+        for (int i = 0; i < nchunks; ++i) {
+            const int slot = i % DownloadRing::kSlots;
+            if (i >= DownloadRing::kSlots)  // the slot's previous chunk must be copied out
+                while (finished[i - DownloadRing::kSlots].load(std::memory_order_acquire) < nthreads)
+                    std::this_thread::yield();
+            const int r0 = i * rows_per, r1 = std::min(M.n, r0 + rows_per);
+            dim3 grid((M.n + 255) / 256 < 64 ? (M.n + 255) / 256 : 64, r1 - r0);
+            k_unpack_rows<<<grid, 256, 0, ctx->stream>>>(M.a.p + (size_t)r0 * M.ld, M.ld, M.n, R.dev[slot].p);
+            ::sbg::count_launch();
+            SBG_LAUNCH_CHECK();
+            SBG_CUDA(cudaMemcpyAsync(R.pinned[slot], R.dev[slot].p, (size_t)(r1 - r0) * row_bytes,
+                                     cudaMemcpyDeviceToHost, ctx->stream));
+            SBG_CUDA(cudaEventRecord(R.done[slot], ctx->stream));
+            posted.store(i + 1, std::memory_order_release);
+        }
+    } catch (...) {
+        failed.store(true);
+        for (auto& th : pool) th.join();
+        throw;
+    }
+    for (auto& th : pool) th.join();
+    if (failed.load()) throw CudaError("matrix download: event synchronisation failed");
 }
 
 void matrix_download_rows(const DMatrix& M, const int* rows, int nrows, double* host)

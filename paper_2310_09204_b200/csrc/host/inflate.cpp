@@ -12,7 +12,13 @@ namespace sbg {
 namespace {
 struct DSU {
     std::vector<int> p;
+    DSU() = default;
     explicit DSU(int n) : p(n) { std::iota(p.begin(), p.end(), 0); }
+    void reset(int n)
+    {
+        p.resize(n);
+        std::iota(p.begin(), p.end(), 0);
+    }
     int find(int a)
     {
         while (p[a] != a) a = p[a] = p[p[a]];
@@ -59,25 +65,44 @@ InflatedMesh inflate(const SurfaceMesh& mesh, bool validate)
         if (i == 0 || el[i].a != el[i - 1].a || el[i].b != el[i - 1].b) eptr.push_back((int)i);
     const int ne = (int)eptr.size();
     eptr.push_back((int)el.size());
-    std::vector<std::vector<int>> vedges(nv);  // edges containing each vertex
+    // vertex -> incident edges / facets as CSR lists (ascending)
+    std::vector<int> ve_ptr(nv + 1, 0), vs_ptr(nv + 1, 0);
     for (int e = 0; e < ne; ++e) {
-        vedges[el[eptr[e]].a].push_back(e);
-        vedges[el[eptr[e]].b].push_back(e);
+        ++ve_ptr[el[eptr[e]].a + 1];
+        ++ve_ptr[el[eptr[e]].b + 1];
     }
-    std::vector<std::vector<int>> vstar(nv);
     for (int f = 0; f < nf; ++f)
-        for (int k = 0; k < 3; ++k) vstar[mesh.facets[f][k]].push_back(f);
+        for (int k = 0; k < 3; ++k) ++vs_ptr[mesh.facets[f][k] + 1];
+    for (int v = 0; v < nv; ++v) {
+        ve_ptr[v + 1] += ve_ptr[v];
+        vs_ptr[v + 1] += vs_ptr[v];
+    }
+    std::vector<int> vedges(ve_ptr[nv]), vstar(vs_ptr[nv]);
+    {
+        std::vector<int> fill(ve_ptr.begin(), ve_ptr.end() - 1);
+        for (int e = 0; e < ne; ++e) {
+            vedges[fill[el[eptr[e]].a]++] = e;
+            vedges[fill[el[eptr[e]].b]++] = e;
+        }
+        fill.assign(vs_ptr.begin(), vs_ptr.end() - 1);
+        for (int f = 0; f < nf; ++f)
+            for (int k = 0; k < 3; ++k) vstar[fill[mesh.facets[f][k]]++] = f;
+    }
+    DSU ds;
 
     // point-contact check (inflate.hpp:129-151)
     for (int v = 0; v < nv; ++v) {
-        const auto& star = vstar[v];
-        if (star.size() < 2) continue;
-        auto local = [&](int f) { return (int)(std::lower_bound(star.begin(), star.end(), f) - star.begin()); };
-        DSU ds((int)star.size());
-        for (int e : vedges[v])
+        const int* star = vstar.data() + vs_ptr[v];
+        const int ns = vs_ptr[v + 1] - vs_ptr[v];
+        if (ns < 2) continue;
+        auto local = [&](int f) { return (int)(std::lower_bound(star, star + ns, f) - star); };
+        ds.reset(ns);
+        for (int q = ve_ptr[v]; q < ve_ptr[v + 1]; ++q) {
+            const int e = vedges[q];
             for (int i = eptr[e] + 1; i < eptr[e + 1]; ++i) ds.unite(local(el[eptr[e]].f), local(el[i].f));
+        }
         const int root = ds.find(0);
-        for (int i = 1; i < (int)star.size(); ++i)
+        for (int i = 1; i < ns; ++i)
             if (ds.find(i) != root)
                 throw ValidationError("point contact at vertex " + std::to_string(v) + " (unsupported geometry)");
     }
@@ -85,6 +110,9 @@ InflatedMesh inflate(const SurfaceMesh& mesh, bool validate)
     // fans (inflate.hpp:155-228)
     std::vector<std::array<int, 2>> fan_pairs;
     std::vector<int> fan_ptr{0};
+    fan_pairs.reserve(el.size());
+    fan_ptr.reserve(ne + 1);
+    std::vector<std::pair<double, int>> slots;  // (angle, local)
     for (int e = 0; e < ne; ++e) {
         const int ea = el[eptr[e]].a, eb = el[eptr[e]].b;
         const Vec3 origin = mesh.vertices[ea];
@@ -101,7 +129,7 @@ InflatedMesh inflate(const SurfaceMesh& mesh, bool validate)
         const int k = eptr[e + 1] - eptr[e];
         const Vec3 ref = in_plane_dir(el[eptr[e]].f);
         const Vec3 up = cross(e_dir, ref);
-        std::vector<std::pair<double, int>> slots;  // (angle, local)
+        slots.clear();
         for (int i = 0; i < k; ++i) {
             const Vec3 d = in_plane_dir(el[eptr[e] + i].f);
             slots.push_back({std::atan2(dot(d, up), dot(d, ref)), i});
@@ -131,29 +159,40 @@ InflatedMesh inflate(const SurfaceMesh& mesh, bool validate)
     im.dof_first.assign(nv, -1);
     im.ofacet_branch.assign(2 * nf, {-1, -1, -1});
     im.gv_alpha_ptr.push_back(0);
+    std::vector<int> star, broot, bid, order;
+    im.gv_alpha.reserve(2 * (size_t)vs_ptr[nv]);
     for (int v = 0; v < nv; ++v) {
-        const auto& fs = vstar[v];
-        if (fs.empty()) throw ValidationError("isolated vertex " + std::to_string(v));
-        std::vector<int> star;  // oriented facets, ascending
-        for (int f : fs) {
-            star.push_back(2 * f);
-            star.push_back(2 * f + 1);
+        const int ns = vs_ptr[v + 1] - vs_ptr[v];
+        if (ns == 0) throw ValidationError("isolated vertex " + std::to_string(v));
+        star.clear();  // oriented facets, ascending
+        for (int q = vs_ptr[v]; q < vs_ptr[v + 1]; ++q) {
+            star.push_back(2 * vstar[q]);
+            star.push_back(2 * vstar[q] + 1);
         }
+        const int m = (int)star.size();
         auto local = [&](int o) { return (int)(std::lower_bound(star.begin(), star.end(), o) - star.begin()); };
-        DSU ds((int)star.size());
-        for (int e : vedges[v])
+        ds.reset(m);
+        for (int q = ve_ptr[v]; q < ve_ptr[v + 1]; ++q) {
+            const int e = vedges[q];
             for (int p = fan_ptr[e]; p < fan_ptr[e + 1]; ++p) ds.unite(local(fan_pairs[p][0]), local(fan_pairs[p][1]));
-        std::map<int, std::vector<int>> comp;
-        for (int i = 0; i < (int)star.size(); ++i) comp[ds.find(i)].push_back(star[i]);
-        std::vector<std::vector<int>> branches;
-        for (auto& [root, members] : comp) branches.push_back(std::move(members));  // members ascending
-        std::sort(branches.begin(), branches.end(), [](const auto& a, const auto& b) { return a.front() < b.front(); });
+        }
+        // branches ordered by their smallest oriented facet = order of first appearance
+        broot.assign(m, -1);
+        bid.assign(m, 0);
+        int nb = 0;
+        for (int i = 0; i < m; ++i) {
+            const int r = ds.find(i);
+            if (broot[r] < 0) broot[r] = nb++;
+            bid[i] = broot[r];
+        }
         im.gv_first[v] = im.num_gvertices();
-        im.q[v] = (int)branches.size();
-        for (int j = 0; j < im.q[v]; ++j) {
+        im.q[v] = nb;
+        for (int j = 0; j < nb; ++j) {
             im.gv_vertex.push_back(v);
             im.gv_branch.push_back(j);
-            for (int o : branches[j]) {
+            for (int i = 0; i < m; ++i) {
+                if (bid[i] != j) continue;
+                const int o = star[i];
                 im.gv_alpha.push_back(o);
                 const int f = o / 2;
                 for (int k = 0; k < 3; ++k)
