@@ -234,7 +234,9 @@ def run_ours(args):
     tm = {k: ctx.timer(k) for k in ("step", "assemble_W", "far_tiles", "near", "near_leaves", "sauter", "classify",
                                      "local_scatter", "mirror", "near_classify", "build_preconditioner", "cholesky",
                                      "block_inverse", "coarse_galerkin", "pcg", "gemv_f64", "precond_apply")}
-    ms = {k: (v[0] / v[1] if v[1] else 0.0) for k, v in tm.items()}
+    # per-step totals (a phase may run several launches per step, e.g. one near level each)
+    ms = {k: v[0] / args.steps for k, v in tm.items()}
+    launches_per_step = {k: v[1] / args.steps for k, v in tm.items()}
     t_asm = ms["assemble_W"] * 1e-3
     step_ms = ms["step"]
     t_asm, step_ms = reduce_max([t_asm, step_ms], dist, f"cuda:{local}")
@@ -242,8 +244,7 @@ def run_ours(args):
     stats = W.stats
     # ---- dominant-kernel roofline (FP64 pipe): SURVEY.md §8d 20 flop per tensor-rule evaluation
     fp64_peak = S.fp64_peak_tflops(ctx)
-    far_ms = tm["far_tiles"][0] / max(tm["far_tiles"][1], 1)
-    near_ms = tm["near_leaves"][0] / max(tm["near_leaves"][1], 1)
+    far_ms, near_ms = ms["far_tiles"], ms["near_leaves"]
     far_flop = 20.0 * 256 * stats["far_pairs"]
     near_flop = 20.0 * 1296 * stats["near_leaves"]
     dom = ("far_tiles", far_flop, far_ms) if far_ms >= near_ms else ("near_leaves", near_flop, near_ms)
@@ -311,7 +312,12 @@ def run_ours(args):
             "roofline": {"bound": "fp64", "kernel": dom[0], "achieved": achieved, "peak": fp64_peak,
                          "unit": "TFLOP/s", "frac": achieved / fp64_peak if fp64_peak else None, "traffic": None,
                          "peak_source": "DFMA loop measured by bench.py on this GPU (MEASURED_PEAKS.json has no fp64)",
-                         "flop_convention": "20 flop per tensor-rule kernel evaluation (SURVEY.md §8d)"},
+                         "flop_convention": "20 flop per tensor-rule kernel evaluation (SURVEY.md §8d)",
+                         "ms_per_step": dom[2], "launches_per_step": launches_per_step[dom[0]],
+                         "achieved_other": {"kernel": ("near_leaves" if dom[0] == "far_tiles" else "far_tiles"),
+                                            "tflops": (near_flop / (near_ms * 1e-3) / 1e12 if dom[0] == "far_tiles"
+                                                       else far_flop / (far_ms * 1e-3) / 1e12)
+                                            if min(far_ms, near_ms) > 0 else None}},
             "roofline_matvec": {"bound": "hbm", "kernel": "gemv_f64", "achieved": matvec_gbs, "peak": hbm_peak,
                                 "unit": "GB/s", "frac": matvec_gbs / hbm_peak, "traffic": None,
                                 "bytes_per_launch": matvec_bytes, "us_per_launch": matvec_s * 1e6,
@@ -322,6 +328,7 @@ def run_ours(args):
                     "precond_factor_bytes": prec.factor_bytes()},
             "time_to_solution_ms": step_ms,
             "phases_ms": {k: round(v, 4) for k, v in ms.items()},
+            "phase_launches_per_step": launches_per_step,
             "plan_build_ms_host": plan_ms,
             "assembly_stats": stats,
             "e2e": {"value": world * npairs / e2e_t, "unit": UNIT, "h2d_bytes_per_step": h2d,

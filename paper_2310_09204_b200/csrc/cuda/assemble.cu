@@ -186,23 +186,26 @@ __device__ __forceinline__ double4 far_ypoint(const double* s, const double* o, 
     return make_double4(y0, y1, y2, fma(y0, y0, fma(y1, y1, y2 * y2)));
 }
 
-// sum_j w_j sum_{q in pass} w_{4 pass + q} / |x_q - y_j|  (16 y-points x 4 x-points)
+// sum_{q in pass} w_{4 pass + q} sum_j w_j / |x_q - y_j|  (16 y-points x 4 x-points); one
+// accumulator per x point, so the four evaluations per y point are independent chains
 __device__ __forceinline__ double far_pass_sum(const XPts& X, const double4* __restrict__ Y, int pass)
 {
-    double acc = 0.0;
+    double a[FAR_PASS];
+#pragma unroll
+    for (int q = 0; q < FAR_PASS; ++q) a[q] = 0.0;
 #pragma unroll 2
     for (int j = 0; j < NF; ++j) {
         const double4 y = Y[j];
-        double in0 = 0.0, in1 = 0.0;
+        const double wj = c_far_w[j];
 #pragma unroll
-        for (int q = 0; q < FAR_PASS; q += 2) {
-            const double ra = fma(X.m2x[q], y.x, fma(X.m2y[q], y.y, fma(X.m2z[q], y.z, X.x2[q] + y.w)));
-            const double rb = fma(X.m2x[q + 1], y.x, fma(X.m2y[q + 1], y.y, fma(X.m2z[q + 1], y.z, X.x2[q + 1] + y.w)));
-            in0 = fma(c_far_w[FAR_PASS * pass + q], rsqrt_fast(ra), in0);
-            in1 = fma(c_far_w[FAR_PASS * pass + q + 1], rsqrt_fast(rb), in1);
+        for (int q = 0; q < FAR_PASS; ++q) {
+            const double r2 = fma(X.m2x[q], y.x, fma(X.m2y[q], y.y, fma(X.m2z[q], y.z, X.x2[q] + y.w)));
+            a[q] = fma(wj, rsqrt_fast(r2), a[q]);
         }
-        acc = fma(c_far_w[j], in0 + in1, acc);
     }
+    double acc = 0.0;
+#pragma unroll
+    for (int q = 0; q < FAR_PASS; ++q) acc = fma(c_far_w[FAR_PASS * pass + q], a[q], acc);
     return acc;
 }
 
@@ -429,23 +432,34 @@ __device__ __forceinline__ void path_triangle(const double* __restrict__ root, i
 // leaves: four per warp; lane (ia, jb) of each 8-lane group owns i in [18ia, 18ia+18), j in [9jb, 9jb+9).
 // Leaf triangles come from the composed split4 maps (exact dyadic weights; the
 // classification pass already reproduced the reference's recursion bit for bit),
-// and their areas are the root areas / 4^depth.
-__global__ void __launch_bounds__(256, 2) k_near_leaves(const NearNode* __restrict__ leaves,
+// and their areas are the root areas / 4^depth.  Distances use the expansion
+// |x-y|^2 = |x|^2 + |y|^2 - 2 x.y in leaf-local coordinates (origin t0): the
+// 36 x points of each leaf (x, |x|^2) are staged once in shared memory by the
+// leaf's 8 lanes, the y side keeps (-2y, |y|^2) in registers, so one
+// evaluation is 3 FMA + 1 ADD for r^2, MUFU.RSQ64H + 4 FP64 for the refined
+// 1/r and 1 FMA to accumulate.
+constexpr int NEAR_LEAF_THREADS = 256;
+__global__ void __launch_bounds__(NEAR_LEAF_THREADS, 2) k_near_leaves(const NearNode* __restrict__ leaves,
                                                         const unsigned long long* __restrict__ nleaves_dev,
                                                         long long cap, const int2* __restrict__ pairs,
                                                         const double* __restrict__ GV,
                                                         const double* __restrict__ GA, double inv_pi,
                                                         double* __restrict__ out)
 {
+    __shared__ double4 xs[NEAR_LEAF_THREADS / 32][4][NN];
+    __shared__ double wsm[NN];
+    if (threadIdx.x < NN) wsm[threadIdx.x] = c_near_w[threadIdx.x];
+    __syncthreads();
     const long long nl = min((long long)*nleaves_dev, cap);
-    const int lane = threadIdx.x & 31;
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int h = lane >> 3, l8 = lane & 7, ia = l8 >> 2, jb = l8 & 3;
     const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
-    for (long long w = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); 4 * w < nl; w += warps) {
+    for (long long w = (long long)blockIdx.x * (blockDim.x >> 5) + wib; 4 * w < nl; w += warps) {
         const long long q = 4 * w + h;
         const bool active = q < nl;
         double acc = 0.0, scale = 0.0;
         int pair = 0;
+        double Yx[9], Yy[9], Yz[9], y2[9];
         if (active) {
             const NearNode nd = leaves[q];
             pair = nd.pair;
@@ -466,42 +480,51 @@ __global__ void __launch_bounds__(256, 2) k_near_leaves(const NearNode* __restri
             path_triangle(GV + 9 * pr.x, ((1 << 2 * dt) - 1) / 3 + it, t);
             path_triangle(GV + 9 * pr.y, ((1 << 2 * ds) - 1) / 3 + is, s);
             scale = __ldg(GA + pr.x) * __ldg(GA + pr.y) * ldexp(inv_pi, -2 * (dt + ds));
-            // leaf-local origin t0: |x-y|^2 = |x|^2 + |y|^2 - 2 x.y (leaves satisfy dist >= 2 diam
-            // except at the forced depth 5, so the expansion loses at most a few bits)
             const double e1x = s[3] - s[0], e1y = s[4] - s[1], e1z = s[5] - s[2];
             const double e2x = s[6] - s[0], e2y = s[7] - s[1], e2z = s[8] - s[2];
             const double bx = s[0] - t[0], by = s[1] - t[1], bz = s[2] - t[2];
-            double yx[9], yy[9], yz[9], y2[9];
 #pragma unroll
             for (int k = 0; k < 9; ++k) {
                 const int j = 9 * jb + k;
-                yx[k] = fma(c_near_v[j], e2x, fma(c_near_u[j], e1x, bx));
-                yy[k] = fma(c_near_v[j], e2y, fma(c_near_u[j], e1y, by));
-                yz[k] = fma(c_near_v[j], e2z, fma(c_near_u[j], e1z, bz));
-                y2[k] = fma(yx[k], yx[k], fma(yy[k], yy[k], yz[k] * yz[k]));
+                const double yx = fma(c_near_v[j], e2x, fma(c_near_u[j], e1x, bx));
+                const double yy = fma(c_near_v[j], e2y, fma(c_near_u[j], e1y, by));
+                const double yz = fma(c_near_v[j], e2z, fma(c_near_u[j], e1z, bz));
+                y2[k] = fma(yx, yx, fma(yy, yy, yz * yz));
+                Yx[k] = -2.0 * yx;
+                Yy[k] = -2.0 * yy;
+                Yz[k] = -2.0 * yz;
             }
             const double f1x = t[3] - t[0], f1y = t[4] - t[1], f1z = t[5] - t[2];
             const double f2x = t[6] - t[0], f2y = t[7] - t[1], f2z = t[8] - t[2];
-#pragma unroll 1
-            for (int p = 0; p < 18; ++p) {
-                const int i = 18 * ia + p;
+            for (int i = l8; i < NN; i += 8) {
                 const double xx = fma(c_near_v[i], f2x, c_near_u[i] * f1x);
                 const double xy = fma(c_near_v[i], f2y, c_near_u[i] * f1y);
                 const double xz = fma(c_near_v[i], f2z, c_near_u[i] * f1z);
-                const double x2 = fma(xx, xx, fma(xy, xy, xz * xz));
-                const double mx = -2.0 * xx, my = -2.0 * xy, mz = -2.0 * xz;
-                double in0 = 0.0, in1 = 0.0;
-#pragma unroll
-                for (int k = 0; k < 9; ++k) {
-                    const double r2 = fma(mx, yx[k], fma(my, yy[k], fma(mz, yz[k], x2 + y2[k])));
-                    if (k & 1)
-                        in1 = fma(c_near_w[9 * jb + k], rsqrt_fast(r2), in1);
-                    else
-                        in0 = fma(c_near_w[9 * jb + k], rsqrt_fast(r2), in0);
-                }
-                acc = fma(c_near_w[i], in0 + in1, acc);
+                xs[wib][h][i] = make_double4(xx, xy, xz, fma(xx, xx, fma(xy, xy, xz * xz)));
             }
         }
+        __syncwarp();
+        if (active) {
+            // one accumulator per y point: nine independent FMA chains per x point
+            const double4* X = xs[wib][h] + 18 * ia;
+            const double* WX = wsm + 18 * ia;
+            double a[9];
+#pragma unroll
+            for (int k = 0; k < 9; ++k) a[k] = 0.0;
+#pragma unroll 2
+            for (int p = 0; p < 18; ++p) {
+                const double4 x = X[p];
+                const double wx = WX[p];
+#pragma unroll
+                for (int k = 0; k < 9; ++k) {
+                    const double r2 = fma(x.x, Yx[k], fma(x.y, Yy[k], fma(x.z, Yz[k], x.w + y2[k])));
+                    a[k] = fma(wx, rsqrt_fast(r2), a[k]);
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < 9; ++k) acc = fma(c_near_w[9 * jb + k], a[k], acc);
+        }
+        __syncwarp();
         for (int o = 4; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
         if (active && l8 == 0) atomicAdd(out + pair, acc * scale);
     }
@@ -923,7 +946,7 @@ long long run_near(Ctx* ctx, const double* GV, const double* GA, const int2* pai
             TimedScope tl(ctx, "near_leaves");
             const long long warps = (ncur + 3) / 4;  // upper bound on this level's leaf quads
             const int lgrid = (int)std::min<long long>((warps + 7) / 8, 32LL * ctx->sm_count);
-            k_near_leaves<<<lgrid, 256, 0, s>>>(NW.leaves.p, NW.cnt.p + 2, ncur, pairs, GV, GA, 1.0 / M_PI, out);
+            k_near_leaves<<<lgrid, NEAR_LEAF_THREADS, 0, s>>>(NW.leaves.p, NW.cnt.p + 2, ncur, pairs, GV, GA, 1.0 / M_PI, out);
             count_launch();
         }
         SBG_LAUNCH_CHECK();
