@@ -429,37 +429,41 @@ __device__ __forceinline__ void path_triangle(const double* __restrict__ root, i
     }
 }
 
-// leaves: four per warp; lane (ia, jb) of each 8-lane group owns i in [18ia, 18ia+18), j in [9jb, 9jb+9).
-// Leaf triangles come from the composed split4 maps (exact dyadic weights; the
-// classification pass already reproduced the reference's recursion bit for bit),
-// and their areas are the root areas / 4^depth.  Distances use the expansion
-// |x-y|^2 = |x|^2 + |y|^2 - 2 x.y in leaf-local coordinates (origin t0): the
-// 36 x points of each leaf (x, |x|^2) are staged once in shared memory by the
-// leaf's 8 lanes, the y side keeps (-2y, |y|^2) in registers, so one
-// evaluation is 3 FMA + 1 ADD for r^2, MUFU.RSQ64H + 4 FP64 for the refined
-// 1/r and 1 FMA to accumulate.
+// Leaves: eight per warp, four lanes per leaf.  Leaf triangles come from the
+// composed split4 maps (exact dyadic weights; the classification pass already
+// reproduced the reference's recursion bit for bit), and their areas are the
+// root areas / 4^depth.  Distances use the expansion |x-y|^2 = |x|^2 + |y|^2 -
+// 2 x.y in leaf-local coordinates (origin t0).  The leaf's 36 y points (y,
+// |y|^2) are staged in shared memory; lane xg of the leaf owns the x points
+// x groups of four points (three passes, below) held in registers as (-2x,
+// |x|^2), with one accumulator per x point: an evaluation is 3 FMA + 1 ADD for
+// r^2, MUFU.RSQ64H + 4 FP64 for the refined 1/r and 1 FMA, and the four
+// evaluations per loaded y point are independent chains (tools/micro_eval.cu:
+// this 4-point block is the fastest register blocking of the pattern).
 constexpr int NEAR_LEAF_THREADS = 256;
+constexpr int NEAR_XP = 4;  // x points per pass (register block)
+constexpr int NEAR_LEAF_WARPS = NEAR_LEAF_THREADS / 32;
+constexpr size_t NEAR_LEAF_SMEM = (size_t)NEAR_LEAF_WARPS * 8 * NN * sizeof(double4);
 __global__ void __launch_bounds__(NEAR_LEAF_THREADS, 2) k_near_leaves(const NearNode* __restrict__ leaves,
-                                                        const unsigned long long* __restrict__ nleaves_dev,
-                                                        long long cap, const int2* __restrict__ pairs,
-                                                        const double* __restrict__ GV,
-                                                        const double* __restrict__ GA, double inv_pi,
-                                                        double* __restrict__ out)
+                                                                       const unsigned long long* __restrict__ nleaves_dev,
+                                                                       long long cap, const int2* __restrict__ pairs,
+                                                                       const double* __restrict__ GV,
+                                                                       const double* __restrict__ GA, double inv_pi,
+                                                                       double* __restrict__ out)
 {
-    __shared__ double4 xs[NEAR_LEAF_THREADS / 32][4][NN];
-    __shared__ double wsm[NN];
-    if (threadIdx.x < NN) wsm[threadIdx.x] = c_near_w[threadIdx.x];
-    __syncthreads();
-    const long long nl = min((long long)*nleaves_dev, cap);
+    extern __shared__ __align__(16) unsigned char near_smem[];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    const int h = lane >> 3, l8 = lane & 7, ia = l8 >> 2, jb = l8 & 3;
-    const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
-    for (long long w = (long long)blockIdx.x * (blockDim.x >> 5) + wib; 4 * w < nl; w += warps) {
-        const long long q = 4 * w + h;
+    const int h = lane >> 2, xg = lane & 3;
+    double4* Ys = reinterpret_cast<double4*>(near_smem) + ((size_t)wib * 8 + h) * NN;
+    const long long nl = min((long long)*nleaves_dev, cap);
+    const long long warps = (long long)gridDim.x * NEAR_LEAF_WARPS;
+    for (long long w = (long long)blockIdx.x * NEAR_LEAF_WARPS + wib; 8 * w < nl; w += warps) {
+        const long long q = 8 * w + h;
         const bool active = q < nl;
         double acc = 0.0, scale = 0.0;
+        double f1x = 0, f1y = 0, f1z = 0, f2x = 0, f2y = 0, f2z = 0;
         int pair = 0;
-        double Yx[9], Yy[9], Yz[9], y2[9];
+        __syncwarp();  // the previous iteration's reads of Ys are done
         if (active) {
             const NearNode nd = leaves[q];
             pair = nd.pair;
@@ -483,50 +487,52 @@ __global__ void __launch_bounds__(NEAR_LEAF_THREADS, 2) k_near_leaves(const Near
             const double e1x = s[3] - s[0], e1y = s[4] - s[1], e1z = s[5] - s[2];
             const double e2x = s[6] - s[0], e2y = s[7] - s[1], e2z = s[8] - s[2];
             const double bx = s[0] - t[0], by = s[1] - t[1], bz = s[2] - t[2];
-#pragma unroll
-            for (int k = 0; k < 9; ++k) {
-                const int j = 9 * jb + k;
+            for (int j = xg; j < NN; j += 4) {
                 const double yx = fma(c_near_v[j], e2x, fma(c_near_u[j], e1x, bx));
                 const double yy = fma(c_near_v[j], e2y, fma(c_near_u[j], e1y, by));
                 const double yz = fma(c_near_v[j], e2z, fma(c_near_u[j], e1z, bz));
-                y2[k] = fma(yx, yx, fma(yy, yy, yz * yz));
-                Yx[k] = -2.0 * yx;
-                Yy[k] = -2.0 * yy;
-                Yz[k] = -2.0 * yz;
+                Ys[j] = make_double4(yx, yy, yz, fma(yx, yx, fma(yy, yy, yz * yz)));
             }
-            const double f1x = t[3] - t[0], f1y = t[4] - t[1], f1z = t[5] - t[2];
-            const double f2x = t[6] - t[0], f2y = t[7] - t[1], f2z = t[8] - t[2];
-            for (int i = l8; i < NN; i += 8) {
-                const double xx = fma(c_near_v[i], f2x, c_near_u[i] * f1x);
-                const double xy = fma(c_near_v[i], f2y, c_near_u[i] * f1y);
-                const double xz = fma(c_near_v[i], f2z, c_near_u[i] * f1z);
-                xs[wib][h][i] = make_double4(xx, xy, xz, fma(xx, xx, fma(xy, xy, xz * xz)));
-            }
+            f1x = t[3] - t[0], f1y = t[4] - t[1], f1z = t[5] - t[2];
+            f2x = t[6] - t[0], f2y = t[7] - t[1], f2z = t[8] - t[2];
         }
         __syncwarp();
         if (active) {
-            // one accumulator per y point: nine independent FMA chains per x point
-            const double4* X = xs[wib][h] + 18 * ia;
-            const double* WX = wsm + 18 * ia;
-            double a[9];
+            // x groups of 4 consecutive points: lane xg takes groups xg and xg + 4 against all
+            // 36 y points, and group 8 against y in [9 xg, 9 xg + 9)
+#pragma unroll 1
+            for (int pass = 0; pass < 3; ++pass) {
+                const int g = pass < 2 ? xg + 4 * pass : 8;
+                const int j0 = pass < 2 ? 0 : 9 * xg, j1 = pass < 2 ? NN : 9 * xg + 9;
+                double mx[NEAR_XP], my[NEAR_XP], mz[NEAR_XP], x2[NEAR_XP], a[NEAR_XP];
 #pragma unroll
-            for (int k = 0; k < 9; ++k) a[k] = 0.0;
-#pragma unroll 2
-            for (int p = 0; p < 18; ++p) {
-                const double4 x = X[p];
-                const double wx = WX[p];
-#pragma unroll
-                for (int k = 0; k < 9; ++k) {
-                    const double r2 = fma(x.x, Yx[k], fma(x.y, Yy[k], fma(x.z, Yz[k], x.w + y2[k])));
-                    a[k] = fma(wx, rsqrt_fast(r2), a[k]);
+                for (int r = 0; r < NEAR_XP; ++r) {
+                    const int i = NEAR_XP * g + r;
+                    const double xx = fma(c_near_v[i], f2x, c_near_u[i] * f1x);
+                    const double xy = fma(c_near_v[i], f2y, c_near_u[i] * f1y);
+                    const double xz = fma(c_near_v[i], f2z, c_near_u[i] * f1z);
+                    x2[r] = fma(xx, xx, fma(xy, xy, xz * xz));
+                    mx[r] = -2.0 * xx;
+                    my[r] = -2.0 * xy;
+                    mz[r] = -2.0 * xz;
+                    a[r] = 0.0;
                 }
-            }
+#pragma unroll 3
+                for (int j = j0; j < j1; ++j) {
+                    const double4 y = Ys[j];
+                    const double wj = c_near_w[j];
 #pragma unroll
-            for (int k = 0; k < 9; ++k) acc = fma(c_near_w[9 * jb + k], a[k], acc);
+                    for (int r = 0; r < NEAR_XP; ++r) {
+                        const double r2 = fma(mx[r], y.x, fma(my[r], y.y, fma(mz[r], y.z, x2[r] + y.w)));
+                        a[r] = fma(wj, rsqrt_fast(r2), a[r]);
+                    }
+                }
+#pragma unroll
+                for (int r = 0; r < NEAR_XP; ++r) acc = fma(c_near_w[NEAR_XP * g + r], a[r], acc);
+            }
         }
-        __syncwarp();
-        for (int o = 4; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if (active && l8 == 0) atomicAdd(out + pair, acc * scale);
+        for (int o = 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (active && xg == 0) atomicAdd(out + pair, acc * scale);
     }
 }
 
@@ -911,6 +917,11 @@ long long run_near(Ctx* ctx, const double* GV, const double* GA, const int2* pai
     cudaStream_t s = ctx->stream;
     TimedScope ts(ctx, "near");
     if (!NW.cnt.n) NW.cnt.alloc(3);
+    static bool attr = false;
+    if (!attr) {
+        SBG_CUDA(cudaFuncSetAttribute(k_near_leaves, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)NEAR_LEAF_SMEM));
+        attr = true;
+    }
     if ((long long)NW.cur.n < cap) NW.cur.alloc(cap);
     k_near_init<<<(int)((cap + 255) / 256), 256, 0, s>>>(np_dev, cap, NW.cur.p, out, NW.cnt.p);
     count_launch();
@@ -944,9 +955,9 @@ long long run_near(Ctx* ctx, const double* GV, const double* GA, const int2* pai
         }
         {
             TimedScope tl(ctx, "near_leaves");
-            const long long warps = (ncur + 3) / 4;  // upper bound on this level's leaf quads
-            const int lgrid = (int)std::min<long long>((warps + 7) / 8, 32LL * ctx->sm_count);
-            k_near_leaves<<<lgrid, NEAR_LEAF_THREADS, 0, s>>>(NW.leaves.p, NW.cnt.p + 2, ncur, pairs, GV, GA, 1.0 / M_PI, out);
+            const long long warps = (ncur + 7) / 8;  // upper bound on this level's leaf octets
+            const int lgrid = (int)std::min<long long>((warps + NEAR_LEAF_WARPS - 1) / NEAR_LEAF_WARPS, 2LL * ctx->sm_count);
+            k_near_leaves<<<lgrid, NEAR_LEAF_THREADS, NEAR_LEAF_SMEM, s>>>(NW.leaves.p, NW.cnt.p + 2, ncur, pairs, GV, GA, 1.0 / M_PI, out);
             count_launch();
         }
         SBG_LAUNCH_CHECK();
