@@ -121,7 +121,9 @@ int sbg_ctx_create(int device, sbg_ctx** out)
         auto* c = new sbg_ctx;
         c->c.device = device;
         c->c.sm_count = prop.multiProcessorCount;
-        SBG_CUDA(cudaStreamCreateWithFlags(&c->c.stream, cudaStreamNonBlocking));
+        device_pool_init(device);
+        // a blocking stream: the pool's legacy-stream allocations order against it (common.cuh)
+        SBG_CUDA(cudaStreamCreateWithFlags(&c->c.stream, cudaStreamDefault));
         *out = c;
     });
 }
@@ -749,14 +751,14 @@ int sbg_device_alloc(sbg_ctx* ctx, long long bytes, void** dptr)
 {
     return guard([&] {
         SBG_CUDA(cudaSetDevice(ctx->c.device));
-        SBG_CUDA(cudaMalloc(dptr, (size_t)bytes));
+        *dptr = device_alloc((size_t)bytes);
         SBG_CUDA(cudaMemsetAsync(*dptr, 0, (size_t)bytes, ctx->c.stream));
         SBG_CUDA(cudaStreamSynchronize(ctx->c.stream));
     });
 }
 int sbg_device_free(void* dptr)
 {
-    return guard([&] { SBG_CUDA(cudaFree(dptr)); });
+    return guard([&] { device_free(dptr); });
 }
 int sbg_memcpy_h2d(sbg_ctx* ctx, void* dst, const void* src, long long bytes)
 {

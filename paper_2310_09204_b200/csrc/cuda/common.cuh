@@ -30,6 +30,16 @@ long long launch_count();
 
 // Device buffer owned by the host object (RAII, stream-ordered free not needed:
 // objects are destroyed after a context synchronize).
+// Device memory comes from the device's stream-ordered pool, allocated and freed
+// on the legacy default stream: every context stream is a blocking stream, so a
+// free is ordered after all work already queued on them and an allocation before
+// all work queued after it.  The pool keeps freed memory (release threshold
+// = max), so steady-state allocations make no driver calls (a plain cudaMalloc /
+// cudaFree pair costs ~2-4 ms on the B200 boxes and synchronises the device).
+void* device_alloc(size_t bytes);
+void device_free(void* p);
+void device_pool_init(int device);
+
 template <class T>
 struct DBuf {
     T* p = nullptr;
@@ -54,12 +64,12 @@ struct DBuf {
     void alloc(size_t count)
     {
         release();
+        if (count) p = static_cast<T*>(device_alloc(count * sizeof(T)));
         n = count;
-        if (count) SBG_CUDA(cudaMalloc(&p, count * sizeof(T)));
     }
     void release()
     {
-        if (p) cudaFree(p);
+        if (p) device_free(p);
         p = nullptr;
         n = 0;
     }

@@ -14,6 +14,26 @@ namespace {
 std::atomic<long long> g_launches{0};
 }
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+void device_pool_init(int device)
+{
+    cudaMemPool_t pool;
+    SBG_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+    unsigned long long keep = ~0ull;
+    SBG_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+}
+
+void* device_alloc(size_t bytes)
+{
+    void* p = nullptr;
+    SBG_CUDA(cudaMallocAsync(&p, bytes, 0));
+    return p;
+}
+
+void device_free(void* p)
+{
+    if (p) cudaFreeAsync(p, 0);
+}
 long long launch_count() { return g_launches.load(); }
 
 cudaEvent_t Timers::get()
