@@ -897,6 +897,14 @@ struct NearWork {
     DBuf<unsigned long long> cnt;  // [0] current frontier, [1] next frontier, [2] leaves
 };
 
+// frontier buffers are cached on the context, so a fresh plan (every assemble_W
+// call through the reference-style API) reuses the previous call's capacity
+NearWork& near_work(Ctx* ctx)
+{
+    if (!ctx->near_ws) ctx->near_ws = std::make_shared<NearWork>();
+    return *static_cast<NearWork*>(ctx->near_ws.get());
+}
+
 __global__ void k_near_init(const unsigned long long* __restrict__ np_dev, long long cap, NearNode* __restrict__ nodes,
                             double* __restrict__ out, unsigned long long* __restrict__ cnt)
 {
@@ -997,7 +1005,6 @@ struct AssemblyPlan {
     DBuf<int2> loc_pairs;
     DBuf<double> loc_I;
     DBuf<unsigned long long> near_cnt;
-    NearWork NW;
 };
 
 AssemblyPlan* assembly_plan_create(Ctx* ctx, const InflatedMesh& im, const QuadCfg& cfg)
@@ -1178,7 +1185,7 @@ void assembly_run(AssemblyPlan* P, DMatrix& W, AssemblyStats* stats)
             SBG_LAUNCH_CHECK();
         }
         leaves = run_near(ctx, P->G.v.p, P->G.area.p, P->loc_pairs.p + P->nsing, P->near_cnt.p, P->near_cap, thr,
-                          P->loc_I.p + P->nsing, P->NW);
+                          P->loc_I.p + P->nsing, near_work(ctx));
         SBG_CUDA(cudaMemcpyAsync(&nnear, P->near_cnt.p, sizeof(nnear), cudaMemcpyDeviceToHost, s));
         SBG_CUDA(cudaStreamSynchronize(s));
         if ((long long)nnear <= P->near_cap) break;

@@ -105,6 +105,7 @@ struct Ctx {
     Timers timers;
     std::shared_ptr<void> pcg_ws;  // cached PCG workspace (linalg.cu)
     std::shared_ptr<void> dl_ws;   // cached pinned download ring (context.cu)
+    std::shared_ptr<void> near_ws; // cached near-field frontier buffers (assemble.cu)
     ~Ctx();
 };
 

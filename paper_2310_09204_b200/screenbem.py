@@ -403,10 +403,14 @@ class GalerkinMatrix(_Handle):
         _check(lib().sbg_matrix_create(ctx.h, W.shape[0], W.ctypes.data_as(C.c_void_p), C.byref(h)))
         return cls(h, ctx)
 
-    def download(self):
-        out = np.zeros(self.n * self.n)
-        _check(lib().sbg_matrix_download(self.h, out))
-        return out.reshape(self.n, self.n)
+    def download(self, out=None):
+        """Row-major host copy (n x n); `out` may supply a C-contiguous float64 buffer."""
+        if out is None:
+            out = np.empty((self.n, self.n))
+        elif out.shape != (self.n, self.n) or out.dtype != np.float64 or not out.flags.c_contiguous:
+            raise ValidationError("download: out must be a C-contiguous float64 (n, n) array")
+        _check(lib().sbg_matrix_download(self.h, out.reshape(-1)))
+        return out
 
     def rows(self, rows):
         rows = np.ascontiguousarray(rows, dtype=np.int32)
