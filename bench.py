@@ -39,6 +39,9 @@ def parse():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-phases", action="store_true",
+                    help="skip the CPU restatement's setup/preconditioner/PCG timings")
+    ap.add_argument("--cpu-phases-max-n", type=int, default=8000)
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--ratio", type=int, default=0, help="H/h for config 5 (default 8)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -149,6 +152,51 @@ def cpu_assembly_sample(cfg: int, ratio: int, target_s: float):
                       f"{t:.1f} s", "seconds": t, "pairs": pairs}
 
 
+def cpu_phases(cfg: int, ratio: int, W_host=None, max_n: int = 8000):
+    """The reference's other phases on the CPU restatement, single-threaded as in the
+    reference (Eigen without OpenMP): setup (inflate both levels, partition_dofs,
+    build_prolongation), build_preconditioner, one preconditioner apply, and PCG to
+    1e-8 on W_host (the GPU-assembled matrix when given, else the oracle's own full
+    assembly on all host threads, timed as assembly_s).  Skipped above max_n DOFs
+    (the WB Cholesky and dense coarse product take minutes at config 5)."""
+    import numpy as np
+
+    from oracle import oracle as O
+    from paper_2310_09204_b200 import screenbem as S
+    pair = S.make_config(cfg, ratio)
+    t0 = time.perf_counter()
+    opair = O.LevelPair(O.Mesh(pair.coarse.vertices, pair.coarse.facets),
+                        O.Mesh(pair.fine.vertices, pair.fine.facets), pair.parent)
+    fine, coarse = O.inflate(opair.fine, validate=False), O.inflate(opair.coarse)
+    part, R = O.partition_dofs(opair, fine), O.build_prolongation(opair, coarse, fine)
+    out = {"setup_s": time.perf_counter() - t0, "dofs": fine.n}
+    if fine.n > max_n:
+        out["skipped"] = f"n = {fine.n} > {max_n}: single-threaded WB Cholesky and dense coarse product take minutes"
+        return out
+    if W_host is None:
+        t0 = time.perf_counter()
+        W_host = O.assemble_W(fine, workers=os.cpu_count() or 1)
+        out["assembly_s"] = time.perf_counter() - t0
+        out["assembly_workers"] = os.cpu_count() or 1
+    t0 = time.perf_counter()
+    prec = O.build_preconditioner(W_host, part, R)
+    out["build_preconditioner_s"] = time.perf_counter() - t0
+    r = O.normal_draws(17, fine.n)
+    t0 = time.perf_counter()
+    for _ in range(3):
+        prec.apply(r)
+    out["precond_apply_s"] = (time.perf_counter() - t0) / 3
+    L = O.assemble_rhs(fine, S.config_g(cfg))
+    t0 = time.perf_counter()
+    rep = O.pcg(W_host, prec, L, 1e-8)
+    dt = time.perf_counter() - t0
+    out.update({"pcg_s": dt, "pcg_iterations": rep.iterations,
+                "pcg_iters_per_s": rep.iterations / dt if dt > 0 else None, "threads": 1,
+                "matrix": "GPU-assembled W (downloaded)" if "assembly_s" not in out else "oracle assemble_W"})
+    del np
+    return out
+
+
 def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
@@ -160,12 +208,18 @@ def run_reference(args):
         if i >= args.warmup:
             samples.append(r)
     v = sum(s["pairs"] for s in samples) / sum(s["seconds"] for s in samples)
+    phases = None
+    if not args.no_cpu_phases:
+        try:
+            phases = cpu_phases(cfg, args.ratio or (8 if cfg == 5 else 0), None, max_n=args.cpu_phases_max_n)
+        except Exception as e:  # pragma: no cover
+            phases = {"failed": str(e)}
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(s["seconds"] for s in samples) / len(samples),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"config {cfg}: {CFG_NAMES[cfg]}", "sample": samples[-1]["sample"]},
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": samples[-1]["cores"], "kind": "port",
-                             "sample": samples[-1]["sample"]},
+                             "sample": samples[-1]["sample"], "phases": phases},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -298,6 +352,9 @@ def run_ours(args):
         try:
             cpu = cpu_assembly_sample(cfg, ratio, args.cpu_seconds)
             cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
+            if not args.no_cpu_phases:
+                cpu["phases"] = cpu_phases(cfg, ratio, W.download() if n <= args.cpu_phases_max_n else None,
+                                           max_n=args.cpu_phases_max_n)
         except Exception as e:  # pragma: no cover
             cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "port", "sample": f"failed: {e}"}
     if rank == 0:
