@@ -60,6 +60,13 @@ typedef struct {
     int history_len; /* iterations + 1 residual norms */
 } sbg_pcg_report;
 
+/* SpectrumResult (inc/schwarz.hpp:150-154) + Lanczos bookkeeping */
+typedef struct {
+    double lambda_min, lambda_max, kappa;
+    int iterations; /* CG / PCG steps of the Lanczos process */
+    int converged;  /* the CG residual reached tol */
+} sbg_spectrum;
+
 /* assembly work counters (roofline bookkeeping) */
 typedef struct {
     long long far_pairs, near_pairs, identical, edge, vertex, near_leaves, tiles, tiles_skipped;
@@ -170,6 +177,18 @@ int sbg_prec_block_diag(sbg_ctx* ctx, sbg_prec* p, int which, double* diag, int*
 int sbg_coarse_matrix(sbg_ctx* ctx, const sbg_matrix* W, const sbg_prolong* R, double* H);
 double sbg_prec_factor_bytes(const sbg_prec* p);
 void sbg_prec_destroy(sbg_prec* p);
+
+/* ---- condition numbers (inc/schwarz.hpp:142-190) --------------------------- */
+/* materialize_preconditioner (:142-148): the dense n x n M with columns apply(e_j),
+ * built on the device from the block inverses and the coarse term */
+int sbg_materialize_preconditioner(sbg_ctx* ctx, sbg_prec* p, sbg_matrix** out);
+/* a dense SPD matrix M (device) used as the preconditioner, for condition_number(W, M) */
+int sbg_prec_from_dense(sbg_ctx* ctx, const sbg_matrix* M, sbg_prec** out);
+/* condition_number(W) (:168-172) when p is NULL, condition_number(W, prec) (:174-190)
+ * otherwise: extreme eigenvalues by Lanczos on M W in the W inner product (seeded
+ * start, full reorthogonalisation) until both extreme Ritz residuals are
+ * <= tol |theta|; maxit <= 0: min(n, 1500) steps.  Replaces the dense eigensolve. */
+int sbg_condition_number(sbg_ctx* ctx, const sbg_matrix* W, sbg_prec* p, double tol, int maxit, sbg_spectrum* out);
 
 /* ---- PCG (device) --------------------------------------------------------- */
 /* pcg (inc/pcg.hpp:33-116); prec nullable.  history/alphas/betas have hist_cap

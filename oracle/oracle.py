@@ -485,6 +485,32 @@ def materialize_preconditioner(prec: SchwarzPreconditioner):
     return M
 
 
+def spectrum_of(S):
+    """reference: inc/schwarz.hpp:156-166 (Eigen SelfAdjointEigenSolver -> LAPACK syevd via numpy)"""
+    S = np.asarray(S, dtype=np.float64)
+    if S.size == 0:
+        raise ValidationError("spectrum of an empty matrix")
+    ev = np.linalg.eigvalsh(S)
+    return ev[0], ev[-1], ev[-1] / ev[0]
+
+
+def condition_number(W, M=None):
+    """reference: inc/schwarz.hpp:168-190: kappa(W) from 0.5 (W + W^T); with a
+    preconditioner (SchwarzPreconditioner or materialized M) the spectrum of the
+    Cholesky congruence L^T M L.  Returns (lambda_min, lambda_max, kappa)."""
+    W = np.asarray(W, dtype=np.float64)
+    if M is None:
+        return spectrum_of(0.5 * (W + W.T))
+    if isinstance(M, SchwarzPreconditioner):
+        M = materialize_preconditioner(M)
+    try:
+        L = np.linalg.cholesky(W)
+    except np.linalg.LinAlgError as e:
+        raise NumericalError("Cholesky factorization failed: matrix not positive definite") from e
+    S = L.T @ M @ L
+    return spectrum_of(0.5 * (S + S.T))
+
+
 def coarse_matrix(W, P: Prolongation):
     W = np.ascontiguousarray(W, dtype=np.float64)
     H = np.zeros(P.cols * P.cols)

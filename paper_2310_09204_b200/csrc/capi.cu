@@ -717,6 +717,51 @@ int sbg_coarse_matrix(sbg_ctx* ctx, const sbg_matrix* W, const sbg_prolong* R, d
     });
 }
 double sbg_prec_factor_bytes(const sbg_prec* p) { return prec_factor_bytes(p->P); }
+
+// ---------------------------------------------------------------- condition numbers
+int sbg_materialize_preconditioner(sbg_ctx* ctx, sbg_prec* p, sbg_matrix** out)
+{
+    return guard([&] {
+        need(out, "out");
+        need(p, "preconditioner");
+        auto* m = new sbg_matrix;
+        try {
+            prec_materialize(&ctx->c, p->P, m->M);
+        } catch (...) {
+            delete m;
+            throw;
+        }
+        *out = m;
+    });
+}
+int sbg_prec_from_dense(sbg_ctx* ctx, const sbg_matrix* M, sbg_prec** out)
+{
+    return guard([&] {
+        need(out, "out");
+        need(M, "matrix");
+        auto* p = new sbg_prec;
+        try {
+            p->P = prec_from_dense(&ctx->c, M->M);
+        } catch (...) {
+            delete p;
+            throw;
+        }
+        *out = p;
+    });
+}
+int sbg_condition_number(sbg_ctx* ctx, const sbg_matrix* W, sbg_prec* p, double tol, int maxit, sbg_spectrum* out)
+{
+    return guard([&] {
+        need(out, "out");
+        need(W, "matrix");
+        const Spectrum sp = spectrum(&ctx->c, W->M, p ? p->P : nullptr, tol, maxit);
+        out->lambda_min = sp.lambda_min;
+        out->lambda_max = sp.lambda_max;
+        out->kappa = sp.kappa;
+        out->iterations = sp.iterations;
+        out->converged = sp.converged ? 1 : 0;
+    });
+}
 void sbg_prec_destroy(sbg_prec* p) { delete p; }
 
 // ---------------------------------------------------------------- PCG

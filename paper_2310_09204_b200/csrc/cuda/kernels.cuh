@@ -67,6 +67,8 @@ int prec_num_subspaces(const Prec* p);
 void prec_apply(Ctx* ctx, Prec* p, const double* r, double* z, const int* done_flag);
 void prec_block_diag(Ctx* ctx, Prec* p, int which, std::vector<double>& diag);
 double prec_factor_bytes(const Prec* p);  // sum n_b^2 * 8 (roofline bookkeeping)
+void prec_materialize(Ctx* ctx, Prec* p, DMatrix& M);  // schwarz.hpp:142-148
+Prec* prec_from_dense(Ctx* ctx, const DMatrix& M);     // a dense SPD M as the preconditioner
 // coarse Galerkin matrix R^T W R (n_c x n_c, row-major) — exposed for parity tests
 void coarse_galerkin(Ctx* ctx, const DMatrix& W, const Prolongation& R, std::vector<double>& H);
 
@@ -81,6 +83,14 @@ struct PcgResult {
 void pcg_run(Ctx* ctx, const DMatrix& W, Prec* prec, const double* rhs, double* x, bool on_device, double tol,
              int maxit, PcgResult& out);
 double lanczos_kappa(const std::vector<double>& alphas, const std::vector<double>& betas);
+void lanczos_extremes(const std::vector<double>& alphas, const std::vector<double>& betas, double& lmin, double& lmax);
+struct Spectrum {
+    double lambda_min = 0, lambda_max = 0, kappa = 0;
+    int iterations = 0;
+    bool converged = false;
+};
+// schwarz.hpp:150-190 (condition_number) by Lanczos on the device (see linalg.cu)
+Spectrum spectrum(Ctx* ctx, const DMatrix& W, Prec* prec, double tol, int maxit);
 
 // ---------------------------------------------------------------- assembly
 struct QuadCfg {

@@ -3,6 +3,8 @@
 #include <algorithm>
 #include <cmath>
 
+#include <random>
+
 #include "kernels.cuh"
 
 namespace sbg {
@@ -256,11 +258,15 @@ void gemv(Ctx* ctx, const DMatrix& W, GemvPlan& plan, const double* x, double* y
 }
 
 // Symmetric tridiagonal extreme eigenvalues by Sturm bisection (replaces the
-// dense eigensolve on the Lanczos matrix, pcg.hpp:96-113).
-double lanczos_kappa(const std::vector<double>& alphas, const std::vector<double>& betas)
+// dense eigensolve on the Lanczos matrix, pcg.hpp:96-113).  The CG coefficients
+// give the Lanczos matrix T: T_jj = 1/a_j + b_{j-1}/a_{j-1}, T_j,j+1 = sqrt(b_j)/a_j.
+void lanczos_extremes(const std::vector<double>& alphas, const std::vector<double>& betas, double& lmin, double& lmax)
 {
     const int k = (int)alphas.size();
-    if (k == 0) return 1.0;
+    if (k == 0) {
+        lmin = lmax = 0.0;
+        return;
+    }
     std::vector<double> d(k), e(k > 1 ? k - 1 : 0);
     for (int i = 0; i < k; ++i) {
         d[i] = 1.0 / alphas[i];
@@ -295,8 +301,16 @@ double lanczos_kappa(const std::vector<double>& alphas, const std::vector<double
         }
         return 0.5 * (a + b);
     };
-    const double lmin = kth(0), lmax = kth(k - 1);
-    double kappa = lmin > 0 ? lmax / lmin : 1.0;
+    lmin = kth(0);
+    lmax = kth(k - 1);
+}
+
+double lanczos_kappa(const std::vector<double>& alphas, const std::vector<double>& betas)
+{
+    if (alphas.empty()) return 1.0;
+    double lmin, lmax;
+    lanczos_extremes(alphas, betas, lmin, lmax);
+    const double kappa = lmin > 0 ? lmax / lmin : 1.0;
     return kappa < 1.0 ? 1.0 : kappa;
 }
 

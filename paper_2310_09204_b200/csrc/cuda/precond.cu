@@ -41,6 +41,8 @@ struct Prec {
     DBuf<long long> d_Poff, d_Moff;
     DBuf<double> Lp, Xp, D, Mc, loc, locy;
     DBuf<int> pos;  // dof -> loc index (face/WB), -1 if none
+    DBuf<int> d_bptr, d_bdofs;  // face/WB block dof lists (CSR), for materialisation
+    int ngather = 0;
     // R in CSC (restriction, ascending rows) and CSR (prolongation, ascending cols)
     DBuf<int> Rc_ptr, Rc_row, Rr_ptr, Rr_col;
     DBuf<double> Rc_val, Rr_val;
@@ -480,7 +482,7 @@ __global__ void k_prec_scatter(const double* __restrict__ locy, const int* __res
 }
 
 template <int KIND>
-void launch_gemm(Ctx* ctx, Prec* P, int k, const GTask* dev_tasks, int count)
+void launch_gemm(Ctx* ctx, Prec* P, int k, const GTask* dev_tasks, int count, double* Lp, double* Xp)
 {
     if (count <= 0) return;
     const size_t smem = 2 * TB * TLD * sizeof(double);
@@ -489,8 +491,8 @@ void launch_gemm(Ctx* ctx, Prec* P, int k, const GTask* dev_tasks, int count)
         SBG_CUDA(cudaFuncSetAttribute(k_tile_gemm<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         configured = true;
     }
-    k_tile_gemm<KIND><<<count, 128, smem, ctx->stream>>>(k, dev_tasks, P->d_T.p, P->d_Poff.p, P->d_Doff.p, P->Lp.p,
-                                                        P->Xp.p, P->D.p);
+    k_tile_gemm<KIND><<<count, 128, smem, ctx->stream>>>(k, dev_tasks, P->d_T.p, P->d_Poff.p, P->d_Doff.p, Lp, Xp,
+                                                        P->D.p);
     count_launch();
     SBG_LAUNCH_CHECK();
 }
@@ -502,6 +504,48 @@ struct StepTasks {
     void close() { off.push_back((int)all.size()); }
     int count(int st) const { return off[st + 1] - off[st]; }
 };
+
+// W_bb^-1 = L^-T L^-1 for every block from the tiled factor in Lwork (overwritten):
+// X = L^-1 right-looking in one-stage tile tasks, then M = X^T X over Lwork, then
+// the compact row-major inverses (row stride ldm_b) into Mc.
+void form_inverses(Ctx* ctx, Prec* P, DBuf<double>& Lwork, DBuf<double>& Mc)
+{
+    cudaStream_t s = ctx->stream;
+    DBuf<double> Xp(std::max<size_t>(Lwork.n, 1));
+    SBG_CUDA(cudaMemsetAsync(Xp.p, 0, Xp.n * sizeof(double), s));
+    StepTasks xd, xu;
+    std::vector<GTask> la;
+    for (int k = 0; k < P->Tmax; ++k) {
+        for (int b = 0; b < P->nblocks; ++b) {
+            const int T = P->h_T[b];
+            if (T <= k) continue;
+            for (int j = 0; j <= k; ++j) xd.all.push_back({b, k, j, 0});
+            for (int i = k + 1; i < T; ++i)
+                for (int j = 0; j <= k; ++j) xu.all.push_back({b, i, j, 0});
+        }
+        xd.close();
+        xu.close();
+    }
+    for (int b = 0; b < P->nblocks; ++b)
+        for (int i = 0; i < P->h_T[b]; ++i)
+            for (int j = 0; j <= i; ++j) la.push_back({b, i, j, 0});
+    DBuf<GTask> d_xd, d_xu, d_la;
+    d_xd.upload(xd.all, s);
+    d_xu.upload(xu.all, s);
+    d_la.upload(la, s);
+    for (int k = 0; k < P->Tmax; ++k) {
+        launch_gemm<K_XDIAG>(ctx, P, k, d_xd.p + xd.off[k], xd.count(k), Lwork.p, Xp.p);
+        launch_gemm<K_XUPD>(ctx, P, k, d_xu.p + xu.off[k], xu.count(k), Lwork.p, Xp.p);
+    }
+    launch_gemm<K_LAUUM>(ctx, P, 0, d_la.p, (int)la.size(), Lwork.p, Xp.p);
+    const long long Msize = P->h_Moff.empty() ? 0 : P->h_Moff.back() + (long long)P->h_nb.back() * P->h_ldm.back();
+    Mc.alloc(std::max<long long>(Msize, 1));
+    k_compact_inverse<<<dim3(P->nblocks, 64), 128, 0, s>>>(Lwork.p, P->d_Poff.p, P->d_T.p, P->d_nb.p, P->d_ldm.p,
+                                                           P->d_Moff.p, Mc.p);
+    count_launch();
+    SBG_LAUNCH_CHECK();
+    SBG_CUDA(cudaStreamSynchronize(s));
+}
 
 }  // namespace
 
@@ -581,12 +625,12 @@ Prec* prec_build(Ctx* ctx, const DMatrix& W, const DofPartition& part, const Pro
         for (int b = 0; b < ngather; ++b)
             for (int q = bptr[b]; q < bptr[b + 1]; ++q) pos[bdofs[q]] = P->h_loc[b] + (q - bptr[b]);
         P->pos.upload(pos, s);
+        P->ngather = ngather;
+        P->d_bptr.upload(bptr, s);
+        P->d_bdofs.upload(bdofs, s);
         if (ngather > 0) {  // factor_block's submatrix (schwarz.hpp:77-83)
-            DBuf<int> d_bptr, d_bdofs;
-            d_bptr.upload(bptr, s);
-            d_bdofs.upload(bdofs, s);
-            k_gather_blocks<<<dim3(ngather, 64), 128, 0, s>>>(W.a.p, W.ld, d_bptr.p, d_bdofs.p, P->d_T.p, P->d_Poff.p,
-                                                              P->Lp.p);
+            k_gather_blocks<<<dim3(ngather, 64), 128, 0, s>>>(W.a.p, W.ld, P->d_bptr.p, P->d_bdofs.p, P->d_T.p,
+                                                              P->d_Poff.p, P->Lp.p);
             count_launch();
             SBG_LAUNCH_CHECK();
             SBG_CUDA(cudaStreamSynchronize(s));
@@ -656,8 +700,8 @@ Prec* prec_build(Ctx* ctx, const DMatrix& W, const DofPartition& part, const Pro
                                                                              P->D.p, fail.p);
                 count_launch();
                 SBG_LAUNCH_CHECK();
-                launch_gemm<K_TRSM>(ctx, P, k, d_trsm.p + trsm.off[k], trsm.count(k));
-                launch_gemm<K_UPDATE>(ctx, P, k, d_upd.p + upd.off[k], upd.count(k));
+                launch_gemm<K_TRSM>(ctx, P, k, d_trsm.p + trsm.off[k], trsm.count(k), P->Lp.p, nullptr);
+                launch_gemm<K_UPDATE>(ctx, P, k, d_upd.p + upd.off[k], upd.count(k), P->Lp.p, nullptr);
             }
             SBG_CUDA(cudaStreamSynchronize(s));
         }
@@ -671,42 +715,10 @@ Prec* prec_build(Ctx* ctx, const DMatrix& W, const DofPartition& part, const Pro
                                      "): partition inconsistent with the assembled matrix");
             }
         if (mode == kPrecInverse) {
-            // ---- W_bb^-1 = L^-T L^-1: X = L^-1 (right-looking, one-stage tile tasks), then M = X^T X over L
-            TimedScope ts(ctx, "block_inverse");
-            P->Xp.alloc(std::max<long long>(Poff, 1));
-            SBG_CUDA(cudaMemsetAsync(P->Xp.p, 0, P->Xp.n * sizeof(double), s));
-            StepTasks xd, xu;
-            std::vector<GTask> la;
-            for (int k = 0; k < P->Tmax; ++k) {
-                for (int b = 0; b < P->nblocks; ++b) {
-                    const int T = P->h_T[b];
-                    if (T <= k) continue;
-                    for (int j = 0; j <= k; ++j) xd.all.push_back({b, k, j, 0});
-                    for (int i = k + 1; i < T; ++i)
-                        for (int j = 0; j <= k; ++j) xu.all.push_back({b, i, j, 0});
-                }
-                xd.close();
-                xu.close();
+            {
+                TimedScope ts(ctx, "block_inverse");
+                form_inverses(ctx, P, P->Lp, P->Mc);
             }
-            for (int b = 0; b < P->nblocks; ++b)
-                for (int i = 0; i < P->h_T[b]; ++i)
-                    for (int j = 0; j <= i; ++j) la.push_back({b, i, j, 0});
-            DBuf<GTask> d_xd, d_xu, d_la;
-            d_xd.upload(xd.all, s);
-            d_xu.upload(xu.all, s);
-            d_la.upload(la, s);
-            for (int k = 0; k < P->Tmax; ++k) {
-                launch_gemm<K_XDIAG>(ctx, P, k, d_xd.p + xd.off[k], xd.count(k));
-                launch_gemm<K_XUPD>(ctx, P, k, d_xu.p + xu.off[k], xu.count(k));
-            }
-            launch_gemm<K_LAUUM>(ctx, P, 0, d_la.p, (int)la.size());
-            SBG_CUDA(cudaStreamSynchronize(s));
-            P->Xp.release();
-            P->Mc.alloc(std::max<long long>(Moff, 1));
-            k_compact_inverse<<<dim3(P->nblocks, 64), 128, 0, s>>>(P->Lp.p, P->d_Poff.p, P->d_T.p, P->d_nb.p,
-                                                                   P->d_ldm.p, P->d_Moff.p, P->Mc.p);
-            count_launch();
-            SBG_LAUNCH_CHECK();
             std::vector<int2> gt;
             for (int b = 0; b < P->nblocks; ++b)
                 for (int r = 0; r < P->h_nb[b]; r += GEMV_ROWS) gt.push_back({b, r});
@@ -820,6 +832,132 @@ void prec_block_diag(Ctx* ctx, Prec* P, int which, std::vector<double>& diag)
         for (int i = 0; i < nb; ++i) diag.push_back(h[(size_t)i * ld + i]);
     }
     (void)ctx;
+}
+
+namespace {
+// M[d_r][d_c] = (W_bb^-1)[r][c] for the face / WB blocks (their DOF sets are disjoint)
+__global__ void k_mat_blocks(const int* __restrict__ bptr, const int* __restrict__ bdofs,
+                             const int* __restrict__ nbv, const int* __restrict__ ldmv,
+                             const long long* __restrict__ Moff, const double* __restrict__ Mc, double* __restrict__ M,
+                             int ld)
+{
+    const int b = blockIdx.x, p0 = bptr[b], nb = nbv[b], ldm = ldmv[b];
+    const double* Mb = Mc + Moff[b];
+    for (int r = blockIdx.y; r < nb; r += gridDim.y) {
+        double* row = M + (size_t)bdofs[p0 + r] * ld;
+        for (int c = threadIdx.x; c < nb; c += blockDim.x) row[bdofs[p0 + c]] = Mb[(size_t)r * ldm + c];
+    }
+}
+
+// M[i][j] += sum_a R(i,a) sum_c H^-1[a][c] R(j,c)  (the coarse term of apply(e_j), schwarz.hpp:132-138)
+__global__ void k_mat_coarse(int n, const int* __restrict__ rptr, const int* __restrict__ rcol,
+                             const double* __restrict__ rval, const double* __restrict__ Hinv, int ldh,
+                             double* __restrict__ M, int ld)
+{
+    for (int i = blockIdx.x; i < n; i += gridDim.x) {
+        const int q0 = rptr[i], q1 = rptr[i + 1];
+        if (q0 == q1) continue;
+        double* row = M + (size_t)i * ld;
+        for (int j = threadIdx.x; j < n; j += blockDim.x) {
+            double z = 0.0;
+            for (int q = q0; q < q1; ++q) {
+                const double* Ha = Hinv + (size_t)rcol[q] * ldh;
+                double y = 0.0;
+                for (int q2 = rptr[j]; q2 < rptr[j + 1]; ++q2) y += Ha[rcol[q2]] * rval[q2];
+                z += rval[q] * y;
+            }
+            row[j] += z;
+        }
+    }
+}
+}  // namespace
+
+// reference: inc/schwarz.hpp:142-148 (materialize_preconditioner).  The columns of M
+// are apply(e_j); M is assembled from the block inverses (formed from a copy of the
+// factor in TRSV mode) and the coarse term instead of n applies.
+void prec_materialize(Ctx* ctx, Prec* P, DMatrix& M)
+{
+    cudaStream_t s = ctx->stream;
+    const int n = P->n;
+    matrix_alloc(ctx, n, M);
+    if (n == 0) return;
+    DBuf<double> work, Mtmp;
+    const DBuf<double>* Mc = &P->Mc;
+    if (P->mode != kPrecInverse) {
+        work.alloc(P->Lp.n);
+        SBG_CUDA(cudaMemcpyAsync(work.p, P->Lp.p, P->Lp.n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+        form_inverses(ctx, P, work, Mtmp);
+        Mc = &Mtmp;
+    }
+    if (P->ngather > 0) {
+        k_mat_blocks<<<dim3(P->ngather, 64), 128, 0, s>>>(P->d_bptr.p, P->d_bdofs.p, P->d_nb.p, P->d_ldm.p,
+                                                          P->d_Moff.p, Mc->p, M.a.p, M.ld);
+        count_launch();
+    }
+    if (P->coarse_block >= 0) {
+        const int cb = P->coarse_block;
+        k_mat_coarse<<<std::min(n, 16 * ctx->sm_count), 256, 0, s>>>(
+            n, P->Rr_ptr.p, P->Rr_col.p, P->Rr_val.p, Mc->p + P->h_Moff[cb], P->h_ldm[cb], M.a.p, M.ld);
+        count_launch();
+    }
+    SBG_LAUNCH_CHECK();
+    SBG_CUDA(cudaStreamSynchronize(s));
+}
+
+// A dense SPD matrix used as the preconditioner M (condition_number(W, M),
+// schwarz.hpp:174-183): one inverse-mode block over all DOFs holding M itself.
+Prec* prec_from_dense(Ctx* ctx, const DMatrix& Mdense)
+{
+    cudaStream_t s = ctx->stream;
+    auto* P = new Prec;
+    try {
+        const int n = Mdense.n;
+        P->ctx = ctx;
+        P->n = n;
+        P->mode = kPrecInverse;
+        P->nblocks = n > 0 ? 1 : 0;
+        P->ngather = P->nblocks;
+        if (n > 0) {
+            const int T = (n + TB - 1) / TB, ldm = (n + 3) / 4 * 4;
+            P->h_nb = {n};
+            P->h_T = {T};
+            P->h_loc = {0};
+            P->h_Poff = {0};
+            P->h_Doff = {0};
+            P->h_Moff = {0};
+            P->h_ldm = {ldm};
+            P->Tmax = T;
+            P->maxnb = ldm;
+            P->apply_bytes = (double)n * n * 8.0;
+            P->d_nb.upload(P->h_nb, s);
+            P->d_T.upload(P->h_T, s);
+            P->d_loc.upload(P->h_loc, s);
+            P->d_Moff.upload(P->h_Moff, s);
+            P->d_ldm.upload(P->h_ldm, s);
+            P->loc.alloc((size_t)T * TB);
+            P->locy.alloc((size_t)T * TB);
+            SBG_CUDA(cudaMemsetAsync(P->loc.p, 0, P->loc.n * sizeof(double), s));
+            SBG_CUDA(cudaMemsetAsync(P->locy.p, 0, P->locy.n * sizeof(double), s));
+            std::vector<int> pos(n), bptr{0, n};
+            for (int d = 0; d < n; ++d) pos[d] = d;
+            P->pos.upload(pos, s);
+            P->d_bptr.upload(bptr, s);
+            P->d_bdofs.upload(pos, s);
+            P->Mc.alloc((size_t)n * ldm);
+            SBG_CUDA(cudaMemsetAsync(P->Mc.p, 0, P->Mc.n * sizeof(double), s));
+            SBG_CUDA(cudaMemcpy2DAsync(P->Mc.p, ldm * sizeof(double), Mdense.a.p, Mdense.ld * sizeof(double),
+                                       n * sizeof(double), n, cudaMemcpyDeviceToDevice, s));
+            std::vector<int2> gt;
+            for (int r = 0; r < n; r += GEMV_ROWS) gt.push_back({0, r});
+            P->gemv_tasks.upload(gt, s);
+            P->ngemv = (int)gt.size();
+            SBG_CUDA(cudaStreamSynchronize(s));
+        }
+    } catch (...) {
+        delete P;
+        throw;
+    }
+    return P;
 }
 
 void coarse_galerkin(Ctx* ctx, const DMatrix& W, const Prolongation& R, std::vector<double>& H)

@@ -114,6 +114,9 @@ SIGNATURES = {
     "sbg_prec_block_diag": (C.c_int, [vp, vp, C.c_int, C.c_void_p, C.POINTER(C.c_int)]),
     "sbg_coarse_matrix": (C.c_int, [vp, vp, vp, f64p]),
     "sbg_prec_factor_bytes": (C.c_double, [vp]),
+    "sbg_materialize_preconditioner": (C.c_int, [vp, vp, C.POINTER(vp)]),
+    "sbg_prec_from_dense": (C.c_int, [vp, vp, C.POINTER(vp)]),
+    "sbg_condition_number": (C.c_int, [vp, vp, vp, C.c_double, C.c_int, C.c_void_p]),
     "sbg_prec_destroy": (None, [vp]),
     "sbg_pcg": (C.c_int, [vp, vp, vp, f64p, C.c_int, C.c_double, C.c_int, f64p, f64p, f64p, f64p, C.c_int,
                           C.POINTER(PcgReportC)]),
@@ -649,14 +652,53 @@ def apply_preconditioner(prec: SchwarzPreconditioner, r):
     return prec.apply(r)
 
 
-def materialize_preconditioner(prec: SchwarzPreconditioner):
-    """reference: inc/schwarz.hpp:142-148"""
-    M = np.zeros((prec.n, prec.n))
-    for j in range(prec.n):
-        e = np.zeros(prec.n)
-        e[j] = 1.0
-        M[:, j] = prec.apply(e)
-    return M
+def materialize_preconditioner(prec: SchwarzPreconditioner, device: bool = False):
+    """reference: inc/schwarz.hpp:142-148.  M (columns apply(e_j)) is built on the
+    device from the block inverses and the coarse term; device=True keeps it in HBM
+    (a GalerkinMatrix handle), else a host (n, n) array."""
+    h = vp()
+    _check(lib().sbg_materialize_preconditioner(prec.ctx.h, prec.h, C.byref(h)))
+    M = GalerkinMatrix(h, prec.ctx)
+    return M if device else M.download()
+
+
+class _Spectrum(C.Structure):
+    _fields_ = [("lambda_min", C.c_double), ("lambda_max", C.c_double), ("kappa", C.c_double),
+                ("iterations", C.c_int), ("converged", C.c_int)]
+
+
+@dataclass
+class SpectrumResult:
+    """reference: inc/schwarz.hpp:150-154 (+ the Lanczos step count)"""
+    lambda_min: float
+    lambda_max: float
+    kappa: float
+    iterations: int = 0
+    converged: bool = True
+
+
+def condition_number(W: GalerkinMatrix, M=None, tol: float = 1e-10, maxit: int = 0) -> SpectrumResult:
+    """reference: inc/schwarz.hpp:166-190.  condition_number(W) when M is None;
+    condition_number(W, prec) for a SchwarzPreconditioner; condition_number(W, M) for a
+    materialized M (host array or device GalerkinMatrix).  Extreme eigenvalues by
+    Lanczos on the device (W inner product, full reorthogonalisation, stopped when both
+    extreme Ritz residuals are <= tol |theta|) instead of the dense eigensolve."""
+    keep = None
+    if M is None:
+        ph = None
+    elif isinstance(M, SchwarzPreconditioner):
+        ph = M.h
+    else:
+        Md = M if isinstance(M, GalerkinMatrix) else GalerkinMatrix.from_host(M, W.ctx)
+        if Md.n != W.n:
+            raise ValidationError("condition_number: preconditioner size mismatch")
+        h = vp()
+        _check(lib().sbg_prec_from_dense(W.ctx.h, Md.h, C.byref(h)))
+        keep = SchwarzPreconditioner(h, W.ctx, W.n)
+        ph = keep.h
+    out = _Spectrum()
+    _check(lib().sbg_condition_number(W.ctx.h, W.h, ph, tol, maxit, C.byref(out)))
+    return SpectrumResult(out.lambda_min, out.lambda_max, out.kappa, out.iterations, bool(out.converged))
 
 
 def coarse_matrix(W: GalerkinMatrix, P: Prolongation):
