@@ -316,11 +316,13 @@ __global__ void k_compact_inverse(const double* __restrict__ Lp, const long long
 
 // ---------------------------------------------------------------- apply
 // gather r into the block-local vector (faces/WB) and restrict to the coarse space:
-// blocks [0, dof_blocks) gather one dof per thread, the rest one coarse column per warp
-__global__ void k_prec_gather(const double* __restrict__ r, int n, const int* __restrict__ pos,
-                              double* __restrict__ loc, const int* __restrict__ cptr, const int* __restrict__ crow,
-                              const double* __restrict__ cval, int nc, double* __restrict__ loc_c, int dof_blocks,
-                              const int* done)
+// blocks [0, dof_blocks) gather one dof per thread, block dof_blocks + c restricts
+// coarse column c (its support is ~n / nc DOFs: thousands at H/h = 40, so a whole
+// CTA with four independent loads per thread, then a fixed-order reduction)
+__global__ void __launch_bounds__(256) k_prec_gather(const double* __restrict__ r, int n, const int* __restrict__ pos,
+                                                     double* __restrict__ loc, const int* __restrict__ cptr,
+                                                     const int* __restrict__ crow, const double* __restrict__ cval,
+                                                     int nc, double* __restrict__ loc_c, int dof_blocks, const int* done)
 {
     if (done && *done) return;
     if ((int)blockIdx.x < dof_blocks) {
@@ -328,13 +330,29 @@ __global__ void k_prec_gather(const double* __restrict__ r, int n, const int* __
         if (d < n && pos[d] >= 0) loc[pos[d]] = r[d];
         return;
     }
-    const int c = ((int)blockIdx.x - dof_blocks) * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    const int lane = threadIdx.x & 31;
+    __shared__ double red[8];
+    const int c = (int)blockIdx.x - dof_blocks;
     if (c >= nc) return;
-    double s = 0.0;
-    for (int q = cptr[c] + lane; q < cptr[c + 1]; q += 32) s += cval[q] * r[crow[q]];
+    const int q0 = cptr[c], q1 = cptr[c + 1];
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    int q = q0 + threadIdx.x;
+    for (; q + 3 * 256 < q1; q += 4 * 256) {
+        const int i0 = crow[q], i1 = crow[q + 256], i2 = crow[q + 512], i3 = crow[q + 768];
+        s0 += cval[q] * r[i0];
+        s1 += cval[q + 256] * r[i1];
+        s2 += cval[q + 512] * r[i2];
+        s3 += cval[q + 768] * r[i3];
+    }
+    for (; q < q1; q += 256) s0 += cval[q] * r[crow[q]];
+    double s = (s0 + s1) + (s2 + s3);
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (lane == 0) loc_c[c] = s;
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < 8; ++w) t += red[w];
+        loc_c[c] = t;
+    }
 }
 
 // y_b = M_b x_b: one row per warp, 8 rows per CTA; 128-bit streaming loads of M
@@ -354,21 +372,33 @@ __global__ void __launch_bounds__(256) k_block_gemv(const int2* __restrict__ tas
     const double2* row = reinterpret_cast<const double2*>(Mc + Moff[b] + (size_t)r * ldm);
     const int half = ldm >> 1;
     double s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    int c = lane;
-    for (; c + 7 * 32 < half; c += 8 * 32) {
-        double2 a[8];
+    if (half > 8 * 32) {  // long rows (WB): 8 x 128-bit loads in flight per lane, serial tail
+        int c = lane;
+        for (; c + 7 * 32 < half; c += 8 * 32) {
+            double2 a[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) a[u] = __ldcs(row + c + 32 * u);
+            for (int u = 0; u < 8; ++u) a[u] = __ldcs(row + c + 32 * u);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const double2 xv = __ldg(x2 + c + 32 * u);
+                s[u] = fma(a[u].x, xv.x, fma(a[u].y, xv.y, s[u]));
+            }
+        }
+        for (; c < half; c += 32) {
+            const double2 a = __ldcs(row + c);
+            const double2 xv = __ldg(x2 + c);
+            s[0] = fma(a.x, xv.x, fma(a.y, xv.y, s[0]));
+        }
+    } else {  // short rows (faces): one predicated chunk, every load issued before the FMAs
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
-            const double2 xv = __ldg(x2 + c + 32 * u);
-            s[u] = fma(a[u].x, xv.x, fma(a[u].y, xv.y, s[u]));
+            const int c = lane + 32 * u;
+            if (c < half) {
+                const double2 a = __ldcs(row + c);
+                const double2 xv = __ldg(x2 + c);
+                s[u] = fma(a.x, xv.x, fma(a.y, xv.y, s[u]));
+            }
         }
-    }
-    for (; c < half; c += 32) {
-        const double2 a = __ldcs(row + c);
-        const double2 xv = __ldg(x2 + c);
-        s[0] = fma(a.x, xv.x, fma(a.y, xv.y, s[0]));
     }
     double v = ((s[0] + s[1]) + (s[2] + s[3])) + ((s[4] + s[5]) + (s[6] + s[7]));
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -773,7 +803,7 @@ void prec_apply(Ctx* ctx, Prec* P, const double* r, double* z, const int* done)
     const int cb = P->coarse_block;
     double* loc_c = cb >= 0 ? P->loc.p + P->h_loc[cb] : nullptr;
     const int dof_blocks = (n + 255) / 256;
-    k_prec_gather<<<dof_blocks + (P->nc + 7) / 8, 256, 0, s>>>(r, n, P->pos.p, P->loc.p, P->Rc_ptr.p, P->Rc_row.p,
+    k_prec_gather<<<dof_blocks + P->nc, 256, 0, s>>>(r, n, P->pos.p, P->loc.p, P->Rc_ptr.p, P->Rc_row.p,
                                                                P->Rc_val.p, P->nc, loc_c, dof_blocks, done);
     count_launch();
     const double* yloc;
