@@ -66,54 +66,93 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
 }
 
 // ---------------------------------------------------------------- gather / coarse Galerkin
-// padded block b <- W[dofs, dofs] (full square) with identity on the padding
-__global__ void k_gather_blocks(const double* __restrict__ W, int ld, const int* __restrict__ bptr,
-                                const int* __restrict__ bdofs, const int* __restrict__ Tv,
-                                const long long* __restrict__ Poff, double* __restrict__ Lp)
+// padded block b <- W[dofs, dofs] (full square) with identity on the padding; tasks
+// (block, first row) of 8 rows, one warp per row (the big WB block gets enough CTAs)
+__global__ void __launch_bounds__(256) k_gather_blocks(const double* __restrict__ W, int ld,
+                                                       const int* __restrict__ bptr, const int* __restrict__ bdofs,
+                                                       const int* __restrict__ Tv, const long long* __restrict__ Poff,
+                                                       const int2* __restrict__ tasks, double* __restrict__ Lp)
 {
-    const int b = blockIdx.x;
+    const int2 t = tasks[blockIdx.x];
+    const int b = t.x, i = t.y + (threadIdx.x >> 5), lane = threadIdx.x & 31;
     const int p0 = bptr[b], nb = bptr[b + 1] - p0;
     const int np = Tv[b] * TB;
-    double* Lb = Lp + Poff[b];
-    for (int i = blockIdx.y; i < np; i += gridDim.y) {
-        if (i < nb) {
-            const size_t wi = (size_t)bdofs[p0 + i] * ld;
-            for (int j = threadIdx.x; j < np; j += blockDim.x)
-                Lb[(size_t)i * np + j] = j < nb ? W[wi + bdofs[p0 + j]] : 0.0;
-        } else {
-            for (int j = threadIdx.x; j < np; j += blockDim.x) Lb[(size_t)i * np + j] = (i == j) ? 1.0 : 0.0;
-        }
+    if (i >= np) return;
+    double* dst = Lp + Poff[b] + (size_t)i * np;
+    if (i < nb) {
+        const double* wi = W + (size_t)bdofs[p0 + i] * ld;
+        const int* cols = bdofs + p0;
+#pragma unroll 4
+        for (int j = lane; j < np; j += 32) dst[j] = j < nb ? wi[cols[j]] : 0.0;
+    } else {
+        for (int j = lane; j < np; j += 32) dst[j] = (i == j) ? 1.0 : 0.0;
     }
 }
 
-// WR[i][c] = sum_{r in col c} W[i][r] R(r,c), rows ascending (deterministic)
-__global__ void k_coarse_WR(const double* __restrict__ W, int ld, int n, const int* __restrict__ cptr,
-                            const int* __restrict__ crow, const double* __restrict__ cval, int nc,
-                            double* __restrict__ WR)
+// WRt[c][i] = (W R)[i][c] = sum_{q in col c} R(r_q, c) W[r_q][i]  (W symmetric).
+// Pass 1: task (column chunk of <= kQC support rows, 2048-wide i range): the chunk's rows
+// of W are streamed coalesced and accumulated in registers (8 per thread) into a
+// partial row; pass 2 sums a column's chunk partials in ascending order
+// (deterministic).  Every row of W is read once per coarse column containing it
+// (<= 3 for P1 prolongations), with thousands of CTAs whatever H/h is.
+constexpr int kQC = 64, kIR = 2048;
+__global__ void __launch_bounds__(256) k_coarse_WR_chunks(const double* __restrict__ W, int ld, int n,
+                                                          const int4* __restrict__ chunks,
+                                                          const int* __restrict__ crow,
+                                                          const double* __restrict__ cval, double* __restrict__ part)
 {
-    for (int i = blockIdx.x; i < n; i += gridDim.x) {
-        const double* Wi = W + (size_t)i * ld;
-        for (int c = threadIdx.x; c < nc; c += blockDim.x) {
-            double s = 0.0;
-            for (int q = cptr[c]; q < cptr[c + 1]; ++q) s += Wi[crow[q]] * cval[q];
-            WR[(size_t)i * nc + c] = s;
+    const int4 ch = chunks[blockIdx.x];  // (column, q begin, q end, chunk index)
+    const int i0 = blockIdx.y * kIR + threadIdx.x;
+    double acc[kIR / 256];
+#pragma unroll
+    for (int k = 0; k < kIR / 256; ++k) acc[k] = 0.0;
+    for (int q = ch.y; q < ch.z; ++q) {
+        const double v = cval[q];
+        const double* row = W + (size_t)crow[q] * ld;
+#pragma unroll
+        for (int k = 0; k < kIR / 256; ++k) {
+            const int i = i0 + 256 * k;
+            if (i < n) acc[k] = fma(v, __ldg(row + i), acc[k]);
         }
+    }
+    double* out = part + (size_t)ch.w * n;
+#pragma unroll
+    for (int k = 0; k < kIR / 256; ++k) {
+        const int i = i0 + 256 * k;
+        if (i < n) out[i] = acc[k];
     }
 }
 
-// H[a][b] = sum_{r in col a} R(r,a) WR[r][b]  into a padded block (ldh), identity padding
-__global__ void k_coarse_H(const double* __restrict__ WR, const int* __restrict__ cptr, const int* __restrict__ crow,
-                           const double* __restrict__ cval, int nc, int ldh, double* __restrict__ H)
+__global__ void k_coarse_WR_reduce(const double* __restrict__ part, const int* __restrict__ cfirst, int n,
+                                   double* __restrict__ WRt)
+{
+    const int c = blockIdx.y;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double s = 0.0;
+    for (int k = cfirst[c]; k < cfirst[c + 1]; ++k) s += part[(size_t)k * n + i];
+    WRt[(size_t)c * n + i] = s;
+}
+
+// H[a][b] = sum_{q in col b} R(r_q, b) WRt[a][r_q] (= (R^T W R)[b][a]) into a padded block
+// (ldh) with identity padding; one warp per entry b of row a
+__global__ void __launch_bounds__(256) k_coarse_Ht(const double* __restrict__ WRt, int n,
+                                                   const int* __restrict__ cptr, const int* __restrict__ crow,
+                                                   const double* __restrict__ cval, int nc, int ldh,
+                                                   double* __restrict__ H)
 {
     const int a = blockIdx.x;
-    for (int b = threadIdx.x; b < ldh; b += blockDim.x) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const double* wa = WRt + (size_t)a * n;
+    for (int b = warp; b < ldh; b += blockDim.x >> 5) {
         double s = 0.0;
         if (a < nc && b < nc) {
-            for (int q = cptr[a]; q < cptr[a + 1]; ++q) s += cval[q] * WR[(size_t)crow[q] * nc + b];
+            for (int q = cptr[b] + lane; q < cptr[b + 1]; q += 32) s += cval[q] * wa[crow[q]];
+            for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
         } else {
             s = (a == b) ? 1.0 : 0.0;
         }
-        H[(size_t)a * ldh + b] = s;
+        if (lane == 0) H[(size_t)a * ldh + b] = s;
     }
 }
 
@@ -137,20 +176,37 @@ __global__ void __launch_bounds__(256) k_potrf(int k, const int* __restrict__ bl
     }
     if (threadIdx.x == 0) bad = 0;
     __syncthreads();
-    for (int j = 0; j < TB; ++j) {
-        if (threadIdx.x == 0) {
-            const double d = a[j * (TB + 1) + j];
-            if (!(d > 0.0) || !isfinite(d)) bad = 1;
-            a[j * (TB + 1) + j] = sqrt(d);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    constexpr int PW = 8;  // panel width
+    // blocked right-looking: warp 0 factors the 8-column panel (rows c0..63) with warp
+    // syncs only, then all threads apply the rank-8 update to the trailing lower part
+    for (int c0 = 0; c0 < TB; c0 += PW) {
+        if (warp == 0) {
+            for (int j = c0; j < c0 + PW; ++j) {
+                const double d = a[j * (TB + 1) + j];
+                if (lane == 0 && (!(d > 0.0) || !isfinite(d))) bad = 1;
+                const double djj = sqrt(d);
+                __syncwarp();
+                if (lane == 0) a[j * (TB + 1) + j] = djj;
+                for (int r = j + 1 + lane; r < TB; r += 32) a[r * (TB + 1) + j] /= djj;
+                __syncwarp();
+                for (int r = j + 1 + lane; r < TB; r += 32) {
+                    const double arj = a[r * (TB + 1) + j];
+                    for (int jj = j + 1; jj < c0 + PW && jj <= r; ++jj) a[r * (TB + 1) + jj] -= arj * a[jj * (TB + 1) + j];
+                }
+                __syncwarp();
+            }
         }
         __syncthreads();
-        const double djj = a[j * (TB + 1) + j];
-        for (int i = j + 1 + threadIdx.x; i < TB; i += blockDim.x) a[i * (TB + 1) + j] /= djj;
-        __syncthreads();
-        const int m = TB - j - 1;
+        const int t0 = c0 + PW, m = TB - t0;
         for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
-            const int i = j + 1 + e / m, l = j + 1 + e % m;
-            if (l <= i) a[i * (TB + 1) + l] -= a[i * (TB + 1) + j] * a[l * (TB + 1) + j];
+            const int i = t0 + e / m, l = t0 + e % m;
+            if (l <= i) {
+                double acc = a[i * (TB + 1) + l];
+#pragma unroll
+                for (int q = 0; q < PW; ++q) acc -= a[i * (TB + 1) + c0 + q] * a[l * (TB + 1) + c0 + q];
+                a[i * (TB + 1) + l] = acc;
+            }
         }
         __syncthreads();
     }
@@ -159,18 +215,70 @@ __global__ void __launch_bounds__(256) k_potrf(int k, const int* __restrict__ bl
         const int i = e / TB, j = e % TB;
         Lt[(size_t)i * ld + j] = (j <= i) ? a[i * (TB + 1) + j] : 0.0;
     }
-    // inverse of the lower-triangular tile, one column per thread
-    const int c = threadIdx.x;
-    if (c < TB) {
-        for (int i = 0; i < TB; ++i) x[i * (TB + 1) + c] = 0.0;
-        x[c * (TB + 1) + c] = 1.0 / a[c * (TB + 1) + c];
-        for (int i = c + 1; i < TB; ++i) {
-            double s = 0.0;
-            for (int l = c; l < i; ++l) s += a[i * (TB + 1) + l] * x[l * (TB + 1) + c];
-            x[i * (TB + 1) + c] = -s / a[i * (TB + 1) + i];
+    // X = L^-1 blocked by 8x8: diagonal blocks by one warp each (lane = column), then
+    // block row i: S_ij = sum_{q=j}^{i-1} L_iq X_qj, X_ij = -X_ii S_ij, one element per thread
+    for (int e = threadIdx.x; e < TB * TB; e += blockDim.x) x[(e / TB) * (TB + 1) + (e % TB)] = 0.0;
+    __syncthreads();
+    {
+        const int o = warp * PW;  // block `warp`
+        if (lane < PW) {
+            const int c = o + lane;
+            x[c * (TB + 1) + c] = 1.0 / a[c * (TB + 1) + c];
+            for (int i = c + 1; i < o + PW; ++i) {
+                double sacc = 0.0;
+                for (int l = c; l < i; ++l) sacc += a[i * (TB + 1) + l] * x[l * (TB + 1) + c];
+                x[i * (TB + 1) + c] = -sacc / a[i * (TB + 1) + i];
+            }
         }
     }
     __syncthreads();
+    for (int bi = 1; bi < TB / PW; ++bi) {
+        // S_{bi,bj} (bj < bi), element (r, c): at most 7 * 64 = 448 elements, <= 2 per thread
+        const int total = bi * PW * PW;
+        double sv[2] = {0.0, 0.0};
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int e = threadIdx.x + h * 256;
+            if (e < total) {
+                const int bj = e / (PW * PW), r = (e / PW) % PW, c = e % PW;
+                const int row = bi * PW + r, col = bj * PW + c;
+                double acc = 0.0;
+                for (int l = bj * PW; l < bi * PW; ++l) acc += a[row * (TB + 1) + l] * x[l * (TB + 1) + col];
+                sv[h] = acc;
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {  // S into the (still zero) X_{bi,bj} slots
+            const int e = threadIdx.x + h * 256;
+            if (e < total) {
+                const int bj = e / (PW * PW), r = (e / PW) % PW, c = e % PW;
+                x[(bi * PW + r) * (TB + 1) + bj * PW + c] = sv[h];
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {  // X_{bi,bj} = -X_ii S
+            const int e = threadIdx.x + h * 256;
+            if (e < total) {
+                const int bj = e / (PW * PW), r = (e / PW) % PW, c = e % PW;
+                double acc = 0.0;
+                for (int q = 0; q <= r; ++q)
+                    acc += x[(bi * PW + r) * (TB + 1) + bi * PW + q] * x[(bi * PW + q) * (TB + 1) + bj * PW + c];
+                sv[h] = -acc;
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int e = threadIdx.x + h * 256;
+            if (e < total) {
+                const int bj = e / (PW * PW), r = (e / PW) % PW, c = e % PW;
+                x[(bi * PW + r) * (TB + 1) + bj * PW + c] = sv[h];
+            }
+        }
+        __syncthreads();
+    }
     double* Dt = D + Doff[b] + (size_t)k * TB * TB;
     for (int e = threadIdx.x; e < TB * TB; e += blockDim.x) Dt[e] = x[(e / TB) * (TB + 1) + (e % TB)];
 }
@@ -299,19 +407,40 @@ __global__ void __launch_bounds__(128) k_tile_gemm(int k, const GTask* __restric
 }
 
 // compact inverse: Mc_b[r][c] = M[max(r,c)][min(r,c)] over the valid n_b x n_b part,
-// rows padded with zeros to ldm_b (a multiple of 4) so every row is 32-byte aligned
-__global__ void k_compact_inverse(const double* __restrict__ Lp, const long long* __restrict__ Poff,
-                                  const int* __restrict__ Tv, const int* __restrict__ nbv, const int* __restrict__ ldmv,
-                                  const long long* __restrict__ Moff, double* __restrict__ Mc)
+// rows padded with zeros to ldm_b (a multiple of 4) so every row is 32-byte aligned.
+// Tasks (block, tile row, tile col) of 32 x 32 output tiles; strictly-upper tiles read
+// the mirrored lower tile coalesced and transpose it through shared memory.
+__global__ void __launch_bounds__(256) k_compact_inverse(const double* __restrict__ Lp,
+                                                         const long long* __restrict__ Poff,
+                                                         const int* __restrict__ Tv, const int* __restrict__ nbv,
+                                                         const int* __restrict__ ldmv,
+                                                         const long long* __restrict__ Moff,
+                                                         const int4* __restrict__ tasks, double* __restrict__ Mc)
 {
-    const int b = blockIdx.x;
+    __shared__ double t[32][33];
+    const int4 tk = tasks[blockIdx.x];
+    const int b = tk.x, ti = tk.y, tj = tk.z;
     const int nb = nbv[b], ldm = ldmv[b];
     const size_t ld = (size_t)Tv[b] * TB;
     const double* M = Lp + Poff[b];
     double* out = Mc + Moff[b];
-    for (int r = blockIdx.y; r < nb; r += gridDim.y)
-        for (int c = threadIdx.x; c < ldm; c += blockDim.x)
-            out[(size_t)r * ldm + c] = c >= nb ? 0.0 : (r >= c ? M[(size_t)r * ld + c] : M[(size_t)c * ld + r]);
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    if (ti >= tj) {
+        for (int yy = ty; yy < 32; yy += 8) {
+            const int r = ti * 32 + yy, c = tj * 32 + tx;
+            if (r < nb && c < ldm) out[(size_t)r * ldm + c] = c >= nb ? 0.0 : (r >= c ? M[r * ld + c] : M[c * ld + r]);
+        }
+    } else {
+        for (int yy = ty; yy < 32; yy += 8) {
+            const int rr = tj * 32 + yy, cc = ti * 32 + tx;
+            t[yy][tx] = (rr < nb && cc < nb) ? M[rr * ld + cc] : 0.0;
+        }
+        __syncthreads();
+        for (int yy = ty; yy < 32; yy += 8) {
+            const int r = ti * 32 + yy, c = tj * 32 + tx;
+            if (r < nb && c < ldm) out[(size_t)r * ldm + c] = c >= nb ? 0.0 : t[tx][yy];
+        }
+    }
 }
 
 // ---------------------------------------------------------------- apply
@@ -511,6 +640,43 @@ __global__ void k_prec_scatter(const double* __restrict__ locy, const int* __res
     z[d] = out;
 }
 
+// H = R^T W R (schwarz.hpp:110-116 with the sparse R) into a padded ldh x ldh block
+void coarse_galerkin_device(Ctx* ctx, const DMatrix& W, const std::vector<int>& col_ptr, const int* cptr,
+                            const int* crow, const double* cval, int nc, int ldh, double* H)
+{
+    const int n = W.n;
+    cudaStream_t s = ctx->stream;
+    std::vector<int4> chunks;
+    std::vector<int> cfirst{0};
+    for (int c = 0; c < nc; ++c) {
+        for (int q = col_ptr[c]; q < col_ptr[c + 1]; q += kQC)
+            chunks.push_back(make_int4(c, q, std::min(q + kQC, col_ptr[c + 1]), (int)chunks.size()));
+        cfirst.push_back((int)chunks.size());
+    }
+    DBuf<double> WRt((size_t)n * std::max(nc, 1));
+    if (!chunks.empty()) {
+        DBuf<int4> d_chunks;
+        DBuf<int> d_cfirst;
+        d_chunks.upload(chunks, s);
+        d_cfirst.upload(cfirst, s);
+        DBuf<double> part((size_t)chunks.size() * n);
+        k_coarse_WR_chunks<<<dim3((unsigned)chunks.size(), (n + kIR - 1) / kIR), 256, 0, s>>>(W.a.p, W.ld, n,
+                                                                                         d_chunks.p, crow, cval,
+                                                                                         part.p);
+        count_launch();
+        k_coarse_WR_reduce<<<dim3((n + 255) / 256, nc), 256, 0, s>>>(part.p, d_cfirst.p, n, WRt.p);
+        count_launch();
+        SBG_LAUNCH_CHECK();
+        SBG_CUDA(cudaStreamSynchronize(s));
+    } else {
+        SBG_CUDA(cudaMemsetAsync(WRt.p, 0, WRt.n * sizeof(double), s));
+    }
+    k_coarse_Ht<<<ldh, 256, 0, s>>>(WRt.p, n, cptr, crow, cval, nc, ldh, H);
+    count_launch();
+    SBG_LAUNCH_CHECK();
+    SBG_CUDA(cudaStreamSynchronize(s));
+}
+
 template <int KIND>
 void launch_gemm(Ctx* ctx, Prec* P, int k, const GTask* dev_tasks, int count, double* Lp, double* Xp)
 {
@@ -570,9 +736,19 @@ void form_inverses(Ctx* ctx, Prec* P, DBuf<double>& Lwork, DBuf<double>& Mc)
     launch_gemm<K_LAUUM>(ctx, P, 0, d_la.p, (int)la.size(), Lwork.p, Xp.p);
     const long long Msize = P->h_Moff.empty() ? 0 : P->h_Moff.back() + (long long)P->h_nb.back() * P->h_ldm.back();
     Mc.alloc(std::max<long long>(Msize, 1));
-    k_compact_inverse<<<dim3(P->nblocks, 64), 128, 0, s>>>(Lwork.p, P->d_Poff.p, P->d_T.p, P->d_nb.p, P->d_ldm.p,
-                                                           P->d_Moff.p, Mc.p);
-    count_launch();
+    std::vector<int4> ct;
+    for (int b = 0; b < P->nblocks; ++b) {
+        const int tr = (P->h_nb[b] + 31) / 32, tc = (P->h_ldm[b] + 31) / 32;
+        for (int ti = 0; ti < tr; ++ti)
+            for (int tj = 0; tj < tc; ++tj) ct.push_back(make_int4(b, ti, tj, 0));
+    }
+    DBuf<int4> d_ct;
+    d_ct.upload(ct, s);
+    if (!ct.empty()) {
+        k_compact_inverse<<<(int)ct.size(), 256, 0, s>>>(Lwork.p, P->d_Poff.p, P->d_T.p, P->d_nb.p, P->d_ldm.p,
+                                                         P->d_Moff.p, d_ct.p, Mc.p);
+        count_launch();
+    }
     SBG_LAUNCH_CHECK();
     SBG_CUDA(cudaStreamSynchronize(s));
 }
@@ -659,8 +835,13 @@ Prec* prec_build(Ctx* ctx, const DMatrix& W, const DofPartition& part, const Pro
         P->d_bptr.upload(bptr, s);
         P->d_bdofs.upload(bdofs, s);
         if (ngather > 0) {  // factor_block's submatrix (schwarz.hpp:77-83)
-            k_gather_blocks<<<dim3(ngather, 64), 128, 0, s>>>(W.a.p, W.ld, P->d_bptr.p, P->d_bdofs.p, P->d_T.p,
-                                                              P->d_Poff.p, P->Lp.p);
+            std::vector<int2> gt;
+            for (int b = 0; b < ngather; ++b)
+                for (int r = 0; r < P->h_T[b] * TB; r += 8) gt.push_back({b, r});
+            DBuf<int2> d_gt;
+            d_gt.upload(gt, s);
+            k_gather_blocks<<<(int)gt.size(), 256, 0, s>>>(W.a.p, W.ld, P->d_bptr.p, P->d_bdofs.p, P->d_T.p,
+                                                           P->d_Poff.p, d_gt.p, P->Lp.p);
             count_launch();
             SBG_LAUNCH_CHECK();
             SBG_CUDA(cudaStreamSynchronize(s));
@@ -685,17 +866,10 @@ Prec* prec_build(Ctx* ctx, const DMatrix& W, const DofPartition& part, const Pro
             P->Rr_ptr.upload(rptr, s);
             P->Rr_col.upload(rcol, s);
             P->Rr_val.upload(rval, s);
-            DBuf<double> WR((size_t)n * P->nc);
             TimedScope ts(ctx, "coarse_galerkin");
-            k_coarse_WR<<<std::min(n, 8 * ctx->sm_count), 128, 0, s>>>(W.a.p, W.ld, n, P->Rc_ptr.p, P->Rc_row.p,
-                                                                      P->Rc_val.p, P->nc, WR.p);
-            count_launch();
             const int ldh = P->h_T[P->coarse_block] * TB;
-            k_coarse_H<<<ldh, 128, 0, s>>>(WR.p, P->Rc_ptr.p, P->Rc_row.p, P->Rc_val.p, P->nc, ldh,
-                                           P->Lp.p + P->h_Poff[P->coarse_block]);
-            count_launch();
-            SBG_LAUNCH_CHECK();
-            SBG_CUDA(cudaStreamSynchronize(s));
+            coarse_galerkin_device(ctx, W, R.col_ptr, P->Rc_ptr.p, P->Rc_row.p, P->Rc_val.p, P->nc, ldh,
+                                   P->Lp.p + P->h_Poff[P->coarse_block]);
         }
         // ---- batched tiled Cholesky: per step k, potrf of tile (k,k), trsm of column k, trailing update
         DBuf<int> fail(std::max(P->nblocks, 1));
@@ -993,19 +1167,15 @@ Prec* prec_from_dense(Ctx* ctx, const DMatrix& Mdense)
 void coarse_galerkin(Ctx* ctx, const DMatrix& W, const Prolongation& R, std::vector<double>& H)
 {
     cudaStream_t s = ctx->stream;
-    const int n = W.n, nc = R.cols;
+    const int nc = R.cols;
     H.assign((size_t)nc * nc, 0.0);
     if (nc == 0) return;
     DBuf<int> cp, cr;
-    DBuf<double> cv, WR((size_t)n * nc), dH((size_t)nc * nc);
+    DBuf<double> cv, dH((size_t)nc * nc);
     cp.upload(R.col_ptr, s);
     cr.upload(R.row_idx, s);
     cv.upload(R.val, s);
-    k_coarse_WR<<<std::min(n, 8 * ctx->sm_count), 128, 0, s>>>(W.a.p, W.ld, n, cp.p, cr.p, cv.p, nc, WR.p);
-    count_launch();
-    k_coarse_H<<<nc, 128, 0, s>>>(WR.p, cp.p, cr.p, cv.p, nc, nc, dH.p);
-    count_launch();
-    SBG_LAUNCH_CHECK();
+    coarse_galerkin_device(ctx, W, R.col_ptr, cp.p, cr.p, cv.p, nc, nc, dH.p);
     SBG_CUDA(cudaMemcpyAsync(H.data(), dH.p, H.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
     SBG_CUDA(cudaStreamSynchronize(s));
 }
