@@ -25,6 +25,7 @@ namespace {
 constexpr int TB = 64;   // tile size
 constexpr int TLD = 68;  // padded shared-memory leading dimension (conflict-free DMMA fragments)
 constexpr int GEMV_ROWS = 8;  // one row per warp
+constexpr int kPanel = 8;     // tile columns per panel of the blocked factorisation / inversion
 enum { K_TRSM = 0, K_UPDATE = 1, K_XDIAG = 2, K_LAUUM = 3, K_XUPD = 4 };
 struct GTask {
     int b, i, j, pad;
@@ -284,33 +285,96 @@ __global__ void __launch_bounds__(256) k_potrf(int k, const int* __restrict__ bl
 }
 
 // ---------------------------------------------------------------- tile GEMMs on DMMA
-// stage a 64x64 tile (row-major, ld) into shared memory, optionally transposed
-__device__ __forceinline__ void stage(double* __restrict__ dst, const double* __restrict__ src, size_t ld, bool trans)
+// 64x64 output tile per CTA (4 warps x 32x32), K streamed in half tiles of 32 through a
+// two-stage cp.async pipeline.  Operands are staged as plain row copies in either
+// layout — [m][k] (a row-major tile whose rows are output rows) or [k][m] (a tile whose
+// rows are k) — and the DMMA fragments are read from whichever layout, so no operand is
+// ever transposed on the way into shared memory.  Row strides 36 ([m][k]) and 68
+// ([k][m]) keep both fragment reads bank-conflict free.
+constexpr int HS_MK = 36, HS_KM = 68;          // half-tile row strides (doubles)
+constexpr int HBUF = TB * HS_MK;               // >= 32 * HS_KM, doubles per staged half tile
+constexpr size_t GEMM_SMEM = 4 * HBUF * sizeof(double);
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem)
 {
-    if (!trans) {
-        for (int e = threadIdx.x; e < TB * TB; e += blockDim.x) dst[(e / TB) * TLD + (e % TB)] = src[(size_t)(e / TB) * ld + (e % TB)];
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait()
+{
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+// half h (k in [32h, 32h+32)) of a 64x64 row-major tile: KM = false -> [m][k] copy of the
+// columns, KM = true -> [k][m] copy of the rows
+template <bool KM>
+__device__ __forceinline__ void stage_half(double* __restrict__ dst, const double* __restrict__ src, size_t ld, int h)
+{
+    if (!KM) {
+        for (int e = threadIdx.x; e < TB * 16; e += blockDim.x) {
+            const int r = e >> 4, c = (e & 15) * 2;
+            cp_async16(dst + r * HS_MK + c, src + (size_t)r * ld + 32 * h + c);
+        }
     } else {
-        for (int e = threadIdx.x; e < TB * TB; e += blockDim.x) dst[(e % TB) * TLD + (e / TB)] = src[(size_t)(e / TB) * ld + (e % TB)];
+        for (int e = threadIdx.x; e < 32 * 32; e += blockDim.x) {
+            const int r = e >> 5, c = (e & 31) * 2;
+            cp_async16(dst + r * HS_KM + c, src + (size_t)(32 * h + r) * ld + c);
+        }
     }
 }
 
-// acc += As * Bs^T (As: rows = output rows, Bs: rows = output cols, k contiguous); 4 warps x 32x32
-__device__ __forceinline__ void mma_tiles(const double* __restrict__ As, const double* __restrict__ Bs, double (&acc)[4][4][2])
+// acc[m][n] += sum_k A[m][k] B'[k][n] over one half tile; AK: A staged [k][m]; BK: B staged
+// [k][n] (else [n][k], i.e. the product with the staged tile transposed)
+template <bool AK, bool BK>
+__device__ __forceinline__ void mma_half(const double* __restrict__ As, const double* __restrict__ Bs,
+                                         double (&acc)[4][4][2])
 {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int gid = lane >> 2, tig = lane & 3;
     const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
-#pragma unroll 4
-    for (int kk = 0; kk < TB; kk += 4) {
+#pragma unroll
+    for (int kk = 0; kk < 32; kk += 4) {
         double af[4], bf[4];
 #pragma unroll
-        for (int x = 0; x < 4; ++x) af[x] = As[(wm + 8 * x + gid) * TLD + kk + tig];
+        for (int x = 0; x < 4; ++x)
+            af[x] = AK ? As[(kk + tig) * HS_KM + wm + 8 * x + gid] : As[(wm + 8 * x + gid) * HS_MK + kk + tig];
 #pragma unroll
-        for (int y = 0; y < 4; ++y) bf[y] = Bs[(wn + 8 * y + gid) * TLD + kk + tig];
+        for (int y = 0; y < 4; ++y)
+            bf[y] = BK ? Bs[(kk + tig) * HS_KM + wn + 8 * y + gid] : Bs[(wn + 8 * y + gid) * HS_MK + kk + tig];
 #pragma unroll
         for (int x = 0; x < 4; ++x)
 #pragma unroll
             for (int y = 0; y < 4; ++y) dmma(acc[x][y][0], acc[x][y][1], af[x], bf[y]);
+    }
+}
+
+// acc += sum_{q < nq} op(A_q) op(B_q), tiles given by the callables (pointer, ld)
+template <bool AK, bool BK, class FA, class FB>
+__device__ __forceinline__ void gemm_pipeline(double* sm, int nq, FA tileA, FB tileB, size_t lda, size_t ldb,
+                                              double (&acc)[4][4][2])
+{
+    const int steps = 2 * nq;
+    if (steps == 0) return;
+    stage_half<AK>(sm, tileA(0), lda, 0);
+    stage_half<BK>(sm + HBUF, tileB(0), ldb, 0);
+    cp_commit();
+    for (int st = 0; st < steps; ++st) {
+        double* cur = sm + (st & 1) * 2 * HBUF;
+        if (st + 1 < steps) {
+            double* nxt = sm + ((st + 1) & 1) * 2 * HBUF;
+            const int q = (st + 1) >> 1, h = (st + 1) & 1;
+            stage_half<AK>(nxt, tileA(q), lda, h);
+            stage_half<BK>(nxt + HBUF, tileB(q), ldb, h);
+            cp_commit();
+            cp_wait<1>();
+        } else {
+            cp_wait<0>();
+        }
+        __syncthreads();
+        mma_half<AK, BK>(cur, cur + HBUF, acc);
+        __syncthreads();
     }
 }
 
@@ -330,9 +394,9 @@ __device__ __forceinline__ void for_acc(const double (&acc)[4][4][2], F f)
 }
 
 // KIND K_TRSM  : L(i,k) = L(i,k) D_k^T            (task.i = i)
-//      K_UPDATE: L(i,j) -= L(i,k) L(j,k)^T        (task.i, task.j)
+//      K_UPDATE: L(i,j) -= sum_{q=k0}^{k1-1} L(i,q) L(j,q)^T   (task.i, task.j, K range in task.pad)
 //      K_XDIAG : X(i,j) = -D_i S(i,j) (S accumulated in X), X(i,i) = D_i   (step k = i)
-//      K_XUPD  : X(i',j) += L(i',k) X(k,j)  for i' > k >= j          (step k)
+//      K_XUPD  : X(i',j) += sum_{q=k0}^{k1-1} L(i',q) X(q,j)          (K range in task.pad)
 //                (right-looking blocked L^-1: X(i,j) = -D_i sum_{q=j}^{i-1} L(i,q) X(q,j))
 //      K_LAUUM : M(i,j) = sum_{q=i}^{T-1} X(q,i)^T X(q,j)   (written over L)
 template <int KIND>
@@ -341,9 +405,7 @@ __global__ void __launch_bounds__(128) k_tile_gemm(int k, const GTask* __restric
                                                    double* __restrict__ Lp, double* __restrict__ Xp,
                                                    const double* __restrict__ D)
 {
-    extern __shared__ double sm[];
-    double* As = sm;
-    double* Bs = sm + TB * TLD;
+    extern __shared__ __align__(16) double sm[];
     const GTask t = tasks[blockIdx.x];
     const int T = Tv[t.b];
     const size_t ld = (size_t)T * TB;
@@ -357,23 +419,19 @@ __global__ void __launch_bounds__(128) k_tile_gemm(int k, const GTask* __restric
 #pragma unroll
         for (int y = 0; y < 4; ++y) acc[x][y][0] = acc[x][y][1] = 0.0;
 
-    if (KIND == K_TRSM || KIND == K_UPDATE) {
-        stage(As, tile(L, t.i, k), ld, false);
-        if (KIND == K_TRSM)
-            stage(Bs, Db + (size_t)k * TB * TB, TB, false);
-        else
-            stage(Bs, tile(L, t.j, k), ld, false);
-        __syncthreads();
-        mma_tiles(As, Bs, acc);
-        double* C = tile(L, t.i, KIND == K_TRSM ? k : t.j);
-        if (KIND == K_TRSM) __syncthreads();  // C aliases the staged A
-        for_acc(acc, [&](int r, int c, double v) {
-            double* dst = C + (size_t)r * ld + c;
-            if (KIND == K_TRSM)
-                *dst = v;
-            else
-                *dst -= v;
-        });
+    if (KIND == K_TRSM) {
+        gemm_pipeline<false, false>(
+            sm, 1, [&](int) { return (const double*)tile(L, t.i, k); },
+            [&](int) { return Db + (size_t)k * TB * TB; }, ld, (size_t)TB, acc);
+        double* C = tile(L, t.i, k);
+        for_acc(acc, [&](int r, int c, double v) { C[(size_t)r * ld + c] = v; });
+    } else if (KIND == K_UPDATE) {  // K range [k0, k1) packed in t.pad (panel-blocked trailing update)
+        const int k0 = t.pad >> 16, k1 = t.pad & 0xffff;
+        gemm_pipeline<false, false>(
+            sm, k1 - k0, [&](int q) { return (const double*)tile(L, t.i, k0 + q); },
+            [&](int q) { return (const double*)tile(L, t.j, k0 + q); }, ld, ld, acc);
+        double* C = tile(L, t.i, t.j);
+        for_acc(acc, [&](int r, int c, double v) { C[(size_t)r * ld + c] -= v; });
     } else if (KIND == K_XDIAG) {
         double* C = tile(X, t.i, t.j);
         if (t.i == t.j) {
@@ -381,26 +439,21 @@ __global__ void __launch_bounds__(128) k_tile_gemm(int k, const GTask* __restric
             for (int e = threadIdx.x; e < TB * TB; e += blockDim.x) C[(size_t)(e / TB) * ld + (e % TB)] = Di[e];
             return;
         }
-        stage(As, Db + (size_t)t.i * TB * TB, TB, false);
-        stage(Bs, C, ld, true);
-        __syncthreads();
-        mma_tiles(As, Bs, acc);
+        gemm_pipeline<false, true>(
+            sm, 1, [&](int) { return Db + (size_t)t.i * TB * TB; }, [&](int) { return (const double*)C; },
+            (size_t)TB, ld, acc);
         for_acc(acc, [&](int r, int c, double v) { C[(size_t)r * ld + c] = -v; });
-    } else if (KIND == K_XUPD) {
-        stage(As, tile(L, t.i, k), ld, false);
-        stage(Bs, tile(X, k, t.j), ld, true);
-        __syncthreads();
-        mma_tiles(As, Bs, acc);
+    } else if (KIND == K_XUPD) {  // K range [k0, k1) packed in t.pad
+        const int k0 = t.pad >> 16, k1 = t.pad & 0xffff;
+        gemm_pipeline<false, true>(
+            sm, k1 - k0, [&](int q) { return (const double*)tile(L, t.i, k0 + q); },
+            [&](int q) { return (const double*)tile(X, k0 + q, t.j); }, ld, ld, acc);
         double* C = tile(X, t.i, t.j);
         for_acc(acc, [&](int r, int c, double v) { C[(size_t)r * ld + c] += v; });
     } else {  // K_LAUUM
-        for (int q = t.i; q < T; ++q) {
-            __syncthreads();
-            stage(As, tile(X, q, t.i), ld, true);
-            stage(Bs, tile(X, q, t.j), ld, true);
-            __syncthreads();
-            mma_tiles(As, Bs, acc);
-        }
+        gemm_pipeline<true, true>(
+            sm, T - t.i, [&](int q) { return (const double*)tile(X, t.i + q, t.i); },
+            [&](int q) { return (const double*)tile(X, t.i + q, t.j); }, ld, ld, acc);
         double* C = tile(L, t.i, t.j);
         for_acc(acc, [&](int r, int c, double v) { C[(size_t)r * ld + c] = v; });
     }
@@ -681,7 +734,7 @@ template <int KIND>
 void launch_gemm(Ctx* ctx, Prec* P, int k, const GTask* dev_tasks, int count, double* Lp, double* Xp)
 {
     if (count <= 0) return;
-    const size_t smem = 2 * TB * TLD * sizeof(double);
+    const size_t smem = GEMM_SMEM;
     static bool configured = false;
     if (!configured) {
         SBG_CUDA(cudaFuncSetAttribute(k_tile_gemm<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -712,12 +765,19 @@ void form_inverses(Ctx* ctx, Prec* P, DBuf<double>& Lwork, DBuf<double>& Mc)
     StepTasks xd, xu;
     std::vector<GTask> la;
     for (int k = 0; k < P->Tmax; ++k) {
+        const int p0 = k - k % kPanel;
         for (int b = 0; b < P->nblocks; ++b) {
             const int T = P->h_T[b];
             if (T <= k) continue;
             for (int j = 0; j <= k; ++j) xd.all.push_back({b, k, j, 0});
-            for (int i = k + 1; i < T; ++i)
-                for (int j = 0; j <= k; ++j) xu.all.push_back({b, i, j, 0});
+            const int p1 = std::min(p0 + kPanel, T);
+            if (k + 1 < p1) {  // rows inside the panel: the contribution of row k only
+                for (int i = k + 1; i < p1; ++i)
+                    for (int j = 0; j <= k; ++j) xu.all.push_back({b, i, j, (k << 16) | (k + 1)});
+            } else {  // panel complete: rows below take K = the panel rows at once
+                for (int i = p1; i < T; ++i)
+                    for (int j = 0; j < p1; ++j) xu.all.push_back({b, i, j, (std::max(p0, j) << 16) | p1});
+            }
         }
         xd.close();
         xu.close();
@@ -880,14 +940,24 @@ Prec* prec_build(Ctx* ctx, const DMatrix& W, const DofPartition& part, const Pro
             SBG_CUDA(cudaFuncSetAttribute(k_potrf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_potrf));
             std::vector<int> pot, pot_off{0};
             StepTasks trsm, upd;
+            // panel-blocked right-looking: inside a panel of kPanel tile columns only the
+            // panel's own columns are updated per step; the trailing matrix takes one update
+            // with K = the whole panel when the panel is complete
             for (int k = 0; k < P->Tmax; ++k) {
+                const int p0 = k - k % kPanel;
                 for (int b = 0; b < P->nblocks; ++b) {
                     const int T = P->h_T[b];
                     if (T <= k) continue;
                     pot.push_back(b);
                     for (int i = k + 1; i < T; ++i) trsm.all.push_back({b, i, k, 0});
-                    for (int j = k + 1; j < T; ++j)
-                        for (int i = j; i < T; ++i) upd.all.push_back({b, i, j, 0});
+                    const int p1 = std::min(p0 + kPanel, T);
+                    if (k + 1 < p1) {
+                        for (int j = k + 1; j < p1; ++j)
+                            for (int i = j; i < T; ++i) upd.all.push_back({b, i, j, (k << 16) | (k + 1)});
+                    } else {
+                        for (int j = p1; j < T; ++j)
+                            for (int i = j; i < T; ++i) upd.all.push_back({b, i, j, (p0 << 16) | p1});
+                    }
                 }
                 pot_off.push_back((int)pot.size());
                 trsm.close();
