@@ -848,14 +848,13 @@ int sbg_fp64_peak(sbg_ctx* ctx, double* tflops)
 {
     return guard([&] { *tflops = fp64_peak_tflops(&ctx->c); });
 }
+// L2 flush between timed launches: write 256 MiB (> the 126 MB L2), then read another
+// 256 MiB, so the next timed kernel starts with a cold L2 holding only clean lines (a
+// write-only flush leaves ~126 MB of dirty lines whose write-back lands inside the
+// next timed kernel)
 int sbg_l2_flush(sbg_ctx* ctx)
 {
-    return guard([&] {
-        static DBuf<char> buf;
-        const size_t bytes = 256u << 20;  // > 126 MB L2
-        if (buf.n < bytes) buf.alloc(bytes);
-        SBG_CUDA(cudaMemsetAsync(buf.p, 1, bytes, ctx->c.stream));
-    });
+    return guard([&] { l2_flush(&ctx->c); });
 }
 
 }  // extern "C"

@@ -106,6 +106,7 @@ struct Ctx {
     std::shared_ptr<void> pcg_ws;  // cached PCG workspace (linalg.cu)
     std::shared_ptr<void> dl_ws;   // cached pinned download ring (context.cu)
     std::shared_ptr<void> near_ws; // cached near-field frontier buffers (assemble.cu)
+    std::shared_ptr<void> flush_ws; // L2 flush buffers (context.cu)
     ~Ctx();
 };
 

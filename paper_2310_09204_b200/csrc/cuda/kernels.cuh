@@ -38,6 +38,7 @@ __device__ __forceinline__ double rsqrt_fast(double r2)
 }
 
 double fp64_peak_tflops(Ctx* ctx);
+void l2_flush(Ctx* ctx);  // write 256 MiB then read 256 MiB: cold, clean L2
 
 // ---------------------------------------------------------------- matrices
 void matrix_alloc(Ctx* ctx, int n, DMatrix& M);

@@ -59,14 +59,27 @@ def report(path, out):
     raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(raw.splitlines()))
     h = rows[0]
+    units = {h[i]: rows[1][i] for i in range(min(len(h), len(rows[1])))}
+    # one launch per kernel: the longest (the representative large launch)
+    best = {}
+    for v in rows[2:]:
+        d = {h[i]: v[i] for i in range(min(len(h), len(v)))}
+        name = d.get("Kernel Name", "?").split("(")[0]
+        try:
+            dur = float(d.get("gpu__time_duration.sum", "0").replace(",", ""))
+        except ValueError:
+            dur = 0.0
+        if name not in best or dur > best[name][0]:
+            best[name] = (dur, d)
     with open(out, "w") as f:
         f.write(f"# ncu --set full summary: `{path}`\n\n")
-        for v in rows[2:]:
-            d = {h[i]: v[i] for i in range(min(len(h), len(v)))}
+        f.write("One launch per kernel (the longest captured); `--clock-control none`, cold caches and "
+                "serialised launches, so durations are not the live ones.\n\n")
+        for _, d in sorted(best.values(), key=lambda x: -x[0]):
             f.write(f"## `{d.get('Kernel Name', '?')[:120]}`\n\n| metric | value |\n|---|---:|\n")
             for key, label in WANT:
                 if key in d:
-                    f.write(f"| {label} (`{key}`) | {d[key]} |\n")
+                    f.write(f"| {label} (`{key}`) | {d[key]} {units.get(key, '')} |\n")
             stalls = []
             for k, val in d.items():
                 if k.startswith("smsp__average_warps_issue_stalled_") and k.endswith("_per_issue_active.ratio"):
