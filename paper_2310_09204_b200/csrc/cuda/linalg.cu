@@ -242,16 +242,18 @@ void gemv_plan(Ctx* ctx, int n, int ld, GemvPlan& plan)
 
 static void gemv_partial_launch(Ctx* ctx, const DMatrix& W, GemvPlan& plan, const double* x, const int* done)
 {
-    TimedScope ts(ctx, "gemv_f64");
     const size_t smem = (size_t)plan.rows_per_chunk * sizeof(double);
     k_gemv_partial<<<dim3(plan.strips, plan.chunks), kGemvThreads, smem, ctx->stream>>>(
         W.a.p, W.ld, W.n, x, plan.rows_per_chunk, plan.part.p, done); ::sbg::count_launch();
     SBG_LAUNCH_CHECK();
 }
 
+// "gemv_f64" times the whole matvec (partials + their reduction); inside PCG the
+// reduction is fused into k_pcg_alpha and the scope covers the partial pass
 void gemv(Ctx* ctx, const DMatrix& W, GemvPlan& plan, const double* x, double* y)
 {
     if (W.n == 0) return;
+    TimedScope ts(ctx, "gemv_f64");
     gemv_partial_launch(ctx, W, plan, x, nullptr);
     k_gemv_reduce<<<(W.n + 255) / 256, 256, 0, ctx->stream>>>(plan.part.p, plan.chunks, W.ld, W.n, y); ::sbg::count_launch();
     SBG_LAUNCH_CHECK();
@@ -394,7 +396,10 @@ void pcg_run(Ctx* ctx, const DMatrix& W, Prec* prec, const double* rhs, double* 
         if (w.hs->done || enqueued >= maxit) break;
         const int todo = std::min(batch, maxit - enqueued);
         for (int t = 0; t < todo; ++t) {
-            gemv_partial_launch(ctx, W, w.plan, p, done);
+            {
+                TimedScope ts(ctx, "gemv_f64");
+                gemv_partial_launch(ctx, W, w.plan, p, done);
+            }
             k_pcg_alpha<<<nb, 256, 0, s>>>(w.st.p, w.plan.part.p, w.plan.chunks, W.ld, n, p, Wp, w.partials.p);
             count_launch();
             k_pcg_update<<<nb, 256, 0, s>>>(w.st.p, x, r, p, Wp, n);
