@@ -235,8 +235,8 @@ void gemv_plan(Ctx* ctx, int n, int ld, GemvPlan& plan)
     const int target = 4 * ctx->sm_count;
     int chunks = std::max(1, (target + plan.strips - 1) / plan.strips);
     chunks = std::min(chunks, std::max(1, n / 32));
-    plan.rows_per_chunk = ((n + chunks - 1) / chunks + 7) / 8 * 8;
-    plan.chunks = (n + plan.rows_per_chunk - 1) / plan.rows_per_chunk;
+    plan.rows_per_chunk = std::max(8, ((n + chunks - 1) / chunks + 7) / 8 * 8);
+    plan.chunks = std::max(1, (n + plan.rows_per_chunk - 1) / plan.rows_per_chunk);
     plan.part.alloc((size_t)plan.chunks * ld);
 }
 
@@ -361,6 +361,12 @@ void pcg_run(Ctx* ctx, const DMatrix& W, Prec* prec, const double* rhs, double* 
     if (tol <= 0) throw ValidationError("pcg: tolerance must be positive");
     if (prec && prec_n(prec) != n) throw ValidationError("preconditioner length mismatch");
     if (maxit <= 0) maxit = std::max(10 * n, 100);
+    if (n == 0) {  // empty system: converged at iteration 0 (pcg.hpp:41-49 with r0 = 0)
+        out = PcgResult{};
+        out.converged = true;
+        out.history.assign(1, 0.0);
+        return;
+    }
     TimedScope tpcg(ctx, "pcg");
     cudaStream_t s = ctx->stream;
     PcgWork& w = pcg_work(ctx, W, maxit);

@@ -1,0 +1,78 @@
+"""Edge cases of the device path (GPU, `-m gpu`): empty DOF spaces, quadrature
+configuration, reproducibility of the atomic scatter, and input errors mapped to the
+reference's exception types (inc/common.hpp:16-26)."""
+import os
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+S = pytest.importorskip("paper_2310_09204_b200.screenbem")
+WORKERS = os.cpu_count() or 1
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    return S.Context(0)
+
+
+def check_W(Wg, Wo):
+    scale = np.abs(Wo).max()
+    bad = np.abs(Wg - Wo) > 1e-10 * np.abs(Wo) + 1e-13 * scale
+    assert not bad.any(), (bad.sum(), np.abs(Wg - Wo).max() / scale)
+    assert np.array_equal(Wg, Wg.T)
+
+
+def test_no_interior_dofs(ctx):
+    """A single triangle (and a two-triangle square) has only boundary vertices: n = 0."""
+    for m in (S.SurfaceMesh([[0, 0, 0], [1, 0, 0], [0, 1, 0]], [[0, 1, 2]]),
+              S.SurfaceMesh([[0, 0, 0], [1, 0, 0], [1, 1, 0], [0, 1, 0]], [[0, 1, 2], [0, 2, 3]])):
+        im = S.inflate(m)
+        assert im.n == 0
+        W = S.assemble_W(im, ctx=ctx)
+        assert W.n == 0 and W.download().shape == (0, 0)
+        assert S.assemble_rhs(im, [0.0, 0.0, 1.0], ctx=ctx).shape == (0,)
+        rep = S.pcg(W, None, np.zeros(0), 1e-8)
+        assert rep.converged and rep.iterations == 0
+
+
+def test_repeated_assembly_within_reorder_bound(ctx):
+    """fp64 atomics reorder the scatter: two assemblies agree to the reference's own
+    worker-reorder bound (tests/test_assemble.cpp:271-279), symmetry stays exact."""
+    im = S.inflate(S.make_builtin("bowtie:3"))
+    Wa = S.assemble_W(im, ctx=ctx).download()
+    Wb = S.assemble_W(im, ctx=ctx).download()
+    assert np.abs(Wa - Wb).max() <= 1e-13 * np.abs(Wa).max()
+    assert np.array_equal(Wa, Wa.T) and np.array_equal(Wb, Wb.T)
+
+
+def test_singular_order_and_threshold_configurations(ctx):
+    """QuadratureConfig (quadrature.hpp:12-16) other than the default: singular order 10
+    moves W by < 1e-8 max|W| (tests/test_assemble.cpp:260-269) and matches the oracle at
+    the same setting; a near threshold of 3 (more near-field recursion) matches too."""
+    m = S.make_builtin("bowtie:2")
+    im = S.inflate(m)
+    oim = O.inflate(O.Mesh(m.vertices, m.facets))
+    W8 = S.assemble_W(im, ctx=ctx).download()
+    W10 = S.assemble_W(im, S.QuadratureConfig(singular_order=10), ctx=ctx).download()
+    assert np.abs(W8 - W10).max() < 1e-8 * np.abs(W8).max()
+    check_W(W10, O.assemble_W(oim, O.QuadratureConfig(singular_order=10), workers=WORKERS))
+    W3 = S.assemble_W(im, S.QuadratureConfig(near_threshold=3.0), ctx=ctx).download()
+    check_W(W3, O.assemble_W(oim, O.QuadratureConfig(near_threshold=3.0), workers=WORKERS))
+
+
+def test_unsupported_far_order_is_a_validation_error(ctx):
+    im = S.inflate(S.make_builtin("bowtie:1"))
+    with pytest.raises(S.ValidationError, match="far_order"):
+        S.assemble_W(im, S.QuadratureConfig(far_order=5), ctx=ctx)
+
+
+def test_malformed_meshes_raise_validation_error(ctx):
+    with pytest.raises(S.ValidationError):
+        S.inflate(S.SurfaceMesh([[0, 0, 0], [1, 0, 0], [0, 1, 0]], [[0, 1, 3]]))
+    with pytest.raises(S.ValidationError):
+        S.inflate(S.SurfaceMesh([[0, 0, 0], [1, 0, 0], [np.nan, 1, 0]], [[0, 1, 2]]))
+    with pytest.raises(S.ValidationError):
+        S.inflate(S.SurfaceMesh([[0, 0, 0], [1, 0, 0], [2, 0, 0]], [[0, 1, 2]]))  # degenerate facet
