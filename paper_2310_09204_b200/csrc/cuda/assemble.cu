@@ -20,6 +20,8 @@
 #include <algorithm>
 #include <cmath>
 #include <numeric>
+#include <stdexcept>
+#include <string>
 
 #include "kernels.cuh"
 
@@ -33,13 +35,35 @@ namespace {
 
 constexpr int BS = 64;          // facets per block
 constexpr int FAR_THREADS = 256;
-constexpr int NF = 16;          // far rule points (far_order 4)
-constexpr int NN = 36;          // near rule points (far_order + 2 = 6)
+constexpr int NF = 16;          // far rule points at the default far_order 4
+constexpr int NN = 36;          // near rule points at the default ((far_order + 2)^2)
+constexpr int MAX_FAR_ORDER = 8;
+constexpr int NF_MAX = 64;      // far rule capacity, padded to a multiple of 4 (far_order <= 8)
+constexpr int NN_MAX = 112;     // near rule capacity, padded to a multiple of 16
 constexpr int SAUTER_THREADS = 128;
 constexpr int SAUTER_STAGE = 1024;  // rule points staged per smem pass
 
-__constant__ double c_far_u[NF], c_far_v[NF], c_far_w[NF];
-__constant__ double c_near_u[NN], c_near_v[NN], c_near_w[NN];
+// rule sizes for a far_order (quadrature.hpp:105-112: far rule of far_order, near
+// rule of far_order + 2), and the padded sizes the kernels are instantiated for
+struct RuleDims {
+    int far_order = 4, nf = NF, nfp = NF, nn = NN, nnp = NN;
+};
+RuleDims rule_dims(int far_order)
+{
+    if (far_order < 1 || far_order > MAX_FAR_ORDER)
+        throw ValidationError("far_order must be in [1, " + std::to_string(MAX_FAR_ORDER) + "] on the GPU path");
+    RuleDims r;
+    r.far_order = far_order;
+    r.nf = far_order * far_order;
+    r.nfp = (r.nf + 3) / 4 * 4;
+    r.nn = (far_order + 2) * (far_order + 2);
+    r.nnp = far_order == 4 ? NN : (r.nn + 15) / 16 * 16;  // the default keeps its exact-fit kernel
+    return r;
+}
+
+// rules padded with zero-weight points at the centroid (their terms add exact zeros)
+__constant__ double c_far_u[NF_MAX], c_far_v[NF_MAX], c_far_w[NF_MAX];
+__constant__ double c_near_u[NN_MAX], c_near_v[NN_MAX], c_near_w[NN_MAX];
 // composed split4 maps: for every child path of depth <= 5 (index (4^d-1)/3 + base-4 digits),
 // the barycentric weights (x32, exact dyadics) of the leaf vertices on the root vertices
 constexpr int NPATH = 1365;
@@ -155,7 +179,6 @@ __device__ void tile_contract_flush(const double* __restrict__ It, int fb, int g
 // satisfy dist >= 2 diam, so (|x|^2+|y|^2)/|x-y|^2 stays O(10) inside a tile and
 // ~1 between distant tiles: the rounding stays at the 1e-15 level.
 constexpr int FAR_PASS = 4;            // rule points of f held in registers per pass
-constexpr int FAR_NPASS = NF / FAR_PASS;
 struct XPts {
     double m2x[FAR_PASS], m2y[FAR_PASS], m2z[FAR_PASS], x2[FAR_PASS];  // -2x, -2y, -2z, |x|^2
 };
@@ -188,13 +211,14 @@ __device__ __forceinline__ double4 far_ypoint(const double* s, const double* o, 
 
 // sum_{q in pass} w_{4 pass + q} sum_j w_j / |x_q - y_j|  (16 y-points x 4 x-points); one
 // accumulator per x point, so the four evaluations per y point are independent chains
+template <int NFP>
 __device__ __forceinline__ double far_pass_sum(const XPts& X, const double4* __restrict__ Y, int pass)
 {
     double a[FAR_PASS];
 #pragma unroll
     for (int q = 0; q < FAR_PASS; ++q) a[q] = 0.0;
 #pragma unroll 2
-    for (int j = 0; j < NF; ++j) {
+    for (int j = 0; j < NFP; ++j) {
         const double4 y = Y[j];
         const double wj = c_far_w[j];
 #pragma unroll
@@ -209,15 +233,20 @@ __device__ __forceinline__ double far_pass_sum(const XPts& X, const double4* __r
     return acc;
 }
 
-constexpr size_t FAR_SMEM = (size_t)BS * (BS + 1) * 8 + (size_t)BS * NF * 32 + (size_t)BS * 6 * 8 + (size_t)BS * 4 * 4;
+constexpr size_t far_smem_bytes(int nfp)
+{
+    return (size_t)BS * (BS + 1) * 8 + (size_t)BS * nfp * 32 + (size_t)BS * 6 * 8 + (size_t)BS * 4 * 4;
+}
 
+// NFP: far rule size padded to a multiple of FAR_PASS (16 at the default far_order 4)
+template <int NFP>
 __global__ void __launch_bounds__(FAR_THREADS, 3)
     k_far_tiles(const TileInfo* __restrict__ tiles, GeoPtrs G, BlockPtrs B, double thr, double* __restrict__ W,
                 int ld, double inv_pi)
 {
     extern __shared__ __align__(16) unsigned char far_smem[];
-    double4* Ys = reinterpret_cast<double4*>(far_smem);                 // BS x 16 y-points (y, |y|^2)
-    double* It = reinterpret_cast<double*>(Ys + BS * NF);               // BS x (BS+1)
+    double4* Ys = reinterpret_cast<double4*>(far_smem);                 // BS x NFP y-points (y, |y|^2)
+    double* It = reinterpret_cast<double*>(Ys + BS * NFP);              // BS x (BS+1)
     double* gcr = It + BS * (BS + 1);                                   // cx, cy, cz, rad, diam, area
     int* gid = reinterpret_cast<int*>(gcr + BS * 6);
     int* gvid = gid + BS;
@@ -240,9 +269,9 @@ __global__ void __launch_bounds__(FAR_THREADS, 3)
     }
     for (int e = threadIdx.x; e < BS * (BS + 1); e += blockDim.x) It[e] = 0.0;
     __syncthreads();
-    for (int e = threadIdx.x; e < BS * NF; e += blockDim.x) {
-        const int g = gid[e / NF];
-        Ys[e] = g >= 0 ? far_ypoint(G.v + 9 * g, o, e % NF) : make_double4(0, 0, 0, 1);
+    for (int e = threadIdx.x; e < BS * NFP; e += blockDim.x) {
+        const int g = gid[e / NFP];
+        Ys[e] = g >= 0 ? far_ypoint(G.v + 9 * g, o, e % NFP) : make_double4(0, 0, 0, 1);
     }
     __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -272,12 +301,12 @@ __global__ void __launch_bounds__(FAR_THREADS, 3)
             }
         }
         const double sf = G.area[f] * inv_pi;
-        for (int pass = 0; pass < FAR_NPASS; ++pass) {
+        for (int pass = 0; pass < NFP / FAR_PASS; ++pass) {
             XPts X;
             far_xpoints(G.v + 9 * f, o, pass, X);
             for (int m = 0, gl = warp >> 1; gl < BS; gl += FAR_THREADS / 64, ++m) {
                 if (!(mask >> m & 1)) continue;
-                It[fl * (BS + 1) + gl] += far_pass_sum(X, Ys + gl * NF, pass) * sf * gcr[gl * 6 + 5];
+                It[fl * (BS + 1) + gl] += far_pass_sum<NFP>(X, Ys + gl * NFP, pass) * sf * gcr[gl * 6 + 5];
             }
         }
     }
@@ -536,6 +565,117 @@ __global__ void __launch_bounds__(NEAR_LEAF_THREADS, 2) k_near_leaves(const Near
     }
 }
 
+// Near leaves for a non-default far_order: the same layout as k_near_leaves with the
+// near rule padded to NNP (a multiple of 16) by zero-weight points, so lane xg takes
+// the x groups xg, xg + 4, ... against all NNP y points; 4 warps per CTA keep the
+// staged y points within shared memory for the larger rules.
+constexpr int NEAR_G_THREADS = 128;
+template <int NNP>
+__global__ void __launch_bounds__(NEAR_G_THREADS) k_near_leaves_g(const NearNode* __restrict__ leaves,
+                                                                  const unsigned long long* __restrict__ nleaves_dev,
+                                                                  long long cap, const int2* __restrict__ pairs,
+                                                                  const double* __restrict__ GV,
+                                                                  const double* __restrict__ GA, double inv_pi,
+                                                                  double* __restrict__ out)
+{
+    extern __shared__ __align__(16) unsigned char near_g_smem[];
+    constexpr int WARPS = NEAR_G_THREADS / 32;
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int h = lane >> 2, xg = lane & 3;
+    double4* Ys = reinterpret_cast<double4*>(near_g_smem) + ((size_t)wib * 8 + h) * NNP;
+    const long long nl = min((long long)*nleaves_dev, cap);
+    const long long warps = (long long)gridDim.x * WARPS;
+    for (long long w = (long long)blockIdx.x * WARPS + wib; 8 * w < nl; w += warps) {
+        const long long q = 8 * w + h;
+        const bool active = q < nl;
+        double acc = 0.0, scale = 0.0;
+        double f1x = 0, f1y = 0, f1z = 0, f2x = 0, f2y = 0, f2z = 0;
+        int pair = 0;
+        __syncwarp();
+        if (active) {
+            const NearNode nd = leaves[q];
+            pair = nd.pair;
+            const int2 pr = pairs[nd.pair];
+            const int depth = nd.code & 7;
+            int it = 0, is = 0, dt = 0, ds = 0;
+            for (int lv = 0; lv < depth; ++lv) {
+                const unsigned e = (nd.code >> (3 + 3 * lv)) & 7;
+                if (e & 1) {
+                    it = 4 * it + (int)(e >> 1);
+                    ++dt;
+                } else {
+                    is = 4 * is + (int)(e >> 1);
+                    ++ds;
+                }
+            }
+            double t[9], s[9];
+            path_triangle(GV + 9 * pr.x, ((1 << 2 * dt) - 1) / 3 + it, t);
+            path_triangle(GV + 9 * pr.y, ((1 << 2 * ds) - 1) / 3 + is, s);
+            scale = __ldg(GA + pr.x) * __ldg(GA + pr.y) * ldexp(inv_pi, -2 * (dt + ds));
+            const double e1x = s[3] - s[0], e1y = s[4] - s[1], e1z = s[5] - s[2];
+            const double e2x = s[6] - s[0], e2y = s[7] - s[1], e2z = s[8] - s[2];
+            const double bx = s[0] - t[0], by = s[1] - t[1], bz = s[2] - t[2];
+            for (int j = xg; j < NNP; j += 4) {
+                const double yx = fma(c_near_v[j], e2x, fma(c_near_u[j], e1x, bx));
+                const double yy = fma(c_near_v[j], e2y, fma(c_near_u[j], e1y, by));
+                const double yz = fma(c_near_v[j], e2z, fma(c_near_u[j], e1z, bz));
+                Ys[j] = make_double4(yx, yy, yz, fma(yx, yx, fma(yy, yy, yz * yz)));
+            }
+            f1x = t[3] - t[0], f1y = t[4] - t[1], f1z = t[5] - t[2];
+            f2x = t[6] - t[0], f2y = t[7] - t[1], f2z = t[8] - t[2];
+        }
+        __syncwarp();
+        if (active) {
+#pragma unroll 1
+            for (int g = xg; g < NNP / NEAR_XP; g += 4) {
+                double mx[NEAR_XP], my[NEAR_XP], mz[NEAR_XP], x2[NEAR_XP], a[NEAR_XP];
+#pragma unroll
+                for (int r = 0; r < NEAR_XP; ++r) {
+                    const int i = NEAR_XP * g + r;
+                    const double xx = fma(c_near_v[i], f2x, c_near_u[i] * f1x);
+                    const double xy = fma(c_near_v[i], f2y, c_near_u[i] * f1y);
+                    const double xz = fma(c_near_v[i], f2z, c_near_u[i] * f1z);
+                    x2[r] = fma(xx, xx, fma(xy, xy, xz * xz));
+                    mx[r] = -2.0 * xx;
+                    my[r] = -2.0 * xy;
+                    mz[r] = -2.0 * xz;
+                    a[r] = 0.0;
+                }
+#pragma unroll 2
+                for (int j = 0; j < NNP; ++j) {
+                    const double4 y = Ys[j];
+                    const double wj = c_near_w[j];
+#pragma unroll
+                    for (int r = 0; r < NEAR_XP; ++r) {
+                        const double r2 = fma(mx[r], y.x, fma(my[r], y.y, fma(mz[r], y.z, x2[r] + y.w)));
+                        a[r] = fma(wj, rsqrt_fast(r2), a[r]);
+                    }
+                }
+#pragma unroll
+                for (int r = 0; r < NEAR_XP; ++r) acc = fma(c_near_w[NEAR_XP * g + r], a[r], acc);
+            }
+        }
+        for (int o = 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (active && xg == 0) atomicAdd(out + pair, acc * scale);
+    }
+}
+
+template <int NNP>
+void launch_near_leaves_g(Ctx* ctx, const NearNode* leaves, const unsigned long long* cnt, long long ncur,
+                          const int2* pairs, const double* GV, const double* GA, double* out)
+{
+    const size_t smem = (size_t)(NEAR_G_THREADS / 32) * 8 * NNP * sizeof(double4);
+    static bool attr = false;
+    if (!attr) {
+        SBG_CUDA(cudaFuncSetAttribute(k_near_leaves_g<NNP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = true;
+    }
+    const long long warps = (ncur + 7) / 8;
+    const int grid = (int)std::min<long long>((warps + NEAR_G_THREADS / 32 - 1) / (NEAR_G_THREADS / 32),
+                                              4LL * ctx->sm_count);
+    k_near_leaves_g<NNP><<<grid, NEAR_G_THREADS, smem, ctx->stream>>>(leaves, cnt, ncur, pairs, GV, GA, 1.0 / M_PI, out);
+}
+
 // ---------------------------------------------------------------- Sauter (singular) pairs
 // pairs: 6 ints per pair = permuted vertex ids of t then s (quadrature.hpp:297-322)
 __global__ void __launch_bounds__(SAUTER_THREADS)
@@ -670,13 +810,13 @@ __global__ void k_mirror(double* __restrict__ W, int n, int ld)
 }
 
 // ---------------------------------------------------------------- RHS (assemble.hpp:143-184)
-__global__ void k_rhs(int nf, const double* __restrict__ GV, const double* __restrict__ onormal,
+__global__ void k_rhs(int nf, int nr, const double* __restrict__ GV, const double* __restrict__ onormal,
                       const double* __restrict__ g, int g_is_field, const int* __restrict__ sptr,
                       const int* __restrict__ sdof, const double* __restrict__ ssgn, double* __restrict__ L)
 {
     const int e = blockIdx.x * blockDim.x + threadIdx.x;
-    if (e >= nf * NF) return;
-    const int f = e / NF, i = e % NF;
+    if (e >= nf * nr) return;
+    const int f = e / nr, i = e % nr;
     const double* t = GV + 9 * f;
     const double meas = tri_area(t);
     const double u = c_far_u[i], v = c_far_v[i], w = c_far_w[i] * 2.0 * meas;
@@ -704,22 +844,48 @@ std::uint64_t spread3(std::uint64_t x)
     return x;
 }
 
-void upload_rules(Ctx* ctx, const QuadCfg& cfg)
+RuleDims upload_rules(Ctx* ctx, const QuadCfg& cfg)
 {
-    if (cfg.far_order != 4)
-        throw ValidationError("the GPU assembly path is specialised for far_order 4 (the reference default)");
-    const TriangleRule far = triangle_rule(4), nr = triangle_rule(6);
+    const RuleDims R = rule_dims(cfg.far_order);
+    // the rules of quadrature.hpp:105-112, padded with zero-weight centroid points
+    static std::mutex mu;
+    static std::map<int, std::shared_ptr<const std::vector<double>>> cache;  // far_order -> u,v,w far | u,v,w near
+    std::shared_ptr<const std::vector<double>> rules;
+    {
+        std::lock_guard<std::mutex> lock(mu);
+        auto& slot = cache[R.far_order];
+        if (!slot) {
+            auto buf = std::make_shared<std::vector<double>>(3 * NF_MAX + 3 * NN_MAX, 0.0);
+            const TriangleRule far = triangle_rule(R.far_order), nr = triangle_rule(R.far_order + 2);
+            for (int i = 0; i < NF_MAX; ++i) {
+                const bool real = i < R.nf;
+                (*buf)[i] = real ? far.u[i] : 1.0 / 3.0;
+                (*buf)[NF_MAX + i] = real ? far.v[i] : 1.0 / 3.0;
+                (*buf)[2 * NF_MAX + i] = real ? far.w[i] : 0.0;
+            }
+            double* nb = buf->data() + 3 * NF_MAX;
+            for (int i = 0; i < NN_MAX; ++i) {
+                const bool real = i < R.nn;
+                nb[i] = real ? nr.u[i] : 1.0 / 3.0;
+                nb[NN_MAX + i] = real ? nr.v[i] : 1.0 / 3.0;
+                nb[2 * NN_MAX + i] = real ? nr.w[i] : 0.0;
+            }
+            slot = buf;
+        }
+        rules = slot;
+    }
     cudaStream_t s = ctx->stream;
-    SBG_CUDA(cudaMemcpyToSymbolAsync(c_far_u, far.u.data(), NF * sizeof(double), 0, cudaMemcpyHostToDevice, s));
-    SBG_CUDA(cudaMemcpyToSymbolAsync(c_far_v, far.v.data(), NF * sizeof(double), 0, cudaMemcpyHostToDevice, s));
-    SBG_CUDA(cudaMemcpyToSymbolAsync(c_far_w, far.w.data(), NF * sizeof(double), 0, cudaMemcpyHostToDevice, s));
-    SBG_CUDA(cudaMemcpyToSymbolAsync(c_near_u, nr.u.data(), NN * sizeof(double), 0, cudaMemcpyHostToDevice, s));
-    SBG_CUDA(cudaMemcpyToSymbolAsync(c_near_v, nr.v.data(), NN * sizeof(double), 0, cudaMemcpyHostToDevice, s));
-    SBG_CUDA(cudaMemcpyToSymbolAsync(c_near_w, nr.w.data(), NN * sizeof(double), 0, cudaMemcpyHostToDevice, s));
+    const double* rb = rules->data();
+    SBG_CUDA(cudaMemcpyToSymbolAsync(c_far_u, rb, NF_MAX * sizeof(double), 0, cudaMemcpyHostToDevice, s));
+    SBG_CUDA(cudaMemcpyToSymbolAsync(c_far_v, rb + NF_MAX, NF_MAX * sizeof(double), 0, cudaMemcpyHostToDevice, s));
+    SBG_CUDA(cudaMemcpyToSymbolAsync(c_far_w, rb + 2 * NF_MAX, NF_MAX * sizeof(double), 0, cudaMemcpyHostToDevice, s));
+    rb += 3 * NF_MAX;
+    SBG_CUDA(cudaMemcpyToSymbolAsync(c_near_u, rb, NN_MAX * sizeof(double), 0, cudaMemcpyHostToDevice, s));
+    SBG_CUDA(cudaMemcpyToSymbolAsync(c_near_v, rb + NN_MAX, NN_MAX * sizeof(double), 0, cudaMemcpyHostToDevice, s));
+    SBG_CUDA(cudaMemcpyToSymbolAsync(c_near_w, rb + 2 * NN_MAX, NN_MAX * sizeof(double), 0, cudaMemcpyHostToDevice, s));
     // composed split4 maps (quadrature.hpp:222-229 child order), weights x32
-    static std::vector<unsigned char> paths;
-    if (paths.empty()) {
-        paths.resize(NPATH * 9);
+    static const std::vector<unsigned char> paths = [] {
+        std::vector<unsigned char> paths(NPATH * 9);
         int idx = 0;
         for (int d = 0; d <= 5; ++d) {
             int count = 1;
@@ -750,8 +916,10 @@ void upload_rules(Ctx* ctx, const QuadCfg& cfg)
                     for (int c = 0; c < 3; ++c) paths[9 * idx + 3 * r + c] = (unsigned char)B[r][c];
             }
         }
-    }
+        return paths;
+    }();
     SBG_CUDA(cudaMemcpyToSymbolAsync(c_paths, paths.data(), paths.size(), 0, cudaMemcpyHostToDevice, s));
+    return R;
 }
 
 struct DeviceGeometry {
@@ -918,7 +1086,7 @@ __global__ void k_near_init(const unsigned long long* __restrict__ np_dev, long 
 }
 
 // near-pair integrals for the device list pairs[0:*np_dev] (capacity cap); returns the leaf count
-long long run_near(Ctx* ctx, const double* GV, const double* GA, const int2* pairs,
+long long run_near(Ctx* ctx, const RuleDims& R, const double* GV, const double* GA, const int2* pairs,
                    const unsigned long long* np_dev, long long cap, double thr, double* out, NearWork& NW)
 {
     if (cap <= 0) return 0;
@@ -965,7 +1133,18 @@ long long run_near(Ctx* ctx, const double* GV, const double* GA, const int2* pai
             TimedScope tl(ctx, "near_leaves");
             const long long warps = (ncur + 7) / 8;  // upper bound on this level's leaf octets
             const int lgrid = (int)std::min<long long>((warps + NEAR_LEAF_WARPS - 1) / NEAR_LEAF_WARPS, 2LL * ctx->sm_count);
-            k_near_leaves<<<lgrid, NEAR_LEAF_THREADS, NEAR_LEAF_SMEM, s>>>(NW.leaves.p, NW.cnt.p + 2, ncur, pairs, GV, GA, 1.0 / M_PI, out);
+            if (R.nnp == NN) {
+                k_near_leaves<<<lgrid, NEAR_LEAF_THREADS, NEAR_LEAF_SMEM, s>>>(NW.leaves.p, NW.cnt.p + 2, ncur, pairs,
+                                                                               GV, GA, 1.0 / M_PI, out);
+            } else {
+                switch (R.nnp) {
+#define SBG_NEAR_G(N) \
+    case N: launch_near_leaves_g<N>(ctx, NW.leaves.p, NW.cnt.p + 2, ncur, pairs, GV, GA, out); break;
+                    SBG_NEAR_G(16) SBG_NEAR_G(32) SBG_NEAR_G(48) SBG_NEAR_G(64) SBG_NEAR_G(96) SBG_NEAR_G(112)
+#undef SBG_NEAR_G
+                default: throw std::logic_error("near rule size not instantiated");
+                }
+            }
             count_launch();
         }
         SBG_LAUNCH_CHECK();
@@ -981,12 +1160,41 @@ long long run_near(Ctx* ctx, const double* GV, const double* GA, const int2* pai
 
 }  // namespace
 
+template <int NFP>
+void launch_far_tiles_n(Ctx* ctx, const TileInfo* tiles, long long ntiles, const GeoPtrs& G, const BlockPtrs& BP,
+                        double thr, DMatrix& W)
+{
+    constexpr size_t smem = far_smem_bytes(NFP);
+    static bool attr = false;
+    if (!attr) {
+        SBG_CUDA(cudaFuncSetAttribute(k_far_tiles<NFP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = true;
+    }
+    k_far_tiles<NFP><<<(int)ntiles, FAR_THREADS, smem, ctx->stream>>>(tiles, G, BP, thr, W.a.p, W.ld, 1.0 / M_PI);
+}
+
+void launch_far_tiles(Ctx* ctx, const RuleDims& R, const TileInfo* tiles, long long ntiles, const GeoPtrs& G,
+                      const BlockPtrs& BP, double thr, DMatrix& W)
+{
+    if (ntiles <= 0) return;
+    switch (R.nfp) {
+#define SBG_FAR_TILES(N) \
+    case N: launch_far_tiles_n<N>(ctx, tiles, ntiles, G, BP, thr, W); break;
+        SBG_FAR_TILES(4) SBG_FAR_TILES(12) SBG_FAR_TILES(16) SBG_FAR_TILES(28) SBG_FAR_TILES(36) SBG_FAR_TILES(52)
+        SBG_FAR_TILES(64)
+#undef SBG_FAR_TILES
+    default: throw std::logic_error("far rule size not instantiated");
+    }
+    count_launch();
+}
+
 // ---------------------------------------------------------------- assembly plan
 // Host-side preparation of one mesh (facet blocks, curl lists, tile list,
 // singular lists, rules), uploaded once; assembly_run only launches kernels.
 struct AssemblyPlan {
     Ctx* ctx = nullptr;
     QuadCfg cfg;
+    RuleDims dims;
     int nf = 0, n = 0;
     DeviceGeometry G;
     DBuf<int> uptr, udof;
@@ -1020,7 +1228,7 @@ AssemblyPlan* assembly_plan_create(Ctx* ctx, const InflatedMesh& im, const QuadC
         P->nf = nf;
         P->n = im.num_jump_dofs();
         if (nf == 0 || P->n == 0) return P;
-        upload_rules(ctx, cfg);
+        P->dims = upload_rules(ctx, cfg);
         upload_geometry(ctx, m, P->G);
         HostScope hs1(ctx, "plan_curls");
         const FacetCurls U = facet_curls(im);
@@ -1170,7 +1378,7 @@ void assembly_run(AssemblyPlan* P, DMatrix& W, AssemblyStats* stats)
     if (W.n != P->n || !W.a.p) matrix_alloc(ctx, P->n, W);
     else SBG_CUDA(cudaMemsetAsync(W.a.p, 0, W.a.n * sizeof(double), s));
     if (P->nf == 0 || P->n == 0) return;
-    upload_rules(ctx, P->cfg);
+    const RuleDims R = upload_rules(ctx, P->cfg);
     const double thr = P->cfg.near_threshold;
     // near list (classification of the non-certainly-far tiles)
     long long leaves = 0;
@@ -1184,7 +1392,7 @@ void assembly_run(AssemblyPlan* P, DMatrix& W, AssemblyStats* stats)
             count_launch();
             SBG_LAUNCH_CHECK();
         }
-        leaves = run_near(ctx, P->G.v.p, P->G.area.p, P->loc_pairs.p + P->nsing, P->near_cnt.p, P->near_cap, thr,
+        leaves = run_near(ctx, R, P->G.v.p, P->G.area.p, P->loc_pairs.p + P->nsing, P->near_cnt.p, P->near_cap, thr,
                           P->loc_I.p + P->nsing, near_work(ctx));
         SBG_CUDA(cudaMemcpyAsync(&nnear, P->near_cnt.p, sizeof(nnear), cudaMemcpyDeviceToHost, s));
         SBG_CUDA(cudaStreamSynchronize(s));
@@ -1217,14 +1425,7 @@ void assembly_run(AssemblyPlan* P, DMatrix& W, AssemblyStats* stats)
     {
         TimedScope ts(ctx, "far_tiles");
         BlockPtrs BP{P->bfac.p, P->dof_ptr.p, P->dofs.p, P->ent_ptr.p, P->ents.p};
-        static bool attr = false;
-        if (!attr) {
-            SBG_CUDA(cudaFuncSetAttribute(k_far_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FAR_SMEM));
-            attr = true;
-        }
-        k_far_tiles<<<(int)P->ntiles, FAR_THREADS, FAR_SMEM, s>>>(P->tiles.p, P->G.ptrs(), BP, thr, W.a.p, W.ld,
-                                                                  1.0 / M_PI);
-        count_launch();
+        launch_far_tiles(ctx, R, P->tiles.p, P->ntiles, P->G.ptrs(), BP, thr, W);
         SBG_LAUNCH_CHECK();
     }
     // per-pair scatter of singular + near integrals
@@ -1269,6 +1470,7 @@ void assemble_W(Ctx* ctx, const InflatedMesh& im, const QuadCfg& cfg, DMatrix& W
 }
 
 namespace {
+template <int NFP>
 __global__ void k_far_pair_list(GeoPtrs G, const int2* __restrict__ pairs, long long np, double* __restrict__ out,
                                 double inv_pi)
 {
@@ -1277,19 +1479,29 @@ __global__ void k_far_pair_list(GeoPtrs G, const int2* __restrict__ pairs, long 
     const int f = pairs[k].x, g = pairs[k].y;
     const double* t = G.v + 9 * f;
     const double* sv = G.v + 9 * g;
-    double4 Y[NF];
-    for (int j = 0; j < NF; ++j) Y[j] = far_ypoint(sv, t, j);
+    double4 Y[NFP];
+    for (int j = 0; j < NFP; ++j) Y[j] = far_ypoint(sv, t, j);
     double acc = 0.0;
-    for (int pass = 0; pass < FAR_NPASS; ++pass) {
+    for (int pass = 0; pass < NFP / FAR_PASS; ++pass) {
         XPts X;
         far_xpoints(t, t, pass, X);
-        acc += far_pass_sum(X, Y, pass) * (G.area[f] * inv_pi) * G.area[g];
+        acc += far_pass_sum<NFP>(X, Y, pass) * (G.area[f] * inv_pi) * G.area[g];
     }
     out[k] = acc;
 }
-void far_pair_list(Ctx* ctx, const GeoPtrs& G, const int2* pairs, long long np, double* out)
+void far_pair_list(Ctx* ctx, const RuleDims& R, const GeoPtrs& G, const int2* pairs, long long np, double* out)
 {
-    k_far_pair_list<<<(int)((np + 127) / 128), 128, 0, ctx->stream>>>(G, pairs, np, out, 1.0 / M_PI); ::sbg::count_launch();
+    const int grid = (int)((np + 127) / 128);
+    cudaStream_t s = ctx->stream;
+    switch (R.nfp) {
+#define SBG_FAR_LIST(N) \
+    case N: k_far_pair_list<N><<<grid, 128, 0, s>>>(G, pairs, np, out, 1.0 / M_PI); break;
+        SBG_FAR_LIST(4) SBG_FAR_LIST(12) SBG_FAR_LIST(16) SBG_FAR_LIST(28) SBG_FAR_LIST(36) SBG_FAR_LIST(52)
+        SBG_FAR_LIST(64)
+#undef SBG_FAR_LIST
+    default: throw std::logic_error("far rule size not instantiated");
+    }
+    ::sbg::count_launch();
     SBG_LAUNCH_CHECK();
 }
 
@@ -1302,7 +1514,7 @@ void pair_integrals(Ctx* ctx, const SurfaceMesh& m, const QuadCfg& cfg, const in
                     double* out)
 {
     cudaStream_t s = ctx->stream;
-    upload_rules(ctx, cfg);
+    const RuleDims R = upload_rules(ctx, cfg);
     DeviceGeometry G;
     upload_geometry(ctx, m, G);
     SauterRulesDev SR;
@@ -1378,7 +1590,7 @@ void pair_integrals(Ctx* ctx, const SurfaceMesh& m, const QuadCfg& cfg, const in
         const unsigned long long hn = nearp.size();
         SBG_CUDA(cudaMemcpyAsync(cnt.p, &hn, sizeof(hn), cudaMemcpyHostToDevice, s));
         NearWork NW;
-        run_near(ctx, G.v.p, G.area.p, d_p.p, cnt.p, (long long)nearp.size(), cfg.near_threshold, o.p, NW);
+        run_near(ctx, R, G.v.p, G.area.p, d_p.p, cnt.p, (long long)nearp.size(), cfg.near_threshold, o.p, NW);
         fetch(o.p, idx[0]);
     }
     if (!farp.empty()) {
@@ -1388,7 +1600,7 @@ void pair_integrals(Ctx* ctx, const SurfaceMesh& m, const QuadCfg& cfg, const in
         DBuf<int2> d_p;
         d_p.upload(farp, s);
         DBuf<double> o(farp.size());
-        far_pair_list(ctx, G.ptrs(), d_p.p, (long long)farp.size(), o.p);
+        far_pair_list(ctx, R, G.ptrs(), d_p.p, (long long)farp.size(), o.p);
         fetch(o.p, idx[4]);
     }
 }
@@ -1417,7 +1629,8 @@ void assemble_rhs(Ctx* ctx, const InflatedMesh& im, const QuadCfg& cfg, const do
     cudaStream_t s = ctx->stream;
     const SurfaceMesh& m = im.base;
     const int nf = m.num_facets(), n = im.num_jump_dofs();
-    const size_t ng = g_is_field ? (size_t)nf * NF * 3 : 3;
+    const RuleDims R = rule_dims(cfg.far_order);
+    const size_t ng = g_is_field ? (size_t)nf * R.nf * 3 : 3;
     for (size_t i = 0; i < ng; ++i)
         if (!std::isfinite(g[i])) throw NumericalError("g returned a non-finite value");
     upload_rules(ctx, cfg);
@@ -1455,7 +1668,7 @@ void assemble_rhs(Ctx* ctx, const InflatedMesh& im, const QuadCfg& cfg, const do
     d_g.upload(g, ng, s);
     SBG_CUDA(cudaMemsetAsync(d_L.p, 0, d_L.n * sizeof(double), s));
     if (nf)
-        k_rhs<<<(nf * NF + 127) / 128, 128, 0, s>>>(nf, G.v.p, d_on.p, d_g.p, g_is_field ? 1 : 0, d_sptr.p, d_sdof.p,
+        k_rhs<<<(nf * R.nf + 127) / 128, 128, 0, s>>>(nf, R.nf, G.v.p, d_on.p, d_g.p, g_is_field ? 1 : 0, d_sptr.p, d_sdof.p,
                                                     d_ssgn.p, d_L.p); ::sbg::count_launch();
     SBG_LAUNCH_CHECK();
     if (n) SBG_CUDA(cudaMemcpyAsync(L_host, d_L.p, n * sizeof(double), cudaMemcpyDeviceToHost, s));

@@ -63,10 +63,24 @@ def test_singular_order_and_threshold_configurations(ctx):
     check_W(W3, O.assemble_W(oim, O.QuadratureConfig(near_threshold=3.0), workers=WORKERS))
 
 
-def test_unsupported_far_order_is_a_validation_error(ctx):
+@pytest.mark.parametrize("far_order", [1, 2, 3, 5, 6])
+def test_far_order_configurations_match_oracle(ctx, far_order):
+    """far_order sets both the far rule (far_order^2 points) and the near-leaf rule
+    ((far_order+2)^2, quadrature.hpp:105-112): the padded device rules reproduce the
+    oracle's W and RHS at every order."""
+    m = S.make_builtin("bowtie:2")
+    im = S.inflate(m)
+    oim = O.inflate(O.Mesh(m.vertices, m.facets))
+    cfg, ocfg = S.QuadratureConfig(far_order=far_order), O.QuadratureConfig(far_order=far_order)
+    check_W(S.assemble_W(im, cfg, ctx=ctx).download(), O.assemble_W(oim, ocfg, workers=WORKERS))
+    L, Lo = S.assemble_rhs(im, [0.3, -0.2, 1.0], cfg, ctx=ctx), O.assemble_rhs(oim, [0.3, -0.2, 1.0], ocfg)
+    np.testing.assert_allclose(L, Lo, rtol=1e-12, atol=1e-15 * np.abs(Lo).max())
+
+
+def test_far_order_out_of_range_is_a_validation_error(ctx):
     im = S.inflate(S.make_builtin("bowtie:1"))
     with pytest.raises(S.ValidationError, match="far_order"):
-        S.assemble_W(im, S.QuadratureConfig(far_order=5), ctx=ctx)
+        S.assemble_W(im, S.QuadratureConfig(far_order=9), ctx=ctx)
 
 
 def test_malformed_meshes_raise_validation_error(ctx):
