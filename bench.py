@@ -39,6 +39,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--clocks", default="nvml", choices=["nvml", "smi", "off"],
+                    help="clock/throttle sampler during the timed region (nvml: in-process NVML queries)")
     ap.add_argument("--no-cpu-phases", action="store_true",
                     help="skip the CPU restatement's setup/preconditioner/PCG timings")
     ap.add_argument("--cpu-phases-max-n", type=int, default=8000)
@@ -66,6 +68,67 @@ def reduce_max(values, dist=None, device="cpu"):
 
 
 # --------------------------------------------------------------------------- clocks
+class NvmlSampler:
+    """SM clock + throttle reasons sampled every 200 ms during the timed region through
+    in-process NVML (the nvidia-smi loop contends for the driver with the timed step)."""
+    REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20, "sw_power_cap": 0x4}
+
+    def __init__(self, device: int):
+        self.device, self.rows, self.stop, self.t = device, [], threading.Event(), None
+
+    def __enter__(self):
+        try:
+            import pynvml as N
+            N.nvmlInit()
+            h = N.nvmlDeviceGetHandleByIndex(self.device)
+            self.mx = N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM)
+            reasons_fn = getattr(N, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                N.nvmlDeviceGetCurrentClocksThrottleReasons
+
+            def run():
+                while True:
+                    try:
+                        sm = N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)
+                        r = reasons_fn(h)
+                        self.rows.append((sm, r))
+                    except Exception:
+                        pass
+                    if self.stop.wait(0.2):
+                        break
+            self.t = threading.Thread(target=run, daemon=True)
+            self.t.start()
+        except Exception:
+            self.t = None
+        return self
+
+    def __exit__(self, *a):
+        self.stop.set()
+        if self.t:
+            self.t.join(timeout=2)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = sorted(r[0] for r in self.rows)
+        reasons = sorted({k for _, bits in self.rows for k, m in self.REASONS.items() if bits & m})
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": self.mx, "reasons": reasons, "samples": len(self.rows),
+                "source": "NVML"}
+
+
+class NullSampler:
+    def __init__(self, device: int):
+        pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        pass
+
+    def summary(self):
+        return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled (--clocks off)"]}
+
+
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
@@ -276,7 +339,8 @@ def run_ours(args):
     iters = []
     if dist:
         dist.barrier()
-    with ClockSampler(local) as clocks:
+    sampler = {"nvml": NvmlSampler, "smi": ClockSampler, "off": NullSampler}[args.clocks]
+    with sampler(local) as clocks:
         for _ in range(args.steps):
             ctx.l2_flush()
             ctx.begin("step")
@@ -287,7 +351,8 @@ def run_ours(args):
     launches = S.launch_count() - launches0
     tm = {k: ctx.timer(k) for k in ("step", "assemble_W", "far_tiles", "near", "near_leaves", "sauter", "classify",
                                      "local_scatter", "mirror", "near_classify", "build_preconditioner", "cholesky",
-                                     "block_inverse", "coarse_galerkin", "pcg", "gemv_f64", "precond_apply")}
+                                     "block_inverse", "coarse_galerkin", "pcg", "gemv_f64", "precond_apply", "inv_alloc",
+                                     "inv_lower", "inv_lauum")}
     # per-step totals (a phase may run several launches per step, e.g. one near level each)
     ms = {k: v[0] / args.steps for k, v in tm.items()}
     launches_per_step = {k: v[1] / args.steps for k, v in tm.items()}

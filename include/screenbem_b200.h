@@ -208,6 +208,7 @@ int sbg_matvec_device(sbg_ctx* ctx, const sbg_matrix* W, const double* d_x, doub
 int sbg_apply_preconditioner_device(sbg_ctx* ctx, sbg_prec* p, const double* d_r, double* d_z, int reps);
 /* write a buffer larger than L2 (L2 flush between timed iterations) */
 int sbg_l2_flush(sbg_ctx* ctx);
+int sbg_pool_stats(sbg_ctx* ctx, long long* reserved, long long* used); /* device memory pool, bytes */
 /* measured DFMA throughput of this device (TFLOP/s), the FP64 roofline denominator */
 int sbg_fp64_peak(sbg_ctx* ctx, double* tflops);
 

@@ -852,6 +852,19 @@ int sbg_fp64_peak(sbg_ctx* ctx, double* tflops)
 // 256 MiB, so the next timed kernel starts with a cold L2 holding only clean lines (a
 // write-only flush leaves ~126 MB of dirty lines whose write-back lands inside the
 // next timed kernel)
+// device memory pool statistics (bytes): reserved by the pool, in use by allocations
+int sbg_pool_stats(sbg_ctx* ctx, long long* reserved, long long* used)
+{
+    return guard([&] {
+        cudaMemPool_t pool;
+        SBG_CUDA(cudaDeviceGetDefaultMemPool(&pool, ctx->c.device));
+        unsigned long long r = 0, u = 0;
+        SBG_CUDA(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &r));
+        SBG_CUDA(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &u));
+        *reserved = (long long)r;
+        *used = (long long)u;
+    });
+}
 int sbg_l2_flush(sbg_ctx* ctx)
 {
     return guard([&] { l2_flush(&ctx->c); });

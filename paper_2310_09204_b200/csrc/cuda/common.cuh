@@ -107,6 +107,8 @@ struct Ctx {
     std::shared_ptr<void> dl_ws;   // cached pinned download ring (context.cu)
     std::shared_ptr<void> near_ws; // cached near-field frontier buffers (assemble.cu)
     std::shared_ptr<void> flush_ws; // L2 flush buffers (context.cu)
+    std::shared_ptr<void> prec_sched; // last preconditioner task schedule (precond.cu)
+    std::shared_ptr<void> scratch_ws; // grow-only scratch buffers (context.cu: scratch())
     ~Ctx();
 };
 

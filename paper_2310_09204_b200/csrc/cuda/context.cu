@@ -252,6 +252,17 @@ __global__ void k_l2_read(const double4* __restrict__ src, size_t n, double* __r
 }
 }  // namespace
 
+double* scratch(Ctx* ctx, int slot, size_t count)
+{
+    struct Scratch {
+        DBuf<double> b[kScratchSlots];
+    };
+    if (!ctx->scratch_ws) ctx->scratch_ws = std::make_shared<Scratch>();
+    DBuf<double>& b = static_cast<Scratch*>(ctx->scratch_ws.get())->b[slot];
+    if (b.n < count) b.alloc(count + count / 8);
+    return b.p;
+}
+
 void l2_flush(Ctx* ctx)
 {
     const size_t bytes = 256u << 20;

@@ -39,6 +39,10 @@ __device__ __forceinline__ double rsqrt_fast(double r2)
 
 double fp64_peak_tflops(Ctx* ctx);
 void l2_flush(Ctx* ctx);  // write 256 MiB then read 256 MiB: cold, clean L2
+// grow-only device scratch buffer `slot` of at least `count` doubles, cached on the
+// context (large per-call temporaries: no pool growth or fragmentation between calls)
+enum { kScratchInverse = 0, kScratchCoarseWR = 1, kScratchCoarsePart = 2, kScratchSlots = 3 };
+double* scratch(Ctx* ctx, int slot, size_t count);
 
 // ---------------------------------------------------------------- matrices
 void matrix_alloc(Ctx* ctx, int n, DMatrix& M);

@@ -32,6 +32,10 @@ struct GTask {
 };
 }  // namespace
 
+namespace {
+struct PrecSchedule;
+}
+
 struct Prec {
     Ctx* ctx = nullptr;
     int n = 0, nfaces = 0, nwb = 0, nc = 0, mode = kPrecInverse;
@@ -47,12 +51,7 @@ struct Prec {
     // R in CSC (restriction, ascending rows) and CSR (prolongation, ascending cols)
     DBuf<int> Rc_ptr, Rc_row, Rr_ptr, Rr_col;
     DBuf<double> Rc_val, Rr_val;
-    // trsv tasks (block, tile row) per step
-    DBuf<int2> fwd_tasks, bwd_tasks;
-    std::vector<int> fwd_off, bwd_off;
-    // gemv tasks (block, first row)
-    DBuf<int2> gemv_tasks;
-    int ngemv = 0;
+    std::shared_ptr<PrecSchedule> sched;  // task lists of build and apply (shared, cached per shape)
     double apply_bytes = 0;
 };
 
@@ -706,25 +705,25 @@ void coarse_galerkin_device(Ctx* ctx, const DMatrix& W, const std::vector<int>& 
             chunks.push_back(make_int4(c, q, std::min(q + kQC, col_ptr[c + 1]), (int)chunks.size()));
         cfirst.push_back((int)chunks.size());
     }
-    DBuf<double> WRt((size_t)n * std::max(nc, 1));
+    double* WRt = scratch(ctx, kScratchCoarseWR, (size_t)n * std::max(nc, 1));
     if (!chunks.empty()) {
         DBuf<int4> d_chunks;
         DBuf<int> d_cfirst;
         d_chunks.upload(chunks, s);
         d_cfirst.upload(cfirst, s);
-        DBuf<double> part((size_t)chunks.size() * n);
+        double* part = scratch(ctx, kScratchCoarsePart, chunks.size() * (size_t)n);
         k_coarse_WR_chunks<<<dim3((unsigned)chunks.size(), (n + kIR - 1) / kIR), 256, 0, s>>>(W.a.p, W.ld, n,
                                                                                          d_chunks.p, crow, cval,
-                                                                                         part.p);
+                                                                                         part);
         count_launch();
-        k_coarse_WR_reduce<<<dim3((n + 255) / 256, nc), 256, 0, s>>>(part.p, d_cfirst.p, n, WRt.p);
+        k_coarse_WR_reduce<<<dim3((n + 255) / 256, nc), 256, 0, s>>>(part, d_cfirst.p, n, WRt);
         count_launch();
         SBG_LAUNCH_CHECK();
         SBG_CUDA(cudaStreamSynchronize(s));
     } else {
-        SBG_CUDA(cudaMemsetAsync(WRt.p, 0, WRt.n * sizeof(double), s));
+        SBG_CUDA(cudaMemsetAsync(WRt, 0, (size_t)n * std::max(nc, 1) * sizeof(double), s));
     }
-    k_coarse_Ht<<<ldh, 256, 0, s>>>(WRt.p, n, cptr, crow, cval, nc, ldh, H);
+    k_coarse_Ht<<<ldh, 256, 0, s>>>(WRt, n, cptr, crow, cval, nc, ldh, H);
     count_launch();
     SBG_LAUNCH_CHECK();
     SBG_CUDA(cudaStreamSynchronize(s));
@@ -754,59 +753,145 @@ struct StepTasks {
     int count(int st) const { return off[st + 1] - off[st]; }
 };
 
+// Every task list of the build and the apply depends only on the block sizes, so it
+// is generated once per partition shape and cached on the context (rebuilding the
+// preconditioner after a re-assembly — the common pattern — does no host work).
+struct PrecSchedule {
+    std::vector<int> key;  // ngather, then n_b of every block
+    std::vector<int2> gather;                // (block, first row), 8 rows each
+    std::vector<int> pot, pot_off{0};        // potrf blocks per step
+    StepTasks trsm, upd, xd, xu;
+    std::vector<GTask> la;
+    std::vector<int4> ct;                    // compact-inverse 32x32 output tiles
+    std::vector<int2> gemv, fw, bw;
+    std::vector<int> fw_off{0}, bw_off{0};
+    DBuf<int2> d_gather, d_gemv, d_fw, d_bw;
+    DBuf<int> d_pot;
+    DBuf<GTask> d_trsm, d_upd, d_xd, d_xu, d_la;
+    DBuf<int4> d_ct;
+};
+
+std::shared_ptr<PrecSchedule> prec_schedule(Ctx* ctx, const Prec* P)
+{
+    std::vector<int> key{P->ngather};
+    key.insert(key.end(), P->h_nb.begin(), P->h_nb.end());
+    if (auto* c = static_cast<std::shared_ptr<PrecSchedule>*>(ctx->prec_sched.get()))
+        if (*c && (*c)->key == key) return *c;
+    auto S = std::make_shared<PrecSchedule>();
+    S->key = key;
+    const int nb = P->nblocks;
+    for (int b = 0; b < P->ngather; ++b)
+        for (int r = 0; r < P->h_T[b] * TB; r += 8) S->gather.push_back({b, r});
+    // Cholesky: panel-blocked right-looking (see prec_build)
+    for (int k = 0; k < P->Tmax; ++k) {
+        const int p0 = k - k % kPanel;
+        for (int b = 0; b < nb; ++b) {
+            const int T = P->h_T[b];
+            if (T <= k) continue;
+            S->pot.push_back(b);
+            for (int i = k + 1; i < T; ++i) S->trsm.all.push_back({b, i, k, 0});
+            const int p1 = std::min(p0 + kPanel, T);
+            if (k + 1 < p1) {
+                for (int j = k + 1; j < p1; ++j)
+                    for (int i = j; i < T; ++i) S->upd.all.push_back({b, i, j, (k << 16) | (k + 1)});
+            } else {
+                for (int j = p1; j < T; ++j)
+                    for (int i = j; i < T; ++i) S->upd.all.push_back({b, i, j, (p0 << 16) | p1});
+            }
+        }
+        S->pot_off.push_back((int)S->pot.size());
+        S->trsm.close();
+        S->upd.close();
+    }
+    // blocked L^-1 (right-looking by panels), then L^-T L^-1
+    for (int k = 0; k < P->Tmax; ++k) {
+        const int p0 = k - k % kPanel;
+        for (int b = 0; b < nb; ++b) {
+            const int T = P->h_T[b];
+            if (T <= k) continue;
+            for (int j = 0; j <= k; ++j) S->xd.all.push_back({b, k, j, 0});
+            const int p1 = std::min(p0 + kPanel, T);
+            if (k + 1 < p1) {  // rows inside the panel: the contribution of row k only
+                for (int i = k + 1; i < p1; ++i)
+                    for (int j = 0; j <= k; ++j) S->xu.all.push_back({b, i, j, (k << 16) | (k + 1)});
+            } else {  // panel complete: rows below take K = the panel rows at once
+                for (int i = p1; i < T; ++i)
+                    for (int j = 0; j < p1; ++j) S->xu.all.push_back({b, i, j, (std::max(p0, j) << 16) | p1});
+            }
+        }
+        S->xd.close();
+        S->xu.close();
+    }
+    for (int b = 0; b < nb; ++b)
+        for (int i = 0; i < P->h_T[b]; ++i)
+            for (int j = 0; j <= i; ++j) S->la.push_back({b, i, j, 0});
+    for (int b = 0; b < nb; ++b) {
+        const int tr = (P->h_nb[b] + 31) / 32, tc = (P->h_ldm[b] + 31) / 32;
+        for (int ti = 0; ti < tr; ++ti)
+            for (int tj = 0; tj < tc; ++tj) S->ct.push_back(make_int4(b, ti, tj, 0));
+    }
+    for (int b = 0; b < nb; ++b)
+        for (int r = 0; r < P->h_nb[b]; r += GEMV_ROWS) S->gemv.push_back({b, r});
+    for (int k = 0; k < P->Tmax; ++k) {
+        for (int b = 0; b < nb; ++b)
+            for (int i = k; i < P->h_T[b]; ++i) S->fw.push_back({b, i});
+        S->fw_off.push_back((int)S->fw.size());
+    }
+    for (int st = 0; st < P->Tmax; ++st) {
+        for (int b = 0; b < nb; ++b) {
+            const int kk = P->h_T[b] - 1 - st;
+            for (int i = 0; i <= kk; ++i) S->bw.push_back({b, i});
+        }
+        S->bw_off.push_back((int)S->bw.size());
+    }
+    cudaStream_t s = ctx->stream;
+    S->d_gather.upload(S->gather, s);
+    S->d_pot.upload(S->pot, s);
+    S->d_trsm.upload(S->trsm.all, s);
+    S->d_upd.upload(S->upd.all, s);
+    S->d_xd.upload(S->xd.all, s);
+    S->d_xu.upload(S->xu.all, s);
+    S->d_la.upload(S->la, s);
+    S->d_ct.upload(S->ct, s);
+    S->d_gemv.upload(S->gemv, s);
+    S->d_fw.upload(S->fw, s);
+    S->d_bw.upload(S->bw, s);
+    SBG_CUDA(cudaStreamSynchronize(s));
+    ctx->prec_sched = std::make_shared<std::shared_ptr<PrecSchedule>>(S);
+    return S;
+}
+
 // W_bb^-1 = L^-T L^-1 for every block from the tiled factor in Lwork (overwritten):
 // X = L^-1 right-looking in one-stage tile tasks, then M = X^T X over Lwork, then
 // the compact row-major inverses (row stride ldm_b) into Mc.
 void form_inverses(Ctx* ctx, Prec* P, DBuf<double>& Lwork, DBuf<double>& Mc)
 {
     cudaStream_t s = ctx->stream;
-    DBuf<double> Xp(std::max<size_t>(Lwork.n, 1));
-    SBG_CUDA(cudaMemsetAsync(Xp.p, 0, Xp.n * sizeof(double), s));
-    StepTasks xd, xu;
-    std::vector<GTask> la;
-    for (int k = 0; k < P->Tmax; ++k) {
-        const int p0 = k - k % kPanel;
-        for (int b = 0; b < P->nblocks; ++b) {
-            const int T = P->h_T[b];
-            if (T <= k) continue;
-            for (int j = 0; j <= k; ++j) xd.all.push_back({b, k, j, 0});
-            const int p1 = std::min(p0 + kPanel, T);
-            if (k + 1 < p1) {  // rows inside the panel: the contribution of row k only
-                for (int i = k + 1; i < p1; ++i)
-                    for (int j = 0; j <= k; ++j) xu.all.push_back({b, i, j, (k << 16) | (k + 1)});
-            } else {  // panel complete: rows below take K = the panel rows at once
-                for (int i = p1; i < T; ++i)
-                    for (int j = 0; j < p1; ++j) xu.all.push_back({b, i, j, (std::max(p0, j) << 16) | p1});
-            }
+    const PrecSchedule& S = *P->sched;
+    double* Xp_p = scratch(ctx, kScratchInverse, std::max<size_t>(Lwork.n, 1));
+    {
+        TimedScope t0(ctx, "inv_alloc");
+        SBG_CUDA(cudaMemsetAsync(Xp_p, 0, std::max<size_t>(Lwork.n, 1) * sizeof(double), s));
+    }
+    struct {
+        double* p;
+    } Xp{Xp_p};
+    {
+        TimedScope t1(ctx, "inv_lower");
+        for (int k = 0; k < P->Tmax; ++k) {
+            launch_gemm<K_XDIAG>(ctx, P, k, S.d_xd.p + S.xd.off[k], S.xd.count(k), Lwork.p, Xp.p);
+            launch_gemm<K_XUPD>(ctx, P, k, S.d_xu.p + S.xu.off[k], S.xu.count(k), Lwork.p, Xp.p);
         }
-        xd.close();
-        xu.close();
     }
-    for (int b = 0; b < P->nblocks; ++b)
-        for (int i = 0; i < P->h_T[b]; ++i)
-            for (int j = 0; j <= i; ++j) la.push_back({b, i, j, 0});
-    DBuf<GTask> d_xd, d_xu, d_la;
-    d_xd.upload(xd.all, s);
-    d_xu.upload(xu.all, s);
-    d_la.upload(la, s);
-    for (int k = 0; k < P->Tmax; ++k) {
-        launch_gemm<K_XDIAG>(ctx, P, k, d_xd.p + xd.off[k], xd.count(k), Lwork.p, Xp.p);
-        launch_gemm<K_XUPD>(ctx, P, k, d_xu.p + xu.off[k], xu.count(k), Lwork.p, Xp.p);
+    {
+        TimedScope t2(ctx, "inv_lauum");
+        launch_gemm<K_LAUUM>(ctx, P, 0, S.d_la.p, (int)S.la.size(), Lwork.p, Xp.p);
     }
-    launch_gemm<K_LAUUM>(ctx, P, 0, d_la.p, (int)la.size(), Lwork.p, Xp.p);
     const long long Msize = P->h_Moff.empty() ? 0 : P->h_Moff.back() + (long long)P->h_nb.back() * P->h_ldm.back();
     Mc.alloc(std::max<long long>(Msize, 1));
-    std::vector<int4> ct;
-    for (int b = 0; b < P->nblocks; ++b) {
-        const int tr = (P->h_nb[b] + 31) / 32, tc = (P->h_ldm[b] + 31) / 32;
-        for (int ti = 0; ti < tr; ++ti)
-            for (int tj = 0; tj < tc; ++tj) ct.push_back(make_int4(b, ti, tj, 0));
-    }
-    DBuf<int4> d_ct;
-    d_ct.upload(ct, s);
-    if (!ct.empty()) {
-        k_compact_inverse<<<(int)ct.size(), 256, 0, s>>>(Lwork.p, P->d_Poff.p, P->d_T.p, P->d_nb.p, P->d_ldm.p,
-                                                         P->d_Moff.p, d_ct.p, Mc.p);
+    if (!S.ct.empty()) {
+        k_compact_inverse<<<(int)S.ct.size(), 256, 0, s>>>(Lwork.p, P->d_Poff.p, P->d_T.p, P->d_nb.p, P->d_ldm.p,
+                                                           P->d_Moff.p, S.d_ct.p, Mc.p);
         count_launch();
     }
     SBG_LAUNCH_CHECK();
@@ -894,14 +979,11 @@ Prec* prec_build(Ctx* ctx, const DMatrix& W, const DofPartition& part, const Pro
         P->ngather = ngather;
         P->d_bptr.upload(bptr, s);
         P->d_bdofs.upload(bdofs, s);
+        P->sched = prec_schedule(ctx, P);
+        const PrecSchedule& S = *P->sched;
         if (ngather > 0) {  // factor_block's submatrix (schwarz.hpp:77-83)
-            std::vector<int2> gt;
-            for (int b = 0; b < ngather; ++b)
-                for (int r = 0; r < P->h_T[b] * TB; r += 8) gt.push_back({b, r});
-            DBuf<int2> d_gt;
-            d_gt.upload(gt, s);
-            k_gather_blocks<<<(int)gt.size(), 256, 0, s>>>(W.a.p, W.ld, P->d_bptr.p, P->d_bdofs.p, P->d_T.p,
-                                                           P->d_Poff.p, d_gt.p, P->Lp.p);
+            k_gather_blocks<<<(int)S.gather.size(), 256, 0, s>>>(W.a.p, W.ld, P->d_bptr.p, P->d_bdofs.p, P->d_T.p,
+                                                                 P->d_Poff.p, S.d_gather.p, P->Lp.p);
             count_launch();
             SBG_LAUNCH_CHECK();
             SBG_CUDA(cudaStreamSynchronize(s));
@@ -938,44 +1020,16 @@ Prec* prec_build(Ctx* ctx, const DMatrix& W, const DofPartition& part, const Pro
             TimedScope ts(ctx, "cholesky");
             const size_t smem_potrf = 2 * TB * (TB + 1) * sizeof(double);
             SBG_CUDA(cudaFuncSetAttribute(k_potrf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_potrf));
-            std::vector<int> pot, pot_off{0};
-            StepTasks trsm, upd;
-            // panel-blocked right-looking: inside a panel of kPanel tile columns only the
-            // panel's own columns are updated per step; the trailing matrix takes one update
-            // with K = the whole panel when the panel is complete
+            // panel-blocked right-looking (task lists in the schedule): inside a panel of
+            // kPanel tile columns only the panel's own columns are updated per step; the
+            // trailing matrix takes one update with K = the whole panel when it is complete
             for (int k = 0; k < P->Tmax; ++k) {
-                const int p0 = k - k % kPanel;
-                for (int b = 0; b < P->nblocks; ++b) {
-                    const int T = P->h_T[b];
-                    if (T <= k) continue;
-                    pot.push_back(b);
-                    for (int i = k + 1; i < T; ++i) trsm.all.push_back({b, i, k, 0});
-                    const int p1 = std::min(p0 + kPanel, T);
-                    if (k + 1 < p1) {
-                        for (int j = k + 1; j < p1; ++j)
-                            for (int i = j; i < T; ++i) upd.all.push_back({b, i, j, (k << 16) | (k + 1)});
-                    } else {
-                        for (int j = p1; j < T; ++j)
-                            for (int i = j; i < T; ++i) upd.all.push_back({b, i, j, (p0 << 16) | p1});
-                    }
-                }
-                pot_off.push_back((int)pot.size());
-                trsm.close();
-                upd.close();
-            }
-            DBuf<int> d_pot;
-            DBuf<GTask> d_trsm, d_upd;
-            d_pot.upload(pot, s);
-            d_trsm.upload(trsm.all, s);
-            d_upd.upload(upd.all, s);
-            for (int k = 0; k < P->Tmax; ++k) {
-                k_potrf<<<pot_off[k + 1] - pot_off[k], 256, smem_potrf, s>>>(k, d_pot.p + pot_off[k], P->d_T.p,
-                                                                             P->d_Poff.p, P->d_Doff.p, P->Lp.p,
-                                                                             P->D.p, fail.p);
+                k_potrf<<<S.pot_off[k + 1] - S.pot_off[k], 256, smem_potrf, s>>>(
+                    k, S.d_pot.p + S.pot_off[k], P->d_T.p, P->d_Poff.p, P->d_Doff.p, P->Lp.p, P->D.p, fail.p);
                 count_launch();
                 SBG_LAUNCH_CHECK();
-                launch_gemm<K_TRSM>(ctx, P, k, d_trsm.p + trsm.off[k], trsm.count(k), P->Lp.p, nullptr);
-                launch_gemm<K_UPDATE>(ctx, P, k, d_upd.p + upd.off[k], upd.count(k), P->Lp.p, nullptr);
+                launch_gemm<K_TRSM>(ctx, P, k, S.d_trsm.p + S.trsm.off[k], S.trsm.count(k), P->Lp.p, nullptr);
+                launch_gemm<K_UPDATE>(ctx, P, k, S.d_upd.p + S.upd.off[k], S.upd.count(k), P->Lp.p, nullptr);
             }
             SBG_CUDA(cudaStreamSynchronize(s));
         }
@@ -993,33 +1047,8 @@ Prec* prec_build(Ctx* ctx, const DMatrix& W, const DofPartition& part, const Pro
                 TimedScope ts(ctx, "block_inverse");
                 form_inverses(ctx, P, P->Lp, P->Mc);
             }
-            std::vector<int2> gt;
-            for (int b = 0; b < P->nblocks; ++b)
-                for (int r = 0; r < P->h_nb[b]; r += GEMV_ROWS) gt.push_back({b, r});
-            P->gemv_tasks.upload(gt, s);
-            P->ngemv = (int)gt.size();
-            SBG_CUDA(cudaStreamSynchronize(s));
             P->Lp.release();
             P->D.release();
-        } else {
-            std::vector<int2> fw, bw;
-            P->fwd_off.assign(1, 0);
-            P->bwd_off.assign(1, 0);
-            for (int k = 0; k < P->Tmax; ++k) {
-                for (int b = 0; b < P->nblocks; ++b)
-                    for (int i = k; i < P->h_T[b]; ++i) fw.push_back({b, i});
-                P->fwd_off.push_back((int)fw.size());
-            }
-            for (int st = 0; st < P->Tmax; ++st) {
-                for (int b = 0; b < P->nblocks; ++b) {
-                    const int kk = P->h_T[b] - 1 - st;
-                    for (int i = 0; i <= kk; ++i) bw.push_back({b, i});
-                }
-                P->bwd_off.push_back((int)bw.size());
-            }
-            P->fwd_tasks.upload(fw, s);
-            P->bwd_tasks.upload(bw, s);
-            SBG_CUDA(cudaStreamSynchronize(s));
         }
     } catch (...) {
         delete P;
@@ -1052,23 +1081,24 @@ void prec_apply(Ctx* ctx, Prec* P, const double* r, double* z, const int* done)
     count_launch();
     const double* yloc;
     if (P->mode == kPrecInverse) {
-        k_block_gemv<<<P->ngemv, 256, 0, s>>>(
-            P->gemv_tasks.p, P->d_nb.p, P->d_ldm.p, P->d_loc.p, P->d_Moff.p, P->Mc.p, P->loc.p, P->locy.p, done);
+        k_block_gemv<<<(int)P->sched->gemv.size(), 256, 0, s>>>(P->sched->d_gemv.p, P->d_nb.p, P->d_ldm.p,
+                                                                P->d_loc.p, P->d_Moff.p, P->Mc.p, P->loc.p,
+                                                                P->locy.p, done);
         count_launch();
         yloc = P->locy.p;
     } else {
         for (int k = 0; k < P->Tmax; ++k) {
-            const int cnt = P->fwd_off[k + 1] - P->fwd_off[k];
+            const int cnt = P->sched->fw_off[k + 1] - P->sched->fw_off[k];
             if (cnt) {
-                k_trsv_fwd<<<cnt, 256, 0, s>>>(k, P->fwd_tasks.p + P->fwd_off[k], P->d_T.p, P->d_loc.p, P->d_Poff.p,
+                k_trsv_fwd<<<cnt, 256, 0, s>>>(k, P->sched->d_fw.p + P->sched->fw_off[k], P->d_T.p, P->d_loc.p, P->d_Poff.p,
                                                P->d_Doff.p, P->Lp.p, P->D.p, P->loc.p, done);
                 count_launch();
             }
         }
         for (int st = 0; st < P->Tmax; ++st) {
-            const int cnt = P->bwd_off[st + 1] - P->bwd_off[st];
+            const int cnt = P->sched->bw_off[st + 1] - P->sched->bw_off[st];
             if (cnt) {
-                k_trsv_bwd<<<cnt, 256, 0, s>>>(st, P->bwd_tasks.p + P->bwd_off[st], P->d_T.p, P->d_loc.p,
+                k_trsv_bwd<<<cnt, 256, 0, s>>>(st, P->sched->d_bw.p + P->sched->bw_off[st], P->d_T.p, P->d_loc.p,
                                                P->d_Poff.p, P->d_Doff.p, P->Lp.p, P->D.p, P->loc.p, done);
                 count_launch();
             }
@@ -1221,10 +1251,10 @@ Prec* prec_from_dense(Ctx* ctx, const DMatrix& Mdense)
             SBG_CUDA(cudaMemsetAsync(P->Mc.p, 0, P->Mc.n * sizeof(double), s));
             SBG_CUDA(cudaMemcpy2DAsync(P->Mc.p, ldm * sizeof(double), Mdense.a.p, Mdense.ld * sizeof(double),
                                        n * sizeof(double), n, cudaMemcpyDeviceToDevice, s));
-            std::vector<int2> gt;
-            for (int r = 0; r < n; r += GEMV_ROWS) gt.push_back({0, r});
-            P->gemv_tasks.upload(gt, s);
-            P->ngemv = (int)gt.size();
+            auto S = std::make_shared<PrecSchedule>();  // apply-only schedule (not cached)
+            for (int r = 0; r < n; r += GEMV_ROWS) S->gemv.push_back({0, r});
+            S->d_gemv.upload(S->gemv, s);
+            P->sched = S;
             SBG_CUDA(cudaStreamSynchronize(s));
         }
     } catch (...) {

@@ -128,6 +128,7 @@ SIGNATURES = {
     "sbg_matvec_device": (C.c_int, [vp, vp, vp, vp, C.c_int]),
     "sbg_apply_preconditioner_device": (C.c_int, [vp, vp, vp, vp, C.c_int]),
     "sbg_l2_flush": (C.c_int, [vp]),
+    "sbg_pool_stats": (C.c_int, [vp, C.POINTER(C.c_longlong), C.POINTER(C.c_longlong)]),
     "sbg_fp64_peak": (C.c_int, [vp, C.POINTER(C.c_double)]),
     "sbg_config_g": (C.c_int, [C.c_int, f64p]),
 }
@@ -203,6 +204,12 @@ class Context(_Handle):
 
     def l2_flush(self):
         _check(lib().sbg_l2_flush(self.h))
+
+    def pool_stats(self):
+        """(reserved, used) bytes of the device memory pool"""
+        r, u = C.c_longlong(), C.c_longlong()
+        _check(lib().sbg_pool_stats(self.h, C.byref(r), C.byref(u)))
+        return r.value, u.value
 
     def begin(self, name: str):
         _check(lib().sbg_timer_begin(self.h, name.encode()))

@@ -19,3 +19,12 @@ for rep in range(3):
     print({k: round(ctx.timer(k)[0], 2) for k in ("build_preconditioner", "cholesky", "block_inverse",
                                                    "coarse_galerkin")}, flush=True)
     del prec
+
+# rebuild while the previous preconditioner is still alive (the bench's step pattern)
+old = S.build_preconditioner(W, part, P)
+for rep in range(3):
+    ctx.reset_timers()
+    new = S.build_preconditioner(W, part, P)
+    print("keep-alive", {k: round(ctx.timer(k)[0], 2) for k in ("build_preconditioner", "cholesky", "block_inverse",
+                                                                "coarse_galerkin")}, flush=True)
+    old = new

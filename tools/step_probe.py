@@ -17,7 +17,7 @@ part, P = S.partition_dofs(pair, fine), S.build_prolongation(pair, coarse, fine)
 g = S.config_g(cfg)
 plan = S.AssemblyPlan(fine, ctx=ctx)
 W = prec = None
-for rep in range(4):
+for rep in range(6):
     ctx.reset_timers()
     t = [time.perf_counter()]
     W = plan.run(W)
@@ -25,7 +25,8 @@ for rep in range(4):
     t.append(time.perf_counter())
     L = S.assemble_rhs(fine, g, ctx=ctx)
     t.append(time.perf_counter())
-    prec = None
+    if os.environ.get("FREE_FIRST"):
+        prec = None
     t.append(time.perf_counter())
     prec = S.build_preconditioner(W, part, P)
     ctx.synchronize()
@@ -36,7 +37,8 @@ for rep in range(4):
     dev = {k: round(ctx.timer(k)[0], 2) for k in ("assemble_W", "build_preconditioner", "cholesky", "block_inverse",
                                                    "coarse_galerkin", "pcg")}
     print(f"rep {rep}: assemble {d[0]:.1f}  rhs {d[1]:.1f}  free prec {d[2]:.1f}  build prec {d[3]:.1f}  "
-          f"pcg {d[4]:.1f} ms wall ({res.iterations} it); device {dev}", flush=True)
+          f"pcg {d[4]:.1f} ms wall ({res.iterations} it); device {dev}; pool (reserved, used) GB "
+          f"{tuple(round(x / 1e9, 2) for x in ctx.pool_stats())}", flush=True)
 
 # end-to-end pieces of S.assemble_W(host mesh) + W.download()
 for rep in range(3):
