@@ -276,5 +276,44 @@ inline PcgReport pcg(Context& ctx, const GalerkinMatrix& W, const SchwarzPrecond
     return rep;
 }
 
+// reference: inc/schwarz.hpp:142-148 — M stays on the device (download() for a host copy)
+inline GalerkinMatrix materialize_preconditioner(Context& ctx, const SchwarzPreconditioner& P)
+{
+    sbg_matrix* m = nullptr;
+    check(sbg_materialize_preconditioner(ctx.get(), P.get(), &m));
+    return GalerkinMatrix(m);
+}
+
+struct SpectrumResult {  // reference: inc/schwarz.hpp:150-154
+    double lambda_min = 0;
+    double lambda_max = 0;
+    double kappa = 0;
+};
+inline SpectrumResult to_spectrum(const sbg_spectrum& s) { return {s.lambda_min, s.lambda_max, s.kappa}; }
+// reference: inc/schwarz.hpp:168-172 (device Lanczos instead of the dense eigensolve)
+inline SpectrumResult condition_number(Context& ctx, const GalerkinMatrix& W, double tol = 1e-10)
+{
+    sbg_spectrum s{};
+    check(sbg_condition_number(ctx.get(), W.get(), nullptr, tol, 0, &s));
+    return to_spectrum(s);
+}
+// reference: inc/schwarz.hpp:185-190
+inline SpectrumResult condition_number(Context& ctx, const GalerkinMatrix& W, const SchwarzPreconditioner& P,
+                                       double tol = 1e-10)
+{
+    sbg_spectrum s{};
+    check(sbg_condition_number(ctx.get(), W.get(), P.get(), tol, 0, &s));
+    return to_spectrum(s);
+}
+// reference: inc/schwarz.hpp:174-183 (M materialized, dense)
+inline SpectrumResult condition_number(Context& ctx, const GalerkinMatrix& W, const GalerkinMatrix& M,
+                                       double tol = 1e-10)
+{
+    sbg_prec* p = nullptr;
+    check(sbg_prec_from_dense(ctx.get(), M.get(), &p));
+    SchwarzPreconditioner P(p);
+    return condition_number(ctx, W, P, tol);
+}
+
 }  // namespace gpu
 }  // namespace screenbem

@@ -750,6 +750,7 @@ class SolveResult:
     report: PcgReport
     W: GalerkinMatrix
     rhs: np.ndarray
+    prec: "SchwarzPreconditioner" = None
 
 
 def solve(pair: MeshLevelPair, g, tol: float = 1e-8, cfg: QuadratureConfig = None, precondition: bool = True,
@@ -768,4 +769,4 @@ def solve(pair: MeshLevelPair, g, tol: float = 1e-8, cfg: QuadratureConfig = Non
     rep = pcg(W, prec, L, tol)
     if not rep.converged:
         raise NumericalError("solver did not converge")
-    return SolveResult(fine.n, rep, W, L)
+    return SolveResult(fine.n, rep, W, L, prec)

@@ -39,3 +39,5 @@ def test_cpp_dropin_runs_cfg1(tmp_path):
     from paper_2310_09204_b200 import screenbem as S
     res = S.solve(S.make_config(1), [0.0, 0.0, 1.0], 1e-8)
     assert f"iterations {res.report.iterations}" in r.stdout
+    kp = float(r.stdout.split("kappa_prec")[1].split()[0])
+    assert kp == pytest.approx(S.condition_number(res.W, res.prec).kappa, rel=1e-8)

@@ -23,6 +23,8 @@ int main(int argc, char** argv)
         const sb::PcgReport rep = sb::pcg(ctx, W, &P, L, 1e-8);
         std::printf("dofs %d iterations %d converged %d kappa %.4f\n", W.rows(), rep.iterations, (int)rep.converged,
                     rep.kappa_estimate);
+        const sb::SpectrumResult sp = sb::condition_number(ctx, W, P);  // schwarz.hpp:185-190
+        std::printf("kappa_prec %.8f\n", sp.kappa);
         return rep.converged ? 0 : 3;
     } catch (const screenbem::ValidationError& e) {
         std::fprintf(stderr, "validation error: %s\n", e.what());
