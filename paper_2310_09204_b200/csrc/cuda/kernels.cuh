@@ -54,6 +54,7 @@ double matrix_symmetry_defect(const DMatrix& M);
 // ---------------------------------------------------------------- dense fp64 GEMV (y = W x, W symmetric)
 struct GemvPlan {
     int n = 0, ld = 0, strips = 0, chunks = 0, rows_per_chunk = 0;
+    bool rows = false;  // row-per-warp form: the result lands in part directly (chunks = 1)
     DBuf<double> part;  // chunks x ld partial column sums
 };
 void gemv_plan(Ctx* ctx, int n, int ld, GemvPlan& plan);
