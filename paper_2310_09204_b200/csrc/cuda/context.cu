@@ -17,6 +17,15 @@ namespace {
 std::atomic<long long> g_launches{0};
 }
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+void add_launches(long long k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
+bool pcg_graph_enabled()
+{
+    static const bool on = [] {
+        const char* e = getenv("SBG_PCG_GRAPH");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
 
 void device_pool_init(int device)
 {

@@ -38,6 +38,8 @@ __device__ __forceinline__ double rsqrt_fast(double r2)
 }
 
 double fp64_peak_tflops(Ctx* ctx);
+void add_launches(long long k);  // launch bookkeeping for graph-replayed kernels
+bool pcg_graph_enabled();        // PCG loop as one graph with a device-side while node (SBG_PCG_GRAPH=0: off)
 void l2_flush(Ctx* ctx);  // write 256 MiB then read 256 MiB: cold, clean L2
 // grow-only device scratch buffer `slot` of at least `count` doubles, cached on the
 // context (large per-call temporaries: no pool growth or fragmentation between calls)
@@ -66,6 +68,7 @@ struct Prec;
 enum { kPrecTrsv = 0, kPrecInverse = 1 };
 Prec* prec_build(Ctx* ctx, const DMatrix& W, const DofPartition& part, const Prolongation& R, int mode);
 int prec_mode(const Prec* p);
+unsigned long long prec_uid(const Prec* p);  // unique per preconditioner object
 void prec_destroy(Prec* p);
 int prec_n(const Prec* p);
 int prec_num_subspaces(const Prec* p);

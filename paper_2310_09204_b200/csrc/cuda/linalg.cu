@@ -216,6 +216,13 @@ __global__ void k_pcg_rz(PcgDev* st, const double* __restrict__ r, const double*
     }
 }
 
+// device-side loop control of the graph form: the while node runs its body while the
+// handle is non-zero
+__global__ void k_pcg_gate(const PcgDev* st, cudaGraphConditionalHandle h)
+{
+    if (threadIdx.x == 0) cudaGraphSetConditional(h, st->done ? 0u : 1u);
+}
+
 // p = z + beta p (pcg.hpp:93)
 __global__ void k_pcg_p(const PcgDev* st, double* __restrict__ p, const double* __restrict__ z, int n)
 {
@@ -383,8 +390,24 @@ struct PcgWork {
     DBuf<PcgDev> st;
     GemvPlan plan;
     PcgDev* hs = nullptr;
+    // the whole iteration loop as one graph (a device-side while node), per (W, prec)
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    const void* gW = nullptr;
+    unsigned long long gP = 0;  // preconditioner uid (addresses are reused after a free)
+    int kernels_per_iter = 0;
+    void drop_graph()
+    {
+        if (exec) cudaGraphExecDestroy(exec);
+        if (graph) cudaGraphDestroy(graph);
+        exec = nullptr;
+        graph = nullptr;
+        gW = nullptr;
+        gP = 0;
+    }
     ~PcgWork()
     {
+        drop_graph();
         if (hs) cudaFreeHost(hs);
     }
 };
@@ -454,28 +477,99 @@ void pcg_run(Ctx* ctx, const DMatrix& W, Prec* prec, const double* rhs, double* 
         h.done = 1;
         SBG_CUDA(cudaMemcpyAsync(w.st.p, &h, sizeof(h), cudaMemcpyHostToDevice, s));
     }
-    int batch = 4, enqueued = 0;
+    // one PCG iteration (pcg.hpp:69-93) on the context stream
+    auto enqueue_iteration = [&]() {
+        {
+            TimedScope ts(ctx, "gemv_f64");
+            gemv_partial_launch(ctx, W, w.plan, p, done);
+        }
+        k_pcg_alpha<<<nb, 256, 0, s>>>(w.st.p, w.plan.part.p, w.plan.chunks, W.ld, n, p, Wp, w.partials.p);
+        count_launch();
+        k_pcg_update<<<nb, 256, 0, s>>>(w.st.p, x, r, p, Wp, n);
+        count_launch();
+        if (prec) prec_apply(ctx, prec, r, z, done);
+        k_pcg_rz<<<nb, 256, 0, s>>>(w.st.p, r, z, n, w.partials.p, w.hist.p, w.alphas.p, w.betas.p);
+        count_launch();
+        k_pcg_p<<<nb, 256, 0, s>>>(w.st.p, p, z, n);
+        count_launch();
+        SBG_LAUNCH_CHECK();
+    };
+    if (n > 0 && pcg_graph_enabled()) {
+        // graph form: [gate] -> while(handle) { iteration ; gate } — the loop runs on the device
+        // with no host round trips and no launches past convergence
+        if (!w.exec || w.gW != W.a.p || w.gP != (prec ? prec_uid(prec) : 0)) {
+            const bool timers = ctx->timers.enabled;
+            ctx->timers.enabled = false;  // no timer events inside the captured body
+            const long long launches0 = launch_count();
+            long long captured = 0;
+            cudaGraph_t ng = nullptr;
+            try {
+                SBG_CUDA(cudaGraphCreate(&ng, 0));
+                cudaGraphConditionalHandle handle;
+                SBG_CUDA(cudaGraphConditionalHandleCreate(&handle, ng, 0, 0));
+                SBG_CUDA(cudaStreamBeginCaptureToGraph(s, ng, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+                k_pcg_gate<<<1, 32, 0, s>>>(w.st.p, handle);
+                cudaGraph_t g_out = nullptr;
+                SBG_CUDA(cudaStreamEndCapture(s, &g_out));
+                size_t nroots = 0;
+                SBG_CUDA(cudaGraphGetNodes(ng, nullptr, &nroots));
+                std::vector<cudaGraphNode_t> nodes(nroots);
+                SBG_CUDA(cudaGraphGetNodes(ng, nodes.data(), &nroots));
+                cudaGraphNodeParams cp = {};
+                cp.type = cudaGraphNodeTypeConditional;
+                cp.conditional.handle = handle;
+                cp.conditional.type = cudaGraphCondTypeWhile;
+                cp.conditional.size = 1;
+                cudaGraphNode_t cond;
+                SBG_CUDA(cudaGraphAddNode(&cond, ng, nodes.data(), nroots, &cp));
+                cudaGraph_t body = cp.conditional.phGraph_out[0];
+                SBG_CUDA(cudaStreamBeginCaptureToGraph(s, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+                enqueue_iteration();
+                k_pcg_gate<<<1, 32, 0, s>>>(w.st.p, handle);
+                SBG_CUDA(cudaStreamEndCapture(s, &g_out));
+                // same topology (a new preconditioner of the same kind): update the
+                // instantiated graph in place instead of instantiating again
+                bool updated = false;
+                if (w.exec) {
+                    cudaGraphExecUpdateResultInfo info;
+                    if (cudaGraphExecUpdate(w.exec, ng, &info) == cudaSuccess) {
+                        updated = true;
+                    } else {
+                        (void)cudaGetLastError();
+                    }
+                }
+                if (!updated) {
+                    w.drop_graph();
+                    SBG_CUDA(cudaGraphInstantiate(&w.exec, ng, 0));
+                }
+                if (w.graph) cudaGraphDestroy(w.graph);
+                w.graph = ng;
+                ng = nullptr;
+            } catch (...) {
+                ctx->timers.enabled = timers;
+                if (ng) cudaGraphDestroy(ng);
+                w.drop_graph();
+                throw;
+            }
+            ctx->timers.enabled = timers;
+            captured = launch_count() - launches0;  // one iteration's kernels (recorded, not run)
+            add_launches(-captured);
+            w.kernels_per_iter = (int)captured;
+            w.gW = W.a.p;
+            w.gP = prec ? prec_uid(prec) : 0;
+        }
+        SBG_CUDA(cudaGraphLaunch(w.exec, s));
+        SBG_CUDA(cudaMemcpyAsync(w.hs, w.st.p, sizeof(PcgDev), cudaMemcpyDeviceToHost, s));
+        SBG_CUDA(cudaStreamSynchronize(s));
+        add_launches((long long)w.kernels_per_iter * w.hs->it + 1 + w.hs->it);  // body kernels + gates
+    }
+    int batch = 4, enqueued = pcg_graph_enabled() ? maxit : 0;
     while (true) {
         SBG_CUDA(cudaMemcpyAsync(w.hs, w.st.p, sizeof(PcgDev), cudaMemcpyDeviceToHost, s));
         SBG_CUDA(cudaStreamSynchronize(s));
         if (w.hs->done || enqueued >= maxit) break;
         const int todo = std::min(batch, maxit - enqueued);
-        for (int t = 0; t < todo; ++t) {
-            {
-                TimedScope ts(ctx, "gemv_f64");
-                gemv_partial_launch(ctx, W, w.plan, p, done);
-            }
-            k_pcg_alpha<<<nb, 256, 0, s>>>(w.st.p, w.plan.part.p, w.plan.chunks, W.ld, n, p, Wp, w.partials.p);
-            count_launch();
-            k_pcg_update<<<nb, 256, 0, s>>>(w.st.p, x, r, p, Wp, n);
-            count_launch();
-            if (prec) prec_apply(ctx, prec, r, z, done);
-            k_pcg_rz<<<nb, 256, 0, s>>>(w.st.p, r, z, n, w.partials.p, w.hist.p, w.alphas.p, w.betas.p);
-            count_launch();
-            k_pcg_p<<<nb, 256, 0, s>>>(w.st.p, p, z, n);
-            count_launch();
-            SBG_LAUNCH_CHECK();
-        }
+        for (int t = 0; t < todo; ++t) enqueue_iteration();
         enqueued += todo;
         batch = std::min(batch * 2, 64);
     }

@@ -15,6 +15,7 @@
 //     apply is one batched dense GEMV over all blocks — the same HBM bytes as
 //     two triangular solves with L, without their sequential tile chain.
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 
 #include "kernels.cuh"
@@ -52,6 +53,12 @@ struct Prec {
     DBuf<int> Rc_ptr, Rc_row, Rr_ptr, Rr_col;
     DBuf<double> Rc_val, Rr_val;
     std::shared_ptr<PrecSchedule> sched;  // task lists of build and apply (shared, cached per shape)
+    unsigned long long uid = next_uid();
+    static unsigned long long next_uid()
+    {
+        static std::atomic<unsigned long long> c{1};
+        return c.fetch_add(1);
+    }
     double apply_bytes = 0;
 };
 
@@ -1060,6 +1067,7 @@ Prec* prec_build(Ctx* ctx, const DMatrix& W, const DofPartition& part, const Pro
 void prec_destroy(Prec* p) { delete p; }
 int prec_n(const Prec* p) { return p->n; }
 int prec_mode(const Prec* p) { return p->mode; }
+unsigned long long prec_uid(const Prec* p) { return p->uid; }
 int prec_num_subspaces(const Prec* p)  // schwarz.hpp:66-72
 {
     return p->nfaces + (p->nwb > 0 ? 1 : 0) + (p->nc > 0 ? 1 : 0);
