@@ -39,6 +39,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--exact-far", action="store_true",
+                    help="far pairs bitwise like the CPU restatement (SURVEY Appendix B parity-gate path)")
     ap.add_argument("--clocks", default="nvml", choices=["nvml", "smi", "off"],
                     help="clock/throttle sampler during the timed region (nvml: in-process NVML queries)")
     ap.add_argument("--no-cpu-phases", action="store_true",
@@ -319,7 +321,8 @@ def run_ours(args):
     g = S.config_g(cfg)
     nf, n = pair.fine.nf, fine.n
     npairs = nf * (nf + 1) // 2
-    plan = S.AssemblyPlan(fine, ctx=ctx)
+    qcfg = S.QuadratureConfig(exact_far=args.exact_far)
+    plan = S.AssemblyPlan(fine, qcfg, ctx=ctx)
     plan_ms = {k: round(ctx.timer(k)[0], 3) for k in ("plan_total", "plan_curls", "plan_tiles", "plan_singular")}
 
     def step(W):
@@ -430,7 +433,8 @@ def run_ours(args):
             "config": {"workload": f"config {cfg}: {CFG_NAMES[cfg]}" + (f", H/h {ratio}" if cfg == 5 else ""),
                        "triangles": nf, "dofs": n, "tri_pairs": npairs, "parallelism": f"replicas x{world}",
                        "l2": "flushed (256 MiB write + 256 MiB read: cold L2 with clean lines) before every timed step and every matvec launch",
-                       "pcg_tol": 1e-8},
+                       "pcg_tol": 1e-8, "far_field": "exact (IEEE, oracle order)" if args.exact_far else
+                       "fast (distance expansion + refined rsqrt)"},
             "roofline": {"bound": "fp64", "kernel": dom[0], "achieved": achieved, "peak": fp64_peak,
                          "unit": "TFLOP/s", "frac": achieved / fp64_peak if fp64_peak else None, "traffic": None,
                          "peak_source": "DFMA loop measured by bench.py on this GPU (MEASURED_PEAKS.json has no fp64)",

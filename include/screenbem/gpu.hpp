@@ -91,7 +91,8 @@ struct QuadratureConfig {  // reference: inc/quadrature.hpp:12-16
     int far_order = 4;
     int singular_order = 8;
     double near_threshold = 2.0;
-    sbg_quad_cfg c() const { return {far_order, singular_order, near_threshold}; }
+    bool exact_far = false;  // depth-0 far pairs bitwise like the CPU restatement (slower)
+    sbg_quad_cfg c() const { return {far_order, singular_order, near_threshold, exact_far ? 1 : 0}; }
 };
 
 class Context : public Handle<sbg_ctx, sbg_ctx_destroy> {

@@ -50,6 +50,8 @@ typedef struct {
     int far_order;         /* 4 */
     int singular_order;    /* 8 */
     double near_threshold; /* 2.0 */
+    int exact_far;         /* 0: fast far field; 1: depth-0 far pairs bitwise like the CPU
+                              restatement (IEEE sqrt/division, no FMA, sequential order) */
 } sbg_quad_cfg;
 
 /* PcgReport (inc/pcg.hpp:9-16) */

@@ -83,6 +83,7 @@ QuadCfg qcfg(const sbg_quad_cfg* c)
         q.far_order = c->far_order;
         q.singular_order = c->singular_order;
         q.near_threshold = c->near_threshold;
+        q.exact_far = c->exact_far != 0;
     }
     if (q.far_order < 1 || q.singular_order < 1) throw ValidationError("quadrature orders must be positive");
     return q;

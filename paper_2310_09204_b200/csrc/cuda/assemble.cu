@@ -233,20 +233,47 @@ __device__ __forceinline__ double far_pass_sum(const XPts& X, const double4* __r
     return acc;
 }
 
+// SURVEY Appendix B switch: the oracle's triangle_pair_rule (quadrature.hpp:208-220) in its
+// exact operation order — affine points, |x-y| by IEEE sqrt, 1/(4 pi r) by IEEE division,
+// (w_i w_j) k summed i-major, then (acc 4) A_t A_s — so the depth-0 far integral is
+// bitwise the CPU restatement's (t = the facet with the larger index)
+__device__ __forceinline__ D3 affine_exact(const double* t, double u, double v)
+{
+    return {__dadd_rn(__dadd_rn(t[0], __dmul_rn(u, __dsub_rn(t[3], t[0]))), __dmul_rn(v, __dsub_rn(t[6], t[0]))),
+            __dadd_rn(__dadd_rn(t[1], __dmul_rn(u, __dsub_rn(t[4], t[1]))), __dmul_rn(v, __dsub_rn(t[7], t[1]))),
+            __dadd_rn(__dadd_rn(t[2], __dmul_rn(u, __dsub_rn(t[5], t[2]))), __dmul_rn(v, __dsub_rn(t[8], t[2])))};
+}
+__device__ double far_pair_exact(const double* t, const double* s, double area_t, double area_s, int nr)
+{
+    const double four_pi = 4.0 * M_PI;
+    double acc = 0.0;
+    for (int i = 0; i < nr; ++i) {
+        const D3 x = affine_exact(t, c_far_u[i], c_far_v[i]);
+        const double wi = c_far_w[i];
+        for (int j = 0; j < nr; ++j) {
+            const D3 y = affine_exact(s, c_far_u[j], c_far_v[j]);
+            const double r = d3_norm(d3_sub(x, y));
+            const double k = __ddiv_rn(1.0, __dmul_rn(four_pi, r));
+            acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(wi, c_far_w[j]), k));
+        }
+    }
+    return __dmul_rn(__dmul_rn(__dmul_rn(acc, 4.0), area_t), area_s);
+}
+
 constexpr size_t far_smem_bytes(int nfp)
 {
     return (size_t)BS * (BS + 1) * 8 + (size_t)BS * nfp * 32 + (size_t)BS * 6 * 8 + (size_t)BS * 4 * 4;
 }
 
 // NFP: far rule size padded to a multiple of FAR_PASS (16 at the default far_order 4)
-template <int NFP>
+template <int NFP, bool EXACT>
 __global__ void __launch_bounds__(FAR_THREADS, 3)
     k_far_tiles(const TileInfo* __restrict__ tiles, GeoPtrs G, BlockPtrs B, double thr, double* __restrict__ W,
-                int ld, double inv_pi)
+                int ld, double inv_pi, int nr)
 {
     extern __shared__ __align__(16) unsigned char far_smem[];
     double4* Ys = reinterpret_cast<double4*>(far_smem);                 // BS x NFP y-points (y, |y|^2)
-    double* It = reinterpret_cast<double*>(Ys + BS * NFP);              // BS x (BS+1)
+    double* It = reinterpret_cast<double*>(Ys + (EXACT ? 0 : BS * NFP)); // BS x (BS+1)
     double* gcr = It + BS * (BS + 1);                                   // cx, cy, cz, rad, diam, area
     int* gid = reinterpret_cast<int*>(gcr + BS * 6);
     int* gvid = gid + BS;
@@ -269,10 +296,11 @@ __global__ void __launch_bounds__(FAR_THREADS, 3)
     }
     for (int e = threadIdx.x; e < BS * (BS + 1); e += blockDim.x) It[e] = 0.0;
     __syncthreads();
-    for (int e = threadIdx.x; e < BS * NFP; e += blockDim.x) {
-        const int g = gid[e / NFP];
-        Ys[e] = g >= 0 ? far_ypoint(G.v + 9 * g, o, e % NFP) : make_double4(0, 0, 0, 1);
-    }
+    if (!EXACT)
+        for (int e = threadIdx.x; e < BS * NFP; e += blockDim.x) {
+            const int g = gid[e / NFP];
+            Ys[e] = g >= 0 ? far_ypoint(G.v + 9 * g, o, e % NFP) : make_double4(0, 0, 0, 1);
+        }
     __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int fl = (warp & 1) * 32 + lane;
@@ -300,8 +328,16 @@ __global__ void __launch_bounds__(FAR_THREADS, 3)
                 if (far) mask |= 1u << m;
             }
         }
+        if (EXACT) {
+            for (int m = 0, gl = warp >> 1; gl < BS; gl += FAR_THREADS / 64, ++m) {
+                if (!(mask >> m & 1)) continue;
+                const int g = gid[gl];
+                const int tt = f > g ? f : g, ss = f > g ? g : f;
+                It[fl * (BS + 1) + gl] = far_pair_exact(G.v + 9 * tt, G.v + 9 * ss, G.area[tt], G.area[ss], nr);
+            }
+        }
         const double sf = G.area[f] * inv_pi;
-        for (int pass = 0; pass < NFP / FAR_PASS; ++pass) {
+        for (int pass = 0; !EXACT && pass < NFP / FAR_PASS; ++pass) {
             XPts X;
             far_xpoints(G.v + 9 * f, o, pass, X);
             for (int m = 0, gl = warp >> 1; gl < BS; gl += FAR_THREADS / 64, ++m) {
@@ -1160,26 +1196,32 @@ long long run_near(Ctx* ctx, const RuleDims& R, const double* GV, const double* 
 
 }  // namespace
 
-template <int NFP>
+template <int NFP, bool EXACT>
 void launch_far_tiles_n(Ctx* ctx, const TileInfo* tiles, long long ntiles, const GeoPtrs& G, const BlockPtrs& BP,
-                        double thr, DMatrix& W)
+                        double thr, DMatrix& W, int nr)
 {
-    constexpr size_t smem = far_smem_bytes(NFP);
+    constexpr size_t smem = far_smem_bytes(EXACT ? 0 : NFP);
     static bool attr = false;
     if (!attr) {
-        SBG_CUDA(cudaFuncSetAttribute(k_far_tiles<NFP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        SBG_CUDA(cudaFuncSetAttribute(k_far_tiles<NFP, EXACT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr = true;
     }
-    k_far_tiles<NFP><<<(int)ntiles, FAR_THREADS, smem, ctx->stream>>>(tiles, G, BP, thr, W.a.p, W.ld, 1.0 / M_PI);
+    k_far_tiles<NFP, EXACT><<<(int)ntiles, FAR_THREADS, smem, ctx->stream>>>(tiles, G, BP, thr, W.a.p, W.ld,
+                                                                            1.0 / M_PI, nr);
 }
 
 void launch_far_tiles(Ctx* ctx, const RuleDims& R, const TileInfo* tiles, long long ntiles, const GeoPtrs& G,
-                      const BlockPtrs& BP, double thr, DMatrix& W)
+                      const BlockPtrs& BP, double thr, DMatrix& W, bool exact)
 {
     if (ntiles <= 0) return;
+    if (exact) {  // one instantiation: the rule size is a runtime loop bound there
+        launch_far_tiles_n<4, true>(ctx, tiles, ntiles, G, BP, thr, W, R.nf);
+        count_launch();
+        return;
+    }
     switch (R.nfp) {
 #define SBG_FAR_TILES(N) \
-    case N: launch_far_tiles_n<N>(ctx, tiles, ntiles, G, BP, thr, W); break;
+    case N: launch_far_tiles_n<N, false>(ctx, tiles, ntiles, G, BP, thr, W, R.nf); break;
         SBG_FAR_TILES(4) SBG_FAR_TILES(12) SBG_FAR_TILES(16) SBG_FAR_TILES(28) SBG_FAR_TILES(36) SBG_FAR_TILES(52)
         SBG_FAR_TILES(64)
 #undef SBG_FAR_TILES
@@ -1425,7 +1467,7 @@ void assembly_run(AssemblyPlan* P, DMatrix& W, AssemblyStats* stats)
     {
         TimedScope ts(ctx, "far_tiles");
         BlockPtrs BP{P->bfac.p, P->dof_ptr.p, P->dofs.p, P->ent_ptr.p, P->ents.p};
-        launch_far_tiles(ctx, R, P->tiles.p, P->ntiles, P->G.ptrs(), BP, thr, W);
+        launch_far_tiles(ctx, R, P->tiles.p, P->ntiles, P->G.ptrs(), BP, thr, W, P->cfg.exact_far);
         SBG_LAUNCH_CHECK();
     }
     // per-pair scatter of singular + near integrals
@@ -1470,6 +1512,15 @@ void assemble_W(Ctx* ctx, const InflatedMesh& im, const QuadCfg& cfg, DMatrix& W
 }
 
 namespace {
+__global__ void k_far_pair_list_exact(GeoPtrs G, const int2* __restrict__ pairs, long long np,
+                                      double* __restrict__ out, int nr)
+{
+    const long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= np) return;
+    const int f = pairs[k].x, g = pairs[k].y;  // f = t (the larger index, host-ordered)
+    out[k] = far_pair_exact(G.v + 9 * f, G.v + 9 * g, G.area[f], G.area[g], nr);
+}
+
 template <int NFP>
 __global__ void k_far_pair_list(GeoPtrs G, const int2* __restrict__ pairs, long long np, double* __restrict__ out,
                                 double inv_pi)
@@ -1489,10 +1540,17 @@ __global__ void k_far_pair_list(GeoPtrs G, const int2* __restrict__ pairs, long 
     }
     out[k] = acc;
 }
-void far_pair_list(Ctx* ctx, const RuleDims& R, const GeoPtrs& G, const int2* pairs, long long np, double* out)
+void far_pair_list(Ctx* ctx, const RuleDims& R, const GeoPtrs& G, const int2* pairs, long long np, double* out,
+                   bool exact)
 {
     const int grid = (int)((np + 127) / 128);
     cudaStream_t s = ctx->stream;
+    if (exact) {
+        k_far_pair_list_exact<<<grid, 128, 0, s>>>(G, pairs, np, out, R.nf);
+        ::sbg::count_launch();
+        SBG_LAUNCH_CHECK();
+        return;
+    }
     switch (R.nfp) {
 #define SBG_FAR_LIST(N) \
     case N: k_far_pair_list<N><<<grid, 128, 0, s>>>(G, pairs, np, out, 1.0 / M_PI); break;
@@ -1600,7 +1658,7 @@ void pair_integrals(Ctx* ctx, const SurfaceMesh& m, const QuadCfg& cfg, const in
         DBuf<int2> d_p;
         d_p.upload(farp, s);
         DBuf<double> o(farp.size());
-        far_pair_list(ctx, R, G.ptrs(), d_p.p, (long long)farp.size(), o.p);
+        far_pair_list(ctx, R, G.ptrs(), d_p.p, (long long)farp.size(), o.p, cfg.exact_far);
         fetch(o.p, idx[4]);
     }
 }

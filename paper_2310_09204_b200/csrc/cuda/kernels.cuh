@@ -106,6 +106,10 @@ struct QuadCfg {
     int far_order = 4;
     int singular_order = 8;
     double near_threshold = 2.0;
+    // SURVEY Appendix B switch: depth-0 far pairs evaluated bitwise like the oracle (one
+    // thread per pair, i-major 16x16 order, IEEE sqrt and division, no FMA) instead of the
+    // distance expansion with the refined rsqrt
+    bool exact_far = false;
 };
 struct AssemblyStats {
     long long far_pairs = 0, near_pairs = 0, identical = 0, edge = 0, vertex = 0;

@@ -36,7 +36,8 @@ vp = C.c_void_p
 
 
 class QuadCfgC(C.Structure):
-    _fields_ = [("far_order", C.c_int), ("singular_order", C.c_int), ("near_threshold", C.c_double)]
+    _fields_ = [("far_order", C.c_int), ("singular_order", C.c_int), ("near_threshold", C.c_double),
+                ("exact_far", C.c_int)]
 
 
 class PcgReportC(C.Structure):
@@ -390,9 +391,10 @@ class QuadratureConfig:
     far_order: int = 4
     singular_order: int = 8
     near_threshold: float = 2.0
+    exact_far: bool = False  # far pairs bitwise like the CPU restatement
 
     def c(self):
-        return QuadCfgC(self.far_order, self.singular_order, self.near_threshold)
+        return QuadCfgC(self.far_order, self.singular_order, self.near_threshold, 1 if self.exact_far else 0)
 
 
 class GalerkinMatrix(_Handle):

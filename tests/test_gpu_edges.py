@@ -90,3 +90,30 @@ def test_malformed_meshes_raise_validation_error(ctx):
         S.inflate(S.SurfaceMesh([[0, 0, 0], [1, 0, 0], [np.nan, 1, 0]], [[0, 1, 2]]))
     with pytest.raises(S.ValidationError):
         S.inflate(S.SurfaceMesh([[0, 0, 0], [1, 0, 0], [2, 0, 0]], [[0, 1, 2]]))  # degenerate facet
+
+
+def test_exact_far_switch_is_bitwise_on_far_pairs(ctx):
+    """with exact_far the depth-0 far pair integrals are bitwise the
+    CPU restatement's (one thread per pair, i-major order, IEEE sqrt/division, no FMA);
+    the W it assembles matches the oracle per entry and the fast path to the reorder bound."""
+    m = S.make_config(1).fine
+    om = O.Mesh(m.vertices, m.facets)
+    f, g = np.tril_indices(m.nf, -1)
+    sel = np.random.default_rng(3).choice(len(f), 1500, replace=False)
+    f, g = f[sel].astype(np.int32), g[sel].astype(np.int32)
+    dev = S.pair_integrals(m, f, g, S.QuadratureConfig(exact_far=True), ctx=ctx)
+    far = np.zeros(len(f), dtype=bool)
+    ref = np.zeros(len(f))
+    for k in range(len(f)):
+        v, st = O.pair_integrals(om, f[k:k + 1], g[k:k + 1], workers=1, stats=True)
+        ref[k] = v[0]
+        far[k] = st[0] == 1 and st[1] == 0 and st[2] == 0
+    assert far.sum() > 1000
+    assert np.array_equal(dev[far], ref[far]), np.abs(dev[far] - ref[far]).max()
+    assert (np.abs(dev[~far] - ref[~far]) <= 1e-12 * np.abs(ref[~far])).all()
+    im = S.inflate(m)
+    oim = O.inflate(om)
+    We = S.assemble_W(im, S.QuadratureConfig(exact_far=True), ctx=ctx).download()
+    Wf = S.assemble_W(im, ctx=ctx).download()
+    check_W(We, O.assemble_W(oim, workers=WORKERS))
+    assert np.abs(We - Wf).max() <= 1e-13 * np.abs(We).max()

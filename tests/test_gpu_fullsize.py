@@ -36,20 +36,24 @@ def omesh(m):
 @pytest.mark.parametrize("cfg,ratio,rows", [
     (3, 0, [0, 1, 46, 47, 3000, 6720]),      # junction DOFs (q = 3) sit next to the shared edge
     (4, 0, [0, 3000, 6048, 6049, 12096]),    # 6048/6049: DOFs of the origin vertex (q = 8)
-    (5, 40, [0, 12640, 25280]),
+    (5, 40, [0, 12640, 25280]),              # corner rows: the farthest, most cancelling entries
 ])
 def test_fullsize_W_symmetric_and_sampled_rows(ctx, cfg, ratio, rows):
+    """Both far-field paths: the fast one (distance expansion + refined rsqrt) and the
+    SURVEY Appendix B parity-gate path (exact_far: far pairs bitwise the oracle's)."""
     pair = S.make_config(cfg, ratio)
     im = S.inflate(pair.fine, validate=False)
-    W = S.assemble_W(im, ctx=ctx)
-    assert W.symmetry_defect() == 0.0
     rows = np.array([r for r in rows if r < im.n], dtype=np.int32)
     oim = O.inflate(omesh(pair.fine), validate=False)
     Wo = O.assemble_W_rows(oim, rows, workers=WORKERS)
-    Wg = W.rows(rows)
     scale = np.abs(Wo).max()
-    bad = np.abs(Wg - Wo) > 1e-10 * np.abs(Wo) + 1e-13 * scale
-    assert not bad.any(), (bad.sum(), np.abs(Wg - Wo).max() / scale)
+    for exact in (False, True):
+        W = S.assemble_W(im, S.QuadratureConfig(exact_far=exact), ctx=ctx)
+        assert W.symmetry_defect() == 0.0
+        Wg = W.rows(rows)
+        bad = np.abs(Wg - Wo) > 1e-10 * np.abs(Wo) + 1e-13 * scale
+        assert not bad.any(), (exact, bad.sum(), np.abs(Wg - Wo).max() / scale)
+        del W
 
 
 @pytest.mark.parametrize("cfg,ratio", [(3, 0), (4, 0), (5, 40)])
