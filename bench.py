@@ -290,6 +290,16 @@ def run_reference(args):
 
 
 # --------------------------------------------------------------------------- ours
+def matvec_traffic(cfg: int):
+    """DRAM bytes per matvec launch from the committed ncu capture for this config (or None)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_traffic.json")) as f:
+            e = json.load(f)["gemv_f64"].get(str(cfg))
+        return None if e is None else e["dram_read"] + e["dram_write"]
+    except Exception:
+        return None
+
+
 def load_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -445,7 +455,7 @@ def run_ours(args):
                                                        else far_flop / (far_ms * 1e-3) / 1e12)
                                             if min(far_ms, near_ms) > 0 else None}},
             "roofline_matvec": {"bound": "hbm", "kernel": "gemv_f64", "achieved": matvec_gbs, "peak": hbm_peak,
-                                "unit": "GB/s", "frac": matvec_gbs / hbm_peak, "traffic": None,
+                                "unit": "GB/s", "frac": matvec_gbs / hbm_peak, "traffic": matvec_traffic(cfg),
                                 "bytes_per_launch": matvec_bytes, "us_per_launch": matvec_s * 1e6,
                                 "peak_source": ("of measured: MEASURED_PEAKS.json hbm_gbs (a copy; a read-only "
                                                 "stream can exceed it)") if peaks.get("hbm_gbs") else "of fallback",
