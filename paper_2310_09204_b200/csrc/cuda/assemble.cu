@@ -748,7 +748,7 @@ __global__ void __launch_bounds__(SAUTER_THREADS)
         g2z = s2[2] - s0[2];
     }
     const int q0 = blockIdx.y * chunk, q1 = min(npts, q0 + chunk);
-    double acc0 = 0.0, acc1 = 0.0;
+    double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
     for (int base = q0; base < q1; base += SAUTER_STAGE) {
         const int cnt = min(SAUTER_STAGE, q1 - base);
         __syncthreads();
@@ -756,18 +756,21 @@ __global__ void __launch_bounds__(SAUTER_THREADS)
         __syncthreads();
         if (active) {
             int i = 0;
-            for (; i + 2 <= cnt; i += 2) {
-                const double* a = R + 5 * i;
-                const double* b = a + 5;
-                // x - y = (t0 - s0) + a1 e1t + a2 e2t - b1 e1s - b2 e2s
-                const double ax = fma(-a[3], g2x, fma(-a[2], g1x, fma(a[1], e2x, fma(a[0], e1x, d0x))));
-                const double ay = fma(-a[3], g2y, fma(-a[2], g1y, fma(a[1], e2y, fma(a[0], e1y, d0y))));
-                const double az = fma(-a[3], g2z, fma(-a[2], g1z, fma(a[1], e2z, fma(a[0], e1z, d0z))));
-                const double bx = fma(-b[3], g2x, fma(-b[2], g1x, fma(b[1], e2x, fma(b[0], e1x, d0x))));
-                const double by = fma(-b[3], g2y, fma(-b[2], g1y, fma(b[1], e2y, fma(b[0], e1y, d0y))));
-                const double bz = fma(-b[3], g2z, fma(-b[2], g1z, fma(b[1], e2z, fma(b[0], e1z, d0z))));
-                acc0 = fma(a[4], rsqrt_fast(fma(ax, ax, fma(ay, ay, az * az))), acc0);
-                acc1 = fma(b[4], rsqrt_fast(fma(bx, bx, fma(by, by, bz * bz))), acc1);
+            // four independent evaluations per step: x - y = (t0 - s0) + a1 e1t + a2 e2t - b1 e1s - b2 e2s
+            for (; i + 4 <= cnt; i += 4) {
+                double r2[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const double* a = R + 5 * (i + u);
+                    const double ax = fma(-a[3], g2x, fma(-a[2], g1x, fma(a[1], e2x, fma(a[0], e1x, d0x))));
+                    const double ay = fma(-a[3], g2y, fma(-a[2], g1y, fma(a[1], e2y, fma(a[0], e1y, d0y))));
+                    const double az = fma(-a[3], g2z, fma(-a[2], g1z, fma(a[1], e2z, fma(a[0], e1z, d0z))));
+                    r2[u] = fma(ax, ax, fma(ay, ay, az * az));
+                }
+                acc0 = fma(R[5 * i + 4], rsqrt_fast(r2[0]), acc0);
+                acc1 = fma(R[5 * i + 9], rsqrt_fast(r2[1]), acc1);
+                acc2 = fma(R[5 * i + 14], rsqrt_fast(r2[2]), acc2);
+                acc3 = fma(R[5 * i + 19], rsqrt_fast(r2[3]), acc3);
             }
             for (; i < cnt; ++i) {
                 const double* a = R + 5 * i;
@@ -778,7 +781,7 @@ __global__ void __launch_bounds__(SAUTER_THREADS)
             }
         }
     }
-    if (active) part[(size_t)blockIdx.y * npairs + p] = acc0 + acc1;
+    if (active) part[(size_t)blockIdx.y * npairs + p] = (acc0 + acc1) + (acc2 + acc3);
 }
 
 // I = (sum of chunk partials) * 4 A_t A_s / (4 pi)   (quadrature.hpp:254-261)
