@@ -82,3 +82,20 @@ def test_fullsize_pcg_matches_oracle_on_device_W(ctx, cfg, ratio):
     assert abs(rep.iterations - orep.iterations) <= 1, (rep.iterations, orep.iterations)
     xerr = np.linalg.norm(rep.solution - orep.solution) / np.linalg.norm(orep.solution)
     assert xerr <= 1e-8, xerr
+
+
+def test_config2_full_W_every_entry(ctx):
+    """The bench workload (BASELINE configs[1]): all 15.75M entries of the device W against
+    the oracle's full assemble_W (all host threads, ~15 s), per entry, with the worst
+    entries reported both ways."""
+    pair = S.make_config(2)
+    im = S.inflate(pair.fine)
+    Wg = S.assemble_W(im, ctx=ctx).download()
+    Wo = O.assemble_W(O.inflate(omesh(pair.fine)), workers=WORKERS)
+    scale = np.abs(Wo).max()
+    err = np.abs(Wg - Wo)
+    bad = err > 1e-10 * np.abs(Wo) + 1e-13 * scale
+    rel = err / np.maximum(np.abs(Wo), 1e-300)
+    assert not bad.any(), (bad.sum(), err.max() / scale, rel.max())
+    assert err.max() / scale < 1e-12, err.max() / scale      # norm-relative: far below 1e-10
+    assert np.array_equal(Wg, Wg.T)
