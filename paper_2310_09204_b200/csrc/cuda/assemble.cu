@@ -1146,27 +1146,27 @@ long long run_near(Ctx* ctx, const RuleDims& R, const double* GV, const double* 
     SBG_CUDA(cudaStreamSynchronize(s));
     long long ncur = (long long)h[0], total_leaves = 0;
     for (int depth = 0; depth <= 5 && ncur > 0; ++depth) {
-        const long long cap_next = depth < 5 ? 4 * ncur : 0;
-        // cur/next swap every level: grow both together (and with headroom) so a
-        // plan that is run again never reallocates (cudaFree synchronises the device)
-        if ((long long)NW.next.n < cap_next) {
-            const long long want = std::max<long long>(cap_next, (long long)NW.cur.n) * 5 / 4;
-            NW.next.alloc(want);
-            if ((long long)NW.cur.n < want) {
-                DBuf<NearNode> grown(want);
-                SBG_CUDA(cudaMemcpyAsync(grown.p, NW.cur.p, ncur * sizeof(NearNode), cudaMemcpyDeviceToDevice, s));
-                std::swap(NW.cur, grown);
-                SBG_CUDA(cudaStreamSynchronize(s));
-            }
-        }
         if ((long long)NW.leaves.n < ncur) NW.leaves.alloc(ncur * 5 / 4);
-        SBG_CUDA(cudaMemsetAsync(NW.cnt.p + 1, 0, 2 * sizeof(unsigned long long), s));
-        {
-            TimedScope tc(ctx, "near_classify");
-            const int grid = (int)std::min<long long>((ncur + 127) / 128, 16LL * ctx->sm_count);
-            k_near_level<<<grid, 128, 0, s>>>(NW.cur.p, NW.cnt.p, ncur, depth, pairs, GV, thr, NW.leaves.p,
-                                              NW.cnt.p + 2, ncur, NW.next.p, NW.cnt.p + 1, cap_next);
-            count_launch();
+        // classify into the existing next-frontier capacity; on overflow grow it to the
+        // exact count (+25%) and classify again (idempotent), so the frontier buffers size
+        // to the real level populations instead of the 4x upper bound, and a plan that is
+        // run again never reallocates
+        for (int attempt = 0;; ++attempt) {
+            const long long cap_next = depth < 5 ? (long long)NW.next.n : 0;
+            SBG_CUDA(cudaMemsetAsync(NW.cnt.p + 1, 0, 2 * sizeof(unsigned long long), s));
+            {
+                TimedScope tc(ctx, "near_classify");
+                const int grid = (int)std::min<long long>((ncur + 127) / 128, 16LL * ctx->sm_count);
+                k_near_level<<<grid, 128, 0, s>>>(NW.cur.p, NW.cnt.p, ncur, depth, pairs, GV, thr, NW.leaves.p,
+                                                  NW.cnt.p + 2, ncur, NW.next.p, NW.cnt.p + 1, cap_next);
+                count_launch();
+                SBG_LAUNCH_CHECK();
+            }
+            SBG_CUDA(cudaMemcpyAsync(h, NW.cnt.p, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+            SBG_CUDA(cudaStreamSynchronize(s));
+            if (depth == 5 || (long long)h[1] <= cap_next) break;
+            if (attempt > 0) throw std::logic_error("near frontier: inconsistent level count");
+            NW.next.alloc((long long)h[1] * 5 / 4);
         }
         {
             TimedScope tl(ctx, "near_leaves");
@@ -1187,8 +1187,6 @@ long long run_near(Ctx* ctx, const RuleDims& R, const double* GV, const double* 
             count_launch();
         }
         SBG_LAUNCH_CHECK();
-        SBG_CUDA(cudaMemcpyAsync(h, NW.cnt.p, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
-        SBG_CUDA(cudaStreamSynchronize(s));
         total_leaves += (long long)h[2];
         ncur = (long long)h[1];
         std::swap(NW.cur, NW.next);

@@ -288,6 +288,9 @@ void gemv_plan(Ctx* ctx, int n, int ld, GemvPlan& plan)
     const int target = 4 * ctx->sm_count;
     int chunks = std::max(1, (target + plan.strips - 1) / plan.strips);
     chunks = std::min(chunks, std::max(1, n / 32));
+    // x of a row chunk is staged in shared memory: keep it within the 48 KB default
+    constexpr int kMaxChunkRows = (48 << 10) / (int)sizeof(double) - 8;
+    chunks = std::max(chunks, (n + kMaxChunkRows - 1) / kMaxChunkRows);
     plan.rows_per_chunk = std::max(8, ((n + chunks - 1) / chunks + 7) / 8 * 8);
     plan.chunks = std::max(1, (n + plan.rows_per_chunk - 1) / plan.rows_per_chunk);
     plan.part.alloc((size_t)plan.chunks * ld);
@@ -547,6 +550,13 @@ void pcg_run(Ctx* ctx, const DMatrix& W, Prec* prec, const double* rhs, double* 
                 ng = nullptr;
             } catch (...) {
                 ctx->timers.enabled = timers;
+                cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+                if (cudaStreamIsCapturing(s, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone) {
+                    cudaGraph_t junk = nullptr;  // leave capture mode before anything else touches the stream
+                    cudaStreamEndCapture(s, &junk);
+                    if (junk && junk != ng) cudaGraphDestroy(junk);
+                }
+                (void)cudaGetLastError();
                 if (ng) cudaGraphDestroy(ng);
                 w.drop_graph();
                 throw;
