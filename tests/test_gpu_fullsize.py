@@ -99,3 +99,20 @@ def test_config2_full_W_every_entry(ctx):
     assert not bad.any(), (bad.sum(), err.max() / scale, rel.max())
     assert err.max() / scale < 1e-12, err.max() / scale      # norm-relative: far below 1e-10
     assert np.array_equal(Wg, Wg.T)
+
+
+def test_beyond_configs_size_independent_properties(ctx):
+    """A flat 200x200 screen (80 000 triangles, 39 601 DOFs, 12.5 GB W) — larger than any
+    BASELINE config: W exactly symmetric, PCG converges, and the returned solution's true
+    residual ||b - W x|| (device matvec, independent of the PCG recurrences) is consistent
+    with the stopping rule."""
+    pair = S.make_panels(0, 200, 20)
+    fine, coarse = S.inflate(pair.fine, validate=False), S.inflate(pair.coarse)
+    W = S.assemble_W(fine, ctx=ctx)
+    assert W.n == 39601 and W.symmetry_defect() == 0.0
+    L = S.assemble_rhs(fine, [0.0, 0.0, 1.0], ctx=ctx)
+    prec = S.build_preconditioner(W, S.partition_dofs(pair, fine), S.build_prolongation(pair, coarse, fine))
+    rep = S.pcg(W, prec, L, 1e-8)
+    assert rep.converged and rep.iterations < 40
+    res = L - W.matvec(rep.solution)
+    assert np.linalg.norm(res) <= 1e-6 * np.linalg.norm(L), np.linalg.norm(res) / np.linalg.norm(L)
