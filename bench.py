@@ -217,6 +217,17 @@ def cpu_assembly_sample(cfg: int, ratio: int, target_s: float):
                       f"{t:.1f} s", "seconds": t, "pairs": pairs}
 
 
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip() + f" ({os.cpu_count()} logical CPUs)"
+    except Exception:
+        pass
+    return f"unknown ({os.cpu_count()} logical CPUs)"
+
+
 def cpu_phases(cfg: int, ratio: int, W_host=None, max_n: int = 8000):
     """The reference's other phases on the CPU restatement, single-threaded as in the
     reference (Eigen without OpenMP): setup (inflate both levels, partition_dofs,
@@ -246,6 +257,12 @@ def cpu_phases(cfg: int, ratio: int, W_host=None, max_n: int = 8000):
     t0 = time.perf_counter()
     prec = O.build_preconditioner(W_host, part, R)
     out["build_preconditioner_s"] = time.perf_counter() - t0
+    xv = O.normal_draws(5, fine.n)
+    t0 = time.perf_counter()
+    O.matvec(W_host, xv, reps=3)
+    mv = (time.perf_counter() - t0) / 3
+    out["matvec_s"] = mv
+    out["matvec_gbs"] = 8.0 * fine.n * fine.n / mv / 1e9
     r = O.normal_draws(17, fine.n)
     t0 = time.perf_counter()
     for _ in range(3):
@@ -255,6 +272,7 @@ def cpu_phases(cfg: int, ratio: int, W_host=None, max_n: int = 8000):
     t0 = time.perf_counter()
     rep = O.pcg(W_host, prec, L, 1e-8)
     dt = time.perf_counter() - t0
+    out["cpu_model"] = cpu_model()
     out.update({"pcg_s": dt, "pcg_iterations": rep.iterations,
                 "pcg_iters_per_s": rep.iterations / dt if dt > 0 else None, "threads": 1,
                 "matrix": "GPU-assembled W (downloaded)" if "assembly_s" not in out else "oracle assemble_W"})
@@ -431,8 +449,13 @@ def run_ours(args):
             cpu = cpu_assembly_sample(cfg, ratio, args.cpu_seconds)
             cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
             if not args.no_cpu_phases:
-                cpu["phases"] = cpu_phases(cfg, ratio, W.download() if n <= args.cpu_phases_max_n else None,
-                                           max_n=args.cpu_phases_max_n)
+                ph = cpu_phases(cfg, ratio, W.download() if n <= args.cpu_phases_max_n else None,
+                                max_n=args.cpu_phases_max_n)
+                if "pcg_s" in ph and cpu.get("value"):
+                    # setup + full assembly at the sampled rate + preconditioner + PCG
+                    ph["time_to_solution_s_est"] = (ph["setup_s"] + npairs / cpu["value"] + ph["build_preconditioner_s"]
+                                                    + ph["pcg_s"])
+                cpu["phases"] = ph
         except Exception as e:  # pragma: no cover
             cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "port", "sample": f"failed: {e}"}
     if rank == 0:

@@ -98,6 +98,7 @@ def lib():
                                   C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_double), f64p,
                                   C.c_void_p, f64p, f64p, C.c_int, C.POINTER(C.c_int)]),
             "orc_direct_solve": (C.c_int, [f64p, C.c_int, f64p, f64p]),
+            "orc_matvec": (C.c_int, [f64p, C.c_int, f64p, f64p, C.c_int]),
             "orc_lanczos_kappa": (C.c_double, [f64p, f64p, C.c_int]),
             "orc_random_spd": (C.c_int, [C.c_int, C.c_uint, f64p]),
             "orc_normal_draws": (C.c_int, [C.c_uint, C.c_int, f64p]),
@@ -551,6 +552,14 @@ def pcg(W, prec, rhs, tol=1e-8, maxit=0, exact=None) -> PcgReport:
     return PcgReport(x, k, bool(conv.value), hist[:hl.value].copy(),
                      en[:hl.value].copy() if ex is not None else np.zeros(0), kap.value, al[:k].copy(),
                      be[:nb].copy())
+
+
+def matvec(W, x, reps: int = 1):
+    """y = W x as in the PCG loop (pcg.hpp:70), dense row-major, single thread."""
+    W = np.ascontiguousarray(W, dtype=np.float64)
+    y = np.zeros(W.shape[0])
+    _check(lib().orc_matvec(W.reshape(-1), W.shape[0], np.ascontiguousarray(x, dtype=np.float64), y, reps))
+    return y
 
 
 def direct_solve(W, rhs):

@@ -520,6 +520,20 @@ int orc_normal_draws(unsigned seed, int count, double* out)
     return 0;
 }
 
+// y = W x, the PCG matvec of pcg.hpp:70 (dense row-major, single thread), `reps` times
+int orc_matvec(const double* W, int n, const double* x, double* y, int reps)
+{
+    return guard([&] {
+        for (int r = 0; r < reps; ++r)
+            for (int i = 0; i < n; ++i) {
+                double s = 0;
+                const double* row = W + (size_t)i * n;
+                for (int j = 0; j < n; ++j) s += row[j] * x[j];
+                y[i] = s;
+            }
+    });
+}
+
 double orc_wall_seconds()
 {
     return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
