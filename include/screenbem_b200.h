@@ -72,6 +72,7 @@ typedef struct {
 /* assembly work counters (roofline bookkeeping) */
 typedef struct {
     long long far_pairs, near_pairs, identical, edge, vertex, near_leaves, tiles, tiles_skipped;
+    long long h2d_bytes; /* host-to-device bytes of the plan build (mesh data, curl lists, tiles) */
 } sbg_assembly_stats;
 
 const char* sbg_last_error(void);

@@ -392,6 +392,7 @@ int sbg_assemble_w(sbg_ctx* ctx, const sbg_inflated* im, const sbg_quad_cfg* cfg
                 stats->near_leaves = st.near_leaves;
                 stats->tiles = st.tiles;
                 stats->tiles_skipped = st.tiles_skipped;
+                stats->h2d_bytes = st.h2d_bytes;
             }
         } catch (...) {
             delete W;
@@ -433,6 +434,7 @@ int sbg_assembly_run(sbg_aplan* plan, sbg_matrix** W, sbg_assembly_stats* stats)
                 stats->near_leaves = st.near_leaves;
                 stats->tiles = st.tiles;
                 stats->tiles_skipped = st.tiles_skipped;
+                stats->h2d_bytes = st.h2d_bytes;
             }
         } catch (...) {
             if (fresh) {

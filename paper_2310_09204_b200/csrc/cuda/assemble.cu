@@ -1074,6 +1074,22 @@ void upload_sauter(Ctx* ctx, const QuadCfg& cfg, SauterRulesDev& R)
     R.npts[1] = vx.size();
 }
 
+// device copies of the Sauter rules, cached on the context per singular order (a fresh
+// plan — every reference-style assemble_W call — does not upload the 5 MB of rules again)
+std::shared_ptr<const SauterRulesDev> device_sauter(Ctx* ctx, const QuadCfg& cfg)
+{
+    using Cache = std::map<int, std::shared_ptr<SauterRulesDev>>;
+    if (!ctx->sauter_ws) ctx->sauter_ws = std::make_shared<Cache>();
+    auto& cache = *static_cast<Cache*>(ctx->sauter_ws.get());
+    auto& slot = cache[cfg.singular_order];
+    if (!slot) {
+        auto R = std::make_shared<SauterRulesDev>();
+        upload_sauter(ctx, cfg, *R);
+        slot = R;
+    }
+    return slot;
+}
+
 void run_sauter(Ctx* ctx, const DBuf<double>& X, const std::vector<int>& pv, const SauterRulesDev& R, int cls,
                 double* out_dev)
 {
@@ -1251,8 +1267,9 @@ struct AssemblyPlan {
     DBuf<int> pv[4];
     DBuf<double> spart[4];
     int schunks[4] = {0, 0, 0, 0}, schunk[4] = {0, 0, 0, 0};
-    SauterRulesDev SR;
+    std::shared_ptr<const SauterRulesDev> SR;
     long long near_cap = 0;
+    long long h2d_bytes = 0;  // host-to-device bytes of the plan build (e2e bookkeeping)
     DBuf<int2> loc_pairs;
     DBuf<double> loc_I;
     DBuf<unsigned long long> near_cnt;
@@ -1376,7 +1393,7 @@ AssemblyPlan* assembly_plan_create(Ctx* ctx, const InflatedMesh& im, const QuadC
         // ---- singular lists (host adjacency, deterministic order) and Sauter workspaces
         SingularLists S;
         singular_pairs(m, S);
-        upload_sauter(ctx, cfg, P->SR);
+        P->SR = device_sauter(ctx, cfg);
         P->near_cap = std::max<long long>(1024, 64LL * nf);
         long long off = 0;
         for (int cls = 1; cls <= 3; ++cls) {
@@ -1393,7 +1410,7 @@ AssemblyPlan* assembly_plan_create(Ctx* ctx, const InflatedMesh& im, const QuadC
             SBG_CUDA(cudaMemcpyAsync(P->loc_pairs.p + P->cls_off[cls], S.pairs[cls].data(), np * sizeof(int2),
                                      cudaMemcpyHostToDevice, s));
             P->pv[cls].upload(S.pv[cls], s);
-            const int npts = P->SR.npts[cls];
+            const int npts = P->SR->npts[cls];
             const int pblocks = (int)((np + SAUTER_THREADS - 1) / SAUTER_THREADS);
             int nchunks = std::max(1, std::min((4 * ctx->sm_count + pblocks - 1) / pblocks, (npts + 999) / 1000));
             const int chunk = (npts + nchunks - 1) / nchunks;
@@ -1403,6 +1420,12 @@ AssemblyPlan* assembly_plan_create(Ctx* ctx, const InflatedMesh& im, const QuadC
         }
         P->near_cnt.alloc(1);
         SBG_CUDA(cudaStreamSynchronize(s));
+        // host-to-device bytes of this plan (e2e bookkeeping; rules are cached per context)
+        auto bytes = [](const auto& b) { return (long long)(b.n * sizeof(*b.p)); };
+        P->h2d_bytes = bytes(P->G.X) + bytes(P->G.F) + bytes(P->uptr) + bytes(P->udof) + bytes(P->uval) +
+                       bytes(P->bfac) + bytes(P->dof_ptr) + bytes(P->dofs) + bytes(P->ent_ptr) + bytes(P->ents) +
+                       bytes(P->tiles) + bytes(P->cand) + P->nsing * (long long)sizeof(int2);
+        for (int cls = 1; cls <= 3; ++cls) P->h2d_bytes += bytes(P->pv[cls]);
     } catch (...) {
         delete P;
         throw;
@@ -1457,7 +1480,7 @@ void assembly_run(AssemblyPlan* P, DMatrix& W, AssemblyStats* stats)
         TimedScope ts(ctx, "sauter");
         const int pblocks = (int)((np + SAUTER_THREADS - 1) / SAUTER_THREADS);
         k_sauter_partial<<<dim3(pblocks, P->schunks[cls]), SAUTER_THREADS, 0, s>>>(
-            P->pv[cls].p, (int)np, P->G.X.p, P->SR.r[cls].p, P->SR.npts[cls], P->schunk[cls], P->spart[cls].p);
+            P->pv[cls].p, (int)np, P->G.X.p, P->SR->r[cls].p, P->SR->npts[cls], P->schunk[cls], P->spart[cls].p);
         count_launch();
         k_sauter_finish<<<(int)((np + 127) / 128), 128, 0, s>>>(P->spart[cls].p, (int)np, P->schunks[cls],
                                                                  P->pv[cls].p, P->G.X.p, P->loc_I.p + P->cls_off[cls]);
@@ -1496,6 +1519,7 @@ void assembly_run(AssemblyPlan* P, DMatrix& W, AssemblyStats* stats)
         stats->far_pairs = (long long)P->nf * (P->nf + 1) / 2 - nloc;
         stats->tiles = P->ntiles;
         stats->tiles_skipped = P->ntiles - P->ncand;
+        stats->h2d_bytes = P->h2d_bytes;
     }
 }
 
@@ -1576,8 +1600,7 @@ void pair_integrals(Ctx* ctx, const SurfaceMesh& m, const QuadCfg& cfg, const in
     const RuleDims R = upload_rules(ctx, cfg);
     DeviceGeometry G;
     upload_geometry(ctx, m, G);
-    SauterRulesDev SR;
-    upload_sauter(ctx, cfg, SR);
+    const SauterRulesDev& SR = *device_sauter(ctx, cfg);
     std::vector<double> hgc(3 * (size_t)m.num_facets()), hrad(m.num_facets()), hdiam(m.num_facets());
     SBG_CUDA(cudaMemcpyAsync(hgc.data(), G.c.p, hgc.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
     SBG_CUDA(cudaMemcpyAsync(hrad.data(), G.rad.p, hrad.size() * sizeof(double), cudaMemcpyDeviceToHost, s));

@@ -109,6 +109,7 @@ struct Ctx {
     std::shared_ptr<void> flush_ws; // L2 flush buffers (context.cu)
     std::shared_ptr<void> prec_sched; // last preconditioner task schedule (precond.cu)
     std::shared_ptr<void> scratch_ws; // grow-only scratch buffers (context.cu: scratch())
+    std::shared_ptr<void> sauter_ws;  // device Sauter rules per singular order (assemble.cu)
     ~Ctx();
 };
 

@@ -114,6 +114,7 @@ struct QuadCfg {
 struct AssemblyStats {
     long long far_pairs = 0, near_pairs = 0, identical = 0, edge = 0, vertex = 0;
     long long near_leaves = 0, tiles = 0, tiles_skipped = 0;
+    long long h2d_bytes = 0;  // bytes uploaded by the plan build
 };
 struct AssemblyPlan;
 AssemblyPlan* assembly_plan_create(Ctx* ctx, const InflatedMesh& im, const QuadCfg& cfg);

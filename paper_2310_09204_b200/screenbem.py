@@ -47,7 +47,7 @@ class PcgReportC(C.Structure):
 
 class AssemblyStatsC(C.Structure):
     _fields_ = [(n, C.c_longlong) for n in ("far_pairs", "near_pairs", "identical", "edge", "vertex",
-                                             "near_leaves", "tiles", "tiles_skipped")]
+                                             "near_leaves", "tiles", "tiles_skipped", "h2d_bytes")]
 
 
 # signature table: name -> (restype, argtypes); also the exported-symbol contract
