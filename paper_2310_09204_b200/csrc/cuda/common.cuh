@@ -131,6 +131,27 @@ struct TimedScope {
     ~TimedScope();
 };
 
+// Programmatic dependent launch: the next kernel of a dependent chain (the PCG iteration)
+// is launched while the previous one drains; it waits in pdl_wait() until its predecessor
+// has completed and flushed, so only launch latency and grid tails overlap.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args)
+{
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    SBG_CUDA(cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...));
+}
+
 // Dense symmetric fp64 matrix resident in HBM (GalerkinMatrix, assemble.hpp:12).
 // Row-major with a leading dimension padded to 32 doubles (256-byte rows) so
 // every row starts 16-byte aligned for 128-bit streaming loads; the padding

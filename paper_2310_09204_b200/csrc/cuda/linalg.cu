@@ -24,6 +24,7 @@ __global__ void __launch_bounds__(kGemvThreads) k_gemv_partial(const double* __r
                                                                const double* __restrict__ x, int rows_per_chunk,
                                                                double* __restrict__ part, const int* done)
 {
+    pdl_wait();
     if (done && *done) return;
     extern __shared__ double sx[];
     const int r0 = blockIdx.y * rows_per_chunk;
@@ -144,6 +145,7 @@ __global__ void k_pcg_init(PcgDev* st, const double* __restrict__ r, const doubl
 __global__ void k_pcg_alpha(PcgDev* st, const double* __restrict__ part, int chunks, int ld, int n,
                             const double* __restrict__ p, double* __restrict__ Wp, double* partials)
 {
+    pdl_wait();
     if (st->done) return;
     __shared__ double sh[32];
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
@@ -172,6 +174,7 @@ __global__ void k_pcg_alpha(PcgDev* st, const double* __restrict__ part, int chu
 __global__ void k_pcg_update(const PcgDev* st, double* __restrict__ x, double* __restrict__ r,
                              const double* __restrict__ p, const double* __restrict__ Wp, int n)
 {
+    pdl_wait();
     if (st->done) return;
     const double a = st->alpha;
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
@@ -185,6 +188,7 @@ __global__ void k_pcg_update(const PcgDev* st, double* __restrict__ x, double* _
 __global__ void k_pcg_rz(PcgDev* st, const double* __restrict__ r, const double* __restrict__ z, int n,
                          double* partials, double* hist, double* alphas, double* betas)
 {
+    pdl_wait();
     if (st->done) return;
     __shared__ double sh[32];
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
@@ -220,12 +224,14 @@ __global__ void k_pcg_rz(PcgDev* st, const double* __restrict__ r, const double*
 // handle is non-zero
 __global__ void k_pcg_gate(const PcgDev* st, cudaGraphConditionalHandle h)
 {
+    pdl_wait();
     if (threadIdx.x == 0) cudaGraphSetConditional(h, st->done ? 0u : 1u);
 }
 
 // p = z + beta p (pcg.hpp:93)
 __global__ void k_pcg_p(const PcgDev* st, double* __restrict__ p, const double* __restrict__ z, int n)
 {
+    pdl_wait();
     if (st->done) return;
     const double b = st->beta;
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
@@ -239,6 +245,7 @@ __global__ void __launch_bounds__(256) k_gemv_rows(const double* __restrict__ W,
                                                    const double* __restrict__ x, double* __restrict__ y,
                                                    const int* done)
 {
+    pdl_wait();
     if (done && *done) return;
     const int row = blockIdx.x * kRowsPerCta + (threadIdx.x >> 5), lane = threadIdx.x & 31;
     if (row >= n) return;
@@ -299,15 +306,16 @@ void gemv_plan(Ctx* ctx, int n, int ld, GemvPlan& plan)
 static void gemv_partial_launch(Ctx* ctx, const DMatrix& W, GemvPlan& plan, const double* x, const int* done)
 {
     if (plan.rows) {
-        k_gemv_rows<<<(W.n + kRowsPerCta - 1) / kRowsPerCta, 256, 0, ctx->stream>>>(W.a.p, W.ld, W.n, x,
-                                                                                    plan.part.p, done);
+        launch_pdl(k_gemv_rows, dim3((W.n + kRowsPerCta - 1) / kRowsPerCta), dim3(256), 0, ctx->stream, W.a.p, W.ld,
+                   W.n, x, plan.part.p, done);
         ::sbg::count_launch();
         SBG_LAUNCH_CHECK();
         return;
     }
     const size_t smem = (size_t)plan.rows_per_chunk * sizeof(double);
-    k_gemv_partial<<<dim3(plan.strips, plan.chunks), kGemvThreads, smem, ctx->stream>>>(
-        W.a.p, W.ld, W.n, x, plan.rows_per_chunk, plan.part.p, done); ::sbg::count_launch();
+    launch_pdl(k_gemv_partial, dim3(plan.strips, plan.chunks), dim3(kGemvThreads), smem, ctx->stream, W.a.p, W.ld, W.n,
+               x, plan.rows_per_chunk, plan.part.p, done);
+    ::sbg::count_launch();
     SBG_LAUNCH_CHECK();
 }
 
@@ -486,14 +494,15 @@ void pcg_run(Ctx* ctx, const DMatrix& W, Prec* prec, const double* rhs, double* 
             TimedScope ts(ctx, "gemv_f64");
             gemv_partial_launch(ctx, W, w.plan, p, done);
         }
-        k_pcg_alpha<<<nb, 256, 0, s>>>(w.st.p, w.plan.part.p, w.plan.chunks, W.ld, n, p, Wp, w.partials.p);
+        launch_pdl(k_pcg_alpha, dim3(nb), dim3(256), 0, s, w.st.p, w.plan.part.p, w.plan.chunks, W.ld, n, p, Wp,
+                   w.partials.p);
         count_launch();
-        k_pcg_update<<<nb, 256, 0, s>>>(w.st.p, x, r, p, Wp, n);
+        launch_pdl(k_pcg_update, dim3(nb), dim3(256), 0, s, w.st.p, x, r, p, Wp, n);
         count_launch();
         if (prec) prec_apply(ctx, prec, r, z, done);
-        k_pcg_rz<<<nb, 256, 0, s>>>(w.st.p, r, z, n, w.partials.p, w.hist.p, w.alphas.p, w.betas.p);
+        launch_pdl(k_pcg_rz, dim3(nb), dim3(256), 0, s, w.st.p, r, z, n, w.partials.p, w.hist.p, w.alphas.p, w.betas.p);
         count_launch();
-        k_pcg_p<<<nb, 256, 0, s>>>(w.st.p, p, z, n);
+        launch_pdl(k_pcg_p, dim3(nb), dim3(256), 0, s, w.st.p, p, z, n);
         count_launch();
         SBG_LAUNCH_CHECK();
     };

@@ -512,6 +512,7 @@ __global__ void __launch_bounds__(256) k_prec_gather(const double* __restrict__ 
                                                      const int* __restrict__ crow, const double* __restrict__ cval,
                                                      int nc, double* __restrict__ loc_c, int dof_blocks, const int* done)
 {
+    pdl_wait();
     if (done && *done) return;
     if ((int)blockIdx.x < dof_blocks) {
         const int d = blockIdx.x * blockDim.x + threadIdx.x;
@@ -551,6 +552,7 @@ __global__ void __launch_bounds__(256) k_block_gemv(const int2* __restrict__ tas
                                                     const double* __restrict__ loc, double* __restrict__ locy,
                                                     const int* done)
 {
+    pdl_wait();
     if (done && *done) return;
     const int2 t = tasks[blockIdx.x];
     const int b = t.x, nb = nbv[b], ldm = ldmv[b];
@@ -687,6 +689,7 @@ __global__ void k_prec_scatter(const double* __restrict__ locy, const int* __res
                                const double* __restrict__ rval, const double* __restrict__ y_c,
                                double* __restrict__ z, const int* done)
 {
+    pdl_wait();
     if (done && *done) return;
     const int d = blockIdx.x * blockDim.x + threadIdx.x;
     if (d >= n) return;
@@ -1084,14 +1087,13 @@ void prec_apply(Ctx* ctx, Prec* P, const double* r, double* z, const int* done)
     const int cb = P->coarse_block;
     double* loc_c = cb >= 0 ? P->loc.p + P->h_loc[cb] : nullptr;
     const int dof_blocks = (n + 255) / 256;
-    k_prec_gather<<<dof_blocks + P->nc, 256, 0, s>>>(r, n, P->pos.p, P->loc.p, P->Rc_ptr.p, P->Rc_row.p,
-                                                               P->Rc_val.p, P->nc, loc_c, dof_blocks, done);
+    launch_pdl(k_prec_gather, dim3(dof_blocks + P->nc), dim3(256), 0, s, r, n, P->pos.p, P->loc.p, P->Rc_ptr.p,
+               P->Rc_row.p, P->Rc_val.p, P->nc, loc_c, dof_blocks, done);
     count_launch();
     const double* yloc;
     if (P->mode == kPrecInverse) {
-        k_block_gemv<<<(int)P->sched->gemv.size(), 256, 0, s>>>(P->sched->d_gemv.p, P->d_nb.p, P->d_ldm.p,
-                                                                P->d_loc.p, P->d_Moff.p, P->Mc.p, P->loc.p,
-                                                                P->locy.p, done);
+        launch_pdl(k_block_gemv, dim3((unsigned)P->sched->gemv.size()), dim3(256), 0, s, P->sched->d_gemv.p,
+                   P->d_nb.p, P->d_ldm.p, P->d_loc.p, P->d_Moff.p, P->Mc.p, P->loc.p, P->locy.p, done);
         count_launch();
         yloc = P->locy.p;
     } else {
@@ -1113,8 +1115,9 @@ void prec_apply(Ctx* ctx, Prec* P, const double* r, double* z, const int* done)
         }
         yloc = P->loc.p;
     }
-    k_prec_scatter<<<(n + 255) / 256, 256, 0, s>>>(yloc, P->pos.p, n, P->nc > 0 ? P->Rr_ptr.p : nullptr, P->Rr_col.p,
-                                                   P->Rr_val.p, cb >= 0 ? yloc + P->h_loc[cb] : nullptr, z, done);
+    launch_pdl(k_prec_scatter, dim3((n + 255) / 256), dim3(256), 0, s, (const double*)yloc, (const int*)P->pos.p, n,
+               (const int*)(P->nc > 0 ? P->Rr_ptr.p : nullptr), (const int*)P->Rr_col.p, (const double*)P->Rr_val.p,
+               (const double*)(cb >= 0 ? yloc + P->h_loc[cb] : nullptr), z, done);
     count_launch();
     SBG_LAUNCH_CHECK();
 }
