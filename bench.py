@@ -50,6 +50,11 @@ def parse():
     ap.add_argument("--ratio", type=int, default=0, help="H/h for config 5 (default 8)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU sample length")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo: functional check of the N>1 paths (ranks may share one GPU; not a timing)")
+    ap.add_argument("--shard", action="store_true",
+                    help="N>1: assemble ONE W across the ranks (1/N of the pair work each, NCCL all-reduce "
+                         "of the partial W), strong scaling; default is N independent replicas")
     return ap.parse_args()
 
 
@@ -335,9 +340,20 @@ def run_ours(args):
     if world > 1:
         import torch
         import torch.distributed as dist
+        if args.dist_backend == "gloo":  # functional check of the N>1 paths; ranks may share a GPU
+            local = local % torch.cuda.device_count()
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
+        dist.init_process_group(args.dist_backend)
     ctx = S.Context(local)
+    rdev = "cpu" if args.dist_backend == "gloo" else f"cuda:{local}"
+
+    def allreduce_(t):
+        if rdev == "cpu":
+            h = t.cpu()
+            dist.all_reduce(h)
+            t.copy_(h)
+        else:
+            dist.all_reduce(t)
     ctx.timers(True)
     cfg = args.config
     ratio = args.ratio if args.ratio else (8 if cfg == 5 else 0)
@@ -353,8 +369,27 @@ def run_ours(args):
     plan = S.AssemblyPlan(fine, qcfg, ctx=ctx)
     plan_ms = {k: round(ctx.timer(k)[0], 3) for k in ("plan_total", "plan_curls", "plan_tiles", "plan_singular")}
 
+    shard = args.shard and world > 1
+
+    def assemble(plan, W):
+        """the timed assembly: the whole W, or this rank's shard + the all-reduce of the
+        partial W over NCCL (in place on W's device storage, through __cuda_array_interface__)"""
+        if not shard:
+            return plan.run(W)
+        import torch
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        ev[0].record()  # legacy stream; the context stream is a blocking stream
+        W = plan.run(W, shard=(rank, world))
+        allreduce_(torch.as_tensor(W, device=f"cuda:{local}"))
+        ev[1].record()
+        ev[1].synchronize()
+        shard_ms.append(ev[0].elapsed_time(ev[1]))
+        return W
+
+    shard_ms = []
+
     def step(W):
-        W = plan.run(W)
+        W = assemble(plan, W)
         L = S.assemble_rhs(fine, g, ctx=ctx)
         prec = S.build_preconditioner(W, part, P)
         rep = S.pcg(W, prec, L, 1e-8)
@@ -388,10 +423,19 @@ def run_ours(args):
     ms = {k: v[0] / args.steps for k, v in tm.items()}
     launches_per_step = {k: v[1] / args.steps for k, v in tm.items()}
     t_asm = ms["assemble_W"] * 1e-3
+    if shard:  # shard compute + all-reduce, per step
+        t_asm = sum(shard_ms[-args.steps:]) / args.steps * 1e-3
     step_ms = ms["step"]
-    t_asm, step_ms = reduce_max([t_asm, step_ms], dist, f"cuda:{local}")
-    value = world * npairs / t_asm
-    stats = W.stats
+    t_asm, step_ms = reduce_max([t_asm, step_ms], dist, rdev)
+    value = (1 if shard else world) * npairs / t_asm
+    stats = dict(W.stats)
+    if shard:  # a shard does not separate its far count: total far pairs (exact) / world
+        import torch
+        loc = torch.tensor([sum(stats[k] for k in ("identical", "edge", "vertex", "near_pairs"))],
+                           dtype=torch.float64, device=rdev)
+        dist.all_reduce(loc)
+        stats["far_pairs"] = int(round((npairs - float(loc[0])) / world))
+        stats["far_pairs_estimated"] = True
     # ---- dominant-kernel roofline (FP64 pipe): SURVEY.md §8d 20 flop per tensor-rule evaluation
     fp64_peak = S.fp64_peak_tflops(ctx)
     far_ms, near_ms = ms["far_tiles"], ms["near_leaves"]
@@ -436,7 +480,10 @@ def run_ours(args):
         ctx.reset_timers()
         t0 = time.perf_counter()
         ctx.begin("e2e")
-        W2 = S.assemble_W(im2, ctx=ctx)
+        if shard:
+            W2 = assemble(S.AssemblyPlan(im2, qcfg, ctx=ctx), None)
+        else:
+            W2 = S.assemble_W(im2, ctx=ctx)
         h2d = int(W2.stats["h2d_bytes"])
         Wh = W2.download()
         ctx.end()
@@ -444,7 +491,7 @@ def run_ours(args):
         e2e_times.append(ctx.timer("e2e")[0] * 1e-3)
         del W2, Wh
     e2e_t = min(e2e_times[1:]) if len(e2e_times) > 1 else e2e_times[0]
-    e2e_t = reduce_max([e2e_t], dist, f"cuda:{local}")[0]
+    e2e_t = reduce_max([e2e_t], dist, rdev)[0]
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
@@ -463,10 +510,12 @@ def run_ours(args):
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "strong" if shard else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"config {cfg}: {CFG_NAMES[cfg]}" + (f", H/h {ratio}" if cfg == 5 else ""),
-                       "triangles": nf, "dofs": n, "tri_pairs": npairs, "parallelism": f"replicas x{world}",
+                       "triangles": nf, "dofs": n, "tri_pairs": npairs, "parallelism": (f"assembly sharded x{world} (NCCL all-reduce of W), "
+                                                                   f"preconditioner + PCG replicated") if shard
+                       else f"replicas x{world}",
                        "l2": "flushed (256 MiB write + 256 MiB read: cold L2 with clean lines) before every timed step and every matvec launch",
                        "pcg_tol": 1e-8, "far_field": "exact (IEEE, oracle order)" if args.exact_far else
                        "fast (distance expansion + refined rsqrt)"},
@@ -494,7 +543,7 @@ def run_ours(args):
             "phase_launches_per_step": launches_per_step,
             "plan_build_ms_host": plan_ms,
             "assembly_stats": stats,
-            "e2e": {"value": world * npairs / e2e_t, "unit": UNIT, "h2d_bytes_per_step": h2d,
+            "e2e": {"value": (1 if shard else world) * npairs / e2e_t, "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": 8 * n * n, "ms": e2e_t * 1e3,
                     "what": "S.assemble_W(host InflatedMesh) + W.download(): plan build (host), H2D, kernels, "
                             "D2H of the n x n W into host memory (the reference arm times assemble_W on an "

@@ -129,9 +129,17 @@ int sbg_assemble_w(sbg_ctx* ctx, const sbg_inflated* im, const sbg_quad_cfg* cfg
  * (re)fills *W (allocated on first use) */
 int sbg_assembly_plan_create(sbg_ctx* ctx, const sbg_inflated* im, const sbg_quad_cfg* cfg, sbg_aplan** out);
 int sbg_assembly_run(sbg_aplan* plan, sbg_matrix** W, sbg_assembly_stats* stats);
+/* one shard (rank of world) of sbg_assembly_run for multi-GPU assembly of one W:
+ * far / near-candidate tiles k with k % world == rank and a contiguous 1/world
+ * of each singular class; the world shards' W sum entrywise to the full W (the
+ * caller reduces them, e.g. an NCCL all-reduce over sbg_matrix_device_view).
+ * The reference's per-worker partial W + sum (inc/assemble.hpp:91-133), across processes. */
+int sbg_assembly_run_shard(sbg_aplan* plan, sbg_matrix** W, int rank, int world, sbg_assembly_stats* stats);
 void sbg_assembly_plan_destroy(sbg_aplan* plan);
 int sbg_matrix_create(sbg_ctx* ctx, int n, const double* host_rowmajor, sbg_matrix** out);
 int sbg_matrix_n(const sbg_matrix* W);
+/* device storage of W: row-major n x ld doubles (ld >= n, padding zero), count = n * ld */
+int sbg_matrix_device_view(const sbg_matrix* W, void** data, int* ld, long long* count);
 int sbg_matrix_download(const sbg_matrix* W, double* host_rowmajor);
 int sbg_matrix_download_rows(const sbg_matrix* W, const int32_t* rows, int nrows, double* host);
 int sbg_matrix_symmetry_defect(const sbg_matrix* W, double* max_abs);

@@ -417,13 +417,19 @@ int sbg_assembly_plan_create(sbg_ctx* ctx, const sbg_inflated* im, const sbg_qua
 }
 int sbg_assembly_run(sbg_aplan* plan, sbg_matrix** W, sbg_assembly_stats* stats)
 {
+    return sbg_assembly_run_shard(plan, W, 0, 1, stats);
+}
+int sbg_assembly_run_shard(sbg_aplan* plan, sbg_matrix** W, int rank, int world, sbg_assembly_stats* stats)
+{
     return guard([&] {
+        need(plan, "plan");
+        if (world < 1 || rank < 0 || rank >= world) throw ValidationError("shard: need 0 <= rank < world");
         need(W, "W");
         const bool fresh = *W == nullptr;
         if (fresh) *W = new sbg_matrix;
         try {
             AssemblyStats st;
-            assembly_run(plan->P, (*W)->M, &st);
+            assembly_run(plan->P, (*W)->M, &st, rank, world);
             SBG_CUDA(cudaStreamSynchronize(plan->ctx->stream));
             if (stats) {
                 stats->far_pairs = st.far_pairs;
@@ -464,6 +470,15 @@ int sbg_matrix_create(sbg_ctx* ctx, int n, const double* host, sbg_matrix** out)
     });
 }
 int sbg_matrix_n(const sbg_matrix* W) { return W ? W->M.n : -1; }
+int sbg_matrix_device_view(const sbg_matrix* W, void** data, int* ld, long long* count)
+{
+    return guard([&] {
+        need(W, "W");
+        if (data) *data = W->M.a.p;
+        if (ld) *ld = W->M.ld;
+        if (count) *count = (long long)W->M.a.n;
+    });
+}
 int sbg_matrix_download(const sbg_matrix* W, double* host)
 {
     return guard([&] { matrix_download(W->M, host); });

@@ -268,8 +268,8 @@ constexpr size_t far_smem_bytes(int nfp)
 // NFP: far rule size padded to a multiple of FAR_PASS (16 at the default far_order 4)
 template <int NFP, bool EXACT>
 __global__ void __launch_bounds__(FAR_THREADS, 3)
-    k_far_tiles(const TileInfo* __restrict__ tiles, GeoPtrs G, BlockPtrs B, double thr, double* __restrict__ W,
-                int ld, double inv_pi, int nr)
+    k_far_tiles(const TileInfo* __restrict__ tiles, int tstride, GeoPtrs G, BlockPtrs B, double thr,
+                double* __restrict__ W, int ld, double inv_pi, int nr)
 {
     extern __shared__ __align__(16) unsigned char far_smem[];
     double4* Ys = reinterpret_cast<double4*>(far_smem);                 // BS x NFP y-points (y, |y|^2)
@@ -278,7 +278,7 @@ __global__ void __launch_bounds__(FAR_THREADS, 3)
     int* gid = reinterpret_cast<int*>(gcr + BS * 6);
     int* gvid = gid + BS;
     __shared__ double o[3];
-    const TileInfo T = tiles[blockIdx.x];
+    const TileInfo T = tiles[(size_t)blockIdx.x * tstride];  // tstride > 1: one shard of the tile list
     const bool diag = T.fb == T.gb;
     if (threadIdx.x < 3) o[threadIdx.x] = G.v[9 * B.facets[T.fb * BS] + threadIdx.x];
     for (int e = threadIdx.x; e < BS; e += blockDim.x) {
@@ -358,11 +358,11 @@ __global__ void __launch_bounds__(FAR_THREADS, 3)
 }
 
 // near-list builder: pairs of non-certainly-far tiles that are disjoint but not far
-__global__ void k_classify_near(const TileInfo* __restrict__ tiles, GeoPtrs G, const int* __restrict__ bfacets,
-                                double thr, int2* __restrict__ near_list, unsigned long long cap,
-                                unsigned long long* __restrict__ count)
+__global__ void k_classify_near(const TileInfo* __restrict__ tiles, int tstride, GeoPtrs G,
+                                const int* __restrict__ bfacets, double thr, int2* __restrict__ near_list,
+                                unsigned long long cap, unsigned long long* __restrict__ count)
 {
-    const TileInfo T = tiles[blockIdx.x];
+    const TileInfo T = tiles[(size_t)blockIdx.x * tstride];
     const bool diag = T.fb == T.gb;
     for (int e = threadIdx.x; e < BS * BS; e += blockDim.x) {
         const int fl = e / BS, gl = e % BS;
@@ -1214,8 +1214,8 @@ long long run_near(Ctx* ctx, const RuleDims& R, const double* GV, const double* 
 }  // namespace
 
 template <int NFP, bool EXACT>
-void launch_far_tiles_n(Ctx* ctx, const TileInfo* tiles, long long ntiles, const GeoPtrs& G, const BlockPtrs& BP,
-                        double thr, DMatrix& W, int nr)
+void launch_far_tiles_n(Ctx* ctx, const TileInfo* tiles, long long ntiles, int tstride, const GeoPtrs& G,
+                        const BlockPtrs& BP, double thr, DMatrix& W, int nr)
 {
     constexpr size_t smem = far_smem_bytes(EXACT ? 0 : NFP);
     static bool attr = false;
@@ -1223,22 +1223,23 @@ void launch_far_tiles_n(Ctx* ctx, const TileInfo* tiles, long long ntiles, const
         SBG_CUDA(cudaFuncSetAttribute(k_far_tiles<NFP, EXACT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr = true;
     }
-    k_far_tiles<NFP, EXACT><<<(int)ntiles, FAR_THREADS, smem, ctx->stream>>>(tiles, G, BP, thr, W.a.p, W.ld,
-                                                                            1.0 / M_PI, nr);
+    k_far_tiles<NFP, EXACT><<<(int)ntiles, FAR_THREADS, smem, ctx->stream>>>(tiles, tstride, G, BP, thr, W.a.p,
+                                                                            W.ld, 1.0 / M_PI, nr);
 }
 
-void launch_far_tiles(Ctx* ctx, const RuleDims& R, const TileInfo* tiles, long long ntiles, const GeoPtrs& G,
-                      const BlockPtrs& BP, double thr, DMatrix& W, bool exact)
+// ntiles launches: tile k of the launch is tiles[k * tstride]
+void launch_far_tiles(Ctx* ctx, const RuleDims& R, const TileInfo* tiles, long long ntiles, int tstride,
+                      const GeoPtrs& G, const BlockPtrs& BP, double thr, DMatrix& W, bool exact)
 {
     if (ntiles <= 0) return;
     if (exact) {  // one instantiation: the rule size is a runtime loop bound there
-        launch_far_tiles_n<4, true>(ctx, tiles, ntiles, G, BP, thr, W, R.nf);
+        launch_far_tiles_n<4, true>(ctx, tiles, ntiles, tstride, G, BP, thr, W, R.nf);
         count_launch();
         return;
     }
     switch (R.nfp) {
 #define SBG_FAR_TILES(N) \
-    case N: launch_far_tiles_n<N, false>(ctx, tiles, ntiles, G, BP, thr, W, R.nf); break;
+    case N: launch_far_tiles_n<N, false>(ctx, tiles, ntiles, tstride, G, BP, thr, W, R.nf); break;
         SBG_FAR_TILES(4) SBG_FAR_TILES(12) SBG_FAR_TILES(16) SBG_FAR_TILES(28) SBG_FAR_TILES(36) SBG_FAR_TILES(52)
         SBG_FAR_TILES(64)
 #undef SBG_FAR_TILES
@@ -1436,8 +1437,13 @@ AssemblyPlan* assembly_plan_create(Ctx* ctx, const InflatedMesh& im, const QuadC
 void assembly_plan_destroy(AssemblyPlan* P) { delete P; }
 
 // reference: inc/assemble.hpp:72-139 (device kernels only; the plan holds the mesh data)
-void assembly_run(AssemblyPlan* P, DMatrix& W, AssemblyStats* stats)
+// Shard (rank, world) of world > 1 computes only its share of the work into a
+// zeroed W: far tiles and near candidate tiles k with k % world == rank, and a
+// contiguous 1/world range of each singular class.  The shards' W sum to the
+// full W (up to fp64 atomic reordering); DESIGN.md §5.3.
+void assembly_run(AssemblyPlan* P, DMatrix& W, AssemblyStats* stats, int rank, int world)
 {
+    if (world < 1 || rank < 0 || rank >= world) throw ValidationError("shard: need 0 <= rank < world");
     Ctx* ctx = P->ctx;
     cudaStream_t s = ctx->stream;
     TimedScope total(ctx, "assemble_W");
@@ -1446,15 +1452,22 @@ void assembly_run(AssemblyPlan* P, DMatrix& W, AssemblyStats* stats)
     if (P->nf == 0 || P->n == 0) return;
     const RuleDims R = upload_rules(ctx, P->cfg);
     const double thr = P->cfg.near_threshold;
+    auto share = [&](long long cnt) { return cnt > rank ? (cnt - rank + world - 1) / world : 0LL; };
+    const long long my_tiles = share(P->ntiles), my_cand = share(P->ncand);
+    long long sing_lo[4] = {0, 0, 0, 0}, sing_cnt[4] = {0, 0, 0, 0};
+    for (int cls = 1; cls <= 3; ++cls) {
+        sing_lo[cls] = P->cls_cnt[cls] * rank / world;
+        sing_cnt[cls] = P->cls_cnt[cls] * (rank + 1) / world - sing_lo[cls];
+    }
     // near list (classification of the non-certainly-far tiles)
     long long leaves = 0;
     unsigned long long nnear = 0;
     for (int attempt = 0; attempt < 2; ++attempt) {
         SBG_CUDA(cudaMemsetAsync(P->near_cnt.p, 0, sizeof(unsigned long long), s));
-        if (P->ncand) {
+        if (my_cand) {
             TimedScope ts(ctx, "classify");
-            k_classify_near<<<(int)P->ncand, 256, 0, s>>>(P->cand.p, P->G.ptrs(), P->bfac.p, thr,
-                                                          P->loc_pairs.p + P->nsing, P->near_cap, P->near_cnt.p);
+            k_classify_near<<<(int)my_cand, 256, 0, s>>>(P->cand.p + rank, world, P->G.ptrs(), P->bfac.p, thr,
+                                                         P->loc_pairs.p + P->nsing, P->near_cap, P->near_cnt.p);
             count_launch();
             SBG_LAUNCH_CHECK();
         }
@@ -1473,17 +1486,20 @@ void assembly_run(AssemblyPlan* P, DMatrix& W, AssemblyStats* stats)
         P->loc_pairs = std::move(np2);
         P->loc_I = std::move(ni2);
     }
-    // singular pairs (Sauter rules)
+    // singular pairs (Sauter rules); a shard zeroes the integrals it does not own
+    if (world > 1 && P->nsing) SBG_CUDA(cudaMemsetAsync(P->loc_I.p, 0, P->nsing * sizeof(double), s));
     for (int cls = 1; cls <= 3; ++cls) {
-        const long long np = P->cls_cnt[cls];
+        const long long np = sing_cnt[cls];
         if (!np) continue;
         TimedScope ts(ctx, "sauter");
+        const int* pv = P->pv[cls].p + 6 * sing_lo[cls];
         const int pblocks = (int)((np + SAUTER_THREADS - 1) / SAUTER_THREADS);
         k_sauter_partial<<<dim3(pblocks, P->schunks[cls]), SAUTER_THREADS, 0, s>>>(
-            P->pv[cls].p, (int)np, P->G.X.p, P->SR->r[cls].p, P->SR->npts[cls], P->schunk[cls], P->spart[cls].p);
+            pv, (int)np, P->G.X.p, P->SR->r[cls].p, P->SR->npts[cls], P->schunk[cls], P->spart[cls].p);
         count_launch();
-        k_sauter_finish<<<(int)((np + 127) / 128), 128, 0, s>>>(P->spart[cls].p, (int)np, P->schunks[cls],
-                                                                 P->pv[cls].p, P->G.X.p, P->loc_I.p + P->cls_off[cls]);
+        k_sauter_finish<<<(int)((np + 127) / 128), 128, 0, s>>>(P->spart[cls].p, (int)np, P->schunks[cls], pv,
+                                                                 P->G.X.p,
+                                                                 P->loc_I.p + P->cls_off[cls] + sing_lo[cls]);
         count_launch();
         SBG_LAUNCH_CHECK();
     }
@@ -1491,7 +1507,7 @@ void assembly_run(AssemblyPlan* P, DMatrix& W, AssemblyStats* stats)
     {
         TimedScope ts(ctx, "far_tiles");
         BlockPtrs BP{P->bfac.p, P->dof_ptr.p, P->dofs.p, P->ent_ptr.p, P->ents.p};
-        launch_far_tiles(ctx, R, P->tiles.p, P->ntiles, P->G.ptrs(), BP, thr, W, P->cfg.exact_far);
+        launch_far_tiles(ctx, R, P->tiles.p + rank, my_tiles, world, P->G.ptrs(), BP, thr, W, P->cfg.exact_far);
         SBG_LAUNCH_CHECK();
     }
     // per-pair scatter of singular + near integrals
@@ -1511,14 +1527,15 @@ void assembly_run(AssemblyPlan* P, DMatrix& W, AssemblyStats* stats)
         SBG_LAUNCH_CHECK();
     }
     if (stats) {
-        stats->identical = P->cls_cnt[3];
-        stats->edge = P->cls_cnt[2];
-        stats->vertex = P->cls_cnt[1];
+        stats->identical = sing_cnt[3];
+        stats->edge = sing_cnt[2];
+        stats->vertex = sing_cnt[1];
         stats->near_pairs = (long long)nnear;
         stats->near_leaves = leaves;
-        stats->far_pairs = (long long)P->nf * (P->nf + 1) / 2 - nloc;
-        stats->tiles = P->ntiles;
-        stats->tiles_skipped = P->ntiles - P->ncand;
+        // per shard the far count is not separated from the tiles' own classification
+        stats->far_pairs = world == 1 ? (long long)P->nf * (P->nf + 1) / 2 - nloc : -1;
+        stats->tiles = my_tiles;
+        stats->tiles_skipped = my_tiles - my_cand;
         stats->h2d_bytes = P->h2d_bytes;
     }
 }

@@ -119,7 +119,8 @@ struct AssemblyStats {
 struct AssemblyPlan;
 AssemblyPlan* assembly_plan_create(Ctx* ctx, const InflatedMesh& im, const QuadCfg& cfg);
 void assembly_plan_destroy(AssemblyPlan* p);
-void assembly_run(AssemblyPlan* p, DMatrix& W, AssemblyStats* stats);
+// (rank, world): one shard of the work (world 1 = the whole assembly), see assemble.cu
+void assembly_run(AssemblyPlan* p, DMatrix& W, AssemblyStats* stats, int rank = 0, int world = 1);
 void assemble_W(Ctx* ctx, const InflatedMesh& im, const QuadCfg& cfg, DMatrix& W, AssemblyStats* stats);
 void pair_integrals(Ctx* ctx, const SurfaceMesh& m, const QuadCfg& cfg, const int* f, const int* g, long long np,
                     double* out);

@@ -66,6 +66,8 @@ SIGNATURES = {
     "sbg_launch_count": (C.c_longlong, []),
     "sbg_assembly_plan_create": (C.c_int, [vp, vp, C.POINTER(QuadCfgC), C.POINTER(vp)]),
     "sbg_assembly_run": (C.c_int, [vp, C.POINTER(vp), C.POINTER(AssemblyStatsC)]),
+    "sbg_assembly_run_shard": (C.c_int, [vp, C.POINTER(vp), C.c_int, C.c_int, C.POINTER(AssemblyStatsC)]),
+    "sbg_matrix_device_view": (C.c_int, [vp, C.POINTER(vp), C.POINTER(C.c_int), C.POINTER(C.c_longlong)]),
     "sbg_assembly_plan_destroy": (None, [vp]),
     "sbg_mesh_create": (C.c_int, [C.c_int, f64p, C.c_int, i32p, C.POINTER(vp)]),
     "sbg_mesh_destroy": (None, [vp]),
@@ -424,6 +426,15 @@ class GalerkinMatrix(_Handle):
         _check(lib().sbg_matrix_download(self.h, out.reshape(-1)))
         return out
 
+    @property
+    def __cuda_array_interface__(self):
+        """The device storage, row-major (n, ld) float64 with zero padding columns: lets
+        torch / NCCL reduce the shards of a sharded assembly in place (AssemblyPlan.run)."""
+        p, ld, cnt = vp(), C.c_int(), C.c_longlong()
+        _check(lib().sbg_matrix_device_view(self.h, C.byref(p), C.byref(ld), C.byref(cnt)))
+        return {"shape": (self.n, ld.value), "typestr": "<f8", "data": (p.value or 0, False), "version": 3,
+                "strides": None, "stream": None}
+
     def rows(self, rows):
         rows = np.ascontiguousarray(rows, dtype=np.int32)
         out = np.zeros(len(rows) * self.n)
@@ -481,10 +492,14 @@ class AssemblyPlan(_Handle):
         self.n, self.nf = im.n, im.base.nf
         self._W = None
 
-    def run(self, W: GalerkinMatrix = None) -> GalerkinMatrix:
+    def run(self, W: GalerkinMatrix = None, shard=None) -> GalerkinMatrix:
+        """shard=(rank, world): only that share of the pair work, into a zeroed W; the
+        world shards sum entrywise to the full W (reference: the per-worker partial
+        matrices of inc/assemble.hpp:91-133, here one per process / GPU)."""
         st = AssemblyStatsC()
         hw = vp(W.h.value if W is not None else None)
-        _check(lib().sbg_assembly_run(self.h, C.byref(hw), C.byref(st)))
+        rank, world = shard if shard is not None else (0, 1)
+        _check(lib().sbg_assembly_run_shard(self.h, C.byref(hw), int(rank), int(world), C.byref(st)))
         stats = {n: getattr(st, n) for n, _ in AssemblyStatsC._fields_}
         if W is None:
             W = GalerkinMatrix(hw, self.ctx, stats)

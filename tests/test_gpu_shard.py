@@ -1,0 +1,60 @@
+"""Sharded assembly of one W (multi-GPU assembly), checked on one GPU:
+the world shards of AssemblyPlan.run(shard=(rank, world)) sum entrywise to the full W,
+as the reference's per-worker partial matrices do (inc/assemble.hpp:91-133), and the
+in-place device reduction through __cuda_array_interface__ (what bench.py --shard
+hands to NCCL) reproduces the sum."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+S = pytest.importorskip("paper_2310_09204_b200.screenbem")
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    return S.Context(0)
+
+
+@pytest.mark.parametrize("spec", ["config1", "bowtie:3"])
+def test_shards_sum_to_full_W(ctx, spec):
+    m = S.make_config(1).fine if spec == "config1" else S.make_builtin(spec)
+    im = S.inflate(m)
+    plan = S.AssemblyPlan(im, ctx=ctx)
+    full = plan.run()
+    Wf = full.download()
+    scale = np.abs(Wf).max()
+    for world in (2, 3, 5):
+        parts = [plan.run(shard=(r, world)) for r in range(world)]
+        Ws = sum(p.download() for p in parts)
+        # the reference's own worker-reorder bound (tests/test_assemble.cpp:271-279)
+        assert np.abs(Ws - Wf).max() <= 1e-13 * scale, (world, np.abs(Ws - Wf).max() / scale)
+        assert np.array_equal(Ws, Ws.T)
+        for k in ("identical", "edge", "vertex", "near_pairs", "tiles", "tiles_skipped"):
+            assert sum(p.stats[k] for p in parts) == full.stats[k], k
+        assert all(p.stats["far_pairs"] == -1 for p in parts)
+        # every shard is non-trivial
+        assert all(np.abs(p.download()).max() > 0 for p in parts)
+
+
+def test_device_reduction_through_array_interface(ctx):
+    torch = pytest.importorskip("torch")
+    im = S.inflate(S.make_builtin("bowtie:3"))
+    plan = S.AssemblyPlan(im, ctx=ctx)
+    Wf = plan.run().download()
+    a, b = plan.run(shard=(0, 2)), plan.run(shard=(1, 2))
+    ta = torch.as_tensor(a, device="cuda:0")
+    tb = torch.as_tensor(b, device="cuda:0")
+    assert ta.shape[0] == a.n and ta.shape[1] >= a.n and ta.dtype == torch.float64
+    ta += tb  # in place on W's own storage
+    torch.cuda.synchronize()
+    Wa = a.download()
+    assert np.abs(Wa - Wf).max() <= 1e-13 * np.abs(Wf).max()
+    assert np.array_equal(Wa, Wa.T)
+    assert not ta[:, a.n:].any()  # padding columns stay zero
+
+
+def test_bad_shard_is_a_validation_error(ctx):
+    plan = S.AssemblyPlan(S.inflate(S.make_builtin("bowtie:1")), ctx=ctx)
+    for shard in ((2, 2), (-1, 2), (0, 0)):
+        with pytest.raises(S.ValidationError, match="shard"):
+            plan.run(shard=shard)
