@@ -194,6 +194,21 @@ inline GalerkinMatrix assemble_W(Context& ctx, const InflatedMesh& im, const Qua
     check(sbg_assemble_w(ctx.get(), im.get(), &c, workers, &p, nullptr));
     return GalerkinMatrix(p);
 }
+// one process's partial W of a multi-GPU assembly (the reference's per-worker partial
+// matrices, inc/assemble.hpp:91-133): the `world` shards sum entrywise to assemble_W's W;
+// reduce them in place over sbg_matrix_device_view (e.g. ncclAllReduce)
+inline GalerkinMatrix assemble_W_shard(Context& ctx, const InflatedMesh& im, int rank, int world,
+                                       const QuadratureConfig& cfg = {})
+{
+    const sbg_quad_cfg c = cfg.c();
+    sbg_aplan* plan = nullptr;
+    check(sbg_assembly_plan_create(ctx.get(), im.get(), &c, &plan));
+    sbg_matrix* p = nullptr;
+    const int rc = sbg_assembly_run_shard(plan, &p, rank, world, nullptr);
+    sbg_assembly_plan_destroy(plan);
+    check(rc);
+    return GalerkinMatrix(p);
+}
 // reference: inc/assemble.hpp:143-184 with a constant field g
 inline std::vector<double> assemble_rhs(Context& ctx, const InflatedMesh& im, const double g[3],
                                         const QuadratureConfig& cfg = {})

@@ -41,3 +41,4 @@ def test_cpp_dropin_runs_cfg1(tmp_path):
     assert f"iterations {res.report.iterations}" in r.stdout
     kp = float(r.stdout.split("kappa_prec")[1].split()[0])
     assert kp == pytest.approx(S.condition_number(res.W, res.prec).kappa, rel=1e-8)
+    assert float(r.stdout.split("shard_sum_rel")[1].split()[0]) <= 1e-13

@@ -1,6 +1,8 @@
 // The reference's cmd_solve hot path (inc/experiments.hpp:130-145) written against
 // the C++ drop-in header screenbem/gpu.hpp.  Built and run by tests/test_cpp_dropin.py.
 //   g++ -std=c++17 -I include tools/cpp_dropin_example.cpp -L paper_2310_09204_b200/_lib -lscreenbem_b200
+#include <algorithm>
+#include <cmath>
 #include <cstdio>
 
 #include "screenbem/gpu.hpp"
@@ -25,6 +27,16 @@ int main(int argc, char** argv)
                     rep.kappa_estimate);
         const sb::SpectrumResult sp = sb::condition_number(ctx, W, P);  // schwarz.hpp:185-190
         std::printf("kappa_prec %.8f\n", sp.kappa);
+        // two shards of a multi-GPU assembly sum to W (here both on this GPU)
+        const std::vector<double> Wh = W.download();
+        std::vector<double> Ws = sb::assemble_W_shard(ctx, fine, 0, 2).download();
+        const std::vector<double> W1 = sb::assemble_W_shard(ctx, fine, 1, 2).download();
+        double dmax = 0.0, wmax = 0.0;
+        for (size_t k = 0; k < Wh.size(); ++k) {
+            dmax = std::max(dmax, std::fabs(Ws[k] + W1[k] - Wh[k]));
+            wmax = std::max(wmax, std::fabs(Wh[k]));
+        }
+        std::printf("shard_sum_rel %.3e\n", dmax / wmax);
         return rep.converged ? 0 : 3;
     } catch (const screenbem::ValidationError& e) {
         std::fprintf(stderr, "validation error: %s\n", e.what());
