@@ -210,6 +210,9 @@ int sbg_pcg(sbg_ctx* ctx, const sbg_matrix* W, sbg_prec* prec, const double* rhs
 /* ---- device-resident benchmarking helpers (inputs already in HBM) --------- */
 int sbg_device_alloc(sbg_ctx* ctx, long long bytes, void** dptr);
 int sbg_device_free(void* dptr);
+/* page-locked host memory: sbg_matrix_download into it is one pitched DMA (no staging copy) */
+int sbg_host_alloc(long long bytes, void** hptr);
+int sbg_host_free(void* hptr);
 int sbg_memcpy_h2d(sbg_ctx* ctx, void* dst, const void* src, long long bytes);
 int sbg_memcpy_d2h(sbg_ctx* ctx, void* dst, const void* src, long long bytes);
 int sbg_pcg_device(sbg_ctx* ctx, const sbg_matrix* W, sbg_prec* prec, const double* d_rhs, double tol, int maxit,

@@ -823,6 +823,20 @@ int sbg_device_free(void* dptr)
 {
     return guard([&] { device_free(dptr); });
 }
+int sbg_host_alloc(long long bytes, void** hptr)
+{
+    return guard([&] {
+        need(hptr, "hptr");
+        *hptr = nullptr;
+        if (bytes > 0) SBG_CUDA(cudaHostAlloc(hptr, (size_t)bytes, cudaHostAllocDefault));
+    });
+}
+int sbg_host_free(void* hptr)
+{
+    return guard([&] {
+        if (hptr) SBG_CUDA(cudaFreeHost(hptr));
+    });
+}
 int sbg_memcpy_h2d(sbg_ctx* ctx, void* dst, const void* src, long long bytes)
 {
     return guard([&] {

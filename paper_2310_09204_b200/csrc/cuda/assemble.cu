@@ -19,6 +19,7 @@
 //   in its upper triangle and mirrored at the end (assemble.hpp:136-137).
 #include <algorithm>
 #include <cmath>
+#include <future>
 #include <numeric>
 #include <stdexcept>
 #include <string>
@@ -1289,13 +1290,17 @@ AssemblyPlan* assembly_plan_create(Ctx* ctx, const InflatedMesh& im, const QuadC
         P->nf = nf;
         P->n = im.num_jump_dofs();
         if (nf == 0 || P->n == 0) return P;
+        // host preparation that depends only on the mesh runs beside the main thread:
+        // the singular lists (vertex adjacency) and the curl lists
+        auto sing_fut = std::async(std::launch::async, [&m] {
+            SingularLists S;
+            singular_pairs(m, S);
+            return S;
+        });
+        auto curl_fut = std::async(std::launch::async, [&im] { return facet_curls(im); });
         P->dims = upload_rules(ctx, cfg);
         upload_geometry(ctx, m, P->G);
         HostScope hs1(ctx, "plan_curls");
-        const FacetCurls U = facet_curls(im);
-        P->uptr.upload(U.ptr, s);
-        P->udof.upload(U.dof, s);
-        P->uval.upload(U.u, s);
         // ---- Morton-ordered facet blocks
         std::vector<Vec3> cen(nf);
         double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
@@ -1321,6 +1326,10 @@ AssemblyPlan* assembly_plan_create(Ctx* ctx, const InflatedMesh& im, const QuadC
         std::vector<int> perm(nf);
         std::iota(perm.begin(), perm.end(), 0);
         std::stable_sort(perm.begin(), perm.end(), [&](int a, int b) { return key[a] < key[b]; });
+        const FacetCurls U = curl_fut.get();
+        P->uptr.upload(U.ptr, s);
+        P->udof.upload(U.dof, s);
+        P->uval.upload(U.u, s);
         const int nblk = (nf + BS - 1) / BS;
         std::vector<int> bfac((size_t)nblk * BS, -1);
         for (int k = 0; k < nf; ++k) bfac[k] = perm[k];
@@ -1392,8 +1401,7 @@ AssemblyPlan* assembly_plan_create(Ctx* ctx, const InflatedMesh& im, const QuadC
         P->ncand = (long long)cand.size();
         HostScope hs3(ctx, "plan_singular");
         // ---- singular lists (host adjacency, deterministic order) and Sauter workspaces
-        SingularLists S;
-        singular_pairs(m, S);
+        SingularLists S = sing_fut.get();
         P->SR = device_sauter(ctx, cfg);
         P->near_cap = std::max<long long>(1024, 64LL * nf);
         long long off = 0;

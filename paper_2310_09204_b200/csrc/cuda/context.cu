@@ -294,6 +294,15 @@ void matrix_download(const DMatrix& M, double* host)
     if (!ctx->dl_ws) ctx->dl_ws = std::make_shared<DownloadRing>();
     auto& R = *static_cast<DownloadRing*>(ctx->dl_ws.get());
     const size_t row_bytes = sizeof(double) * (size_t)M.n;
+    cudaPointerAttributes pa{};
+    if (cudaPointerGetAttributes(&pa, host) == cudaSuccess && pa.type == cudaMemoryTypeHost) {
+        // page-locked destination (sbg_host_alloc / cudaHostRegister): one pitched DMA straight into it
+        SBG_CUDA(cudaMemcpy2DAsync(host, row_bytes, M.a.p, sizeof(double) * (size_t)M.ld, row_bytes, M.n,
+                                   cudaMemcpyDeviceToHost, ctx->stream));
+        SBG_CUDA(cudaStreamSynchronize(ctx->stream));
+        return;
+    }
+    (void)cudaGetLastError();  // a pageable pointer is not an error
     if (row_bytes > DownloadRing::kSlotBytes) {  // n > 4M: row by row through pageable copies
         for (int r = 0; r < M.n; ++r)
             SBG_CUDA(cudaMemcpyAsync(host + (size_t)r * M.n, M.a.p + (size_t)r * M.ld, row_bytes,

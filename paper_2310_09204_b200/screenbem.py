@@ -125,6 +125,8 @@ SIGNATURES = {
                           C.POINTER(PcgReportC)]),
     "sbg_device_alloc": (C.c_int, [vp, C.c_longlong, C.POINTER(vp)]),
     "sbg_device_free": (C.c_int, [vp]),
+    "sbg_host_alloc": (C.c_int, [C.c_longlong, C.POINTER(vp)]),
+    "sbg_host_free": (C.c_int, [vp]),
     "sbg_memcpy_h2d": (C.c_int, [vp, vp, vp, C.c_longlong]),
     "sbg_memcpy_d2h": (C.c_int, [vp, vp, vp, C.c_longlong]),
     "sbg_pcg_device": (C.c_int, [vp, vp, vp, vp, C.c_double, C.c_int, vp, C.POINTER(PcgReportC)]),
@@ -239,6 +241,30 @@ def config_g(cfg: int):
 def launch_count() -> int:
     """Kernels launched by libscreenbem_b200 so far (all contexts)."""
     return lib().sbg_launch_count()
+
+
+class _PinnedBlock:
+    """Owner of one sbg_host_alloc block (freed when the last array view goes away)."""
+
+    def __init__(self, nbytes):
+        self.p = vp()
+        _check(lib().sbg_host_alloc(max(int(nbytes), 1), C.byref(self.p)))
+
+    def __del__(self):
+        if getattr(self, "p", None) and _lib is not None:
+            _lib.sbg_host_free(self.p)
+            self.p = None
+
+
+def pinned_empty(shape, dtype=np.float64):
+    """Uninitialised numpy array in page-locked host memory: GalerkinMatrix.download(out=)
+    into it is a single DMA, without the staging copy a pageable destination needs."""
+    dtype = np.dtype(dtype)
+    count = int(np.prod(shape)) if np.ndim(shape) else int(shape)
+    blk = _PinnedBlock(count * dtype.itemsize)
+    raw = (C.c_char * max(count * dtype.itemsize, 1)).from_address(blk.p.value)
+    raw._owner = blk  # keep the block alive as long as any view of it
+    return np.frombuffer(raw, dtype=dtype, count=count).reshape(shape)
 
 
 _default_ctx = None

@@ -117,3 +117,18 @@ def test_exact_far_switch_is_bitwise_on_far_pairs(ctx):
     Wf = S.assemble_W(im, ctx=ctx).download()
     check_W(We, O.assemble_W(oim, workers=WORKERS))
     assert np.abs(We - Wf).max() <= 1e-13 * np.abs(We).max()
+
+
+def test_download_into_pinned_buffer(ctx):
+    """download(out=) into page-locked memory (one pitched DMA, ld > n here) equals the
+    staged download into pageable memory bit for bit."""
+    im = S.inflate(S.make_config(1).fine)
+    W = S.assemble_W(im, ctx=ctx)
+    assert W.n == 225  # ld = 256: the pitched copy drops the padding columns
+    ref = W.download()
+    buf = S.pinned_empty((W.n, W.n))
+    out = W.download(out=buf)
+    assert out is buf and np.array_equal(buf, ref)
+    big = S.assemble_W(S.inflate(S.make_builtin("bowtie:3")), ctx=ctx)
+    b2 = S.pinned_empty((big.n, big.n))
+    assert np.array_equal(big.download(out=b2), big.download())
