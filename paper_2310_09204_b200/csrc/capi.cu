@@ -71,6 +71,18 @@ int guard(F&& fn)
     }
 }
 
+// entry points run on the device of the context they are given (whatever the calling
+// thread's current device is)
+void bind_device(int dev)
+{
+    int cur = -1;
+    if (cudaGetDevice(&cur) != cudaSuccess || cur != dev) SBG_CUDA(cudaSetDevice(dev));
+}
+void bind_device(const Ctx* c)
+{
+    if (c) bind_device(c->device);
+}
+
 void need(const void* p, const char* what)
 {
     if (!p) throw ValidationError(std::string("null argument: ") + what);
@@ -156,6 +168,7 @@ int sbg_timers_reset(sbg_ctx* ctx)
 int sbg_timer_get(sbg_ctx* ctx, const char* name, double* total_ms, long long* count)
 {
     return guard([&] {
+        bind_device(ctx ? &ctx->c : nullptr);
         ctx->c.timers.collect();
         *total_ms = 0;
         *count = 0;
@@ -170,6 +183,7 @@ int sbg_timer_get(sbg_ctx* ctx, const char* name, double* total_ms, long long* c
 int sbg_timer_begin(sbg_ctx* ctx, const char* name)
 {
     return guard([&] {
+        bind_device(ctx ? &ctx->c : nullptr);
         auto u = std::make_unique<UserScope>();
         u->name = name;
         u->ts = std::make_unique<TimedScope>(&ctx->c, u->name.c_str());
@@ -179,6 +193,7 @@ int sbg_timer_begin(sbg_ctx* ctx, const char* name)
 int sbg_timer_end(sbg_ctx* ctx)
 {
     return guard([&] {
+        bind_device(ctx ? &ctx->c : nullptr);
         (void)ctx;
         if (g_user_scopes.empty()) throw ValidationError("sbg_timer_end without sbg_timer_begin");
         g_user_scopes.back()->ts.reset();
@@ -379,6 +394,7 @@ int sbg_assemble_w(sbg_ctx* ctx, const sbg_inflated* im, const sbg_quad_cfg* cfg
     (void)workers;  // the reference's std::thread count; the GPU path ignores it
     return guard([&] {
         need(ctx, "ctx");
+        bind_device(&ctx->c);
         auto* W = new sbg_matrix;
         try {
             AssemblyStats st;
@@ -404,6 +420,7 @@ int sbg_assemble_w(sbg_ctx* ctx, const sbg_inflated* im, const sbg_quad_cfg* cfg
 int sbg_assembly_plan_create(sbg_ctx* ctx, const sbg_inflated* im, const sbg_quad_cfg* cfg, sbg_aplan** out)
 {
     return guard([&] {
+        bind_device(ctx ? &ctx->c : nullptr);
         auto* p = new sbg_aplan;
         p->ctx = &ctx->c;
         try {
@@ -422,6 +439,7 @@ int sbg_assembly_run(sbg_aplan* plan, sbg_matrix** W, sbg_assembly_stats* stats)
 int sbg_assembly_run_shard(sbg_aplan* plan, sbg_matrix** W, int rank, int world, sbg_assembly_stats* stats)
 {
     return guard([&] {
+        bind_device(plan ? plan->ctx : nullptr);
         need(plan, "plan");
         if (world < 1 || rank < 0 || rank >= world) throw ValidationError("shard: need 0 <= rank < world");
         need(W, "W");
@@ -455,6 +473,7 @@ void sbg_assembly_plan_destroy(sbg_aplan* plan) { delete plan; }
 int sbg_matrix_create(sbg_ctx* ctx, int n, const double* host, sbg_matrix** out)
 {
     return guard([&] {
+        bind_device(ctx ? &ctx->c : nullptr);
         need(ctx, "ctx");
         if (n < 0) throw ValidationError("negative matrix size");
         auto* W = new sbg_matrix;
@@ -473,6 +492,7 @@ int sbg_matrix_n(const sbg_matrix* W) { return W ? W->M.n : -1; }
 int sbg_matrix_device_view(const sbg_matrix* W, void** data, int* ld, long long* count)
 {
     return guard([&] {
+        bind_device(W ? W->M.ctx : nullptr);
         need(W, "W");
         if (data) *data = W->M.a.p;
         if (ld) *ld = W->M.ld;
@@ -481,19 +501,29 @@ int sbg_matrix_device_view(const sbg_matrix* W, void** data, int* ld, long long*
 }
 int sbg_matrix_download(const sbg_matrix* W, double* host)
 {
-    return guard([&] { matrix_download(W->M, host); });
+    return guard([&] {
+        bind_device(W ? W->M.ctx : nullptr);
+        matrix_download(W->M, host);
+    });
 }
 int sbg_matrix_download_rows(const sbg_matrix* W, const int32_t* rows, int nrows, double* host)
 {
-    return guard([&] { matrix_download_rows(W->M, rows, nrows, host); });
+    return guard([&] {
+        bind_device(W ? W->M.ctx : nullptr);
+        matrix_download_rows(W->M, rows, nrows, host);
+    });
 }
 int sbg_matrix_symmetry_defect(const sbg_matrix* W, double* m)
 {
-    return guard([&] { *m = matrix_symmetry_defect(W->M); });
+    return guard([&] {
+        bind_device(W ? W->M.ctx : nullptr);
+        *m = matrix_symmetry_defect(W->M);
+    });
 }
 int sbg_matvec(sbg_ctx* ctx, const sbg_matrix* W, const double* x, double* y)
 {
     return guard([&] {
+        bind_device(ctx ? &ctx->c : nullptr);
         const int n = W->M.n;
         cudaStream_t s = ctx->c.stream;
         DBuf<double> dx(W->M.ld), dy(W->M.ld);
@@ -512,6 +542,7 @@ void sbg_matrix_destroy(sbg_matrix* W) { delete W; }
 int sbg_matrix_dump_binary(const sbg_matrix* W, const char* path)
 {
     return guard([&] {
+        bind_device(W ? W->M.ctx : nullptr);
         std::ofstream os(path, std::ios::binary);
         if (!os) throw ValidationError(std::string("cannot open matrix dump file: ") + path);
         char header[16] = {};
@@ -535,6 +566,7 @@ int sbg_matrix_dump_binary(const sbg_matrix* W, const char* path)
 int sbg_matrix_load_binary(sbg_ctx* ctx, const char* path, sbg_matrix** out)
 {
     return guard([&] {
+        bind_device(ctx ? &ctx->c : nullptr);
         std::ifstream is(path, std::ios::binary);
         if (!is) throw ValidationError(std::string("cannot open matrix dump file: ") + path);
         char header[16] = {};
@@ -561,6 +593,7 @@ int sbg_pair_integrals(sbg_ctx* ctx, const sbg_mesh* m, const sbg_quad_cfg* cfg,
                        long long np, double* out)
 {
     return guard([&] {
+        bind_device(ctx ? &ctx->c : nullptr);
         pair_integrals(&ctx->c, m->m, qcfg(cfg), f, g, np, out);
         for (long long i = 0; i < np; ++i)
             if (!std::isfinite(out[i])) throw NumericalError("quadrature produced a non-finite pair integral");
@@ -577,7 +610,10 @@ int sbg_rhs_points(const sbg_inflated* im, const sbg_quad_cfg* cfg, double* pts)
 int sbg_assemble_rhs(sbg_ctx* ctx, const sbg_inflated* im, const sbg_quad_cfg* cfg, const double* g, int g_is_field,
                      double* L)
 {
-    return guard([&] { assemble_rhs(&ctx->c, im->im, qcfg(cfg), g, g_is_field != 0, L); });
+    return guard([&] {
+        bind_device(ctx ? &ctx->c : nullptr);
+        assemble_rhs(&ctx->c, im->im, qcfg(cfg), g, g_is_field != 0, L);
+    });
 }
 
 // ---------------------------------------------------------------- partition / prolongation
@@ -675,6 +711,7 @@ int sbg_build_preconditioner(sbg_ctx* ctx, const sbg_matrix* W, const sbg_partit
                              sbg_prec** out)
 {
     return guard([&] {
+        bind_device(ctx ? &ctx->c : nullptr);
         Prolongation none;
         none.rows = W->M.n;
         auto* p = new sbg_prec;
@@ -691,6 +728,7 @@ int sbg_build_preconditioner_mode(sbg_ctx* ctx, const sbg_matrix* W, const sbg_p
                                   int mode, sbg_prec** out)
 {
     return guard([&] {
+        bind_device(ctx ? &ctx->c : nullptr);
         if (mode != kPrecTrsv && mode != kPrecInverse) throw ValidationError("unknown preconditioner apply mode");
         Prolongation none;
         none.rows = W->M.n;
@@ -707,6 +745,7 @@ int sbg_build_preconditioner_mode(sbg_ctx* ctx, const sbg_matrix* W, const sbg_p
 int sbg_apply_preconditioner(sbg_ctx* ctx, sbg_prec* p, const double* r, int n, double* z)
 {
     return guard([&] {
+        bind_device(ctx ? &ctx->c : nullptr);
         if (n != prec_n(p->P)) throw ValidationError("preconditioner length mismatch");
         cudaStream_t s = ctx->c.stream;
         DBuf<double> dr(std::max(n, 1)), dz(std::max(n, 1));
@@ -720,6 +759,7 @@ int sbg_prec_num_subspaces(const sbg_prec* p) { return prec_num_subspaces(p->P);
 int sbg_prec_block_diag(sbg_ctx* ctx, sbg_prec* p, int which, double* diag, int* n_out)
 {
     return guard([&] {
+        bind_device(ctx ? &ctx->c : nullptr);
         std::vector<double> d;
         prec_block_diag(&ctx->c, p->P, which, d);
         *n_out = (int)d.size();
@@ -729,6 +769,7 @@ int sbg_prec_block_diag(sbg_ctx* ctx, sbg_prec* p, int which, double* diag, int*
 int sbg_coarse_matrix(sbg_ctx* ctx, const sbg_matrix* W, const sbg_prolong* R, double* H)
 {
     return guard([&] {
+        bind_device(ctx ? &ctx->c : nullptr);
         std::vector<double> h;
         coarse_galerkin(&ctx->c, W->M, R->R, h);
         std::copy(h.begin(), h.end(), H);
@@ -740,6 +781,7 @@ double sbg_prec_factor_bytes(const sbg_prec* p) { return prec_factor_bytes(p->P)
 int sbg_materialize_preconditioner(sbg_ctx* ctx, sbg_prec* p, sbg_matrix** out)
 {
     return guard([&] {
+        bind_device(ctx ? &ctx->c : nullptr);
         need(out, "out");
         need(p, "preconditioner");
         auto* m = new sbg_matrix;
@@ -755,6 +797,7 @@ int sbg_materialize_preconditioner(sbg_ctx* ctx, sbg_prec* p, sbg_matrix** out)
 int sbg_prec_from_dense(sbg_ctx* ctx, const sbg_matrix* M, sbg_prec** out)
 {
     return guard([&] {
+        bind_device(ctx ? &ctx->c : nullptr);
         need(out, "out");
         need(M, "matrix");
         auto* p = new sbg_prec;
@@ -770,6 +813,7 @@ int sbg_prec_from_dense(sbg_ctx* ctx, const sbg_matrix* M, sbg_prec** out)
 int sbg_condition_number(sbg_ctx* ctx, const sbg_matrix* W, sbg_prec* p, double tol, int maxit, sbg_spectrum* out)
 {
     return guard([&] {
+        bind_device(ctx ? &ctx->c : nullptr);
         need(out, "out");
         need(W, "matrix");
         const Spectrum sp = spectrum(&ctx->c, W->M, p ? p->P : nullptr, tol, maxit);
@@ -802,6 +846,7 @@ int sbg_pcg(sbg_ctx* ctx, const sbg_matrix* W, sbg_prec* prec, const double* rhs
             double* x, double* history, double* alphas, double* betas, int hist_cap, sbg_pcg_report* rep)
 {
     return guard([&] {
+        bind_device(ctx ? &ctx->c : nullptr);
         if (n != W->M.n) throw ValidationError("pcg: right-hand side length mismatch");
         PcgResult r;
         pcg_run(&ctx->c, W->M, prec ? prec->P : nullptr, rhs, x, false, tol, maxit, r);
@@ -813,6 +858,7 @@ int sbg_pcg(sbg_ctx* ctx, const sbg_matrix* W, sbg_prec* prec, const double* rhs
 int sbg_device_alloc(sbg_ctx* ctx, long long bytes, void** dptr)
 {
     return guard([&] {
+        bind_device(ctx ? &ctx->c : nullptr);
         SBG_CUDA(cudaSetDevice(ctx->c.device));
         *dptr = device_alloc((size_t)bytes);
         SBG_CUDA(cudaMemsetAsync(*dptr, 0, (size_t)bytes, ctx->c.stream));
@@ -840,6 +886,7 @@ int sbg_host_free(void* hptr)
 int sbg_memcpy_h2d(sbg_ctx* ctx, void* dst, const void* src, long long bytes)
 {
     return guard([&] {
+        bind_device(ctx ? &ctx->c : nullptr);
         SBG_CUDA(cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyHostToDevice, ctx->c.stream));
         SBG_CUDA(cudaStreamSynchronize(ctx->c.stream));
     });
@@ -847,6 +894,7 @@ int sbg_memcpy_h2d(sbg_ctx* ctx, void* dst, const void* src, long long bytes)
 int sbg_memcpy_d2h(sbg_ctx* ctx, void* dst, const void* src, long long bytes)
 {
     return guard([&] {
+        bind_device(ctx ? &ctx->c : nullptr);
         SBG_CUDA(cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyDeviceToHost, ctx->c.stream));
         SBG_CUDA(cudaStreamSynchronize(ctx->c.stream));
     });
@@ -855,6 +903,7 @@ int sbg_pcg_device(sbg_ctx* ctx, const sbg_matrix* W, sbg_prec* prec, const doub
                    double* d_x, sbg_pcg_report* rep)
 {
     return guard([&] {
+        bind_device(ctx ? &ctx->c : nullptr);
         PcgResult r;
         pcg_run(&ctx->c, W->M, prec ? prec->P : nullptr, d_rhs, d_x, true, tol, maxit, r);
         fill_report(r, nullptr, nullptr, nullptr, 0, rep);
@@ -863,6 +912,7 @@ int sbg_pcg_device(sbg_ctx* ctx, const sbg_matrix* W, sbg_prec* prec, const doub
 int sbg_matvec_device(sbg_ctx* ctx, const sbg_matrix* W, const double* d_x, double* d_y, int reps)
 {
     return guard([&] {
+        bind_device(ctx ? &ctx->c : nullptr);
         GemvPlan plan;
         gemv_plan(&ctx->c, W->M.n, W->M.ld, plan);
         for (int i = 0; i < reps; ++i) gemv(&ctx->c, W->M, plan, d_x, d_y);
@@ -872,13 +922,17 @@ int sbg_matvec_device(sbg_ctx* ctx, const sbg_matrix* W, const double* d_x, doub
 int sbg_apply_preconditioner_device(sbg_ctx* ctx, sbg_prec* p, const double* d_r, double* d_z, int reps)
 {
     return guard([&] {
+        bind_device(ctx ? &ctx->c : nullptr);
         for (int i = 0; i < reps; ++i) prec_apply(&ctx->c, p->P, d_r, d_z, nullptr);
         SBG_CUDA(cudaStreamSynchronize(ctx->c.stream));
     });
 }
 int sbg_fp64_peak(sbg_ctx* ctx, double* tflops)
 {
-    return guard([&] { *tflops = fp64_peak_tflops(&ctx->c); });
+    return guard([&] {
+        bind_device(ctx ? &ctx->c : nullptr);
+        *tflops = fp64_peak_tflops(&ctx->c);
+    });
 }
 // L2 flush between timed launches: write 256 MiB (> the 126 MB L2), then read another
 // 256 MiB, so the next timed kernel starts with a cold L2 holding only clean lines (a
@@ -888,6 +942,7 @@ int sbg_fp64_peak(sbg_ctx* ctx, double* tflops)
 int sbg_pool_stats(sbg_ctx* ctx, long long* reserved, long long* used)
 {
     return guard([&] {
+        bind_device(ctx ? &ctx->c : nullptr);
         cudaMemPool_t pool;
         SBG_CUDA(cudaDeviceGetDefaultMemPool(&pool, ctx->c.device));
         unsigned long long r = 0, u = 0;
@@ -899,7 +954,10 @@ int sbg_pool_stats(sbg_ctx* ctx, long long* reserved, long long* used)
 }
 int sbg_l2_flush(sbg_ctx* ctx)
 {
-    return guard([&] { l2_flush(&ctx->c); });
+    return guard([&] {
+        bind_device(ctx ? &ctx->c : nullptr);
+        l2_flush(&ctx->c);
+    });
 }
 
 }  // extern "C"
