@@ -45,7 +45,9 @@ typedef struct sbg_prolong sbg_prolong;     /* Prolongation     (inc/jump.hpp:87
 typedef struct sbg_prec sbg_prec;           /* SchwarzPreconditioner (inc/schwarz.hpp:55-73), device-resident */
 typedef struct sbg_aplan sbg_aplan;         /* assembly plan: mesh-derived device data of assemble_W */
 
-/* QuadratureConfig (inc/quadrature.hpp:12-16) */
+/* QuadratureConfig (inc/quadrature.hpp:12-16).  The far / near tensor rules live in the
+ * device's constant memory, written on each assembly's stream: assemblies with different
+ * far_order must not run concurrently on one device (different threads / streams). */
 typedef struct {
     int far_order;         /* 4 */
     int singular_order;    /* 8 */

@@ -702,11 +702,7 @@ void launch_near_leaves_g(Ctx* ctx, const NearNode* leaves, const unsigned long 
                           const int2* pairs, const double* GV, const double* GA, double* out)
 {
     const size_t smem = (size_t)(NEAR_G_THREADS / 32) * 8 * NNP * sizeof(double4);
-    static bool attr = false;
-    if (!attr) {
-        SBG_CUDA(cudaFuncSetAttribute(k_near_leaves_g<NNP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr = true;
-    }
+    set_max_dynamic_smem(k_near_leaves_g<NNP>, smem);
     const long long warps = (ncur + 7) / 8;
     const int grid = (int)std::min<long long>((warps + NEAR_G_THREADS / 32 - 1) / (NEAR_G_THREADS / 32),
                                               4LL * ctx->sm_count);
@@ -1149,11 +1145,7 @@ long long run_near(Ctx* ctx, const RuleDims& R, const double* GV, const double* 
     cudaStream_t s = ctx->stream;
     TimedScope ts(ctx, "near");
     if (!NW.cnt.n) NW.cnt.alloc(3);
-    static bool attr = false;
-    if (!attr) {
-        SBG_CUDA(cudaFuncSetAttribute(k_near_leaves, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)NEAR_LEAF_SMEM));
-        attr = true;
-    }
+    set_max_dynamic_smem(k_near_leaves, NEAR_LEAF_SMEM);
     if ((long long)NW.cur.n < cap) NW.cur.alloc(cap);
     k_near_init<<<(int)((cap + 255) / 256), 256, 0, s>>>(np_dev, cap, NW.cur.p, out, NW.cnt.p);
     count_launch();
@@ -1219,11 +1211,7 @@ void launch_far_tiles_n(Ctx* ctx, const TileInfo* tiles, long long ntiles, int t
                         const BlockPtrs& BP, double thr, DMatrix& W, int nr)
 {
     constexpr size_t smem = far_smem_bytes(EXACT ? 0 : NFP);
-    static bool attr = false;
-    if (!attr) {
-        SBG_CUDA(cudaFuncSetAttribute(k_far_tiles<NFP, EXACT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr = true;
-    }
+    set_max_dynamic_smem(k_far_tiles<NFP, EXACT>, smem);
     k_far_tiles<NFP, EXACT><<<(int)ntiles, FAR_THREADS, smem, ctx->stream>>>(tiles, tstride, G, BP, thr, W.a.p,
                                                                             W.ld, 1.0 / M_PI, nr);
 }

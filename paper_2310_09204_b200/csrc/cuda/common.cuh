@@ -152,6 +152,14 @@ void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cu
     SBG_CUDA(cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...));
 }
 
+// Opt a kernel into more than 48 KB of dynamic shared memory, once per (kernel, device).
+void set_max_dynamic_smem(const void* kernel, size_t bytes);
+template <typename... KArgs>
+void set_max_dynamic_smem(void (*kernel)(KArgs...), size_t bytes)
+{
+    set_max_dynamic_smem(reinterpret_cast<const void*>(kernel), bytes);
+}
+
 // Dense symmetric fp64 matrix resident in HBM (GalerkinMatrix, assemble.hpp:12).
 // Row-major with a leading dimension padded to 32 doubles (256-byte rows) so
 // every row starts 16-byte aligned for 128-bit streaming loads; the padding

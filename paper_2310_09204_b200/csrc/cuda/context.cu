@@ -6,6 +6,8 @@
 #include <sys/mman.h>
 #include <condition_variable>
 #include <mutex>
+#include <set>
+#include <tuple>
 #include <thread>
 #include <vector>
 
@@ -188,6 +190,18 @@ __global__ void k_symmetry_defect(const double* __restrict__ a, int ld, int n, d
 }
 
 }  // namespace
+
+void set_max_dynamic_smem(const void* kernel, size_t bytes)
+{
+    static std::mutex mu;
+    static std::set<std::tuple<const void*, int, size_t>> done;
+    int dev = 0;
+    SBG_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(mu);
+    if (done.count({kernel, dev, bytes})) return;
+    SBG_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    done.insert({kernel, dev, bytes});
+}
 
 void matrix_alloc(Ctx* ctx, int n, DMatrix& M)
 {

@@ -744,11 +744,7 @@ void launch_gemm(Ctx* ctx, Prec* P, int k, const GTask* dev_tasks, int count, do
 {
     if (count <= 0) return;
     const size_t smem = GEMM_SMEM;
-    static bool configured = false;
-    if (!configured) {
-        SBG_CUDA(cudaFuncSetAttribute(k_tile_gemm<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        configured = true;
-    }
+    set_max_dynamic_smem(k_tile_gemm<KIND>, smem);
     k_tile_gemm<KIND><<<count, 128, smem, ctx->stream>>>(k, dev_tasks, P->d_T.p, P->d_Poff.p, P->d_Doff.p, Lp, Xp,
                                                         P->D.p);
     count_launch();
@@ -1029,7 +1025,7 @@ Prec* prec_build(Ctx* ctx, const DMatrix& W, const DofPartition& part, const Pro
         {
             TimedScope ts(ctx, "cholesky");
             const size_t smem_potrf = 2 * TB * (TB + 1) * sizeof(double);
-            SBG_CUDA(cudaFuncSetAttribute(k_potrf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_potrf));
+            set_max_dynamic_smem(k_potrf, smem_potrf);
             // panel-blocked right-looking (task lists in the schedule): inside a panel of
             // kPanel tile columns only the panel's own columns are updated per step; the
             // trailing matrix takes one update with K = the whole panel when it is complete
