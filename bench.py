@@ -323,6 +323,17 @@ def matvec_traffic(cfg: int):
         return None
 
 
+def kernel_traffic(kernel: str, cfg: int):
+    """DRAM bytes per step of an assembly kernel (summed over its launches in one step) from
+    the committed ncu --set full capture for this config (or None)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_traffic.json")) as f:
+            e = json.load(f)[kernel].get(str(cfg))
+        return None if e is None else int(sum(e["dram_bytes_per_step"]))
+    except Exception:
+        return None
+
+
 def load_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -535,7 +546,11 @@ def run_ours(args):
                        "pcg_tol": 1e-8, "far_field": "exact (IEEE, oracle order)" if args.exact_far else
                        "fast (distance expansion + refined rsqrt)"},
             "roofline": {"bound": "fp64", "kernel": dom[0], "achieved": achieved, "peak": fp64_peak,
-                         "unit": "TFLOP/s", "frac": achieved / fp64_peak if fp64_peak else None, "traffic": None,
+                         "unit": "TFLOP/s", "frac": achieved / fp64_peak if fp64_peak else None,
+                         "traffic": kernel_traffic(dom[0], cfg),
+                         "traffic_note": "DRAM bytes per step (all launches of the kernel in one step) from "
+                                         "profiles/r01_traffic.json; the kernel is FP64-bound, so the bytes only "
+                                         "show it re-reads nothing (leaf list, geometry and W updates)",
                          "peak_source": "DFMA loop measured by bench.py on this GPU (MEASURED_PEAKS.json has no fp64)",
                          "flop_convention": "20 flop per tensor-rule kernel evaluation (SURVEY.md §8d)",
                          "ms_per_step": dom[2], "launches_per_step": launches_per_step[dom[0]],

@@ -38,6 +38,8 @@ def launches(path, out):
     print(open(out).read())
 
 
+UNITB = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6, "GB": 1e9}
+
 WANT = [
     ("gpu__time_duration.sum", "duration"),
     ("sm__throughput.avg.pct_of_peak_sustained_elapsed", "SM throughput %"),
@@ -71,8 +73,26 @@ def report(path, out):
             dur = 0.0
         if name not in best or dur > best[name][0]:
             best[name] = (dur, d)
+    allrows = []
+    for v in rows[2:]:
+        d = {h[i]: v[i] for i in range(min(len(h), len(v)))}
+        allrows.append(d)
     with open(out, "w") as f:
         f.write(f"# ncu --set full summary: `{path}`\n\n")
+        f.write("Every captured launch (in launch order):\n\n| # | kernel | duration | FP64 pipe % | DRAM read + write |\n"
+                "|---:|---|---:|---:|---:|\n")
+        for i, d in enumerate(allrows):
+            def num(k):
+                try:
+                    return float(d.get(k, "nan").replace(",", ""))
+                except ValueError:
+                    return float("nan")
+            rw = num("dram__bytes_read.sum") * UNITB.get(units.get("dram__bytes_read.sum"), 1) + \
+                num("dram__bytes_write.sum") * UNITB.get(units.get("dram__bytes_write.sum"), 1)
+            f.write(f"| {i} | `{d.get('Kernel Name', '?').split('(')[0].split('::')[-1]}` | "
+                    f"{d.get('gpu__time_duration.sum', '?')} {units.get('gpu__time_duration.sum', '')} | "
+                    f"{num('sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active'):.1f} | {rw / 1e6:.2f} MB |\n")
+        f.write("\n")
         f.write("One launch per kernel (the longest captured); `--clock-control none`, cold caches and "
                 "serialised launches, so durations are not the live ones.\n\n")
         for _, d in sorted(best.values(), key=lambda x: -x[0]):
