@@ -1154,8 +1154,17 @@ long long run_near(Ctx* ctx, const RuleDims& R, const double* GV, const double* 
     SBG_CUDA(cudaMemcpyAsync(h, NW.cnt.p, sizeof(h[0]), cudaMemcpyDeviceToHost, s));
     SBG_CUDA(cudaStreamSynchronize(s));
     long long ncur = (long long)h[0], total_leaves = 0;
+    // classify level by level (each level's leaves appended to one list), then evaluate
+    // every leaf in one launch: no per-level grid tails, and the host's per-level count
+    // reads never wait on leaf work
     for (int depth = 0; depth <= 5 && ncur > 0; ++depth) {
-        if ((long long)NW.leaves.n < ncur) NW.leaves.alloc(ncur * 5 / 4);
+        if ((long long)NW.leaves.n < total_leaves + ncur) {  // grow, keeping the leaves so far
+            DBuf<NearNode> grown((total_leaves + ncur) * 5 / 4);
+            if (total_leaves)
+                SBG_CUDA(cudaMemcpyAsync(grown.p, NW.leaves.p, total_leaves * sizeof(NearNode),
+                                         cudaMemcpyDeviceToDevice, s));
+            NW.leaves = std::move(grown);
+        }
         // classify into the existing next-frontier capacity; on overflow grow it to the
         // exact count (+25%) and classify again (idempotent), so the frontier buffers size
         // to the real level populations instead of the 4x upper bound, and a plan that is
@@ -1166,8 +1175,9 @@ long long run_near(Ctx* ctx, const RuleDims& R, const double* GV, const double* 
             {
                 TimedScope tc(ctx, "near_classify");
                 const int grid = (int)std::min<long long>((ncur + 127) / 128, 16LL * ctx->sm_count);
-                k_near_level<<<grid, 128, 0, s>>>(NW.cur.p, NW.cnt.p, ncur, depth, pairs, GV, thr, NW.leaves.p,
-                                                  NW.cnt.p + 2, ncur, NW.next.p, NW.cnt.p + 1, cap_next);
+                k_near_level<<<grid, 128, 0, s>>>(NW.cur.p, NW.cnt.p, ncur, depth, pairs, GV, thr,
+                                                  NW.leaves.p + total_leaves, NW.cnt.p + 2, ncur, NW.next.p,
+                                                  NW.cnt.p + 1, cap_next);
                 count_launch();
                 SBG_LAUNCH_CHECK();
             }
@@ -1177,29 +1187,31 @@ long long run_near(Ctx* ctx, const RuleDims& R, const double* GV, const double* 
             if (attempt > 0) throw std::logic_error("near frontier: inconsistent level count");
             NW.next.alloc((long long)h[1] * 5 / 4);
         }
-        {
-            TimedScope tl(ctx, "near_leaves");
-            const long long warps = (ncur + 7) / 8;  // upper bound on this level's leaf octets
-            const int lgrid = (int)std::min<long long>((warps + NEAR_LEAF_WARPS - 1) / NEAR_LEAF_WARPS, 2LL * ctx->sm_count);
-            if (R.nnp == NN) {
-                k_near_leaves<<<lgrid, NEAR_LEAF_THREADS, NEAR_LEAF_SMEM, s>>>(NW.leaves.p, NW.cnt.p + 2, ncur, pairs,
-                                                                               GV, GA, 1.0 / M_PI, out);
-            } else {
-                switch (R.nnp) {
-#define SBG_NEAR_G(N) \
-    case N: launch_near_leaves_g<N>(ctx, NW.leaves.p, NW.cnt.p + 2, ncur, pairs, GV, GA, out); break;
-                    SBG_NEAR_G(16) SBG_NEAR_G(32) SBG_NEAR_G(48) SBG_NEAR_G(64) SBG_NEAR_G(96) SBG_NEAR_G(112)
-#undef SBG_NEAR_G
-                default: throw std::logic_error("near rule size not instantiated");
-                }
-            }
-            count_launch();
-        }
-        SBG_LAUNCH_CHECK();
         total_leaves += (long long)h[2];
         ncur = (long long)h[1];
         std::swap(NW.cur, NW.next);
         if (ncur > 0) SBG_CUDA(cudaMemcpyAsync(NW.cnt.p, &h[1], sizeof(h[1]), cudaMemcpyHostToDevice, s));
+    }
+    if (total_leaves > 0) {
+        const unsigned long long tl = (unsigned long long)total_leaves;
+        SBG_CUDA(cudaMemcpyAsync(NW.cnt.p + 2, &tl, sizeof(tl), cudaMemcpyHostToDevice, s));
+        TimedScope tl_scope(ctx, "near_leaves");
+        const long long warps = (total_leaves + 7) / 8;
+        const int lgrid = (int)std::min<long long>((warps + NEAR_LEAF_WARPS - 1) / NEAR_LEAF_WARPS, 2LL * ctx->sm_count);
+        if (R.nnp == NN) {
+            k_near_leaves<<<lgrid, NEAR_LEAF_THREADS, NEAR_LEAF_SMEM, s>>>(NW.leaves.p, NW.cnt.p + 2, total_leaves,
+                                                                           pairs, GV, GA, 1.0 / M_PI, out);
+        } else {
+            switch (R.nnp) {
+#define SBG_NEAR_G(N) \
+    case N: launch_near_leaves_g<N>(ctx, NW.leaves.p, NW.cnt.p + 2, total_leaves, pairs, GV, GA, out); break;
+                SBG_NEAR_G(16) SBG_NEAR_G(32) SBG_NEAR_G(48) SBG_NEAR_G(64) SBG_NEAR_G(96) SBG_NEAR_G(112)
+#undef SBG_NEAR_G
+            default: throw std::logic_error("near rule size not instantiated");
+            }
+        }
+        count_launch();
+        SBG_LAUNCH_CHECK();
     }
     return total_leaves;
 }
