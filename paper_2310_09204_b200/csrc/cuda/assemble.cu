@@ -394,14 +394,15 @@ __global__ void k_classify_near(const TileInfo* __restrict__ tiles, int tstride,
 __device__ __forceinline__ double tri_diam(const double* t)
 {
     const D3 a = {t[0], t[1], t[2]}, b = {t[3], t[4], t[5]}, c = {t[6], t[7], t[8]};
-    return fmax(fmax(d3_norm(d3_sub(a, b)), d3_norm(d3_sub(b, c))), d3_norm(d3_sub(a, c)));
+    // sqrt is monotone and correctly rounded: sqrt(max) == max(sqrt), one sqrt instead of three
+    return __dsqrt_rn(fmax(fmax(d3_sqnorm(d3_sub(a, b)), d3_sqnorm(d3_sub(b, c))), d3_sqnorm(d3_sub(a, c))));
 }
 __device__ __forceinline__ void tri_centroid_rad(const double* t, D3& c, double& r)
 {
     const D3 a = {t[0], t[1], t[2]}, b = {t[3], t[4], t[5]}, d = {t[6], t[7], t[8]};
     const D3 s = d3_add(d3_add(a, b), d);
     c = {__ddiv_rn(s.x, 3.0), __ddiv_rn(s.y, 3.0), __ddiv_rn(s.z, 3.0)};
-    r = fmax(fmax(fmax(0.0, d3_norm(d3_sub(a, c))), d3_norm(d3_sub(b, c))), d3_norm(d3_sub(d, c)));
+    r = __dsqrt_rn(fmax(fmax(d3_sqnorm(d3_sub(a, c)), d3_sqnorm(d3_sub(b, c))), d3_sqnorm(d3_sub(d, c))));
 }
 __device__ __forceinline__ double tri_area(const double* t)
 {

@@ -132,3 +132,27 @@ def test_download_into_pinned_buffer(ctx):
     big = S.assemble_W(S.inflate(S.make_builtin("bowtie:3")), ctx=ctx)
     b2 = S.pinned_empty((big.n, big.n))
     assert np.array_equal(big.download(out=b2), big.download())
+
+
+@pytest.mark.parametrize("spec", ["config1", "bowtie:3"])
+def test_recursion_counts_equal_the_oracle(ctx, spec):
+    """The device near-field classification makes every leaf/split decision of the
+    reference recursion (quadrature.hpp:231-249): its near-leaf count equals the oracle's
+    exactly, and the depth-0 far pairs plus near and singular pairs cover all pairs."""
+    m = S.make_config(1).fine if spec == "config1" else S.make_builtin(spec)
+    im = S.inflate(m)
+    W = S.assemble_W(im, ctx=ctx)
+    _, st = O.assemble_W(O.inflate(O.Mesh(m.vertices, m.facets)), workers=WORKERS, stats=True)
+    far_leaves, near_leaves, _ = (int(v) for v in st)
+    s = W.stats
+    assert s["near_leaves"] == near_leaves
+    assert s["far_pairs"] == far_leaves
+    assert s["far_pairs"] + s["near_pairs"] + s["identical"] + s["edge"] + s["vertex"] == m.nf * (m.nf + 1) // 2
+
+
+def test_config2_work_counts_match_the_survey_probe(ctx):
+    """SURVEY §8a probe counts for config 2 (a8, a9): 400 082 near-subdivided pairs,
+    1.87e7 near leaves, 8 192 / 12 160 / 35 973 identical / edge / vertex pairs."""
+    s = S.assemble_W(S.inflate(S.make_config(2).fine), ctx=ctx).stats
+    assert (s["identical"], s["edge"], s["vertex"], s["near_pairs"]) == (8192, 12160, 35973, 400082)
+    assert round(s["near_leaves"] / 1e5) == 187
