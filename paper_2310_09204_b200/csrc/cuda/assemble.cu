@@ -711,7 +711,33 @@ void launch_near_leaves_g(Ctx* ctx, const NearNode* leaves, const unsigned long 
 }
 
 // ---------------------------------------------------------------- Sauter (singular) pairs
-// pairs: 6 ints per pair = permuted vertex ids of t then s (quadrature.hpp:297-322)
+// pairs: 6 ints per pair = permuted vertex ids of t then s (quadrature.hpp:297-322).
+// The permutation puts the shared vertices first, so t0 = s0 in every class (d0 = 0),
+// and per class the rule table is stored in the form the difference needs
+// (upload_sauter): identical (s = t): x - y = (a1-b1) e1 + (a2-b2) e2, 2 FMA per
+// coordinate; edge (t1 = s1 as well): x - y = (a1-b1) e1 + a2 e2t - b2 e2s, 3; vertex:
+// x - y = a1 e1t + a2 e2t - b1 e1s - b2 e2s, 4.
+template <int CLS>
+__device__ __forceinline__ double sauter_r2(const double* a, const double (&e)[12])
+{
+    double dx, dy, dz;
+    if (CLS == 3) {
+        dx = fma(a[1], e[3], a[0] * e[0]);
+        dy = fma(a[1], e[4], a[0] * e[1]);
+        dz = fma(a[1], e[5], a[0] * e[2]);
+    } else if (CLS == 2) {
+        dx = fma(-a[2], e[9], fma(a[1], e[3], a[0] * e[0]));
+        dy = fma(-a[2], e[10], fma(a[1], e[4], a[0] * e[1]));
+        dz = fma(-a[2], e[11], fma(a[1], e[5], a[0] * e[2]));
+    } else {
+        dx = fma(-a[3], e[9], fma(-a[2], e[6], fma(a[1], e[3], a[0] * e[0])));
+        dy = fma(-a[3], e[10], fma(-a[2], e[7], fma(a[1], e[4], a[0] * e[1])));
+        dz = fma(-a[3], e[11], fma(-a[2], e[8], fma(a[1], e[5], a[0] * e[2])));
+    }
+    return fma(dx, dx, fma(dy, dy, dz * dz));
+}
+
+template <int CLS>
 __global__ void __launch_bounds__(SAUTER_THREADS)
     k_sauter_partial(const int* __restrict__ pv, int npairs, const double* __restrict__ X,
                      const double* __restrict__ rule, int npts, int chunk, double* __restrict__ part)
@@ -719,8 +745,7 @@ __global__ void __launch_bounds__(SAUTER_THREADS)
     __shared__ double R[SAUTER_STAGE * 5];
     const int p = blockIdx.x * blockDim.x + threadIdx.x;
     const bool active = p < npairs;
-    double d0x = 0, d0y = 0, d0z = 0, e1x = 0, e1y = 0, e1z = 0, e2x = 0, e2y = 0, e2z = 0;
-    double g1x = 0, g1y = 0, g1z = 0, g2x = 0, g2y = 0, g2z = 0;
+    double e[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};  // e1t, e2t, e1s, e2s
     if (active) {
         const int* q = pv + 6 * p;
         const double* t0 = X + 3 * q[0];
@@ -729,57 +754,80 @@ __global__ void __launch_bounds__(SAUTER_THREADS)
         const double* s0 = X + 3 * q[3];
         const double* s1 = X + 3 * q[4];
         const double* s2 = X + 3 * q[5];
-        d0x = t0[0] - s0[0];
-        d0y = t0[1] - s0[1];
-        d0z = t0[2] - s0[2];
-        e1x = t1[0] - t0[0];
-        e1y = t1[1] - t0[1];
-        e1z = t1[2] - t0[2];
-        e2x = t2[0] - t0[0];
-        e2y = t2[1] - t0[1];
-        e2z = t2[2] - t0[2];
-        g1x = s1[0] - s0[0];
-        g1y = s1[1] - s0[1];
-        g1z = s1[2] - s0[2];
-        g2x = s2[0] - s0[0];
-        g2y = s2[1] - s0[1];
-        g2z = s2[2] - s0[2];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            e[c] = t1[c] - t0[c];
+            e[3 + c] = t2[c] - t0[c];
+            e[6 + c] = s1[c] - s0[c];
+            e[9 + c] = s2[c] - s0[c];
+        }
     }
     const int q0 = blockIdx.y * chunk, q1 = min(npts, q0 + chunk);
     double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
     for (int base = q0; base < q1; base += SAUTER_STAGE) {
         const int cnt = min(SAUTER_STAGE, q1 - base);
         __syncthreads();
-        for (int e = threadIdx.x; e < cnt * 5; e += blockDim.x) R[e] = rule[(size_t)base * 5 + e];
+        for (int k = threadIdx.x; k < cnt * 5; k += blockDim.x) R[k] = rule[(size_t)base * 5 + k];
         __syncthreads();
         if (active) {
             int i = 0;
-            // four independent evaluations per step: x - y = (t0 - s0) + a1 e1t + a2 e2t - b1 e1s - b2 e2s
+            // four independent evaluations per step
             for (; i + 4 <= cnt; i += 4) {
                 double r2[4];
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const double* a = R + 5 * (i + u);
-                    const double ax = fma(-a[3], g2x, fma(-a[2], g1x, fma(a[1], e2x, fma(a[0], e1x, d0x))));
-                    const double ay = fma(-a[3], g2y, fma(-a[2], g1y, fma(a[1], e2y, fma(a[0], e1y, d0y))));
-                    const double az = fma(-a[3], g2z, fma(-a[2], g1z, fma(a[1], e2z, fma(a[0], e1z, d0z))));
-                    r2[u] = fma(ax, ax, fma(ay, ay, az * az));
-                }
+                for (int u = 0; u < 4; ++u) r2[u] = sauter_r2<CLS>(R + 5 * (i + u), e);
                 acc0 = fma(R[5 * i + 4], rsqrt_fast(r2[0]), acc0);
                 acc1 = fma(R[5 * i + 9], rsqrt_fast(r2[1]), acc1);
                 acc2 = fma(R[5 * i + 14], rsqrt_fast(r2[2]), acc2);
                 acc3 = fma(R[5 * i + 19], rsqrt_fast(r2[3]), acc3);
             }
-            for (; i < cnt; ++i) {
-                const double* a = R + 5 * i;
-                const double ax = fma(-a[3], g2x, fma(-a[2], g1x, fma(a[1], e2x, fma(a[0], e1x, d0x))));
-                const double ay = fma(-a[3], g2y, fma(-a[2], g1y, fma(a[1], e2y, fma(a[0], e1y, d0y))));
-                const double az = fma(-a[3], g2z, fma(-a[2], g1z, fma(a[1], e2z, fma(a[0], e1z, d0z))));
-                acc0 = fma(a[4], rsqrt_fast(fma(ax, ax, fma(ay, ay, az * az))), acc0);
-            }
+            for (; i < cnt; ++i) acc0 = fma(R[5 * i + 4], rsqrt_fast(sauter_r2<CLS>(R + 5 * i, e)), acc0);
         }
     }
     if (active) part[(size_t)blockIdx.y * npairs + p] = (acc0 + acc1) + (acc2 + acc3);
+}
+
+// launch of one class: chunk count chosen (sauter_chunking) so the grid fills whole waves
+void launch_sauter_partial(Ctx* ctx, int cls, const int* pv, int np, const double* X, const double* rule, int npts,
+                           int chunk, int nchunks, double* part)
+{
+    const dim3 grid((np + SAUTER_THREADS - 1) / SAUTER_THREADS, nchunks);
+    cudaStream_t s = ctx->stream;
+    switch (cls) {
+    case 1: k_sauter_partial<1><<<grid, SAUTER_THREADS, 0, s>>>(pv, np, X, rule, npts, chunk, part); break;
+    case 2: k_sauter_partial<2><<<grid, SAUTER_THREADS, 0, s>>>(pv, np, X, rule, npts, chunk, part); break;
+    case 3: k_sauter_partial<3><<<grid, SAUTER_THREADS, 0, s>>>(pv, np, X, rule, npts, chunk, part); break;
+    default: throw std::logic_error("Sauter class out of range");
+    }
+    count_launch();
+}
+
+// (chunk, nchunks) for np pairs of a class: chunks of >= ~600 rule points, and among
+// those the count whose grid (pair blocks x chunks) best fills whole waves of resident CTAs
+void sauter_chunking(Ctx* ctx, int cls, int np, int npts, int& chunk, int& nchunks)
+{
+    int per_sm = 1;
+    const void* fn = cls == 1 ? (const void*)k_sauter_partial<1>
+                              : (cls == 2 ? (const void*)k_sauter_partial<2> : (const void*)k_sauter_partial<3>);
+    SBG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, SAUTER_THREADS, 0));
+    const long long slots = (long long)std::max(per_sm, 1) * ctx->sm_count;
+    const long long pblocks = (np + SAUTER_THREADS - 1) / SAUTER_THREADS;
+    const int cmax = std::max(1, npts / 600);
+    double best = -1.0;
+    int best_c = 1;
+    for (int c = 1; c <= cmax; ++c) {
+        const int ch = (npts + c - 1) / c, cc = (npts + ch - 1) / ch;
+        const double waves = (double)(pblocks * cc) / (double)slots;
+        const double eff = waves / std::ceil(waves);  // busy fraction of the launched waves
+        // prefer fuller waves; among equally full, more waves (smaller tail per wave)
+        const double score = eff + 1e-3 * std::min(waves, 8.0);
+        if (score > best + 1e-12) {
+            best = score;
+            best_c = cc;
+        }
+    }
+    chunk = (npts + best_c - 1) / best_c;
+    nchunks = (npts + chunk - 1) / chunk;
 }
 
 // I = (sum of chunk partials) * 4 A_t A_s / (4 pi)   (quadrature.hpp:254-261)
@@ -1064,9 +1112,21 @@ void upload_sauter(Ctx* ctx, const QuadCfg& cfg, SauterRulesDev& R)
         rules = slot;
     }
     const SauterRule &id = rules->id, &ed = rules->ed, &vx = rules->vx;
-    R.r[3].upload(id.pts, ctx->stream);
+    // identical: (a1 - b1, a2 - b2, -, -, w); edge: (a1 - b1, a2, b2, -, w) (k_sauter_partial)
+    std::vector<double> idp(id.pts), edp(ed.pts);
+    for (size_t i = 0; i < idp.size(); i += 5) {
+        idp[i] = id.pts[i] - id.pts[i + 2];
+        idp[i + 1] = id.pts[i + 1] - id.pts[i + 3];
+        idp[i + 2] = idp[i + 3] = 0.0;
+    }
+    for (size_t i = 0; i < edp.size(); i += 5) {
+        edp[i] = ed.pts[i] - ed.pts[i + 2];
+        edp[i + 2] = ed.pts[i + 3];
+        edp[i + 3] = 0.0;
+    }
+    R.r[3].upload(idp, ctx->stream);
     R.npts[3] = id.size();
-    R.r[2].upload(ed.pts, ctx->stream);
+    R.r[2].upload(edp, ctx->stream);
     R.npts[2] = ed.size();
     R.r[1].upload(vx.pts, ctx->stream);
     R.npts[1] = vx.size();
@@ -1097,16 +1157,12 @@ void run_sauter(Ctx* ctx, const DBuf<double>& X, const std::vector<int>& pv, con
     DBuf<int> d_pv;
     d_pv.upload(pv, s);
     const int npts = R.npts[cls];
-    const int pblocks = (np + SAUTER_THREADS - 1) / SAUTER_THREADS;
-    // enough CTAs for ~4 waves; chunks of rule points in multiples of the stage size
-    int nchunks = std::max(1, std::min((4 * ctx->sm_count + pblocks - 1) / pblocks, (npts + 999) / 1000));
-    const int chunk = (npts + nchunks - 1) / nchunks;
-    nchunks = (npts + chunk - 1) / chunk;
+    int chunk = 0, nchunks = 0;
+    sauter_chunking(ctx, cls, np, npts, chunk, nchunks);
     DBuf<double> part((size_t)nchunks * np);
     {
         TimedScope ts(ctx, "sauter");
-        k_sauter_partial<<<dim3(pblocks, nchunks), SAUTER_THREADS, 0, s>>>(d_pv.p, np, X.p, R.r[cls].p, npts, chunk,
-                                                                          part.p); ::sbg::count_launch();
+        launch_sauter_partial(ctx, cls, d_pv.p, np, X.p, R.r[cls].p, npts, chunk, nchunks, part.p);
         k_sauter_finish<<<(np + 127) / 128, 128, 0, s>>>(part.p, np, nchunks, d_pv.p, X.p, out_dev); ::sbg::count_launch();
         SBG_LAUNCH_CHECK();
     }
@@ -1420,12 +1476,7 @@ AssemblyPlan* assembly_plan_create(Ctx* ctx, const InflatedMesh& im, const QuadC
             SBG_CUDA(cudaMemcpyAsync(P->loc_pairs.p + P->cls_off[cls], S.pairs[cls].data(), np * sizeof(int2),
                                      cudaMemcpyHostToDevice, s));
             P->pv[cls].upload(S.pv[cls], s);
-            const int npts = P->SR->npts[cls];
-            const int pblocks = (int)((np + SAUTER_THREADS - 1) / SAUTER_THREADS);
-            int nchunks = std::max(1, std::min((4 * ctx->sm_count + pblocks - 1) / pblocks, (npts + 999) / 1000));
-            const int chunk = (npts + nchunks - 1) / nchunks;
-            P->schunk[cls] = chunk;
-            P->schunks[cls] = (npts + chunk - 1) / chunk;
+            sauter_chunking(ctx, cls, (int)np, P->SR->npts[cls], P->schunk[cls], P->schunks[cls]);
             P->spart[cls].alloc((size_t)P->schunks[cls] * np);
         }
         P->near_cnt.alloc(1);
@@ -1502,10 +1553,8 @@ void assembly_run(AssemblyPlan* P, DMatrix& W, AssemblyStats* stats, int rank, i
         if (!np) continue;
         TimedScope ts(ctx, "sauter");
         const int* pv = P->pv[cls].p + 6 * sing_lo[cls];
-        const int pblocks = (int)((np + SAUTER_THREADS - 1) / SAUTER_THREADS);
-        k_sauter_partial<<<dim3(pblocks, P->schunks[cls]), SAUTER_THREADS, 0, s>>>(
-            pv, (int)np, P->G.X.p, P->SR->r[cls].p, P->SR->npts[cls], P->schunk[cls], P->spart[cls].p);
-        count_launch();
+        launch_sauter_partial(ctx, cls, pv, (int)np, P->G.X.p, P->SR->r[cls].p, P->SR->npts[cls], P->schunk[cls],
+                              P->schunks[cls], P->spart[cls].p);
         k_sauter_finish<<<(int)((np + 127) / 128), 128, 0, s>>>(P->spart[cls].p, (int)np, P->schunks[cls], pv,
                                                                  P->G.X.p,
                                                                  P->loc_I.p + P->cls_off[cls] + sing_lo[cls]);
