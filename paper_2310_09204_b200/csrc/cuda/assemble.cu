@@ -1447,6 +1447,13 @@ AssemblyPlan* assembly_plan_create(Ctx* ctx, const InflatedMesh& im, const QuadC
                 tiles.push_back({fb, gb, certain ? 1 : 0, 0});
                 if (!certain) cand.push_back({fb, gb, 0, 0});
             }
+        // launch order: full-cost tiles first (certain-far, off-diagonal), then the tiles with
+        // per-pair tests and near pairs skipped, diagonal (half) tiles last, so the grid's
+        // last wave holds the cheapest tiles (stable: fb-major within each class)
+        std::stable_sort(tiles.begin(), tiles.end(), [](const TileInfo& x, const TileInfo& y) {
+            auto rank = [](const TileInfo& t) { return t.fb == t.gb ? 2 : (t.certain_far ? 0 : 1); };
+            return rank(x) < rank(y);
+        });
         P->bfac.upload(bfac, s);
         P->dof_ptr.upload(dof_ptr, s);
         P->dofs.upload(dofs, s);
