@@ -291,8 +291,12 @@ def run_reference(args):
         return
     cfg = args.config
     samples = []
+    # timed steps: the same sample as our arm's cpu_baseline (the whole W when it takes about
+    # cpu_seconds or less: config 2 is assembled in full, since the last rows alone are
+    # dominated by far pairs and run faster per pair than the whole matrix); warm-up steps
+    # are short untimed samples
     for i in range(args.warmup + args.steps):
-        r = cpu_assembly_sample(cfg, args.ratio, max(2.0, args.cpu_seconds / 2))
+        r = cpu_assembly_sample(cfg, args.ratio, args.cpu_seconds if i >= args.warmup else 1.0)
         if i >= args.warmup:
             samples.append(r)
     v = sum(s["pairs"] for s in samples) / sum(s["seconds"] for s in samples)
