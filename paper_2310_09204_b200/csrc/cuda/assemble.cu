@@ -877,16 +877,22 @@ __global__ void k_local_scatter(const int2* __restrict__ pairs, const double* __
 }
 
 // W(j,i) = W(i,j), j > i  (assemble.hpp:136-137), 32x32 tiles through smem
-__global__ void k_mirror(double* __restrict__ W, int n, int ld)
+// also flags a non-finite entry of the upper triangle, where every pair integral lands
+// (the reference throws NumericalError on a non-finite pair integral, assemble.hpp:106-107)
+__global__ void k_mirror(double* __restrict__ W, int n, int ld, int* __restrict__ bad)
 {
     __shared__ double tile[32][33];
     const int bi = blockIdx.y, bj = blockIdx.x;  // source tile (bi, bj), bi <= bj
     if (bi > bj) return;
     const int tx = threadIdx.x, ty = threadIdx.y;
+    bool finite = true;
     for (int r = ty; r < 32; r += blockDim.y) {
         const int i = bi * 32 + r, j = bj * 32 + tx;
-        tile[r][tx] = (i < n && j < n) ? W[(size_t)i * ld + j] : 0.0;
+        const double v = (i < n && j < n) ? W[(size_t)i * ld + j] : 0.0;
+        finite &= isfinite(v);
+        tile[r][tx] = v;
     }
+    if (__any_sync(0xffffffffu, !finite) && tx == 0) *bad = 1;
     __syncthreads();
     for (int r = ty; r < 32; r += blockDim.y) {
         const int i = bj * 32 + r, j = bi * 32 + tx;  // destination (lower) element (i, j) = source (j, i)
@@ -1332,6 +1338,7 @@ struct AssemblyPlan {
     DBuf<int2> loc_pairs;
     DBuf<double> loc_I;
     DBuf<unsigned long long> near_cnt;
+    DBuf<int> bad;  // non-finite flag of the mirror pass
 };
 
 AssemblyPlan* assembly_plan_create(Ctx* ctx, const InflatedMesh& im, const QuadCfg& cfg)
@@ -1487,6 +1494,7 @@ AssemblyPlan* assembly_plan_create(Ctx* ctx, const InflatedMesh& im, const QuadC
             P->spart[cls].alloc((size_t)P->schunks[cls] * np);
         }
         P->near_cnt.alloc(1);
+        P->bad.alloc(1);
         SBG_CUDA(cudaStreamSynchronize(s));
         // host-to-device bytes of this plan (e2e bookkeeping; rules are cached per context)
         auto bytes = [](const auto& b) { return (long long)(b.n * sizeof(*b.p)); };
@@ -1587,9 +1595,14 @@ void assembly_run(AssemblyPlan* P, DMatrix& W, AssemblyStats* stats, int rank, i
     {
         TimedScope ts(ctx, "mirror");
         const int nt = (P->n + 31) / 32;
-        k_mirror<<<dim3(nt, nt), dim3(32, 8), 0, s>>>(W.a.p, P->n, W.ld);
+        SBG_CUDA(cudaMemsetAsync(P->bad.p, 0, sizeof(int), s));
+        k_mirror<<<dim3(nt, nt), dim3(32, 8), 0, s>>>(W.a.p, P->n, W.ld, P->bad.p);
         count_launch();
         SBG_LAUNCH_CHECK();
+        int bad = 0;
+        SBG_CUDA(cudaMemcpyAsync(&bad, P->bad.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+        SBG_CUDA(cudaStreamSynchronize(s));
+        if (bad) throw NumericalError("quadrature produced a non-finite pair integral");
     }
     if (stats) {
         stats->identical = sing_cnt[3];
