@@ -36,7 +36,7 @@ CFG_NAMES = {1: "flat 16x16 (512 tri), H/h 8", 2: "flat 64x64 (8192 tri), H/h 16
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--exact-far", action="store_true",
@@ -76,7 +76,7 @@ def reduce_max(values, dist=None, device="cpu"):
 
 # --------------------------------------------------------------------------- clocks
 class NvmlSampler:
-    """SM clock + throttle reasons sampled every 200 ms during the timed region through
+    """SM clock + throttle reasons sampled every 20 ms during the timed region through
     in-process NVML (the nvidia-smi loop contends for the driver with the timed step)."""
     REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20, "sw_power_cap": 0x4}
 
@@ -100,7 +100,7 @@ class NvmlSampler:
                         self.rows.append((sm, r))
                     except Exception:
                         pass
-                    if self.stop.wait(0.2):
+                    if self.stop.wait(0.02):
                         break
             self.t = threading.Thread(target=run, daemon=True)
             self.t.start()
