@@ -295,8 +295,9 @@ def run_reference(args):
     # cpu_seconds or less: config 2 is assembled in full, since the last rows alone are
     # dominated by far pairs and run faster per pair than the whole matrix); warm-up steps
     # are short untimed samples
+    per_step = max(4.0, min(args.cpu_seconds, 150.0 / max(args.steps, 1)))  # whole run within a few minutes
     for i in range(args.warmup + args.steps):
-        r = cpu_assembly_sample(cfg, args.ratio, args.cpu_seconds if i >= args.warmup else 1.0)
+        r = cpu_assembly_sample(cfg, args.ratio, per_step if i >= args.warmup else 1.0)
         if i >= args.warmup:
             samples.append(r)
     v = sum(s["pairs"] for s in samples) / sum(s["seconds"] for s in samples)
