@@ -20,6 +20,7 @@
 #include <algorithm>
 #include <cmath>
 #include <future>
+#include <thread>
 #include <numeric>
 #include <stdexcept>
 #include <string>
@@ -1052,45 +1053,57 @@ struct SingularLists {
     std::vector<int2> pairs[4];    // (t, s)
 };
 
+// vertex-adjacent (f, g <= f) pairs with the permutation of pair_integral
+// (quadrature.hpp:297-322): t = facet f (the larger index), shared vertices first in f's
+// order, the rest ascending.
 void singular_pairs(const SurfaceMesh& m, SingularLists& S)
 {
     const int nf = m.num_facets(), nv = m.num_vertices();
-    std::vector<std::vector<int>> star(nv);
+    std::vector<int> sptr(nv + 1, 0), sfac(3 * (size_t)nf);  // vertex -> facets (CSR, ascending)
     for (int f = 0; f < nf; ++f)
-        for (int k = 0; k < 3; ++k) star[m.facets[f][k]].push_back(f);
-    std::vector<int> nb;
-    for (int f = 0; f < nf; ++f) {
-        nb.clear();
-        for (int k = 0; k < 3; ++k)
-            for (int g : star[m.facets[f][k]])
-                if (g <= f) nb.push_back(g);
-        std::sort(nb.begin(), nb.end());
-        nb.erase(std::unique(nb.begin(), nb.end()), nb.end());
-        for (int g : nb) {
-            // permutation of pair_integral (quadrature.hpp:297-322): t = facet f (larger index)
-            int pf[3] = {-1, -1, -1}, pg[3] = {-1, -1, -1}, shared = 0;
-            for (int i = 0; i < 3; ++i)
-                for (int j = 0; j < 3; ++j)
-                    if (m.facets[f][i] == m.facets[g][j]) {
-                        pf[shared] = i;
-                        pg[shared] = j;
-                        ++shared;
-                        break;
-                    }
-            auto fill = [](int* p, int have) {
-                for (int k = 0; k < 3; ++k) {
-                    bool used = false;
-                    for (int q = 0; q < have; ++q) used |= (p[q] == k);
-                    if (!used) p[have++] = k;
-                }
-            };
-            fill(pf, shared);
-            fill(pg, shared);
-            for (int k = 0; k < 3; ++k) S.pv[shared].push_back(m.facets[f][pf[k]]);
-            for (int k = 0; k < 3; ++k) S.pv[shared].push_back(m.facets[g][pg[k]]);
-            S.pairs[shared].push_back(make_int2(f, g));
-        }
+        for (int k = 0; k < 3; ++k) ++sptr[m.facets[f][k] + 1];
+    for (int v = 0; v < nv; ++v) sptr[v + 1] += sptr[v];
+    {
+        std::vector<int> fill(sptr.begin(), sptr.end() - 1);
+        for (int f = 0; f < nf; ++f)
+            for (int k = 0; k < 3; ++k) sfac[fill[m.facets[f][k]]++] = f;
     }
+    auto range = [&](int f0, int f1, SingularLists& L) {
+        std::vector<int> nb;
+        for (int f = f0; f < f1; ++f) {
+            nb.clear();
+            for (int k = 0; k < 3; ++k) {
+                const int v = m.facets[f][k];
+                for (int p = sptr[v]; p < sptr[v + 1] && sfac[p] <= f; ++p) nb.push_back(sfac[p]);
+            }
+            std::sort(nb.begin(), nb.end());
+            nb.erase(std::unique(nb.begin(), nb.end()), nb.end());
+            for (int g : nb) {
+                int pf[3] = {-1, -1, -1}, pg[3] = {-1, -1, -1}, shared = 0;
+                for (int i = 0; i < 3; ++i)
+                    for (int j = 0; j < 3; ++j)
+                        if (m.facets[f][i] == m.facets[g][j]) {
+                            pf[shared] = i;
+                            pg[shared] = j;
+                            ++shared;
+                            break;
+                        }
+                auto fill = [](int* p, int have) {
+                    for (int k = 0; k < 3; ++k) {
+                        bool used = false;
+                        for (int q = 0; q < have; ++q) used |= (p[q] == k);
+                        if (!used) p[have++] = k;
+                    }
+                };
+                fill(pf, shared);
+                fill(pg, shared);
+                for (int k = 0; k < 3; ++k) L.pv[shared].push_back(m.facets[f][pf[k]]);
+                for (int k = 0; k < 3; ++k) L.pv[shared].push_back(m.facets[g][pg[k]]);
+                L.pairs[shared].push_back(make_int2(f, g));
+            }
+        }
+    };
+    range(0, nf, S);  // runs beside the plan's main thread (assembly_plan_create)
 }
 
 struct SauterRulesDev {
