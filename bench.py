@@ -74,6 +74,17 @@ def reduce_max(values, dist=None, device="cpu"):
     return [float(v) for v in t]
 
 
+def allreduce_sum_(t, dist, rdev: str):
+    """In-place sum over ranks of a partial W (the --shard reduction): NCCL on the device
+    tensor, or through host memory for gloo (tests/test_distributed.py, functional runs)."""
+    if rdev == "cpu" and t.device.type != "cpu":
+        h = t.cpu()
+        dist.all_reduce(h)
+        t.copy_(h)
+    else:
+        dist.all_reduce(t)
+
+
 # --------------------------------------------------------------------------- clocks
 class NvmlSampler:
     """SM clock + throttle reasons sampled every 20 ms during the timed region through
@@ -364,12 +375,7 @@ def run_ours(args):
     rdev = "cpu" if args.dist_backend == "gloo" else f"cuda:{local}"
 
     def allreduce_(t):
-        if rdev == "cpu":
-            h = t.cpu()
-            dist.all_reduce(h)
-            t.copy_(h)
-        else:
-            dist.all_reduce(t)
+        allreduce_sum_(t, dist, rdev)
     ctx.timers(True)
     cfg = args.config
     ratio = args.ratio if args.ratio else (8 if cfg == 5 else 0)
