@@ -500,7 +500,13 @@ def run_ours(args):
     im2 = S.inflate(S.SurfaceMesh(pair.fine.vertices, pair.fine.facets), validate=False)
     # W lands in a page-locked host buffer allocated once, as the inputs of a step come from
     # pinned memory (the pageable-destination time is reported beside it)
-    Wbuf = S.pinned_empty((n, n))
+    try:
+        Wbuf = S.pinned_empty((n, n))
+        dest = "page-locked host buffer allocated once"
+    except Exception:  # not enough page-lockable host memory: a pageable buffer, reused
+        Wbuf = np.empty((n, n))
+        Wbuf.fill(0.0)
+        dest = "pageable host buffer allocated (and touched) once"
     pageable_ms = None
     for it in range(2 + max(args.steps, 4)):  # first run warms the host paths; min over the rest
         if it == 1:  # one run into a fresh pageable numpy array, for the record
@@ -587,8 +593,8 @@ def run_ours(args):
             "e2e": {"value": (1 if shard else world) * npairs / e2e_t, "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": 8 * n * n, "ms": e2e_t * 1e3,
                     "ms_pageable_destination": pageable_ms,
-                    "what": "S.assemble_W(host InflatedMesh) + W.download(out=pinned): plan build (host), H2D, kernels, "
-                            "D2H of the n x n W into a page-locked host buffer allocated once (the reference arm times assemble_W on an "
+                    "what": "S.assemble_W(host InflatedMesh) + W.download(out=buf): plan build (host), H2D, kernels, "
+                            f"D2H of the n x n W into a {dest} (the reference arm times assemble_W on an "
                             "inflated mesh the same way)"},
             "gpu_launches": launches,
             "clocks": clocks.summary(),
