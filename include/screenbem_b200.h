@@ -132,8 +132,9 @@ int sbg_assemble_w(sbg_ctx* ctx, const sbg_inflated* im, const sbg_quad_cfg* cfg
 int sbg_assembly_plan_create(sbg_ctx* ctx, const sbg_inflated* im, const sbg_quad_cfg* cfg, sbg_aplan** out);
 int sbg_assembly_run(sbg_aplan* plan, sbg_matrix** W, sbg_assembly_stats* stats);
 /* one shard (rank of world) of sbg_assembly_run for multi-GPU assembly of one W:
- * far / near-candidate tiles k with k % world == rank and a contiguous 1/world
- * of each singular class; the world shards' W sum entrywise to the full W (the
+ * far tiles k with k % world == rank, the near pairs whose pair hash maps to
+ * rank, and a contiguous 1/world of each singular class; stats count the shard's
+ * own work (far_pairs = -1); the world shards' W sum entrywise to the full W (the
  * caller reduces them, e.g. an NCCL all-reduce over sbg_matrix_device_view).
  * The reference's per-worker partial W + sum (inc/assemble.hpp:91-133), across processes. */
 int sbg_assembly_run_shard(sbg_aplan* plan, sbg_matrix** W, int rank, int world, sbg_assembly_stats* stats);

@@ -1201,21 +1201,41 @@ NearWork& near_work(Ctx* ctx)
     return *static_cast<NearWork*>(ctx->near_ws.get());
 }
 
+// owner rank of a near pair in a sharded assembly: by pair identity (every rank builds
+// the near list itself, in its own atomic order), hashed so ranks get similar mixes
+__device__ __forceinline__ int near_owner(int2 p, int world)
+{
+    const unsigned h = ((unsigned)p.x * 2654435761u) ^ ((unsigned)p.y * 2246822519u);
+    return (int)((h ^ (h >> 15)) % (unsigned)world);
+}
+
+// root nodes of the near pairs (world > 1: only those this rank owns; cnt[0] zeroed)
 __global__ void k_near_init(const unsigned long long* __restrict__ np_dev, long long cap, NearNode* __restrict__ nodes,
-                            double* __restrict__ out, unsigned long long* __restrict__ cnt)
+                            double* __restrict__ out, unsigned long long* __restrict__ cnt,
+                            const int2* __restrict__ pairs, int rank, int world)
 {
     const long long np = min((long long)*np_dev, cap);
     const long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (k < np) {
-        nodes[k] = {(int)k, 0u};
-        out[k] = 0.0;
+    if (world == 1) {
+        if (k < np) {
+            nodes[k] = {(int)k, 0u};
+            out[k] = 0.0;
+        }
+        if (k == 0) cnt[0] = (unsigned long long)np;
+        return;
     }
-    if (k == 0) cnt[0] = (unsigned long long)np;
+    if (k < np) {
+        out[k] = 0.0;
+        if (near_owner(pairs[k], world) == rank) nodes[atomicAdd(cnt, 1ull)] = {(int)k, 0u};
+    }
 }
 
 // near-pair integrals for the device list pairs[0:*np_dev] (capacity cap); returns the leaf count
+// (rank, world): only the near pairs this rank owns are integrated (the others' out = 0);
+// *owned receives their count
 long long run_near(Ctx* ctx, const RuleDims& R, const double* GV, const double* GA, const int2* pairs,
-                   const unsigned long long* np_dev, long long cap, double thr, double* out, NearWork& NW)
+                   const unsigned long long* np_dev, long long cap, double thr, double* out, NearWork& NW,
+                   int rank = 0, int world = 1, long long* owned = nullptr)
 {
     if (cap <= 0) return 0;
     cudaStream_t s = ctx->stream;
@@ -1223,13 +1243,15 @@ long long run_near(Ctx* ctx, const RuleDims& R, const double* GV, const double* 
     if (!NW.cnt.n) NW.cnt.alloc(3);
     set_max_dynamic_smem(k_near_leaves, NEAR_LEAF_SMEM);
     if ((long long)NW.cur.n < cap) NW.cur.alloc(cap);
-    k_near_init<<<(int)((cap + 255) / 256), 256, 0, s>>>(np_dev, cap, NW.cur.p, out, NW.cnt.p);
+    if (world > 1) SBG_CUDA(cudaMemsetAsync(NW.cnt.p, 0, sizeof(unsigned long long), s));
+    k_near_init<<<(int)((cap + 255) / 256), 256, 0, s>>>(np_dev, cap, NW.cur.p, out, NW.cnt.p, pairs, rank, world);
     count_launch();
     SBG_LAUNCH_CHECK();
     unsigned long long h[3] = {0, 0, 0};
     SBG_CUDA(cudaMemcpyAsync(h, NW.cnt.p, sizeof(h[0]), cudaMemcpyDeviceToHost, s));
     SBG_CUDA(cudaStreamSynchronize(s));
     long long ncur = (long long)h[0], total_leaves = 0;
+    if (owned) *owned = ncur;
     // classify level by level (each level's leaves appended to one list), then evaluate
     // every leaf in one launch: no per-level grid tails, and the host's per-level count
     // reads never wait on leaf work
@@ -1526,8 +1548,8 @@ void assembly_plan_destroy(AssemblyPlan* P) { delete P; }
 
 // reference: inc/assemble.hpp:72-139 (device kernels only; the plan holds the mesh data)
 // Shard (rank, world) of world > 1 computes only its share of the work into a
-// zeroed W: far tiles and near candidate tiles k with k % world == rank, and a
-// contiguous 1/world range of each singular class.  The shards' W sum to the
+// zeroed W: far tiles k with k % world == rank, the near pairs it owns
+// (near_owner), and a contiguous 1/world range of each singular class.  The shards' W sum to the
 // full W (up to fp64 atomic reordering); DESIGN.md §5.3.
 void assembly_run(AssemblyPlan* P, DMatrix& W, AssemblyStats* stats, int rank, int world)
 {
@@ -1541,26 +1563,28 @@ void assembly_run(AssemblyPlan* P, DMatrix& W, AssemblyStats* stats, int rank, i
     const RuleDims R = upload_rules(ctx, P->cfg);
     const double thr = P->cfg.near_threshold;
     auto share = [&](long long cnt) { return cnt > rank ? (cnt - rank + world - 1) / world : 0LL; };
-    const long long my_tiles = share(P->ntiles), my_cand = share(P->ncand);
+    // far tiles are strided over the ranks; every rank classifies all candidate tiles (cheap)
+    // and integrates the near pairs it owns (near_owner), which balances the near work
+    const long long my_tiles = share(P->ntiles), my_cand = P->ncand;
     long long sing_lo[4] = {0, 0, 0, 0}, sing_cnt[4] = {0, 0, 0, 0};
     for (int cls = 1; cls <= 3; ++cls) {
         sing_lo[cls] = P->cls_cnt[cls] * rank / world;
         sing_cnt[cls] = P->cls_cnt[cls] * (rank + 1) / world - sing_lo[cls];
     }
     // near list (classification of the non-certainly-far tiles)
-    long long leaves = 0;
+    long long leaves = 0, near_owned = 0;
     unsigned long long nnear = 0;
     for (int attempt = 0; attempt < 2; ++attempt) {
         SBG_CUDA(cudaMemsetAsync(P->near_cnt.p, 0, sizeof(unsigned long long), s));
         if (my_cand) {
             TimedScope ts(ctx, "classify");
-            k_classify_near<<<(int)my_cand, 256, 0, s>>>(P->cand.p + rank, world, P->G.ptrs(), P->bfac.p, thr,
+            k_classify_near<<<(int)my_cand, 256, 0, s>>>(P->cand.p, 1, P->G.ptrs(), P->bfac.p, thr,
                                                          P->loc_pairs.p + P->nsing, P->near_cap, P->near_cnt.p);
             count_launch();
             SBG_LAUNCH_CHECK();
         }
         leaves = run_near(ctx, R, P->G.v.p, P->G.area.p, P->loc_pairs.p + P->nsing, P->near_cnt.p, P->near_cap, thr,
-                          P->loc_I.p + P->nsing, near_work(ctx));
+                          P->loc_I.p + P->nsing, near_work(ctx), rank, world, &near_owned);
         SBG_CUDA(cudaMemcpyAsync(&nnear, P->near_cnt.p, sizeof(nnear), cudaMemcpyDeviceToHost, s));
         SBG_CUDA(cudaStreamSynchronize(s));
         if ((long long)nnear <= P->near_cap) break;
@@ -1621,12 +1645,12 @@ void assembly_run(AssemblyPlan* P, DMatrix& W, AssemblyStats* stats, int rank, i
         stats->identical = sing_cnt[3];
         stats->edge = sing_cnt[2];
         stats->vertex = sing_cnt[1];
-        stats->near_pairs = (long long)nnear;
+        stats->near_pairs = world == 1 ? (long long)nnear : near_owned;
         stats->near_leaves = leaves;
         // per shard the far count is not separated from the tiles' own classification
         stats->far_pairs = world == 1 ? (long long)P->nf * (P->nf + 1) / 2 - nloc : -1;
         stats->tiles = my_tiles;
-        stats->tiles_skipped = my_tiles - my_cand;
+        stats->tiles_skipped = my_tiles - share(P->ncand);  // sums to the total over the ranks
         stats->h2d_bytes = P->h2d_bytes;
     }
 }
