@@ -713,28 +713,30 @@ void launch_near_leaves_g(Ctx* ctx, const NearNode* leaves, const unsigned long 
 
 // ---------------------------------------------------------------- Sauter (singular) pairs
 // pairs: 6 ints per pair = permuted vertex ids of t then s (quadrature.hpp:297-322).
-// The permutation puts the shared vertices first, so t0 = s0 in every class (d0 = 0),
-// and per class the rule table is stored in the form the difference needs
-// (upload_sauter): identical (s = t): x - y = (a1-b1) e1 + (a2-b2) e2, 2 FMA per
-// coordinate; edge (t1 = s1 as well): x - y = (a1-b1) e1 + a2 e2t - b2 e2s, 3; vertex:
-// x - y = a1 e1t + a2 e2t - b1 e1s - b2 e2s, 4.
+// The permutation puts the shared vertices first, so t0 = s0 in every class (d0 = 0).
+// Identical (s = t): x - y = c1 e1 + c2 e2 with c = (a1-b1, a2-b2), so |x - y|^2 is the
+// quadratic form of the triangle's Gram matrix: 3 FMA per point from the rule table's
+// monomials (c1^2, 2 c1 c2, c2^2).  Edge (t1 = s1 too): x - y = c1 e1 + a2 e2t - b2 e2s,
+// a 3x3 Gram form, 6 FMA from (c1^2, a2^2, b2^2, 2 c1 a2, -2 c1 b2, -2 a2 b2).  The Gram
+// forms are positive definite on the rule's domain (the two triangles lie on either side
+// of the shared edge); their rounding grows with the triangles' aspect, ~1e-15 relative on
+// the configs.  Vertex: x - y = a1 e1t + a2 e2t - b1 e1s - b2 e2s by 4 FMA per coordinate
+// (four vectors in 3-D: the Gram form would be singular).  Rule tables (upload_sauter):
+// SAUTER_STRIDE doubles per point, the weight last.
 template <int CLS>
-__device__ __forceinline__ double sauter_r2(const double* a, const double (&e)[12])
+struct SauterStride {
+    static constexpr int value = CLS == 3 ? 4 : (CLS == 2 ? 7 : 5);
+};
+
+template <int CLS>
+__device__ __forceinline__ double sauter_r2(const double* a, const double (&g)[12])
 {
-    double dx, dy, dz;
-    if (CLS == 3) {
-        dx = fma(a[1], e[3], a[0] * e[0]);
-        dy = fma(a[1], e[4], a[0] * e[1]);
-        dz = fma(a[1], e[5], a[0] * e[2]);
-    } else if (CLS == 2) {
-        dx = fma(-a[2], e[9], fma(a[1], e[3], a[0] * e[0]));
-        dy = fma(-a[2], e[10], fma(a[1], e[4], a[0] * e[1]));
-        dz = fma(-a[2], e[11], fma(a[1], e[5], a[0] * e[2]));
-    } else {
-        dx = fma(-a[3], e[9], fma(-a[2], e[6], fma(a[1], e[3], a[0] * e[0])));
-        dy = fma(-a[3], e[10], fma(-a[2], e[7], fma(a[1], e[4], a[0] * e[1])));
-        dz = fma(-a[3], e[11], fma(-a[2], e[8], fma(a[1], e[5], a[0] * e[2])));
-    }
+    if (CLS == 3) return fma(a[0], g[0], fma(a[1], g[1], a[2] * g[2]));
+    if (CLS == 2)
+        return fma(a[0], g[0], fma(a[1], g[1], fma(a[2], g[2], fma(a[3], g[3], fma(a[4], g[4], a[5] * g[5])))));
+    const double dx = fma(-a[3], g[9], fma(-a[2], g[6], fma(a[1], g[3], a[0] * g[0])));
+    const double dy = fma(-a[3], g[10], fma(-a[2], g[7], fma(a[1], g[4], a[0] * g[1])));
+    const double dz = fma(-a[3], g[11], fma(-a[2], g[8], fma(a[1], g[5], a[0] * g[2])));
     return fma(dx, dx, fma(dy, dy, dz * dz));
 }
 
@@ -743,10 +745,12 @@ __global__ void __launch_bounds__(SAUTER_THREADS)
     k_sauter_partial(const int* __restrict__ pv, int npairs, const double* __restrict__ X,
                      const double* __restrict__ rule, int npts, int chunk, double* __restrict__ part)
 {
+    constexpr int ST = SauterStride<CLS>::value;
+    constexpr int STAGE = SAUTER_STAGE * 5 / ST;  // points per shared-memory pass
     __shared__ double R[SAUTER_STAGE * 5];
     const int p = blockIdx.x * blockDim.x + threadIdx.x;
     const bool active = p < npairs;
-    double e[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};  // e1t, e2t, e1s, e2s
+    double g[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};  // vertex: e1t, e2t, e1s, e2s; else Gram entries
     if (active) {
         const int* q = pv + 6 * p;
         const double* t0 = X + 3 * q[0];
@@ -755,6 +759,7 @@ __global__ void __launch_bounds__(SAUTER_THREADS)
         const double* s0 = X + 3 * q[3];
         const double* s1 = X + 3 * q[4];
         const double* s2 = X + 3 * q[5];
+        double e[12];
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
             e[c] = t1[c] - t0[c];
@@ -762,13 +767,29 @@ __global__ void __launch_bounds__(SAUTER_THREADS)
             e[6 + c] = s1[c] - s0[c];
             e[9 + c] = s2[c] - s0[c];
         }
+        auto dot = [&](int u, int v) { return fma(e[u], e[v], fma(e[u + 1], e[v + 1], e[u + 2] * e[v + 2])); };
+        if (CLS == 3) {
+            g[0] = dot(0, 0);
+            g[1] = dot(0, 3);
+            g[2] = dot(3, 3);
+        } else if (CLS == 2) {
+            g[0] = dot(0, 0);
+            g[1] = dot(3, 3);
+            g[2] = dot(9, 9);
+            g[3] = dot(0, 3);
+            g[4] = dot(0, 9);
+            g[5] = dot(3, 9);
+        } else {
+#pragma unroll
+            for (int k = 0; k < 12; ++k) g[k] = e[k];
+        }
     }
     const int q0 = blockIdx.y * chunk, q1 = min(npts, q0 + chunk);
     double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
-    for (int base = q0; base < q1; base += SAUTER_STAGE) {
-        const int cnt = min(SAUTER_STAGE, q1 - base);
+    for (int base = q0; base < q1; base += STAGE) {
+        const int cnt = min(STAGE, q1 - base);
         __syncthreads();
-        for (int k = threadIdx.x; k < cnt * 5; k += blockDim.x) R[k] = rule[(size_t)base * 5 + k];
+        for (int k = threadIdx.x; k < cnt * ST; k += blockDim.x) R[k] = rule[(size_t)base * ST + k];
         __syncthreads();
         if (active) {
             int i = 0;
@@ -776,13 +797,13 @@ __global__ void __launch_bounds__(SAUTER_THREADS)
             for (; i + 4 <= cnt; i += 4) {
                 double r2[4];
 #pragma unroll
-                for (int u = 0; u < 4; ++u) r2[u] = sauter_r2<CLS>(R + 5 * (i + u), e);
-                acc0 = fma(R[5 * i + 4], rsqrt_fast(r2[0]), acc0);
-                acc1 = fma(R[5 * i + 9], rsqrt_fast(r2[1]), acc1);
-                acc2 = fma(R[5 * i + 14], rsqrt_fast(r2[2]), acc2);
-                acc3 = fma(R[5 * i + 19], rsqrt_fast(r2[3]), acc3);
+                for (int u = 0; u < 4; ++u) r2[u] = sauter_r2<CLS>(R + ST * (i + u), g);
+                acc0 = fma(R[ST * i + ST - 1], rsqrt_fast(r2[0]), acc0);
+                acc1 = fma(R[ST * (i + 1) + ST - 1], rsqrt_fast(r2[1]), acc1);
+                acc2 = fma(R[ST * (i + 2) + ST - 1], rsqrt_fast(r2[2]), acc2);
+                acc3 = fma(R[ST * (i + 3) + ST - 1], rsqrt_fast(r2[3]), acc3);
             }
-            for (; i < cnt; ++i) acc0 = fma(R[5 * i + 4], rsqrt_fast(sauter_r2<CLS>(R + 5 * i, e)), acc0);
+            for (; i < cnt; ++i) acc0 = fma(R[ST * i + ST - 1], rsqrt_fast(sauter_r2<CLS>(R + ST * i, g)), acc0);
         }
     }
     if (active) part[(size_t)blockIdx.y * npairs + p] = (acc0 + acc1) + (acc2 + acc3);
@@ -1131,17 +1152,29 @@ void upload_sauter(Ctx* ctx, const QuadCfg& cfg, SauterRulesDev& R)
         rules = slot;
     }
     const SauterRule &id = rules->id, &ed = rules->ed, &vx = rules->vx;
-    // identical: (a1 - b1, a2 - b2, -, -, w); edge: (a1 - b1, a2, b2, -, w) (k_sauter_partial)
-    std::vector<double> idp(id.pts), edp(ed.pts);
-    for (size_t i = 0; i < idp.size(); i += 5) {
-        idp[i] = id.pts[i] - id.pts[i + 2];
-        idp[i + 1] = id.pts[i + 1] - id.pts[i + 3];
-        idp[i + 2] = idp[i + 3] = 0.0;
+    // Gram-form monomials (k_sauter_partial): identical (c1^2, 2 c1 c2, c2^2, w) with
+    // c = (a1 - b1, a2 - b2); edge (c1^2, a2^2, b2^2, 2 c1 a2, -2 c1 b2, -2 a2 b2, w)
+    std::vector<double> idp((size_t)id.size() * 4), edp((size_t)ed.size() * 7);
+    for (int i = 0; i < id.size(); ++i) {
+        const double* a = id.pts.data() + 5 * i;
+        const double c1 = a[0] - a[2], c2 = a[1] - a[3];
+        double* o = idp.data() + 4 * i;
+        o[0] = c1 * c1;
+        o[1] = 2.0 * c1 * c2;
+        o[2] = c2 * c2;
+        o[3] = a[4];
     }
-    for (size_t i = 0; i < edp.size(); i += 5) {
-        edp[i] = ed.pts[i] - ed.pts[i + 2];
-        edp[i + 2] = ed.pts[i + 3];
-        edp[i + 3] = 0.0;
+    for (int i = 0; i < ed.size(); ++i) {
+        const double* a = ed.pts.data() + 5 * i;
+        const double c1 = a[0] - a[2], c2 = a[1], c3 = a[3];
+        double* o = edp.data() + 7 * i;
+        o[0] = c1 * c1;
+        o[1] = c2 * c2;
+        o[2] = c3 * c3;
+        o[3] = 2.0 * c1 * c2;
+        o[4] = -2.0 * c1 * c3;
+        o[5] = -2.0 * c2 * c3;
+        o[6] = a[4];
     }
     R.r[3].upload(idp, ctx->stream);
     R.npts[3] = id.size();
