@@ -725,7 +725,7 @@ void launch_near_leaves_g(Ctx* ctx, const NearNode* leaves, const unsigned long 
 // SAUTER_STRIDE doubles per point, the weight last.
 template <int CLS>
 struct SauterStride {
-    static constexpr int value = CLS == 3 ? 4 : (CLS == 2 ? 7 : 5);
+    static constexpr int value = CLS == 3 ? 4 : (CLS == 2 ? 8 : 5);  // 4, 8: 32-byte rows (LDS.128)
 };
 
 template <int CLS>
@@ -747,7 +747,7 @@ __global__ void __launch_bounds__(SAUTER_THREADS)
 {
     constexpr int ST = SauterStride<CLS>::value;
     constexpr int STAGE = SAUTER_STAGE * 5 / ST;  // points per shared-memory pass
-    __shared__ double R[SAUTER_STAGE * 5];
+    __shared__ __align__(16) double R[SAUTER_STAGE * 5];
     const int p = blockIdx.x * blockDim.x + threadIdx.x;
     const bool active = p < npairs;
     double g[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};  // vertex: e1t, e2t, e1s, e2s; else Gram entries
@@ -1153,8 +1153,8 @@ void upload_sauter(Ctx* ctx, const QuadCfg& cfg, SauterRulesDev& R)
     }
     const SauterRule &id = rules->id, &ed = rules->ed, &vx = rules->vx;
     // Gram-form monomials (k_sauter_partial): identical (c1^2, 2 c1 c2, c2^2, w) with
-    // c = (a1 - b1, a2 - b2); edge (c1^2, a2^2, b2^2, 2 c1 a2, -2 c1 b2, -2 a2 b2, w)
-    std::vector<double> idp((size_t)id.size() * 4), edp((size_t)ed.size() * 7);
+    // c = (a1 - b1, a2 - b2); edge (c1^2, a2^2, b2^2, 2 c1 a2, -2 c1 b2, -2 a2 b2, 0, w)
+    std::vector<double> idp((size_t)id.size() * 4), edp((size_t)ed.size() * 8, 0.0);
     for (int i = 0; i < id.size(); ++i) {
         const double* a = id.pts.data() + 5 * i;
         const double c1 = a[0] - a[2], c2 = a[1] - a[3];
@@ -1167,14 +1167,14 @@ void upload_sauter(Ctx* ctx, const QuadCfg& cfg, SauterRulesDev& R)
     for (int i = 0; i < ed.size(); ++i) {
         const double* a = ed.pts.data() + 5 * i;
         const double c1 = a[0] - a[2], c2 = a[1], c3 = a[3];
-        double* o = edp.data() + 7 * i;
+        double* o = edp.data() + 8 * i;
         o[0] = c1 * c1;
         o[1] = c2 * c2;
         o[2] = c3 * c3;
         o[3] = 2.0 * c1 * c2;
         o[4] = -2.0 * c1 * c3;
         o[5] = -2.0 * c2 * c3;
-        o[6] = a[4];
+        o[7] = a[4];  // o[6] = 0: padding to 32-byte rows
     }
     R.r[3].upload(idp, ctx->stream);
     R.npts[3] = id.size();
