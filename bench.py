@@ -410,11 +410,17 @@ def run_ours(args):
 
     shard_ms = []
 
+    # --shard: the PCG runs by row panels — this rank's rows of each W p, then
+    # one all-gather of W p per iteration over NCCL on the PCG stream
+    rows = S.row_ranges(n, world)[rank] if shard else None
+    exchange = (S.allgather_exchange(dist, rank, world, n, device=f"cuda:{local}", host_staging=(rdev == "cpu"))
+                if shard else None)
+
     def step(W):
         W = assemble(plan, W)
         L = S.assemble_rhs(fine, g, ctx=ctx)
         prec = S.build_preconditioner(W, part, P)
-        rep = S.pcg(W, prec, L, 1e-8)
+        rep = S.pcg_rows(W, prec, L, rows, exchange, 1e-8) if shard else S.pcg(W, prec, L, 1e-8)
         return W, prec, rep
 
     W = None
@@ -557,7 +563,7 @@ def run_ours(args):
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"config {cfg}: {CFG_NAMES[cfg]}" + (f", H/h {ratio}" if cfg == 5 else ""),
                        "triangles": nf, "dofs": n, "tri_pairs": npairs, "parallelism": (f"assembly sharded x{world} (NCCL all-reduce of W), "
-                                                                   f"preconditioner + PCG replicated") if shard
+                                                                   f"preconditioner replicated, PCG by row panels (NCCL all-gather of W p per iteration)") if shard
                        else f"replicas x{world}",
                        "l2": "flushed (256 MiB write + 256 MiB read: cold L2 with clean lines) before every timed step and every matvec launch",
                        "pcg_tol": 1e-8, "far_field": "exact (IEEE, oracle order)" if args.exact_far else

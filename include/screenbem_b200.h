@@ -210,6 +210,24 @@ int sbg_condition_number(sbg_ctx* ctx, const sbg_matrix* W, sbg_prec* p, double 
 int sbg_pcg(sbg_ctx* ctx, const sbg_matrix* W, sbg_prec* prec, const double* rhs, int n, double tol, int maxit,
             double* x, double* history, double* alphas, double* betas, int hist_cap, sbg_pcg_report* rep);
 
+/* Row-panel PCG for one GPU per rank (the multi-worker counterpart of
+ * pcg, inc/pcg.hpp:33-116): W is replicated, this rank computes rows
+ * [row_lo, row_hi) of y = W p each iteration, and `exchange` — called on the host
+ * thread once per enqueued iteration, after those rows are enqueued on `stream` — must
+ * enqueue on that stream the all-gather that fills the other ranks' rows of d_y
+ * (e.g. NCCL over NVLink; d_p is the current search direction, for single-process
+ * emulation).  Return non-zero to abort.  All other steps (dot products, updates,
+ * preconditioner apply) are replicated and bitwise identical on every rank, so every
+ * rank stops at the same iteration.  rhs/x are device buffers when on_device. */
+typedef int (*sbg_exchange_fn)(void* user, const double* d_p, double* d_y, int n, void* stream);
+int sbg_pcg_rows(sbg_ctx* ctx, const sbg_matrix* W, sbg_prec* prec, const double* rhs, int n, int on_device,
+                 double tol, int maxit, int row_lo, int row_hi, sbg_exchange_fn exchange, void* user, double* x,
+                 double* history, double* alphas, double* betas, int hist_cap, sbg_pcg_report* rep);
+/* d_y[lo:hi] = W[lo:hi, :] d_x, enqueued on the context stream (no synchronisation) */
+int sbg_matvec_rows_device(sbg_ctx* ctx, const sbg_matrix* W, const double* d_x, double* d_y, int row_lo, int row_hi);
+/* the context's CUDA stream (cudaStream_t), for enqueuing collectives in order with it */
+int sbg_ctx_stream(sbg_ctx* ctx, void** stream);
+
 /* ---- device-resident benchmarking helpers (inputs already in HBM) --------- */
 int sbg_device_alloc(sbg_ctx* ctx, long long bytes, void** dptr);
 int sbg_device_free(void* dptr);

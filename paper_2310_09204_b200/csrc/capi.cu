@@ -854,6 +854,42 @@ int sbg_pcg(sbg_ctx* ctx, const sbg_matrix* W, sbg_prec* prec, const double* rhs
     });
 }
 
+int sbg_pcg_rows(sbg_ctx* ctx, const sbg_matrix* W, sbg_prec* prec, const double* rhs, int n, int on_device,
+                 double tol, int maxit, int row_lo, int row_hi, sbg_exchange_fn exchange, void* user, double* x,
+                 double* history, double* alphas, double* betas, int hist_cap, sbg_pcg_report* rep)
+{
+    return guard([&] {
+        bind_device(ctx ? &ctx->c : nullptr);
+        need(W, "W");
+        if (n != W->M.n) throw ValidationError("pcg: right-hand side length mismatch");
+        if (!exchange) throw ValidationError("pcg: row panel needs an exchange");
+        RowPanel rows;
+        rows.lo = row_lo;
+        rows.hi = row_hi;
+        rows.exchange = exchange;
+        rows.user = user;
+        PcgResult r;
+        pcg_run(&ctx->c, W->M, prec ? prec->P : nullptr, rhs, x, on_device != 0, tol, maxit, r, &rows);
+        fill_report(r, history, alphas, betas, hist_cap, rep);
+    });
+}
+int sbg_matvec_rows_device(sbg_ctx* ctx, const sbg_matrix* W, const double* d_x, double* d_y, int row_lo, int row_hi)
+{
+    return guard([&] {
+        bind_device(ctx ? &ctx->c : nullptr);
+        need(W, "W");
+        gemv_rows_range(&ctx->c, W->M, d_x, d_y, row_lo, row_hi);
+    });
+}
+int sbg_ctx_stream(sbg_ctx* ctx, void** stream)
+{
+    return guard([&] {
+        need(ctx, "ctx");
+        need(stream, "stream");
+        *stream = (void*)ctx->c.stream;
+    });
+}
+
 // ---------------------------------------------------------------- device-resident helpers
 int sbg_device_alloc(sbg_ctx* ctx, long long bytes, void** dptr)
 {

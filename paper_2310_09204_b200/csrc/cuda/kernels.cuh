@@ -88,9 +88,20 @@ struct PcgResult {
     double kappa = 1.0;
     std::vector<double> history, alphas, betas;
 };
-// rhs/x: device vectors when on_device, else host
+// Row-panel PCG: this rank computes rows [lo, hi) of y = W p; `exchange`
+// enqueues on `stream` the collective that fills the other ranks' rows of y (an
+// all-gather).  Every other step of the iteration is replicated on each rank.
+typedef int (*ExchangeFn)(void* user, const double* d_p, double* d_y, int n, void* stream);
+struct RowPanel {
+    int lo = 0, hi = 0;
+    ExchangeFn exchange = nullptr;
+    void* user = nullptr;
+};
+// rhs/x: device vectors when on_device, else host; rows: null = the whole matvec here
 void pcg_run(Ctx* ctx, const DMatrix& W, Prec* prec, const double* rhs, double* x, bool on_device, double tol,
-             int maxit, PcgResult& out);
+             int maxit, PcgResult& out, const RowPanel* rows = nullptr);
+// y[lo:hi] = W[lo:hi, :] x on device vectors, enqueued on the context stream (no sync)
+void gemv_rows_range(Ctx* ctx, const DMatrix& W, const double* x, double* y, int lo, int hi);
 double lanczos_kappa(const std::vector<double>& alphas, const std::vector<double>& betas);
 void lanczos_extremes(const std::vector<double>& alphas, const std::vector<double>& betas, double& lmin, double& lmax);
 struct Spectrum {

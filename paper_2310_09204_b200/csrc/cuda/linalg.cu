@@ -343,6 +343,16 @@ static void gemv_partial_launch(Ctx* ctx, const DMatrix& W, GemvPlan& plan, cons
 
 // "gemv_f64" times the whole matvec (partials + their reduction); inside PCG the
 // reduction is fused into k_pcg_alpha and the scope covers the partial pass
+void gemv_rows_range(Ctx* ctx, const DMatrix& W, const double* x, double* y, int lo, int hi)
+{
+    if (lo < 0 || hi > W.n || lo > hi) throw ValidationError("matvec rows: range outside the matrix");
+    if (hi == lo) return;
+    launch_gemv_rows(false, ctx->stream, hi - lo, (const double*)W.a.p + (size_t)lo * W.ld, W.ld, hi - lo, x, y + lo,
+                     (const int*)nullptr);
+    ::sbg::count_launch();
+    SBG_LAUNCH_CHECK();
+}
+
 void gemv(Ctx* ctx, const DMatrix& W, GemvPlan& plan, const double* x, double* y)
 {
     if (W.n == 0) return;
@@ -419,7 +429,7 @@ double lanczos_kappa(const std::vector<double>& alphas, const std::vector<double
 // pinned-memory registration per solve).
 struct PcgWork {
     int ld = 0, cap = 0;
-    DBuf<double> buf, partials, hist, alphas, betas;
+    DBuf<double> buf, partials, hist, alphas, betas, xbuf;  // xbuf: row-panel exchange buffer (ld)
     DBuf<PcgDev> st;
     GemvPlan plan;
     PcgDev* hs = nullptr;
@@ -458,6 +468,8 @@ static PcgWork& pcg_work(Ctx* ctx, const DMatrix& W, int maxit)
         fresh->alphas.alloc(fresh->cap);
         fresh->betas.alloc(fresh->cap);
         fresh->st.alloc(1);
+        fresh->xbuf.alloc((size_t)W.ld);
+        SBG_CUDA(cudaMemsetAsync(fresh->xbuf.p, 0, (size_t)W.ld * sizeof(double), ctx->stream));
         gemv_plan(ctx, W.n, W.ld, fresh->plan);
         SBG_CUDA(cudaMallocHost(&fresh->hs, sizeof(PcgDev)));
         ctx->pcg_ws = fresh;
@@ -470,10 +482,12 @@ static PcgWork& pcg_work(Ctx* ctx, const DMatrix& W, int maxit)
 // the host enqueues iterations in growing batches and reads back one small
 // state record per batch (iterations past convergence are no-op launches).
 void pcg_run(Ctx* ctx, const DMatrix& W, Prec* prec, const double* rhs, double* x_out, bool on_device, double tol,
-             int maxit, PcgResult& out)
+             int maxit, PcgResult& out, const RowPanel* rows)
 {
     const int n = W.n;
     if (tol <= 0) throw ValidationError("pcg: tolerance must be positive");
+    if (rows && (rows->lo < 0 || rows->hi > n || rows->lo > rows->hi || !rows->exchange))
+        throw ValidationError("pcg: row panel outside the matrix or no exchange");
     if (prec && prec_n(prec) != n) throw ValidationError("preconditioner length mismatch");
     if (maxit <= 0) maxit = std::max(10 * n, 100);
     if (n == 0) {  // empty system: converged at iteration 0 (pcg.hpp:41-49 with r0 = 0)
@@ -512,12 +526,33 @@ void pcg_run(Ctx* ctx, const DMatrix& W, Prec* prec, const double* rhs, double* 
     }
     // one PCG iteration (pcg.hpp:69-93) on the context stream
     auto enqueue_iteration = [&]() {
-        {
-            TimedScope ts(ctx, "gemv_f64");
-            gemv_partial_launch(ctx, W, w.plan, p, done);
+        if (rows) {
+            // row panel: this rank's rows of W p into the exchange buffer, then the
+            // caller's all-gather fills the rest (issued even past convergence, so every
+            // rank enqueues the same collectives; the kernels around it are no-ops then)
+            {
+                TimedScope ts(ctx, "gemv_f64");
+                if (rows->hi > rows->lo)
+                    launch_gemv_rows(true, s, rows->hi - rows->lo, (const double*)W.a.p + (size_t)rows->lo * W.ld, W.ld,
+                                     rows->hi - rows->lo, (const double*)p, w.xbuf.p + rows->lo, done);
+                count_launch();
+                SBG_LAUNCH_CHECK();
+            }
+            {
+                TimedScope ts(ctx, "pcg_exchange");
+                if (rows->exchange(rows->user, p, w.xbuf.p, n, (void*)s) != 0)
+                    throw std::runtime_error("pcg: the row-panel exchange failed");
+            }
+            launch_pdl(k_pcg_alpha, dim3(nb), dim3(256), 0, s, w.st.p, (const double*)w.xbuf.p, 1, W.ld, n, p, Wp,
+                       w.partials.p);
+        } else {
+            {
+                TimedScope ts(ctx, "gemv_f64");
+                gemv_partial_launch(ctx, W, w.plan, p, done);
+            }
+            launch_pdl(k_pcg_alpha, dim3(nb), dim3(256), 0, s, w.st.p, w.plan.part.p, w.plan.chunks, W.ld, n, p, Wp,
+                       w.partials.p);
         }
-        launch_pdl(k_pcg_alpha, dim3(nb), dim3(256), 0, s, w.st.p, w.plan.part.p, w.plan.chunks, W.ld, n, p, Wp,
-                   w.partials.p);
         count_launch();
         launch_pdl(k_pcg_update, dim3(nb), dim3(256), 0, s, w.st.p, x, r, p, Wp, n);
         count_launch();
@@ -528,7 +563,8 @@ void pcg_run(Ctx* ctx, const DMatrix& W, Prec* prec, const double* rhs, double* 
         count_launch();
         SBG_LAUNCH_CHECK();
     };
-    if (n > 0 && pcg_graph_enabled()) {
+    const bool graph = n > 0 && pcg_graph_enabled() && !rows;  // the exchange is a host call
+    if (graph) {
         // graph form: [gate] -> while(handle) { iteration ; gate } — the loop runs on the device
         // with no host round trips and no launches past convergence
         if (!w.exec || w.gW != W.a.p || w.gP != (prec ? prec_uid(prec) : 0)) {
@@ -604,7 +640,7 @@ void pcg_run(Ctx* ctx, const DMatrix& W, Prec* prec, const double* rhs, double* 
         SBG_CUDA(cudaStreamSynchronize(s));
         add_launches((long long)w.kernels_per_iter * w.hs->it + 1 + w.hs->it);  // body kernels + gates
     }
-    int batch = 4, enqueued = pcg_graph_enabled() ? maxit : 0;
+    int batch = 4, enqueued = graph ? maxit : 0;
     while (true) {
         SBG_CUDA(cudaMemcpyAsync(w.hs, w.st.p, sizeof(PcgDev), cudaMemcpyDeviceToHost, s));
         SBG_CUDA(cudaStreamSynchronize(s));

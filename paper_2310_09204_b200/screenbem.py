@@ -123,6 +123,10 @@ SIGNATURES = {
     "sbg_prec_destroy": (None, [vp]),
     "sbg_pcg": (C.c_int, [vp, vp, vp, f64p, C.c_int, C.c_double, C.c_int, f64p, f64p, f64p, f64p, C.c_int,
                           C.POINTER(PcgReportC)]),
+    "sbg_pcg_rows": (C.c_int, [vp, vp, vp, vp, C.c_int, C.c_int, C.c_double, C.c_int, C.c_int, C.c_int,
+                               vp, vp, vp, f64p, f64p, f64p, C.c_int, C.POINTER(PcgReportC)]),
+    "sbg_matvec_rows_device": (C.c_int, [vp, vp, vp, vp, C.c_int, C.c_int]),
+    "sbg_ctx_stream": (C.c_int, [vp, C.POINTER(vp)]),
     "sbg_device_alloc": (C.c_int, [vp, C.c_longlong, C.POINTER(vp)]),
     "sbg_device_free": (C.c_int, [vp]),
     "sbg_host_alloc": (C.c_int, [C.c_longlong, C.POINTER(vp)]),
@@ -195,6 +199,13 @@ class Context(_Handle):
 
     def synchronize(self):
         _check(lib().sbg_ctx_synchronize(self.h))
+
+    @property
+    def stream(self) -> int:
+        """The context's cudaStream_t (address), e.g. for torch.cuda.ExternalStream."""
+        p = vp()
+        _check(lib().sbg_ctx_stream(self.h, C.byref(p)))
+        return p.value or 0
 
     def timers(self, on: bool = True):
         _check(lib().sbg_timers_enable(self.h, 1 if on else 0))
@@ -783,6 +794,118 @@ def pcg(W: GalerkinMatrix, prec, rhs, tol: float = 1e-8, maxit: int = 0) -> PcgR
     k = rep.iterations
     return PcgReport(x[:n], k, bool(rep.converged), hist[:rep.history_len].copy(), rep.kappa_estimate,
                      al[:k].copy(), be[:k].copy())
+
+
+# --------------------------------------------------------------------------- row-panel PCG
+# exchange hook of sbg_pcg_rows: (user, d_p, d_y, n, stream) -> 0 | error
+EXCHANGE_FN = C.CFUNCTYPE(C.c_int, vp, vp, vp, C.c_int, vp)
+
+
+def row_ranges(n: int, world: int):
+    """Row panels of the multi-GPU PCG: rank r owns rows
+    [r*k, min(n, (r+1)*k)) with k = ceil(n / world) — equal panels, so the all-gather
+    of W p moves k doubles per rank (the last panel is padded)."""
+    if world < 1:
+        raise ValidationError("world size must be positive")
+    k = -(-n // world) if n else 0
+    return [(min(n, r * k), min(n, (r + 1) * k)) for r in range(world)]
+
+
+class DeviceVector:
+    """A float64 device vector given by address and length (`__cuda_array_interface__`),
+    so torch / NCCL can read and write PCG buffers in place."""
+
+    def __init__(self, ptr: int, n: int):
+        self.ptr, self.n = int(ptr or 0), int(n)
+
+    @property
+    def __cuda_array_interface__(self):
+        return {"shape": (self.n,), "typestr": "<f8", "data": (self.ptr, False), "version": 3, "strides": None,
+                "stream": None}
+
+
+def allgather_exchange(dist, rank: int, world: int, n: int, device=None, wrap=None, host_staging=False):
+    """The exchange of the row-panel PCG over torch.distributed: every rank contributes its
+    panel of y = W p (row_ranges) and receives the others', in place in y.  On the GPU the
+    collective is enqueued on the PCG's own stream (torch's current stream is switched to
+    it), so no host synchronisation happens per iteration; NCCL moves the panels over
+    NVLink.  `wrap(ptr, n)` maps a buffer address to a tensor (default: the device vector
+    through __cuda_array_interface__; tests pass a host-memory wrapper to run it on gloo).
+    host_staging: gather through host memory (gloo functional runs, ranks sharing a GPU).
+    Returns f(d_p, d_y, n, stream) for pcg_rows."""
+    import torch
+    ranges = row_ranges(n, world)
+    k = ranges[0][1] - ranges[0][0] if n else 0
+    if wrap is None:
+        def wrap(ptr, m):
+            return torch.as_tensor(DeviceVector(ptr, m), device=device)
+    state = {}
+
+    def exchange(d_p, d_y, m, stream):
+        if m != n:
+            raise ValidationError("row exchange: length mismatch")
+        y = wrap(d_y, n)
+        lo, hi = ranges[rank]
+        ctxm = torch.cuda.stream(torch.cuda.ExternalStream(stream, device=y.device)) if y.is_cuda else _nullctx()
+        with ctxm:
+            if "mine" not in state:  # staging allocated once, on the PCG stream
+                sd = "cpu" if host_staging else y.device
+                state["mine"] = torch.zeros(k, dtype=torch.float64, device=sd)
+                state["all"] = [torch.zeros(k, dtype=torch.float64, device=sd) for _ in range(world)]
+            mine, parts = state["mine"], state["all"]
+            mine[:hi - lo].copy_(y[lo:hi])
+            dist.all_gather(parts, mine)
+            for r, (a, b) in enumerate(ranges):
+                if r != rank and b > a:
+                    y[a:b].copy_(parts[r][:b - a])
+        return 0
+    return exchange
+
+
+class _nullctx:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        return False
+
+
+def pcg_rows(W: GalerkinMatrix, prec, rhs, rows, exchange, tol: float = 1e-8, maxit: int = 0) -> PcgReport:
+    """Row-panel PCG (sbg_pcg_rows): the reference's pcg (inc/pcg.hpp:33-116) with this
+    rank computing rows `rows = (lo, hi)` of each matvec and `exchange(d_p, d_y, n,
+    stream)` filling in the rest (allgather_exchange for one GPU per rank).  The result
+    equals pcg's (same kernels per row, same replicated reductions)."""
+    rhs = np.ascontiguousarray(rhs, dtype=np.float64)
+    n = len(rhs)
+    cap = (maxit if maxit > 0 else max(10 * n, 100)) + 2
+    x = np.zeros(max(n, 1))
+    hist, al, be = np.zeros(cap), np.zeros(cap), np.zeros(cap)
+    rep = PcgReportC()
+    err = []
+
+    def hook(user, d_p, d_y, m, stream):
+        try:
+            exchange(d_p, d_y, m, stream)
+            return 0
+        except BaseException as e:  # surfaced after the C call returns
+            err.append(e)
+            return 1
+    cb = EXCHANGE_FN(hook)
+    rb = (rhs if n else np.zeros(1))
+    code = lib().sbg_pcg_rows(W.ctx.h, W.h, prec.h if prec is not None else None, rb.ctypes.data, n, 0, tol, maxit,
+                              int(rows[0]), int(rows[1]), C.cast(cb, vp), None, x.ctypes.data, hist, al, be, cap,
+                              C.byref(rep))
+    if err:
+        raise err[0]
+    _check(code)
+    k = rep.iterations
+    return PcgReport(x[:n], k, bool(rep.converged), hist[:rep.history_len].copy(), rep.kappa_estimate,
+                     al[:k].copy(), be[:k].copy())
+
+
+def matvec_rows_device(W: GalerkinMatrix, d_x: int, d_y: int, lo: int, hi: int) -> None:
+    """d_y[lo:hi] = W[lo:hi, :] d_x on device buffers, enqueued on the context stream."""
+    _check(lib().sbg_matvec_rows_device(W.ctx.h, W.h, d_x, d_y, lo, hi))
 
 
 # --------------------------------------------------------------------------- pipeline

@@ -52,6 +52,57 @@ def test_two_rank_gloo_max_over_ranks():
         assert err < 1e-14
 
 
+def _exchange_worker(rank, world, port, n, out):
+    """the row-panel PCG's all-gather hook (screenbem.allgather_exchange) on gloo, with
+    host buffers standing in for the device vectors"""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import numpy as np
+    import torch
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2310_09204_b200 import screenbem as S
+    full = np.arange(1.0, n + 1.0) * 0.5
+    y = np.full(n, -1.0)  # only this rank's panel is filled, as after its row kernel
+    lo, hi = S.row_ranges(n, world)[rank]
+    y[lo:hi] = full[lo:hi]
+    keep = {}
+
+    def wrap(ptr, m):
+        assert ptr == y.ctypes.data and m == n
+        keep["t"] = torch.from_numpy(y)
+        return keep["t"]
+    ex = S.allgather_exchange(dist, rank, world, n, wrap=wrap)
+    ex(0, y.ctypes.data, n, 0)
+    first = np.abs(y - full).max()
+    y[:] = -1.0
+    y[lo:hi] = 2 * full[lo:hi]
+    ex(0, y.ctypes.data, n, 0)  # reused staging buffers
+    out[rank] = (first, np.abs(y - 2 * full).max())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("world,n", [(2, 11), (3, 10), (2, 1)])
+def test_row_panel_exchange_gloo(world, n):
+    port = _free_port()
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_exchange_worker, args=(world, port, n, out), nprocs=world, join=True)
+    for rank in range(world):
+        assert out[rank] == (0.0, 0.0)
+
+
+def test_row_ranges():
+    from paper_2310_09204_b200 import screenbem as S
+    assert S.row_ranges(10, 3) == [(0, 4), (4, 8), (8, 10)]
+    assert S.row_ranges(3969, 8)[-1] == (3479, 3969)
+    assert S.row_ranges(2, 4) == [(0, 1), (1, 2), (2, 2), (2, 2)]
+    assert S.row_ranges(0, 2) == [(0, 0), (0, 0)]
+    for n, w in [(25281, 8), (7, 7), (100, 3)]:
+        rr = S.row_ranges(n, w)
+        assert rr[0][0] == 0 and rr[-1][1] == n and all(a[1] == b[0] for a, b in zip(rr, rr[1:]))
+
+
 def test_single_rank_passthrough():
     import bench
     assert bench.reduce_max([3.0, 4.0]) == [3.0, 4.0]
