@@ -1,5 +1,5 @@
 """Matvec per-launch time with the L2 flushed before each launch (as bench.py measures it)
-for configs 1-3 (development aid; SBG_GEMV_RPC selects the rows-form CTA size).
+for configs 1-3 (development aid; W symmetric random).
 
     python tools/matvec_probe.py [--configs 1,2,3] [--reps 30]
 """
@@ -23,7 +23,9 @@ def main():
     ctx.timers(True)
     for cfg in [int(c) for c in args.configs.split(",")]:
         n = S.inflate(S.make_config(cfg).fine, validate=False).n
-        W = S.GalerkinMatrix.from_host(np.random.default_rng(cfg).standard_normal((n, n)), ctx)
+        A = np.random.default_rng(cfg).standard_normal((n, n))
+        W = S.GalerkinMatrix.from_host(A + A.T, ctx)  # symmetric, as W (the column-sum form relies on it)
+        del A
         ldp = (n + 31) // 32 * 32
         dx, dy = C.c_void_p(), C.c_void_p()
         S._check(S.lib().sbg_device_alloc(ctx.h, 8 * ldp, C.byref(dx)))
