@@ -18,6 +18,7 @@
 //   Near and singular pair integrals are scattered per pair; W is accumulated
 //   in its upper triangle and mirrored at the end (assemble.hpp:136-137).
 #include <algorithm>
+#include <optional>
 #include <cmath>
 #include <future>
 #include <thread>
@@ -1433,6 +1434,7 @@ AssemblyPlan* assembly_plan_create(Ctx* ctx, const InflatedMesh& im, const QuadC
         P->dims = upload_rules(ctx, cfg);
         upload_geometry(ctx, m, P->G);
         HostScope hs1(ctx, "plan_curls");
+        std::optional<HostScope> hs_morton(std::in_place, ctx, "plan_morton");
         // ---- Morton-ordered facet blocks
         std::vector<Vec3> cen(nf);
         double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
@@ -1458,7 +1460,10 @@ AssemblyPlan* assembly_plan_create(Ctx* ctx, const InflatedMesh& im, const QuadC
         std::vector<int> perm(nf);
         std::iota(perm.begin(), perm.end(), 0);
         std::stable_sort(perm.begin(), perm.end(), [&](int a, int b) { return key[a] < key[b]; });
+        hs_morton.reset();
+        std::optional<HostScope> hs_wait(std::in_place, ctx, "plan_curl_wait");
         const FacetCurls U = curl_fut.get();
+        hs_wait.reset();
         P->uptr.upload(U.ptr, s);
         P->udof.upload(U.dof, s);
         P->uval.upload(U.u, s);

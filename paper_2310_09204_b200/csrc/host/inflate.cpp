@@ -5,6 +5,9 @@
 #include <numeric>
 #include <unordered_map>
 
+#include <cstdlib>
+#include <thread>
+
 #include "host.hpp"
 
 namespace sbg {
@@ -369,23 +372,29 @@ DofPartition partition_dofs(const MeshLevelPair& pair, const InflatedMesh& fine)
 }
 
 // reference: inc/assemble.hpp:18-29 (shape gradient), :34-53 (scatter), :83-89 (slot curls)
-FacetCurls facet_curls(const InflatedMesh& im)
+// facets [f0, f1): ptr holds the running entry counts relative to the range start
+static void facet_curls_range(const InflatedMesh& im, int f0, int f1, FacetCurls& out)
 {
     const SurfaceMesh& m = im.base;
-    FacetCurls out;
+    out.ptr.clear();
+    out.ptr.reserve((size_t)(f1 - f0));
+    out.dof.reserve((size_t)(f1 - f0) * 3);
+    out.u.reserve((size_t)(f1 - f0) * 9);
     std::vector<std::pair<int, Vec3>> acc;
-    for (int f = 0; f < m.num_facets(); ++f) {
+    for (int f = f0; f < f1; ++f) {
         acc.clear();
         const auto& t = m.facets[f];
         const Vec3 n = m.facet_normal(f);
         const double two_area = 2.0 * m.facet_measure(f);
+        // n x e_k / (2A) is the same for both sides (computed once; same values)
+        Vec3 g[3];
+        for (int k = 0; k < 3; ++k) g[k] = cross(n, m.vertices[t[(k + 2) % 3]] - m.vertices[t[(k + 1) % 3]]) / two_area;
         for (int s = 0; s < 2; ++s) {
             const int o = 2 * f + s;
             for (int k = 0; k < 3; ++k) {
-                const Vec3 e = m.vertices[t[(k + 2) % 3]] - m.vertices[t[(k + 1) % 3]];
-                const Vec3 curl = cross(im.onormal[o], cross(n, e) / two_area);
                 const int v = t[k], b = im.ofacet_branch[o][k], q = im.q[v];
                 if (q < 2) continue;
+                const Vec3 curl = cross(im.onormal[o], g[k]);
                 auto add = [&](int d, double w) {
                     for (auto& [dd, u] : acc)
                         if (dd == d) {
@@ -409,6 +418,39 @@ FacetCurls facet_curls(const InflatedMesh& im)
         }
         out.ptr.push_back((int)out.dof.size());
         out.kmax = std::max(out.kmax, (int)acc.size());
+    }
+}
+
+// Facets are independent: large meshes split into contiguous ranges on a few threads,
+// concatenated in facet order (the same lists as one pass).
+FacetCurls facet_curls(const InflatedMesh& im)
+{
+    const int nf = im.base.num_facets();
+    int want = std::thread::hardware_concurrency() >= 8 ? 4 : 1;
+    if (const char* e = std::getenv("SBG_CURL_THREADS")) want = std::max(1, std::atoi(e));
+    const int nt = std::min(want, std::max(1, nf / 2048));
+    std::vector<FacetCurls> parts(std::max(nt, 1));
+    if (nt <= 1) {
+        facet_curls_range(im, 0, nf, parts[0]);
+    } else {
+        std::vector<std::thread> th;
+        for (int i = 1; i < nt; ++i)
+            th.emplace_back([&, i] { facet_curls_range(im, (int)((long long)nf * i / nt), (int)((long long)nf * (i + 1) / nt), parts[i]); });
+        facet_curls_range(im, 0, (int)((long long)nf / nt), parts[0]);
+        for (auto& t : th) t.join();
+    }
+    FacetCurls out;
+    size_t ne = 0;
+    for (const auto& p : parts) ne += p.dof.size();
+    out.ptr.reserve((size_t)nf + 1);
+    out.dof.reserve(ne);
+    out.u.reserve(3 * ne);
+    for (const auto& p : parts) {
+        const int base = (int)out.dof.size();
+        for (int c : p.ptr) out.ptr.push_back(base + c);
+        out.dof.insert(out.dof.end(), p.dof.begin(), p.dof.end());
+        out.u.insert(out.u.end(), p.u.begin(), p.u.end());
+        out.kmax = std::max(out.kmax, p.kmax);
     }
     return out;
 }
