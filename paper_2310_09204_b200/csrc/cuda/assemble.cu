@@ -18,6 +18,7 @@
 //   Near and singular pair integrals are scattered per pair; W is accumulated
 //   in its upper triangle and mirrored at the end (assemble.hpp:136-137).
 #include <algorithm>
+#include <cstring>
 #include <optional>
 #include <cmath>
 #include <future>
@@ -1042,7 +1043,60 @@ struct DeviceGeometry {
     GeoPtrs ptrs() const { return {v.p, c.p, rad.p, diam.p, area.p, vid.p}; }
 };
 
-void upload_geometry(Ctx* ctx, const SurfaceMesh& m, DeviceGeometry& G)
+// Plan uploads through a page-locked staging arena (cached on the context, grow-only):
+// a host memcpy into the arena and an asynchronous DMA, instead of a pageable
+// cudaMemcpyAsync per array (each stages and synchronises inside the driver).  The
+// arena is reused only after a stream synchronisation (the plan build ends with one).
+struct StageArena {
+    char* p = nullptr;
+    size_t cap = 0;
+    ~StageArena()
+    {
+        if (p) cudaFreeHost(p);
+    }
+};
+struct Stager {
+    Ctx* ctx;
+    StageArena* A;
+    size_t off = 0;
+    explicit Stager(Ctx* c) : ctx(c)
+    {
+        if (!c->stage_ws) c->stage_ws = std::make_shared<StageArena>();
+        A = static_cast<StageArena*>(c->stage_ws.get());
+    }
+    template <typename T>
+    void upload(DBuf<T>& b, const T* h, size_t count)
+    {
+        if (count > b.n) b.alloc(count);
+        raw(b.p, h, count * sizeof(T));
+    }
+    void raw(void* dst, const void* h, size_t bytes)
+    {
+        if (!bytes) return;
+        if (off + bytes > A->cap) {  // arena full: wait for its copies, then reuse or grow it
+            SBG_CUDA(cudaStreamSynchronize(ctx->stream));
+            off = 0;
+            if (bytes > A->cap) {
+                if (A->p) SBG_CUDA(cudaFreeHost(A->p));
+                A->p = nullptr;
+                A->cap = 0;
+                const size_t cap = std::max(bytes, (size_t)16 << 20);
+                SBG_CUDA(cudaHostAlloc((void**)&A->p, cap, cudaHostAllocDefault));
+                A->cap = cap;
+            }
+        }
+        std::memcpy(A->p + off, h, bytes);
+        SBG_CUDA(cudaMemcpyAsync(dst, A->p + off, bytes, cudaMemcpyHostToDevice, ctx->stream));
+        off = (off + bytes + 255) & ~(size_t)255;
+    }
+    template <typename T>
+    void upload(DBuf<T>& b, const std::vector<T>& v)
+    {
+        upload(b, v.data(), v.size());
+    }
+};
+
+void upload_geometry(Ctx* ctx, const SurfaceMesh& m, DeviceGeometry& G, Stager* st)
 {
     cudaStream_t s = ctx->stream;
     const int nf = m.num_facets(), nv = m.num_vertices();
@@ -1055,8 +1109,13 @@ void upload_geometry(Ctx* ctx, const SurfaceMesh& m, DeviceGeometry& G)
     std::vector<int> F(3 * (size_t)nf);
     for (int f = 0; f < nf; ++f)
         for (int k = 0; k < 3; ++k) F[3 * f + k] = m.facets[f][k];
-    G.X.upload(X, s);
-    G.F.upload(F, s);
+    if (st) {
+        st->upload(G.X, X);
+        st->upload(G.F, F);
+    } else {
+        G.X.upload(X, s);
+        G.F.upload(F, s);
+    }
     G.v.alloc(9 * (size_t)nf);
     G.c.alloc(3 * (size_t)nf);
     G.rad.alloc(nf);
@@ -1431,8 +1490,9 @@ AssemblyPlan* assembly_plan_create(Ctx* ctx, const InflatedMesh& im, const QuadC
             return S;
         });
         auto curl_fut = std::async(std::launch::async, [&im] { return facet_curls(im); });
+        Stager st(ctx);
         P->dims = upload_rules(ctx, cfg);
-        upload_geometry(ctx, m, P->G);
+        upload_geometry(ctx, m, P->G, &st);
         HostScope hs1(ctx, "plan_curls");
         std::optional<HostScope> hs_morton(std::in_place, ctx, "plan_morton");
         // ---- Morton-ordered facet blocks
@@ -1464,51 +1524,83 @@ AssemblyPlan* assembly_plan_create(Ctx* ctx, const InflatedMesh& im, const QuadC
         std::optional<HostScope> hs_wait(std::in_place, ctx, "plan_curl_wait");
         const FacetCurls U = curl_fut.get();
         hs_wait.reset();
-        P->uptr.upload(U.ptr, s);
-        P->udof.upload(U.dof, s);
-        P->uval.upload(U.u, s);
+        {
+            HostScope hsu(ctx, "plan_upload_curls");
+            st.upload(P->uptr, U.ptr);
+            st.upload(P->udof, U.dof);
+            st.upload(P->uval, U.u);
+        }
         const int nblk = (nf + BS - 1) / BS;
         std::vector<int> bfac((size_t)nblk * BS, -1);
         for (int k = 0; k < nf; ++k) bfac[k] = perm[k];
+        std::vector<double> bcx(nblk), bcy(nblk), bcz(nblk), brad(nblk);
+        // per block: centre, radius and the DOF-sorted curl entries; blocks are independent,
+        // built on a few threads over contiguous block ranges and concatenated in block order
+        struct BlockLists {
+            std::vector<int> dofs, ent_ptr, ndofs;
+            std::vector<double4> ents;
+        };
+        auto build_blocks = [&](int b0, int b1, BlockLists& out) {
+            struct DE {
+                int dof, l, p;
+            };
+            std::vector<DE> dl;
+            for (int b = b0; b < b1; ++b) {
+                dl.clear();
+                Vec3 cs;
+                int cnt = 0;
+                for (int l = 0; l < BS; ++l) {
+                    const int f = bfac[b * BS + l];
+                    if (f < 0) continue;
+                    cs = cs + cen[f];
+                    ++cnt;
+                    for (int p = U.ptr[f]; p < U.ptr[f + 1]; ++p) dl.push_back({U.dof[p], l, p});
+                }
+                const Vec3 cc = cs / (double)cnt;
+                double R = 0;
+                for (int l = 0; l < BS; ++l) {
+                    const int f = bfac[b * BS + l];
+                    if (f >= 0) R = std::max(R, norm(cen[f] - cc));
+                }
+                bcx[b] = cc.x;
+                bcy[b] = cc.y;
+                bcz[b] = cc.z;
+                brad[b] = R;
+                std::sort(dl.begin(), dl.end(),
+                          [](const DE& x, const DE& y) { return x.dof != y.dof ? x.dof < y.dof : x.l < y.l; });
+                int nd = 0;
+                for (size_t i = 0; i < dl.size(); ++i) {
+                    if (i == 0 || dl[i].dof != dl[i - 1].dof) {
+                        out.dofs.push_back(dl[i].dof);
+                        out.ent_ptr.push_back((int)out.ents.size());
+                        ++nd;
+                    }
+                    const int p = dl[i].p;
+                    out.ents.push_back(make_double4(U.u[3 * p], U.u[3 * p + 1], U.u[3 * p + 2], (double)dl[i].l));
+                }
+                out.ndofs.push_back(nd);
+            }
+        };
+        const int nth = std::max(1, std::min(4, nblk / 32));
+        std::vector<BlockLists> parts(nth);
+        {
+            HostScope hsb(ctx, "plan_blocks");
+            std::vector<std::thread> th;
+            for (int t = 1; t < nth; ++t)
+                th.emplace_back(build_blocks, (int)((long long)nblk * t / nth), (int)((long long)nblk * (t + 1) / nth),
+                                std::ref(parts[t]));
+            build_blocks(0, (int)((long long)nblk / nth), parts[0]);
+            for (auto& t : th) t.join();
+        }
         std::vector<int> dof_ptr{0}, dofs, ent_ptr;
         std::vector<double4> ents;
-        std::vector<double> bcx(nblk), bcy(nblk), bcz(nblk), brad(nblk);
-        struct DE {
-            int dof, l, p;
-        };
-        std::vector<DE> dl;
-        for (int b = 0; b < nblk; ++b) {
-            dl.clear();
-            Vec3 cs;
-            int cnt = 0;
-            for (int l = 0; l < BS; ++l) {
-                const int f = bfac[b * BS + l];
-                if (f < 0) continue;
-                cs = cs + cen[f];
-                ++cnt;
-                for (int p = U.ptr[f]; p < U.ptr[f + 1]; ++p) dl.push_back({U.dof[p], l, p});
-            }
-            const Vec3 cc = cs / (double)cnt;
-            double R = 0;
-            for (int l = 0; l < BS; ++l) {
-                const int f = bfac[b * BS + l];
-                if (f >= 0) R = std::max(R, norm(cen[f] - cc));
-            }
-            bcx[b] = cc.x;
-            bcy[b] = cc.y;
-            bcz[b] = cc.z;
-            brad[b] = R;
-            std::sort(dl.begin(), dl.end(),
-                      [](const DE& x, const DE& y) { return x.dof != y.dof ? x.dof < y.dof : x.l < y.l; });
-            for (size_t i = 0; i < dl.size(); ++i) {
-                if (i == 0 || dl[i].dof != dl[i - 1].dof) {
-                    dofs.push_back(dl[i].dof);
-                    ent_ptr.push_back((int)ents.size());
-                }
-                const int p = dl[i].p;
-                ents.push_back(make_double4(U.u[3 * p], U.u[3 * p + 1], U.u[3 * p + 2], (double)dl[i].l));
-            }
-            dof_ptr.push_back((int)dofs.size());
+        dof_ptr.reserve((size_t)nblk + 1);
+        for (const auto& q : parts) {
+            const int ebase = (int)ents.size();
+            for (int c : q.ent_ptr) ent_ptr.push_back(ebase + c);
+            for (int nd : q.ndofs) dof_ptr.push_back(dof_ptr.back() + nd);
+            dofs.insert(dofs.end(), q.dofs.begin(), q.dofs.end());
+            ents.insert(ents.end(), q.ents.begin(), q.ents.end());
         }
         ent_ptr.push_back((int)ents.size());
         HostScope hs2(ctx, "plan_tiles");
@@ -1530,17 +1622,21 @@ AssemblyPlan* assembly_plan_create(Ctx* ctx, const InflatedMesh& im, const QuadC
         // launch order: full-cost tiles first (certain-far, off-diagonal), then the tiles with
         // per-pair tests and near pairs skipped, diagonal (half) tiles last, so the grid's
         // last wave holds the cheapest tiles (stable: fb-major within each class)
-        std::stable_sort(tiles.begin(), tiles.end(), [](const TileInfo& x, const TileInfo& y) {
-            auto rank = [](const TileInfo& t) { return t.fb == t.gb ? 2 : (t.certain_far ? 0 : 1); };
-            return rank(x) < rank(y);
-        });
-        P->bfac.upload(bfac, s);
-        P->dof_ptr.upload(dof_ptr, s);
-        P->dofs.upload(dofs, s);
-        P->ent_ptr.upload(ent_ptr, s);
-        P->ents.upload(ents, s);
-        P->tiles.upload(tiles, s);
-        P->cand.upload(cand, s);
+        {  // = stable_sort by class: three buckets filled in generation order
+            std::vector<TileInfo> sorted;
+            sorted.reserve(tiles.size());
+            for (int r = 0; r < 3; ++r)
+                for (const TileInfo& t : tiles)
+                    if ((t.fb == t.gb ? 2 : (t.certain_far ? 0 : 1)) == r) sorted.push_back(t);
+            tiles.swap(sorted);
+        }
+        st.upload(P->bfac, bfac);
+        st.upload(P->dof_ptr, dof_ptr);
+        st.upload(P->dofs, dofs);
+        st.upload(P->ent_ptr, ent_ptr);
+        st.upload(P->ents, ents);
+        st.upload(P->tiles, tiles);
+        st.upload(P->cand, cand);
         P->ntiles = (long long)tiles.size();
         P->ncand = (long long)cand.size();
         HostScope hs3(ctx, "plan_singular");
@@ -1560,9 +1656,8 @@ AssemblyPlan* assembly_plan_create(Ctx* ctx, const InflatedMesh& im, const QuadC
         for (int cls = 1; cls <= 3; ++cls) {
             const long long np = P->cls_cnt[cls];
             if (!np) continue;
-            SBG_CUDA(cudaMemcpyAsync(P->loc_pairs.p + P->cls_off[cls], S.pairs[cls].data(), np * sizeof(int2),
-                                     cudaMemcpyHostToDevice, s));
-            P->pv[cls].upload(S.pv[cls], s);
+            st.raw(P->loc_pairs.p + P->cls_off[cls], S.pairs[cls].data(), np * sizeof(int2));
+            st.upload(P->pv[cls], S.pv[cls]);
             sauter_chunking(ctx, cls, (int)np, P->SR->npts[cls], P->schunk[cls], P->schunks[cls]);
             P->spart[cls].alloc((size_t)P->schunks[cls] * np);
         }
@@ -1576,6 +1671,7 @@ AssemblyPlan* assembly_plan_create(Ctx* ctx, const InflatedMesh& im, const QuadC
                        bytes(P->tiles) + bytes(P->cand) + P->nsing * (long long)sizeof(int2);
         for (int cls = 1; cls <= 3; ++cls) P->h2d_bytes += bytes(P->pv[cls]);
     } catch (...) {
+        cudaStreamSynchronize(ctx->stream);  // staged copies may still read the arena
         delete P;
         throw;
     }
@@ -1769,7 +1865,7 @@ void pair_integrals(Ctx* ctx, const SurfaceMesh& m, const QuadCfg& cfg, const in
     cudaStream_t s = ctx->stream;
     const RuleDims R = upload_rules(ctx, cfg);
     DeviceGeometry G;
-    upload_geometry(ctx, m, G);
+    upload_geometry(ctx, m, G, nullptr);
     const SauterRulesDev& SR = *device_sauter(ctx, cfg);
     std::vector<double> hgc(3 * (size_t)m.num_facets()), hrad(m.num_facets()), hdiam(m.num_facets());
     SBG_CUDA(cudaMemcpyAsync(hgc.data(), G.c.p, hgc.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
@@ -1887,7 +1983,7 @@ void assemble_rhs(Ctx* ctx, const InflatedMesh& im, const QuadCfg& cfg, const do
         if (!std::isfinite(g[i])) throw NumericalError("g returned a non-finite value");
     upload_rules(ctx, cfg);
     DeviceGeometry G;
-    upload_geometry(ctx, m, G);
+    upload_geometry(ctx, m, G, nullptr);
     // scatter terms per (oriented facet, slot) (assemble.hpp:34-53)
     std::vector<int> sptr{0}, sdof;
     std::vector<double> ssgn, onorm(6 * (size_t)nf);
