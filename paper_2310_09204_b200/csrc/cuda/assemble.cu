@@ -1080,7 +1080,7 @@ struct Stager {
                 if (A->p) SBG_CUDA(cudaFreeHost(A->p));
                 A->p = nullptr;
                 A->cap = 0;
-                const size_t cap = std::max(bytes, (size_t)16 << 20);
+                const size_t cap = std::max(bytes, (size_t)64 << 20);
                 SBG_CUDA(cudaHostAlloc((void**)&A->p, cap, cudaHostAllocDefault));
                 A->cap = cap;
             }
@@ -1184,7 +1184,29 @@ void singular_pairs(const SurfaceMesh& m, SingularLists& S)
             }
         }
     };
-    range(0, nf, S);  // runs beside the plan's main thread (assembly_plan_create)
+    // runs beside the plan's main thread (assembly_plan_create); facet ranges on a few
+    // threads, each class list concatenated in range order (= the single-pass lists)
+    const int nt = std::max(1, std::min(4, nf / 2048));
+    if (nt == 1) {
+        range(0, nf, S);
+        return;
+    }
+    std::vector<SingularLists> parts(nt);
+    std::vector<std::thread> th;
+    for (int t = 1; t < nt; ++t)
+        th.emplace_back(range, (int)((long long)nf * t / nt), (int)((long long)nf * (t + 1) / nt), std::ref(parts[t]));
+    range(0, (int)((long long)nf / nt), parts[0]);
+    for (auto& t : th) t.join();
+    for (int c = 1; c <= 3; ++c) {
+        size_t np = 0;
+        for (const auto& q : parts) np += q.pairs[c].size();
+        S.pairs[c].reserve(np);
+        S.pv[c].reserve(6 * np);
+        for (const auto& q : parts) {
+            S.pairs[c].insert(S.pairs[c].end(), q.pairs[c].begin(), q.pairs[c].end());
+            S.pv[c].insert(S.pv[c].end(), q.pv[c].begin(), q.pv[c].end());
+        }
+    }
 }
 
 struct SauterRulesDev {
@@ -1467,9 +1489,99 @@ struct AssemblyPlan {
     DBuf<double> loc_I;
     DBuf<unsigned long long> near_cnt;
     DBuf<int> bad;  // non-finite flag of the mirror pass
+    // deferred curl-dependent half (plan_finish)
+    std::unique_ptr<Stager> st;
+    std::future<FacetCurls> curl_fut;
+    std::vector<int> bfac_h;
+    bool pending = false;
 };
+void plan_finish(AssemblyPlan* P);
 
-AssemblyPlan* assembly_plan_create(Ctx* ctx, const InflatedMesh& im, const QuadCfg& cfg)
+// The curl-dependent half of a plan: curl lists (helper thread) and the per-block DOF
+// lists of the far-tile contraction, uploaded through the plan's staging arena.
+void plan_finish(AssemblyPlan* P)
+{
+    if (!P->pending) return;
+    P->pending = false;
+    Ctx* ctx = P->ctx;
+    Stager& st = *P->st;
+    const std::vector<int>& bfac = P->bfac_h;
+    const int nblk = (int)(bfac.size() / BS);
+    std::optional<HostScope> hs_wait(std::in_place, ctx, "plan_curl_wait");
+    const FacetCurls U = P->curl_fut.get();
+    hs_wait.reset();
+    {
+        HostScope hsu(ctx, "plan_upload_curls");
+        st.upload(P->uptr, U.ptr);
+        st.upload(P->udof, U.dof);
+        st.upload(P->uval, U.u);
+    }
+    struct BlockLists {
+        std::vector<int> dofs, ent_ptr, ndofs;
+        std::vector<double4> ents;
+    };
+    auto build_blocks = [&](int b0, int b1, BlockLists& out) {
+        struct DE {
+            int dof, l, p;
+        };
+        std::vector<DE> dl;
+        for (int b = b0; b < b1; ++b) {
+            dl.clear();
+            for (int l = 0; l < BS; ++l) {
+                const int f = bfac[b * BS + l];
+                if (f < 0) continue;
+                for (int p = U.ptr[f]; p < U.ptr[f + 1]; ++p) dl.push_back({U.dof[p], l, p});
+            }
+            std::sort(dl.begin(), dl.end(),
+                      [](const DE& x, const DE& y) { return x.dof != y.dof ? x.dof < y.dof : x.l < y.l; });
+            int nd = 0;
+            for (size_t i = 0; i < dl.size(); ++i) {
+                if (i == 0 || dl[i].dof != dl[i - 1].dof) {
+                    out.dofs.push_back(dl[i].dof);
+                    out.ent_ptr.push_back((int)out.ents.size());
+                    ++nd;
+                }
+                const int p = dl[i].p;
+                out.ents.push_back(make_double4(U.u[3 * p], U.u[3 * p + 1], U.u[3 * p + 2], (double)dl[i].l));
+            }
+            out.ndofs.push_back(nd);
+        }
+    };
+    const int nth = std::max(1, std::min(4, nblk / 32));
+    std::vector<BlockLists> parts(nth);
+    {
+        HostScope hsb(ctx, "plan_blocks");
+        std::vector<std::thread> th;
+        for (int t = 1; t < nth; ++t)
+            th.emplace_back(build_blocks, (int)((long long)nblk * t / nth), (int)((long long)nblk * (t + 1) / nth),
+                            std::ref(parts[t]));
+        build_blocks(0, (int)((long long)nblk / nth), parts[0]);
+        for (auto& t : th) t.join();
+    }
+    std::vector<int> dof_ptr{0}, dofs, ent_ptr;
+    std::vector<double4> ents;
+    dof_ptr.reserve((size_t)nblk + 1);
+    for (const auto& q : parts) {
+        const int ebase = (int)ents.size();
+        for (int c : q.ent_ptr) ent_ptr.push_back(ebase + c);
+        for (int nd : q.ndofs) dof_ptr.push_back(dof_ptr.back() + nd);
+        dofs.insert(dofs.end(), q.dofs.begin(), q.dofs.end());
+        ents.insert(ents.end(), q.ents.begin(), q.ents.end());
+    }
+    ent_ptr.push_back((int)ents.size());
+    st.upload(P->dof_ptr, dof_ptr);
+    st.upload(P->dofs, dofs);
+    st.upload(P->ent_ptr, ent_ptr);
+    st.upload(P->ents, ents);
+    // host-to-device bytes of this plan (e2e bookkeeping; rules are cached per context)
+    auto bytes = [](const auto& b) { return (long long)(b.n * sizeof(*b.p)); };
+    P->h2d_bytes = bytes(P->G.X) + bytes(P->G.F) + bytes(P->uptr) + bytes(P->udof) + bytes(P->uval) +
+                   bytes(P->bfac) + bytes(P->dof_ptr) + bytes(P->dofs) + bytes(P->ent_ptr) + bytes(P->ents) +
+                   bytes(P->tiles) + bytes(P->cand) + P->nsing * (long long)sizeof(int2);
+    for (int cls = 1; cls <= 3; ++cls) P->h2d_bytes += bytes(P->pv[cls]);
+}
+
+AssemblyPlan* assembly_plan_create(Ctx* ctx, const InflatedMesh& im, const QuadCfg& cfg, bool defer)
 {
     HostScope hs_all(ctx, "plan_total");
     auto* P = new AssemblyPlan;
@@ -1490,7 +1602,8 @@ AssemblyPlan* assembly_plan_create(Ctx* ctx, const InflatedMesh& im, const QuadC
             return S;
         });
         auto curl_fut = std::async(std::launch::async, [&im] { return facet_curls(im); });
-        Stager st(ctx);
+        P->st = std::make_unique<Stager>(ctx);
+        Stager& st = *P->st;
         P->dims = upload_rules(ctx, cfg);
         upload_geometry(ctx, m, P->G, &st);
         HostScope hs1(ctx, "plan_curls");
@@ -1521,88 +1634,35 @@ AssemblyPlan* assembly_plan_create(Ctx* ctx, const InflatedMesh& im, const QuadC
         std::iota(perm.begin(), perm.end(), 0);
         std::stable_sort(perm.begin(), perm.end(), [&](int a, int b) { return key[a] < key[b]; });
         hs_morton.reset();
-        std::optional<HostScope> hs_wait(std::in_place, ctx, "plan_curl_wait");
-        const FacetCurls U = curl_fut.get();
-        hs_wait.reset();
-        {
-            HostScope hsu(ctx, "plan_upload_curls");
-            st.upload(P->uptr, U.ptr);
-            st.upload(P->udof, U.dof);
-            st.upload(P->uval, U.u);
-        }
         const int nblk = (nf + BS - 1) / BS;
         std::vector<int> bfac((size_t)nblk * BS, -1);
         for (int k = 0; k < nf; ++k) bfac[k] = perm[k];
         std::vector<double> bcx(nblk), bcy(nblk), bcz(nblk), brad(nblk);
-        // per block: centre, radius and the DOF-sorted curl entries; blocks are independent,
-        // built on a few threads over contiguous block ranges and concatenated in block order
-        struct BlockLists {
-            std::vector<int> dofs, ent_ptr, ndofs;
-            std::vector<double4> ents;
-        };
-        auto build_blocks = [&](int b0, int b1, BlockLists& out) {
-            struct DE {
-                int dof, l, p;
-            };
-            std::vector<DE> dl;
-            for (int b = b0; b < b1; ++b) {
-                dl.clear();
-                Vec3 cs;
-                int cnt = 0;
-                for (int l = 0; l < BS; ++l) {
-                    const int f = bfac[b * BS + l];
-                    if (f < 0) continue;
-                    cs = cs + cen[f];
-                    ++cnt;
-                    for (int p = U.ptr[f]; p < U.ptr[f + 1]; ++p) dl.push_back({U.dof[p], l, p});
-                }
-                const Vec3 cc = cs / (double)cnt;
-                double R = 0;
-                for (int l = 0; l < BS; ++l) {
-                    const int f = bfac[b * BS + l];
-                    if (f >= 0) R = std::max(R, norm(cen[f] - cc));
-                }
-                bcx[b] = cc.x;
-                bcy[b] = cc.y;
-                bcz[b] = cc.z;
-                brad[b] = R;
-                std::sort(dl.begin(), dl.end(),
-                          [](const DE& x, const DE& y) { return x.dof != y.dof ? x.dof < y.dof : x.l < y.l; });
-                int nd = 0;
-                for (size_t i = 0; i < dl.size(); ++i) {
-                    if (i == 0 || dl[i].dof != dl[i - 1].dof) {
-                        out.dofs.push_back(dl[i].dof);
-                        out.ent_ptr.push_back((int)out.ents.size());
-                        ++nd;
-                    }
-                    const int p = dl[i].p;
-                    out.ents.push_back(make_double4(U.u[3 * p], U.u[3 * p + 1], U.u[3 * p + 2], (double)dl[i].l));
-                }
-                out.ndofs.push_back(nd);
+        for (int b = 0; b < nblk; ++b) {  // block centres and radii (the tile classification)
+            Vec3 cs;
+            int cnt = 0;
+            for (int l = 0; l < BS; ++l) {
+                const int f = bfac[b * BS + l];
+                if (f < 0) continue;
+                cs = cs + cen[f];
+                ++cnt;
             }
-        };
-        const int nth = std::max(1, std::min(4, nblk / 32));
-        std::vector<BlockLists> parts(nth);
-        {
-            HostScope hsb(ctx, "plan_blocks");
-            std::vector<std::thread> th;
-            for (int t = 1; t < nth; ++t)
-                th.emplace_back(build_blocks, (int)((long long)nblk * t / nth), (int)((long long)nblk * (t + 1) / nth),
-                                std::ref(parts[t]));
-            build_blocks(0, (int)((long long)nblk / nth), parts[0]);
-            for (auto& t : th) t.join();
+            const Vec3 cc = cs / (double)cnt;
+            double R = 0;
+            for (int l = 0; l < BS; ++l) {
+                const int f = bfac[b * BS + l];
+                if (f >= 0) R = std::max(R, norm(cen[f] - cc));
+            }
+            bcx[b] = cc.x;
+            bcy[b] = cc.y;
+            bcz[b] = cc.z;
+            brad[b] = R;
         }
-        std::vector<int> dof_ptr{0}, dofs, ent_ptr;
-        std::vector<double4> ents;
-        dof_ptr.reserve((size_t)nblk + 1);
-        for (const auto& q : parts) {
-            const int ebase = (int)ents.size();
-            for (int c : q.ent_ptr) ent_ptr.push_back(ebase + c);
-            for (int nd : q.ndofs) dof_ptr.push_back(dof_ptr.back() + nd);
-            dofs.insert(dofs.end(), q.dofs.begin(), q.dofs.end());
-            ents.insert(ents.end(), q.ents.begin(), q.ents.end());
-        }
-        ent_ptr.push_back((int)ents.size());
+        // the curl-dependent half (curl lists, per-block DOF lists) waits for the helper
+        // thread; a deferred plan (one-shot assemble_W) runs it after the near-field launches
+        P->curl_fut = std::move(curl_fut);
+        P->bfac_h = bfac;
+        P->pending = true;
         HostScope hs2(ctx, "plan_tiles");
         // ---- tiles (fb >= gb); certainly-far tiles skip per-pair classification
         const double thr = cfg.near_threshold;
@@ -1631,17 +1691,15 @@ AssemblyPlan* assembly_plan_create(Ctx* ctx, const InflatedMesh& im, const QuadC
             tiles.swap(sorted);
         }
         st.upload(P->bfac, bfac);
-        st.upload(P->dof_ptr, dof_ptr);
-        st.upload(P->dofs, dofs);
-        st.upload(P->ent_ptr, ent_ptr);
-        st.upload(P->ents, ents);
         st.upload(P->tiles, tiles);
         st.upload(P->cand, cand);
         P->ntiles = (long long)tiles.size();
         P->ncand = (long long)cand.size();
         HostScope hs3(ctx, "plan_singular");
         // ---- singular lists (host adjacency, deterministic order) and Sauter workspaces
+        std::optional<HostScope> hs_sw(std::in_place, ctx, "plan_singular_wait");
         SingularLists S = sing_fut.get();
+        hs_sw.reset();
         P->SR = device_sauter(ctx, cfg);
         P->near_cap = std::max<long long>(1024, 64LL * nf);
         long long off = 0;
@@ -1663,13 +1721,9 @@ AssemblyPlan* assembly_plan_create(Ctx* ctx, const InflatedMesh& im, const QuadC
         }
         P->near_cnt.alloc(1);
         P->bad.alloc(1);
+        if (!defer) plan_finish(P);
+        HostScope hs_sync(ctx, "plan_sync");
         SBG_CUDA(cudaStreamSynchronize(s));
-        // host-to-device bytes of this plan (e2e bookkeeping; rules are cached per context)
-        auto bytes = [](const auto& b) { return (long long)(b.n * sizeof(*b.p)); };
-        P->h2d_bytes = bytes(P->G.X) + bytes(P->G.F) + bytes(P->uptr) + bytes(P->udof) + bytes(P->uval) +
-                       bytes(P->bfac) + bytes(P->dof_ptr) + bytes(P->dofs) + bytes(P->ent_ptr) + bytes(P->ents) +
-                       bytes(P->tiles) + bytes(P->cand) + P->nsing * (long long)sizeof(int2);
-        for (int cls = 1; cls <= 3; ++cls) P->h2d_bytes += bytes(P->pv[cls]);
     } catch (...) {
         cudaStreamSynchronize(ctx->stream);  // staged copies may still read the arena
         delete P;
@@ -1719,6 +1773,8 @@ void assembly_run(AssemblyPlan* P, DMatrix& W, AssemblyStats* stats, int rank, i
         }
         leaves = run_near(ctx, R, P->G.v.p, P->G.area.p, P->loc_pairs.p + P->nsing, P->near_cnt.p, P->near_cap, thr,
                           P->loc_I.p + P->nsing, near_work(ctx), rank, world, &near_owned);
+        // a deferred plan builds its curl-dependent half while the near-field leaves run
+        plan_finish(P);
         SBG_CUDA(cudaMemcpyAsync(&nnear, P->near_cnt.p, sizeof(nnear), cudaMemcpyDeviceToHost, s));
         SBG_CUDA(cudaStreamSynchronize(s));
         if ((long long)nnear <= P->near_cap) break;
@@ -1791,7 +1847,7 @@ void assembly_run(AssemblyPlan* P, DMatrix& W, AssemblyStats* stats, int rank, i
 
 void assemble_W(Ctx* ctx, const InflatedMesh& im, const QuadCfg& cfg, DMatrix& W, AssemblyStats* stats)
 {
-    AssemblyPlan* P = assembly_plan_create(ctx, im, cfg);
+    AssemblyPlan* P = assembly_plan_create(ctx, im, cfg, /*defer=*/true);
     try {
         assembly_run(P, W, stats);
         SBG_CUDA(cudaStreamSynchronize(ctx->stream));

@@ -128,7 +128,9 @@ struct AssemblyStats {
     long long h2d_bytes = 0;  // bytes uploaded by the plan build
 };
 struct AssemblyPlan;
-AssemblyPlan* assembly_plan_create(Ctx* ctx, const InflatedMesh& im, const QuadCfg& cfg);
+// defer: leave the curl-dependent half (plan_finish) to the first assembly_run, which builds
+// it on the host while the near-field kernels run (the one-shot assemble_W)
+AssemblyPlan* assembly_plan_create(Ctx* ctx, const InflatedMesh& im, const QuadCfg& cfg, bool defer = false);
 void assembly_plan_destroy(AssemblyPlan* p);
 // (rank, world): one shard of the work (world 1 = the whole assembly), see assemble.cu
 void assembly_run(AssemblyPlan* p, DMatrix& W, AssemblyStats* stats, int rank = 0, int world = 1);

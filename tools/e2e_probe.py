@@ -38,7 +38,7 @@ def main():
         W2 = S.assemble_W(im, ctx=ctx)
         Wh2 = W2.download()
         t5 = time.perf_counter()
-        tm = {k: ctx.timer(k)[0] for k in ("plan_total", "plan_morton", "plan_curl_wait", "plan_upload_curls", "plan_blocks", "plan_curls", "plan_tiles", "plan_singular", "assemble_W")}
+        tm = {k: ctx.timer(k)[0] for k in ("plan_total", "plan_morton", "plan_curl_wait", "plan_upload_curls", "plan_blocks", "plan_curls", "plan_tiles", "plan_singular", "plan_singular_wait", "plan_sync", "assemble_W")}
         rows.append((t1 - t0, t2 - t1, t3 - t2, t5 - t4, tm))
         del W, Wh, W2, Wh2, plan
     for p, a, d, e, tm in rows:
