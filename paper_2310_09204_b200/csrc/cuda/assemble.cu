@@ -1150,6 +1150,13 @@ void singular_pairs(const SurfaceMesh& m, SingularLists& S)
             for (int k = 0; k < 3; ++k) sfac[fill[m.facets[f][k]]++] = f;
     }
     auto range = [&](int f0, int f1, SingularLists& L) {
+        // reserve for a regular triangulation: 1 identical, 1.5 edge, 4.5 vertex pairs per facet
+        const size_t nfr = (size_t)(f1 - f0);
+        const size_t est[4] = {0, 5 * nfr, 2 * nfr, nfr + 16};
+        for (int c = 1; c <= 3; ++c) {
+            L.pairs[c].reserve(est[c]);
+            L.pv[c].reserve(6 * est[c]);
+        }
         std::vector<int> nb;
         for (int f = f0; f < f1; ++f) {
             nb.clear();
@@ -1186,7 +1193,7 @@ void singular_pairs(const SurfaceMesh& m, SingularLists& S)
     };
     // runs beside the plan's main thread (assembly_plan_create); facet ranges on a few
     // threads, each class list concatenated in range order (= the single-pass lists)
-    const int nt = std::max(1, std::min(4, nf / 2048));
+    const int nt = std::max(1, std::min(8, nf / 1024));
     if (nt == 1) {
         range(0, nf, S);
         return;
