@@ -292,6 +292,28 @@ inline PcgReport pcg(Context& ctx, const GalerkinMatrix& W, const SchwarzPrecond
     return rep;
 }
 
+// pcg with one GPU per worker: this process computes rows [lo, hi) of each
+// W p; `exchange` enqueues the all-gather of the other rows on the given stream (e.g. NCCL
+// over NVLink).  Same result as pcg on every rank.
+inline PcgReport pcg_rows(Context& ctx, const GalerkinMatrix& W, const SchwarzPreconditioner* prec,
+                          const std::vector<double>& rhs, int lo, int hi, sbg_exchange_fn exchange, void* user,
+                          double tol = 1e-8, int maxit = 0)
+{
+    const int n = (int)rhs.size();
+    const int cap = (maxit > 0 ? maxit : std::max(10 * n, 100)) + 2;
+    PcgReport rep;
+    rep.solution.assign(n, 0.0);
+    rep.residual_history.assign(cap, 0.0);
+    sbg_pcg_report r{};
+    check(sbg_pcg_rows(ctx.get(), W.get(), prec ? prec->get() : nullptr, rhs.data(), n, 0, tol, maxit, lo, hi,
+                       exchange, user, rep.solution.data(), rep.residual_history.data(), nullptr, nullptr, cap, &r));
+    rep.iterations = r.iterations;
+    rep.converged = r.converged != 0;
+    rep.kappa_estimate = r.kappa_estimate;
+    rep.residual_history.resize(r.history_len);
+    return rep;
+}
+
 // reference: inc/schwarz.hpp:142-148 — M stays on the device (download() for a host copy)
 inline GalerkinMatrix materialize_preconditioner(Context& ctx, const SchwarzPreconditioner& P)
 {

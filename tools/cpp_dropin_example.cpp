@@ -9,6 +9,19 @@
 
 namespace sb = screenbem::gpu;
 
+// row-panel PCG exchange of "rank 1 of 2", emulated in one process: the other panel's
+// rows of W p are computed here on the same stream (a real run all-gathers them over NCCL)
+struct Emul {
+    sbg_ctx* ctx;
+    const sbg_matrix* W;
+    int lo, hi;
+};
+static int emulated_exchange(void* user, const double* d_p, double* d_y, int, void*)
+{
+    const Emul* e = static_cast<const Emul*>(user);
+    return sbg_matvec_rows_device(e->ctx, e->W, d_p, d_y, e->lo, e->hi);
+}
+
 int main(int argc, char** argv)
 {
     const int cfg = argc > 1 ? std::atoi(argv[1]) : 1;
@@ -37,6 +50,12 @@ int main(int argc, char** argv)
             wmax = std::max(wmax, std::fabs(Wh[k]));
         }
         std::printf("shard_sum_rel %.3e\n", dmax / wmax);
+        const int half = (W.rows() + 1) / 2;
+        Emul em{ctx.get(), W.get(), 0, half};
+        const sb::PcgReport rr = sb::pcg_rows(ctx, W, &P, L, half, W.rows(), emulated_exchange, &em, 1e-8);
+        double xd = 0.0;
+        for (size_t k = 0; k < rr.solution.size(); ++k) xd = std::max(xd, std::fabs(rr.solution[k] - rep.solution[k]));
+        std::printf("rows_iterations %d rows_max_dx %.3e\n", rr.iterations, xd);
         return rep.converged ? 0 : 3;
     } catch (const screenbem::ValidationError& e) {
         std::fprintf(stderr, "validation error: %s\n", e.what());
