@@ -2,16 +2,23 @@
 
 A step is one pass of the hot path over the config's synthetic mesh: assemble_W,
 assemble_rhs, build_preconditioner and PCG to 1e-8 (inc/experiments.hpp:130-145).
+Default workload: config 5 (flat 160x160, 25 281 DOFs, 5.1 GB W) at H/h 8 — the largest
+BASELINE config, which fits one B200.
   value : assembly triangle-pairs/s (nf(nf+1)/2 per assembly) with the mesh-derived
           data resident in HBM (AssemblyPlan built before the timed region),
-          device time from CUDA events, max over ranks, x N ranks (replicas);
+          device time from CUDA events, max over ranks;
   e2e   : the same metric through the public assemble_W call (host mesh in, host W
           out: plan build + H2D + kernels + D2H of the n x n matrix), the drop-in for
-          the reference's assemble_W (inc/assemble.hpp:72-139);
+          the reference's assemble_W (inc/assemble.hpp:72-139); median over runs;
+  tts_e2e_ms: time to solution through the public API, host mesh pair -> host x
+          (inflate, partition, prolongation, plan, assembly, RHS, preconditioner, PCG);
   extras: PCG iterations/s, matvec GB/s (HBM roofline), preconditioner applies/s,
-          time-to-solution, per-phase device times.
---impl reference runs the CPU restatement of the reference's assemble_W
-(oracle/, all host threads, run_partitioned semantics) on a bounded sample.
+          per-phase device times.
+--gpus N without a launcher re-executes itself under torch.distributed.run with N ranks
+(one GPU each).  N > 1 assembles ONE W across the ranks (strong scaling) unless
+--replicas.  --impl reference times the CPU restatement of the reference's assemble_W
+(oracle/, all host threads, run_partitioned semantics) on an unbiased sample of the pair
+space; it never loads the product library.
 """
 from __future__ import annotations
 
@@ -28,9 +35,9 @@ sys.path.insert(0, ROOT)
 
 METRIC = "assembly tri-pairs/s; PCG iters/s & matvec GB/s vs HBM peak (fp64, 1 B200)"
 UNIT = "tri-pairs/s"
-CFG_NAMES = {1: "flat 16x16 (512 tri), H/h 8", 2: "flat 64x64 (8192 tri), H/h 16",
-             3: "T-junction 3x48x48 (13824 tri), H/h 12", 4: "triple cross 3x64x64 (24576 tri), H/h 8",
-             5: "flat 160x160 (51200 tri)"}
+CFG_NAMES = {1: "flat 16x16 (512 tri)", 2: "flat 64x64 (8192 tri)", 3: "T-junction 3x48x48 (13824 tri)",
+             4: "triple cross 3x64x64 (24576 tri)", 5: "flat 160x160 (51200 tri)"}
+DEFAULT_RATIO = {1: 8, 2: 16, 3: 12, 4: 8, 5: 8}   # BASELINE.json configs (H/h)
 
 
 def parse():
@@ -46,15 +53,17 @@ def parse():
     ap.add_argument("--no-cpu-phases", action="store_true",
                     help="skip the CPU restatement's setup/preconditioner/PCG timings")
     ap.add_argument("--cpu-phases-max-n", type=int, default=8000)
-    ap.add_argument("--config", type=int, default=2)
-    ap.add_argument("--ratio", type=int, default=0, help="H/h for config 5 (default 8)")
+    ap.add_argument("--config", type=int, default=5)
+    ap.add_argument("--ratio", type=int, default=0, help="H/h (default: the config's, 8 for config 5)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU sample length")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo: functional check of the N>1 paths (ranks may share one GPU; not a timing)")
-    ap.add_argument("--shard", action="store_true",
-                    help="N>1: assemble ONE W across the ranks (1/N of the pair work each, NCCL all-reduce "
-                         "of the partial W), strong scaling; default is N independent replicas")
+    ap.add_argument("--replicas", action="store_true",
+                    help="N>1: N independent replicas of the whole step (weak scaling) instead of one W "
+                         "assembled across the ranks")
+    ap.add_argument("--shard", action="store_true", help="(default for N>1) one W across the ranks")
+    ap.add_argument("--tts-runs", type=int, default=3, help="time-to-solution runs (median reported)")
     return ap.parse_args()
 
 
@@ -193,44 +202,78 @@ class ClockSampler:
 
 
 # --------------------------------------------------------------------------- CPU restatement (oracle)
-def cpu_assembly_sample(cfg: int, ratio: int, target_s: float):
-    """Reference assemble_W restated in oracle/ (CPU, all host threads, contiguous
-    pair ranges + per-worker dense partials as in inc/assemble.hpp:91-133) on the
-    last rows of the reference's pair ordering (rows ff cover all partners g <= ff)."""
-    from oracle import oracle as O
-    from paper_2310_09204_b200 import screenbem as S
-    pair = S.make_config(cfg, ratio)
-    m = O.Mesh(pair.fine.vertices, pair.fine.facets)
-    im = O.inflate(m, validate=False)
-    nf = m.nf
-    workers = os.cpu_count() or 1
-    n = im.n
-    # per-worker dense partials are n^2 doubles (assemble.hpp:92-96): cap workers by RAM
+def host_ram_bytes() -> int:
     try:
-        ram = os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_PHYS_PAGES")
-        workers = max(1, min(workers, int(0.5 * ram // max(8 * n * n, 1))))
+        with open("/proc/meminfo") as f:
+            for line in f:
+                if line.startswith("MemAvailable:"):
+                    return int(line.split()[1]) * 1024
     except Exception:
         pass
-    total = nf * (nf + 1) // 2
+    return os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_PHYS_PAGES")
 
-    def run_rows(k):
-        lo = total - sum(nf - i for i in range(k))  # last k rows ff = nf-k .. nf-1
-        t0 = time.perf_counter()
-        O.assemble_W(im, workers=workers, pair_range=(lo, total))
-        return total - lo, time.perf_counter() - t0
 
-    # calibrate the per-row cost net of the fixed per-call cost (zeroing the
-    # per-worker n x n partials and their ordered sum), then take a sample of
-    # about target_s seconds
-    k1, k2 = max(1, workers), 4 * max(1, workers)
-    _, t1 = run_rows(k1)
-    _, t2 = run_rows(k2)
-    per_row = max((t2 - t1) / (k2 - k1), 1e-6)
-    k = max(k2, min(nf, int(target_s / per_row)))
-    pairs, t = run_rows(k)
-    return {"value": pairs / t, "unit": UNIT, "cores": workers, "kind": "port",
-            "sample": f"oracle assemble_W on the last {k} pair rows ({pairs} of {total} pairs) of config {cfg}, "
-                      f"{t:.1f} s", "seconds": t, "pairs": pairs}
+def config_dict(cfg: int, ratio: int, nf: int, n: int) -> dict:
+    """The workload, identical in both arms (the driver compares them)."""
+    return {"workload": f"config {cfg}: {CFG_NAMES[cfg]}, H/h {ratio}", "triangles": nf, "dofs": n,
+            "tri_pairs": nf * (nf + 1) // 2, "h_ratio": ratio, "pcg_tol": 1e-8}
+
+
+class CpuAssembly:
+    """The reference's assemble_W restated in oracle/ on the host cores (all threads, RAM
+    permitting: each worker holds a dense n x n partial, inc/assemble.hpp:92-96), timed
+    on an unbiased bounded sample of the pair space (oracle.AssemblySampler):
+      t_full = t_call + (npairs / k) * t_loop(k systematically sampled pairs)
+    t_call = the per-call work with no pairs (partials allocated and zeroed in their
+    threads, worker-ordered sum, mirror), measured once; t_loop = the pair loop over the
+    sample split into contiguous per-worker chunks as run_partitioned splits the full
+    range (common.hpp:31-59).  value = npairs / t_full.  Meshes come from the oracle's
+    own config generator: the product library is never loaded."""
+
+    def __init__(self, cfg: int, ratio: int, target_s: float):
+        from oracle import oracle as O
+        pair = O.make_config(cfg, ratio)
+        self.im = O.inflate(pair.fine, validate=False)
+        self.nf, self.n = pair.fine.nf, self.im.n
+        self.npairs = self.nf * (self.nf + 1) // 2
+        cores = os.cpu_count() or 1
+        cap = max(1, int(0.8 * host_ram_bytes() // max(8 * self.n * self.n, 1)))
+        self.workers = max(1, min(cores, cap))
+        self.sampler = O.AssemblySampler(self.im, self.workers)
+        self.t_call = self.sampler.fixed()
+        # calibrate the per-pair cost on a small sample, then size the timed sample
+        k0 = min(self.npairs, max(2000 * self.workers, 20000))
+        t0 = self.sampler.run(O.systematic_pair_sample(self.nf, k0, seed=1))
+        self.k = int(min(self.npairs, max(k0, target_s * k0 / max(t0, 1e-9))))
+        self.idx = O.systematic_pair_sample(self.nf, self.k, seed=0)
+        self.loops = []
+
+    def step(self, timed: bool = True, short: bool = False) -> float:
+        if short:  # untimed warm-up on a small sample
+            from oracle import oracle as O
+            return self.sampler.run(O.systematic_pair_sample(self.nf, min(self.k, 20000), seed=2))
+        t = self.sampler.run(self.idx)
+        if timed:
+            self.loops.append(t)
+        return t
+
+    def summary(self) -> dict:
+        loop = sum(self.loops) / len(self.loops)
+        t_full = self.t_call + self.npairs / self.k * loop
+        return {"value": self.npairs / t_full, "unit": UNIT, "cores": self.workers, "kind": "port",
+                "sample": (f"oracle assemble_W pair loop on {self.k} of {self.npairs} pairs (systematic sample of the "
+                           f"reference pair order, seeded offset) {loop:.1f} s/step on {self.workers} threads, plus the "
+                           f"per-call work (partials, ordered sum, mirror) {self.t_call:.2f} s, measured once; "
+                           f"value = npairs / (t_call + npairs/k * t_loop) = full assemble_W {t_full:.1f} s"),
+                "seconds_full_estimate": t_full, "seconds_loop": loop, "seconds_call": self.t_call,
+                "pairs_sampled": self.k, "workers_ram_cap": self.workers < (os.cpu_count() or 1)}
+
+
+def cpu_assembly_sample(cfg: int, ratio: int, target_s: float):
+    """one timed sample (our arm's cpu_baseline leg)"""
+    ca = CpuAssembly(cfg, ratio, target_s)
+    ca.step()
+    return ca.summary()
 
 
 def cpu_model() -> str:
@@ -254,11 +297,8 @@ def cpu_phases(cfg: int, ratio: int, W_host=None, max_n: int = 8000):
     import numpy as np
 
     from oracle import oracle as O
-    from paper_2310_09204_b200 import screenbem as S
-    pair = S.make_config(cfg, ratio)
     t0 = time.perf_counter()
-    opair = O.LevelPair(O.Mesh(pair.coarse.vertices, pair.coarse.facets),
-                        O.Mesh(pair.fine.vertices, pair.fine.facets), pair.parent)
+    opair = O.make_config(cfg, ratio)
     fine, coarse = O.inflate(opair.fine, validate=False), O.inflate(opair.coarse)
     part, R = O.partition_dofs(opair, fine), O.build_prolongation(opair, coarse, fine)
     out = {"setup_s": time.perf_counter() - t0, "dofs": fine.n}
@@ -284,7 +324,7 @@ def cpu_phases(cfg: int, ratio: int, W_host=None, max_n: int = 8000):
     for _ in range(3):
         prec.apply(r)
     out["precond_apply_s"] = (time.perf_counter() - t0) / 3
-    L = O.assemble_rhs(fine, S.config_g(cfg))
+    L = O.assemble_rhs(fine, O.config_g(cfg))
     t0 = time.perf_counter()
     rep = O.pcg(W_host, prec, L, 1e-8)
     dt = time.perf_counter() - t0
@@ -298,32 +338,34 @@ def cpu_phases(cfg: int, ratio: int, W_host=None, max_n: int = 8000):
 
 def run_reference(args):
     rank, world, _ = dist_env()
-    if rank != 0:
+    if rank != 0:  # the reference is the CPU path: rank 0 alone runs and prints it
         return
     cfg = args.config
-    samples = []
-    # timed steps: the same sample as our arm's cpu_baseline (the whole W when it takes about
-    # cpu_seconds or less: config 2 is assembled in full, since the last rows alone are
-    # dominated by far pairs and run faster per pair than the whole matrix); warm-up steps
-    # are short untimed samples
-    per_step = max(4.0, min(args.cpu_seconds, 150.0 / max(args.steps, 1)))  # whole run within a few minutes
-    for i in range(args.warmup + args.steps):
-        r = cpu_assembly_sample(cfg, args.ratio, per_step if i >= args.warmup else 1.0)
-        if i >= args.warmup:
-            samples.append(r)
-    v = sum(s["pairs"] for s in samples) / sum(s["seconds"] for s in samples)
+    ratio = args.ratio or DEFAULT_RATIO[cfg]
+    # each timed step: the pair loop over the same unbiased sample, sized so the whole run
+    # stays within a few minutes
+    per_step = max(3.0, min(args.cpu_seconds, 150.0 / max(args.steps, 1)))
+    ca = CpuAssembly(cfg, ratio, per_step)
+    for _ in range(args.warmup):
+        ca.step(timed=False, short=True)
+    for _ in range(args.steps):
+        ca.step()
+    cb = ca.summary()
+    v = cb["value"]
     phases = None
     if not args.no_cpu_phases:
         try:
-            phases = cpu_phases(cfg, args.ratio or (8 if cfg == 5 else 0), None, max_n=args.cpu_phases_max_n)
+            phases = cpu_phases(cfg, ratio, None, max_n=args.cpu_phases_max_n)
         except Exception as e:  # pragma: no cover
             phases = {"failed": str(e)}
+    cb["phases"] = phases
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(s["seconds"] for s in samples) / len(samples),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"config {cfg}: {CFG_NAMES[cfg]}", "sample": samples[-1]["sample"]},
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": samples[-1]["cores"], "kind": "port",
-                             "sample": samples[-1]["sample"], "phases": phases},
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(ca.loops) / len(ca.loops),
+            "higher_is_better": True, "scaling": "strong" if args.gpus > 1 and not args.replicas else "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": config_dict(cfg, ratio, ca.nf, ca.n),
+            "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample", "phases")},
+            "cpu_model": cpu_model(),
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -378,7 +420,7 @@ def run_ours(args):
         allreduce_sum_(t, dist, rdev)
     ctx.timers(True)
     cfg = args.config
-    ratio = args.ratio if args.ratio else (8 if cfg == 5 else 0)
+    ratio = args.ratio or DEFAULT_RATIO[cfg]
     pair = S.make_config(cfg, ratio)
     fine = S.inflate(pair.fine, validate=cfg <= 3)
     coarse = S.inflate(pair.coarse)
@@ -391,7 +433,7 @@ def run_ours(args):
     plan = S.AssemblyPlan(fine, qcfg, ctx=ctx)
     plan_ms = {k: round(ctx.timer(k)[0], 3) for k in ("plan_total", "plan_curls", "plan_tiles", "plan_singular")}
 
-    shard = args.shard and world > 1
+    shard = world > 1 and not args.replicas
 
     def assemble(plan, W):
         """the timed assembly: the whole W, or this rank's shard + the all-reduce of the
@@ -415,12 +457,26 @@ def run_ours(args):
     rows = S.row_ranges(n, world)[rank] if shard else None
     exchange = (S.allgather_exchange(dist, rank, world, n, device=f"cuda:{local}", host_staging=(rdev == "cpu"))
                 if shard else None)
+    # the stop decision of the row-panel PCG is collective (every rank enqueues the same
+    # all-gathers even if its state differs in the last bits)
+    agree = S.allreduce_agree(dist, device=None if rdev == "cpu" else rdev) if shard else None
+
+    def rhs():
+        L = S.assemble_rhs(fine, g, ctx=ctx)
+        if shard:  # the RHS is assembled with fp64 atomics: take rank 0's on every rank
+            import torch
+            t = torch.from_numpy(L)
+            if rdev != "cpu":
+                t = t.to(rdev)
+            dist.broadcast(t, 0)
+            L = t.cpu().numpy()
+        return L
 
     def step(W):
         W = assemble(plan, W)
-        L = S.assemble_rhs(fine, g, ctx=ctx)
+        L = rhs()
         prec = S.build_preconditioner(W, part, P)
-        rep = S.pcg_rows(W, prec, L, rows, exchange, 1e-8) if shard else S.pcg(W, prec, L, 1e-8)
+        rep = S.pcg_rows(W, prec, L, rows, exchange, 1e-8, agree=agree) if shard else S.pcg(W, prec, L, 1e-8)
         return W, prec, rep
 
     W = None
@@ -514,7 +570,7 @@ def run_ours(args):
         Wbuf.fill(0.0)
         dest = "pageable host buffer allocated (and touched) once"
     pageable_ms = None
-    for it in range(2 + max(args.steps, 4)):  # first run warms the host paths; min over the rest
+    for it in range(2 + max(args.steps, 4)):  # first run warms the host paths; median over the rest
         if it == 1:  # one run into a fresh pageable numpy array, for the record
             ctx.reset_timers()
             ctx.begin("e2e")
@@ -539,8 +595,28 @@ def run_ours(args):
         e2e_times.append(ctx.timer("e2e")[0] * 1e-3)
         del W2
     del Wbuf
-    e2e_t = min(e2e_times[1:]) if len(e2e_times) > 1 else e2e_times[0]
-    e2e_t = reduce_max([e2e_t], dist, rdev)[0]
+    runs = sorted(e2e_times[1:] if len(e2e_times) > 1 else e2e_times)
+    e2e_t = runs[len(runs) // 2]
+    e2e_min = runs[0]
+    e2e_t, e2e_min = reduce_max([e2e_t, e2e_min], dist, rdev)
+    # ---- time to solution through the public API: host MeshLevelPair -> host x
+    # (inflate both levels, partition_dofs, build_prolongation, assemble_W with its plan,
+    # assemble_rhs, build_preconditioner, pcg to 1e-8, the solution copied to the host)
+    tts = []
+    if not shard:
+        hpair = S.MeshLevelPair(S.SurfaceMesh(pair.coarse.vertices, pair.coarse.facets),
+                                S.SurfaceMesh(pair.fine.vertices, pair.fine.facets), pair.parent)
+        for it in range(1 + max(args.tts_runs, 1)):
+            ctx.synchronize()
+            t0 = time.perf_counter()
+            res = S.solve(hpair, g, 1e-8, qcfg, ctx=ctx)
+            x = res.report.solution
+            dt = time.perf_counter() - t0
+            if it:  # the first run warms the host paths
+                tts.append(dt * 1e3)
+            tts_iters = res.report.iterations
+            del res, x
+        tts.sort()
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
@@ -561,13 +637,13 @@ def run_ours(args):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "strong" if shard else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"config {cfg}: {CFG_NAMES[cfg]}" + (f", H/h {ratio}" if cfg == 5 else ""),
-                       "triangles": nf, "dofs": n, "tri_pairs": npairs, "parallelism": (f"assembly sharded x{world} (NCCL all-reduce of W), "
-                                                                   f"preconditioner replicated, PCG by row panels (NCCL all-gather of W p per iteration)") if shard
-                       else f"replicas x{world}",
-                       "l2": "flushed (256 MiB write + 256 MiB read: cold L2 with clean lines) before every timed step and every matvec launch",
-                       "pcg_tol": 1e-8, "far_field": "exact (IEEE, oracle order)" if args.exact_far else
-                       "fast (distance expansion + refined rsqrt)"},
+            "config": config_dict(cfg, ratio, nf, n),
+            "parallelism": (f"assembly sharded x{world} (NCCL all-reduce of W), preconditioner replicated, PCG by "
+                            f"row panels (NCCL all-gather of W p per iteration)") if shard
+            else (f"replicas x{world}" if world > 1 else "single GPU"),
+            "l2": "flushed (256 MiB write + 256 MiB read: cold L2 with clean lines) before every timed step and "
+                  "every matvec launch",
+            "far_field": "exact (IEEE, oracle order)" if args.exact_far else "fast (distance expansion + refined rsqrt)",
             "roofline": {"bound": "fp64", "kernel": dom[0], "achieved": achieved, "peak": fp64_peak,
                          "unit": "TFLOP/s", "frac": achieved / fp64_peak if fp64_peak else None,
                          "traffic": kernel_traffic(dom[0], cfg),
@@ -592,12 +668,19 @@ def run_ours(args):
                     "precond_applies_per_s": 1e3 / (am / ac) if ac else None, "precond_apply_us": 1e3 * am / ac if ac else None,
                     "precond_factor_bytes": prec.factor_bytes()},
             "time_to_solution_ms": step_ms,
+            "tts_e2e_ms": tts[len(tts) // 2] if tts else None,
+            "tts_e2e": ({"ms_median": tts[len(tts) // 2], "ms_min": tts[0], "runs": len(tts), "pcg_iterations": tts_iters,
+                         "what": "S.solve(host MeshLevelPair, g): inflate (fine + coarse), partition_dofs, "
+                                 "build_prolongation, assemble_W (plan build, H2D, kernels), assemble_rhs, "
+                                 "build_preconditioner, pcg to 1e-8, solution on the host; wall clock"}
+                        if tts else None),
             "phases_ms": {k: round(v, 4) for k, v in ms.items()},
             "phase_launches_per_step": launches_per_step,
             "plan_build_ms_host": plan_ms,
             "assembly_stats": stats,
             "e2e": {"value": (1 if shard else world) * npairs / e2e_t, "unit": UNIT, "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": 8 * n * n, "ms": e2e_t * 1e3,
+                    "d2h_bytes_per_step": 8 * n * n, "ms": e2e_t * 1e3, "ms_min": e2e_min * 1e3,
+                    "runs": len(e2e_times) - 1 if len(e2e_times) > 1 else 1, "statistic": "median",
                     "ms_pageable_destination": pageable_ms,
                     "what": "S.assemble_W(host InflatedMesh) + W.download(out=buf): plan build (host), H2D, kernels, "
                             f"D2H of the n x n W into a {dest} (the reference arm times assemble_W on an "
@@ -612,8 +695,29 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def launch_ranks(args) -> int:
+    """`bench.py --gpus N` started without a launcher: re-execute under
+    torch.distributed.run with N ranks on this node (one GPU each, 127.0.0.1 rendezvous),
+    NCCL's init lines left on so the communicator size is visible in the log."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.run(cmd, env=env).returncode
+
+
 def main():
     args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "0"))
+    if args.gpus > 1 and world == 0:
+        sys.exit(launch_ranks(args))
+    if world and world != args.gpus:
+        sys.exit(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}")
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -24,7 +24,9 @@
 // Host arrays are std::vector<double> (row-major for matrices) instead of Eigen types.
 #pragma once
 
+#include <cmath>
 #include <cstdint>
+#include <functional>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -86,6 +88,34 @@ public:
 private:
     T* p_ = nullptr;
 };
+
+// reference: inc/common.hpp:14 (Vec3 = Eigen::Vector3d) — the accessors and arithmetic a
+// Neumann-data callback uses, without Eigen
+struct Vec3 {
+    double v[3] = {0.0, 0.0, 0.0};
+    Vec3() = default;
+    Vec3(double a, double b, double c) : v{a, b, c} {}
+    double& operator[](int i) { return v[i]; }
+    double operator[](int i) const { return v[i]; }
+    double& operator()(int i) { return v[i]; }
+    double operator()(int i) const { return v[i]; }
+    double x() const { return v[0]; }
+    double y() const { return v[1]; }
+    double z() const { return v[2]; }
+    double dot(const Vec3& o) const { return (v[0] * o.v[0] + v[1] * o.v[1]) + v[2] * o.v[2]; }
+    double squaredNorm() const { return dot(*this); }
+    double norm() const { return std::sqrt(squaredNorm()); }
+    Vec3 cross(const Vec3& o) const
+    {
+        return {v[1] * o.v[2] - v[2] * o.v[1], v[2] * o.v[0] - v[0] * o.v[2], v[0] * o.v[1] - v[1] * o.v[0]};
+    }
+    Vec3 operator+(const Vec3& o) const { return {v[0] + o.v[0], v[1] + o.v[1], v[2] + o.v[2]}; }
+    Vec3 operator-(const Vec3& o) const { return {v[0] - o.v[0], v[1] - o.v[1], v[2] - o.v[2]}; }
+    Vec3 operator-() const { return {-v[0], -v[1], -v[2]}; }
+    Vec3 operator*(double s) const { return {v[0] * s, v[1] * s, v[2] * s}; }
+    Vec3 operator/(double s) const { return {v[0] / s, v[1] / s, v[2] / s}; }
+};
+inline Vec3 operator*(double s, const Vec3& a) { return a * s; }
 
 struct QuadratureConfig {  // reference: inc/quadrature.hpp:12-16
     int far_order = 4;
@@ -218,6 +248,26 @@ inline std::vector<double> assemble_rhs(Context& ctx, const InflatedMesh& im, co
     check(sbg_assemble_rhs(ctx.get(), im.get(), &c, g, 0, L.data()));
     return L;
 }
+// reference: inc/assemble.hpp:143-184 with a Neumann field g(x): g is evaluated on the host at
+// the far-rule points of every facet (sbg_rhs_points, the loop order of assemble.hpp:155-160)
+// and the integration runs on the device
+inline std::vector<double> assemble_rhs(Context& ctx, const InflatedMesh& im,
+                                        const std::function<Vec3(const Vec3&)>& g, const QuadratureConfig& cfg = {})
+{
+    const sbg_quad_cfg c = cfg.c();
+    int n, ng, nv, nf;
+    check(sbg_inflated_sizes(im.get(), &n, &ng, &nv, &nf));
+    const size_t npts = (size_t)nf * cfg.far_order * cfg.far_order;
+    std::vector<double> pts(3 * npts), gv(3 * std::max<size_t>(npts, 1));
+    check(sbg_rhs_points(im.get(), &c, pts.data()));
+    for (size_t i = 0; i < npts; ++i) {
+        const Vec3 v = g(Vec3(pts[3 * i], pts[3 * i + 1], pts[3 * i + 2]));
+        for (int k = 0; k < 3; ++k) gv[3 * i + k] = v[k];
+    }
+    std::vector<double> L(n);
+    check(sbg_assemble_rhs(ctx.get(), im.get(), &c, gv.data(), 1, L.data()));
+    return L;
+}
 // reference: inc/assemble.hpp:191-226
 inline void dump_matrix_binary(const GalerkinMatrix& W, const std::string& path)
 {
@@ -270,12 +320,14 @@ struct PcgReport {  // reference: inc/pcg.hpp:9-16
     std::vector<double> solution;
     int iterations = 0;
     bool converged = false;
-    std::vector<double> residual_history;
+    std::vector<double> residual_history;      // preconditioned residual norms
+    std::vector<double> energy_error_history;  // filled when an exact solution is given
     double kappa_estimate = 1.0;
 };
-// reference: inc/pcg.hpp:33-116 (prec nullable)
+// reference: inc/pcg.hpp:33-116 (prec nullable; exact nullable: energy_error_history)
 inline PcgReport pcg(Context& ctx, const GalerkinMatrix& W, const SchwarzPreconditioner* prec,
-                     const std::vector<double>& rhs, double tol = 1e-8, int maxit = 0)
+                     const std::vector<double>& rhs, double tol = 1e-8, int maxit = 0,
+                     const std::vector<double>* exact = nullptr)
 {
     const int n = (int)rhs.size();
     const int cap = (maxit > 0 ? maxit : std::max(10 * n, 100)) + 2;
@@ -283,8 +335,17 @@ inline PcgReport pcg(Context& ctx, const GalerkinMatrix& W, const SchwarzPrecond
     rep.solution.assign(n, 0.0);
     rep.residual_history.assign(cap, 0.0);
     sbg_pcg_report r{};
-    check(sbg_pcg(ctx.get(), W.get(), prec ? prec->get() : nullptr, rhs.data(), n, tol, maxit, rep.solution.data(),
-                  rep.residual_history.data(), nullptr, nullptr, cap, &r));
+    if (exact) {
+        if ((int)exact->size() != n) throw ValidationError("pcg: exact solution length mismatch");
+        rep.energy_error_history.assign(cap, 0.0);
+        check(sbg_pcg_exact(ctx.get(), W.get(), prec ? prec->get() : nullptr, rhs.data(), n, tol, maxit,
+                            exact->data(), rep.solution.data(), rep.residual_history.data(),
+                            rep.energy_error_history.data(), nullptr, nullptr, cap, &r));
+        rep.energy_error_history.resize(r.history_len);
+    } else {
+        check(sbg_pcg(ctx.get(), W.get(), prec ? prec->get() : nullptr, rhs.data(), n, tol, maxit,
+                      rep.solution.data(), rep.residual_history.data(), nullptr, nullptr, cap, &r));
+    }
     rep.iterations = r.iterations;
     rep.converged = r.converged != 0;
     rep.kappa_estimate = r.kappa_estimate;
@@ -294,10 +355,11 @@ inline PcgReport pcg(Context& ctx, const GalerkinMatrix& W, const SchwarzPrecond
 
 // pcg with one GPU per worker: this process computes rows [lo, hi) of each
 // W p; `exchange` enqueues the all-gather of the other rows on the given stream (e.g. NCCL
-// over NVLink).  Same result as pcg on every rank.
+// over NVLink); `agree` (nullable) makes the stop decision collective (a MIN over ranks of
+// the local stop flag, see sbg_pcg_rows_agree).  Same result as pcg on every rank.
 inline PcgReport pcg_rows(Context& ctx, const GalerkinMatrix& W, const SchwarzPreconditioner* prec,
                           const std::vector<double>& rhs, int lo, int hi, sbg_exchange_fn exchange, void* user,
-                          double tol = 1e-8, int maxit = 0)
+                          double tol = 1e-8, int maxit = 0, sbg_agree_fn agree = nullptr)
 {
     const int n = (int)rhs.size();
     const int cap = (maxit > 0 ? maxit : std::max(10 * n, 100)) + 2;
@@ -305,8 +367,9 @@ inline PcgReport pcg_rows(Context& ctx, const GalerkinMatrix& W, const SchwarzPr
     rep.solution.assign(n, 0.0);
     rep.residual_history.assign(cap, 0.0);
     sbg_pcg_report r{};
-    check(sbg_pcg_rows(ctx.get(), W.get(), prec ? prec->get() : nullptr, rhs.data(), n, 0, tol, maxit, lo, hi,
-                       exchange, user, rep.solution.data(), rep.residual_history.data(), nullptr, nullptr, cap, &r));
+    check(sbg_pcg_rows_agree(ctx.get(), W.get(), prec ? prec->get() : nullptr, rhs.data(), n, 0, tol, maxit, lo, hi,
+                             exchange, agree, user, rep.solution.data(), rep.residual_history.data(), nullptr, nullptr,
+                             cap, &r));
     rep.iterations = r.iterations;
     rep.converged = r.converged != 0;
     rep.kappa_estimate = r.kappa_estimate;

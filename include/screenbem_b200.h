@@ -210,6 +210,13 @@ int sbg_condition_number(sbg_ctx* ctx, const sbg_matrix* W, sbg_prec* p, double 
 int sbg_pcg(sbg_ctx* ctx, const sbg_matrix* W, sbg_prec* prec, const double* rhs, int n, double tol, int maxit,
             double* x, double* history, double* alphas, double* betas, int hist_cap, sbg_pcg_report* rep);
 
+/* pcg with the reference's optional exact solution (inc/pcg.hpp:33-35, 48-53, 59, 82):
+ * energy[k] = sqrt(max(0, e_k^T W e_k)), e_k = x_k - exact, for k = 0..iterations
+ * (history_len entries, as the residual history); one extra matvec per iteration. */
+int sbg_pcg_exact(sbg_ctx* ctx, const sbg_matrix* W, sbg_prec* prec, const double* rhs, int n, double tol, int maxit,
+                  const double* exact, double* x, double* history, double* energy, double* alphas, double* betas,
+                  int hist_cap, sbg_pcg_report* rep);
+
 /* Row-panel PCG for one GPU per rank (the multi-worker counterpart of
  * pcg, inc/pcg.hpp:33-116): W is replicated, this rank computes rows
  * [row_lo, row_hi) of y = W p each iteration, and `exchange` — called on the host
@@ -217,13 +224,25 @@ int sbg_pcg(sbg_ctx* ctx, const sbg_matrix* W, sbg_prec* prec, const double* rhs
  * enqueue on that stream the all-gather that fills the other ranks' rows of d_y
  * (e.g. NCCL over NVLink; d_p is the current search direction, for single-process
  * emulation).  Return non-zero to abort.  All other steps (dot products, updates,
- * preconditioner apply) are replicated and bitwise identical on every rank, so every
- * rank stops at the same iteration.  rhs/x are device buffers when on_device. */
+ * preconditioner apply) are replicated.  Iterations are enqueued in batches; at each
+ * batch boundary the host reads this rank's convergence state.  With `agree` (see
+ * sbg_pcg_rows_agree) the stop decision is collective: `agree(user, local_stop,
+ * &global_stop)` must return in global_stop the minimum of local_stop over the ranks
+ * (e.g. an all-reduce MIN), so every rank enqueues the same exchanges even if its W or
+ * rhs differ from the others' in the last bits (fp64 atomics in assembly).  Without it
+ * (sbg_pcg_rows) each rank decides alone, which is safe only when W and rhs are bitwise
+ * identical on every rank.  rhs/x are device buffers when on_device. */
 typedef int (*sbg_exchange_fn)(void* user, const double* d_p, double* d_y, int n, void* stream);
+typedef int (*sbg_agree_fn)(void* user, int local_stop, int* global_stop);
 int sbg_pcg_rows(sbg_ctx* ctx, const sbg_matrix* W, sbg_prec* prec, const double* rhs, int n, int on_device,
                  double tol, int maxit, int row_lo, int row_hi, sbg_exchange_fn exchange, void* user, double* x,
                  double* history, double* alphas, double* betas, int hist_cap, sbg_pcg_report* rep);
-/* d_y[lo:hi] = W[lo:hi, :] d_x, enqueued on the context stream (no synchronisation) */
+int sbg_pcg_rows_agree(sbg_ctx* ctx, const sbg_matrix* W, sbg_prec* prec, const double* rhs, int n, int on_device,
+                       double tol, int maxit, int row_lo, int row_hi, sbg_exchange_fn exchange, sbg_agree_fn agree,
+                       void* user, double* x, double* history, double* alphas, double* betas, int hist_cap,
+                       sbg_pcg_report* rep);
+/* d_y[lo:hi] = W[lo:hi, :] d_x, enqueued on the context stream (no synchronisation).
+ * d_x: n doubles, any alignment (copied into a zero-padded context scratch vector). */
 int sbg_matvec_rows_device(sbg_ctx* ctx, const sbg_matrix* W, const double* d_x, double* d_y, int row_lo, int row_hi);
 /* the context's CUDA stream (cudaStream_t), for enqueuing collectives in order with it */
 int sbg_ctx_stream(sbg_ctx* ctx, void** stream);
@@ -238,7 +257,8 @@ int sbg_memcpy_h2d(sbg_ctx* ctx, void* dst, const void* src, long long bytes);
 int sbg_memcpy_d2h(sbg_ctx* ctx, void* dst, const void* src, long long bytes);
 int sbg_pcg_device(sbg_ctx* ctx, const sbg_matrix* W, sbg_prec* prec, const double* d_rhs, double tol, int maxit,
                    double* d_x, sbg_pcg_report* rep);
-/* y = W x repeated `reps` times on device vectors; per-launch time via timers ("gemv_f64") */
+/* y = W x repeated `reps` times on device vectors; per-launch time via timers ("gemv_f64").
+ * d_x: n doubles, any alignment (copied into a zero-padded context scratch vector). */
 int sbg_matvec_device(sbg_ctx* ctx, const sbg_matrix* W, const double* d_x, double* d_y, int reps);
 int sbg_apply_preconditioner_device(sbg_ctx* ctx, sbg_prec* p, const double* d_r, double* d_z, int reps);
 /* write a buffer larger than L2 (L2 flush between timed iterations) */

@@ -75,6 +75,10 @@ def lib():
             "orc_assemble_W": (C.c_int, [vp, C.c_int, C.c_int, C.c_double, C.c_int, C.c_longlong,
                                          C.c_longlong, f64p, i64p]),
             "orc_assemble_W_rows": (C.c_int, [vp, C.c_int, C.c_int, C.c_double, i32p, C.c_int, C.c_int, f64p]),
+            "orc_sampler_new": (vp, [vp, C.c_int, C.c_int, C.c_double, C.c_int, C.POINTER(C.c_int)]),
+            "orc_sampler_free": (None, [vp]),
+            "orc_sampler_fixed": (C.c_int, [vp, C.POINTER(C.c_double)]),
+            "orc_sampler_run": (C.c_int, [vp, i64p, C.c_longlong, C.POINTER(C.c_double)]),
             "orc_rhs_points": (C.c_int, [vp, C.c_int, f64p]),
             "orc_assemble_rhs": (C.c_int, [vp, C.c_int, f64p, f64p]),
             "orc_build_prolongation": (vp, [vp, vp, vp, C.POINTER(C.c_int)]),
@@ -322,6 +326,48 @@ def assemble_W(im: InflatedMesh, cfg: QuadratureConfig = QuadratureConfig(), wor
                                 W, st))
     W = W.reshape(n, n)
     return (W, st) if stats else W
+
+
+class AssemblySampler:
+    """Timing model of the reference assemble_W (oracle/sbo.hpp AssemblySampler) for the
+    CPU baseline: fixed() times the per-call work (per-worker dense partials allocated and
+    zeroed, worker-ordered sum, mirror), run(idx) the pair loop over a sorted sample of
+    pair indices split across workers as run_partitioned splits the full range.  Holds
+    `workers` resident n x n partials (8 n^2 bytes each)."""
+
+    def __init__(self, im: InflatedMesh, workers: int, cfg: QuadratureConfig = QuadratureConfig()):
+        st = C.c_int()
+        self.h = lib().orc_sampler_new(im.h, cfg.far_order, cfg.singular_order, cfg.near_threshold, workers,
+                                       C.byref(st))
+        _check(st.value)
+        self.workers = workers
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.orc_sampler_free(self.h)
+            self.h = None
+
+    def fixed(self) -> float:
+        t = C.c_double()
+        _check(lib().orc_sampler_fixed(self.h, C.byref(t)))
+        return t.value
+
+    def run(self, idx) -> float:
+        idx = np.ascontiguousarray(idx, dtype=np.int64)
+        t = C.c_double()
+        _check(lib().orc_sampler_run(self.h, idx, len(idx), C.byref(t)))
+        return t.value
+
+
+def systematic_pair_sample(nf: int, k: int, seed: int = 0):
+    """k pair indices spread evenly over the reference's pair order (f <= g ranked as
+    f(f+1)/2 + g, inc/assemble.hpp:97-103) with one seeded random offset: every region of
+    the pair space — near-heavy early rows, far-heavy late rows — in proportion."""
+    total = nf * (nf + 1) // 2
+    k = max(1, min(int(k), total))
+    u = np.random.default_rng(seed).random()
+    idx = np.floor((np.arange(k) + u) * (total / k)).astype(np.int64)
+    return np.minimum(idx, total - 1)
 
 
 def assemble_W_rows(im: InflatedMesh, rows, cfg: QuadratureConfig = QuadratureConfig(), workers: int = 0):
@@ -594,3 +640,97 @@ def seeded_unit_vector(seed: int):
     """g from std::mt19937(seed), 3 normal draws, normalised (SURVEY.md §8d cfg 2/4)."""
     v = normal_draws(seed, 3)
     return v / np.sqrt((v[0] * v[0] + v[1] * v[1]) + v[2] * v[2])
+
+
+# --------------------------------------------------------------------------- BASELINE configs
+# The oracle's own restatement of the SURVEY.md Appendix A panel generator, so the CPU
+# baseline and the reference arm of bench.py never load the product library.  The
+# geometry follows the reference's flat-square fixture (tests/test_inflate.cpp:14-15:
+# cell (i,j) -> {p00,p10,p11},{p00,p11,p01}); coincident vertices of different panels
+# are merged by position quantised to 1e-9 (conformity, inc/mesh.hpp:191-234); the
+# parent map is Appendix A's.  tests/test_host_parity.py checks it bit for bit against
+# the product's make_config.
+def _llround(x: float) -> int:
+    import math
+    return int(math.copysign(math.floor(abs(x) + 0.5), x))
+
+
+def _panel_mesh(panels, L: float, m: int):
+    verts, facets, ids = [], [], {}
+    for o, a, b in panels:
+        local = np.zeros((m + 1, m + 1), dtype=np.int64)  # [j][i]
+        for j in range(m + 1):
+            sj = (L * j) / m
+            for i in range(m + 1):
+                si = (L * i) / m
+                p = ((o[0] + si * a[0]) + sj * b[0], (o[1] + si * a[1]) + sj * b[1],
+                     (o[2] + si * a[2]) + sj * b[2])
+                k = (_llround(p[0] * 1e9), _llround(p[1] * 1e9), _llround(p[2] * 1e9))
+                vid = ids.get(k)
+                if vid is None:
+                    vid = ids[k] = len(verts)
+                    verts.append(p)
+                local[j, i] = vid
+        for j in range(m):
+            for i in range(m):
+                p00, p10, p11, p01 = local[j, i], local[j, i + 1], local[j + 1, i + 1], local[j + 1, i]
+                facets.append((p00, p10, p11))
+                facets.append((p00, p11, p01))
+    return Mesh(np.array(verts, dtype=np.float64), np.array(facets, dtype=np.int32))
+
+
+def make_panels(kind: int, m: int, r: int) -> LevelPair:
+    """kind 0: flat unit square; 1: T-junction of three unit squares about the z-axis
+    (azimuth 0, 120, 240 degrees); 2: triple cross of [-1,1]^2 in the coordinate planes."""
+    import math
+    if r < 1 or m % r:
+        raise ValidationError("panel refinement ratio must divide the cell count")
+    L = 1.0
+    if kind == 0:
+        P = [((0.0, 0.0, 0.0), (1.0, 0.0, 0.0), (0.0, 1.0, 0.0))]
+    elif kind == 1:
+        P = []
+        for k in range(3):
+            th = 2.0 * math.pi * k / 3.0
+            P.append(((0.0, 0.0, 0.0), (math.cos(th), math.sin(th), 0.0), (0.0, 0.0, 1.0)))
+    elif kind == 2:
+        if m % 2:
+            raise ValidationError("triple cross needs an even cell count")
+        L = 2.0
+        P = [((-1.0, -1.0, 0.0), (1.0, 0.0, 0.0), (0.0, 1.0, 0.0)),
+             ((0.0, -1.0, -1.0), (0.0, 1.0, 0.0), (0.0, 0.0, 1.0)),
+             ((-1.0, 0.0, -1.0), (1.0, 0.0, 0.0), (0.0, 0.0, 1.0))]
+    else:
+        raise ValidationError(f"unknown panel geometry kind {kind}")
+    mc = m // r
+    fine, coarse = _panel_mesh(P, L, m), _panel_mesh(P, L, mc)
+    parent = np.zeros(fine.nf, dtype=np.int32)
+    for p in range(len(P)):
+        for j in range(m):
+            for i in range(m):
+                I, J, a, b = i // r, j // r, i % r, j % r
+                cbase = p * 2 * mc * mc + 2 * (J * mc + I)
+                fbase = p * 2 * m * m + 2 * (j * m + i)
+                parent[fbase] = cbase + (0 if b <= a else 1)
+                parent[fbase + 1] = cbase + (1 if a <= b else 0)
+    return LevelPair(coarse, fine, parent)
+
+
+CONFIG_DEFAULT_RATIO = {1: 8, 2: 16, 3: 12, 4: 8, 5: 8}
+
+
+def make_config(cfg: int, ratio: int = 0) -> LevelPair:
+    """BASELINE.json configs[cfg-1]."""
+    kind, m = {1: (0, 16), 2: (0, 64), 3: (1, 48), 4: (2, 64), 5: (0, 160)}[cfg]
+    return make_panels(kind, m, ratio if ratio > 0 else CONFIG_DEFAULT_RATIO[cfg])
+
+
+def config_g(cfg: int):
+    """Neumann field g of a BASELINE config (seeded unit vectors for cfg 2/4)."""
+    if cfg in (2, 4):
+        return seeded_unit_vector(1 if cfg == 2 else 7)
+    if cfg == 3:
+        return np.array([1.0, 0.5, 0.25])
+    if cfg in (1, 5):
+        return np.array([0.0, 0.0, 1.0])
+    raise ValidationError(f"unknown BASELINE config {cfg}")

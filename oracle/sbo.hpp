@@ -39,6 +39,7 @@
 #include <stdexcept>
 #include <string>
 #include <thread>
+#include <chrono>
 #include <vector>
 
 namespace sbo {
@@ -1055,21 +1056,71 @@ inline Vec3 surface_curl(const InflatedMesh& im, int o, const TraceField& tr)
 
 // reference: inc/assemble.hpp:72-139.  `pair_lo/pair_hi` restrict the pair
 // index range (bounded CPU-baseline samples); the default is the full range.
+namespace detail {
+// Per-pair unrank + integral + scatter of the reference loop body
+// (inc/assemble.hpp:97-128), shared by assemble_W and the timing sampler.
+struct PairScatter {
+    const InflatedMesh& im;
+    const QuadratureEngine eng;
+    const std::vector<Scatter> scatter;
+    std::vector<std::array<Vec3, 3>> slot_curl;
+    PairScatter(const InflatedMesh& m, const QuadratureConfig& cfg)
+        : im(m), eng(cfg), scatter(build_scatter(m)), slot_curl(m.num_oriented())
+    {
+        for (int o = 0; o < im.num_oriented(); ++o) {
+            const int f = o / 2;
+            for (int k = 0; k < 3; ++k)
+                slot_curl[o][k] = cross(im.oriented_facets[o].normal, shape_gradient(im.base, f, k));
+        }
+    }
+    // reference: assemble.hpp:98-103 (unrank the (f <= g) pair index)
+    static void unrank(std::int64_t idx, int& ff, int& g)
+    {
+        const int f = (int)((std::sqrt(8.0 * idx + 1.0) - 1.0) / 2.0);
+        ff = f;
+        while ((std::int64_t)(ff + 1) * (ff + 2) / 2 <= idx) ++ff;
+        while ((std::int64_t)ff * (ff + 1) / 2 > idx) --ff;
+        g = (int)(idx - (std::int64_t)ff * (ff + 1) / 2);
+    }
+    void operator()(std::int64_t idx, Dense& W, QuadStats* stats) const
+    {
+        const SurfaceMesh& m = im.base;
+        int ff, g;
+        unrank(idx, ff, g);
+        const double I = pair_integral(m, ff, g, eng, stats);
+        if (!std::isfinite(I)) throw NumericalError("quadrature produced a non-finite pair integral");
+        for (int sa = 0; sa < 2; ++sa)
+            for (int sb = 0; sb < 2; ++sb) {
+                const int oa = 2 * ff + sa, ob = 2 * g + sb;
+                for (int ka = 0; ka < 3; ++ka) {
+                    const int ga = im.gv_index(m.facets[ff][ka], im.branch_at(oa, ka));
+                    if (scatter[ga].terms.empty()) continue;
+                    for (int kb = 0; kb < 3; ++kb) {
+                        const int gb = im.gv_index(m.facets[g][kb], im.branch_at(ob, kb));
+                        if (scatter[gb].terms.empty()) continue;
+                        const double c = dot(slot_curl[oa][ka], slot_curl[ob][kb]) * I;
+                        for (const auto& [da, wa] : scatter[ga].terms)
+                            for (const auto& [db, wb] : scatter[gb].terms) {
+                                const double v = c * wa * wb;
+                                W(da, db) += v;
+                                if (ff != g) W(db, da) += v;
+                            }
+                    }
+                }
+            }
+    }
+};
+}  // namespace detail
+
+// reference: inc/assemble.hpp:72-139 (per-worker dense partials over contiguous pair
+// ranges, worker-ordered sum, mirror of the upper triangle)
 inline Dense assemble_W(const InflatedMesh& im, const QuadratureConfig& cfg, int workers = 1,
                         std::int64_t pair_lo = 0, std::int64_t pair_hi = -1,
                         detail::QuadStats* stats = nullptr)
 {
-    const SurfaceMesh& m = im.base;
     const int n = im.num_jump_dofs();
-    const int nf = m.num_facets();
-    const QuadratureEngine eng(cfg);
-    const auto scatter = detail::build_scatter(im);
-    std::vector<std::array<Vec3, 3>> slot_curl(im.num_oriented());
-    for (int o = 0; o < im.num_oriented(); ++o) {
-        const int f = o / 2;
-        for (int k = 0; k < 3; ++k)
-            slot_curl[o][k] = cross(im.oriented_facets[o].normal, detail::shape_gradient(m, f, k));
-    }
+    const int nf = im.base.num_facets();
+    const detail::PairScatter body(im, cfg);
     const std::int64_t npairs = (std::int64_t)nf * (nf + 1) / 2;
     if (pair_hi < 0 || pair_hi > npairs) pair_hi = npairs;
     if (pair_lo < 0) pair_lo = 0;
@@ -1079,34 +1130,7 @@ inline Dense assemble_W(const InflatedMesh& im, const QuadratureConfig& cfg, int
         Dense& W = partial[w];
         W.n = n;
         W.a.assign((size_t)n * n, 0.0);
-        for (std::int64_t idx = pair_lo + lo; idx < pair_lo + hi; ++idx) {
-            const int f = (int)((std::sqrt(8.0 * idx + 1.0) - 1.0) / 2.0);
-            int ff = f;
-            while ((std::int64_t)(ff + 1) * (ff + 2) / 2 <= idx) ++ff;
-            while ((std::int64_t)ff * (ff + 1) / 2 > idx) --ff;
-            const int g = (int)(idx - (std::int64_t)ff * (ff + 1) / 2);
-            const double I = pair_integral(m, ff, g, eng, stats ? &wstats[w] : nullptr);
-            if (!std::isfinite(I)) throw NumericalError("quadrature produced a non-finite pair integral");
-            for (int sa = 0; sa < 2; ++sa)
-                for (int sb = 0; sb < 2; ++sb) {
-                    const int oa = 2 * ff + sa, ob = 2 * g + sb;
-                    for (int ka = 0; ka < 3; ++ka) {
-                        const int ga = im.gv_index(m.facets[ff][ka], im.branch_at(oa, ka));
-                        if (scatter[ga].terms.empty()) continue;
-                        for (int kb = 0; kb < 3; ++kb) {
-                            const int gb = im.gv_index(m.facets[g][kb], im.branch_at(ob, kb));
-                            if (scatter[gb].terms.empty()) continue;
-                            const double c = dot(slot_curl[oa][ka], slot_curl[ob][kb]) * I;
-                            for (const auto& [da, wa] : scatter[ga].terms)
-                                for (const auto& [db, wb] : scatter[gb].terms) {
-                                    const double v = c * wa * wb;
-                                    W(da, db) += v;
-                                    if (ff != g) W(db, da) += v;
-                                }
-                        }
-                    }
-                }
-        }
+        for (std::int64_t idx = pair_lo + lo; idx < pair_lo + hi; ++idx) body(idx, W, stats ? &wstats[w] : nullptr);
     });
     Dense W = std::move(partial[0]);
     if (W.a.empty()) {
@@ -1126,6 +1150,71 @@ inline Dense assemble_W(const InflatedMesh& im, const QuadratureConfig& cfg, int
         }
     return W;
 }
+
+// Timing sampler of assemble_W for the CPU baseline (bench.py): the reference's cost
+// split into its per-call part and its per-pair part, so a bounded, unbiased sample of
+// the pair space gives the full call's time without running it for minutes.
+//   fixed():  the per-call work of assemble.hpp:91-137 with no pairs — `workers` dense
+//             n x n partials allocated and zeroed in their worker threads, the
+//             worker-ordered sum and the mirror;
+//   run(idx): the loop body of assemble.hpp:97-128 over a sorted list of pair indices,
+//             split into contiguous chunks per worker exactly as run_partitioned splits
+//             the full range (common.hpp:31-59), each worker scattering into its own
+//             resident dense partial.
+// Full-call estimate: fixed + (npairs / k) * run(k sampled pairs).
+struct AssemblySampler {
+    const InflatedMesh& im;
+    detail::PairScatter body;
+    int workers;
+    std::vector<Dense> partial;
+    AssemblySampler(const InflatedMesh& m, const QuadratureConfig& cfg, int w)
+        : im(m), body(m, cfg), workers(std::max(w, 1)), partial(workers)
+    {
+    }
+    // the resident partials of run(), allocated on first use outside the timed region
+    // (fixed() runs before them, so at most `workers` n x n matrices exist at a time)
+    void prepare()
+    {
+        const int n = im.num_jump_dofs();
+        if (!partial[0].a.empty()) return;
+        run_partitioned(2 * workers, workers, [&](int k, std::int64_t, std::int64_t) {
+            partial[k].n = n;
+            partial[k].a.assign((size_t)n * n, 0.0);
+        });
+    }
+    static double now()
+    {
+        return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+    }
+    double fixed() const
+    {
+        const int n = im.num_jump_dofs();
+        const double t0 = now();
+        std::vector<Dense> p(workers);
+        run_partitioned(2 * workers, workers, [&](int k, std::int64_t, std::int64_t) {
+            p[k].n = n;
+            p[k].a.assign((size_t)n * n, 0.0);
+        });
+        Dense W = std::move(p[0]);
+        for (int k = 1; k < workers; ++k)
+            if (!p[k].a.empty())
+                for (size_t i = 0; i < W.a.size(); ++i) W.a[i] += p[k].a[i];
+        for (int i = 0; i < n; ++i)
+            for (int j = i + 1; j < n; ++j) W(j, i) = W(i, j);
+        volatile double sink = W.a.empty() ? 0.0 : W.a[W.a.size() / 2];
+        (void)sink;
+        return now() - t0;
+    }
+    double run(const std::int64_t* idx, std::int64_t k)
+    {
+        prepare();
+        const double t0 = now();
+        run_partitioned(k, workers, [&](int w, std::int64_t lo, std::int64_t hi) {
+            for (std::int64_t i = lo; i < hi; ++i) body(idx[i], partial[w], nullptr);
+        });
+        return now() - t0;
+    }
+};
 
 // Selected rows of assemble_W (same per-entry summation order restricted to
 // the requested rows; rows-only evaluation of the reference loop at

@@ -287,6 +287,26 @@ int orc_assemble_W(void* imh, int far_order, int singular_order, double near, in
         }
     });
 }
+// timing sampler of assemble_W (bench.py CPU baseline; sbo.hpp AssemblySampler)
+void* orc_sampler_new(void* imh, int far_order, int singular_order, double near, int workers, int* status)
+{
+    void* out = nullptr;
+    *status = guard([&] {
+        out = new AssemblySampler(*static_cast<InflatedMesh*>(imh), qcfg(far_order, singular_order, near), workers);
+    });
+    return out;
+}
+void orc_sampler_free(void* h) { delete static_cast<AssemblySampler*>(h); }
+int orc_sampler_fixed(void* h, double* seconds)
+{
+    return guard([&] { *seconds = static_cast<AssemblySampler*>(h)->fixed(); });
+}
+int orc_sampler_run(void* h, const long long* idx, long long k, double* seconds)
+{
+    return guard([&] {
+        *seconds = static_cast<AssemblySampler*>(h)->run(reinterpret_cast<const std::int64_t*>(idx), k);
+    });
+}
 int orc_assemble_W_rows(void* imh, int far_order, int singular_order, double near, const int* rows,
                         int nrows, int workers, double* out)
 {

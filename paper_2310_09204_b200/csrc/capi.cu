@@ -87,6 +87,31 @@ void need(const void* p, const char* what)
 {
     if (!p) throw ValidationError(std::string("null argument: ") + what);
 }
+// every entry point validates its handles before touching them: a NULL handle is a
+// validation error (status 2), never a crash
+void bind_ctx(const sbg_ctx* ctx)
+{
+    need(ctx, "ctx");
+    bind_device(&ctx->c);
+}
+void bind_mat(const sbg_matrix* W)
+{
+    need(W, "W");
+    bind_device(W->M.ctx);
+}
+
+// The GEMV kernels read x with 16-byte vector loads over the padded row length W.ld
+// (W's padding columns are zero).  A caller's d_x holds exactly n doubles with no
+// alignment promise, so it is copied into a context scratch vector of ld entries whose
+// tail is zeroed: no read past the caller's buffer, no NaN * 0 from garbage padding.
+const double* padded_x(Ctx* c, const DMatrix& M, const double* d_x)
+{
+    need(d_x, "d_x");
+    double* xp = scratch(c, kScratchMatvecX, (size_t)std::max(M.ld, 1));
+    if (M.n) SBG_CUDA(cudaMemcpyAsync(xp, d_x, (size_t)M.n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+    if (M.ld > M.n) SBG_CUDA(cudaMemsetAsync(xp + M.n, 0, (size_t)(M.ld - M.n) * sizeof(double), c->stream));
+    return xp;
+}
 
 QuadCfg qcfg(const sbg_quad_cfg* c)
 {
@@ -143,7 +168,10 @@ int sbg_ctx_create(int device, sbg_ctx** out)
 void sbg_ctx_destroy(sbg_ctx* ctx) { delete ctx; }
 int sbg_ctx_synchronize(sbg_ctx* ctx)
 {
-    return guard([&] { SBG_CUDA(cudaStreamSynchronize(ctx->c.stream)); });
+    return guard([&] {
+        bind_ctx(ctx);
+        SBG_CUDA(cudaStreamSynchronize(ctx->c.stream));
+    });
 }
 int sbg_device_name(int device, char* buf, int cap, int* sm_count)
 {
@@ -159,16 +187,22 @@ int sbg_device_name(int device, char* buf, int cap, int* sm_count)
 }
 int sbg_timers_enable(sbg_ctx* ctx, int on)
 {
-    return guard([&] { ctx->c.timers.enabled = on != 0; });
+    return guard([&] {
+        need(ctx, "ctx");
+        ctx->c.timers.enabled = on != 0;
+    });
 }
 int sbg_timers_reset(sbg_ctx* ctx)
 {
-    return guard([&] { ctx->c.timers.reset(); });
+    return guard([&] {
+        need(ctx, "ctx");
+        ctx->c.timers.reset();
+    });
 }
 int sbg_timer_get(sbg_ctx* ctx, const char* name, double* total_ms, long long* count)
 {
     return guard([&] {
-        bind_device(ctx ? &ctx->c : nullptr);
+        bind_ctx(ctx);
         ctx->c.timers.collect();
         *total_ms = 0;
         *count = 0;
@@ -183,7 +217,7 @@ int sbg_timer_get(sbg_ctx* ctx, const char* name, double* total_ms, long long* c
 int sbg_timer_begin(sbg_ctx* ctx, const char* name)
 {
     return guard([&] {
-        bind_device(ctx ? &ctx->c : nullptr);
+        bind_ctx(ctx);
         auto u = std::make_unique<UserScope>();
         u->name = name;
         u->ts = std::make_unique<TimedScope>(&ctx->c, u->name.c_str());
@@ -193,7 +227,7 @@ int sbg_timer_begin(sbg_ctx* ctx, const char* name)
 int sbg_timer_end(sbg_ctx* ctx)
 {
     return guard([&] {
-        bind_device(ctx ? &ctx->c : nullptr);
+        bind_ctx(ctx);
         (void)ctx;
         if (g_user_scopes.empty()) throw ValidationError("sbg_timer_end without sbg_timer_begin");
         g_user_scopes.back()->ts.reset();
@@ -216,6 +250,7 @@ void sbg_mesh_destroy(sbg_mesh* m) { delete m; }
 int sbg_mesh_sizes(const sbg_mesh* m, int* nv, int* nf)
 {
     return guard([&] {
+        need(m, "m");
         *nv = m->m.num_vertices();
         *nf = m->m.num_facets();
     });
@@ -223,6 +258,7 @@ int sbg_mesh_sizes(const sbg_mesh* m, int* nv, int* nf)
 int sbg_mesh_export(const sbg_mesh* m, double* verts, int32_t* facets)
 {
     return guard([&] {
+        need(m, "m");
         for (int i = 0; i < m->m.num_vertices(); ++i) {
             verts[3 * i] = m->m.vertices[i].x;
             verts[3 * i + 1] = m->m.vertices[i].y;
@@ -234,11 +270,15 @@ int sbg_mesh_export(const sbg_mesh* m, double* verts, int32_t* facets)
 }
 int sbg_validate_mesh(const sbg_mesh* m)
 {
-    return guard([&] { validate_mesh(m->m); });
+    return guard([&] {
+        need(m, "m");
+        validate_mesh(m->m);
+    });
 }
 int sbg_make_builtin(const char* spec, sbg_mesh** out)
 {
     return guard([&] {
+        need(out, "out");
         auto* m = new sbg_mesh;
         try {
             m->m = make_builtin(spec);
@@ -252,6 +292,8 @@ int sbg_make_builtin(const char* spec, sbg_mesh** out)
 int sbg_refine_uniform_times(const sbg_mesh* m, int k, sbg_level** out)
 {
     return guard([&] {
+        need(m, "m");
+        need(out, "out");
         auto* l = new sbg_level;
         l->p = refine_uniform_times(m->m, k);
         *out = l;
@@ -260,6 +302,9 @@ int sbg_refine_uniform_times(const sbg_mesh* m, int k, sbg_level** out)
 int sbg_level_create(const sbg_mesh* coarse, const sbg_mesh* fine, const int32_t* parent, sbg_level** out)
 {
     return guard([&] {
+        need(coarse, "coarse");
+        need(fine, "fine");
+        need(out, "out");
         auto* l = new sbg_level;
         l->p.coarse = coarse->m;
         l->p.fine = fine->m;
@@ -272,6 +317,7 @@ int sbg_level_create(const sbg_mesh* coarse, const sbg_mesh* fine, const int32_t
 int sbg_make_config(int cfg, int ratio, sbg_level** out)
 {
     return guard([&] {
+        need(out, "out");
         auto* l = new sbg_level;
         try {
             l->p = make_config(cfg, ratio);
@@ -285,6 +331,7 @@ int sbg_make_config(int cfg, int ratio, sbg_level** out)
 int sbg_make_panels(int kind, int m, int r, sbg_level** out)
 {
     return guard([&] {
+        need(out, "out");
         auto* l = new sbg_level;
         try {
             l->p = make_panels(kind, m, r);
@@ -321,6 +368,8 @@ int sbg_config_g(int cfg, double* g)
 int sbg_level_mesh(const sbg_level* l, int fine, sbg_mesh** out)
 {
     return guard([&] {
+        need(l, "l");
+        need(out, "out");
         auto* m = new sbg_mesh;
         m->m = fine ? l->p.fine : l->p.coarse;
         *out = m;
@@ -328,11 +377,15 @@ int sbg_level_mesh(const sbg_level* l, int fine, sbg_mesh** out)
 }
 int sbg_level_parent(const sbg_level* l, int32_t* parent)
 {
-    return guard([&] { std::copy(l->p.parent.begin(), l->p.parent.end(), parent); });
+    return guard([&] {
+        need(l, "l");
+        std::copy(l->p.parent.begin(), l->p.parent.end(), parent);
+    });
 }
 int sbg_level_sizes(const sbg_level* l, double* H, double* h)
 {
     return guard([&] {
+        need(l, "l");
         *H = l->p.H;
         *h = l->p.h;
     });
@@ -343,6 +396,8 @@ void sbg_level_destroy(sbg_level* l) { delete l; }
 int sbg_inflate(const sbg_mesh* m, int validate, sbg_inflated** out)
 {
     return guard([&] {
+        need(m, "m");
+        need(out, "out");
         auto* im = new sbg_inflated;
         try {
             im->im = inflate(m->m, validate != 0);
@@ -357,6 +412,7 @@ void sbg_inflated_destroy(sbg_inflated* im) { delete im; }
 int sbg_inflated_sizes(const sbg_inflated* im, int* n, int* ng, int* nv, int* nf)
 {
     return guard([&] {
+        need(im, "im");
         *n = im->im.num_jump_dofs();
         *ng = im->im.num_gvertices();
         *nv = im->im.base.num_vertices();
@@ -367,6 +423,7 @@ int sbg_inflated_export(const sbg_inflated* imh, int32_t* q, int32_t* gv_first, 
                         int32_t* jd, double* normals)
 {
     return guard([&] {
+        need(imh, "imh");
         const InflatedMesh& im = imh->im;
         const int nv = im.base.num_vertices(), no = 2 * im.base.num_facets();
         for (int v = 0; v < nv; ++v) {
@@ -420,7 +477,9 @@ int sbg_assemble_w(sbg_ctx* ctx, const sbg_inflated* im, const sbg_quad_cfg* cfg
 int sbg_assembly_plan_create(sbg_ctx* ctx, const sbg_inflated* im, const sbg_quad_cfg* cfg, sbg_aplan** out)
 {
     return guard([&] {
-        bind_device(ctx ? &ctx->c : nullptr);
+        need(im, "im");
+        need(out, "out");
+        bind_ctx(ctx);
         auto* p = new sbg_aplan;
         p->ctx = &ctx->c;
         try {
@@ -473,7 +532,8 @@ void sbg_assembly_plan_destroy(sbg_aplan* plan) { delete plan; }
 int sbg_matrix_create(sbg_ctx* ctx, int n, const double* host, sbg_matrix** out)
 {
     return guard([&] {
-        bind_device(ctx ? &ctx->c : nullptr);
+        need(out, "out");
+        bind_ctx(ctx);
         need(ctx, "ctx");
         if (n < 0) throw ValidationError("negative matrix size");
         auto* W = new sbg_matrix;
@@ -492,7 +552,7 @@ int sbg_matrix_n(const sbg_matrix* W) { return W ? W->M.n : -1; }
 int sbg_matrix_device_view(const sbg_matrix* W, void** data, int* ld, long long* count)
 {
     return guard([&] {
-        bind_device(W ? W->M.ctx : nullptr);
+        bind_mat(W);
         need(W, "W");
         if (data) *data = W->M.a.p;
         if (ld) *ld = W->M.ld;
@@ -502,28 +562,29 @@ int sbg_matrix_device_view(const sbg_matrix* W, void** data, int* ld, long long*
 int sbg_matrix_download(const sbg_matrix* W, double* host)
 {
     return guard([&] {
-        bind_device(W ? W->M.ctx : nullptr);
+        bind_mat(W);
         matrix_download(W->M, host);
     });
 }
 int sbg_matrix_download_rows(const sbg_matrix* W, const int32_t* rows, int nrows, double* host)
 {
     return guard([&] {
-        bind_device(W ? W->M.ctx : nullptr);
+        bind_mat(W);
         matrix_download_rows(W->M, rows, nrows, host);
     });
 }
 int sbg_matrix_symmetry_defect(const sbg_matrix* W, double* m)
 {
     return guard([&] {
-        bind_device(W ? W->M.ctx : nullptr);
+        bind_mat(W);
         *m = matrix_symmetry_defect(W->M);
     });
 }
 int sbg_matvec(sbg_ctx* ctx, const sbg_matrix* W, const double* x, double* y)
 {
     return guard([&] {
-        bind_device(ctx ? &ctx->c : nullptr);
+        need(W, "W");
+        bind_ctx(ctx);
         const int n = W->M.n;
         cudaStream_t s = ctx->c.stream;
         DBuf<double> dx(W->M.ld), dy(W->M.ld);
@@ -542,7 +603,7 @@ void sbg_matrix_destroy(sbg_matrix* W) { delete W; }
 int sbg_matrix_dump_binary(const sbg_matrix* W, const char* path)
 {
     return guard([&] {
-        bind_device(W ? W->M.ctx : nullptr);
+        bind_mat(W);
         std::ofstream os(path, std::ios::binary);
         if (!os) throw ValidationError(std::string("cannot open matrix dump file: ") + path);
         char header[16] = {};
@@ -566,7 +627,8 @@ int sbg_matrix_dump_binary(const sbg_matrix* W, const char* path)
 int sbg_matrix_load_binary(sbg_ctx* ctx, const char* path, sbg_matrix** out)
 {
     return guard([&] {
-        bind_device(ctx ? &ctx->c : nullptr);
+        need(out, "out");
+        bind_ctx(ctx);
         std::ifstream is(path, std::ios::binary);
         if (!is) throw ValidationError(std::string("cannot open matrix dump file: ") + path);
         char header[16] = {};
@@ -593,7 +655,8 @@ int sbg_pair_integrals(sbg_ctx* ctx, const sbg_mesh* m, const sbg_quad_cfg* cfg,
                        long long np, double* out)
 {
     return guard([&] {
-        bind_device(ctx ? &ctx->c : nullptr);
+        need(m, "m");
+        bind_ctx(ctx);
         pair_integrals(&ctx->c, m->m, qcfg(cfg), f, g, np, out);
         for (long long i = 0; i < np; ++i)
             if (!std::isfinite(out[i])) throw NumericalError("quadrature produced a non-finite pair integral");
@@ -603,6 +666,7 @@ int sbg_pair_integrals(sbg_ctx* ctx, const sbg_mesh* m, const sbg_quad_cfg* cfg,
 int sbg_rhs_points(const sbg_inflated* im, const sbg_quad_cfg* cfg, double* pts)
 {
     return guard([&] {
+        need(im, "im");
         const auto p = rhs_points(im->im, qcfg(cfg));
         std::copy(p.begin(), p.end(), pts);
     });
@@ -611,7 +675,8 @@ int sbg_assemble_rhs(sbg_ctx* ctx, const sbg_inflated* im, const sbg_quad_cfg* c
                      double* L)
 {
     return guard([&] {
-        bind_device(ctx ? &ctx->c : nullptr);
+        need(im, "im");
+        bind_ctx(ctx);
         assemble_rhs(&ctx->c, im->im, qcfg(cfg), g, g_is_field != 0, L);
     });
 }
@@ -620,6 +685,9 @@ int sbg_assemble_rhs(sbg_ctx* ctx, const sbg_inflated* im, const sbg_quad_cfg* c
 int sbg_partition_dofs(const sbg_level* pair, const sbg_inflated* fine, sbg_partition** out)
 {
     return guard([&] {
+        need(pair, "pair");
+        need(fine, "fine");
+        need(out, "out");
         auto* p = new sbg_partition;
         try {
             p->p = partition_dofs(pair->p, fine->im);
@@ -634,6 +702,7 @@ int sbg_partition_create(int nfaces, const int32_t* face_ids, const int32_t* fac
                          int nwb, const int32_t* wb, sbg_partition** out)
 {
     return guard([&] {
+        need(out, "out");
         auto* p = new sbg_partition;
         p->p.face_ids.assign(face_ids, face_ids + nfaces);
         p->p.face_ptr.assign(face_ptr, face_ptr + nfaces + 1);
@@ -645,6 +714,7 @@ int sbg_partition_create(int nfaces, const int32_t* face_ids, const int32_t* fac
 int sbg_partition_sizes(const sbg_partition* p, int* nfaces, int* nface_dofs, int* nwb)
 {
     return guard([&] {
+        need(p, "p");
         *nfaces = (int)p->p.face_ids.size();
         *nface_dofs = (int)p->p.face_dofs.size();
         *nwb = (int)p->p.wirebasket.size();
@@ -653,6 +723,7 @@ int sbg_partition_sizes(const sbg_partition* p, int* nfaces, int* nface_dofs, in
 int sbg_partition_export(const sbg_partition* p, int32_t* ids, int32_t* ptr, int32_t* dofs, int32_t* wb)
 {
     return guard([&] {
+        need(p, "p");
         std::copy(p->p.face_ids.begin(), p->p.face_ids.end(), ids);
         std::copy(p->p.face_ptr.begin(), p->p.face_ptr.end(), ptr);
         std::copy(p->p.face_dofs.begin(), p->p.face_dofs.end(), dofs);
@@ -664,6 +735,10 @@ int sbg_build_prolongation(const sbg_level* pair, const sbg_inflated* coarse, co
                            sbg_prolong** out)
 {
     return guard([&] {
+        need(pair, "pair");
+        need(coarse, "coarse");
+        need(fine, "fine");
+        need(out, "out");
         auto* p = new sbg_prolong;
         try {
             p->R = build_prolongation(pair->p, coarse->im, fine->im);
@@ -678,6 +753,7 @@ int sbg_prolong_create(int rows, int cols, const int32_t* col_ptr, const int32_t
                        sbg_prolong** out)
 {
     return guard([&] {
+        need(out, "out");
         auto* p = new sbg_prolong;
         p->R.rows = rows;
         p->R.cols = cols;
@@ -691,6 +767,7 @@ int sbg_prolong_create(int rows, int cols, const int32_t* col_ptr, const int32_t
 int sbg_prolong_sizes(const sbg_prolong* p, int* rows, int* cols, int* nnz)
 {
     return guard([&] {
+        need(p, "p");
         *rows = p->R.rows;
         *cols = p->R.cols;
         *nnz = (int)p->R.val.size();
@@ -699,6 +776,7 @@ int sbg_prolong_sizes(const sbg_prolong* p, int* rows, int* cols, int* nnz)
 int sbg_prolong_export(const sbg_prolong* p, int32_t* col_ptr, int32_t* row_idx, double* val)
 {
     return guard([&] {
+        need(p, "p");
         std::copy(p->R.col_ptr.begin(), p->R.col_ptr.end(), col_ptr);
         std::copy(p->R.row_idx.begin(), p->R.row_idx.end(), row_idx);
         std::copy(p->R.val.begin(), p->R.val.end(), val);
@@ -711,7 +789,10 @@ int sbg_build_preconditioner(sbg_ctx* ctx, const sbg_matrix* W, const sbg_partit
                              sbg_prec** out)
 {
     return guard([&] {
-        bind_device(ctx ? &ctx->c : nullptr);
+        need(W, "W");
+        need(part, "part");
+        need(out, "out");
+        bind_ctx(ctx);
         Prolongation none;
         none.rows = W->M.n;
         auto* p = new sbg_prec;
@@ -728,7 +809,10 @@ int sbg_build_preconditioner_mode(sbg_ctx* ctx, const sbg_matrix* W, const sbg_p
                                   int mode, sbg_prec** out)
 {
     return guard([&] {
-        bind_device(ctx ? &ctx->c : nullptr);
+        need(W, "W");
+        need(part, "part");
+        need(out, "out");
+        bind_ctx(ctx);
         if (mode != kPrecTrsv && mode != kPrecInverse) throw ValidationError("unknown preconditioner apply mode");
         Prolongation none;
         none.rows = W->M.n;
@@ -745,7 +829,8 @@ int sbg_build_preconditioner_mode(sbg_ctx* ctx, const sbg_matrix* W, const sbg_p
 int sbg_apply_preconditioner(sbg_ctx* ctx, sbg_prec* p, const double* r, int n, double* z)
 {
     return guard([&] {
-        bind_device(ctx ? &ctx->c : nullptr);
+        need(p, "p");
+        bind_ctx(ctx);
         if (n != prec_n(p->P)) throw ValidationError("preconditioner length mismatch");
         cudaStream_t s = ctx->c.stream;
         DBuf<double> dr(std::max(n, 1)), dz(std::max(n, 1));
@@ -755,11 +840,12 @@ int sbg_apply_preconditioner(sbg_ctx* ctx, sbg_prec* p, const double* r, int n, 
         SBG_CUDA(cudaStreamSynchronize(s));
     });
 }
-int sbg_prec_num_subspaces(const sbg_prec* p) { return prec_num_subspaces(p->P); }
+int sbg_prec_num_subspaces(const sbg_prec* p) { return p ? prec_num_subspaces(p->P) : -1; }
 int sbg_prec_block_diag(sbg_ctx* ctx, sbg_prec* p, int which, double* diag, int* n_out)
 {
     return guard([&] {
-        bind_device(ctx ? &ctx->c : nullptr);
+        need(p, "p");
+        bind_ctx(ctx);
         std::vector<double> d;
         prec_block_diag(&ctx->c, p->P, which, d);
         *n_out = (int)d.size();
@@ -769,19 +855,21 @@ int sbg_prec_block_diag(sbg_ctx* ctx, sbg_prec* p, int which, double* diag, int*
 int sbg_coarse_matrix(sbg_ctx* ctx, const sbg_matrix* W, const sbg_prolong* R, double* H)
 {
     return guard([&] {
-        bind_device(ctx ? &ctx->c : nullptr);
+        need(W, "W");
+        need(R, "R");
+        bind_ctx(ctx);
         std::vector<double> h;
         coarse_galerkin(&ctx->c, W->M, R->R, h);
         std::copy(h.begin(), h.end(), H);
     });
 }
-double sbg_prec_factor_bytes(const sbg_prec* p) { return prec_factor_bytes(p->P); }
+double sbg_prec_factor_bytes(const sbg_prec* p) { return p ? prec_factor_bytes(p->P) : -1.0; }
 
 // ---------------------------------------------------------------- condition numbers
 int sbg_materialize_preconditioner(sbg_ctx* ctx, sbg_prec* p, sbg_matrix** out)
 {
     return guard([&] {
-        bind_device(ctx ? &ctx->c : nullptr);
+        bind_ctx(ctx);
         need(out, "out");
         need(p, "preconditioner");
         auto* m = new sbg_matrix;
@@ -797,7 +885,7 @@ int sbg_materialize_preconditioner(sbg_ctx* ctx, sbg_prec* p, sbg_matrix** out)
 int sbg_prec_from_dense(sbg_ctx* ctx, const sbg_matrix* M, sbg_prec** out)
 {
     return guard([&] {
-        bind_device(ctx ? &ctx->c : nullptr);
+        bind_ctx(ctx);
         need(out, "out");
         need(M, "matrix");
         auto* p = new sbg_prec;
@@ -813,7 +901,7 @@ int sbg_prec_from_dense(sbg_ctx* ctx, const sbg_matrix* M, sbg_prec** out)
 int sbg_condition_number(sbg_ctx* ctx, const sbg_matrix* W, sbg_prec* p, double tol, int maxit, sbg_spectrum* out)
 {
     return guard([&] {
-        bind_device(ctx ? &ctx->c : nullptr);
+        bind_ctx(ctx);
         need(out, "out");
         need(W, "matrix");
         const Spectrum sp = spectrum(&ctx->c, W->M, p ? p->P : nullptr, tol, maxit);
@@ -846,7 +934,8 @@ int sbg_pcg(sbg_ctx* ctx, const sbg_matrix* W, sbg_prec* prec, const double* rhs
             double* x, double* history, double* alphas, double* betas, int hist_cap, sbg_pcg_report* rep)
 {
     return guard([&] {
-        bind_device(ctx ? &ctx->c : nullptr);
+        need(W, "W");
+        bind_ctx(ctx);
         if (n != W->M.n) throw ValidationError("pcg: right-hand side length mismatch");
         PcgResult r;
         pcg_run(&ctx->c, W->M, prec ? prec->P : nullptr, rhs, x, false, tol, maxit, r);
@@ -854,12 +943,35 @@ int sbg_pcg(sbg_ctx* ctx, const sbg_matrix* W, sbg_prec* prec, const double* rhs
     });
 }
 
+int sbg_pcg_exact(sbg_ctx* ctx, const sbg_matrix* W, sbg_prec* prec, const double* rhs, int n, double tol, int maxit,
+                  const double* exact, double* x, double* history, double* energy, double* alphas, double* betas,
+                  int hist_cap, sbg_pcg_report* rep)
+{
+    return guard([&] {
+        bind_ctx(ctx);
+        need(W, "W");
+        need(exact, "exact");
+        if (n != W->M.n) throw ValidationError("pcg: right-hand side length mismatch");
+        PcgResult r;
+        pcg_run(&ctx->c, W->M, prec ? prec->P : nullptr, rhs, x, false, tol, maxit, r, nullptr, exact);
+        fill_report(r, history, alphas, betas, hist_cap, rep);
+        for (int i = 0; energy && i < hist_cap && i < (int)r.energy.size(); ++i) energy[i] = r.energy[i];
+    });
+}
 int sbg_pcg_rows(sbg_ctx* ctx, const sbg_matrix* W, sbg_prec* prec, const double* rhs, int n, int on_device,
                  double tol, int maxit, int row_lo, int row_hi, sbg_exchange_fn exchange, void* user, double* x,
                  double* history, double* alphas, double* betas, int hist_cap, sbg_pcg_report* rep)
 {
+    return sbg_pcg_rows_agree(ctx, W, prec, rhs, n, on_device, tol, maxit, row_lo, row_hi, exchange, nullptr, user, x,
+                              history, alphas, betas, hist_cap, rep);
+}
+int sbg_pcg_rows_agree(sbg_ctx* ctx, const sbg_matrix* W, sbg_prec* prec, const double* rhs, int n, int on_device,
+                       double tol, int maxit, int row_lo, int row_hi, sbg_exchange_fn exchange, sbg_agree_fn agree,
+                       void* user, double* x, double* history, double* alphas, double* betas, int hist_cap,
+                       sbg_pcg_report* rep)
+{
     return guard([&] {
-        bind_device(ctx ? &ctx->c : nullptr);
+        bind_ctx(ctx);
         need(W, "W");
         if (n != W->M.n) throw ValidationError("pcg: right-hand side length mismatch");
         if (!exchange) throw ValidationError("pcg: row panel needs an exchange");
@@ -867,6 +979,7 @@ int sbg_pcg_rows(sbg_ctx* ctx, const sbg_matrix* W, sbg_prec* prec, const double
         rows.lo = row_lo;
         rows.hi = row_hi;
         rows.exchange = exchange;
+        rows.agree = agree;
         rows.user = user;
         PcgResult r;
         pcg_run(&ctx->c, W->M, prec ? prec->P : nullptr, rhs, x, on_device != 0, tol, maxit, r, &rows);
@@ -876,9 +989,9 @@ int sbg_pcg_rows(sbg_ctx* ctx, const sbg_matrix* W, sbg_prec* prec, const double
 int sbg_matvec_rows_device(sbg_ctx* ctx, const sbg_matrix* W, const double* d_x, double* d_y, int row_lo, int row_hi)
 {
     return guard([&] {
-        bind_device(ctx ? &ctx->c : nullptr);
+        bind_ctx(ctx);
         need(W, "W");
-        gemv_rows_range(&ctx->c, W->M, d_x, d_y, row_lo, row_hi);
+        gemv_rows_range(&ctx->c, W->M, padded_x(&ctx->c, W->M, d_x), d_y, row_lo, row_hi);
     });
 }
 int sbg_ctx_stream(sbg_ctx* ctx, void** stream)
@@ -894,7 +1007,7 @@ int sbg_ctx_stream(sbg_ctx* ctx, void** stream)
 int sbg_device_alloc(sbg_ctx* ctx, long long bytes, void** dptr)
 {
     return guard([&] {
-        bind_device(ctx ? &ctx->c : nullptr);
+        bind_ctx(ctx);
         SBG_CUDA(cudaSetDevice(ctx->c.device));
         *dptr = device_alloc((size_t)bytes);
         SBG_CUDA(cudaMemsetAsync(*dptr, 0, (size_t)bytes, ctx->c.stream));
@@ -922,7 +1035,7 @@ int sbg_host_free(void* hptr)
 int sbg_memcpy_h2d(sbg_ctx* ctx, void* dst, const void* src, long long bytes)
 {
     return guard([&] {
-        bind_device(ctx ? &ctx->c : nullptr);
+        bind_ctx(ctx);
         SBG_CUDA(cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyHostToDevice, ctx->c.stream));
         SBG_CUDA(cudaStreamSynchronize(ctx->c.stream));
     });
@@ -930,7 +1043,7 @@ int sbg_memcpy_h2d(sbg_ctx* ctx, void* dst, const void* src, long long bytes)
 int sbg_memcpy_d2h(sbg_ctx* ctx, void* dst, const void* src, long long bytes)
 {
     return guard([&] {
-        bind_device(ctx ? &ctx->c : nullptr);
+        bind_ctx(ctx);
         SBG_CUDA(cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyDeviceToHost, ctx->c.stream));
         SBG_CUDA(cudaStreamSynchronize(ctx->c.stream));
     });
@@ -939,7 +1052,8 @@ int sbg_pcg_device(sbg_ctx* ctx, const sbg_matrix* W, sbg_prec* prec, const doub
                    double* d_x, sbg_pcg_report* rep)
 {
     return guard([&] {
-        bind_device(ctx ? &ctx->c : nullptr);
+        need(W, "W");
+        bind_ctx(ctx);
         PcgResult r;
         pcg_run(&ctx->c, W->M, prec ? prec->P : nullptr, d_rhs, d_x, true, tol, maxit, r);
         fill_report(r, nullptr, nullptr, nullptr, 0, rep);
@@ -948,17 +1062,20 @@ int sbg_pcg_device(sbg_ctx* ctx, const sbg_matrix* W, sbg_prec* prec, const doub
 int sbg_matvec_device(sbg_ctx* ctx, const sbg_matrix* W, const double* d_x, double* d_y, int reps)
 {
     return guard([&] {
-        bind_device(ctx ? &ctx->c : nullptr);
+        need(W, "W");
+        bind_ctx(ctx);
         GemvPlan plan;
         gemv_plan(&ctx->c, W->M.n, W->M.ld, plan);
-        for (int i = 0; i < reps; ++i) gemv(&ctx->c, W->M, plan, d_x, d_y);
+        const double* xp = padded_x(&ctx->c, W->M, d_x);
+        for (int i = 0; i < reps; ++i) gemv(&ctx->c, W->M, plan, xp, d_y);
         SBG_CUDA(cudaStreamSynchronize(ctx->c.stream));
     });
 }
 int sbg_apply_preconditioner_device(sbg_ctx* ctx, sbg_prec* p, const double* d_r, double* d_z, int reps)
 {
     return guard([&] {
-        bind_device(ctx ? &ctx->c : nullptr);
+        need(p, "p");
+        bind_ctx(ctx);
         for (int i = 0; i < reps; ++i) prec_apply(&ctx->c, p->P, d_r, d_z, nullptr);
         SBG_CUDA(cudaStreamSynchronize(ctx->c.stream));
     });
@@ -966,7 +1083,7 @@ int sbg_apply_preconditioner_device(sbg_ctx* ctx, sbg_prec* p, const double* d_r
 int sbg_fp64_peak(sbg_ctx* ctx, double* tflops)
 {
     return guard([&] {
-        bind_device(ctx ? &ctx->c : nullptr);
+        bind_ctx(ctx);
         *tflops = fp64_peak_tflops(&ctx->c);
     });
 }
@@ -978,7 +1095,7 @@ int sbg_fp64_peak(sbg_ctx* ctx, double* tflops)
 int sbg_pool_stats(sbg_ctx* ctx, long long* reserved, long long* used)
 {
     return guard([&] {
-        bind_device(ctx ? &ctx->c : nullptr);
+        bind_ctx(ctx);
         cudaMemPool_t pool;
         SBG_CUDA(cudaDeviceGetDefaultMemPool(&pool, ctx->c.device));
         unsigned long long r = 0, u = 0;
@@ -991,7 +1108,7 @@ int sbg_pool_stats(sbg_ctx* ctx, long long* reserved, long long* used)
 int sbg_l2_flush(sbg_ctx* ctx)
 {
     return guard([&] {
-        bind_device(ctx ? &ctx->c : nullptr);
+        bind_ctx(ctx);
         l2_flush(&ctx->c);
     });
 }

@@ -43,7 +43,7 @@ bool pcg_graph_enabled();        // PCG loop as one graph with a device-side whi
 void l2_flush(Ctx* ctx);  // write 256 MiB then read 256 MiB: cold, clean L2
 // grow-only device scratch buffer `slot` of at least `count` doubles, cached on the
 // context (large per-call temporaries: no pool growth or fragmentation between calls)
-enum { kScratchInverse = 0, kScratchCoarseWR = 1, kScratchCoarsePart = 2, kScratchSlots = 3 };
+enum { kScratchInverse = 0, kScratchCoarseWR = 1, kScratchCoarsePart = 2, kScratchMatvecX = 3, kScratchSlots = 4 };
 double* scratch(Ctx* ctx, int slot, size_t count);
 
 // ---------------------------------------------------------------- matrices
@@ -87,19 +87,25 @@ struct PcgResult {
     bool converged = false;
     double kappa = 1.0;
     std::vector<double> history, alphas, betas;
+    std::vector<double> energy;  // energy_error_history when an exact solution is given
 };
 // Row-panel PCG: this rank computes rows [lo, hi) of y = W p; `exchange`
 // enqueues on `stream` the collective that fills the other ranks' rows of y (an
 // all-gather).  Every other step of the iteration is replicated on each rank.
 typedef int (*ExchangeFn)(void* user, const double* d_p, double* d_y, int n, void* stream);
+// Collective stopping decision: given this rank's local "stop" (converged or maxit),
+// return in *global_stop whether EVERY rank stops (a min over ranks), so all ranks
+// enqueue the same number of exchanges even when their states differ in the last bits.
+typedef int (*AgreeFn)(void* user, int local_stop, int* global_stop);
 struct RowPanel {
     int lo = 0, hi = 0;
     ExchangeFn exchange = nullptr;
+    AgreeFn agree = nullptr;
     void* user = nullptr;
 };
 // rhs/x: device vectors when on_device, else host; rows: null = the whole matvec here
 void pcg_run(Ctx* ctx, const DMatrix& W, Prec* prec, const double* rhs, double* x, bool on_device, double tol,
-             int maxit, PcgResult& out, const RowPanel* rows = nullptr);
+             int maxit, PcgResult& out, const RowPanel* rows = nullptr, const double* exact = nullptr);
 // y[lo:hi] = W[lo:hi, :] x on device vectors, enqueued on the context stream (no sync)
 void gemv_rows_range(Ctx* ctx, const DMatrix& W, const double* x, double* y, int lo, int hi);
 double lanczos_kappa(const std::vector<double>& alphas, const std::vector<double>& betas);

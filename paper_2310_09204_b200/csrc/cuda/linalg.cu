@@ -220,6 +220,38 @@ __global__ void k_pcg_rz(PcgDev* st, const double* __restrict__ r, const double*
     }
 }
 
+// e = x - exact, the error of the energy history (pcg.hpp:50-53); `gated`: skip once done
+__global__ void k_pcg_err(const PcgDev* st, const double* __restrict__ x, const double* __restrict__ exact,
+                          double* __restrict__ e, int n, int gated)
+{
+    pdl_wait();
+    if (gated && st->done) return;
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j < n) e[j] = x[j] - exact[j];
+}
+
+// energy[st->it + off] = sqrt(max(0, e . W e)) from the GEMV partials of W e (pcg.hpp:50-53, 59, 82)
+__global__ void k_pcg_energy(PcgDev* st, const double* __restrict__ part, int chunks, int ld, int n,
+                             const double* __restrict__ e, double* partials, double* energy, int off, int gated)
+{
+    pdl_wait();
+    if (gated && st->done) return;
+    __shared__ double sh[32];
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    double v = 0.0;
+    if (j < n) {
+        double s = 0.0;
+        for (int c = 0; c < chunks; ++c) s += part[(size_t)c * ld + j];
+        v = e[j] * s;
+    }
+    v = block_sum(v, sh);
+    if (last_block(v, partials, &st->counter) && threadIdx.x == 0) {
+        const double ewe = sum_partials(partials, gridDim.x);
+        st->counter = 0;
+        energy[st->it + off] = sqrt(fmax(0.0, ewe));
+    }
+}
+
 // device-side loop control of the graph form: the while node runs its body while the
 // handle is non-zero
 __global__ void k_pcg_gate(const PcgDev* st, cudaGraphConditionalHandle h)
@@ -430,6 +462,7 @@ double lanczos_kappa(const std::vector<double>& alphas, const std::vector<double
 struct PcgWork {
     int ld = 0, cap = 0;
     DBuf<double> buf, partials, hist, alphas, betas, xbuf;  // xbuf: row-panel exchange buffer (ld)
+    DBuf<double> ebuf, energy;  // energy history: e and exact (2 ld), per-iteration values (cap)
     DBuf<PcgDev> st;
     GemvPlan plan;
     PcgDev* hs = nullptr;
@@ -482,9 +515,10 @@ static PcgWork& pcg_work(Ctx* ctx, const DMatrix& W, int maxit)
 // the host enqueues iterations in growing batches and reads back one small
 // state record per batch (iterations past convergence are no-op launches).
 void pcg_run(Ctx* ctx, const DMatrix& W, Prec* prec, const double* rhs, double* x_out, bool on_device, double tol,
-             int maxit, PcgResult& out, const RowPanel* rows)
+             int maxit, PcgResult& out, const RowPanel* rows, const double* exact)
 {
     const int n = W.n;
+    if (exact && rows) throw ValidationError("pcg: the energy history is not offered by the row-panel form");
     if (tol <= 0) throw ValidationError("pcg: tolerance must be positive");
     if (rows && (rows->lo < 0 || rows->hi > n || rows->lo > rows->hi || !rows->exchange))
         throw ValidationError("pcg: row panel outside the matrix or no exchange");
@@ -494,6 +528,7 @@ void pcg_run(Ctx* ctx, const DMatrix& W, Prec* prec, const double* rhs, double* 
         out = PcgResult{};
         out.converged = true;
         out.history.assign(1, 0.0);
+        if (exact) out.energy.assign(1, 0.0);
         return;
     }
     TimedScope tpcg(ctx, "pcg");
@@ -514,6 +549,30 @@ void pcg_run(Ctx* ctx, const DMatrix& W, Prec* prec, const double* rhs, double* 
     h.maxit = maxit;
     SBG_CUDA(cudaMemcpyAsync(w.st.p, &h, sizeof(h), cudaMemcpyHostToDevice, s));
     const int* done = &w.st.p->done;
+    // energy error history (pcg.hpp:50-53, 59, 82): e = x - exact, sqrt(e.We) after every
+    // iteration's update and for x0 = 0 — one extra matvec per iteration, as in the reference
+    double* e_err = nullptr;
+    const double* d_exact = nullptr;
+    if (exact) {
+        if ((size_t)w.ebuf.n < 2 * len) w.ebuf.alloc(2 * len);
+        if ((size_t)w.energy.n < (size_t)w.cap) w.energy.alloc(w.cap);
+        e_err = w.ebuf.p;
+        SBG_CUDA(cudaMemsetAsync(w.ebuf.p, 0, 2 * len * sizeof(double), s));
+        SBG_CUDA(cudaMemcpyAsync(w.ebuf.p + len, exact, n * sizeof(double),
+                                 on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
+        d_exact = w.ebuf.p + len;
+    }
+    auto enqueue_energy = [&](int off, int gated) {
+        launch_pdl(k_pcg_err, dim3(nb), dim3(256), 0, s, (const PcgDev*)w.st.p, (const double*)x, d_exact, e_err, n,
+                   gated);
+        count_launch();
+        gemv_partial_launch(ctx, W, w.plan, e_err, gated ? done : nullptr);
+        launch_pdl(k_pcg_energy, dim3(nb), dim3(256), 0, s, w.st.p, (const double*)w.plan.part.p, w.plan.chunks, W.ld,
+                   n, (const double*)e_err, w.partials.p, w.energy.p, off, gated);
+        count_launch();
+        SBG_LAUNCH_CHECK();
+    };
+    if (exact) enqueue_energy(0, 0);
     if (n > 0) {
         if (prec) prec_apply(ctx, prec, r, z, nullptr);
         k_pcg_init<<<nb, 256, 0, s>>>(w.st.p, r, z, p, n, w.partials.p, w.hist.p);
@@ -556,6 +615,7 @@ void pcg_run(Ctx* ctx, const DMatrix& W, Prec* prec, const double* rhs, double* 
         count_launch();
         launch_pdl(k_pcg_update, dim3(nb), dim3(256), 0, s, w.st.p, x, r, p, Wp, n);
         count_launch();
+        if (exact) enqueue_energy(1, 1);
         if (prec) prec_apply(ctx, prec, r, z, done);
         launch_pdl(k_pcg_rz, dim3(nb), dim3(256), 0, s, w.st.p, r, z, n, w.partials.p, w.hist.p, w.alphas.p, w.betas.p);
         count_launch();
@@ -563,7 +623,8 @@ void pcg_run(Ctx* ctx, const DMatrix& W, Prec* prec, const double* rhs, double* 
         count_launch();
         SBG_LAUNCH_CHECK();
     };
-    const bool graph = n > 0 && pcg_graph_enabled() && !rows;  // the exchange is a host call
+    // the exchange is a host call; the energy history (test path) runs host-driven too
+    const bool graph = n > 0 && pcg_graph_enabled() && !rows && !exact;
     if (graph) {
         // graph form: [gate] -> while(handle) { iteration ; gate } — the loop runs on the device
         // with no host round trips and no launches past convergence
@@ -644,7 +705,13 @@ void pcg_run(Ctx* ctx, const DMatrix& W, Prec* prec, const double* rhs, double* 
     while (true) {
         SBG_CUDA(cudaMemcpyAsync(w.hs, w.st.p, sizeof(PcgDev), cudaMemcpyDeviceToHost, s));
         SBG_CUDA(cudaStreamSynchronize(s));
-        if (w.hs->done || enqueued >= maxit) break;
+        int stop = (w.hs->done || enqueued >= maxit) ? 1 : 0;
+        if (rows && rows->agree) {  // every rank takes the same decision (kernels.cuh: AgreeFn)
+            int all = stop;
+            if (rows->agree(rows->user, stop, &all) != 0) throw std::runtime_error("pcg: the row-panel agreement failed");
+            stop = all;
+        }
+        if (stop) break;
         const int todo = std::min(batch, maxit - enqueued);
         for (int t = 0; t < todo; ++t) enqueue_iteration();
         enqueued += todo;
@@ -663,6 +730,11 @@ void pcg_run(Ctx* ctx, const DMatrix& W, Prec* prec, const double* rhs, double* 
         if (fin.it) {
             SBG_CUDA(cudaMemcpyAsync(out.alphas.data(), w.alphas.p, fin.it * sizeof(double), cudaMemcpyDeviceToHost, s));
             SBG_CUDA(cudaMemcpyAsync(out.betas.data(), w.betas.p, fin.it * sizeof(double), cudaMemcpyDeviceToHost, s));
+        }
+        if (exact) {
+            out.energy.assign(fin.it + 1, 0.0);
+            SBG_CUDA(cudaMemcpyAsync(out.energy.data(), w.energy.p, (fin.it + 1) * sizeof(double),
+                                     cudaMemcpyDeviceToHost, s));
         }
         SBG_CUDA(cudaMemcpyAsync(x_out, x, n * sizeof(double), on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s));
     } else {

@@ -123,8 +123,12 @@ SIGNATURES = {
     "sbg_prec_destroy": (None, [vp]),
     "sbg_pcg": (C.c_int, [vp, vp, vp, f64p, C.c_int, C.c_double, C.c_int, f64p, f64p, f64p, f64p, C.c_int,
                           C.POINTER(PcgReportC)]),
+    "sbg_pcg_exact": (C.c_int, [vp, vp, vp, f64p, C.c_int, C.c_double, C.c_int, f64p, f64p, f64p, f64p, f64p, f64p,
+                                C.c_int, C.POINTER(PcgReportC)]),
     "sbg_pcg_rows": (C.c_int, [vp, vp, vp, vp, C.c_int, C.c_int, C.c_double, C.c_int, C.c_int, C.c_int,
                                vp, vp, vp, f64p, f64p, f64p, C.c_int, C.POINTER(PcgReportC)]),
+    "sbg_pcg_rows_agree": (C.c_int, [vp, vp, vp, vp, C.c_int, C.c_int, C.c_double, C.c_int, C.c_int, C.c_int,
+                                     vp, vp, vp, vp, f64p, f64p, f64p, C.c_int, C.POINTER(PcgReportC)]),
     "sbg_matvec_rows_device": (C.c_int, [vp, vp, vp, vp, C.c_int, C.c_int]),
     "sbg_ctx_stream": (C.c_int, [vp, C.POINTER(vp)]),
     "sbg_device_alloc": (C.c_int, [vp, C.c_longlong, C.POINTER(vp)]),
@@ -778,27 +782,41 @@ class PcgReport:
     kappa_estimate: float
     alphas: np.ndarray = field(default_factory=lambda: np.zeros(0))
     betas: np.ndarray = field(default_factory=lambda: np.zeros(0))
+    energy_error_history: np.ndarray = field(default_factory=lambda: np.zeros(0))
 
 
-def pcg(W: GalerkinMatrix, prec, rhs, tol: float = 1e-8, maxit: int = 0) -> PcgReport:
-    """reference: inc/pcg.hpp:33-116 (the optional exact-solution energy history is test-only
-    in the reference and is not part of the device path)."""
+def pcg(W: GalerkinMatrix, prec, rhs, tol: float = 1e-8, maxit: int = 0, exact=None) -> PcgReport:
+    """reference: inc/pcg.hpp:33-116.  `exact` (optional) fills energy_error_history with
+    sqrt(e^T W e), e = x_k - exact, for k = 0..iterations (pcg.hpp:50-53, 59, 82)."""
     rhs = np.ascontiguousarray(rhs, dtype=np.float64)
     n = len(rhs)
     cap = (maxit if maxit > 0 else max(10 * n, 100)) + 2
     x = np.zeros(max(n, 1))
     hist, al, be = np.zeros(cap), np.zeros(cap), np.zeros(cap)
     rep = PcgReportC()
-    _check(lib().sbg_pcg(W.ctx.h, W.h, prec.h if prec is not None else None,
-                         rhs if n else np.zeros(1), n, tol, maxit, x, hist, al, be, cap, C.byref(rep)))
+    energy = np.zeros(0)
+    if exact is None:
+        _check(lib().sbg_pcg(W.ctx.h, W.h, prec.h if prec is not None else None,
+                             rhs if n else np.zeros(1), n, tol, maxit, x, hist, al, be, cap, C.byref(rep)))
+    else:
+        ex = np.ascontiguousarray(exact, dtype=np.float64)
+        if len(ex) != n:
+            raise ValidationError("pcg: exact solution length mismatch")
+        en = np.zeros(cap)
+        _check(lib().sbg_pcg_exact(W.ctx.h, W.h, prec.h if prec is not None else None,
+                                   rhs if n else np.zeros(1), n, tol, maxit, ex if n else np.zeros(1), x, hist, en,
+                                   al, be, cap, C.byref(rep)))
+        energy = en[:rep.history_len].copy()
     k = rep.iterations
     return PcgReport(x[:n], k, bool(rep.converged), hist[:rep.history_len].copy(), rep.kappa_estimate,
-                     al[:k].copy(), be[:k].copy())
+                     al[:k].copy(), be[:k].copy(), energy)
 
 
 # --------------------------------------------------------------------------- row-panel PCG
 # exchange hook of sbg_pcg_rows: (user, d_p, d_y, n, stream) -> 0 | error
 EXCHANGE_FN = C.CFUNCTYPE(C.c_int, vp, vp, vp, C.c_int, vp)
+# agreement hook of sbg_pcg_rows_agree: (user, local_stop, *global_stop) -> 0 | error
+AGREE_FN = C.CFUNCTYPE(C.c_int, vp, C.c_int, C.POINTER(C.c_int))
 
 
 def row_ranges(n: int, world: int):
@@ -862,6 +880,21 @@ def allgather_exchange(dist, rank: int, world: int, n: int, device=None, wrap=No
     return exchange
 
 
+def allreduce_agree(dist, device=None):
+    """The collective stop of the row-panel PCG: every rank passes its local stop flag
+    (converged or out of iterations) at each batch boundary and all ranks get the minimum,
+    so they stop together and enqueue the same all-gathers (include/screenbem_b200.h,
+    sbg_pcg_rows_agree).  `device` is where the flag is reduced (the NCCL device; None =
+    host, gloo).  Returns f(local_stop) -> global_stop for pcg_rows."""
+    import torch
+
+    def agree(local_stop: int) -> int:
+        t = torch.tensor([int(local_stop)], dtype=torch.int32, device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+        return int(t.item())
+    return agree
+
+
 class _nullctx:
     def __enter__(self):
         return self
@@ -870,11 +903,14 @@ class _nullctx:
         return False
 
 
-def pcg_rows(W: GalerkinMatrix, prec, rhs, rows, exchange, tol: float = 1e-8, maxit: int = 0) -> PcgReport:
-    """Row-panel PCG (sbg_pcg_rows): the reference's pcg (inc/pcg.hpp:33-116) with this
-    rank computing rows `rows = (lo, hi)` of each matvec and `exchange(d_p, d_y, n,
-    stream)` filling in the rest (allgather_exchange for one GPU per rank).  The result
-    equals pcg's (same kernels per row, same replicated reductions)."""
+def pcg_rows(W: GalerkinMatrix, prec, rhs, rows, exchange, tol: float = 1e-8, maxit: int = 0,
+             agree=None) -> PcgReport:
+    """Row-panel PCG (sbg_pcg_rows / sbg_pcg_rows_agree): the reference's pcg
+    (inc/pcg.hpp:33-116) with this rank computing rows `rows = (lo, hi)` of each matvec
+    and `exchange(d_p, d_y, n, stream)` filling in the rest (allgather_exchange for one
+    GPU per rank).  `agree(local_stop) -> global_stop` (allreduce_agree) makes the stop
+    decision collective; without it every rank must hold bitwise-identical W and rhs.
+    The result equals pcg's (same kernels per row, same replicated reductions)."""
     rhs = np.ascontiguousarray(rhs, dtype=np.float64)
     n = len(rhs)
     cap = (maxit if maxit > 0 else max(10 * n, 100)) + 2
@@ -890,11 +926,20 @@ def pcg_rows(W: GalerkinMatrix, prec, rhs, rows, exchange, tol: float = 1e-8, ma
         except BaseException as e:  # surfaced after the C call returns
             err.append(e)
             return 1
+    def ahook(user, local_stop, out):
+        try:
+            out[0] = int(agree(int(local_stop)))
+            return 0
+        except BaseException as e:
+            err.append(e)
+            return 1
     cb = EXCHANGE_FN(hook)
+    ab = AGREE_FN(ahook) if agree is not None else None
     rb = (rhs if n else np.zeros(1))
-    code = lib().sbg_pcg_rows(W.ctx.h, W.h, prec.h if prec is not None else None, rb.ctypes.data, n, 0, tol, maxit,
-                              int(rows[0]), int(rows[1]), C.cast(cb, vp), None, x.ctypes.data, hist, al, be, cap,
-                              C.byref(rep))
+    code = lib().sbg_pcg_rows_agree(W.ctx.h, W.h, prec.h if prec is not None else None, rb.ctypes.data, n, 0, tol,
+                                    maxit, int(rows[0]), int(rows[1]), C.cast(cb, vp),
+                                    C.cast(ab, vp) if ab is not None else None, None, x.ctypes.data, hist, al, be,
+                                    cap, C.byref(rep))
     if err:
         raise err[0]
     _check(code)

@@ -45,3 +45,39 @@ def test_cpp_dropin_runs_cfg1(tmp_path):
     # row-panel PCG through the C++ header: the same iterations and (row kernel) the same solution
     assert f"rows_iterations {res.report.iterations}" in r.stdout
     assert float(r.stdout.split("rows_max_dx")[1].split()[0]) == 0.0
+
+
+@pytest.mark.gpu
+def test_cpp_dropin_field_rhs_and_energy_history_cfg2(tmp_path):
+    """Config 2 through the C++ header with a non-constant Neumann field g(x)
+    (std::function<Vec3(const Vec3&)>, inc/assemble.hpp:143-145) and pcg's exact-solution
+    energy history (inc/pcg.hpp:33-35, 48-53): RHS, iterations, solution and the energy
+    history against the oracle's pipeline on the same matrix."""
+    import numpy as np
+    from oracle import oracle as O
+    exe = build_example(tmp_path)
+    out = str(tmp_path / "field.bin")
+    r = subprocess.run([exe, "2", out], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr
+    raw = open(out, "rb").read()
+    n, iters, ne = np.frombuffer(raw[:12], dtype=np.int32)
+    vals = np.frombuffer(raw[12:], dtype=np.float64)
+    L, x, energy, exact = vals[:n], vals[n:2 * n], vals[2 * n:2 * n + ne], vals[2 * n + ne:3 * n + ne]
+    assert n == 3969 and ne == iters + 1
+
+    def g(p):
+        return [0.3 + p[1] * p[0], -0.2 * p[0] + np.sin(3.0 * p[1]), 1.0 + 0.5 * np.sqrt(p[0] ** 2 + p[1] ** 2 + p[2] ** 2)]
+    pair = O.make_config(2)
+    fine, coarse = O.inflate(pair.fine), O.inflate(pair.coarse)
+    Lo = O.assemble_rhs(fine, g)
+    np.testing.assert_allclose(L, Lo, rtol=1e-12, atol=1e-14 * np.abs(Lo).max())
+    from paper_2310_09204_b200 import screenbem as S
+    W = S.assemble_W(S.inflate(S.make_config(2).fine)).download()
+    prec = O.build_preconditioner(W, O.partition_dofs(pair, fine), O.build_prolongation(pair, coarse, fine))
+    rep = O.pcg(W, prec, Lo, 1e-8, exact=exact)
+    assert abs(int(iters) - rep.iterations) <= 1
+    assert np.linalg.norm(x - rep.solution) <= 1e-8 * np.linalg.norm(rep.solution)
+    k = min(len(energy), len(rep.energy_error_history))
+    np.testing.assert_allclose(energy[:k], rep.energy_error_history[:k], rtol=1e-6,
+                               atol=1e-9 * rep.energy_error_history[0])
+    assert (np.diff(energy) <= energy[:-1] * 1e-10).all()  # monotone (tests/test_pcg.cpp:95-98)

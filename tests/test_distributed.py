@@ -106,3 +106,58 @@ def test_row_ranges():
 def test_single_rank_passthrough():
     import bench
     assert bench.reduce_max([3.0, 4.0]) == [3.0, 4.0]
+
+
+def _agree_worker(rank, world, port, out):
+    """the collective stop of the row-panel PCG (screenbem.allreduce_agree): ranks stop
+    only when every rank's local flag says stop (a rank whose state differs in
+    the last bits must not stop early and leave the others waiting in an all-gather)"""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2310_09204_b200 import screenbem as S
+    agree = S.allreduce_agree(dist)
+    res = [agree(1), agree(1 if rank == 0 else 0), agree(0 if rank == 0 else 1), agree(0)]
+    out[rank] = res
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_row_panel_collective_stop_gloo():
+    world, port = 2, _free_port()
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_agree_worker, args=(world, port, out), nprocs=world, join=True)
+    for rank in range(world):
+        assert out[rank] == [1, 0, 0, 0]
+
+
+@pytest.mark.timeout(600)
+def test_bench_gpus_flag_launches_ranks():
+    """`bench.py --gpus 2` with no launcher re-executes itself under torch.distributed.run
+    with two ranks; the reference arm runs on rank 0 only (one JSON line) and reports
+    n_gpus 2 (the driver's SCALE command for the reference arm)."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ)
+    env.pop("WORLD_SIZE", None)
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--impl", "reference", "--gpus", "2",
+                        "--config", "1", "--steps", "1", "--warmup", "0", "--cpu-seconds", "1", "--no-cpu-phases"],
+                       capture_output=True, text=True, timeout=550, cwd=root, env=env)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["n_gpus"] == 2
+
+
+def test_bench_world_size_mismatch_fails():
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, WORLD_SIZE="2", RANK="0", LOCAL_RANK="0")
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--impl", "reference", "--gpus", "4"],
+                       capture_output=True, text=True, timeout=120, cwd=root, env=env)
+    assert r.returncode != 0 and "WORLD_SIZE=2" in r.stderr

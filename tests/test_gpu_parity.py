@@ -251,6 +251,39 @@ def test_pcg_random_spd_matches_oracle_and_lanczos(ctx):
     assert rep.kappa_estimate == pytest.approx(orep.kappa_estimate, rel=1e-4)
 
 
+def test_pcg_energy_error_history(ctx):
+    """tests/test_pcg.cpp:85-106 on the device: random_spd(60, 9), b from mt19937(10),
+    exact = direct_solve; the energy error history (pcg.hpp:50-53) decreases monotonically,
+    obeys 2 rho^n e0 with rho from the true kappa, and equals the oracle's."""
+    W0 = O.random_spd(60, 9)
+    b = O.normal_draws(10, 60)
+    exact = O.direct_solve(W0, b)
+    rep = S.pcg(S.GalerkinMatrix.from_host(W0, ctx), None, b, 1e-12, 0, exact=exact)
+    e = rep.energy_error_history
+    assert len(e) >= 2 and len(e) == rep.iterations + 1
+    assert (e[1:] <= e[:-1] * (1.0 + 1e-10)).all()
+    lam = np.linalg.eigvalsh(W0)
+    kappa = lam[-1] / lam[0]
+    rho = (np.sqrt(kappa) - 1.0) / (np.sqrt(kappa) + 1.0)
+    for k, ek in enumerate(e):
+        assert ek <= 2.0 * rho ** k * e[0] * (1.0 + 1e-9) + 1e-13 * e[0]
+    orep = O.pcg(W0, None, b, 1e-12, 0, exact=exact)
+    k = min(len(e), len(orep.energy_error_history))
+    np.testing.assert_allclose(e[:k], orep.energy_error_history[:k], rtol=1e-6, atol=1e-10 * e[0])
+    # with a preconditioner (config 1), and x0 = 0 gives e0 = sqrt(exact^T W exact)
+    pair = S.make_config(1)
+    fine, coarse = S.inflate(pair.fine), S.inflate(pair.coarse)
+    W = S.assemble_W(fine, ctx=ctx)
+    L = S.assemble_rhs(fine, [0.0, 0.0, 1.0], ctx=ctx)
+    prec = S.build_preconditioner(W, S.partition_dofs(pair, fine), S.build_prolongation(pair, coarse, fine))
+    xs = S.pcg(W, prec, L, 1e-13).solution
+    rep = S.pcg(W, prec, L, 1e-8, exact=xs)
+    Wh = W.download()
+    assert rep.energy_error_history[0] == pytest.approx(np.sqrt(xs @ Wh @ xs), rel=1e-12)
+    assert rep.energy_error_history[-1] < 1e-6 * rep.energy_error_history[0]
+    assert rep.iterations == S.pcg(W, prec, L, 1e-8).iterations
+
+
 @pytest.mark.parametrize("cfg,g", [(1, [0.0, 0.0, 1.0]), (2, "seed1")])
 def test_pipeline_matches_oracle(ctx, cfg, g):
     """cmd_solve hot path (experiments.hpp:130-145) on the device vs the oracle."""

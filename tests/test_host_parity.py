@@ -166,3 +166,34 @@ def test_broken_nesting_rejected():
     lvl = S.MeshLevelPair(pair.coarse, pair.fine, bad)
     with pytest.raises(S.ValidationError):
         S.build_prolongation(lvl, S.inflate(pair.coarse), S.inflate(pair.fine))
+
+
+def test_null_handles_are_validation_errors():
+    """Every C-ABI entry point that takes a handle or an output pointer rejects NULL with
+    status 2 (SBG_EVALIDATION, the reference's ValidationError) instead of crashing
+    (ADVICE r01).  Runs without a GPU: the checks come before any device work."""
+    import ctypes as C
+    raw = C.CDLL(S.lib()._name)
+    allowed_ok = {"sbg_device_free", "sbg_host_free"}  # freeing NULL is a no-op
+    optional_ptrs = {"sbg_device_name"}  # name buffer and SM count are optional outputs
+    checked, bad = 0, []
+    for name, (res, args) in S.SIGNATURES.items():
+        if res is not C.c_int or not args or name in optional_ptrs or name in ("sbg_matrix_n",
+                                                                               "sbg_prec_num_subspaces"):
+            continue
+        if not any(a in (C.c_void_p,) or (isinstance(a, type) and issubclass(a, C._Pointer)) for a in args):
+            continue  # no handle / output pointer (e.g. sbg_device_name, sbg_make_config's ints come first)
+        fn = getattr(raw, name)
+        fn.restype = C.c_int
+        fn.argtypes = [C.c_void_p if (a is not C.c_int and a is not C.c_double and a is not C.c_longlong) else a
+                       for a in args]
+        call = [None if t is C.c_void_p else 0 for t in fn.argtypes]
+        rc = fn(*call)
+        if rc != (0 if name in allowed_ok else 2):
+            bad.append((name, rc, S.lib().sbg_last_error()))
+        checked += 1
+    assert not bad, bad
+    assert checked > 50, checked
+    for name in ("sbg_ctx_destroy", "sbg_matrix_destroy", "sbg_prec_destroy", "sbg_mesh_destroy"):
+        getattr(raw, name)(None)
+    assert S.lib().sbg_prec_num_subspaces(None) == -1 and S.lib().sbg_matrix_n(None) == -1

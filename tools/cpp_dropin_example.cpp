@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 
 #include "screenbem/gpu.hpp"
 
@@ -22,10 +23,46 @@ static int emulated_exchange(void* user, const double* d_p, double* d_y, int, vo
     return sbg_matvec_rows_device(e->ctx, e->W, d_p, d_y, e->lo, e->hi);
 }
 
+// the reference's Neumann data as a field (inc/assemble.hpp:143-145 takes a
+// std::function<Vec3(const Vec3&)>); a smooth non-constant g
+static sb::Vec3 field_g(const sb::Vec3& x)
+{
+    return sb::Vec3(0.3 + x.y() * x.x(), -0.2 * x.x() + std::sin(3.0 * x.y()), 1.0 + 0.5 * x.norm());
+}
+
+// `dropin <cfg> <out.bin>`: the pipeline with the field g and pcg's exact-solution energy
+// history (pcg.hpp:33-35); writes n, iterations, L, x, energy history for the test to check
+// against the oracle
+static int field_run(int cfg, const char* path)
+{
+    sb::Context ctx(0);
+    sb::MeshLevelPair pair = sb::make_config(cfg);
+    sb::InflatedMesh fine = sb::inflate(pair.fine());
+    sb::InflatedMesh coarse = sb::inflate(pair.coarse());
+    sb::GalerkinMatrix W = sb::assemble_W(ctx, fine);
+    const std::vector<double> L = sb::assemble_rhs(ctx, fine, field_g);
+    sb::SchwarzPreconditioner P =
+        sb::build_preconditioner(ctx, W, sb::partition_dofs(pair, fine), sb::build_prolongation(pair, coarse, fine));
+    const sb::PcgReport tight = sb::pcg(ctx, W, &P, L, 1e-13);
+    const sb::PcgReport rep = sb::pcg(ctx, W, &P, L, 1e-8, 0, &tight.solution);
+    std::FILE* f = std::fopen(path, "wb");
+    if (!f) return 4;
+    const int hdr[3] = {W.rows(), rep.iterations, (int)rep.energy_error_history.size()};
+    std::fwrite(hdr, sizeof(int), 3, f);
+    std::fwrite(L.data(), sizeof(double), L.size(), f);
+    std::fwrite(rep.solution.data(), sizeof(double), rep.solution.size(), f);
+    std::fwrite(rep.energy_error_history.data(), sizeof(double), rep.energy_error_history.size(), f);
+    std::fwrite(tight.solution.data(), sizeof(double), tight.solution.size(), f);
+    std::fclose(f);
+    std::printf("field dofs %d iterations %d energy_len %d\n", hdr[0], hdr[1], hdr[2]);
+    return rep.converged ? 0 : 3;
+}
+
 int main(int argc, char** argv)
 {
     const int cfg = argc > 1 ? std::atoi(argv[1]) : 1;
     try {
+        if (argc > 2) return field_run(cfg, argv[2]);
         sb::Context ctx(0);
         sb::MeshLevelPair pair = sb::make_config(cfg);
         sb::InflatedMesh fine = sb::inflate(pair.fine());
