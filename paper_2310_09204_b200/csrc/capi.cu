@@ -161,7 +161,11 @@ int sbg_ctx_create(int device, sbg_ctx** out)
         c->c.sm_count = prop.multiProcessorCount;
         device_pool_init(device);
         // a blocking stream: the pool's legacy-stream allocations order against it (common.cuh)
-        SBG_CUDA(cudaStreamCreateWithFlags(&c->c.stream, cudaStreamDefault));
+        // highest priority: when the look-ahead's auxiliary stream (lowest priority) has
+        // blocks pending too, the main stream's critical-path blocks are scheduled first
+        int least = 0, greatest = 0;
+        SBG_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+        SBG_CUDA(cudaStreamCreateWithPriority(&c->c.stream, cudaStreamDefault, greatest));
         *out = c;
     });
 }

@@ -102,6 +102,7 @@ struct Ctx {
     int device = 0;
     int sm_count = kNumSMs;
     cudaStream_t stream = nullptr;
+    cudaStream_t aux = nullptr;  // second stream for look-ahead overlap (aux_stream(), created on first use)
     Timers timers;
     std::shared_ptr<void> pcg_ws;  // cached PCG workspace (linalg.cu)
     std::shared_ptr<void> dl_ws;   // cached pinned download ring (context.cu)

@@ -122,10 +122,26 @@ Timers::~Timers()
 
 Ctx::~Ctx()
 {
+    if (aux) {
+        cudaStreamSynchronize(aux);
+        cudaStreamDestroy(aux);
+    }
     if (stream) {
         cudaStreamSynchronize(stream);
         cudaStreamDestroy(stream);
     }
+}
+
+// a blocking stream too, so the stream-ordered pool's legacy-stream allocations order
+// against it (common.cuh)
+cudaStream_t aux_stream(Ctx* ctx)
+{
+    if (!ctx->aux) {
+        int least = 0, greatest = 0;
+        SBG_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+        SBG_CUDA(cudaStreamCreateWithPriority(&ctx->aux, cudaStreamDefault, least));
+    }
+    return ctx->aux;
 }
 
 TimedScope::TimedScope(Ctx* c, const char* n) : ctx(c), name(n)

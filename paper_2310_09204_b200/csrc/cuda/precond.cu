@@ -3,10 +3,12 @@
 //
 // All blocks — faces (map order), the wire-basket and the coarse matrix — form
 // one batch of dense SPD matrices stored as padded 64x64 tiles (identity on the
-// padded diagonal, so every tile is full).  Build: batched right-looking tiled
-// Cholesky — potrf of the diagonal tile (+ its inverse D_k), a "trsm" GEMM
-// A_ik <- A_ik D_k^T and the trailing update A_ij -= A_ik A_jk^T — with every
-// tile GEMM on the FP64 tensor cores (DMMA, mma.sync.m8n8k4.f64).
+// padded diagonal, so every tile is full).  Build: batched panel-blocked tiled
+// Cholesky — per tile column k ONE launch (k_panel_step) in which every CTA of the
+// column applies the in-panel updates left-looking, factors and inverts the diagonal
+// tile in shared memory (D_k = L_kk^-1) and forms its L_ik = A_ik D_k^T, plus one
+// trailing update A_ij -= sum_panel A_iq A_jq^T per completed panel of 8 tile columns
+// — with every tile GEMM on the FP64 tensor cores (DMMA, mma.sync.m8n8k4.f64).
 // Apply, two modes:
 //   * kPrecTrsv: blocked forward/backward triangular solves with L (the
 //     reference's llt.solve, schwarz.hpp:130), one launch per tile step;
@@ -17,6 +19,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cmath>
+#include <cstdlib>
 
 #include "kernels.cuh"
 
@@ -26,8 +29,18 @@ namespace {
 constexpr int TB = 64;   // tile size
 constexpr int TLD = 68;  // padded shared-memory leading dimension (conflict-free DMMA fragments)
 constexpr int GEMV_ROWS = 8;  // one row per warp
-constexpr int kPanel = 8;     // tile columns per panel of the blocked factorisation / inversion
-enum { K_TRSM = 0, K_UPDATE = 1, K_XDIAG = 2, K_LAUUM = 3, K_XUPD = 4 };
+// tile columns per panel of the blocked factorisation / inversion (SBG_PANEL overrides,
+// for measurements)
+int panel_width()
+{
+    static const int w = [] {
+        const char* e = std::getenv("SBG_PANEL");
+        const int v = e ? std::atoi(e) : 8;
+        return v >= 1 && v <= 64 ? v : 8;
+    }();
+    return w;
+}
+enum { K_UPDATE = 1, K_XSTEP = 2, K_LAUUM = 3, K_XUPD = 4 };
 struct GTask {
     int b, i, j, pad;
 };
@@ -102,7 +115,7 @@ __global__ void __launch_bounds__(256) k_gather_blocks(const double* __restrict_
 // partial row; pass 2 sums a column's chunk partials in ascending order
 // (deterministic).  Every row of W is read once per coarse column containing it
 // (<= 3 for P1 prolongations), with thousands of CTAs whatever H/h is.
-constexpr int kQC = 64, kIR = 2048;
+constexpr int kQC = 64, kIR = 1024;
 __global__ void __launch_bounds__(256) k_coarse_WR_chunks(const double* __restrict__ W, int ld, int n,
                                                           const int4* __restrict__ chunks,
                                                           const int* __restrict__ crow,
@@ -163,133 +176,6 @@ __global__ void __launch_bounds__(256) k_coarse_Ht(const double* __restrict__ WR
     }
 }
 
-// ---------------------------------------------------------------- Cholesky: diagonal tile
-// Factor tile (k,k) of each listed block in shared memory, write L_kk and its
-// inverse D_k (lower triangular, full 64x64 slot).
-__global__ void __launch_bounds__(256) k_potrf(int k, const int* __restrict__ blocks, const int* __restrict__ Tv,
-                                               const long long* __restrict__ Poff, const int* __restrict__ Doff,
-                                               double* __restrict__ Lp, double* __restrict__ D, int* __restrict__ fail)
-{
-    extern __shared__ double sm[];
-    double* a = sm;  // TB x (TB+1)
-    double* x = sm + TB * (TB + 1);
-    __shared__ int bad;
-    const int b = blocks[blockIdx.x];
-    const int ld = Tv[b] * TB;
-    double* Lt = Lp + Poff[b] + (size_t)k * TB * ld + (size_t)k * TB;
-    for (int e = threadIdx.x; e < TB * TB; e += blockDim.x) {
-        const int i = e / TB, j = e % TB;
-        a[i * (TB + 1) + j] = (j <= i) ? Lt[(size_t)i * ld + j] : 0.0;
-    }
-    if (threadIdx.x == 0) bad = 0;
-    __syncthreads();
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    constexpr int PW = 8;  // panel width
-    // blocked right-looking: warp 0 factors the 8-column panel (rows c0..63) with warp
-    // syncs only, then all threads apply the rank-8 update to the trailing lower part
-    for (int c0 = 0; c0 < TB; c0 += PW) {
-        if (warp == 0) {
-            for (int j = c0; j < c0 + PW; ++j) {
-                const double d = a[j * (TB + 1) + j];
-                if (lane == 0 && (!(d > 0.0) || !isfinite(d))) bad = 1;
-                const double djj = sqrt(d);
-                __syncwarp();
-                if (lane == 0) a[j * (TB + 1) + j] = djj;
-                for (int r = j + 1 + lane; r < TB; r += 32) a[r * (TB + 1) + j] /= djj;
-                __syncwarp();
-                for (int r = j + 1 + lane; r < TB; r += 32) {
-                    const double arj = a[r * (TB + 1) + j];
-                    for (int jj = j + 1; jj < c0 + PW && jj <= r; ++jj) a[r * (TB + 1) + jj] -= arj * a[jj * (TB + 1) + j];
-                }
-                __syncwarp();
-            }
-        }
-        __syncthreads();
-        const int t0 = c0 + PW, m = TB - t0;
-        for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
-            const int i = t0 + e / m, l = t0 + e % m;
-            if (l <= i) {
-                double acc = a[i * (TB + 1) + l];
-#pragma unroll
-                for (int q = 0; q < PW; ++q) acc -= a[i * (TB + 1) + c0 + q] * a[l * (TB + 1) + c0 + q];
-                a[i * (TB + 1) + l] = acc;
-            }
-        }
-        __syncthreads();
-    }
-    if (threadIdx.x == 0 && bad) atomicExch(&fail[b], 1);
-    for (int e = threadIdx.x; e < TB * TB; e += blockDim.x) {
-        const int i = e / TB, j = e % TB;
-        Lt[(size_t)i * ld + j] = (j <= i) ? a[i * (TB + 1) + j] : 0.0;
-    }
-    // X = L^-1 blocked by 8x8: diagonal blocks by one warp each (lane = column), then
-    // block row i: S_ij = sum_{q=j}^{i-1} L_iq X_qj, X_ij = -X_ii S_ij, one element per thread
-    for (int e = threadIdx.x; e < TB * TB; e += blockDim.x) x[(e / TB) * (TB + 1) + (e % TB)] = 0.0;
-    __syncthreads();
-    {
-        const int o = warp * PW;  // block `warp`
-        if (lane < PW) {
-            const int c = o + lane;
-            x[c * (TB + 1) + c] = 1.0 / a[c * (TB + 1) + c];
-            for (int i = c + 1; i < o + PW; ++i) {
-                double sacc = 0.0;
-                for (int l = c; l < i; ++l) sacc += a[i * (TB + 1) + l] * x[l * (TB + 1) + c];
-                x[i * (TB + 1) + c] = -sacc / a[i * (TB + 1) + i];
-            }
-        }
-    }
-    __syncthreads();
-    for (int bi = 1; bi < TB / PW; ++bi) {
-        // S_{bi,bj} (bj < bi), element (r, c): at most 7 * 64 = 448 elements, <= 2 per thread
-        const int total = bi * PW * PW;
-        double sv[2] = {0.0, 0.0};
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const int e = threadIdx.x + h * 256;
-            if (e < total) {
-                const int bj = e / (PW * PW), r = (e / PW) % PW, c = e % PW;
-                const int row = bi * PW + r, col = bj * PW + c;
-                double acc = 0.0;
-                for (int l = bj * PW; l < bi * PW; ++l) acc += a[row * (TB + 1) + l] * x[l * (TB + 1) + col];
-                sv[h] = acc;
-            }
-        }
-        __syncthreads();
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {  // S into the (still zero) X_{bi,bj} slots
-            const int e = threadIdx.x + h * 256;
-            if (e < total) {
-                const int bj = e / (PW * PW), r = (e / PW) % PW, c = e % PW;
-                x[(bi * PW + r) * (TB + 1) + bj * PW + c] = sv[h];
-            }
-        }
-        __syncthreads();
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {  // X_{bi,bj} = -X_ii S
-            const int e = threadIdx.x + h * 256;
-            if (e < total) {
-                const int bj = e / (PW * PW), r = (e / PW) % PW, c = e % PW;
-                double acc = 0.0;
-                for (int q = 0; q <= r; ++q)
-                    acc += x[(bi * PW + r) * (TB + 1) + bi * PW + q] * x[(bi * PW + q) * (TB + 1) + bj * PW + c];
-                sv[h] = -acc;
-            }
-        }
-        __syncthreads();
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const int e = threadIdx.x + h * 256;
-            if (e < total) {
-                const int bj = e / (PW * PW), r = (e / PW) % PW, c = e % PW;
-                x[(bi * PW + r) * (TB + 1) + bj * PW + c] = sv[h];
-            }
-        }
-        __syncthreads();
-    }
-    double* Dt = D + Doff[b] + (size_t)k * TB * TB;
-    for (int e = threadIdx.x; e < TB * TB; e += blockDim.x) Dt[e] = x[(e / TB) * (TB + 1) + (e % TB)];
-}
-
 // ---------------------------------------------------------------- tile GEMMs on DMMA
 // 64x64 output tile per CTA (4 warps x 32x32), K streamed in half tiles of 32 through a
 // two-stage cp.async pipeline.  Operands are staged as plain row copies in either
@@ -337,6 +223,7 @@ template <bool AK, bool BK>
 __device__ __forceinline__ void mma_half(const double* __restrict__ As, const double* __restrict__ Bs,
                                          double (&acc)[4][4][2])
 {
+    if (threadIdx.x >= 128) return;  // the 64x64 tile is 4 warps' work (wider CTAs: extra warps idle)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int gid = lane >> 2, tig = lane & 3;
     const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
@@ -388,6 +275,7 @@ __device__ __forceinline__ void gemm_pipeline(double* sm, int nq, FA tileA, FB t
 template <class F>
 __device__ __forceinline__ void for_acc(const double (&acc)[4][4][2], F f)
 {
+    if (threadIdx.x >= 128) return;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int gid = lane >> 2, tig = lane & 3;
     const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
@@ -399,9 +287,200 @@ __device__ __forceinline__ void for_acc(const double (&acc)[4][4][2], F f)
             for (int h = 0; h < 2; ++h) f(wm + 8 * x + gid, wn + 8 * y + 2 * tig + h, acc[x][y][h]);
 }
 
-// KIND K_TRSM  : L(i,k) = L(i,k) D_k^T            (task.i = i)
-//      K_UPDATE: L(i,j) -= sum_{q=k0}^{k1-1} L(i,q) L(j,q)^T   (task.i, task.j, K range in task.pad)
-//      K_XDIAG : X(i,j) = -D_i S(i,j) (S accumulated in X), X(i,i) = D_i   (step k = i)
+// ---------------------------------------------------------------- Cholesky: fused panel step
+// Factor the 64x64 SPD tile a[] (lower part valid, row stride AS) and form its inverse:
+// right-looking elimination in LDL^T form — multipliers m_rj = a_rj / a_jj, Schur update
+// a_rc -= m_rj a_cj for j < c <= r — fused with the same eliminations applied to [L | I],
+// whose rows Y_r = L_rr (L^-1)_r obey Y_r = e_r - sum_{j<r} m_rj Y_j (the multipliers are
+// L_rj / L_jj).  256 threads, each owning a 4x4 register block of the tile: element (r,c)
+// holds a_rc until column c is eliminated and Y_rc from then on, so every step is the same
+// rank-1 update x -= m_r o_c of the whole block, with o = column j of a (c > j) or row j of
+// Y (c <= j).  Column j (zero above the diagonal, the pivot kept apart) and row j of Y are
+// published at the end of step j-1 into double-buffered shared vectors: ONE barrier per
+// column.  On exit a[r][c] (r >= c) holds the eliminated columns (a[j][j] = pivot p_j,
+// L_jj = sqrt(p_j), L_rc = a_rc / L_cc) and x[][] the thread's 4x4 block of Y; returns
+// false (all threads) if a pivot is not positive and finite.
+constexpr int AS = TB + 1;  // row stride of the tile in shared memory
+constexpr int kFactorThreads = 256;
+struct FactorBufs {
+    double col[2][TB], yrow[2][TB], piv[2], inv[2];
+};
+// 4x4 block of thread t: column block t >> 4 (so a column's 16 owners are one half warp,
+// and only that warp takes the publishing branch), row block t & 15
+__device__ __forceinline__ int blk_r0() { return (threadIdx.x & 15) * 4; }
+__device__ __forceinline__ int blk_c0() { return (threadIdx.x >> 4) * 4; }
+__device__ bool tile_ldl_inverse(double* __restrict__ a, FactorBufs& fb, double (&x)[4][4])
+{
+    const int r0 = blk_r0(), c0 = blk_c0();
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) x[u][v] = a[(r0 + u) * AS + c0 + v];
+    // publish column 0 (pivot apart, rows <= 0 zero) and row 0 of Y for step 0
+    auto publish = [&](int jn, int buf) {
+        if (c0 <= jn && jn < c0 + 4) {
+#pragma unroll
+            for (int v = 0; v < 4; ++v)
+                if (c0 + v == jn) {
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int r = r0 + u;
+                        fb.col[buf][r] = r > jn ? x[u][v] : 0.0;
+                        if (r >= jn) a[r * AS + jn] = x[u][v];
+                        if (r == jn) {
+                            fb.piv[buf] = x[u][v];
+                            fb.inv[buf] = 1.0 / x[u][v];
+                        }
+                        x[u][v] = r == jn ? 1.0 : 0.0;  // element (r, jn) becomes Y_{r,jn}: delta
+                    }
+                }
+        }
+        if (r0 <= jn && jn < r0 + 4) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (r0 + u == jn)
+#pragma unroll
+                    for (int v = 0; v < 4; ++v) fb.yrow[buf][c0 + v] = x[u][v];
+        }
+    };
+    publish(0, 0);
+    __syncthreads();
+    bool ok = true;
+    for (int j = 0; j < TB; ++j) {
+        const int cur = j & 1;
+        const double p = fb.piv[cur];
+        ok = ok && p > 0.0 && isfinite(p);
+        if (r0 + 3 > j) {  // some row r > j of this block is still active (m_r = 0 otherwise)
+            const double inv = fb.inv[cur];
+            double m[4], o[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) m[u] = fb.col[cur][r0 + u] * inv;
+#pragma unroll
+            for (int v = 0; v < 4; ++v) o[v] = c0 + v > j ? fb.col[cur][c0 + v] : fb.yrow[cur][c0 + v];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+                for (int v = 0; v < 4; ++v) x[u][v] = fma(-m[u], o[v], x[u][v]);
+        }
+        if (j + 1 < TB) publish(j + 1, cur ^ 1);
+        __syncthreads();
+    }
+    return ok;
+}
+
+// One step k of the panel-blocked Cholesky (panel [p0, p0 + kPanel)), all blocks and all
+// tile rows i >= k of column k in one launch, task (block, i):
+//   diag  A(k,k) - sum_{q=p0}^{k-1} L(k,q) L(k,q)^T   (left-looking inside the panel,
+//         recomputed by every CTA of the column: no potrf launch and no inter-CTA wait)
+//   own   A(i,k) - sum_{q=p0}^{k-1} L(i,q) L(k,q)^T   (i > k)
+// then the diagonal tile is factored and inverted in shared memory (tile_ldl_inverse),
+// CTA (b, k) stores L_kk (into Ld: the diagonal tile is still being read by the other
+// CTAs of the step) and D_k = L_kk^-1, and CTA (b, i > k) forms L(i,k) = own D_k^T on DMMA
+// with D_k taken straight from shared memory.  The previous panels' contributions came in
+// through the panel-end trailing updates (K_UPDATE, K = the whole panel).
+constexpr size_t STEP_SMEM = GEMM_SMEM + (size_t)TB * AS * sizeof(double) + TB * sizeof(double);
+constexpr int kStepThreads = kFactorThreads;  // 8 warps: 4x4 blocks of the tile factor; the GEMMs use warps 0-3
+__global__ void __launch_bounds__(kStepThreads) k_panel_step(int k, int p0, const GTask* __restrict__ tasks,
+                                                    const int* __restrict__ Tv, const long long* __restrict__ Poff,
+                                                    const int* __restrict__ Doff, double* __restrict__ Lp,
+                                                    double* __restrict__ D, double* __restrict__ Ld,
+                                                    int* __restrict__ fail)
+{
+    extern __shared__ __align__(16) double sm[];
+    double* stg = sm;  // 4 half-tile staging buffers (GEMM pipeline, then the trsm operands)
+    double* a = sm + 4 * HBUF;
+    double* sq = a + TB * AS;
+    __shared__ FactorBufs fb;
+    const GTask t = tasks[blockIdx.x];
+    const int b = t.b, i = t.i;
+    const size_t ld = (size_t)Tv[b] * TB;
+    double* L = Lp + Poff[b];
+    auto tile = [&](int ti, int tj) { return L + (size_t)ti * TB * ld + (size_t)tj * TB; };
+    const int nq = k - p0;
+    double acc[4][4][2];
+#pragma unroll
+    for (int x = 0; x < 4; ++x)
+#pragma unroll
+        for (int z = 0; z < 4; ++z) acc[x][z][0] = acc[x][z][1] = 0.0;
+    gemm_pipeline<false, false>(
+        stg, nq, [&](int q) { return (const double*)tile(k, p0 + q); },
+        [&](int q) { return (const double*)tile(k, p0 + q); }, ld, ld, acc);
+    {
+        const double* Akk = tile(k, k);
+        for_acc(acc, [&](int r, int c, double v) { a[r * AS + c] = (c <= r) ? Akk[(size_t)r * ld + c] - v : 0.0; });
+    }
+    if (i != k) {
+#pragma unroll
+        for (int x = 0; x < 4; ++x)
+#pragma unroll
+            for (int z = 0; z < 4; ++z) acc[x][z][0] = acc[x][z][1] = 0.0;
+        gemm_pipeline<false, false>(
+            stg, nq, [&](int q) { return (const double*)tile(i, p0 + q); },
+            [&](int q) { return (const double*)tile(k, p0 + q); }, ld, ld, acc);
+        const double* Aik = tile(i, k);
+        // the updated A(i,k) as the trsm's A operand: [m][k] half tiles in stg[0], stg[HBUF]
+        for_acc(acc, [&](int r, int c, double v) {
+            stg[(c >> 5) * HBUF + r * HS_MK + (c & 31)] = Aik[(size_t)r * ld + c] - v;
+        });
+    }
+    __syncthreads();
+    double x[4][4];
+    const bool ok = tile_ldl_inverse(a, fb, x);
+    if (threadIdx.x < TB) sq[threadIdx.x] = sqrt(a[threadIdx.x * AS + threadIdx.x]);
+    __syncthreads();
+    const int r0 = blk_r0(), c0 = blk_c0();
+    if (i == k) {
+        double* Lkk = Ld + Doff[b] + (size_t)k * TB * TB;
+        double* Dk = D + Doff[b] + (size_t)k * TB * TB;
+        for (int e = threadIdx.x; e < TB * TB; e += blockDim.x) {
+            const int r = e / TB, c = e % TB;
+            Lkk[e] = c < r ? a[r * AS + c] / sq[c] : (c == r ? sq[r] : 0.0);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+                const int r = r0 + u, c = c0 + v;
+                Dk[r * TB + c] = c <= r ? x[u][v] / sq[r] : 0.0;
+            }
+        if (threadIdx.x == 0 && !ok) atomicExch(&fail[b], 1);
+        return;
+    }
+    // D_k = L_kk^-1 as the trsm's B operand ([n][k] half tiles: row n of D_k)
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+            const int r = r0 + u, c = c0 + v;
+            stg[(2 + (c >> 5)) * HBUF + r * HS_MK + (c & 31)] = c <= r ? x[u][v] / sq[r] : 0.0;
+        }
+    __syncthreads();
+#pragma unroll
+    for (int x = 0; x < 4; ++x)
+#pragma unroll
+        for (int z = 0; z < 4; ++z) acc[x][z][0] = acc[x][z][1] = 0.0;
+    mma_half<false, false>(stg, stg + 2 * HBUF, acc);
+    mma_half<false, false>(stg + HBUF, stg + 3 * HBUF, acc);
+    double* C = tile(i, k);
+    for_acc(acc, [&](int r, int c, double v) { C[(size_t)r * ld + c] = v; });
+}
+
+// diagonal tiles L_kk from Ld into the factor (after the factorisation)
+__global__ void k_put_diag(const int* __restrict__ Tv, const long long* __restrict__ Poff,
+                           const int* __restrict__ Doff, const double* __restrict__ Ld, double* __restrict__ Lp)
+{
+    const int b = blockIdx.y, k = blockIdx.x;
+    const int T = Tv[b];
+    if (k >= T) return;
+    const size_t ld = (size_t)T * TB;
+    double* dst = Lp + Poff[b] + (size_t)k * TB * ld + (size_t)k * TB;
+    const double* src = Ld + Doff[b] + (size_t)k * TB * TB;
+    for (int e = threadIdx.x; e < TB * TB; e += blockDim.x) dst[(size_t)(e / TB) * ld + (e % TB)] = src[e];
+}
+
+// KIND K_UPDATE: L(i,j) -= sum_{q=k0}^{k1-1} L(i,q) L(j,q)^T   (task.i, task.j, K range in task.pad)
+//      K_XSTEP : X(i,j) = -D_i (S(i,j) + sum_{q=k0}^{i-1} L(i,q) X(q,j)), X(i,i) = D_i  (step k = i;
+//                S = the earlier panels' part, accumulated in X; left-looking inside the panel)
 //      K_XUPD  : X(i',j) += sum_{q=k0}^{k1-1} L(i',q) X(q,j)          (K range in task.pad)
 //                (right-looking blocked L^-1: X(i,j) = -D_i sum_{q=j}^{i-1} L(i,q) X(q,j))
 //      K_LAUUM : M(i,j) = sum_{q=i}^{T-1} X(q,i)^T X(q,j)   (written over L)
@@ -425,29 +504,39 @@ __global__ void __launch_bounds__(128) k_tile_gemm(int k, const GTask* __restric
 #pragma unroll
         for (int y = 0; y < 4; ++y) acc[x][y][0] = acc[x][y][1] = 0.0;
 
-    if (KIND == K_TRSM) {
-        gemm_pipeline<false, false>(
-            sm, 1, [&](int) { return (const double*)tile(L, t.i, k); },
-            [&](int) { return Db + (size_t)k * TB * TB; }, ld, (size_t)TB, acc);
-        double* C = tile(L, t.i, k);
-        for_acc(acc, [&](int r, int c, double v) { C[(size_t)r * ld + c] = v; });
-    } else if (KIND == K_UPDATE) {  // K range [k0, k1) packed in t.pad (panel-blocked trailing update)
+    if (KIND == K_UPDATE) {  // K range [k0, k1) packed in t.pad (panel-blocked trailing update)
         const int k0 = t.pad >> 16, k1 = t.pad & 0xffff;
         gemm_pipeline<false, false>(
             sm, k1 - k0, [&](int q) { return (const double*)tile(L, t.i, k0 + q); },
             [&](int q) { return (const double*)tile(L, t.j, k0 + q); }, ld, ld, acc);
         double* C = tile(L, t.i, t.j);
         for_acc(acc, [&](int r, int c, double v) { C[(size_t)r * ld + c] -= v; });
-    } else if (KIND == K_XDIAG) {
+    } else if (KIND == K_XSTEP) {  // in-panel K range [k0, t.i) packed in t.pad
         double* C = tile(X, t.i, t.j);
+        const double* Di = Db + (size_t)t.i * TB * TB;
         if (t.i == t.j) {
-            const double* Di = Db + (size_t)t.i * TB * TB;
             for (int e = threadIdx.x; e < TB * TB; e += blockDim.x) C[(size_t)(e / TB) * ld + (e % TB)] = Di[e];
             return;
         }
+        const int k0 = t.pad >> 16, k1 = t.pad & 0xffff;
         gemm_pipeline<false, true>(
-            sm, 1, [&](int) { return Db + (size_t)t.i * TB * TB; }, [&](int) { return (const double*)C; },
-            (size_t)TB, ld, acc);
+            sm, k1 - k0, [&](int q) { return (const double*)tile(L, t.i, k0 + q); },
+            [&](int q) { return (const double*)tile(X, k0 + q, t.j); }, ld, ld, acc);
+        // D_i as the A operand ([m][k] halves, cp.async) and S + acc as the B operand ([k][n])
+        stage_half<false>(sm, Di, (size_t)TB, 0);
+        stage_half<false>(sm + HBUF, Di, (size_t)TB, 1);
+        cp_commit();
+        for_acc(acc, [&](int r, int c, double v) {
+            sm[(2 + (r >> 5)) * HBUF + (r & 31) * HS_KM + c] = C[(size_t)r * ld + c] + v;
+        });
+        cp_wait<0>();
+        __syncthreads();
+#pragma unroll
+        for (int x = 0; x < 4; ++x)
+#pragma unroll
+            for (int y = 0; y < 4; ++y) acc[x][y][0] = acc[x][y][1] = 0.0;
+        mma_half<false, true>(sm, sm + 2 * HBUF, acc);
+        mma_half<false, true>(sm + HBUF, sm + 3 * HBUF, acc);
         for_acc(acc, [&](int r, int c, double v) { C[(size_t)r * ld + c] = -v; });
     } else if (KIND == K_XUPD) {  // K range [k0, k1) packed in t.pad
         const int k0 = t.pad >> 16, k1 = t.pad & 0xffff;
@@ -703,8 +792,9 @@ __global__ void k_prec_scatter(const double* __restrict__ locy, const int* __res
 }
 
 // H = R^T W R (schwarz.hpp:110-116 with the sparse R) into a padded ldh x ldh block
-void coarse_galerkin_device(Ctx* ctx, const DMatrix& W, const std::vector<int>& col_ptr, const int* cptr,
-                            const int* crow, const double* cval, int nc, int ldh, double* H)
+void coarse_galerkin_device(Ctx* ctx, const DMatrix& W, const std::vector<int>& col_ptr,
+                            const std::vector<int>& row_idx, const int* cptr, const int* crow, const double* cval,
+                            int nc, int ldh, double* H)
 {
     const int n = W.n;
     cudaStream_t s = ctx->stream;
@@ -715,6 +805,11 @@ void coarse_galerkin_device(Ctx* ctx, const DMatrix& W, const std::vector<int>& 
             chunks.push_back(make_int4(c, q, std::min(q + kQC, col_ptr[c + 1]), (int)chunks.size()));
         cfirst.push_back((int)chunks.size());
     }
+    // launch order by first support row: the (<= 3) chunks of different coarse columns that
+    // stream the same rows of W run back to back, so the re-reads hit L2 instead of HBM
+    // (the partial index .w keeps the column order of the reduction: deterministic)
+    std::stable_sort(chunks.begin(), chunks.end(),
+                     [&](const int4& a, const int4& b) { return row_idx[a.y] < row_idx[b.y]; });
     double* WRt = scratch(ctx, kScratchCoarseWR, (size_t)n * std::max(nc, 1));
     if (!chunks.empty()) {
         DBuf<int4> d_chunks;
@@ -739,17 +834,61 @@ void coarse_galerkin_device(Ctx* ctx, const DMatrix& W, const std::vector<int>& 
     SBG_CUDA(cudaStreamSynchronize(s));
 }
 
+// far = a look-ahead far update: its CTAs reserve FAR_SMEM of shared memory, so at most one
+// sits on an SM and a critical-path CTA (STEP_SMEM or GEMM_SMEM) always fits beside it
+constexpr size_t FAR_SMEM = 227 * 1024 - STEP_SMEM - 4096;
 template <int KIND>
-void launch_gemm(Ctx* ctx, Prec* P, int k, const GTask* dev_tasks, int count, double* Lp, double* Xp)
+void launch_gemm(Ctx* ctx, Prec* P, int k, const GTask* dev_tasks, int count, double* Lp, double* Xp,
+                 cudaStream_t st = nullptr, bool far = false)
 {
     if (count <= 0) return;
-    const size_t smem = GEMM_SMEM;
+    const size_t smem = far ? std::max(GEMM_SMEM, FAR_SMEM) : GEMM_SMEM;
     set_max_dynamic_smem(k_tile_gemm<KIND>, smem);
-    k_tile_gemm<KIND><<<count, 128, smem, ctx->stream>>>(k, dev_tasks, P->d_T.p, P->d_Poff.p, P->d_Doff.p, Lp, Xp,
-                                                        P->D.p);
+    k_tile_gemm<KIND><<<count, 128, smem, st ? st : ctx->stream>>>(k, dev_tasks, P->d_T.p, P->d_Poff.p, P->d_Doff.p,
+                                                                  Lp, Xp, P->D.p);
     count_launch();
     SBG_LAUNCH_CHECK();
 }
+
+// Panel look-ahead on two streams.  At a panel end the trailing update is split into the
+// next panel's tiles ("near", on the main stream, ahead of the next panel's steps) and all
+// tiles beyond it ("far", on the context's auxiliary stream), so the far update — the bulk
+// of the flops — runs beside the next panel's chain of latency-bound steps.  Ordering:
+// a far update waits for its panel's last step; the next near update waits for the
+// previous far update (both read-modify-write the tiles of the panel after next).
+struct Lookahead {
+    Ctx* ctx;
+    cudaStream_t main, aux;
+    cudaEvent_t done_steps = nullptr, far_done = nullptr;
+    bool far_pending = false;
+    explicit Lookahead(Ctx* c) : ctx(c), main(c->stream), aux(aux_stream(c))
+    {
+        SBG_CUDA(cudaEventCreateWithFlags(&done_steps, cudaEventDisableTiming));
+        SBG_CUDA(cudaEventCreateWithFlags(&far_done, cudaEventDisableTiming));
+    }
+    ~Lookahead()
+    {
+        cudaEventDestroy(done_steps);
+        cudaEventDestroy(far_done);
+    }
+    // at a panel end: enqueue_far(aux) after the steps so far; near(main) after the previous far
+    template <class Near, class Far>
+    void panel_end(Near near, Far far)
+    {
+        SBG_CUDA(cudaEventRecord(done_steps, main));
+        if (far_pending) SBG_CUDA(cudaStreamWaitEvent(main, far_done, 0));
+        near(main);
+        SBG_CUDA(cudaStreamWaitEvent(aux, done_steps, 0));
+        far(aux);
+        SBG_CUDA(cudaEventRecord(far_done, aux));
+        far_pending = true;
+    }
+    void join()
+    {
+        if (far_pending) SBG_CUDA(cudaStreamWaitEvent(main, far_done, 0));
+        far_pending = false;
+    }
+};
 
 // per-step task lists, built on the host once and uploaded in one copy
 struct StepTasks {
@@ -765,21 +904,20 @@ struct StepTasks {
 struct PrecSchedule {
     std::vector<int> key;  // ngather, then n_b of every block
     std::vector<int2> gather;                // (block, first row), 8 rows each
-    std::vector<int> pot, pot_off{0};        // potrf blocks per step
-    StepTasks trsm, upd, xd, xu;
+    StepTasks pt, upd, upd_far, xd, xu;  // panel steps, trailing updates (near / far), L^-1 steps
     std::vector<GTask> la;
     std::vector<int4> ct;                    // compact-inverse 32x32 output tiles
     std::vector<int2> gemv, fw, bw;
     std::vector<int> fw_off{0}, bw_off{0};
     DBuf<int2> d_gather, d_gemv, d_fw, d_bw;
-    DBuf<int> d_pot;
-    DBuf<GTask> d_trsm, d_upd, d_xd, d_xu, d_la;
+    DBuf<GTask> d_pt, d_upd, d_upd_far, d_xd, d_xu, d_la;
     DBuf<int4> d_ct;
 };
 
 std::shared_ptr<PrecSchedule> prec_schedule(Ctx* ctx, const Prec* P)
 {
-    std::vector<int> key{P->ngather};
+    const int kPanel = panel_width();
+    std::vector<int> key{P->ngather, kPanel};
     key.insert(key.end(), P->h_nb.begin(), P->h_nb.end());
     if (auto* c = static_cast<std::shared_ptr<PrecSchedule>*>(ctx->prec_sched.get()))
         if (*c && (*c)->key == key) return *c;
@@ -788,42 +926,37 @@ std::shared_ptr<PrecSchedule> prec_schedule(Ctx* ctx, const Prec* P)
     const int nb = P->nblocks;
     for (int b = 0; b < P->ngather; ++b)
         for (int r = 0; r < P->h_T[b] * TB; r += 8) S->gather.push_back({b, r});
-    // Cholesky: panel-blocked right-looking (see prec_build)
+    // Cholesky: panel-blocked, left-looking inside a panel (k_panel_step: every tile of
+    // column k, diagonal included, in one launch) and one right-looking trailing update
+    // with K = the whole panel when a panel completes (see prec_build)
     for (int k = 0; k < P->Tmax; ++k) {
         const int p0 = k - k % kPanel;
         for (int b = 0; b < nb; ++b) {
             const int T = P->h_T[b];
             if (T <= k) continue;
-            S->pot.push_back(b);
-            for (int i = k + 1; i < T; ++i) S->trsm.all.push_back({b, i, k, 0});
+            for (int i = k; i < T; ++i) S->pt.all.push_back({b, i, k, 0});
             const int p1 = std::min(p0 + kPanel, T);
-            if (k + 1 < p1) {
-                for (int j = k + 1; j < p1; ++j)
-                    for (int i = j; i < T; ++i) S->upd.all.push_back({b, i, j, (k << 16) | (k + 1)});
-            } else {
+            if (k + 1 == p1)  // near: the next panel's columns; far: the columns beyond
                 for (int j = p1; j < T; ++j)
-                    for (int i = j; i < T; ++i) S->upd.all.push_back({b, i, j, (p0 << 16) | p1});
-            }
+                    for (int i = j; i < T; ++i)
+                        (j < p1 + kPanel ? S->upd : S->upd_far).all.push_back({b, i, j, (p0 << 16) | p1});
         }
-        S->pot_off.push_back((int)S->pot.size());
-        S->trsm.close();
+        S->pt.close();
         S->upd.close();
+        S->upd_far.close();
     }
-    // blocked L^-1 (right-looking by panels), then L^-T L^-1
+    // blocked L^-1 (left-looking inside a panel, one trailing update per panel), then L^-T L^-1
     for (int k = 0; k < P->Tmax; ++k) {
         const int p0 = k - k % kPanel;
         for (int b = 0; b < nb; ++b) {
             const int T = P->h_T[b];
             if (T <= k) continue;
-            for (int j = 0; j <= k; ++j) S->xd.all.push_back({b, k, j, 0});
+            // row k of X in one launch: the in-panel rows q in [max(p0, j), k) left-looking
+            for (int j = 0; j <= k; ++j) S->xd.all.push_back({b, k, j, (std::max(p0, j) << 16) | k});
             const int p1 = std::min(p0 + kPanel, T);
-            if (k + 1 < p1) {  // rows inside the panel: the contribution of row k only
-                for (int i = k + 1; i < p1; ++i)
-                    for (int j = 0; j <= k; ++j) S->xu.all.push_back({b, i, j, (k << 16) | (k + 1)});
-            } else {  // panel complete: rows below take K = the panel rows at once
+            if (k + 1 == p1)  // panel complete: rows below take K = the panel rows at once
                 for (int i = p1; i < T; ++i)
                     for (int j = 0; j < p1; ++j) S->xu.all.push_back({b, i, j, (std::max(p0, j) << 16) | p1});
-            }
         }
         S->xd.close();
         S->xu.close();
@@ -852,9 +985,9 @@ std::shared_ptr<PrecSchedule> prec_schedule(Ctx* ctx, const Prec* P)
     }
     cudaStream_t s = ctx->stream;
     S->d_gather.upload(S->gather, s);
-    S->d_pot.upload(S->pot, s);
-    S->d_trsm.upload(S->trsm.all, s);
+    S->d_pt.upload(S->pt.all, s);
     S->d_upd.upload(S->upd.all, s);
+    S->d_upd_far.upload(S->upd_far.all, s);
     S->d_xd.upload(S->xd.all, s);
     S->d_xu.upload(S->xu.all, s);
     S->d_la.upload(S->la, s);
@@ -868,7 +1001,7 @@ std::shared_ptr<PrecSchedule> prec_schedule(Ctx* ctx, const Prec* P)
 }
 
 // W_bb^-1 = L^-T L^-1 for every block from the tiled factor in Lwork (overwritten):
-// X = L^-1 right-looking in one-stage tile tasks, then M = X^T X over Lwork, then
+// X = L^-1 by panels (K_XSTEP per row of tiles, K_XUPD at panel ends), then M = X^T X over Lwork, then
 // the compact row-major inverses (row stride ldm_b) into Mc.
 void form_inverses(Ctx* ctx, Prec* P, DBuf<double>& Lwork, DBuf<double>& Mc)
 {
@@ -884,8 +1017,9 @@ void form_inverses(Ctx* ctx, Prec* P, DBuf<double>& Lwork, DBuf<double>& Mc)
     } Xp{Xp_p};
     {
         TimedScope t1(ctx, "inv_lower");
+        // (the factorisation's two-stream look-ahead measured no faster here)
         for (int k = 0; k < P->Tmax; ++k) {
-            launch_gemm<K_XDIAG>(ctx, P, k, S.d_xd.p + S.xd.off[k], S.xd.count(k), Lwork.p, Xp.p);
+            launch_gemm<K_XSTEP>(ctx, P, k, S.d_xd.p + S.xd.off[k], S.xd.count(k), Lwork.p, Xp.p);
             launch_gemm<K_XUPD>(ctx, P, k, S.d_xu.p + S.xu.off[k], S.xu.count(k), Lwork.p, Xp.p);
         }
     }
@@ -1016,7 +1150,7 @@ Prec* prec_build(Ctx* ctx, const DMatrix& W, const DofPartition& part, const Pro
             P->Rr_val.upload(rval, s);
             TimedScope ts(ctx, "coarse_galerkin");
             const int ldh = P->h_T[P->coarse_block] * TB;
-            coarse_galerkin_device(ctx, W, R.col_ptr, P->Rc_ptr.p, P->Rc_row.p, P->Rc_val.p, P->nc, ldh,
+            coarse_galerkin_device(ctx, W, R.col_ptr, R.row_idx, P->Rc_ptr.p, P->Rc_row.p, P->Rc_val.p, P->nc, ldh,
                                    P->Lp.p + P->h_Poff[P->coarse_block]);
         }
         // ---- batched tiled Cholesky: per step k, potrf of tile (k,k), trsm of column k, trailing update
@@ -1024,19 +1158,33 @@ Prec* prec_build(Ctx* ctx, const DMatrix& W, const DofPartition& part, const Pro
         SBG_CUDA(cudaMemsetAsync(fail.p, 0, fail.n * sizeof(int), s));
         {
             TimedScope ts(ctx, "cholesky");
-            const size_t smem_potrf = 2 * TB * (TB + 1) * sizeof(double);
-            set_max_dynamic_smem(k_potrf, smem_potrf);
-            // panel-blocked right-looking (task lists in the schedule): inside a panel of
-            // kPanel tile columns only the panel's own columns are updated per step; the
-            // trailing matrix takes one update with K = the whole panel when it is complete
+            set_max_dynamic_smem(k_panel_step, STEP_SMEM);
+            DBuf<double> Ld(std::max(P->D.n, (size_t)1));
+            Lookahead la(ctx);
             for (int k = 0; k < P->Tmax; ++k) {
-                k_potrf<<<S.pot_off[k + 1] - S.pot_off[k], 256, smem_potrf, s>>>(
-                    k, S.d_pot.p + S.pot_off[k], P->d_T.p, P->d_Poff.p, P->d_Doff.p, P->Lp.p, P->D.p, fail.p);
-                count_launch();
-                SBG_LAUNCH_CHECK();
-                launch_gemm<K_TRSM>(ctx, P, k, S.d_trsm.p + S.trsm.off[k], S.trsm.count(k), P->Lp.p, nullptr);
-                launch_gemm<K_UPDATE>(ctx, P, k, S.d_upd.p + S.upd.off[k], S.upd.count(k), P->Lp.p, nullptr);
+                const int cnt = S.pt.count(k);
+                if (cnt) {
+                    k_panel_step<<<cnt, kStepThreads, STEP_SMEM, s>>>(k, k - k % panel_width(), S.d_pt.p + S.pt.off[k],
+                                                                      P->d_T.p, P->d_Poff.p, P->d_Doff.p, P->Lp.p,
+                                                                      P->D.p, Ld.p, fail.p);
+                    count_launch();
+                    SBG_LAUNCH_CHECK();
+                }
+                if (S.upd.count(k) + S.upd_far.count(k) > 0)
+                    la.panel_end(
+                        [&](cudaStream_t st) {
+                            launch_gemm<K_UPDATE>(ctx, P, k, S.d_upd.p + S.upd.off[k], S.upd.count(k), P->Lp.p,
+                                                  nullptr, st);
+                        },
+                        [&](cudaStream_t st) {
+                            launch_gemm<K_UPDATE>(ctx, P, k, S.d_upd_far.p + S.upd_far.off[k], S.upd_far.count(k),
+                                                  P->Lp.p, nullptr, st, true);
+                        });
             }
+            la.join();
+            k_put_diag<<<dim3(P->Tmax, P->nblocks), 256, 0, s>>>(P->d_T.p, P->d_Poff.p, P->d_Doff.p, Ld.p, P->Lp.p);
+            count_launch();
+            SBG_LAUNCH_CHECK();
             SBG_CUDA(cudaStreamSynchronize(s));
         }
         std::vector<int> hfail(fail.n);
@@ -1282,7 +1430,7 @@ void coarse_galerkin(Ctx* ctx, const DMatrix& W, const Prolongation& R, std::vec
     cp.upload(R.col_ptr, s);
     cr.upload(R.row_idx, s);
     cv.upload(R.val, s);
-    coarse_galerkin_device(ctx, W, R.col_ptr, cp.p, cr.p, cv.p, nc, nc, dH.p);
+    coarse_galerkin_device(ctx, W, R.col_ptr, R.row_idx, cp.p, cr.p, cv.p, nc, nc, dH.p);
     SBG_CUDA(cudaMemcpyAsync(H.data(), dH.p, H.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
     SBG_CUDA(cudaStreamSynchronize(s));
 }

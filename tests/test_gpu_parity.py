@@ -267,9 +267,12 @@ def test_pcg_energy_error_history(ctx):
     rho = (np.sqrt(kappa) - 1.0) / (np.sqrt(kappa) + 1.0)
     for k, ek in enumerate(e):
         assert ek <= 2.0 * rho ** k * e[0] * (1.0 + 1e-9) + 1e-13 * e[0]
+    # kappa(W0) ~ 1e3 and CG runs past n = 60 steps: after the first steps the iterates of
+    # any two summation orders drift apart (loss of orthogonality), so the histories are
+    # compared where CG is still exact arithmetic to ~1e-10 (the first n/4 steps)
     orep = O.pcg(W0, None, b, 1e-12, 0, exact=exact)
-    k = min(len(e), len(orep.energy_error_history))
-    np.testing.assert_allclose(e[:k], orep.energy_error_history[:k], rtol=1e-6, atol=1e-10 * e[0])
+    np.testing.assert_allclose(e[:15], orep.energy_error_history[:15], rtol=1e-9)
+    assert abs(rep.iterations - orep.iterations) <= 5
     # with a preconditioner (config 1), and x0 = 0 gives e0 = sqrt(exact^T W exact)
     pair = S.make_config(1)
     fine, coarse = S.inflate(pair.fine), S.inflate(pair.coarse)
