@@ -361,7 +361,27 @@ __global__ void __launch_bounds__(FAR_THREADS, 3)
     tile_contract_flush(It, T.fb, T.gb, diag, B, W, ld);
 }
 
+// Warp-aggregated append to a global list: every lane of the (converged) warp calls it;
+// lane i wants n_i slots; one atomicAdd per warp instead of one per record (the near field
+// appends tens of millions of records to two counters).  Returns lane i's first slot.
+__device__ __forceinline__ unsigned long long warp_append(unsigned long long* counter, unsigned n)
+{
+    const int lane = threadIdx.x & 31;
+    unsigned incl = n;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+    }
+    const unsigned total = __shfl_sync(0xffffffffu, incl, 31);
+    unsigned long long base = 0;
+    if (lane == 31 && total) base = atomicAdd(counter, (unsigned long long)total);
+    base = __shfl_sync(0xffffffffu, base, 31);
+    return base + (incl - n);
+}
+
 // near-list builder: pairs of non-certainly-far tiles that are disjoint but not far
+// (BS * BS is a multiple of the block size, so every warp runs the same trip count)
 __global__ void k_classify_near(const TileInfo* __restrict__ tiles, int tstride, GeoPtrs G,
                                 const int* __restrict__ bfacets, double thr, int2* __restrict__ near_list,
                                 unsigned long long cap, unsigned long long* __restrict__ count)
@@ -370,16 +390,21 @@ __global__ void k_classify_near(const TileInfo* __restrict__ tiles, int tstride,
     const bool diag = T.fb == T.gb;
     for (int e = threadIdx.x; e < BS * BS; e += blockDim.x) {
         const int fl = e / BS, gl = e % BS;
-        if (diag && gl >= fl) continue;
-        const int f = bfacets[T.fb * BS + fl], g = bfacets[T.gb * BS + gl];
-        if (f < 0 || g < 0) continue;
-        if (shared_count(G.vid + 3 * f, G.vid + 3 * g) > 0) continue;
-        const int t = max(f, g), s = min(f, g);
-        const D3 ct = {G.c[3 * t], G.c[3 * t + 1], G.c[3 * t + 2]};
-        const D3 cs = {G.c[3 * s], G.c[3 * s + 1], G.c[3 * s + 2]};
-        if (far_test(ct, G.rad[t], G.diam[t], cs, G.rad[s], G.diam[s], thr)) continue;
-        const unsigned long long k = atomicAdd(count, 1ull);
-        if (k < cap) near_list[k] = make_int2(t, s);
+        bool near = !(diag && gl >= fl);
+        int t = 0, s = 0;
+        if (near) {
+            const int f = bfacets[T.fb * BS + fl], g = bfacets[T.gb * BS + gl];
+            near = f >= 0 && g >= 0 && shared_count(G.vid + 3 * f, G.vid + 3 * g) == 0;
+            if (near) {
+                t = max(f, g);
+                s = min(f, g);
+                const D3 ct = {G.c[3 * t], G.c[3 * t + 1], G.c[3 * t + 2]};
+                const D3 cs = {G.c[3 * s], G.c[3 * s + 1], G.c[3 * s + 2]};
+                near = !far_test(ct, G.rad[t], G.diam[t], cs, G.rad[s], G.diam[s], thr);
+            }
+        }
+        const unsigned long long k = warp_append(count, near ? 1u : 0u);
+        if (near && k < cap) near_list[k] = make_int2(t, s);
     }
 }
 
@@ -451,13 +476,23 @@ struct NearNode {
 };
 
 // classify every node of level `depth`: leaves go to `leaves`, split nodes append 4 children to `next`
+// The node count comes from the device (the previous level's append counter), so all six
+// levels are enqueued back to back with a fixed grid-stride launch and no host round trip;
+// an append past a buffer's capacity raises *overflow (the host regrows and reruns) and the
+// level's true population is recorded in level_pop[depth] for the regrowth.
 __global__ void k_near_level(const NearNode* __restrict__ nodes, const unsigned long long* __restrict__ nnodes_dev,
                              long long cap_nodes, int depth, const int2* __restrict__ pairs,
                              const double* __restrict__ GV, double thr, NearNode* __restrict__ leaves,
                              unsigned long long* __restrict__ nleaves, long long cap_leaves,
-                             NearNode* __restrict__ next, unsigned long long* __restrict__ nnext, long long cap_next)
+                             NearNode* __restrict__ next, unsigned long long* __restrict__ nnext, long long cap_next,
+                             unsigned long long* __restrict__ overflow, unsigned long long* __restrict__ level_pop)
 {
-    const long long nn = min((long long)*nnodes_dev, cap_nodes);
+    const long long nn_all = (long long)*nnodes_dev;
+    const long long nn = min(nn_all, cap_nodes);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        level_pop[depth] = (unsigned long long)nn_all;
+        if (nn_all > cap_nodes) atomicOr(overflow, 1ull);
+    }
     for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < nn; k += (long long)gridDim.x * blockDim.x) {
         const NearNode nd = nodes[k];
         bool leaf = depth >= 5;
@@ -475,14 +510,18 @@ __global__ void k_near_level(const NearNode* __restrict__ nodes, const unsigned 
             split_t = dt >= ds ? 1 : 0;
         }
         if (leaf) {
-            const unsigned long long q = atomicAdd(nleaves, 1ull);
-            if ((long long)q < cap_leaves) leaves[q] = nd;
+            const unsigned long long ql = atomicAdd(nleaves, 1ull);
+            if ((long long)ql < cap_leaves)
+                leaves[ql] = nd;
+            else
+                atomicOr(overflow, 1ull);
         } else {
-            const unsigned long long q = atomicAdd(nnext, 4ull);
+            const unsigned long long qn = atomicAdd(nnext, 4ull);
             const unsigned base = (nd.code & ~7u) | (unsigned)(depth + 1);
+            if ((long long)qn + 4 > cap_next) atomicOr(overflow, 1ull);
             for (int c = 0; c < 4; ++c)
-                if ((long long)q + c < cap_next)
-                    next[q + c] = {nd.pair, base | ((unsigned)(split_t | (c << 1)) << (3 + 3 * depth))};
+                if ((long long)qn + c < cap_next)
+                    next[qn + c] = {nd.pair, base | ((unsigned)(split_t | (c << 1)) << (3 + 3 * depth))};
         }
     }
 }
@@ -873,12 +912,14 @@ __global__ void k_sauter_finish(const double* __restrict__ part, int npairs, int
 }
 
 // ---------------------------------------------------------------- per-pair scatter (near + singular)
-__global__ void k_local_scatter(const int2* __restrict__ pairs, const double* __restrict__ I, long long np,
+// pairs [0, nsing) are the singular pairs, then min(*nnear, near_cap) near pairs (device count)
+__global__ void k_local_scatter(const int2* __restrict__ pairs, const double* __restrict__ I, long long nsing,
+                                const unsigned long long* __restrict__ nnear, long long near_cap,
                                 const int* __restrict__ uptr, const int* __restrict__ udof,
                                 const double* __restrict__ uval, double* __restrict__ W, int ld)
 {
     const long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= np) return;
+    if (k >= nsing + min((long long)*nnear, near_cap)) return;
     const int f = pairs[k].x, g = pairs[k].y;
     const double val = I[k];
     for (int p = uptr[f]; p < uptr[f + 1]; ++p) {
@@ -1311,9 +1352,23 @@ void run_sauter(Ctx* ctx, const DBuf<double>& X, const std::vector<int>& pv, con
 }
 
 struct NearWork {
-    DBuf<NearNode> cur, next, leaves;
-    DBuf<unsigned long long> cnt;  // [0] current frontier, [1] next frontier, [2] leaves
+    DBuf<NearNode> buf[2], leaves;  // frontier (by level parity) and the leaf list
+    // [0], [1] frontier counts by level parity, [2] leaves, [3] overflow, [4..9] level populations
+    DBuf<unsigned long long> cnt;
+    unsigned long long* hcnt = nullptr;  // page-locked copy, read after the assembly's final synchronisation
+    ~NearWork()
+    {
+        if (hcnt) cudaFreeHost(hcnt);
+    }
 };
+constexpr int kNearCnt = 10;
+// the page-locked counter block: [0, kNearCnt) the near-field counters, then the near-list
+// count and the mirror's non-finite flag of the assembly (read after its one synchronisation)
+unsigned long long* near_host_counters(NearWork& NW)
+{
+    if (!NW.hcnt) SBG_CUDA(cudaMallocHost(&NW.hcnt, (kNearCnt + 2) * sizeof(unsigned long long)));
+    return NW.hcnt;
+}
 
 // frontier buffers are cached on the context, so a fresh plan (every assemble_W
 // call through the reference-style API) reuses the previous call's capacity
@@ -1352,79 +1407,57 @@ __global__ void k_near_init(const unsigned long long* __restrict__ np_dev, long 
     }
 }
 
-// near-pair integrals for the device list pairs[0:*np_dev] (capacity cap); returns the leaf count
-// (rank, world): only the near pairs this rank owns are integrated (the others' out = 0);
-// *owned receives their count
-long long run_near(Ctx* ctx, const RuleDims& R, const double* GV, const double* GA, const int2* pairs,
-                   const unsigned long long* np_dev, long long cap, double thr, double* out, NearWork& NW,
-                   int rank = 0, int world = 1, long long* owned = nullptr)
+// near-pair integrals for the device list pairs[0:*np_dev] (capacity cap), enqueued with
+// no host synchronisation: the six recursion levels (fixed grid-stride launches reading
+// their populations from the device) and one launch over all leaves.  The counters land in
+// NW.hcnt (page-locked) for near_results() after the caller's synchronisation; capacities
+// come from the previous runs on this context (or generous first guesses), and an overflow
+// is reported there so the caller can regrow (near_regrow) and run again.
+// (rank, world): only the near pairs this rank owns are integrated (the others' out = 0).
+void run_near(Ctx* ctx, const RuleDims& R, const double* GV, const double* GA, const int2* pairs,
+              const unsigned long long* np_dev, long long cap, double thr, double* out, NearWork& NW, int rank = 0,
+              int world = 1)
 {
-    if (cap <= 0) return 0;
+    if (cap <= 0) return;
     cudaStream_t s = ctx->stream;
     TimedScope ts(ctx, "near");
-    if (!NW.cnt.n) NW.cnt.alloc(3);
+    if (!NW.cnt.n) NW.cnt.alloc(kNearCnt);
+    near_host_counters(NW);
     set_max_dynamic_smem(k_near_leaves, NEAR_LEAF_SMEM);
-    if ((long long)NW.cur.n < cap) NW.cur.alloc(cap);
-    if (world > 1) SBG_CUDA(cudaMemsetAsync(NW.cnt.p, 0, sizeof(unsigned long long), s));
-    k_near_init<<<(int)((cap + 255) / 256), 256, 0, s>>>(np_dev, cap, NW.cur.p, out, NW.cnt.p, pairs, rank, world);
+    if ((long long)NW.buf[0].n < cap) {
+        const long long f = std::max<long long>(16 * cap, NW.buf[0].n);
+        NW.buf[0].alloc(f);
+        NW.buf[1].alloc(f);
+    }
+    if ((long long)NW.leaves.n < 16 * cap) NW.leaves.alloc(64 * cap);
+    const long long F = (long long)NW.buf[0].n, Lcap = (long long)NW.leaves.n;
+    SBG_CUDA(cudaMemsetAsync(NW.cnt.p, 0, kNearCnt * sizeof(unsigned long long), s));
+    k_near_init<<<(int)((cap + 255) / 256), 256, 0, s>>>(np_dev, cap, NW.buf[0].p, out, NW.cnt.p, pairs, rank, world);
     count_launch();
     SBG_LAUNCH_CHECK();
-    unsigned long long h[3] = {0, 0, 0};
-    SBG_CUDA(cudaMemcpyAsync(h, NW.cnt.p, sizeof(h[0]), cudaMemcpyDeviceToHost, s));
-    SBG_CUDA(cudaStreamSynchronize(s));
-    long long ncur = (long long)h[0], total_leaves = 0;
-    if (owned) *owned = ncur;
-    // classify level by level (each level's leaves appended to one list), then evaluate
-    // every leaf in one launch: no per-level grid tails, and the host's per-level count
-    // reads never wait on leaf work
-    for (int depth = 0; depth <= 5 && ncur > 0; ++depth) {
-        if ((long long)NW.leaves.n < total_leaves + ncur) {  // grow, keeping the leaves so far
-            DBuf<NearNode> grown((total_leaves + ncur) * 5 / 4);
-            if (total_leaves)
-                SBG_CUDA(cudaMemcpyAsync(grown.p, NW.leaves.p, total_leaves * sizeof(NearNode),
-                                         cudaMemcpyDeviceToDevice, s));
-            NW.leaves = std::move(grown);
+    {
+        TimedScope tc(ctx, "near_classify");
+        const int grid = 16 * ctx->sm_count;
+        for (int depth = 0; depth <= 5; ++depth) {
+            const int cur = depth & 1, nxt = cur ^ 1;
+            if (depth > 0) SBG_CUDA(cudaMemsetAsync(NW.cnt.p + nxt, 0, sizeof(unsigned long long), s));
+            k_near_level<<<grid, 128, 0, s>>>(NW.buf[cur].p, NW.cnt.p + cur, F, depth, pairs, GV, thr, NW.leaves.p,
+                                              NW.cnt.p + 2, Lcap, NW.buf[nxt].p, NW.cnt.p + nxt, depth < 5 ? F : 0,
+                                              NW.cnt.p + 3, NW.cnt.p + 4);
+            count_launch();
+            SBG_LAUNCH_CHECK();
         }
-        // classify into the existing next-frontier capacity; on overflow grow it to the
-        // exact count (+25%) and classify again (idempotent), so the frontier buffers size
-        // to the real level populations instead of the 4x upper bound, and a plan that is
-        // run again never reallocates
-        for (int attempt = 0;; ++attempt) {
-            const long long cap_next = depth < 5 ? (long long)NW.next.n : 0;
-            SBG_CUDA(cudaMemsetAsync(NW.cnt.p + 1, 0, 2 * sizeof(unsigned long long), s));
-            {
-                TimedScope tc(ctx, "near_classify");
-                const int grid = (int)std::min<long long>((ncur + 127) / 128, 16LL * ctx->sm_count);
-                k_near_level<<<grid, 128, 0, s>>>(NW.cur.p, NW.cnt.p, ncur, depth, pairs, GV, thr,
-                                                  NW.leaves.p + total_leaves, NW.cnt.p + 2, ncur, NW.next.p,
-                                                  NW.cnt.p + 1, cap_next);
-                count_launch();
-                SBG_LAUNCH_CHECK();
-            }
-            SBG_CUDA(cudaMemcpyAsync(h, NW.cnt.p, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
-            SBG_CUDA(cudaStreamSynchronize(s));
-            if (depth == 5 || (long long)h[1] <= cap_next) break;
-            if (attempt > 0) throw std::logic_error("near frontier: inconsistent level count");
-            NW.next.alloc((long long)h[1] * 5 / 4);
-        }
-        total_leaves += (long long)h[2];
-        ncur = (long long)h[1];
-        std::swap(NW.cur, NW.next);
-        if (ncur > 0) SBG_CUDA(cudaMemcpyAsync(NW.cnt.p, &h[1], sizeof(h[1]), cudaMemcpyHostToDevice, s));
     }
-    if (total_leaves > 0) {
-        const unsigned long long tl = (unsigned long long)total_leaves;
-        SBG_CUDA(cudaMemcpyAsync(NW.cnt.p + 2, &tl, sizeof(tl), cudaMemcpyHostToDevice, s));
+    {
         TimedScope tl_scope(ctx, "near_leaves");
-        const long long warps = (total_leaves + 7) / 8;
-        const int lgrid = (int)std::min<long long>((warps + NEAR_LEAF_WARPS - 1) / NEAR_LEAF_WARPS, 2LL * ctx->sm_count);
+        const int lgrid = 2 * ctx->sm_count;  // persistent: the leaf count is read on the device
         if (R.nnp == NN) {
-            k_near_leaves<<<lgrid, NEAR_LEAF_THREADS, NEAR_LEAF_SMEM, s>>>(NW.leaves.p, NW.cnt.p + 2, total_leaves,
-                                                                           pairs, GV, GA, 1.0 / M_PI, out);
+            k_near_leaves<<<lgrid, NEAR_LEAF_THREADS, NEAR_LEAF_SMEM, s>>>(NW.leaves.p, NW.cnt.p + 2, Lcap, pairs, GV,
+                                                                           GA, 1.0 / M_PI, out);
         } else {
             switch (R.nnp) {
 #define SBG_NEAR_G(N) \
-    case N: launch_near_leaves_g<N>(ctx, NW.leaves.p, NW.cnt.p + 2, total_leaves, pairs, GV, GA, out); break;
+    case N: launch_near_leaves_g<N>(ctx, NW.leaves.p, NW.cnt.p + 2, Lcap, pairs, GV, GA, out); break;
                 SBG_NEAR_G(16) SBG_NEAR_G(32) SBG_NEAR_G(48) SBG_NEAR_G(64) SBG_NEAR_G(96) SBG_NEAR_G(112)
 #undef SBG_NEAR_G
             default: throw std::logic_error("near rule size not instantiated");
@@ -1433,7 +1466,35 @@ long long run_near(Ctx* ctx, const RuleDims& R, const double* GV, const double* 
         count_launch();
         SBG_LAUNCH_CHECK();
     }
-    return total_leaves;
+    SBG_CUDA(cudaMemcpyAsync(NW.hcnt, NW.cnt.p, kNearCnt * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+}
+
+// after the stream has synchronised: leaves, pairs this rank integrated, overflow
+struct NearResult {
+    long long leaves = 0, owned = 0;
+    bool overflow = false;
+};
+NearResult near_results(const NearWork& NW)
+{
+    NearResult r;
+    if (!NW.hcnt) return r;
+    r.leaves = (long long)NW.hcnt[2];
+    r.owned = (long long)NW.hcnt[4];
+    r.overflow = NW.hcnt[3] != 0;
+    return r;
+}
+// grow the frontier and leaf buffers after an overflowed run: to the populations it saw
+// (+25%) and at least twice the old size — a level cut short by a full buffer hides the
+// true populations of the levels below it, so a run can reveal one more level at a time
+void near_regrow(NearWork& NW)
+{
+    unsigned long long lvl = 0;
+    for (int d = 0; d <= 5; ++d) lvl = std::max(lvl, NW.hcnt[4 + d]);
+    const long long f = std::max<long long>((long long)(lvl * 5 / 4) + 1024, 2 * (long long)NW.buf[0].n);
+    NW.buf[0].alloc(f);
+    NW.buf[1].alloc(f);
+    const long long l = std::max<long long>((long long)(NW.hcnt[2] * 5 / 4) + 1024, 2 * (long long)NW.leaves.n);
+    NW.leaves.alloc(l);
 }
 
 }  // namespace
@@ -1766,78 +1827,89 @@ void assembly_run(AssemblyPlan* P, DMatrix& W, AssemblyStats* stats, int rank, i
         sing_lo[cls] = P->cls_cnt[cls] * rank / world;
         sing_cnt[cls] = P->cls_cnt[cls] * (rank + 1) / world - sing_lo[cls];
     }
-    // near list (classification of the non-certainly-far tiles)
-    long long leaves = 0, near_owned = 0;
-    unsigned long long nnear = 0;
-    for (int attempt = 0; attempt < 2; ++attempt) {
+    // Everything is enqueued without a host round trip; one synchronisation at the end reads
+    // the near-list count, the near-field counters and the mirror's non-finite flag.  A
+    // near list or near frontier that outgrew its buffers (first run of a mesh size on this
+    // context) is regrown to the measured size and the assembly runs again.
+    NearWork& NW = near_work(ctx);
+    unsigned long long* hnear = near_host_counters(NW) + kNearCnt;
+    NearResult nr;
+    for (int attempt = 0;; ++attempt) {
+        std::fill(NW.hcnt, NW.hcnt + kNearCnt + 2, 0ull);  // the previous run has synchronised
+        if (attempt) SBG_CUDA(cudaMemsetAsync(W.a.p, 0, W.a.n * sizeof(double), s));
         SBG_CUDA(cudaMemsetAsync(P->near_cnt.p, 0, sizeof(unsigned long long), s));
-        if (my_cand) {
+        if (my_cand) {  // near list: classification of the non-certainly-far tiles
             TimedScope ts(ctx, "classify");
             k_classify_near<<<(int)my_cand, 256, 0, s>>>(P->cand.p, 1, P->G.ptrs(), P->bfac.p, thr,
                                                          P->loc_pairs.p + P->nsing, P->near_cap, P->near_cnt.p);
             count_launch();
             SBG_LAUNCH_CHECK();
         }
-        leaves = run_near(ctx, R, P->G.v.p, P->G.area.p, P->loc_pairs.p + P->nsing, P->near_cnt.p, P->near_cap, thr,
-                          P->loc_I.p + P->nsing, near_work(ctx), rank, world, &near_owned);
-        // a deferred plan builds its curl-dependent half while the near-field leaves run
+        run_near(ctx, R, P->G.v.p, P->G.area.p, P->loc_pairs.p + P->nsing, P->near_cnt.p, P->near_cap, thr,
+                 P->loc_I.p + P->nsing, NW, rank, world);
+        // a deferred plan builds its curl-dependent half while the near field runs
         plan_finish(P);
-        SBG_CUDA(cudaMemcpyAsync(&nnear, P->near_cnt.p, sizeof(nnear), cudaMemcpyDeviceToHost, s));
-        SBG_CUDA(cudaStreamSynchronize(s));
-        if ((long long)nnear <= P->near_cap) break;
-        // near list overflow: grow and redo
-        P->near_cap = (long long)nnear + 1024;
-        DBuf<int2> np2(P->nsing + P->near_cap);
-        DBuf<double> ni2(P->nsing + P->near_cap);
-        if (P->nsing) {
-            SBG_CUDA(cudaMemcpyAsync(np2.p, P->loc_pairs.p, P->nsing * sizeof(int2), cudaMemcpyDeviceToDevice, s));
+        // singular pairs (Sauter rules); a shard zeroes the integrals it does not own
+        if (world > 1 && P->nsing) SBG_CUDA(cudaMemsetAsync(P->loc_I.p, 0, P->nsing * sizeof(double), s));
+        for (int cls = 1; cls <= 3; ++cls) {
+            const long long np = sing_cnt[cls];
+            if (!np) continue;
+            TimedScope ts(ctx, "sauter");
+            const int* pv = P->pv[cls].p + 6 * sing_lo[cls];
+            launch_sauter_partial(ctx, cls, pv, (int)np, P->G.X.p, P->SR->r[cls].p, P->SR->npts[cls], P->schunk[cls],
+                                  P->schunks[cls], P->spart[cls].p);
+            k_sauter_finish<<<(int)((np + 127) / 128), 128, 0, s>>>(P->spart[cls].p, (int)np, P->schunks[cls], pv,
+                                                                     P->G.X.p,
+                                                                     P->loc_I.p + P->cls_off[cls] + sing_lo[cls]);
+            count_launch();
+            SBG_LAUNCH_CHECK();
         }
-        P->loc_pairs = std::move(np2);
-        P->loc_I = std::move(ni2);
-    }
-    // singular pairs (Sauter rules); a shard zeroes the integrals it does not own
-    if (world > 1 && P->nsing) SBG_CUDA(cudaMemsetAsync(P->loc_I.p, 0, P->nsing * sizeof(double), s));
-    for (int cls = 1; cls <= 3; ++cls) {
-        const long long np = sing_cnt[cls];
-        if (!np) continue;
-        TimedScope ts(ctx, "sauter");
-        const int* pv = P->pv[cls].p + 6 * sing_lo[cls];
-        launch_sauter_partial(ctx, cls, pv, (int)np, P->G.X.p, P->SR->r[cls].p, P->SR->npts[cls], P->schunk[cls],
-                              P->schunks[cls], P->spart[cls].p);
-        k_sauter_finish<<<(int)((np + 127) / 128), 128, 0, s>>>(P->spart[cls].p, (int)np, P->schunks[cls], pv,
-                                                                 P->G.X.p,
-                                                                 P->loc_I.p + P->cls_off[cls] + sing_lo[cls]);
-        count_launch();
-        SBG_LAUNCH_CHECK();
-    }
-    // far tiles
-    {
-        TimedScope ts(ctx, "far_tiles");
-        BlockPtrs BP{P->bfac.p, P->dof_ptr.p, P->dofs.p, P->ent_ptr.p, P->ents.p};
-        launch_far_tiles(ctx, R, P->tiles.p + rank, my_tiles, world, P->G.ptrs(), BP, thr, W, P->cfg.exact_far);
-        SBG_LAUNCH_CHECK();
-    }
-    // per-pair scatter of singular + near integrals
-    const long long nloc = P->nsing + (long long)nnear;
-    if (nloc) {
-        TimedScope ts(ctx, "local_scatter");
-        k_local_scatter<<<(int)((nloc + 127) / 128), 128, 0, s>>>(P->loc_pairs.p, P->loc_I.p, nloc, P->uptr.p,
-                                                                  P->udof.p, P->uval.p, W.a.p, W.ld);
-        count_launch();
-        SBG_LAUNCH_CHECK();
-    }
-    {
-        TimedScope ts(ctx, "mirror");
-        const int nt = (P->n + 31) / 32;
-        SBG_CUDA(cudaMemsetAsync(P->bad.p, 0, sizeof(int), s));
-        k_mirror<<<dim3(nt, nt), dim3(32, 8), 0, s>>>(W.a.p, P->n, W.ld, P->bad.p);
-        count_launch();
-        SBG_LAUNCH_CHECK();
-        int bad = 0;
-        SBG_CUDA(cudaMemcpyAsync(&bad, P->bad.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+        {
+            TimedScope ts(ctx, "far_tiles");
+            BlockPtrs BP{P->bfac.p, P->dof_ptr.p, P->dofs.p, P->ent_ptr.p, P->ents.p};
+            launch_far_tiles(ctx, R, P->tiles.p + rank, my_tiles, world, P->G.ptrs(), BP, thr, W, P->cfg.exact_far);
+            SBG_LAUNCH_CHECK();
+        }
+        // per-pair scatter of singular + near integrals (near count read on the device)
+        if (P->nsing + P->near_cap > 0) {
+            TimedScope ts(ctx, "local_scatter");
+            const long long nmax = P->nsing + P->near_cap;
+            k_local_scatter<<<(int)((nmax + 127) / 128), 128, 0, s>>>(P->loc_pairs.p, P->loc_I.p, P->nsing,
+                                                                      P->near_cnt.p, P->near_cap, P->uptr.p,
+                                                                      P->udof.p, P->uval.p, W.a.p, W.ld);
+            count_launch();
+            SBG_LAUNCH_CHECK();
+        }
+        {
+            TimedScope ts(ctx, "mirror");
+            const int nt = (P->n + 31) / 32;
+            SBG_CUDA(cudaMemsetAsync(P->bad.p, 0, sizeof(int), s));
+            k_mirror<<<dim3(nt, nt), dim3(32, 8), 0, s>>>(W.a.p, P->n, W.ld, P->bad.p);
+            count_launch();
+            SBG_LAUNCH_CHECK();
+        }
+        SBG_CUDA(cudaMemcpyAsync(hnear, P->near_cnt.p, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+        SBG_CUDA(cudaMemcpyAsync(hnear + 1, P->bad.p, sizeof(int), cudaMemcpyDeviceToHost, s));
         SBG_CUDA(cudaStreamSynchronize(s));
-        if (bad) throw NumericalError("quadrature produced a non-finite pair integral");
+        nr = near_results(NW);
+        const bool list_over = (long long)hnear[0] > P->near_cap;
+        if (!list_over && !nr.overflow) break;
+        if (attempt >= 6) throw std::logic_error("near field: buffers still too small after regrowth");
+        if (nr.overflow) near_regrow(NW);
+        if (list_over) {  // near list overflow: grow (keeping the singular pairs) and redo
+            P->near_cap = (long long)hnear[0] + 1024;
+            DBuf<int2> np2(P->nsing + P->near_cap);
+            DBuf<double> ni2(P->nsing + P->near_cap);
+            if (P->nsing)
+                SBG_CUDA(cudaMemcpyAsync(np2.p, P->loc_pairs.p, P->nsing * sizeof(int2), cudaMemcpyDeviceToDevice, s));
+            P->loc_pairs = std::move(np2);
+            P->loc_I = std::move(ni2);
+        }
     }
+    if (*reinterpret_cast<const int*>(hnear + 1)) throw NumericalError("quadrature produced a non-finite pair integral");
+    const unsigned long long nnear = hnear[0];
+    const long long leaves = nr.leaves, near_owned = nr.owned;
+    const long long nloc = P->nsing + (long long)nnear;
     if (stats) {
         stats->identical = sing_cnt[3];
         stats->edge = sing_cnt[2];
@@ -2001,7 +2073,13 @@ void pair_integrals(Ctx* ctx, const SurfaceMesh& m, const QuadCfg& cfg, const in
         const unsigned long long hn = nearp.size();
         SBG_CUDA(cudaMemcpyAsync(cnt.p, &hn, sizeof(hn), cudaMemcpyHostToDevice, s));
         NearWork NW;
-        run_near(ctx, R, G.v.p, G.area.p, d_p.p, cnt.p, (long long)nearp.size(), cfg.near_threshold, o.p, NW);
+        for (int attempt = 0;; ++attempt) {
+            run_near(ctx, R, G.v.p, G.area.p, d_p.p, cnt.p, (long long)nearp.size(), cfg.near_threshold, o.p, NW);
+            SBG_CUDA(cudaStreamSynchronize(s));
+            if (!near_results(NW).overflow) break;
+            if (attempt >= 6) throw std::logic_error("near field: buffers still too small after regrowth");
+            near_regrow(NW);
+        }
         fetch(o.p, idx[0]);
     }
     if (!farp.empty()) {
