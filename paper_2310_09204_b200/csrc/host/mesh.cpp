@@ -3,6 +3,7 @@
 #include <algorithm>
 #include <cstdint>
 #include <set>
+#include <thread>
 #include <unordered_map>
 
 #include "host.hpp"
@@ -127,7 +128,10 @@ struct CellHash {
 // reference: inc/mesh.hpp:238-272.  Same checks and the same bounding-sphere
 // predicate; candidate pairs come from a uniform grid of facet centroids with
 // cell size >= the largest reject radius, so exactly the pairs the reference's
-// O(nf^2) loop tests are tested.
+// O(nf^2) loop tests are tested.  The per-facet checks and the conformity test run on
+// host threads over facet ranges; the error raised is the one the reference's
+// sequential loops reach first (smallest facet, then smallest partner; per facet the
+// order id range, duplicate, degenerate).
 void validate_mesh(const SurfaceMesh& m)
 {
     const int nv = m.num_vertices(), nf = m.num_facets();
@@ -135,17 +139,50 @@ void validate_mesh(const SurfaceMesh& m)
         if (!std::isfinite(p.x) || !std::isfinite(p.y) || !std::isfinite(p.z))
             throw ValidationError("non-finite vertex coordinate");
     const double eps = 1e-12 * std::max(m.diameter(), 1e-300);
-    std::set<std::array<int, 3>> seen;
-    for (int f = 0; f < nf; ++f) {
-        const auto& t = m.facets[f];
+    // first facet with an id out of range: the facets before it are checked for duplicates
+    // (second occurrence of a sorted vertex triple) and degeneracy
+    int f_range = nf;
+    for (int f = 0; f < nf && f_range == nf; ++f)
         for (int k = 0; k < 3; ++k)
-            if (t[k] < 0 || t[k] >= nv) throw ValidationError("facet vertex id out of range");
-        std::array<int, 3> key = t;
+            if (m.facets[f][k] < 0 || m.facets[f][k] >= nv) {
+                f_range = f;
+                break;
+            }
+    std::vector<std::pair<std::array<int, 3>, int>> keys(f_range);
+    for (int f = 0; f < f_range; ++f) {
+        std::array<int, 3> key = m.facets[f];
         std::sort(key.begin(), key.end());
-        if (!seen.insert(key).second) throw ValidationError("duplicate facet");
-        const double scale = eps * std::max(m.facet_diameter(f), eps);
-        if (m.facet_measure(f) < scale) throw ValidationError("degenerate facet " + std::to_string(f));
+        keys[f] = {key, f};
     }
+    std::sort(keys.begin(), keys.end());
+    int f_dup = nf;
+    for (size_t i = 1; i < keys.size(); ++i)
+        if (keys[i].first == keys[i - 1].first) f_dup = std::min(f_dup, keys[i].second);
+    const int nthreads = (int)std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    auto parallel = [&](int count, const auto& body) {  // body(lo, hi, slot) over contiguous ranges
+        const int nt = std::max(1, std::min(nthreads, count / 2048));
+        std::vector<std::thread> pool;
+        for (int t = 1; t < nt; ++t)
+            pool.emplace_back([&, t] { body((int)((long long)count * t / nt), (int)((long long)count * (t + 1) / nt), t); });
+        body(0, (int)((long long)count / nt), 0);
+        for (auto& th : pool) th.join();
+        return nt;
+    };
+    // degenerate facets before the first id/duplicate error (at that facet its own error wins)
+    std::vector<int> deg(nthreads, nf);
+    const int f_chk = std::min(f_range, f_dup);
+    parallel(f_chk, [&](int lo, int hi, int slot) {
+        for (int f = lo; f < hi; ++f) {
+            const double scale = eps * std::max(m.facet_diameter(f), eps);
+            if (m.facet_measure(f) < scale) {
+                deg[slot] = f;
+                return;
+            }
+        }
+    });
+    const int f_deg = *std::min_element(deg.begin(), deg.end());
+    if (f_deg < f_chk) throw ValidationError("degenerate facet " + std::to_string(f_deg));
+    if (f_chk < nf) throw ValidationError(f_range == f_chk ? "facet vertex id out of range" : "duplicate facet");
     if (nf == 0) return;
     std::vector<Vec3> cen(nf);
     std::vector<double> dia(nf);
@@ -156,31 +193,43 @@ void validate_mesh(const SurfaceMesh& m)
         dmax = std::max(dmax, dia[f]);
     }
     const double cell = (dmax + eps) * (1.0 + 1e-9) + 1e-300;
-    std::unordered_map<CellKey, std::vector<int>, CellHash> grid;
     auto key_of = [&](const Vec3& c) {
         return CellKey{(std::int64_t)std::floor(c.x / cell), (std::int64_t)std::floor(c.y / cell),
                        (std::int64_t)std::floor(c.z / cell)};
     };
+    std::unordered_map<CellKey, std::vector<int>, CellHash> grid;
+    grid.reserve((size_t)nf);
     for (int f = 0; f < nf; ++f) grid[key_of(cen[f])].push_back(f);
-    for (int f = 0; f < nf; ++f) {
-        const CellKey k = key_of(cen[f]);
+    // first non-conforming pair per thread range (facets ascending, partners ascending)
+    std::vector<std::pair<int, int>> bad(nthreads, {nf, nf});
+    parallel(nf, [&](int lo, int hi, int slot) {
         std::vector<int> cand;
-        for (int dx = -1; dx <= 1; ++dx)
-            for (int dy = -1; dy <= 1; ++dy)
-                for (int dz = -1; dz <= 1; ++dz) {
-                    auto it = grid.find(CellKey{k.x + dx, k.y + dy, k.z + dz});
-                    if (it == grid.end()) continue;
-                    for (int g : it->second)
-                        if (g > f) cand.push_back(g);
+        for (int f = lo; f < hi; ++f) {
+            const CellKey k = key_of(cen[f]);
+            cand.clear();
+            for (int dx = -1; dx <= 1; ++dx)
+                for (int dy = -1; dy <= 1; ++dy)
+                    for (int dz = -1; dz <= 1; ++dz) {
+                        auto it = grid.find(CellKey{k.x + dx, k.y + dy, k.z + dz});
+                        if (it == grid.end()) continue;
+                        for (int g : it->second)
+                            if (g > f) cand.push_back(g);
+                    }
+            std::sort(cand.begin(), cand.end());
+            for (int g : cand) {
+                const double rr = 0.5 * (dia[f] + dia[g]) + eps;
+                if (norm(cen[f] - cen[g]) > rr) continue;
+                if (!conforming(m, f, g, eps)) {
+                    bad[slot] = {f, g};
+                    return;
                 }
-        std::sort(cand.begin(), cand.end());
-        for (int g : cand) {
-            const double rr = 0.5 * (dia[f] + dia[g]) + eps;
-            if (norm(cen[f] - cen[g]) > rr) continue;
-            if (!conforming(m, f, g, eps))
-                throw ValidationError("non-conforming facet pair " + std::to_string(f) + "," + std::to_string(g));
+            }
         }
-    }
+    });
+    const auto first = *std::min_element(bad.begin(), bad.end());
+    if (first.first < nf)
+        throw ValidationError("non-conforming facet pair " + std::to_string(first.first) + "," +
+                              std::to_string(first.second));
 }
 
 SurfaceMesh make_bowtie_base()  // mesh.hpp:322-337

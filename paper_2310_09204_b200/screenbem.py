@@ -967,16 +967,35 @@ class SolveResult:
 def solve(pair: MeshLevelPair, g, tol: float = 1e-8, cfg: QuadratureConfig = None, precondition: bool = True,
           ctx: Context = None) -> SolveResult:
     """The cmd_solve hot path (experiments.hpp:130-145): inflate -> assemble_W ->
-    assemble_rhs -> partition/prolongation -> build_preconditioner -> pcg."""
+    assemble_rhs -> partition/prolongation -> build_preconditioner -> pcg.  The coarse
+    level's host setup (inflate, partition_dofs, build_prolongation) runs on a host thread
+    while this thread drives the device assembly (the C calls release the GIL), so it is
+    off the critical path; results are identical to the sequential order."""
     ctx = ctx or default_context()
     fine = inflate(pair.fine)
-    W = assemble_W(fine, cfg, ctx=ctx)
-    L = assemble_rhs(fine, g, cfg, ctx=ctx)
-    prec = None
+    setup, err = {}, []
+
+    def coarse_setup():
+        try:
+            coarse = inflate(pair.coarse)
+            setup["P"] = build_prolongation(pair, coarse, fine)
+            setup["part"] = partition_dofs(pair, fine)
+        except BaseException as e:  # re-raised on the calling thread
+            err.append(e)
+    th = None
     if precondition:
-        coarse = inflate(pair.coarse)
-        P = build_prolongation(pair, coarse, fine)
-        prec = build_preconditioner(W, partition_dofs(pair, fine), P)
+        import threading
+        th = threading.Thread(target=coarse_setup, daemon=True)
+        th.start()
+    try:
+        W = assemble_W(fine, cfg, ctx=ctx)
+        L = assemble_rhs(fine, g, cfg, ctx=ctx)
+    finally:
+        if th is not None:
+            th.join()
+    if err:
+        raise err[0]
+    prec = build_preconditioner(W, setup["part"], setup["P"]) if precondition else None
     rep = pcg(W, prec, L, tol)
     if not rep.converged:
         raise NumericalError("solver did not converge")
