@@ -75,6 +75,16 @@ int prec_n(const Prec* p);
 int prec_num_subspaces(const Prec* p);
 // z = M r on device vectors (length n)
 void prec_apply(Ctx* ctx, Prec* p, const double* r, double* z, const int* done_flag);
+// the PCG-fused apply (precond.cu): update x, r, apply, r.z and the iteration's scalars
+struct PcgDev;
+struct PcgFused {
+    PcgDev* st;
+    double *x, *r, *rn;
+    const double *p, *Wp;
+    double *z, *partials, *hist, *alphas, *betas;
+    const int* done;
+};
+bool prec_apply_pcg(Ctx* ctx, Prec* p, const PcgFused& f);
 void prec_block_diag(Ctx* ctx, Prec* p, int which, std::vector<double>& diag);
 double prec_factor_bytes(const Prec* p);  // sum n_b^2 * 8 (roofline bookkeeping)
 void prec_materialize(Ctx* ctx, Prec* p, DMatrix& M);  // schwarz.hpp:142-148

@@ -6,6 +6,7 @@
 #include <random>
 
 #include "kernels.cuh"
+#include "pcg_dev.cuh"
 
 namespace sbg {
 
@@ -66,48 +67,6 @@ __global__ void k_gemv_reduce(const double* __restrict__ part, int chunks, int l
     double s = 0.0;
     for (int c = 0; c < chunks; ++c) s += part[(size_t)c * ld + j];
     y[j] = s;
-}
-
-__device__ __forceinline__ double block_sum(double v, double* sh)
-{
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
-    if (lane == 0) sh[warp] = v;
-    __syncthreads();
-    v = 0.0;
-    if (warp == 0) {
-        v = lane < (int)(blockDim.x >> 5) ? sh[lane] : 0.0;
-        for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
-    }
-    return v;  // valid in thread 0
-}
-
-// ---------------------------------------------------------------- PCG state
-struct PcgDev {
-    double rz, alpha, beta, r0, tol, pwp;
-    int it, maxit, done, converged, error;
-    unsigned counter;
-};
-
-// Returns true in every thread of the last block to finish (threadfence reduction).
-__device__ bool last_block(double v_thread0, double* partials, unsigned* counter)
-{
-    __shared__ bool is_last;
-    if (threadIdx.x == 0) {
-        partials[blockIdx.x] = v_thread0;
-        __threadfence();
-        const unsigned t = atomicAdd(counter, 1u);
-        is_last = (t == gridDim.x - 1);
-    }
-    __syncthreads();
-    return is_last;
-}
-
-__device__ double sum_partials(const double* partials, int count)
-{
-    double s = 0.0;
-    for (int b = 0; b < count; ++b) s += ((volatile const double*)partials)[b];
-    return s;
 }
 
 // init: p = z, rz = r.z, r0, history[0] (pcg.hpp:53-67)
@@ -197,26 +156,7 @@ __global__ void k_pcg_rz(PcgDev* st, const double* __restrict__ r, const double*
     if (last_block(v, partials, &st->counter) && threadIdx.x == 0) {
         const double rz_new = sum_partials(partials, gridDim.x);
         st->counter = 0;
-        if (rz_new < 0) {
-            st->error = 2;
-            st->done = 1;
-            return;
-        }
-        const int it = st->it;
-        alphas[it] = st->alpha;
-        st->it = it + 1;
-        const double res = sqrt(fmax(rz_new, 0.0));
-        hist[it + 1] = res;
-        const double beta = rz_new / st->rz;
-        betas[it] = beta;
-        st->beta = beta;
-        st->rz = rz_new;
-        if (res <= st->tol * st->r0) {
-            st->converged = 1;
-            st->done = 1;
-        } else if (st->it >= st->maxit) {
-            st->done = 1;
-        }
+        pcg_finish_rz(st, rz_new, hist, alphas, betas);
     }
 }
 
@@ -276,6 +216,113 @@ __global__ void k_pcg_p(const PcgDev* st, double* __restrict__ p, const double* 
 // memory rounds at n = 3969; a segment-at-a-time tail added up to 7 more).  U = 8:
 // 16 was slower (fewer resident CTAs), 4/6/10/12 no better.
 constexpr int kRowsPerCta = 8;
+// row . x for one warp (the row's lanes), U 128-bit loads in flight per lane; KEEP: default
+// caching (W held in L2 by the PCG's access-policy window) instead of evict-first
+template <int U, bool KEEP>
+__device__ __forceinline__ double warp_row_dot(const double* __restrict__ Wrow, int ld, const double* __restrict__ x)
+{
+    const int lane = threadIdx.x & 31;
+    const double2* w = reinterpret_cast<const double2*>(Wrow);
+    const double2* x2 = reinterpret_cast<const double2*>(x);
+    const int half = ld >> 1;  // the padding of W and x is zero
+    auto ld2 = [&](const double2* q) { return KEEP ? __ldg(q) : __ldcs(q); };
+    double s[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) s[u] = 0.0;
+    int c = lane;
+    for (; c + (U - 1) * 32 < half; c += U * 32) {
+        double2 a[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) a[u] = ld2(w + c + 32 * u);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const double2 xv = __ldg(x2 + c + 32 * u);
+            s[u] = fma(a[u].x, xv.x, fma(a[u].y, xv.y, s[u]));
+        }
+    }
+    double2 a[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) a[u] = c + 32 * u < half ? ld2(w + c + 32 * u) : make_double2(0.0, 0.0);
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+        if (c + 32 * u < half) {
+            const double2 xv = __ldg(x2 + c + 32 * u);
+            s[u] = fma(a[u].x, xv.x, fma(a[u].y, xv.y, s[u]));
+        }
+    double v = 0.0;
+#pragma unroll
+    for (int u = 0; u < U; ++u) v += s[u];
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// Wp = W p with alpha = rz / p.Wp fused in (the rows form inside PCG, pcg.hpp:70-73): each
+// warp's row also contributes p_row (W p)_row to the block's partial, and the last block
+// finishes the reduction in the fixed block order (deterministic)
+template <bool KEEP>
+__global__ void __launch_bounds__(256) k_gemv_rows_alpha(PcgDev* st, const double* __restrict__ W, int ld, int n,
+                                                         const double* __restrict__ p, double* __restrict__ Wp,
+                                                         double* partials)
+{
+    pdl_wait();
+    if (st->done) return;
+    __shared__ double sh[32];
+    const int row = blockIdx.x * kRowsPerCta + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+    double v = 0.0;
+    if (row < n) {
+        const double y = warp_row_dot<8, KEEP>(W + (size_t)row * ld, ld, p);
+        if (lane == 0) {
+            Wp[row] = y;
+            v = p[row] * y;
+        }
+    }
+    v = block_sum(v, sh);
+    if (last_block(v, partials, &st->counter)) {
+        const double pwp = sum_partials_block(partials, gridDim.x, sh);
+        if (threadIdx.x != 0) return;
+        st->counter = 0;
+        st->pwp = pwp;
+        if (pwp <= 0) {
+            st->error = 1;
+            st->done = 1;
+            return;
+        }
+        st->alpha = st->rz / pwp;
+    }
+}
+
+// alpha from a complete W p (the row-panel PCG after its exchange) with exactly the
+// reduction tree of k_gemv_rows_alpha (8 rows per block, lane 0 of each warp), so the
+// row-panel PCG stays bitwise equal to pcg; Wp <- y
+__global__ void __launch_bounds__(256) k_pcg_alpha8(PcgDev* st, const double* __restrict__ y, int n,
+                                                    const double* __restrict__ p, double* __restrict__ Wp,
+                                                    double* partials)
+{
+    pdl_wait();
+    if (st->done) return;
+    __shared__ double sh[32];
+    const int row = blockIdx.x * kRowsPerCta + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+    double v = 0.0;
+    if (row < n && lane == 0) {
+        const double yv = y[row];
+        Wp[row] = yv;
+        v = p[row] * yv;
+    }
+    v = block_sum(v, sh);
+    if (last_block(v, partials, &st->counter)) {
+        const double pwp = sum_partials_block(partials, gridDim.x, sh);
+        if (threadIdx.x != 0) return;
+        st->counter = 0;
+        st->pwp = pwp;
+        if (pwp <= 0) {
+            st->error = 1;
+            st->done = 1;
+            return;
+        }
+        st->alpha = st->rz / pwp;
+    }
+}
+
 template <int U>
 __global__ void __launch_bounds__(256) k_gemv_rows(const double* __restrict__ W, int ld, int n,
                                                    const double* __restrict__ x, double* __restrict__ y,
@@ -496,7 +543,7 @@ static PcgWork& pcg_work(Ctx* ctx, const DMatrix& W, int maxit)
         fresh->ld = W.ld;
         fresh->cap = std::max(maxit + 2, 128);
         fresh->buf.alloc(6 * (size_t)W.ld);
-        fresh->partials.alloc(std::max((W.n + 255) / 256, 1));
+        fresh->partials.alloc(std::max((W.n + kRowsPerCta - 1) / kRowsPerCta, 1));  // one per block: the 8-row blocks of the rows form are the most
         fresh->hist.alloc(fresh->cap);
         fresh->alphas.alloc(fresh->cap);
         fresh->betas.alloc(fresh->cap);
@@ -509,6 +556,37 @@ static PcgWork& pcg_work(Ctx* ctx, const DMatrix& W, int maxit)
         w = fresh.get();
     }
     return *w;
+}
+
+// L2 residency of W across the PCG iterations.  B200's 126 MB L2 can hold most of a
+// matrix of up to ~100 MB (config 2: 126 MB, config 3: 361 MB, partly): W is read once per
+// iteration, so an access-policy window marking it persisting keeps the part that fits in
+// the persisting carve-out on chip from one iteration to the next instead of streaming it
+// from HBM every time (hitRatio = carve-out / window when W is larger).  Matrices far larger
+// than L2 (config 5: 5.1 GB) gain nothing and get no window.  SBG_L2_PERSIST=0 disables it.
+static bool l2_window(Ctx* ctx, const DMatrix& W, cudaAccessPolicyWindow& win)
+{
+    static const bool enabled = [] {
+        const char* e = getenv("SBG_L2_PERSIST");
+        return !(e && e[0] == '0');
+    }();
+    if (!enabled || W.n == 0) return false;
+    int maxwin = 0, maxpersist = 0;
+    SBG_CUDA(cudaDeviceGetAttribute(&maxwin, cudaDevAttrMaxAccessPolicyWindowSize, ctx->device));
+    SBG_CUDA(cudaDeviceGetAttribute(&maxpersist, cudaDevAttrMaxPersistingL2CacheSize, ctx->device));
+    const size_t bytes = (size_t)W.n * W.ld * sizeof(double);
+    if (maxwin <= 0 || maxpersist <= 0 || bytes > 4 * (size_t)maxpersist) return false;
+    static bool limit_set = false;
+    if (!limit_set) {
+        SBG_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)maxpersist));
+        limit_set = true;
+    }
+    win.base_ptr = W.a.p;
+    win.num_bytes = std::min(bytes, (size_t)maxwin);
+    win.hitRatio = (float)std::min(1.0, (double)maxpersist / (double)win.num_bytes);
+    win.hitProp = cudaAccessPropertyPersisting;
+    win.missProp = cudaAccessPropertyStreaming;
+    return true;
 }
 
 // reference: inc/pcg.hpp:33-116.  All vectors and scalars stay on the device;
@@ -541,7 +619,10 @@ void pcg_run(Ctx* ctx, const DMatrix& W, Prec* prec, const double* rhs, double* 
     double* zbuf = r + len;
     double* p = zbuf + len;
     double* Wp = p + len;
+    double* rn = Wp + len;  // the fused apply's new residual (copied back into r)
     double* z = prec ? zbuf : r;  // no preconditioner: z = r (pcg.hpp:45-47)
+    cudaAccessPolicyWindow keep_win{};
+    const bool keep_W = !rows && pcg_graph_enabled() && l2_window(ctx, W, keep_win);  // W held in L2 (graph form)
     SBG_CUDA(cudaMemcpyAsync(r, rhs, n * sizeof(double), on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
     const int nb = (n + 255) / 256;
     PcgDev h{};
@@ -602,8 +683,21 @@ void pcg_run(Ctx* ctx, const DMatrix& W, Prec* prec, const double* rhs, double* 
                 if (rows->exchange(rows->user, p, w.xbuf.p, n, (void*)s) != 0)
                     throw std::runtime_error("pcg: the row-panel exchange failed");
             }
-            launch_pdl(k_pcg_alpha, dim3(nb), dim3(256), 0, s, w.st.p, (const double*)w.xbuf.p, 1, W.ld, n, p, Wp,
-                       w.partials.p);
+            if (w.plan.rows)  // the reduction tree of the single-GPU rows form (bitwise the same alpha)
+                launch_pdl(k_pcg_alpha8, dim3((n + kRowsPerCta - 1) / kRowsPerCta), dim3(256), 0, s, w.st.p,
+                           (const double*)w.xbuf.p, n, (const double*)p, Wp, w.partials.p);
+            else
+                launch_pdl(k_pcg_alpha, dim3(nb), dim3(256), 0, s, w.st.p, (const double*)w.xbuf.p, 1, W.ld, n, p,
+                           Wp, w.partials.p);
+        } else if (w.plan.rows) {  // rows form: W p and alpha in one launch
+            TimedScope ts(ctx, "gemv_f64");
+            const dim3 grid((n + kRowsPerCta - 1) / kRowsPerCta);
+            if (keep_W)
+                launch_pdl(k_gemv_rows_alpha<true>, grid, dim3(256), 0, s, w.st.p, (const double*)W.a.p, W.ld, n,
+                           (const double*)p, Wp, w.partials.p);
+            else
+                launch_pdl(k_gemv_rows_alpha<false>, grid, dim3(256), 0, s, w.st.p, (const double*)W.a.p, W.ld, n,
+                           (const double*)p, Wp, w.partials.p);
         } else {
             {
                 TimedScope ts(ctx, "gemv_f64");
@@ -613,12 +707,18 @@ void pcg_run(Ctx* ctx, const DMatrix& W, Prec* prec, const double* rhs, double* 
                        w.partials.p);
         }
         count_launch();
-        launch_pdl(k_pcg_update, dim3(nb), dim3(256), 0, s, w.st.p, x, r, p, Wp, n);
-        count_launch();
-        if (exact) enqueue_energy(1, 1);
-        if (prec) prec_apply(ctx, prec, r, z, done);
-        launch_pdl(k_pcg_rz, dim3(nb), dim3(256), 0, s, w.st.p, r, z, n, w.partials.p, w.hist.p, w.alphas.p, w.betas.p);
-        count_launch();
+        // x += alpha p, r -= alpha Wp, z = M r, r.z and beta: fused into the preconditioner's
+        // three launches when it allows (inverse mode), else one kernel per step
+        const PcgFused fu{w.st.p, x, r, rn, p, Wp, z, w.partials.p, w.hist.p, w.alphas.p, w.betas.p, done};
+        if (exact || !prec || !prec_apply_pcg(ctx, prec, fu)) {
+            launch_pdl(k_pcg_update, dim3(nb), dim3(256), 0, s, w.st.p, x, r, p, Wp, n);
+            count_launch();
+            if (exact) enqueue_energy(1, 1);
+            if (prec) prec_apply(ctx, prec, r, z, done);
+            launch_pdl(k_pcg_rz, dim3(nb), dim3(256), 0, s, w.st.p, r, z, n, w.partials.p, w.hist.p, w.alphas.p,
+                       w.betas.p);
+            count_launch();
+        }
         launch_pdl(k_pcg_p, dim3(nb), dim3(256), 0, s, w.st.p, p, z, n);
         count_launch();
         SBG_LAUNCH_CHECK();
@@ -658,6 +758,21 @@ void pcg_run(Ctx* ctx, const DMatrix& W, Prec* prec, const double* rhs, double* 
                 enqueue_iteration();
                 k_pcg_gate<<<1, 32, 0, s>>>(w.st.p, handle);
                 SBG_CUDA(cudaStreamEndCapture(s, &g_out));
+                cudaAccessPolicyWindow win{};
+                if (l2_window(ctx, W, win)) {  // W persisting in L2 for every kernel of the body
+                    size_t nb = 0;
+                    SBG_CUDA(cudaGraphGetNodes(body, nullptr, &nb));
+                    std::vector<cudaGraphNode_t> bn(nb);
+                    SBG_CUDA(cudaGraphGetNodes(body, bn.data(), &nb));
+                    cudaKernelNodeAttrValue v{};
+                    v.accessPolicyWindow = win;
+                    for (cudaGraphNode_t nd : bn) {
+                        cudaGraphNodeType t;
+                        SBG_CUDA(cudaGraphNodeGetType(nd, &t));
+                        if (t == cudaGraphNodeTypeKernel)
+                            SBG_CUDA(cudaGraphKernelNodeSetAttribute(nd, cudaKernelNodeAttributeAccessPolicyWindow, &v));
+                    }
+                }
                 // same topology (a new preconditioner of the same kind): update the
                 // instantiated graph in place instead of instantiating again
                 bool updated = false;
@@ -716,6 +831,10 @@ void pcg_run(Ctx* ctx, const DMatrix& W, Prec* prec, const double* rhs, double* 
         for (int t = 0; t < todo; ++t) enqueue_iteration();
         enqueued += todo;
         batch = std::min(batch * 2, 64);
+    }
+    {
+        cudaAccessPolicyWindow win{};
+        if (l2_window(ctx, W, win)) SBG_CUDA(cudaCtxResetPersistingL2Cache());  // give L2 back to what follows
     }
     const PcgDev fin = *w.hs;
     if (fin.error == 1) throw NumericalError("pcg: matrix is not positive definite");

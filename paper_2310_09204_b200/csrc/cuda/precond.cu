@@ -22,6 +22,7 @@
 #include <cstdlib>
 
 #include "kernels.cuh"
+#include "pcg_dev.cuh"
 
 namespace sbg {
 
@@ -791,6 +792,90 @@ __global__ void k_prec_scatter(const double* __restrict__ locy, const int* __res
     z[d] = out;
 }
 
+// ---------------------------------------------------------------- PCG-fused apply
+// The preconditioner apply inside a PCG iteration, fused with its neighbours
+// (pcg.hpp:74-79): k_prec_gather_upd does the iteration's update — x += alpha p, the new
+// residual r - alpha Wp into rn — while gathering it into the block-local vector, and the
+// coarse restriction CTAs form R^T (r - alpha Wp) from the untouched r; k_block_gemv is
+// unchanged; k_prec_scatter_rz forms z and r.z in one pass (copying rn back to r) and its
+// last block finishes the iteration's scalars (beta, history, stopping test).
+__global__ void __launch_bounds__(256) k_prec_gather_upd(const PcgDev* st, double* __restrict__ x,
+                                                         const double* __restrict__ r, double* __restrict__ rn,
+                                                         const double* __restrict__ p, const double* __restrict__ Wp,
+                                                         int n, const int* __restrict__ pos, double* __restrict__ loc,
+                                                         const int* __restrict__ cptr, const int* __restrict__ crow,
+                                                         const double* __restrict__ cval, int nc,
+                                                         double* __restrict__ loc_c, int dof_blocks)
+{
+    pdl_wait();
+    if (st->done) return;
+    const double a = st->alpha;
+    if ((int)blockIdx.x < dof_blocks) {
+        const int d = blockIdx.x * blockDim.x + threadIdx.x;
+        if (d < n) {
+            const double rv = r[d] - a * Wp[d];
+            rn[d] = rv;
+            x[d] += a * p[d];
+            if (pos[d] >= 0) loc[pos[d]] = rv;
+        }
+        return;
+    }
+    __shared__ double red[8];
+    const int c = (int)blockIdx.x - dof_blocks;
+    if (c >= nc) return;
+    const int q0 = cptr[c], q1 = cptr[c + 1];
+    double s0 = 0.0, s1 = 0.0;
+    int q = q0 + threadIdx.x;
+    for (; q + 256 < q1; q += 2 * 256) {
+        const int i0 = crow[q], i1 = crow[q + 256];
+        s0 += cval[q] * (r[i0] - a * Wp[i0]);
+        s1 += cval[q + 256] * (r[i1] - a * Wp[i1]);
+    }
+    for (; q < q1; q += 256) s0 += cval[q] * (r[crow[q]] - a * Wp[crow[q]]);
+    double v = s0 + s1;
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < 8; ++w) t += red[w];
+        loc_c[c] = t;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_prec_scatter_rz(PcgDev* st, const double* __restrict__ locy,
+                                                         const int* __restrict__ pos, int n,
+                                                         const int* __restrict__ rptr, const int* __restrict__ rcol,
+                                                         const double* __restrict__ rval,
+                                                         const double* __restrict__ y_c, double* __restrict__ z,
+                                                         double* __restrict__ r, const double* __restrict__ rn,
+                                                         double* partials, double* hist, double* alphas, double* betas)
+{
+    pdl_wait();
+    if (st->done) return;
+    __shared__ double sh[32];
+    const int d = blockIdx.x * blockDim.x + threadIdx.x;
+    double v = 0.0;
+    if (d < n) {
+        double out = pos[d] >= 0 ? locy[pos[d]] : 0.0;
+        if (rptr) {
+            double y = 0.0;
+            for (int q = rptr[d]; q < rptr[d + 1]; ++q) y += rval[q] * y_c[rcol[q]];
+            out += y;
+        }
+        z[d] = out;
+        const double rv = rn[d];
+        r[d] = rv;
+        v = rv * out;
+    }
+    v = block_sum(v, sh);
+    if (last_block(v, partials, &st->counter) && threadIdx.x == 0) {
+        const double rz_new = sum_partials(partials, gridDim.x);
+        st->counter = 0;
+        pcg_finish_rz(st, rz_new, hist, alphas, betas);
+    }
+}
+
 // H = R^T W R (schwarz.hpp:110-116 with the sparse R) into a padded ldh x ldh block
 void coarse_galerkin_device(Ctx* ctx, const DMatrix& W, const std::vector<int>& col_ptr,
                             const std::vector<int>& row_idx, const int* cptr, const int* crow, const double* cval,
@@ -1264,6 +1349,33 @@ void prec_apply(Ctx* ctx, Prec* P, const double* r, double* z, const int* done)
                (const double*)(cb >= 0 ? yloc + P->h_loc[cb] : nullptr), z, done);
     count_launch();
     SBG_LAUNCH_CHECK();
+}
+
+// The PCG-fused apply (inverse mode; see k_prec_gather_upd): the iteration's update, the
+// apply and r.z in three launches.  Returns false for the TRSV mode (not fused).
+bool prec_apply_pcg(Ctx* ctx, Prec* P, const PcgFused& f)
+{
+    if (P->mode != kPrecInverse || P->n == 0) return false;
+    TimedScope ts(ctx, "precond_apply");
+    cudaStream_t s = ctx->stream;
+    const int n = P->n;
+    const int cb = P->coarse_block;
+    double* loc_c = cb >= 0 ? P->loc.p + P->h_loc[cb] : nullptr;
+    const int dof_blocks = (n + 255) / 256;
+    launch_pdl(k_prec_gather_upd, dim3(dof_blocks + P->nc), dim3(256), 0, s, (const PcgDev*)f.st, f.x,
+               (const double*)f.r, f.rn, f.p, f.Wp, n, (const int*)P->pos.p, P->loc.p, (const int*)P->Rc_ptr.p,
+               (const int*)P->Rc_row.p, (const double*)P->Rc_val.p, P->nc, loc_c, dof_blocks);
+    count_launch();
+    launch_pdl(k_block_gemv, dim3((unsigned)P->sched->gemv.size()), dim3(256), 0, s, P->sched->d_gemv.p,
+               P->d_nb.p, P->d_ldm.p, P->d_loc.p, P->d_Moff.p, P->Mc.p, P->loc.p, P->locy.p, f.done);
+    count_launch();
+    launch_pdl(k_prec_scatter_rz, dim3(dof_blocks), dim3(256), 0, s, f.st, (const double*)P->locy.p,
+               (const int*)P->pos.p, n, (const int*)(P->nc > 0 ? P->Rr_ptr.p : nullptr), (const int*)P->Rr_col.p,
+               (const double*)P->Rr_val.p, (const double*)(cb >= 0 ? P->locy.p + P->h_loc[cb] : nullptr), f.z, f.r,
+               (const double*)f.rn, f.partials, f.hist, f.alphas, f.betas);
+    count_launch();
+    SBG_LAUNCH_CHECK();
+    return true;
 }
 
 // diagonal of the block's Cholesky factor (TRSV mode) or of its inverse (inverse mode)

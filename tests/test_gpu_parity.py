@@ -181,6 +181,30 @@ def test_preconditioner_large_blocks_multi_tile(ctx, mode):
     assert np.abs(z - zo).max() <= 1e-11 * np.abs(zo).max()
 
 
+@pytest.mark.parametrize("mode", ["inverse", "trsv"])
+def test_preconditioner_blocks_beyond_one_panel(ctx, mode):
+    """A 1100-DOF wire-basket block = 18 tiles: two panels of 8 tile columns complete, so the
+    panel-end trailing updates (near part on the main stream, far part on the look-ahead
+    stream) and the L^-1 panel updates run; faces of 1 and 2 tiles and a coarse block ride
+    in the same batch."""
+    n = 1300
+    W0 = O.random_spd(n, 31)
+    W = S.GalerkinMatrix.from_host(W0, ctx)
+    faces = {2: list(range(0, 60)), 7: list(range(60, 200))}
+    wb = list(range(200, n))
+    part = S.DofPartition.create(faces, wb)
+    cols = [np.arange(c, n, 97) for c in range(5)]  # a 5-column prolongation with disjoint supports
+    col_ptr = np.cumsum([0] + [len(c) for c in cols]).astype(np.int32)
+    row_idx = np.concatenate(cols).astype(np.int32)
+    val = np.linspace(0.5, 1.5, len(row_idx))
+    P = S.Prolongation.create(n, 5, col_ptr, row_idx, val)
+    prec = S.build_preconditioner(W, part, P, mode)
+    oprec = O.build_preconditioner(W0, O.partition_from(faces, wb), O.prolongation_from(n, 5, col_ptr, row_idx, val))
+    r = O.normal_draws(4, n)
+    z, zo = prec.apply(r), oprec.apply(r)
+    assert np.abs(z - zo).max() <= 1e-10 * np.abs(zo).max()
+
+
 def test_identity_pair_M_is_twice_Winv(ctx):
     m = S.make_builtin("bowtie:1")
     im = S.inflate(m)
