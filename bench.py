@@ -374,7 +374,7 @@ def run_reference(args):
 def matvec_traffic(cfg: int):
     """DRAM bytes per matvec launch from the committed ncu capture for this config (or None)."""
     try:
-        with open(os.path.join(ROOT, "profiles", "r01_traffic.json")) as f:
+        with open(os.path.join(ROOT, "profiles", "r02_traffic.json")) as f:
             e = json.load(f)["gemv_f64"].get(str(cfg))
         return None if e is None else e["dram_read"] + e["dram_write"]
     except Exception:
@@ -385,7 +385,7 @@ def kernel_traffic(kernel: str, cfg: int):
     """DRAM bytes per step of an assembly kernel (summed over its launches in one step) from
     the committed ncu --set full capture for this config (or None)."""
     try:
-        with open(os.path.join(ROOT, "profiles", "r01_traffic.json")) as f:
+        with open(os.path.join(ROOT, "profiles", "r02_traffic.json")) as f:
             e = json.load(f)[kernel].get(str(cfg))
         return None if e is None else int(sum(e["dram_bytes_per_step"]))
     except Exception:
@@ -648,7 +648,7 @@ def run_ours(args):
                          "unit": "TFLOP/s", "frac": achieved / fp64_peak if fp64_peak else None,
                          "traffic": kernel_traffic(dom[0], cfg),
                          "traffic_note": "DRAM bytes per step (all launches of the kernel in one step) from "
-                                         "profiles/r01_traffic.json; the kernel is FP64-bound, so the bytes only "
+                                         "profiles/r02_traffic.json; the kernel is FP64-bound, so the bytes only "
                                          "show it re-reads nothing (leaf list, geometry and W updates)",
                          "peak_source": "DFMA loop measured by bench.py on this GPU (MEASURED_PEAKS.json has no fp64)",
                          "flop_convention": "20 flop per tensor-rule kernel evaluation (SURVEY.md §8d)",
