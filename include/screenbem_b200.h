@@ -126,6 +126,13 @@ int sbg_inflated_export(const sbg_inflated* im, int32_t* q, int32_t* gv_first, i
 /* assemble_W (inc/assemble.hpp:72-139); `workers` is accepted and ignored */
 int sbg_assemble_w(sbg_ctx* ctx, const sbg_inflated* im, const sbg_quad_cfg* cfg, int workers, sbg_matrix** out,
                    sbg_assembly_stats* stats);
+/* assemble_W with the host copy the reference returns (inc/assemble.hpp:72-139 returns W by
+ * value): also fills host_w (n x n row-major doubles).  A page-locked host_w (sbg_host_alloc,
+ * cudaHostRegister) gets the device-to-host copy overlapped with the near field (the far
+ * part of W streams out while the near pairs are integrated, then only the band of entries
+ * they touched is copied again); any other buffer is filled after the assembly. */
+int sbg_assemble_w_host(sbg_ctx* ctx, const sbg_inflated* im, const sbg_quad_cfg* cfg, int workers, double* host_w,
+                        sbg_matrix** out, sbg_assembly_stats* stats);
 /* the same split in two: host preparation of one mesh (facet blocks, curl lists,
  * singular lists, rules, uploaded once) and the device-only assembly, which
  * (re)fills *W (allocated on first use) */

@@ -452,14 +452,30 @@ int sbg_inflated_export(const sbg_inflated* imh, int32_t* q, int32_t* gv_first, 
 int sbg_assemble_w(sbg_ctx* ctx, const sbg_inflated* im, const sbg_quad_cfg* cfg, int workers, sbg_matrix** out,
                    sbg_assembly_stats* stats)
 {
+    return sbg_assemble_w_host(ctx, im, cfg, workers, nullptr, out, stats);
+}
+int sbg_assemble_w_host(sbg_ctx* ctx, const sbg_inflated* im, const sbg_quad_cfg* cfg, int workers, double* host_w,
+                        sbg_matrix** out, sbg_assembly_stats* stats)
+{
     (void)workers;  // the reference's std::thread count; the GPU path ignores it
     return guard([&] {
         need(ctx, "ctx");
+        need(im, "im");
+        need(out, "out");
         bind_device(&ctx->c);
         auto* W = new sbg_matrix;
         try {
             AssemblyStats st;
-            assemble_W(&ctx->c, im->im, qcfg(cfg), W->M, &st);
+            // a page-locked destination gets the copy overlapped with the near field; any other
+            // destination is filled by the ordinary download afterwards
+            bool pinned = false;
+            if (host_w) {
+                cudaPointerAttributes pa{};
+                pinned = cudaPointerGetAttributes(&pa, host_w) == cudaSuccess && pa.type == cudaMemoryTypeHost;
+                (void)cudaGetLastError();
+            }
+            assemble_W(&ctx->c, im->im, qcfg(cfg), W->M, &st, pinned ? host_w : nullptr);
+            if (host_w && !pinned) matrix_download(W->M, host_w);
             if (stats) {
                 stats->far_pairs = st.far_pairs;
                 stats->near_pairs = st.near_pairs;

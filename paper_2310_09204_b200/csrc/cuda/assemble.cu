@@ -913,10 +913,11 @@ __global__ void k_sauter_finish(const double* __restrict__ part, int npairs, int
 
 // ---------------------------------------------------------------- per-pair scatter (near + singular)
 // pairs [0, nsing) are the singular pairs, then min(*nnear, near_cap) near pairs (device count)
+// band (optional): max |da - db| over the entries written, for the host copy's band patch
 __global__ void k_local_scatter(const int2* __restrict__ pairs, const double* __restrict__ I, long long nsing,
                                 const unsigned long long* __restrict__ nnear, long long near_cap,
                                 const int* __restrict__ uptr, const int* __restrict__ udof,
-                                const double* __restrict__ uval, double* __restrict__ W, int ld)
+                                const double* __restrict__ uval, double* __restrict__ W, int ld, int* __restrict__ band)
 {
     const long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= nsing + min((long long)*nnear, near_cap)) return;
@@ -928,6 +929,7 @@ __global__ void k_local_scatter(const int2* __restrict__ pairs, const double* __
         for (int q = uptr[g]; q < uptr[g + 1]; ++q) {
             const int db = udof[q];
             const double v = val * fma(ax, uval[3 * q], fma(ay, uval[3 * q + 1], az * uval[3 * q + 2]));
+            if (band) atomicMax(band, abs(da - db));
             if (f == g) {
                 if (da <= db) atomicAdd(W + (size_t)da * ld + db, v);
             } else if (da < db) {
@@ -963,6 +965,16 @@ __global__ void k_mirror(double* __restrict__ W, int n, int ld, int* __restrict_
         const int i = bj * 32 + r, j = bi * 32 + tx;  // destination (lower) element (i, j) = source (j, i)
         if (i < n && j < n && i > j) W[(size_t)i * ld + j] = tile[tx][r];
     }
+}
+
+// rows' band [max(0, i - K), min(n, i + K + 1)) of W packed contiguously (row i at i * (2K + 1))
+__global__ void k_pack_band(const double* __restrict__ W, int n, int ld, int K, double* __restrict__ out)
+{
+    const int i = blockIdx.y;
+    const int lo = max(0, i - K), hi = min(n, i + K + 1);
+    double* dst = out + (size_t)i * (2 * K + 1);
+    for (int j = lo + blockIdx.x * blockDim.x + threadIdx.x; j < hi; j += gridDim.x * blockDim.x)
+        dst[j - lo] = W[(size_t)i * ld + j];
 }
 
 // ---------------------------------------------------------------- RHS (assemble.hpp:143-184)
@@ -1414,9 +1426,11 @@ __global__ void k_near_init(const unsigned long long* __restrict__ np_dev, long 
 // come from the previous runs on this context (or generous first guesses), and an overflow
 // is reported there so the caller can regrow (near_regrow) and run again.
 // (rank, world): only the near pairs this rank owns are integrated (the others' out = 0).
+void run_near_leaves(Ctx* ctx, const RuleDims& R, const double* GV, const double* GA, const int2* pairs, double* out,
+                     NearWork& NW);
 void run_near(Ctx* ctx, const RuleDims& R, const double* GV, const double* GA, const int2* pairs,
               const unsigned long long* np_dev, long long cap, double thr, double* out, NearWork& NW, int rank = 0,
-              int world = 1)
+              int world = 1, bool leaves_now = true)
 {
     if (cap <= 0) return;
     cudaStream_t s = ctx->stream;
@@ -1448,6 +1462,17 @@ void run_near(Ctx* ctx, const RuleDims& R, const double* GV, const double* GA, c
             SBG_LAUNCH_CHECK();
         }
     }
+    SBG_CUDA(cudaMemcpyAsync(NW.hcnt, NW.cnt.p, kNearCnt * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+    if (leaves_now) run_near_leaves(ctx, R, GV, GA, pairs, out, NW);
+}
+
+// the leaf launch of run_near (separate when the assembly puts the far tiles in between)
+void run_near_leaves(Ctx* ctx, const RuleDims& R, const double* GV, const double* GA, const int2* pairs, double* out,
+                     NearWork& NW)
+{
+    if (!NW.leaves.n) return;
+    cudaStream_t s = ctx->stream;
+    const long long Lcap = (long long)NW.leaves.n;
     {
         TimedScope tl_scope(ctx, "near_leaves");
         const int lgrid = 2 * ctx->sm_count;  // persistent: the leaf count is read on the device
@@ -1466,7 +1491,6 @@ void run_near(Ctx* ctx, const RuleDims& R, const double* GV, const double* GA, c
         count_launch();
         SBG_LAUNCH_CHECK();
     }
-    SBG_CUDA(cudaMemcpyAsync(NW.hcnt, NW.cnt.p, kNearCnt * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
 }
 
 // after the stream has synchronised: leaves, pairs this rank integrated, overflow
@@ -1557,6 +1581,7 @@ struct AssemblyPlan {
     DBuf<double> loc_I;
     DBuf<unsigned long long> near_cnt;
     DBuf<int> bad;  // non-finite flag of the mirror pass
+    DBuf<int> band;  // max |i - j| of the near/singular entries (the host copy's band patch)
     // deferred curl-dependent half (plan_finish)
     std::unique_ptr<Stager> st;
     std::future<FacetCurls> curl_fut;
@@ -1807,7 +1832,7 @@ void assembly_plan_destroy(AssemblyPlan* P) { delete P; }
 // zeroed W: far tiles k with k % world == rank, the near pairs it owns
 // (near_owner), and a contiguous 1/world range of each singular class.  The shards' W sum to the
 // full W (up to fp64 atomic reordering); DESIGN.md §5.3.
-void assembly_run(AssemblyPlan* P, DMatrix& W, AssemblyStats* stats, int rank, int world)
+void assembly_run(AssemblyPlan* P, DMatrix& W, AssemblyStats* stats, int rank, int world, double* host_dst)
 {
     if (world < 1 || rank < 0 || rank >= world) throw ValidationError("shard: need 0 <= rank < world");
     Ctx* ctx = P->ctx;
@@ -1834,10 +1859,49 @@ void assembly_run(AssemblyPlan* P, DMatrix& W, AssemblyStats* stats, int rank, i
     NearWork& NW = near_work(ctx);
     unsigned long long* hnear = near_host_counters(NW) + kNearCnt;
     NearResult nr;
+    // host_dst (page-locked, n x n row-major): W is also copied to the host, overlapped with
+    // the near field — the far tiles run first and are mirrored, the copy of the whole W then
+    // streams out on the auxiliary stream while the near leaves, the Sauter classes and their
+    // scatter run, and afterwards only the band |i - j| <= K of entries the near/singular pairs
+    // touched (K measured on the device) is copied again, straight from the device rows into
+    // the host rows with one pitched DMA (row i's band starts (n + 1) elements after row i-1's)
+    const bool to_host = host_dst != nullptr && world == 1;
+    cudaStream_t cs = to_host ? aux_stream(ctx) : nullptr;
+    cudaEvent_t ev_far = nullptr, ev_copy = nullptr;
+    if (to_host) {
+        SBG_CUDA(cudaEventCreateWithFlags(&ev_far, cudaEventDisableTiming));
+        SBG_CUDA(cudaEventCreateWithFlags(&ev_copy, cudaEventDisableTiming));
+    }
+    struct EvGuard {
+        cudaEvent_t a, b;
+        ~EvGuard()
+        {
+            if (a) cudaEventDestroy(a);
+            if (b) cudaEventDestroy(b);
+        }
+    } evg{ev_far, ev_copy};
+    if (to_host && !P->band.n) P->band.alloc(1);
+    auto enqueue_far = [&]() {
+        {
+            TimedScope ts(ctx, "far_tiles");
+            BlockPtrs BP{P->bfac.p, P->dof_ptr.p, P->dofs.p, P->ent_ptr.p, P->ents.p};
+            launch_far_tiles(ctx, R, P->tiles.p + rank, my_tiles, world, P->G.ptrs(), BP, thr, W, P->cfg.exact_far);
+            SBG_LAUNCH_CHECK();
+        }
+    };
+    auto enqueue_mirror = [&]() {
+        TimedScope ts(ctx, "mirror");
+        const int nt = (P->n + 31) / 32;
+        k_mirror<<<dim3(nt, nt), dim3(32, 8), 0, s>>>(W.a.p, P->n, W.ld, P->bad.p);
+        count_launch();
+        SBG_LAUNCH_CHECK();
+    };
     for (int attempt = 0;; ++attempt) {
         std::fill(NW.hcnt, NW.hcnt + kNearCnt + 2, 0ull);  // the previous run has synchronised
         if (attempt) SBG_CUDA(cudaMemsetAsync(W.a.p, 0, W.a.n * sizeof(double), s));
         SBG_CUDA(cudaMemsetAsync(P->near_cnt.p, 0, sizeof(unsigned long long), s));
+        SBG_CUDA(cudaMemsetAsync(P->bad.p, 0, sizeof(int), s));
+        if (to_host) SBG_CUDA(cudaMemsetAsync(P->band.p, 0, sizeof(int), s));
         if (my_cand) {  // near list: classification of the non-certainly-far tiles
             TimedScope ts(ctx, "classify");
             k_classify_near<<<(int)my_cand, 256, 0, s>>>(P->cand.p, 1, P->G.ptrs(), P->bfac.p, thr,
@@ -1846,9 +1910,19 @@ void assembly_run(AssemblyPlan* P, DMatrix& W, AssemblyStats* stats, int rank, i
             SBG_LAUNCH_CHECK();
         }
         run_near(ctx, R, P->G.v.p, P->G.area.p, P->loc_pairs.p + P->nsing, P->near_cnt.p, P->near_cap, thr,
-                 P->loc_I.p + P->nsing, NW, rank, world);
+                 P->loc_I.p + P->nsing, NW, rank, world, /*leaves_now=*/!to_host);
         // a deferred plan builds its curl-dependent half while the near field runs
         plan_finish(P);
+        if (to_host) {
+            enqueue_far();
+            enqueue_mirror();
+            SBG_CUDA(cudaEventRecord(ev_far, s));
+            SBG_CUDA(cudaStreamWaitEvent(cs, ev_far, 0));
+            SBG_CUDA(cudaMemcpy2DAsync(host_dst, sizeof(double) * (size_t)P->n, W.a.p, sizeof(double) * (size_t)W.ld,
+                                       sizeof(double) * (size_t)P->n, P->n, cudaMemcpyDeviceToHost, cs));
+            SBG_CUDA(cudaEventRecord(ev_copy, cs));
+            run_near_leaves(ctx, R, P->G.v.p, P->G.area.p, P->loc_pairs.p + P->nsing, P->loc_I.p + P->nsing, NW);
+        }
         // singular pairs (Sauter rules); a shard zeroes the integrals it does not own
         if (world > 1 && P->nsing) SBG_CUDA(cudaMemsetAsync(P->loc_I.p, 0, P->nsing * sizeof(double), s));
         for (int cls = 1; cls <= 3; ++cls) {
@@ -1864,32 +1938,24 @@ void assembly_run(AssemblyPlan* P, DMatrix& W, AssemblyStats* stats, int rank, i
             count_launch();
             SBG_LAUNCH_CHECK();
         }
-        {
-            TimedScope ts(ctx, "far_tiles");
-            BlockPtrs BP{P->bfac.p, P->dof_ptr.p, P->dofs.p, P->ent_ptr.p, P->ents.p};
-            launch_far_tiles(ctx, R, P->tiles.p + rank, my_tiles, world, P->G.ptrs(), BP, thr, W, P->cfg.exact_far);
-            SBG_LAUNCH_CHECK();
-        }
+        if (!to_host) enqueue_far();
         // per-pair scatter of singular + near integrals (near count read on the device)
         if (P->nsing + P->near_cap > 0) {
             TimedScope ts(ctx, "local_scatter");
             const long long nmax = P->nsing + P->near_cap;
             k_local_scatter<<<(int)((nmax + 127) / 128), 128, 0, s>>>(P->loc_pairs.p, P->loc_I.p, P->nsing,
                                                                       P->near_cnt.p, P->near_cap, P->uptr.p,
-                                                                      P->udof.p, P->uval.p, W.a.p, W.ld);
+                                                                      P->udof.p, P->uval.p, W.a.p, W.ld,
+                                                                      to_host ? P->band.p : nullptr);
             count_launch();
             SBG_LAUNCH_CHECK();
         }
-        {
-            TimedScope ts(ctx, "mirror");
-            const int nt = (P->n + 31) / 32;
-            SBG_CUDA(cudaMemsetAsync(P->bad.p, 0, sizeof(int), s));
-            k_mirror<<<dim3(nt, nt), dim3(32, 8), 0, s>>>(W.a.p, P->n, W.ld, P->bad.p);
-            count_launch();
-            SBG_LAUNCH_CHECK();
-        }
+        enqueue_mirror();  // (to_host: again — only the entries of the near band change)
         SBG_CUDA(cudaMemcpyAsync(hnear, P->near_cnt.p, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
         SBG_CUDA(cudaMemcpyAsync(hnear + 1, P->bad.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+        if (to_host)
+            SBG_CUDA(cudaMemcpyAsync(reinterpret_cast<int*>(hnear + 1) + 1, P->band.p, sizeof(int),
+                                     cudaMemcpyDeviceToHost, s));
         SBG_CUDA(cudaStreamSynchronize(s));
         nr = near_results(NW);
         const bool list_over = (long long)hnear[0] > P->near_cap;
@@ -1905,6 +1971,32 @@ void assembly_run(AssemblyPlan* P, DMatrix& W, AssemblyStats* stats, int rank, i
             P->loc_pairs = std::move(np2);
             P->loc_I = std::move(ni2);
         }
+    }
+    if (to_host) {
+        // the band patch, after the whole-W copy has landed
+        const int n = P->n;
+        const int K = std::min(reinterpret_cast<const int*>(hnear + 1)[1], n - 1);
+        TimedScope ts(ctx, "band_patch");
+        SBG_CUDA(cudaStreamWaitEvent(s, ev_copy, 0));
+        const size_t es = sizeof(double);
+        if (n > 2 * K + 1 && (size_t)(2 * K + 1) * 4 < (size_t)n) {
+            // interior rows: the diagonal band; the first and last K rows: the fixed window of
+            // 2K + 1 columns at the matrix edge that contains their clipped band (copying a
+            // few more final entries is harmless) — three DMAs in all
+            const size_t w = es * (2 * (size_t)K + 1);
+            SBG_CUDA(cudaMemcpy2DAsync(host_dst + (size_t)K * (n + 1) - K, es * ((size_t)n + 1),
+                                       W.a.p + (size_t)K * (W.ld + 1) - K, es * ((size_t)W.ld + 1), w, n - 2 * K,
+                                       cudaMemcpyDeviceToHost, s));
+            if (K > 0) {
+                SBG_CUDA(cudaMemcpy2DAsync(host_dst, es * n, W.a.p, es * W.ld, w, K, cudaMemcpyDeviceToHost, s));
+                const size_t c0 = (size_t)n - (2 * (size_t)K + 1), r0 = (size_t)n - K;
+                SBG_CUDA(cudaMemcpy2DAsync(host_dst + r0 * n + c0, es * n, W.a.p + r0 * W.ld + c0, es * W.ld, w, K,
+                                           cudaMemcpyDeviceToHost, s));
+            }
+        } else {  // a wide band (junction numberings): copy the whole W again
+            SBG_CUDA(cudaMemcpy2DAsync(host_dst, es * n, W.a.p, es * W.ld, es * n, n, cudaMemcpyDeviceToHost, s));
+        }
+        SBG_CUDA(cudaStreamSynchronize(s));
     }
     if (*reinterpret_cast<const int*>(hnear + 1)) throw NumericalError("quadrature produced a non-finite pair integral");
     const unsigned long long nnear = hnear[0];
@@ -1924,11 +2016,12 @@ void assembly_run(AssemblyPlan* P, DMatrix& W, AssemblyStats* stats, int rank, i
     }
 }
 
-void assemble_W(Ctx* ctx, const InflatedMesh& im, const QuadCfg& cfg, DMatrix& W, AssemblyStats* stats)
+void assemble_W(Ctx* ctx, const InflatedMesh& im, const QuadCfg& cfg, DMatrix& W, AssemblyStats* stats,
+                double* host_dst)
 {
     AssemblyPlan* P = assembly_plan_create(ctx, im, cfg, /*defer=*/true);
     try {
-        assembly_run(P, W, stats);
+        assembly_run(P, W, stats, 0, 1, host_dst);
         SBG_CUDA(cudaStreamSynchronize(ctx->stream));
     } catch (...) {
         delete P;

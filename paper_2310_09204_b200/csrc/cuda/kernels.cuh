@@ -150,8 +150,11 @@ struct AssemblyPlan;
 AssemblyPlan* assembly_plan_create(Ctx* ctx, const InflatedMesh& im, const QuadCfg& cfg, bool defer = false);
 void assembly_plan_destroy(AssemblyPlan* p);
 // (rank, world): one shard of the work (world 1 = the whole assembly), see assemble.cu
-void assembly_run(AssemblyPlan* p, DMatrix& W, AssemblyStats* stats, int rank = 0, int world = 1);
-void assemble_W(Ctx* ctx, const InflatedMesh& im, const QuadCfg& cfg, DMatrix& W, AssemblyStats* stats);
+// host_dst: also copy W to this page-locked n x n row-major buffer, overlapped with the near field
+void assembly_run(AssemblyPlan* p, DMatrix& W, AssemblyStats* stats, int rank = 0, int world = 1,
+                  double* host_dst = nullptr);
+void assemble_W(Ctx* ctx, const InflatedMesh& im, const QuadCfg& cfg, DMatrix& W, AssemblyStats* stats,
+                double* host_dst = nullptr);
 void pair_integrals(Ctx* ctx, const SurfaceMesh& m, const QuadCfg& cfg, const int* f, const int* g, long long np,
                     double* out);
 std::vector<double> rhs_points(const InflatedMesh& im, const QuadCfg& cfg);

@@ -88,6 +88,8 @@ SIGNATURES = {
     "sbg_inflated_sizes": (C.c_int, [vp] + [C.POINTER(C.c_int)] * 4),
     "sbg_inflated_export": (C.c_int, [vp, i32p, i32p, i32p, i32p, i32p, f64p]),
     "sbg_assemble_w": (C.c_int, [vp, vp, C.POINTER(QuadCfgC), C.c_int, C.POINTER(vp), C.POINTER(AssemblyStatsC)]),
+    "sbg_assemble_w_host": (C.c_int, [vp, vp, C.POINTER(QuadCfgC), C.c_int, vp, C.POINTER(vp),
+                                      C.POINTER(AssemblyStatsC)]),
     "sbg_matrix_create": (C.c_int, [vp, C.c_int, C.c_void_p, C.POINTER(vp)]),
     "sbg_matrix_n": (C.c_int, [vp]),
     "sbg_matrix_download": (C.c_int, [vp, f64p]),
@@ -506,14 +508,24 @@ class GalerkinMatrix(_Handle):
         return cls(h, ctx)
 
 
-def assemble_W(im: InflatedMesh, cfg: QuadratureConfig = None, workers: int = 1, ctx: Context = None):
-    """reference: inc/assemble.hpp:72-139.  `workers` is accepted and ignored."""
+def assemble_W(im: InflatedMesh, cfg: QuadratureConfig = None, workers: int = 1, ctx: Context = None, out=None):
+    """reference: inc/assemble.hpp:72-139.  `workers` is accepted and ignored.  `out` (an n x n
+    C-contiguous float64 array): also fill it with W — the reference returns W by value on the
+    host; a page-locked `out` (pinned_empty) gets the copy overlapped with the near field."""
     ctx = ctx or default_context()
     cfg = cfg or QuadratureConfig()
     c = cfg.c()
     st = AssemblyStatsC()
     h = vp()
-    _check(lib().sbg_assemble_w(ctx.h, im.h, C.byref(c), workers, C.byref(h), C.byref(st)))
+    if out is None:
+        _check(lib().sbg_assemble_w(ctx.h, im.h, C.byref(c), workers, C.byref(h), C.byref(st)))
+    else:
+        n = im.n
+        if not (isinstance(out, np.ndarray) and out.dtype == np.float64 and out.flags.c_contiguous
+                and out.size == n * n):
+            raise ValidationError("assemble_W: out must be a C-contiguous float64 array of n*n entries")
+        _check(lib().sbg_assemble_w_host(ctx.h, im.h, C.byref(c), workers, out.ctypes.data, C.byref(h),
+                                         C.byref(st)))
     stats = {n: getattr(st, n) for n, _ in AssemblyStatsC._fields_}
     return GalerkinMatrix(h, ctx, stats)
 

@@ -179,3 +179,22 @@ def test_jittered_nonplanar_mesh_matches_oracle(ctx):
     g = [0.3, -0.2, 1.0]
     L, Lo = S.assemble_rhs(im, g, ctx=ctx), O.assemble_rhs(oim, g)
     np.testing.assert_allclose(L, Lo, rtol=1e-12, atol=1e-15 * np.abs(Lo).max())
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 4])
+def test_assemble_W_into_host_buffer(cfg):
+    """assemble_W(im, out=buf) (C ABI sbg_assemble_w_host): the host copy equals the device W
+    bit for bit — page-locked buffers get the copy overlapped with the near field plus the
+    band patch (config 4's junction numbering takes the wide-band fallback), pageable ones
+    the ordinary download."""
+    ctx = S.Context(0)
+    im = S.inflate(S.make_config(cfg).fine, validate=False)
+    n = im.n
+    for pinned in (True, False):
+        buf = S.pinned_empty((n, n)) if pinned else np.full((n, n), np.nan)
+        W = S.assemble_W(im, ctx=ctx, out=buf)
+        Wd = W.download()
+        assert np.array_equal(buf, Wd), (cfg, pinned, np.abs(buf - Wd).max())
+        assert np.array_equal(Wd, Wd.T)
+    with pytest.raises(S.ValidationError):
+        S.assemble_W(im, ctx=ctx, out=np.zeros((n, n - 1)))
