@@ -570,17 +570,10 @@ def run_ours(args):
         Wbuf.fill(0.0)
         dest = "pageable host buffer allocated (and touched) once"
     pageable_ms = None
-    for it in range(2 + max(args.steps, 4)):  # first run warms the host paths; median over the rest
-        if it == 1:  # one run into a fresh pageable numpy array, for the record
-            ctx.reset_timers()
-            ctx.begin("e2e")
-            W2 = S.assemble_W(im2, ctx=ctx) if not shard else assemble(S.AssemblyPlan(im2, qcfg, ctx=ctx), None)
-            Wh = W2.download()
-            ctx.end()
-            ctx.synchronize()
-            pageable_ms = ctx.timer("e2e")[0]
-            del W2, Wh
-            continue
+    import gc
+    gc.collect()
+    gc.disable()  # no cyclic-GC pauses inside the timed e2e / time-to-solution runs
+    for it in range(1 + max(args.steps, 4)):  # first run warms the host paths; median over the rest
         ctx.reset_timers()
         t0 = time.perf_counter()
         ctx.begin("e2e")
@@ -620,6 +613,17 @@ def run_ours(args):
             del res, x
         tts_runs = [round(t, 2) for t in tts]
         tts.sort()
+    gc.enable()
+    # one assembly into a fresh pageable numpy array, for the record (last: the 5 GB of fresh
+    # pageable memory it faults in and frees does not run beside the timed e2e/tts runs)
+    ctx.reset_timers()
+    ctx.begin("e2e")
+    W2 = S.assemble_W(im2, ctx=ctx) if not shard else assemble(S.AssemblyPlan(im2, qcfg, ctx=ctx), None)
+    Wh = W2.download()
+    ctx.end()
+    ctx.synchronize()
+    pageable_ms = ctx.timer("e2e")[0]
+    del W2, Wh
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:

@@ -188,7 +188,9 @@ void sbg_prolong_destroy(sbg_prolong* p);
 /* ---- Schwarz preconditioner (device) -------------------------------------- */
 int sbg_build_preconditioner(sbg_ctx* ctx, const sbg_matrix* W, const sbg_partition* part, const sbg_prolong* R,
                              sbg_prec** out); /* inc/schwarz.hpp:100-118 */
-/* mode 1 (default): block inverses L^-T L^-1 formed once, apply = one batched GEMV;
+/* mode 1 (default): block inverses L^-T L^-1 formed once, apply = one batched GEMV (when the
+ * largest block exceeds 2048 DOFs, X = L^-1 is kept instead and the apply is X^T (X r), two
+ * triangular GEMVs over the same bytes); mode 2: that factored form always;
  * mode 0: blocked forward/backward triangular solves with L (llt.solve, schwarz.hpp:130) */
 int sbg_build_preconditioner_mode(sbg_ctx* ctx, const sbg_matrix* W, const sbg_partition* part, const sbg_prolong* R,
                                   int mode, sbg_prec** out);

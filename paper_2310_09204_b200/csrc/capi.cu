@@ -833,7 +833,8 @@ int sbg_build_preconditioner_mode(sbg_ctx* ctx, const sbg_matrix* W, const sbg_p
         need(part, "part");
         need(out, "out");
         bind_ctx(ctx);
-        if (mode != kPrecTrsv && mode != kPrecInverse) throw ValidationError("unknown preconditioner apply mode");
+        if (mode != kPrecTrsv && mode != kPrecInverse && mode != kPrecFactored)
+            throw ValidationError("unknown preconditioner apply mode");
         Prolongation none;
         none.rows = W->M.n;
         auto* p = new sbg_prec;

@@ -66,7 +66,11 @@ void gemv(Ctx* ctx, const DMatrix& W, GemvPlan& plan, const double* x, double* y
 
 // ---------------------------------------------------------------- Schwarz preconditioner
 struct Prec;
-enum { kPrecTrsv = 0, kPrecInverse = 1 };
+// kPrecInverse stores W_bb^-1 and applies one GEMV per block; when the largest block is big
+// (n_b > 2048: the L^-T L^-1 product costs more than it saves) it stores X = L^-1 instead
+// and applies z = X^T (X r) as two triangular GEMVs over the same bytes (kPrecFactored
+// forces that form)
+enum { kPrecTrsv = 0, kPrecInverse = 1, kPrecFactored = 2 };
 Prec* prec_build(Ctx* ctx, const DMatrix& W, const DofPartition& part, const Prolongation& R, int mode);
 int prec_mode(const Prec* p);
 unsigned long long prec_uid(const Prec* p);  // unique per preconditioner object

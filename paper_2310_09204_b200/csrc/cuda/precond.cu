@@ -54,12 +54,13 @@ struct PrecSchedule;
 struct Prec {
     Ctx* ctx = nullptr;
     int n = 0, nfaces = 0, nwb = 0, nc = 0, mode = kPrecInverse;
+    bool factored = false;  // inverse mode storing X = L^-1 (Mc: X below the diagonal, X^T above)
     int nblocks = 0, coarse_block = -1, Tmax = 0, maxnb = 0;
     std::vector<int> h_nb, h_T, h_loc, h_Doff, h_ldm;
     std::vector<long long> h_Poff, h_Moff;
     DBuf<int> d_nb, d_T, d_loc, d_Doff, d_ldm;
     DBuf<long long> d_Poff, d_Moff;
-    DBuf<double> Lp, Xp, D, Mc, loc, locy;
+    DBuf<double> Lp, Xp, D, Mc, loc, locy, loct;  // loct: X r of the factored apply
     DBuf<int> pos;  // dof -> loc index (face/WB), -1 if none
     DBuf<int> d_bptr, d_bdofs;  // face/WB block dof lists (CSR), for materialisation
     int ngather = 0;
@@ -685,6 +686,71 @@ __global__ void __launch_bounds__(256) k_block_gemv(const int2* __restrict__ tas
     if (lane == 0) locy[locv[b] + r] = v;
 }
 
+// The factored apply's two passes over Mc (X below the diagonal, X^T above, X's diagonal on
+// it): UPPER = false: t = X x over columns c <= r; UPPER = true: z = X^T t over columns c >= r.
+// Same layout and loads as k_block_gemv; the band edges are masked per element.
+template <bool UPPER>
+__global__ void __launch_bounds__(256) k_block_gemv_tri(const int2* __restrict__ tasks, const int* __restrict__ nbv,
+                                                        const int* __restrict__ ldmv, const int* __restrict__ locv,
+                                                        const long long* __restrict__ Moff,
+                                                        const double* __restrict__ Mc, const double* __restrict__ xin,
+                                                        double* __restrict__ yout, const int* done)
+{
+    pdl_wait();
+    if (done && *done) return;
+    // the lower pass takes the rows longest-first (its rows grow with r), so the last wave
+    // holds the shortest rows instead of the longest
+    const int2 t = tasks[UPPER ? blockIdx.x : gridDim.x - 1 - blockIdx.x];
+    const int b = t.x, nb = nbv[b], ldm = ldmv[b];
+    const int r = t.y + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+    if (r >= nb) return;
+    const double2* x2 = reinterpret_cast<const double2*>(xin + locv[b]);
+    const double2* row = reinterpret_cast<const double2*>(Mc + Moff[b] + (size_t)r * ldm);
+    const int c2lo = UPPER ? (r >> 1) : 0, c2hi = UPPER ? (ldm >> 1) : (r >> 1) + 1;
+    auto term = [&](int c2, const double2& a, const double2& xv) {
+        const int c = 2 * c2;
+        const double ax = (UPPER ? c >= r : c <= r) ? a.x : 0.0;
+        const double ay = (UPPER ? c + 1 >= r : c + 1 <= r) ? a.y : 0.0;
+        return fma(ax, xv.x, ay * xv.y);
+    };
+    double s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    int c2 = c2lo + lane;
+    for (; c2 + 7 * 32 < c2hi; c2 += 8 * 32) {
+        double2 a[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) a[u] = __ldcs(row + c2 + 32 * u);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) s[u] += term(c2 + 32 * u, a[u], __ldg(x2 + c2 + 32 * u));
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+        const int cc = c2 + 32 * u;
+        if (cc < c2hi) s[u] += term(cc, __ldcs(row + cc), __ldg(x2 + cc));
+    }
+    double v = ((s[0] + s[1]) + (s[2] + s[3])) + ((s[4] + s[5]) + (s[6] + s[7]));
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) yout[locv[b] + r] = v;
+}
+
+// full block inverses M_b = X_b^T X_b from the factored storage, for materialize / block_diag:
+// M[r][c] = sum_{q >= max(r,c)} X[q][r] X[q][c] (X[q][r] = Mc[q][r] below the diagonal)
+__global__ void k_factored_to_full(const int* __restrict__ nbv, const int* __restrict__ ldmv,
+                                   const long long* __restrict__ Moff, const double* __restrict__ Mc,
+                                   double* __restrict__ Mfull, int b)
+{
+    const int nb = nbv[b], ldm = ldmv[b];
+    const double* X = Mc + Moff[b];
+    double* M = Mfull + Moff[b];
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < (long long)nb * ldm;
+         e += (long long)gridDim.x * blockDim.x) {
+        const int r = (int)(e / ldm), c = (int)(e % ldm);
+        double acc = 0.0;
+        if (c < nb)
+            for (int q = max(r, c); q < nb; ++q) acc = fma(X[(size_t)q * ldm + r], X[(size_t)q * ldm + c], acc);
+        M[e] = acc;
+    }
+}
+
 // 4 threads per row: partial dot of a 64-wide tile row
 __device__ __forceinline__ double tile_row_dot(const double* __restrict__ T, size_t ld, int r, int kc,
                                                const double* v, int part)
@@ -1088,7 +1154,7 @@ std::shared_ptr<PrecSchedule> prec_schedule(Ctx* ctx, const Prec* P)
 // W_bb^-1 = L^-T L^-1 for every block from the tiled factor in Lwork (overwritten):
 // X = L^-1 by panels (K_XSTEP per row of tiles, K_XUPD at panel ends), then M = X^T X over Lwork, then
 // the compact row-major inverses (row stride ldm_b) into Mc.
-void form_inverses(Ctx* ctx, Prec* P, DBuf<double>& Lwork, DBuf<double>& Mc)
+void form_inverses(Ctx* ctx, Prec* P, DBuf<double>& Lwork, DBuf<double>& Mc, bool factored = false)
 {
     cudaStream_t s = ctx->stream;
     const PrecSchedule& S = *P->sched;
@@ -1108,15 +1174,17 @@ void form_inverses(Ctx* ctx, Prec* P, DBuf<double>& Lwork, DBuf<double>& Mc)
             launch_gemm<K_XUPD>(ctx, P, k, S.d_xu.p + S.xu.off[k], S.xu.count(k), Lwork.p, Xp.p);
         }
     }
-    {
+    if (!factored) {
         TimedScope t2(ctx, "inv_lauum");
         launch_gemm<K_LAUUM>(ctx, P, 0, S.d_la.p, (int)S.la.size(), Lwork.p, Xp.p);
     }
     const long long Msize = P->h_Moff.empty() ? 0 : P->h_Moff.back() + (long long)P->h_nb.back() * P->h_ldm.back();
     Mc.alloc(std::max<long long>(Msize, 1));
     if (!S.ct.empty()) {
-        k_compact_inverse<<<(int)S.ct.size(), 256, 0, s>>>(Lwork.p, P->d_Poff.p, P->d_T.p, P->d_nb.p, P->d_ldm.p,
-                                                           P->d_Moff.p, S.d_ct.p, Mc.p);
+        // the symmetric completion of a lower triangle: of M = X^T X (over Lwork), or of X
+        // itself for the factored storage (X below the diagonal, X^T above)
+        k_compact_inverse<<<(int)S.ct.size(), 256, 0, s>>>(factored ? Xp.p : Lwork.p, P->d_Poff.p, P->d_T.p,
+                                                           P->d_nb.p, P->d_ldm.p, P->d_Moff.p, S.d_ct.p, Mc.p);
         count_launch();
     }
     SBG_LAUNCH_CHECK();
@@ -1281,10 +1349,19 @@ Prec* prec_build(Ctx* ctx, const DMatrix& W, const DofPartition& part, const Pro
                                      (kinds[b] == 0 ? "face" : "wire-basket") +
                                      "): partition inconsistent with the assembled matrix");
             }
-        if (mode == kPrecInverse) {
+        if (mode == kPrecInverse || mode == kPrecFactored) {
+            // the factored storage when the L^-T L^-1 product would cost more than the second
+            // GEMV pass of every apply saves (largest block > 2048 DOFs: config 5 H/h 8-20, 4)
+            static const int force = [] {
+                const char* e = std::getenv("SBG_PREC_FACTORED");
+                return e ? std::atoi(e) : -1;
+            }();
+            P->factored = mode == kPrecFactored || (force < 0 ? P->maxnb > 2048 : force > 0);
+            P->mode = kPrecInverse;
+            if (P->factored) P->loct.alloc(P->loc.n);
             {
                 TimedScope ts(ctx, "block_inverse");
-                form_inverses(ctx, P, P->Lp, P->Mc);
+                form_inverses(ctx, P, P->Lp, P->Mc, P->factored);
             }
             P->Lp.release();
             P->D.release();
@@ -1307,6 +1384,28 @@ int prec_num_subspaces(const Prec* p)  // schwarz.hpp:66-72
 double prec_factor_bytes(const Prec* p) { return p->apply_bytes; }
 
 // reference: inc/schwarz.hpp:121-140
+// y_b = W_bb^-1 x_b for every block (loc -> locy): one GEMV over the stored inverses, or the
+// factored storage's two triangular passes t = X x (loc -> loct), y = X^T t (loct -> locy)
+static void enqueue_block_inverse(Ctx* ctx, Prec* P, const int* done)
+{
+    cudaStream_t s = ctx->stream;
+    const dim3 grid((unsigned)P->sched->gemv.size()), block(256);
+    if (!P->factored) {
+        launch_pdl(k_block_gemv, grid, block, 0, s, P->sched->d_gemv.p, P->d_nb.p, P->d_ldm.p, P->d_loc.p,
+                   P->d_Moff.p, P->Mc.p, P->loc.p, P->locy.p, done);
+        count_launch();
+        return;
+    }
+    launch_pdl(k_block_gemv_tri<false>, grid, block, 0, s, (const int2*)P->sched->d_gemv.p, (const int*)P->d_nb.p,
+               (const int*)P->d_ldm.p, (const int*)P->d_loc.p, (const long long*)P->d_Moff.p, (const double*)P->Mc.p,
+               (const double*)P->loc.p, P->loct.p, done);
+    count_launch();
+    launch_pdl(k_block_gemv_tri<true>, grid, block, 0, s, (const int2*)P->sched->d_gemv.p, (const int*)P->d_nb.p,
+               (const int*)P->d_ldm.p, (const int*)P->d_loc.p, (const long long*)P->d_Moff.p, (const double*)P->Mc.p,
+               (const double*)P->loct.p, P->locy.p, done);
+    count_launch();
+}
+
 void prec_apply(Ctx* ctx, Prec* P, const double* r, double* z, const int* done)
 {
     TimedScope ts(ctx, "precond_apply");
@@ -1321,9 +1420,7 @@ void prec_apply(Ctx* ctx, Prec* P, const double* r, double* z, const int* done)
     count_launch();
     const double* yloc;
     if (P->mode == kPrecInverse) {
-        launch_pdl(k_block_gemv, dim3((unsigned)P->sched->gemv.size()), dim3(256), 0, s, P->sched->d_gemv.p,
-                   P->d_nb.p, P->d_ldm.p, P->d_loc.p, P->d_Moff.p, P->Mc.p, P->loc.p, P->locy.p, done);
-        count_launch();
+        enqueue_block_inverse(ctx, P, done);
         yloc = P->locy.p;
     } else {
         for (int k = 0; k < P->Tmax; ++k) {
@@ -1366,9 +1463,7 @@ bool prec_apply_pcg(Ctx* ctx, Prec* P, const PcgFused& f)
                (const double*)f.r, f.rn, f.p, f.Wp, n, (const int*)P->pos.p, P->loc.p, (const int*)P->Rc_ptr.p,
                (const int*)P->Rc_row.p, (const double*)P->Rc_val.p, P->nc, loc_c, dof_blocks);
     count_launch();
-    launch_pdl(k_block_gemv, dim3((unsigned)P->sched->gemv.size()), dim3(256), 0, s, P->sched->d_gemv.p,
-               P->d_nb.p, P->d_ldm.p, P->d_loc.p, P->d_Moff.p, P->Mc.p, P->loc.p, P->locy.p, f.done);
-    count_launch();
+    enqueue_block_inverse(ctx, P, f.done);
     launch_pdl(k_prec_scatter_rz, dim3(dof_blocks), dim3(256), 0, s, f.st, (const double*)P->locy.p,
                (const int*)P->pos.p, n, (const int*)(P->nc > 0 ? P->Rr_ptr.p : nullptr), (const int*)P->Rr_col.p,
                (const double*)P->Rr_val.p, (const double*)(cb >= 0 ? P->locy.p + P->h_loc[cb] : nullptr), f.z, f.r,
@@ -1395,7 +1490,15 @@ void prec_block_diag(Ctx* ctx, Prec* P, int which, std::vector<double>& diag)
         const int ldm = P->h_ldm[b];
         std::vector<double> h((size_t)nb * ldm);
         SBG_CUDA(cudaMemcpy(h.data(), P->Mc.p + P->h_Moff[b], h.size() * sizeof(double), cudaMemcpyDeviceToHost));
-        for (int i = 0; i < nb; ++i) diag.push_back(h[(size_t)i * ldm + i]);
+        for (int i = 0; i < nb; ++i) {
+            if (!P->factored) {
+                diag.push_back(h[(size_t)i * ldm + i]);
+                continue;
+            }
+            double d = 0.0;  // (X^T X)_ii = sum_{q >= i} X_qi^2, row i above the diagonal holds X_qi
+            for (int c = i; c < nb; ++c) d += h[(size_t)i * ldm + c] * h[(size_t)i * ldm + c];
+            diag.push_back(d);
+        }
     } else {
         const size_t ld = (size_t)P->h_T[b] * TB;
         std::vector<double> h(ld * ld);
@@ -1458,6 +1561,13 @@ void prec_materialize(Ctx* ctx, Prec* P, DMatrix& M)
         work.alloc(P->Lp.n);
         SBG_CUDA(cudaMemcpyAsync(work.p, P->Lp.p, P->Lp.n * sizeof(double), cudaMemcpyDeviceToDevice, s));
         form_inverses(ctx, P, work, Mtmp);
+        Mc = &Mtmp;
+    } else if (P->factored) {  // full inverses X^T X from the factored storage
+        Mtmp.alloc(P->Mc.n);
+        for (int b = 0; b < P->nblocks; ++b) {
+            k_factored_to_full<<<4 * ctx->sm_count, 256, 0, s>>>(P->d_nb.p, P->d_ldm.p, P->d_Moff.p, P->Mc.p, Mtmp.p, b);
+            count_launch();
+        }
         Mc = &Mtmp;
     }
     if (P->ngather > 0) {

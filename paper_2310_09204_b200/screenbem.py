@@ -713,9 +713,11 @@ class SchwarzPreconditioner(_Handle):
 def build_preconditioner(W: GalerkinMatrix, part: DofPartition, P: Prolongation,
                          mode: str = "inverse") -> SchwarzPreconditioner:
     """reference: inc/schwarz.hpp:100-118.  mode "inverse" (default) forms the block
-    inverses L^-T L^-1 once and applies one batched GEMV; "trsv" applies the blocked
-    triangular solves with L as llt.solve does (schwarz.hpp:130)."""
-    modes = {"trsv": 0, "inverse": 1}
+    inverses L^-T L^-1 once and applies one batched GEMV (for a largest block above 2048
+    DOFs it keeps X = L^-1 and applies X^T (X r), two triangular GEMVs over the same bytes);
+    "factored" forces that form; "trsv" applies the blocked triangular solves with L as
+    llt.solve does (schwarz.hpp:130)."""
+    modes = {"trsv": 0, "inverse": 1, "factored": 2}
     if mode not in modes:
         raise ValidationError(f"unknown preconditioner mode {mode!r}")
     h = vp()

@@ -37,7 +37,7 @@ def bowtie_level():
     return pair, fine, coarse, opair, ofine, ocoarse
 
 
-@pytest.mark.parametrize("mode", ["inverse", "trsv"])
+@pytest.mark.parametrize("mode", ["inverse", "trsv", "factored"])
 @pytest.mark.parametrize("which", ["cfg1", "bowtie"])
 def test_materialize_matches_oracle(ctx, mode, which):
     pair, fine, coarse, opair, ofine, ocoarse = level(1) if which == "cfg1" else bowtie_level()

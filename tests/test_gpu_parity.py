@@ -137,7 +137,7 @@ def setup_pair(pair):
     return fine, coarse, opair, ofine, ocoarse
 
 
-@pytest.mark.parametrize("mode", ["inverse", "trsv"])
+@pytest.mark.parametrize("mode", ["inverse", "trsv", "factored"])
 @pytest.mark.parametrize("which", ["cfg1", "bowtie-0-2", "tjunction-12-4", "flat-32-8"])
 def test_preconditioner_apply_matches_oracle(ctx, which, mode):
     pair = {"cfg1": lambda: S.make_config(1),
@@ -166,7 +166,7 @@ def test_preconditioner_apply_matches_oracle(ctx, which, mode):
         np.testing.assert_allclose(prec.block_diag(-1), oprec.block_diag(-1), rtol=1e-12)
 
 
-@pytest.mark.parametrize("mode", ["inverse", "trsv"])
+@pytest.mark.parametrize("mode", ["inverse", "trsv", "factored"])
 def test_preconditioner_large_blocks_multi_tile(ctx, mode):
     # wire-basket and face blocks spanning several 64x64 tiles (blocked Cholesky + TRSV / inverse)
     W0 = O.random_spd(300, 21)
@@ -181,7 +181,7 @@ def test_preconditioner_large_blocks_multi_tile(ctx, mode):
     assert np.abs(z - zo).max() <= 1e-11 * np.abs(zo).max()
 
 
-@pytest.mark.parametrize("mode", ["inverse", "trsv"])
+@pytest.mark.parametrize("mode", ["inverse", "trsv", "factored"])
 def test_preconditioner_blocks_beyond_one_panel(ctx, mode):
     """A 1100-DOF wire-basket block = 18 tiles: two panels of 8 tile columns complete, so the
     panel-end trailing updates (near part on the main stream, far part on the look-ahead
@@ -218,7 +218,7 @@ def test_identity_pair_M_is_twice_Winv(ctx):
     assert np.abs(M - expect).max() < 1e-8 * np.abs(expect).max()
 
 
-@pytest.mark.parametrize("mode", ["inverse", "trsv"])
+@pytest.mark.parametrize("mode", ["inverse", "trsv", "factored"])
 def test_non_spd_block_raises(ctx, mode):
     W0 = O.random_spd(40, 5)
     W0[3, 3] = -50.0
