@@ -31,16 +31,61 @@ struct DSU {
 };
 }  // namespace
 
+// contiguous ranges of [0, count) on up to 16 host threads (the calling thread included);
+// body(lo, hi, slot)
+template <class F>
+static int parallel_ranges(int count, int min_chunk, const F& body)
+{
+    const unsigned hw = std::thread::hardware_concurrency() ? std::thread::hardware_concurrency() : 1u;
+    const int nt = std::max(1, std::min({(int)std::min(16u, hw), count / std::max(min_chunk, 1), 64}));
+    std::vector<std::thread> pool;
+    for (int t = 1; t < nt; ++t)
+        pool.emplace_back([&, t] { body((int)((long long)count * t / nt), (int)((long long)count * (t + 1) / nt), t); });
+    body(0, (int)((long long)count / nt), 0);
+    for (auto& th : pool) th.join();
+    return nt;
+}
+
 // reference: inc/inflate.hpp:98-288.  The edge->facets map is a sorted edge
 // list (same lexicographic order as the reference's std::map), and the
 // point-contact test visits only the edges incident to each vertex (the
 // reference scans every edge for every vertex, O(V*E)); outputs are identical.
+// validate_mesh runs on a helper thread beside the inflation (after a sequential check of
+// the vertex ids, the one thing the inflation itself relies on); the per-vertex and per-edge
+// phases run on host threads.  Errors are raised in the reference's order: validation first,
+// then the first point contact, the first angular tie, the first isolated vertex.
 InflatedMesh inflate(const SurfaceMesh& mesh, bool validate)
 {
-    if (validate) validate_mesh(mesh);
+    const int nf = mesh.num_facets(), nv = mesh.num_vertices();
+    std::thread vthread;
+    std::exception_ptr verr;
+    if (validate) {
+        bool ids_ok = true;
+        for (int f = 0; f < nf && ids_ok; ++f)
+            for (int k = 0; k < 3; ++k)
+                if (mesh.facets[f][k] < 0 || mesh.facets[f][k] >= nv) ids_ok = false;
+        if (!ids_ok) validate_mesh(mesh);  // throws the reference's first error
+        vthread = std::thread([&] {
+            try {
+                validate_mesh(mesh);
+            } catch (...) {
+                verr = std::current_exception();
+            }
+        });
+    }
+    struct Joiner {
+        std::thread& t;
+        ~Joiner()
+        {
+            if (t.joinable()) t.join();
+        }
+    } joiner{vthread};
+    auto raise_validation = [&] {
+        if (vthread.joinable()) vthread.join();
+        if (verr) std::rethrow_exception(verr);
+    };
     InflatedMesh im;
     im.base = mesh;
-    const int nf = mesh.num_facets(), nv = mesh.num_vertices();
     im.onormal.resize(2 * nf);
     for (int f = 0; f < nf; ++f) {
         const Vec3 n = mesh.facet_normal(f);
@@ -91,124 +136,182 @@ InflatedMesh inflate(const SurfaceMesh& mesh, bool validate)
         for (int f = 0; f < nf; ++f)
             for (int k = 0; k < 3; ++k) vstar[fill[mesh.facets[f][k]]++] = f;
     }
-    DSU ds;
+    constexpr int kSlots = 64;
+    auto first_of = [](const std::vector<int>& v) { return *std::min_element(v.begin(), v.end()); };
 
-    // point-contact check (inflate.hpp:129-151)
-    for (int v = 0; v < nv; ++v) {
-        const int* star = vstar.data() + vs_ptr[v];
-        const int ns = vs_ptr[v + 1] - vs_ptr[v];
-        if (ns < 2) continue;
-        auto local = [&](int f) { return (int)(std::lower_bound(star, star + ns, f) - star); };
-        ds.reset(ns);
-        for (int q = ve_ptr[v]; q < ve_ptr[v + 1]; ++q) {
-            const int e = vedges[q];
-            for (int i = eptr[e] + 1; i < eptr[e + 1]; ++i) ds.unite(local(el[eptr[e]].f), local(el[i].f));
+    // point-contact check (inflate.hpp:129-151): the first vertex whose star splits
+    std::vector<int> contact(kSlots, nv);
+    parallel_ranges(nv, 1024, [&](int lo, int hi, int slot) {
+        DSU ds;
+        for (int v = lo; v < hi; ++v) {
+            const int* star = vstar.data() + vs_ptr[v];
+            const int ns = vs_ptr[v + 1] - vs_ptr[v];
+            if (ns < 2) continue;
+            auto local = [&](int f) { return (int)(std::lower_bound(star, star + ns, f) - star); };
+            ds.reset(ns);
+            for (int q = ve_ptr[v]; q < ve_ptr[v + 1]; ++q) {
+                const int e = vedges[q];
+                for (int i = eptr[e] + 1; i < eptr[e + 1]; ++i) ds.unite(local(el[eptr[e]].f), local(el[i].f));
+            }
+            const int root = ds.find(0);
+            for (int i = 1; i < ns; ++i)
+                if (ds.find(i) != root) {
+                    contact[slot] = v;
+                    return;
+                }
         }
-        const int root = ds.find(0);
-        for (int i = 1; i < ns; ++i)
-            if (ds.find(i) != root)
-                throw ValidationError("point contact at vertex " + std::to_string(v) + " (unsupported geometry)");
+    });
+    {
+        const int v = first_of(contact);
+        if (v < nv) {
+            raise_validation();
+            throw ValidationError("point contact at vertex " + std::to_string(v) + " (unsupported geometry)");
+        }
     }
 
-    // fans (inflate.hpp:155-228)
-    std::vector<std::array<int, 2>> fan_pairs;
-    std::vector<int> fan_ptr{0};
-    fan_pairs.reserve(el.size());
-    fan_ptr.reserve(ne + 1);
-    std::vector<std::pair<double, int>> slots;  // (angle, local)
-    for (int e = 0; e < ne; ++e) {
-        const int ea = el[eptr[e]].a, eb = el[eptr[e]].b;
-        const Vec3 origin = mesh.vertices[ea];
-        const Vec3 e_dir = normalized(mesh.vertices[eb] - mesh.vertices[ea]);
-        auto in_plane_dir = [&](int f) {
-            const auto& t = mesh.facets[f];
-            int opp = -1;
-            for (int k = 0; k < 3; ++k)
-                if (t[k] != ea && t[k] != eb) opp = t[k];
-            Vec3 d = mesh.vertices[opp] - origin;
-            d = d - dot(d, e_dir) * e_dir;
-            return normalized(d);
-        };
-        const int k = eptr[e + 1] - eptr[e];
-        const Vec3 ref = in_plane_dir(el[eptr[e]].f);
-        const Vec3 up = cross(e_dir, ref);
-        slots.clear();
-        for (int i = 0; i < k; ++i) {
-            const Vec3 d = in_plane_dir(el[eptr[e] + i].f);
-            slots.push_back({std::atan2(dot(d, up), dot(d, ref)), i});
+    // fans (inflate.hpp:155-228): edge e's k facets give k pairs at fan_pairs[eptr[e]...]
+    std::vector<std::array<int, 2>> fan_pairs(el.size());
+    const std::vector<int>& fan_ptr = eptr;
+    std::vector<int> tie(kSlots, ne);
+    parallel_ranges(ne, 2048, [&](int lo, int hi, int slot) {
+        std::vector<std::pair<double, int>> slots;  // (angle, local)
+        for (int e = lo; e < hi; ++e) {
+            const int ea = el[eptr[e]].a, eb = el[eptr[e]].b;
+            const Vec3 origin = mesh.vertices[ea];
+            const Vec3 e_dir = normalized(mesh.vertices[eb] - mesh.vertices[ea]);
+            auto in_plane_dir = [&](int f) {
+                const auto& t = mesh.facets[f];
+                int opp = -1;
+                for (int k = 0; k < 3; ++k)
+                    if (t[k] != ea && t[k] != eb) opp = t[k];
+                Vec3 d = mesh.vertices[opp] - origin;
+                d = d - dot(d, e_dir) * e_dir;
+                return normalized(d);
+            };
+            const int k = eptr[e + 1] - eptr[e];
+            const Vec3 ref = in_plane_dir(el[eptr[e]].f);
+            const Vec3 up = cross(e_dir, ref);
+            slots.clear();
+            for (int i = 0; i < k; ++i) {
+                const Vec3 d = in_plane_dir(el[eptr[e] + i].f);
+                slots.push_back({std::atan2(dot(d, up), dot(d, ref)), i});
+            }
+            std::sort(slots.begin(), slots.end(),
+                      [](const auto& x, const auto& y) { return x.first < y.first; });
+            bool bad = false;
+            for (int i = 0; i + 1 < k; ++i)
+                if (slots[i + 1].first - slots[i].first < 1e-9) bad = true;
+            if (k > 1 && slots[0].first + 2.0 * M_PI - slots[k - 1].first < 1e-9) bad = true;
+            if (bad) {
+                tie[slot] = e;
+                return;
+            }
+            auto ccw_side = [&](int f) {
+                const Vec3 tangent = cross(e_dir, in_plane_dir(f));
+                return dot(im.onormal[2 * f], tangent) > 0 ? 0 : 1;
+            };
+            for (int i = 0; i < k; ++i) {
+                const int fa = el[eptr[e] + slots[i].second].f;
+                const int fb = el[eptr[e] + slots[(i + 1) % k].second].f;
+                fan_pairs[eptr[e] + i] = {2 * fa + (1 - ccw_side(fa)), 2 * fb + ccw_side(fb)};
+            }
         }
-        std::sort(slots.begin(), slots.end(),
-                  [](const auto& x, const auto& y) { return x.first < y.first; });
-        for (int i = 0; i + 1 < k; ++i)
-            if (slots[i + 1].first - slots[i].first < 1e-9)
-                throw ValidationError("coplanar facets overlap at an edge fan (angular tie)");
-        if (k > 1 && slots[0].first + 2.0 * M_PI - slots[k - 1].first < 1e-9)
-            throw ValidationError("coplanar facets overlap at an edge fan (angular tie)");
-        auto ccw_side = [&](int f) {
-            const Vec3 tangent = cross(e_dir, in_plane_dir(f));
-            return dot(im.onormal[2 * f], tangent) > 0 ? 0 : 1;
-        };
-        for (int i = 0; i < k; ++i) {
-            const int fa = el[eptr[e] + slots[i].second].f;
-            const int fb = el[eptr[e] + slots[(i + 1) % k].second].f;
-            fan_pairs.push_back({2 * fa + (1 - ccw_side(fa)), 2 * fb + ccw_side(fb)});
-        }
-        fan_ptr.push_back((int)fan_pairs.size());
+    });
+    if (first_of(tie) < ne) {
+        raise_validation();
+        throw ValidationError("coplanar facets overlap at an edge fan (angular tie)");
     }
 
-    // branches (inflate.hpp:232-279)
-    im.q.assign(nv, 0);
+    // branches (inflate.hpp:232-279): per vertex the branch of every oriented facet of its
+    // star (bid, at 2 vs_ptr[v] + i) and the branch count, then the numbering in vertex order
+    std::vector<int> bidv(2 * (size_t)vs_ptr[nv]), nbv(nv, 0);
+    std::vector<int> isolated(kSlots, nv);
+    parallel_ranges(nv, 1024, [&](int lo, int hi, int slot) {
+        DSU ds;
+        std::vector<int> star, broot;
+        for (int v = lo; v < hi; ++v) {
+            const int ns = vs_ptr[v + 1] - vs_ptr[v];
+            if (ns == 0) {
+                isolated[slot] = v;
+                return;
+            }
+            star.clear();  // oriented facets, ascending
+            for (int q = vs_ptr[v]; q < vs_ptr[v + 1]; ++q) {
+                star.push_back(2 * vstar[q]);
+                star.push_back(2 * vstar[q] + 1);
+            }
+            const int m = (int)star.size();
+            auto local = [&](int o) { return (int)(std::lower_bound(star.begin(), star.end(), o) - star.begin()); };
+            ds.reset(m);
+            for (int q = ve_ptr[v]; q < ve_ptr[v + 1]; ++q) {
+                const int e = vedges[q];
+                for (int p = fan_ptr[e]; p < fan_ptr[e + 1]; ++p)
+                    ds.unite(local(fan_pairs[p][0]), local(fan_pairs[p][1]));
+            }
+            // branches ordered by their smallest oriented facet = order of first appearance
+            broot.assign(m, -1);
+            int nb = 0;
+            int* bid = bidv.data() + 2 * (size_t)vs_ptr[v];
+            for (int i = 0; i < m; ++i) {
+                const int r = ds.find(i);
+                if (broot[r] < 0) broot[r] = nb++;
+                bid[i] = broot[r];
+            }
+            nbv[v] = nb;
+        }
+    });
+    if (first_of(isolated) < nv) {
+        raise_validation();
+        throw ValidationError("isolated vertex " + std::to_string(first_of(isolated)));
+    }
+    im.q = nbv;
     im.gv_first.assign(nv, -1);
     im.dof_first.assign(nv, -1);
     im.ofacet_branch.assign(2 * nf, {-1, -1, -1});
-    im.gv_alpha_ptr.push_back(0);
-    std::vector<int> star, broot, bid, order;
-    im.gv_alpha.reserve(2 * (size_t)vs_ptr[nv]);
+    int ngv = 0;
     for (int v = 0; v < nv; ++v) {
-        const int ns = vs_ptr[v + 1] - vs_ptr[v];
-        if (ns == 0) throw ValidationError("isolated vertex " + std::to_string(v));
-        star.clear();  // oriented facets, ascending
-        for (int q = vs_ptr[v]; q < vs_ptr[v + 1]; ++q) {
-            star.push_back(2 * vstar[q]);
-            star.push_back(2 * vstar[q] + 1);
-        }
-        const int m = (int)star.size();
-        auto local = [&](int o) { return (int)(std::lower_bound(star.begin(), star.end(), o) - star.begin()); };
-        ds.reset(m);
-        for (int q = ve_ptr[v]; q < ve_ptr[v + 1]; ++q) {
-            const int e = vedges[q];
-            for (int p = fan_ptr[e]; p < fan_ptr[e + 1]; ++p) ds.unite(local(fan_pairs[p][0]), local(fan_pairs[p][1]));
-        }
-        // branches ordered by their smallest oriented facet = order of first appearance
-        broot.assign(m, -1);
-        bid.assign(m, 0);
-        int nb = 0;
-        for (int i = 0; i < m; ++i) {
-            const int r = ds.find(i);
-            if (broot[r] < 0) broot[r] = nb++;
-            bid[i] = broot[r];
-        }
-        im.gv_first[v] = im.num_gvertices();
-        im.q[v] = nb;
-        for (int j = 0; j < nb; ++j) {
-            im.gv_vertex.push_back(v);
-            im.gv_branch.push_back(j);
-            for (int i = 0; i < m; ++i) {
-                if (bid[i] != j) continue;
-                const int o = star[i];
-                im.gv_alpha.push_back(o);
-                const int f = o / 2;
-                for (int k = 0; k < 3; ++k)
-                    if (mesh.facets[f][k] == v) im.ofacet_branch[o][k] = j;
-            }
-            im.gv_alpha_ptr.push_back((int)im.gv_alpha.size());
-        }
+        im.gv_first[v] = ngv;
+        ngv += nbv[v];
     }
+    im.gv_vertex.resize(ngv);
+    im.gv_branch.resize(ngv);
+    im.gv_alpha_ptr.assign(ngv + 1, 0);
+    // a vertex's sectors hold all 2 ns oriented facets of its star, split among its branches
+    for (int v = 0; v < nv; ++v)
+        for (int j = 0; j < nbv[v]; ++j) {
+            const int* bid = bidv.data() + 2 * (size_t)vs_ptr[v];
+            int cnt = 0;
+            for (int i = 0; i < 2 * (vs_ptr[v + 1] - vs_ptr[v]); ++i) cnt += bid[i] == j;
+            im.gv_alpha_ptr[im.gv_first[v] + j + 1] = cnt;
+        }
+    for (int g = 0; g < ngv; ++g) im.gv_alpha_ptr[g + 1] += im.gv_alpha_ptr[g];
+    im.gv_alpha.resize(im.gv_alpha_ptr[ngv]);
+    parallel_ranges(nv, 1024, [&](int lo, int hi, int) {
+        for (int v = lo; v < hi; ++v) {
+            const int* bid = bidv.data() + 2 * (size_t)vs_ptr[v];
+            const int m = 2 * (vs_ptr[v + 1] - vs_ptr[v]);
+            for (int j = 0; j < nbv[v]; ++j) {
+                const int g = im.gv_first[v] + j;
+                im.gv_vertex[g] = v;
+                im.gv_branch[g] = j;
+                int w = im.gv_alpha_ptr[g];
+                for (int i = 0; i < m; ++i) {
+                    if (bid[i] != j) continue;
+                    const int o = 2 * vstar[vs_ptr[v] + i / 2] + (i & 1);
+                    im.gv_alpha[w++] = o;
+                    const int f = o / 2;
+                    for (int k = 0; k < 3; ++k)
+                        if (mesh.facets[f][k] == v) im.ofacet_branch[o][k] = j;
+                }
+            }
+        }
+    });
     for (int v = 0; v < nv; ++v) {  // inflate.hpp:281-285
         if (im.q[v] < 2) continue;
         im.dof_first[v] = im.num_jump_dofs();
         for (int j = 0; j + 1 < im.q[v]; ++j) im.jump_dofs.push_back({v, j});
     }
+    raise_validation();
     return im;
 }
 
