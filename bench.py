@@ -132,6 +132,11 @@ class NvmlSampler:
         self.stop.set()
         if self.t:
             self.t.join(timeout=2)
+            try:
+                import pynvml as N
+                N.nvmlShutdown()
+            except Exception:
+                pass
 
     def summary(self):
         if not self.rows:
@@ -454,13 +459,20 @@ def run_ours(args):
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
         ev[0].record()  # legacy stream; the context stream is a blocking stream
         W = plan.run(W, shard=(rank, world))
-        allreduce_(torch.as_tensor(W, device=f"cuda:{local}"))
+        # W is symmetric: only its upper triangle (n (n + 1) / 2 doubles, half of W) is summed
+        if "packed" not in packed_buf:
+            packed_buf["packed"] = torch.empty(n * (n + 1) // 2, dtype=torch.float64, device=f"cuda:{local}")
+        packed = packed_buf["packed"]
+        W.pack_upper(packed.data_ptr())
+        allreduce_(packed)
+        W.unpack_upper(packed.data_ptr())
         ev[1].record()
         ev[1].synchronize()
         shard_ms.append(ev[0].elapsed_time(ev[1]))
         return W
 
     shard_ms = []
+    packed_buf = {}
 
     # --shard: the PCG runs by row panels — this rank's rows of each W p, then
     # one all-gather of W p per iteration over NCCL on the PCG stream
@@ -588,7 +600,7 @@ def run_ours(args):
         ctx.synchronize()
         e2e_times.append(ctx.timer("e2e")[0] * 1e-3)
         e2e_parts.append({k: round(ctx.timer(k)[0], 1) for k in ("assemble_W", "far_tiles", "near_leaves", "band_patch",
-                                                                  "plan_total")})
+                                                                  "w_copy", "plan_total")})
         del W2
     del Wbuf
     runs = sorted(e2e_times[1:] if len(e2e_times) > 1 else e2e_times)
@@ -646,7 +658,8 @@ def run_ours(args):
             "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "strong" if shard else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": config_dict(cfg, ratio, nf, n),
-            "parallelism": (f"assembly sharded x{world} (NCCL all-reduce of W), preconditioner replicated, PCG by "
+            "parallelism": (f"assembly sharded x{world} (NCCL all-reduce of W's packed upper triangle), preconditioner "
+                            f"replicated, PCG by "
                             f"row panels (NCCL all-gather of W p per iteration)") if shard
             else (f"replicas x{world}" if world > 1 else "single GPU"),
             "l2": "flushed (256 MiB write + 256 MiB read: cold L2 with clean lines) before every timed step and "

@@ -150,6 +150,12 @@ int sbg_matrix_create(sbg_ctx* ctx, int n, const double* host_rowmajor, sbg_matr
 int sbg_matrix_n(const sbg_matrix* W);
 /* device storage of W: row-major n x ld doubles (ld >= n, padding zero), count = n * ld */
 int sbg_matrix_device_view(const sbg_matrix* W, void** data, int* ld, long long* count);
+/* the upper triangle of the symmetric W as one contiguous device vector of n (n + 1) / 2
+ * doubles (row i at i n - i (i - 1) / 2, columns i..n-1), and back (writing both triangles):
+ * a multi-GPU reduction of the shards' W moves half the bytes.  Enqueued on W's context
+ * stream, no synchronisation. */
+int sbg_matrix_pack_upper(const sbg_matrix* W, double* d_packed);
+int sbg_matrix_unpack_upper(sbg_matrix* W, const double* d_packed);
 int sbg_matrix_download(const sbg_matrix* W, double* host_rowmajor);
 int sbg_matrix_download_rows(const sbg_matrix* W, const int32_t* rows, int nrows, double* host);
 int sbg_matrix_symmetry_defect(const sbg_matrix* W, double* max_abs);

@@ -84,6 +84,7 @@ def lib():
             "orc_build_prolongation": (vp, [vp, vp, vp, C.POINTER(C.c_int)]),
             "orc_empty_prolongation": (vp, [C.c_int]),
             "orc_identity_prolongation": (vp, [C.c_int]),
+            "orc_prolongation_from": (vp, [C.c_int, C.c_int, i32p, i32p, f64p]),
             "orc_prolongation_free": (None, [vp]),
             "orc_prolongation_sizes": (C.c_int, [vp, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int)]),
             "orc_prolongation_export": (C.c_int, [vp, i32p, i32p, f64p]),
@@ -433,6 +434,13 @@ def build_prolongation(pair: LevelPair, coarse: InflatedMesh, fine: InflatedMesh
 
 def empty_prolongation(rows: int) -> Prolongation:
     return Prolongation(lib().orc_empty_prolongation(rows))
+
+
+def prolongation_from(rows: int, cols: int, col_ptr, row_idx, val) -> Prolongation:
+    """a given sparse R in CSC form (jump.hpp:87-89 layout)"""
+    return Prolongation(lib().orc_prolongation_from(rows, cols, np.ascontiguousarray(col_ptr, dtype=np.int32),
+                                                    np.ascontiguousarray(row_idx, dtype=np.int32),
+                                                    np.ascontiguousarray(val, dtype=np.float64)))
 
 
 def identity_prolongation(n: int) -> Prolongation:

@@ -358,6 +358,16 @@ void* orc_empty_prolongation(int rows)
     P->col_ptr = {0};
     return P;
 }
+void* orc_prolongation_from(int rows, int cols, const int* col_ptr, const int* row_idx, const double* val)
+{
+    auto* P = new Prolongation;
+    P->rows = rows;
+    P->cols = cols;
+    P->col_ptr.assign(col_ptr, col_ptr + cols + 1);
+    P->row_idx.assign(row_idx, row_idx + col_ptr[cols]);
+    P->val.assign(val, val + col_ptr[cols]);
+    return P;
+}
 void* orc_identity_prolongation(int n)
 {
     auto* P = new Prolongation;

@@ -579,6 +579,22 @@ int sbg_matrix_device_view(const sbg_matrix* W, void** data, int* ld, long long*
         if (count) *count = (long long)W->M.a.n;
     });
 }
+int sbg_matrix_pack_upper(const sbg_matrix* W, double* d_packed)
+{
+    return guard([&] {
+        bind_mat(W);
+        need(d_packed, "d_packed");
+        matrix_pack_upper(W->M, d_packed);
+    });
+}
+int sbg_matrix_unpack_upper(sbg_matrix* W, const double* d_packed)
+{
+    return guard([&] {
+        bind_mat(W);
+        need(d_packed, "d_packed");
+        matrix_unpack_upper(W->M, d_packed);
+    });
+}
 int sbg_matrix_download(const sbg_matrix* W, double* host)
 {
     return guard([&] {

@@ -26,6 +26,9 @@
 #include <numeric>
 #include <stdexcept>
 #include <string>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 
 #include "kernels.cuh"
 
@@ -1832,16 +1835,52 @@ void assembly_plan_destroy(AssemblyPlan* P) { delete P; }
 // zeroed W: far tiles k with k % world == rank, the near pairs it owns
 // (near_owner), and a contiguous 1/world range of each singular class.  The shards' W sum to the
 // full W (up to fp64 atomic reordering); DESIGN.md §5.3.
+namespace {
+// SBG_TRACE_ASM=1: host-side timeline of one assembly (stderr), for diagnosing host stalls
+struct HostTrace {
+    bool on = std::getenv("SBG_TRACE_ASM") != nullptr;
+    std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+    std::string line;
+    void mark(const char* what)
+    {
+        if (!on) return;
+        const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        char b[64];
+        std::snprintf(b, sizeof b, " %s=%.1f", what, ms);
+        line += b;
+    }
+    ~HostTrace()
+    {
+        if (on) std::fprintf(stderr, "[asm trace]%s\n", line.c_str());
+    }
+};
+}  // namespace
+
 void assembly_run(AssemblyPlan* P, DMatrix& W, AssemblyStats* stats, int rank, int world, double* host_dst)
 {
+    HostTrace tr;
     if (world < 1 || rank < 0 || rank >= world) throw ValidationError("shard: need 0 <= rank < world");
     Ctx* ctx = P->ctx;
     cudaStream_t s = ctx->stream;
     TimedScope total(ctx, "assemble_W");
+    if (tr.on) {
+        cudaMemPool_t pool;
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetDefaultMemPool(&pool, dev);
+        unsigned long long res = 0, used = 0;
+        cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &res);
+        cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used);
+        char b[96];
+        std::snprintf(b, sizeof b, " pool_res=%.2fG pool_used=%.2fG", res / 1e9, used / 1e9);
+        tr.line += b;
+    }
     if (W.n != P->n || !W.a.p) matrix_alloc(ctx, P->n, W);
     else SBG_CUDA(cudaMemsetAsync(W.a.p, 0, W.a.n * sizeof(double), s));
+    tr.mark("alloc");
     if (P->nf == 0 || P->n == 0) return;
     const RuleDims R = upload_rules(ctx, P->cfg);
+    tr.mark("rules");
     const double thr = P->cfg.near_threshold;
     auto share = [&](long long cnt) { return cnt > rank ? (cnt - rank + world - 1) / world : 0LL; };
     // far tiles are strided over the ranks; every rank classifies all candidate tiles (cheap)
@@ -1857,6 +1896,7 @@ void assembly_run(AssemblyPlan* P, DMatrix& W, AssemblyStats* stats, int rank, i
     // near list or near frontier that outgrew its buffers (first run of a mesh size on this
     // context) is regrown to the measured size and the assembly runs again.
     NearWork& NW = near_work(ctx);
+    tr.mark("nearwork");
     unsigned long long* hnear = near_host_counters(NW) + kNearCnt;
     NearResult nr;
     // host_dst (page-locked, n x n row-major): W is also copied to the host, overlapped with
@@ -1902,6 +1942,7 @@ void assembly_run(AssemblyPlan* P, DMatrix& W, AssemblyStats* stats, int rank, i
         SBG_CUDA(cudaMemsetAsync(P->near_cnt.p, 0, sizeof(unsigned long long), s));
         SBG_CUDA(cudaMemsetAsync(P->bad.p, 0, sizeof(int), s));
         if (to_host) SBG_CUDA(cudaMemsetAsync(P->band.p, 0, sizeof(int), s));
+        tr.mark("memsets");
         if (my_cand) {  // near list: classification of the non-certainly-far tiles
             TimedScope ts(ctx, "classify");
             k_classify_near<<<(int)my_cand, 256, 0, s>>>(P->cand.p, 1, P->G.ptrs(), P->bfac.p, thr,
@@ -1909,19 +1950,34 @@ void assembly_run(AssemblyPlan* P, DMatrix& W, AssemblyStats* stats, int rank, i
             count_launch();
             SBG_LAUNCH_CHECK();
         }
+        tr.mark("classify");
         run_near(ctx, R, P->G.v.p, P->G.area.p, P->loc_pairs.p + P->nsing, P->near_cnt.p, P->near_cap, thr,
                  P->loc_I.p + P->nsing, NW, rank, world, /*leaves_now=*/!to_host);
+        tr.mark("near");
         // a deferred plan builds its curl-dependent half while the near field runs
         plan_finish(P);
+        tr.mark("plan_finish");
         if (to_host) {
             enqueue_far();
             enqueue_mirror();
             SBG_CUDA(cudaEventRecord(ev_far, s));
             SBG_CUDA(cudaStreamWaitEvent(cs, ev_far, 0));
+            cudaEvent_t ta = nullptr;
+            if (ctx->timers.enabled) {  // "w_copy": the overlapped copy on the second stream
+                ta = ctx->timers.get();
+                SBG_CUDA(cudaEventRecord(ta, cs));
+            }
             SBG_CUDA(cudaMemcpy2DAsync(host_dst, sizeof(double) * (size_t)P->n, W.a.p, sizeof(double) * (size_t)W.ld,
                                        sizeof(double) * (size_t)P->n, P->n, cudaMemcpyDeviceToHost, cs));
+            if (ta) {
+                cudaEvent_t tb = ctx->timers.get();
+                SBG_CUDA(cudaEventRecord(tb, cs));
+                ctx->timers.pending.push_back({"w_copy", ta, tb});
+            }
             SBG_CUDA(cudaEventRecord(ev_copy, cs));
+            tr.mark("far_copy");
             run_near_leaves(ctx, R, P->G.v.p, P->G.area.p, P->loc_pairs.p + P->nsing, P->loc_I.p + P->nsing, NW);
+            tr.mark("leaves");
         }
         // singular pairs (Sauter rules); a shard zeroes the integrals it does not own
         if (world > 1 && P->nsing) SBG_CUDA(cudaMemsetAsync(P->loc_I.p, 0, P->nsing * sizeof(double), s));
@@ -1956,7 +2012,9 @@ void assembly_run(AssemblyPlan* P, DMatrix& W, AssemblyStats* stats, int rank, i
         if (to_host)
             SBG_CUDA(cudaMemcpyAsync(reinterpret_cast<int*>(hnear + 1) + 1, P->band.p, sizeof(int),
                                      cudaMemcpyDeviceToHost, s));
+        tr.mark("enqueued");
         SBG_CUDA(cudaStreamSynchronize(s));
+        tr.mark("sync");
         nr = near_results(NW);
         const bool list_over = (long long)hnear[0] > P->near_cap;
         if (!list_over && !nr.overflow) break;
@@ -1996,7 +2054,9 @@ void assembly_run(AssemblyPlan* P, DMatrix& W, AssemblyStats* stats, int rank, i
         } else {  // a wide band (junction numberings): copy the whole W again
             SBG_CUDA(cudaMemcpy2DAsync(host_dst, es * n, W.a.p, es * W.ld, es * n, n, cudaMemcpyDeviceToHost, s));
         }
+        tr.mark("band_enq");
         SBG_CUDA(cudaStreamSynchronize(s));
+        tr.mark("band_sync");
     }
     if (*reinterpret_cast<const int*>(hnear + 1)) throw NumericalError("quadrature produced a non-finite pair integral");
     const unsigned long long nnear = hnear[0];

@@ -166,12 +166,22 @@ void set_max_dynamic_smem(void (*kernel)(KArgs...), size_t bytes)
 // Row-major with a leading dimension padded to 32 doubles (256-byte rows) so
 // every row starts 16-byte aligned for 128-bit streaming loads; the padding
 // is kept at zero.
+// Parks a large dense buffer being released in a one-slot process-wide spare, so that the
+// next n x n matrix of the same size reuses it instead of having the stream-ordered pool
+// map gigabytes again on the host thread (context.cu).
+void matrix_park(DBuf<double>& a);
+void matrix_spare_release();
+
 struct DMatrix {
     Ctx* ctx = nullptr;
     int n = 0;
     int ld = 0;
     DBuf<double> a;
     static int padded_ld(int n) { return ((n + 31) / 32) * 32; }
+    DMatrix() = default;
+    DMatrix(DMatrix&&) = default;
+    DMatrix& operator=(DMatrix&&) = default;
+    ~DMatrix() { matrix_park(a); }
 };
 
 }  // namespace sbg

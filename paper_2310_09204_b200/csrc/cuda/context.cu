@@ -122,6 +122,7 @@ Timers::~Timers()
 
 Ctx::~Ctx()
 {
+    matrix_spare_release();
     if (aux) {
         cudaStreamSynchronize(aux);
         cudaStreamDestroy(aux);
@@ -188,6 +189,28 @@ __global__ void k_gather_rows(const double* __restrict__ src, int ld, int n, con
         dst[r * n + j] = src[i * ld + j];
 }
 
+// the upper triangle (j >= i) of a symmetric W as one contiguous vector: row i at
+// i n - i (i - 1) / 2, columns i..n-1 (half the bytes of a multi-GPU reduction of W)
+__device__ __forceinline__ size_t upper_off(size_t i, size_t n) { return i * n - i * (i - 1) / 2; }
+__global__ void k_pack_upper(const double* __restrict__ W, int ld, int n, double* __restrict__ out)
+{
+    const size_t i = blockIdx.y;
+    double* row = out + upper_off(i, n) - i;
+    for (int j = (int)i + blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x)
+        row[j] = W[i * ld + j];
+}
+// W(i, j) = W(j, i) = packed(i, j) for j >= i
+__global__ void k_unpack_upper(const double* __restrict__ in, int ld, int n, double* __restrict__ W)
+{
+    const size_t i = blockIdx.y;
+    const double* row = in + upper_off(i, n) - i;
+    for (int j = (int)i + blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+        const double v = row[j];
+        W[i * ld + j] = v;
+        W[(size_t)j * ld + i] = v;
+    }
+}
+
 // max |W(i,j) - W(j,i)| over the upper triangle, per-block maxima
 __global__ void k_symmetry_defect(const double* __restrict__ a, int ld, int n, double* __restrict__ out)
 {
@@ -219,12 +242,64 @@ void set_max_dynamic_smem(const void* kernel, size_t bytes)
     done.insert({kernel, dev, bytes});
 }
 
+namespace {
+constexpr size_t kParkMin = size_t(256) << 20;  // bytes: smaller buffers come from the pool quickly
+struct Spare {
+    std::mutex mu;
+    DBuf<double> buf;
+    int device = -1;
+    cudaEvent_t done = nullptr;  // recorded on the legacy stream when parked
+};
+Spare& spare()
+{
+    static Spare* s = new Spare;  // never destroyed: no CUDA calls during static teardown
+    return *s;
+}
+}  // namespace
+
+void matrix_park(DBuf<double>& a)
+{
+    if (!a.p || a.n * sizeof(double) < kParkMin) return;
+    Spare& S = spare();
+    std::lock_guard<std::mutex> lk(S.mu);
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return;
+    if (!S.done && cudaEventCreateWithFlags(&S.done, cudaEventDisableTiming) != cudaSuccess) {
+        S.done = nullptr;
+        return;
+    }
+    // the legacy stream orders after all earlier work of the (blocking) context streams
+    if (cudaEventRecord(S.done, 0) != cudaSuccess) return;
+    S.buf = std::move(a);  // frees the previous spare, if any
+    S.device = dev;
+}
+
+// a parked buffer of exactly this many elements on this device, or an empty one
+static DBuf<double> matrix_unpark(Ctx* ctx, size_t count)
+{
+    Spare& S = spare();
+    std::lock_guard<std::mutex> lk(S.mu);
+    if (!S.buf.p || S.buf.n != count || S.device != ctx->device) return {};
+    SBG_CUDA(cudaStreamWaitEvent(ctx->stream, S.done, 0));
+    return std::move(S.buf);
+}
+
+void matrix_spare_release()
+{
+    Spare& S = spare();
+    std::lock_guard<std::mutex> lk(S.mu);
+    S.buf.release();
+}
+
 void matrix_alloc(Ctx* ctx, int n, DMatrix& M)
 {
     M.ctx = ctx;
     M.n = n;
     M.ld = DMatrix::padded_ld(n);
-    M.a.alloc((size_t)n * M.ld);
+    const size_t count = (size_t)n * M.ld;
+    DBuf<double> reuse = matrix_unpark(ctx, count);
+    if (reuse.p) M.a = std::move(reuse);
+    else M.a.alloc(count);
     if (M.a.n) SBG_CUDA(cudaMemsetAsync(M.a.p, 0, M.a.n * sizeof(double), ctx->stream));
 }
 
@@ -441,6 +516,21 @@ void matrix_download_rows(const DMatrix& M, const int* rows, int nrows, double* 
     SBG_CUDA(cudaMemcpyAsync(host, out.p, (size_t)nrows * M.n * sizeof(double), cudaMemcpyDeviceToHost,
                              ctx->stream));
     SBG_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+void matrix_pack_upper(const DMatrix& M, double* d_packed)
+{
+    if (M.n == 0) return;
+    k_pack_upper<<<dim3(8, M.n), 256, 0, M.ctx->stream>>>(M.a.p, M.ld, M.n, d_packed);
+    ::sbg::count_launch();
+    SBG_LAUNCH_CHECK();
+}
+void matrix_unpack_upper(DMatrix& M, const double* d_packed)
+{
+    if (M.n == 0) return;
+    k_unpack_upper<<<dim3(8, M.n), 256, 0, M.ctx->stream>>>(d_packed, M.ld, M.n, M.a.p);
+    ::sbg::count_launch();
+    SBG_LAUNCH_CHECK();
 }
 
 double matrix_symmetry_defect(const DMatrix& M)

@@ -49,6 +49,9 @@ cudaStream_t aux_stream(Ctx* ctx);  // the context's second stream (look-ahead o
 
 // ---------------------------------------------------------------- matrices
 void matrix_alloc(Ctx* ctx, int n, DMatrix& M);
+// W's upper triangle <-> a contiguous n (n + 1) / 2 vector (enqueued, no synchronisation)
+void matrix_pack_upper(const DMatrix& M, double* d_packed);
+void matrix_unpack_upper(DMatrix& M, const double* d_packed);
 void matrix_upload(DMatrix& M, const double* host);
 void matrix_download(const DMatrix& M, double* host);
 void matrix_download_rows(const DMatrix& M, const int* rows, int nrows, double* host);

@@ -68,6 +68,8 @@ SIGNATURES = {
     "sbg_assembly_run": (C.c_int, [vp, C.POINTER(vp), C.POINTER(AssemblyStatsC)]),
     "sbg_assembly_run_shard": (C.c_int, [vp, C.POINTER(vp), C.c_int, C.c_int, C.POINTER(AssemblyStatsC)]),
     "sbg_matrix_device_view": (C.c_int, [vp, C.POINTER(vp), C.POINTER(C.c_int), C.POINTER(C.c_longlong)]),
+    "sbg_matrix_pack_upper": (C.c_int, [vp, vp]),
+    "sbg_matrix_unpack_upper": (C.c_int, [vp, vp]),
     "sbg_assembly_plan_destroy": (None, [vp]),
     "sbg_mesh_create": (C.c_int, [C.c_int, f64p, C.c_int, i32p, C.POINTER(vp)]),
     "sbg_mesh_destroy": (None, [vp]),
@@ -477,6 +479,14 @@ class GalerkinMatrix(_Handle):
         _check(lib().sbg_matrix_device_view(self.h, C.byref(p), C.byref(ld), C.byref(cnt)))
         return {"shape": (self.n, ld.value), "typestr": "<f8", "data": (p.value or 0, False), "version": 3,
                 "strides": None, "stream": None}
+
+    def pack_upper(self, d_packed: int):
+        """the upper triangle into the device vector at d_packed (n (n + 1) / 2 doubles)"""
+        _check(lib().sbg_matrix_pack_upper(self.h, d_packed))
+
+    def unpack_upper(self, d_packed: int):
+        """W (both triangles) from a packed upper triangle at d_packed"""
+        _check(lib().sbg_matrix_unpack_upper(self.h, d_packed))
 
     def rows(self, rows):
         rows = np.ascontiguousarray(rows, dtype=np.int32)
