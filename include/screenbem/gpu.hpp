@@ -134,6 +134,8 @@ public:
         *this = Context(p);
     }
     void synchronize() { check(sbg_ctx_synchronize(get())); }
+    // 0 symmetric (default), 1 full matrix (see sbg_ctx_set_matvec_form)
+    void set_matvec_form(int form) { check(sbg_ctx_set_matvec_form(get(), form)); }
 
 private:
     explicit Context(sbg_ctx* p) : Handle(p) {}

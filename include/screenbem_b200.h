@@ -84,6 +84,14 @@ const char* sbg_version(void);
 int sbg_ctx_create(int device, sbg_ctx** out);
 void sbg_ctx_destroy(sbg_ctx* ctx);
 int sbg_ctx_synchronize(sbg_ctx* ctx);
+/* matrix-vector form of sbg_matvec / sbg_pcg / the Lanczos path on this context (no
+ * reference counterpart: the reference's W * p is Eigen's dense product, pcg.hpp:70):
+ *   0 (default) symmetric — W is symmetric by construction (assemble.hpp:136-137), so for
+ *     n >= 2048 only its upper triangle is read, half the bytes;
+ *   1 full-matrix — every entry read; the row kernel shared with sbg_pcg_rows, whose
+ *     results then equal sbg_pcg's bitwise. */
+int sbg_ctx_set_matvec_form(sbg_ctx* ctx, int form);
+int sbg_ctx_get_matvec_form(sbg_ctx* ctx, int* form);
 int sbg_device_name(int device, char* buf, int cap, int* sm_count);
 /* named CUDA-event timers on the context stream */
 int sbg_timers_enable(sbg_ctx* ctx, int on);

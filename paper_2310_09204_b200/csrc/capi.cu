@@ -177,6 +177,22 @@ int sbg_ctx_synchronize(sbg_ctx* ctx)
         SBG_CUDA(cudaStreamSynchronize(ctx->c.stream));
     });
 }
+int sbg_ctx_set_matvec_form(sbg_ctx* ctx, int form)
+{
+    return guard([&] {
+        bind_ctx(ctx);
+        if (form != 0 && form != 1) throw ValidationError("matvec form: 0 (symmetric) or 1 (full matrix)");
+        ctx->c.matvec_form = form;
+    });
+}
+int sbg_ctx_get_matvec_form(sbg_ctx* ctx, int* form)
+{
+    return guard([&] {
+        bind_ctx(ctx);
+        need(form, "form");
+        *form = ctx->c.matvec_form;
+    });
+}
 int sbg_device_name(int device, char* buf, int cap, int* sm_count)
 {
     return guard([&] {

@@ -104,6 +104,9 @@ struct Ctx {
     cudaStream_t stream = nullptr;
     cudaStream_t aux = nullptr;  // second stream for look-ahead overlap (aux_stream(), created on first use)
     Timers timers;
+    // matrix-vector form of gemv / pcg: 0 = symmetric (reads the upper triangle only, for
+    // n >= kSymvMinN), 1 = full-matrix forms (the row kernel the row-panel PCG shares)
+    int matvec_form = 0;
     std::shared_ptr<void> pcg_ws;  // cached PCG workspace (linalg.cu)
     std::shared_ptr<void> dl_ws;   // cached pinned download ring (context.cu)
     std::shared_ptr<void> near_ws; // cached near-field frontier buffers (assemble.cu)

@@ -62,7 +62,17 @@ struct GemvPlan {
     int n = 0, ld = 0, strips = 0, chunks = 0, rows_per_chunk = 0;
     bool rows = false;  // row-per-warp form: the result lands in part directly (chunks = 1)
     DBuf<double> part;  // chunks x ld partial column sums
+    // symmetric form: only the upper triangle is read, in tiles of H rows x C columns; each
+    // tile adds its row sums (W x) and column sums (W^T x) to per-tile partials that one
+    // fixed-order reduction combines (deterministic) — half the bytes of the full forms
+    bool sym = false;
+    int H = 0, C = 0, nstrips = 0, ntiles = 0;
+    DBuf<int2> tiles;      // (strip, global column chunk) per tile, strip-major
+    DBuf<int> tbase;       // first tile of each strip (nstrips + 1)
+    DBuf<double> rowpart;  // ntiles x H row sums
+    DBuf<double> colpart;  // nstrips x ld column sums (only columns right of the strip's block)
 };
+// form: 0 = the symmetric form where it pays (Ctx::matvec_form default), 1 = full-matrix forms
 void gemv_plan(Ctx* ctx, int n, int ld, GemvPlan& plan);
 // y[0:n] = W x ; x,y device vectors of length >= ld (padding zero)
 void gemv(Ctx* ctx, const DMatrix& W, GemvPlan& plan, const double* x, double* y);
@@ -90,6 +100,8 @@ struct PcgFused {
     const double *p, *Wp;
     double *z, *partials, *hist, *alphas, *betas;
     const int* done;
+    cudaGraphConditionalHandle gate;  // graph body: the while node's handle, set by the last kernel
+    bool has_gate;
 };
 bool prec_apply_pcg(Ctx* ctx, Prec* p, const PcgFused& f);
 void prec_block_diag(Ctx* ctx, Prec* p, int which, std::vector<double>& diag);

@@ -216,6 +216,7 @@ __global__ void k_pcg_p(const PcgDev* st, double* __restrict__ p, const double* 
 // memory rounds at n = 3969; a segment-at-a-time tail added up to 7 more).  U = 8:
 // 16 was slower (fewer resident CTAs), 4/6/10/12 no better.
 constexpr int kRowsPerCta = 8;
+constexpr int kSymvMinN = 2048;
 // row . x for one warp (the row's lanes), U 128-bit loads in flight per lane; KEEP: default
 // caching (W held in L2 by the PCG's access-policy window) instead of evict-first
 template <int U, bool KEEP>
@@ -365,6 +366,180 @@ __global__ void __launch_bounds__(256) k_gemv_rows(const double* __restrict__ W,
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     if (lane == 0) y[row] = v;
 }
+// ---------------------------------------------------------------- symmetric form
+// W symmetric: y = W x from the upper triangle alone (half the bytes of the full forms).
+// Tile (I, J) covers rows [I H, I H + H) and columns [J C, J C + C) right of column I H; its
+// row sums W_IJ x_J go to rowpart[tile], and, right of the strip's own diagonal block, its
+// column sums W_IJ^T x_I go to colpart[I][cols].  A warp owns rows warp, warp + 8, ...; a
+// lane owns the column pairs 2 lane + 64 k, loads them with 128-bit evict-first loads (two
+// rows per pass: 2 C / 64 loads in flight) and keeps the column sums in registers until the
+// 8 warps combine them in shared memory in a fixed order.
+// PF (inside PCG): the vector is p = z + beta p_old formed on the fly (pcg.hpp:93; p itself is
+// rewritten by k_symv_alpha once every tile has read p_old), so no separate p-update launch
+template <int H, int C, bool KEEP, bool PF>
+__global__ void __launch_bounds__(256, 2) k_symv_tiles(const double* __restrict__ W, int ld, int n,
+                                                      const double* __restrict__ x, const int2* __restrict__ tiles,
+                                                      double* __restrict__ rowpart, double* __restrict__ colpart,
+                                                      const int* done, const double* __restrict__ z,
+                                                      const PcgDev* st)
+{
+    static_assert(C % 64 == 0 && H % 16 == 0 && C % H == 0, "tile shape");
+    constexpr int KC = C / 64, RW = H / 8;
+    __shared__ double red[8][C];
+    pdl_wait();
+    if (done && *done) return;
+    const int2 t = tiles[blockIdx.x];
+    const int r0 = t.x * H, c0 = t.y * C;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const double beta = PF ? st->beta : 0.0;
+    auto xv = [&](int i) { return PF ? fma(beta, __ldg(x + i), __ldg(z + i)) : __ldg(x + i); };
+    double2 xj[KC], ca[KC];
+    bool in[KC], off[KC];
+#pragma unroll
+    for (int k = 0; k < KC; ++k) {
+        const int c = c0 + 2 * lane + 64 * k;
+        in[k] = c >= r0 && c < ld;
+        off[k] = c >= r0 + H && c < ld;
+        xj[k] = in[k] ? make_double2(xv(c), xv(c + 1)) : make_double2(0.0, 0.0);
+        ca[k] = make_double2(0.0, 0.0);
+    }
+    const double* wbase = W + c0 + 2 * lane;
+#pragma unroll 1
+    for (int j = 0; j < RW; j += 2) {
+        const int ra = r0 + warp + 8 * j, rb = ra + 8;
+        const bool va = ra < n, vb = rb < n;
+        double2 a[KC], b[KC];
+#pragma unroll
+        for (int k = 0; k < KC; ++k) {
+            const double2* qa = reinterpret_cast<const double2*>(wbase + (size_t)ra * ld + 64 * k);
+            const double2* qb = reinterpret_cast<const double2*>(wbase + (size_t)rb * ld + 64 * k);
+            a[k] = va && in[k] ? (KEEP ? __ldg(qa) : __ldcs(qa)) : make_double2(0.0, 0.0);
+            b[k] = vb && in[k] ? (KEEP ? __ldg(qb) : __ldcs(qb)) : make_double2(0.0, 0.0);
+        }
+        const double xa = va ? xv(ra) : 0.0, xb = vb ? xv(rb) : 0.0;
+        double sa0 = 0.0, sa1 = 0.0, sb0 = 0.0, sb1 = 0.0;
+#pragma unroll
+        for (int k = 0; k < KC; ++k) {
+            sa0 = fma(a[k].x, xj[k].x, sa0);
+            sa1 = fma(a[k].y, xj[k].y, sa1);
+            sb0 = fma(b[k].x, xj[k].x, sb0);
+            sb1 = fma(b[k].y, xj[k].y, sb1);
+            if (off[k]) {
+                ca[k].x = fma(b[k].x, xb, fma(a[k].x, xa, ca[k].x));
+                ca[k].y = fma(b[k].y, xb, fma(a[k].y, xa, ca[k].y));
+            }
+        }
+        double sa = sa0 + sa1, sb = sb0 + sb1;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            sa += __shfl_xor_sync(0xffffffffu, sa, o);
+            sb += __shfl_xor_sync(0xffffffffu, sb, o);
+        }
+        if (lane == 0) {
+            if (va) rowpart[(size_t)blockIdx.x * H + (ra - r0)] = sa;
+            if (vb) rowpart[(size_t)blockIdx.x * H + (rb - r0)] = sb;
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < KC; ++k) {
+        red[warp][2 * lane + 64 * k] = ca[k].x;
+        red[warp][2 * lane + 64 * k + 1] = ca[k].y;
+    }
+    __syncthreads();
+    for (int cc = threadIdx.x; cc < C; cc += blockDim.x) {
+        const int c = c0 + cc;
+        if (c < r0 + H || c >= ld) continue;
+        double v = red[0][cc];
+#pragma unroll
+        for (int w = 1; w < 8; ++w) v += red[w][cc];
+        colpart[(size_t)t.x * ld + c] = v;
+    }
+}
+
+// (W x)_i for the 32 entries i = 32 blockIdx.x + lane of a 256-thread block: group g (warp g)
+// sums the strip's row partials k = g, g + 8, ... and the column partials of the strips
+// q = g, g + 8, ... above it; warp 0 adds the 8 group sums in group order (deterministic).
+// Returns the entry in warp 0 (0 elsewhere).
+__device__ __forceinline__ double symv_entry_block(int n, int H, int ld, const int* __restrict__ tbase,
+                                                   const double* __restrict__ rowpart,
+                                                   const double* __restrict__ colpart, double (*sh)[33])
+{
+    const int g = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int i = blockIdx.x * 32 + lane;
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    if (i < n) {
+        const int I = i / H, ri = i - I * H;
+        const int k1 = tbase[I + 1];
+        for (int k = tbase[I] + g; k < k1; k += 8) s0 += rowpart[(size_t)k * H + ri];
+        const double* cp = colpart + i;
+        int q = g;
+        for (; q + 24 < I; q += 32) {  // four loads in flight per thread
+            s0 += cp[(size_t)q * ld];
+            s1 += cp[(size_t)(q + 8) * ld];
+            s2 += cp[(size_t)(q + 16) * ld];
+            s3 += cp[(size_t)(q + 24) * ld];
+        }
+        for (; q < I; q += 8) s0 += cp[(size_t)q * ld];
+    }
+    sh[g][lane] = (s0 + s1) + (s2 + s3);
+    __syncthreads();
+    double y = 0.0;
+    if (g == 0) {
+#pragma unroll
+        for (int w = 0; w < 8; ++w) y += sh[w][lane];
+    }
+    return y;
+}
+
+__global__ void __launch_bounds__(256) k_symv_reduce(int n, int H, int ld, const int* __restrict__ tbase,
+                                                     const double* __restrict__ rowpart,
+                                                     const double* __restrict__ colpart, double* __restrict__ y,
+                                                     const int* done)
+{
+    __shared__ double sh[8][33];
+    pdl_wait();
+    if (done && *done) return;
+    const double v = symv_entry_block(n, H, ld, tbase, rowpart, colpart, sh);
+    const int i = blockIdx.x * 32 + threadIdx.x;
+    if (threadIdx.x < 32 && i < n) y[i] = v;
+}
+
+// Wp from the symmetric form's partials, p = z + beta p (the tiles formed the same values on
+// the fly), alpha = rz / p.Wp (pcg.hpp:70-73, 93)
+__global__ void __launch_bounds__(256) k_symv_alpha(PcgDev* st, int n, int H, int ld, const int* __restrict__ tbase,
+                                                    const double* __restrict__ rowpart,
+                                                    const double* __restrict__ colpart, double* __restrict__ p,
+                                                    const double* __restrict__ z, double* __restrict__ Wp,
+                                                    double* partials)
+{
+    __shared__ double sh[8][33];
+    __shared__ double red[32];
+    pdl_wait();
+    if (st->done) return;
+    const double y = symv_entry_block(n, H, ld, tbase, rowpart, colpart, sh);
+    const int i = blockIdx.x * 32 + threadIdx.x;
+    double v = 0.0;
+    if (threadIdx.x < 32 && i < n) {
+        const double pn = fma(st->beta, p[i], z[i]);
+        p[i] = pn;
+        Wp[i] = y;
+        v = pn * y;
+    }
+    v = block_sum(v, red);
+    if (last_block(v, partials, &st->counter)) {
+        const double pwp = sum_partials_block(partials, gridDim.x, red);
+        if (threadIdx.x != 0) return;
+        st->counter = 0;
+        st->pwp = pwp;
+        if (pwp <= 0) {
+            st->error = 1;
+            st->done = 1;
+            return;
+        }
+        st->alpha = st->rz / pwp;
+    }
+}
+
 template <typename... A>
 void launch_gemv_rows(bool pdl, cudaStream_t s, int n, A... args)
 {
@@ -376,10 +551,81 @@ void launch_gemv_rows(bool pdl, cudaStream_t s, int n, A... args)
 }
 }  // namespace
 
+// smallest n that takes the symmetric form (below it the one-launch row form wins on latency)
+static int symv_min_n()
+{
+    static const int v = [] {
+        const char* e = getenv("SBG_SYMV_MIN_N");
+        return e ? atoi(e) : kSymvMinN;
+    }();
+    return v;
+}
+
+static void symv_plan(Ctx* ctx, int n, int ld, GemvPlan& plan)
+{
+    plan.sym = true;
+    plan.H = n <= 8000 ? 64 : 128;
+    plan.C = 256;  // 512 columns per tile needs more than the 128 registers of 2 CTAs/SM
+    plan.nstrips = (n + plan.H - 1) / plan.H;
+    const int nchunks = (ld + plan.C - 1) / plan.C;
+    std::vector<int2> tiles;
+    std::vector<int> tbase(plan.nstrips + 1, 0);
+    for (int I = 0; I < plan.nstrips; ++I) {
+        tbase[I] = (int)tiles.size();
+        for (int J = I * plan.H / plan.C; J < nchunks; ++J) tiles.push_back(make_int2(I, J));
+    }
+    tbase[plan.nstrips] = (int)tiles.size();
+    plan.ntiles = (int)tiles.size();
+    plan.tiles.alloc(tiles.size());
+    plan.tbase.alloc(tbase.size());
+    plan.rowpart.alloc((size_t)plan.ntiles * plan.H);
+    plan.colpart.alloc((size_t)plan.nstrips * ld);
+    // pageable sources: the copies are staged before the calls return
+    SBG_CUDA(cudaMemcpyAsync(plan.tiles.p, tiles.data(), tiles.size() * sizeof(int2), cudaMemcpyHostToDevice,
+                             ctx->stream));
+    SBG_CUDA(cudaMemcpyAsync(plan.tbase.p, tbase.data(), tbase.size() * sizeof(int), cudaMemcpyHostToDevice,
+                             ctx->stream));
+    SBG_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+// keep: default-cached loads (W held in L2 by the PCG's access-policy window)
+// z, st (PCG): the vector is z + st->beta x (x = p), see k_symv_tiles
+static void symv_tiles_launch(Ctx* ctx, const DMatrix& W, const GemvPlan& plan, const double* x, const int* done,
+                              bool keep = false, const double* z = nullptr, const PcgDev* st = nullptr)
+{
+    const dim3 grid(plan.ntiles), block(256);
+    auto go = [&](auto kern) {
+        launch_pdl(kern, grid, block, 0, ctx->stream, (const double*)W.a.p, W.ld, W.n, x, (const int2*)plan.tiles.p,
+                   plan.rowpart.p, plan.colpart.p, done, z, st);
+    };
+    const bool pf = z != nullptr;
+    if (plan.H == 64) {
+        if (pf) keep ? go(k_symv_tiles<64, 256, true, true>) : go(k_symv_tiles<64, 256, false, true>);
+        else keep ? go(k_symv_tiles<64, 256, true, false>) : go(k_symv_tiles<64, 256, false, false>);
+    } else {
+        if (pf) keep ? go(k_symv_tiles<128, 256, true, true>) : go(k_symv_tiles<128, 256, false, true>);
+        else keep ? go(k_symv_tiles<128, 256, true, false>) : go(k_symv_tiles<128, 256, false, false>);
+    }
+    ::sbg::count_launch();
+    SBG_LAUNCH_CHECK();
+}
+
+static void symv_reduce_launch(Ctx* ctx, const DMatrix& W, const GemvPlan& plan, double* y, const int* done)
+{
+    launch_pdl(k_symv_reduce, dim3((W.n + 31) / 32), dim3(256), 0, ctx->stream, W.n, plan.H, W.ld,
+               (const int*)plan.tbase.p, (const double*)plan.rowpart.p, (const double*)plan.colpart.p, y, done);
+    ::sbg::count_launch();
+    SBG_LAUNCH_CHECK();
+}
+
 void gemv_plan(Ctx* ctx, int n, int ld, GemvPlan& plan)
 {
     plan.n = n;
     plan.ld = ld;
+    if (ctx->matvec_form == 0 && n >= symv_min_n()) {
+        symv_plan(ctx, n, ld, plan);
+        return;
+    }
     // measured crossover (B200, L2 flushed): rows form faster at n = 3969 (27.3 vs 35.9 us)
     // and n = 6721 (67.2 vs 68.6 us), even at 12097 (182 us both), column-sum form faster at
     // 25281 (731 vs 805 us)
@@ -436,6 +682,11 @@ void gemv(Ctx* ctx, const DMatrix& W, GemvPlan& plan, const double* x, double* y
 {
     if (W.n == 0) return;
     TimedScope ts(ctx, "gemv_f64");
+    if (plan.sym) {
+        symv_tiles_launch(ctx, W, plan, x, nullptr);
+        symv_reduce_launch(ctx, W, plan, y, nullptr);
+        return;
+    }
     if (plan.rows) {
         launch_gemv_rows(false, ctx->stream, W.n, (const double*)W.a.p, W.ld, W.n, x, y, (const int*)nullptr);
         ::sbg::count_launch();
@@ -507,7 +758,7 @@ double lanczos_kappa(const std::vector<double>& alphas, const std::vector<double
 // Device workspace of one PCG size, cached on the context (no allocation or
 // pinned-memory registration per solve).
 struct PcgWork {
-    int ld = 0, cap = 0;
+    int ld = 0, cap = 0, form = 0;
     DBuf<double> buf, partials, hist, alphas, betas, xbuf;  // xbuf: row-panel exchange buffer (ld)
     DBuf<double> ebuf, energy;  // energy history: e and exact (2 ld), per-iteration values (cap)
     DBuf<PcgDev> st;
@@ -519,6 +770,7 @@ struct PcgWork {
     const void* gW = nullptr;
     unsigned long long gP = 0;  // preconditioner uid (addresses are reused after a free)
     int kernels_per_iter = 0;
+    bool body_gate = true;  // a gate kernel ends each iteration (else its last kernel sets the handle)
     void drop_graph()
     {
         if (exec) cudaGraphExecDestroy(exec);
@@ -538,9 +790,10 @@ struct PcgWork {
 static PcgWork& pcg_work(Ctx* ctx, const DMatrix& W, int maxit)
 {
     auto* w = static_cast<PcgWork*>(ctx->pcg_ws.get());
-    if (!w || w->ld != W.ld || w->plan.n != W.n || w->cap < maxit + 2) {
+    if (!w || w->ld != W.ld || w->plan.n != W.n || w->cap < maxit + 2 || w->form != ctx->matvec_form) {
         auto fresh = std::make_shared<PcgWork>();
         fresh->ld = W.ld;
+        fresh->form = ctx->matvec_form;
         fresh->cap = std::max(maxit + 2, 128);
         fresh->buf.alloc(6 * (size_t)W.ld);
         fresh->partials.alloc(std::max((W.n + kRowsPerCta - 1) / kRowsPerCta, 1));  // one per block: the 8-row blocks of the rows form are the most
@@ -564,7 +817,7 @@ static PcgWork& pcg_work(Ctx* ctx, const DMatrix& W, int maxit)
 // the persisting carve-out on chip from one iteration to the next instead of streaming it
 // from HBM every time (hitRatio = carve-out / window when W is larger).  Matrices far larger
 // than L2 (config 5: 5.1 GB) gain nothing and get no window.  SBG_L2_PERSIST=0 disables it.
-static bool l2_window(Ctx* ctx, const DMatrix& W, cudaAccessPolicyWindow& win)
+static bool l2_window(Ctx* ctx, const DMatrix& W, bool sym, cudaAccessPolicyWindow& win)
 {
     static const bool enabled = [] {
         const char* e = getenv("SBG_L2_PERSIST");
@@ -574,8 +827,10 @@ static bool l2_window(Ctx* ctx, const DMatrix& W, cudaAccessPolicyWindow& win)
     int maxwin = 0, maxpersist = 0;
     SBG_CUDA(cudaDeviceGetAttribute(&maxwin, cudaDevAttrMaxAccessPolicyWindowSize, ctx->device));
     SBG_CUDA(cudaDeviceGetAttribute(&maxpersist, cudaDevAttrMaxPersistingL2CacheSize, ctx->device));
-    const size_t bytes = (size_t)W.n * W.ld * sizeof(double);
-    if (maxwin <= 0 || maxpersist <= 0 || bytes > 4 * (size_t)maxpersist) return false;
+    size_t bytes = (size_t)W.n * W.ld * sizeof(double);
+    // the symmetric form touches only the upper triangle (and its strips' diagonal blocks)
+    const size_t touched = sym ? bytes / 2 + (size_t)W.n * 64 * sizeof(double) : bytes;
+    if (maxwin <= 0 || maxpersist <= 0 || touched > 4 * (size_t)maxpersist) return false;
     static bool limit_set = false;
     if (!limit_set) {
         SBG_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)maxpersist));
@@ -583,7 +838,7 @@ static bool l2_window(Ctx* ctx, const DMatrix& W, cudaAccessPolicyWindow& win)
     }
     win.base_ptr = W.a.p;
     win.num_bytes = std::min(bytes, (size_t)maxwin);
-    win.hitRatio = (float)std::min(1.0, (double)maxpersist / (double)win.num_bytes);
+    win.hitRatio = (float)std::min(1.0, (double)maxpersist / (double)std::min(touched, win.num_bytes));
     win.hitProp = cudaAccessPropertyPersisting;
     win.missProp = cudaAccessPropertyStreaming;
     return true;
@@ -622,7 +877,7 @@ void pcg_run(Ctx* ctx, const DMatrix& W, Prec* prec, const double* rhs, double* 
     double* rn = Wp + len;  // the fused apply's new residual (copied back into r)
     double* z = prec ? zbuf : r;  // no preconditioner: z = r (pcg.hpp:45-47)
     cudaAccessPolicyWindow keep_win{};
-    const bool keep_W = !rows && pcg_graph_enabled() && l2_window(ctx, W, keep_win);  // W held in L2 (graph form)
+    const bool keep_W = !rows && pcg_graph_enabled() && l2_window(ctx, W, w.plan.sym, keep_win);  // W held in L2 (graph form)
     SBG_CUDA(cudaMemcpyAsync(r, rhs, n * sizeof(double), on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
     const int nb = (n + 255) / 256;
     PcgDev h{};
@@ -635,10 +890,10 @@ void pcg_run(Ctx* ctx, const DMatrix& W, Prec* prec, const double* rhs, double* 
     double* e_err = nullptr;
     const double* d_exact = nullptr;
     if (exact) {
-        if ((size_t)w.ebuf.n < 2 * len) w.ebuf.alloc(2 * len);
+        if ((size_t)w.ebuf.n < 3 * len) w.ebuf.alloc(3 * len);
         if ((size_t)w.energy.n < (size_t)w.cap) w.energy.alloc(w.cap);
         e_err = w.ebuf.p;
-        SBG_CUDA(cudaMemsetAsync(w.ebuf.p, 0, 2 * len * sizeof(double), s));
+        SBG_CUDA(cudaMemsetAsync(w.ebuf.p, 0, 3 * len * sizeof(double), s));
         SBG_CUDA(cudaMemcpyAsync(w.ebuf.p + len, exact, n * sizeof(double),
                                  on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
         d_exact = w.ebuf.p + len;
@@ -647,9 +902,18 @@ void pcg_run(Ctx* ctx, const DMatrix& W, Prec* prec, const double* rhs, double* 
         launch_pdl(k_pcg_err, dim3(nb), dim3(256), 0, s, (const PcgDev*)w.st.p, (const double*)x, d_exact, e_err, n,
                    gated);
         count_launch();
-        gemv_partial_launch(ctx, W, w.plan, e_err, gated ? done : nullptr);
-        launch_pdl(k_pcg_energy, dim3(nb), dim3(256), 0, s, w.st.p, (const double*)w.plan.part.p, w.plan.chunks, W.ld,
-                   n, (const double*)e_err, w.partials.p, w.energy.p, off, gated);
+        const double* We = w.plan.part.p;
+        int chunks = w.plan.chunks;
+        if (w.plan.sym) {  // W e into the third slice of ebuf
+            symv_tiles_launch(ctx, W, w.plan, e_err, gated ? done : nullptr);
+            symv_reduce_launch(ctx, W, w.plan, w.ebuf.p + 2 * len, gated ? done : nullptr);
+            We = w.ebuf.p + 2 * len;
+            chunks = 1;
+        } else {
+            gemv_partial_launch(ctx, W, w.plan, e_err, gated ? done : nullptr);
+        }
+        launch_pdl(k_pcg_energy, dim3(nb), dim3(256), 0, s, w.st.p, We, chunks, W.ld, n, (const double*)e_err,
+                   w.partials.p, w.energy.p, off, gated);
         count_launch();
         SBG_LAUNCH_CHECK();
     };
@@ -665,7 +929,10 @@ void pcg_run(Ctx* ctx, const DMatrix& W, Prec* prec, const double* rhs, double* 
         SBG_CUDA(cudaMemcpyAsync(w.st.p, &h, sizeof(h), cudaMemcpyHostToDevice, s));
     }
     // one PCG iteration (pcg.hpp:69-93) on the context stream
-    auto enqueue_iteration = [&]() {
+    // gate (graph body only): the while node's handle; when the iteration's last kernel sets it
+    // (the fused preconditioner path) no separate gate kernel follows — returns whether it did
+    auto enqueue_iteration = [&](const cudaGraphConditionalHandle* gate) -> bool {
+        bool gated = false;
         if (rows) {
             // row panel: this rank's rows of W p into the exchange buffer, then the
             // caller's all-gather fills the rest (issued even past convergence, so every
@@ -689,6 +956,14 @@ void pcg_run(Ctx* ctx, const DMatrix& W, Prec* prec, const double* rhs, double* 
             else
                 launch_pdl(k_pcg_alpha, dim3(nb), dim3(256), 0, s, w.st.p, (const double*)w.xbuf.p, 1, W.ld, n, p,
                            Wp, w.partials.p);
+        } else if (w.plan.sym) {  // symmetric form: upper-triangle tiles, then W p and alpha
+            {
+                TimedScope ts(ctx, "gemv_f64");
+                symv_tiles_launch(ctx, W, w.plan, p, done, keep_W, z, w.st.p);
+            }
+            launch_pdl(k_symv_alpha, dim3((n + 31) / 32), dim3(256), 0, s, w.st.p, n, w.plan.H, W.ld,
+                       (const int*)w.plan.tbase.p, (const double*)w.plan.rowpart.p, (const double*)w.plan.colpart.p, p,
+                       (const double*)z, Wp, w.partials.p);
         } else if (w.plan.rows) {  // rows form: W p and alpha in one launch
             TimedScope ts(ctx, "gemv_f64");
             const dim3 grid((n + kRowsPerCta - 1) / kRowsPerCta);
@@ -709,8 +984,11 @@ void pcg_run(Ctx* ctx, const DMatrix& W, Prec* prec, const double* rhs, double* 
         count_launch();
         // x += alpha p, r -= alpha Wp, z = M r, r.z and beta: fused into the preconditioner's
         // three launches when it allows (inverse mode), else one kernel per step
-        const PcgFused fu{w.st.p, x, r, rn, p, Wp, z, w.partials.p, w.hist.p, w.alphas.p, w.betas.p, done};
-        if (exact || !prec || !prec_apply_pcg(ctx, prec, fu)) {
+        const PcgFused fu{w.st.p, x, r, rn, p, Wp, z, w.partials.p, w.hist.p, w.alphas.p, w.betas.p, done,
+                          gate ? *gate : cudaGraphConditionalHandle{}, gate != nullptr};
+        if (!exact && prec && prec_apply_pcg(ctx, prec, fu)) {
+            gated = gate != nullptr;
+        } else {
             launch_pdl(k_pcg_update, dim3(nb), dim3(256), 0, s, w.st.p, x, r, p, Wp, n);
             count_launch();
             if (exact) enqueue_energy(1, 1);
@@ -719,9 +997,12 @@ void pcg_run(Ctx* ctx, const DMatrix& W, Prec* prec, const double* rhs, double* 
                        w.betas.p);
             count_launch();
         }
-        launch_pdl(k_pcg_p, dim3(nb), dim3(256), 0, s, w.st.p, p, z, n);
-        count_launch();
+        if (!(w.plan.sym && !rows)) {  // (the symmetric form forms p inside the next matvec)
+            launch_pdl(k_pcg_p, dim3(nb), dim3(256), 0, s, w.st.p, p, z, n);
+            count_launch();
+        }
         SBG_LAUNCH_CHECK();
+        return gated;
     };
     // the exchange is a host call; the energy history (test path) runs host-driven too
     const bool graph = n > 0 && pcg_graph_enabled() && !rows && !exact;
@@ -755,11 +1036,11 @@ void pcg_run(Ctx* ctx, const DMatrix& W, Prec* prec, const double* rhs, double* 
                 SBG_CUDA(cudaGraphAddNode(&cond, ng, nodes.data(), nroots, &cp));
                 cudaGraph_t body = cp.conditional.phGraph_out[0];
                 SBG_CUDA(cudaStreamBeginCaptureToGraph(s, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
-                enqueue_iteration();
-                k_pcg_gate<<<1, 32, 0, s>>>(w.st.p, handle);
+                w.body_gate = !enqueue_iteration(&handle);
+                if (w.body_gate) k_pcg_gate<<<1, 32, 0, s>>>(w.st.p, handle);
                 SBG_CUDA(cudaStreamEndCapture(s, &g_out));
                 cudaAccessPolicyWindow win{};
-                if (l2_window(ctx, W, win)) {  // W persisting in L2 for every kernel of the body
+                if (l2_window(ctx, W, w.plan.sym, win)) {  // W persisting in L2 for every kernel of the body
                     size_t nb = 0;
                     SBG_CUDA(cudaGraphGetNodes(body, nullptr, &nb));
                     std::vector<cudaGraphNode_t> bn(nb);
@@ -814,7 +1095,7 @@ void pcg_run(Ctx* ctx, const DMatrix& W, Prec* prec, const double* rhs, double* 
         SBG_CUDA(cudaGraphLaunch(w.exec, s));
         SBG_CUDA(cudaMemcpyAsync(w.hs, w.st.p, sizeof(PcgDev), cudaMemcpyDeviceToHost, s));
         SBG_CUDA(cudaStreamSynchronize(s));
-        add_launches((long long)w.kernels_per_iter * w.hs->it + 1 + w.hs->it);  // body kernels + gates
+        add_launches((long long)w.kernels_per_iter * w.hs->it + 1 + (w.body_gate ? w.hs->it : 0));  // + gates
     }
     int batch = 4, enqueued = graph ? maxit : 0;
     while (true) {
@@ -828,13 +1109,13 @@ void pcg_run(Ctx* ctx, const DMatrix& W, Prec* prec, const double* rhs, double* 
         }
         if (stop) break;
         const int todo = std::min(batch, maxit - enqueued);
-        for (int t = 0; t < todo; ++t) enqueue_iteration();
+        for (int t = 0; t < todo; ++t) enqueue_iteration(nullptr);
         enqueued += todo;
         batch = std::min(batch * 2, 64);
     }
     {
         cudaAccessPolicyWindow win{};
-        if (l2_window(ctx, W, win)) SBG_CUDA(cudaCtxResetPersistingL2Cache());  // give L2 back to what follows
+        if (l2_window(ctx, W, w.plan.sym, win)) SBG_CUDA(cudaCtxResetPersistingL2Cache());  // give L2 back to what follows
     }
     const PcgDev fin = *w.hs;
     if (fin.error == 1) throw NumericalError("pcg: matrix is not positive definite");

@@ -915,10 +915,14 @@ __global__ void __launch_bounds__(256) k_prec_scatter_rz(PcgDev* st, const doubl
                                                          const double* __restrict__ rval,
                                                          const double* __restrict__ y_c, double* __restrict__ z,
                                                          double* __restrict__ r, const double* __restrict__ rn,
-                                                         double* partials, double* hist, double* alphas, double* betas)
+                                                         double* partials, double* hist, double* alphas, double* betas,
+                                                         cudaGraphConditionalHandle gate, int has_gate)
 {
     pdl_wait();
-    if (st->done) return;
+    if (st->done) {  // (an earlier kernel of this iteration stopped it: end the loop)
+        if (has_gate && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(gate, 0u);
+        return;
+    }
     __shared__ double sh[32];
     const int d = blockIdx.x * blockDim.x + threadIdx.x;
     double v = 0.0;
@@ -939,6 +943,7 @@ __global__ void __launch_bounds__(256) k_prec_scatter_rz(PcgDev* st, const doubl
         const double rz_new = sum_partials(partials, gridDim.x);
         st->counter = 0;
         pcg_finish_rz(st, rz_new, hist, alphas, betas);
+        if (has_gate) cudaGraphSetConditional(gate, st->done ? 0u : 1u);  // the while node's test
     }
 }
 
@@ -1467,7 +1472,7 @@ bool prec_apply_pcg(Ctx* ctx, Prec* P, const PcgFused& f)
     launch_pdl(k_prec_scatter_rz, dim3(dof_blocks), dim3(256), 0, s, f.st, (const double*)P->locy.p,
                (const int*)P->pos.p, n, (const int*)(P->nc > 0 ? P->Rr_ptr.p : nullptr), (const int*)P->Rr_col.p,
                (const double*)P->Rr_val.p, (const double*)(cb >= 0 ? P->locy.p + P->h_loc[cb] : nullptr), f.z, f.r,
-               (const double*)f.rn, f.partials, f.hist, f.alphas, f.betas);
+               (const double*)f.rn, f.partials, f.hist, f.alphas, f.betas, f.gate, f.has_gate ? 1 : 0);
     count_launch();
     SBG_LAUNCH_CHECK();
     return true;

@@ -57,6 +57,8 @@ SIGNATURES = {
     "sbg_ctx_create": (C.c_int, [C.c_int, C.POINTER(vp)]),
     "sbg_ctx_destroy": (None, [vp]),
     "sbg_ctx_synchronize": (C.c_int, [vp]),
+    "sbg_ctx_set_matvec_form": (C.c_int, [vp, C.c_int]),
+    "sbg_ctx_get_matvec_form": (C.c_int, [vp, C.POINTER(C.c_int)]),
     "sbg_device_name": (C.c_int, [C.c_int, C.c_char_p, C.c_int, C.POINTER(C.c_int)]),
     "sbg_timers_enable": (C.c_int, [vp, C.c_int]),
     "sbg_timers_reset": (C.c_int, [vp]),
@@ -207,6 +209,20 @@ class Context(_Handle):
 
     def synchronize(self):
         _check(lib().sbg_ctx_synchronize(self.h))
+
+    @property
+    def matvec_form(self) -> str:
+        """"symmetric" (default: W x from the upper triangle, n >= 2048) or "full" (every entry;
+        the row kernel sbg_pcg_rows shares, so pcg_rows then equals pcg bitwise)"""
+        f = C.c_int()
+        _check(lib().sbg_ctx_get_matvec_form(self.h, C.byref(f)))
+        return ("symmetric", "full")[f.value]
+
+    @matvec_form.setter
+    def matvec_form(self, form: str):
+        if form not in ("symmetric", "full"):
+            raise ValidationError("matvec_form: 'symmetric' or 'full'")
+        _check(lib().sbg_ctx_set_matvec_form(self.h, 0 if form == "symmetric" else 1))
 
     @property
     def stream(self) -> int:

@@ -129,6 +129,30 @@ def test_matvec_and_dump_roundtrip(ctx, tmp_path):
     assert np.array_equal(R.download(), W0)
 
 
+@pytest.mark.parametrize("n", [2047, 2048, 2113, 4000, 8001, 9000])
+def test_symmetric_matvec_form(ctx, n):
+    """matvec_form "symmetric" (n >= 2048: the upper triangle only, tiles of 64 rows up to
+    n = 8000 and of 128 above, fixed-order partial sums) against numpy and against the
+    full-matrix form, across the threshold and on ragged sizes; deterministic run to run"""
+    rng = np.random.default_rng(n)
+    A = rng.standard_normal((n, n))
+    W0 = A + A.T
+    del A
+    x = rng.standard_normal(n)
+    W = S.GalerkinMatrix.from_host(W0, ctx)
+    ref = W0 @ x
+    bound = 1e-13 * (np.abs(W0) @ np.abs(x)) + 1e-15 * np.abs(ref).max()
+    ys = W.matvec(x)
+    assert np.array_equal(ys, W.matvec(x))
+    ctx.matvec_form = "full"
+    try:
+        yf = W.matvec(x)
+    finally:
+        ctx.matvec_form = "symmetric"
+    for y in (ys, yf):
+        assert (np.abs(y - ref) <= bound).all(), np.abs(y - ref).max()
+
+
 # ------------------------------------------------------------------ preconditioner
 def setup_pair(pair):
     fine, coarse = S.inflate(pair.fine), S.inflate(pair.coarse)

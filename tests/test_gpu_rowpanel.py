@@ -3,8 +3,9 @@ GPU.  Ranks cannot be stood in for on one device (their collectives would wait o
 other), so the panels are checked two ways:
   * emulated exchange: one process owns panel r and its exchange hook computes the other
     panels' rows with the same row kernel on the same stream — the result must equal the
-    single-GPU pcg bitwise (n <= 8000, where pcg uses the same row kernel) or to the PCG
-    tolerances (larger n, where pcg uses the column-sum form);
+    single-GPU pcg bitwise when that runs the full-matrix form (matvec_form "full", n <= 8000:
+    the same row kernel), and the default symmetric-form pcg (upper triangle only) or the
+    column-sum form (larger n) to the PCG tolerances;
   * the real torch.distributed exchange (NCCL, world size 1) on the PCG's own stream.
 The two-rank exchange logic itself is covered on CPU with gloo (tests/test_distributed.py).
 """
@@ -22,6 +23,14 @@ S = pytest.importorskip("paper_2310_09204_b200.screenbem")
 @pytest.fixture(scope="module")
 def ctx():
     return S.Context(0)
+
+
+@pytest.fixture
+def full_form(ctx):
+    """pcg with the full-matrix form (the row kernel the panels share) for this test"""
+    ctx.matvec_form = "full"
+    yield ctx
+    ctx.matvec_form = "symmetric"
 
 
 def system(ctx, cfg=1, kind=None, m=0, r=0):
@@ -50,7 +59,8 @@ def emulated(W, world, rank):
 
 @pytest.mark.parametrize("cfg", [1, 2])
 @pytest.mark.parametrize("world,rank", [(1, 0), (2, 0), (2, 1), (3, 2), (8, 5)])
-def test_row_panels_equal_pcg_bitwise(ctx, cfg, world, rank):
+def test_row_panels_equal_pcg_bitwise(full_form, cfg, world, rank):
+    ctx = full_form
     W, L, prec = system(ctx, cfg)
     ref = S.pcg(W, prec, L, 1e-8)
     rows, ex, calls = emulated(W, world, rank)
@@ -59,6 +69,18 @@ def test_row_panels_equal_pcg_bitwise(ctx, cfg, world, rank):
     assert np.array_equal(rep.solution, ref.solution)
     assert np.array_equal(rep.residual_history, ref.residual_history)
     assert len(calls) >= rep.iterations  # one exchange per enqueued iteration
+
+
+@pytest.mark.parametrize("world,rank", [(2, 1), (4, 3)])
+def test_row_panels_match_symmetric_form_pcg(ctx, world, rank):
+    # config 2 (n = 3969 >= 2048): pcg's default matvec reads the upper triangle only
+    assert ctx.matvec_form == "symmetric"
+    W, L, prec = system(ctx, 2)
+    ref = S.pcg(W, prec, L, 1e-8)
+    rows, ex, _ = emulated(W, world, rank)
+    rep = S.pcg_rows(W, prec, L, rows, ex, 1e-8)
+    assert rep.converged and abs(rep.iterations - ref.iterations) <= 1
+    assert np.linalg.norm(rep.solution - ref.solution) / np.linalg.norm(ref.solution) < 1e-8
 
 
 def test_row_panels_large_n_column_form_reference(ctx):
@@ -72,7 +94,8 @@ def test_row_panels_large_n_column_form_reference(ctx):
     assert np.linalg.norm(rep.solution - ref.solution) / np.linalg.norm(ref.solution) < 1e-8
 
 
-def test_row_panels_unpreconditioned_and_edges(ctx):
+def test_row_panels_unpreconditioned_and_edges(full_form):
+    ctx = full_form
     W, L, prec = system(ctx, 1)
     ref = S.pcg(W, None, L, 1e-8)
     rows, ex, _ = emulated(W, 2, 1)
@@ -106,10 +129,12 @@ def test_nccl_exchange_world1_on_pcg_stream(ctx):
     torch.cuda.set_device(0)
     dist.init_process_group("nccl", rank=0, world_size=1)
     try:
+        ctx.matvec_form = "full"  # bitwise against the row kernel
         W, L, prec = system(ctx, 2)
         ref = S.pcg(W, prec, L, 1e-8)
         ex = S.allgather_exchange(dist, 0, 1, W.n, device="cuda:0")
         rep = S.pcg_rows(W, prec, L, S.row_ranges(W.n, 1)[0], ex, 1e-8)
         assert rep.iterations == ref.iterations and np.array_equal(rep.solution, ref.solution)
     finally:
+        ctx.matvec_form = "symmetric"
         dist.destroy_process_group()
