@@ -572,7 +572,11 @@ def run_ours(args):
     S.lib().sbg_device_free(dx)
     S.lib().sbg_device_free(dy)
     matvec_s = gm / gc * 1e-3
-    matvec_bytes = 8.0 * n * n + 16.0 * n
+    # algorithmic bytes of the context's matvec form (symmetric: the upper triangle, x, y and
+    # the partial sums; linalg.cu gemv_bytes)
+    mb = C.c_double()
+    S._check(S.lib().sbg_matvec_bytes(ctx.h, W.h, C.byref(mb)))
+    matvec_bytes = mb.value
     matvec_gbs = matvec_bytes / matvec_s / 1e9
     peaks = load_peaks()
     hbm_peak = peaks.get("hbm_gbs") or 6650.0
@@ -680,7 +684,8 @@ def run_ours(args):
                                             if min(far_ms, near_ms) > 0 else None}},
             "roofline_matvec": {"bound": "hbm", "kernel": "gemv_f64", "achieved": matvec_gbs, "peak": hbm_peak,
                                 "unit": "GB/s", "frac": matvec_gbs / hbm_peak, "traffic": matvec_traffic(cfg),
-                                "bytes_per_launch": matvec_bytes, "us_per_launch": matvec_s * 1e6,
+                                "form": ctx.matvec_form, "bytes_per_launch": matvec_bytes,
+                                "bytes_full_matrix": 8.0 * n * n + 16.0 * n, "us_per_launch": matvec_s * 1e6,
                                 "peak_source": ("of measured: MEASURED_PEAKS.json hbm_gbs (a copy; a read-only "
                                                 "stream can exceed it)") if peaks.get("hbm_gbs") else "of fallback",
                                 "peak_nominal": 7700.0, "frac_nominal": matvec_gbs / 7700.0},

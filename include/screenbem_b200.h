@@ -283,6 +283,10 @@ int sbg_pcg_device(sbg_ctx* ctx, const sbg_matrix* W, sbg_prec* prec, const doub
 /* y = W x repeated `reps` times on device vectors; per-launch time via timers ("gemv_f64").
  * d_x: n doubles, any alignment (copied into a zero-padded context scratch vector). */
 int sbg_matvec_device(sbg_ctx* ctx, const sbg_matrix* W, const double* d_x, double* d_y, int reps);
+/* algorithmic DRAM bytes of one matvec on this context's form (roofline bookkeeping): the
+ * entries read (8 n^2 full; the upper triangle and its diagonal blocks symmetric), x, y and
+ * the symmetric form's partial sums */
+int sbg_matvec_bytes(sbg_ctx* ctx, const sbg_matrix* W, double* bytes);
 int sbg_apply_preconditioner_device(sbg_ctx* ctx, sbg_prec* p, const double* d_r, double* d_z, int reps);
 /* write a buffer larger than L2 (L2 flush between timed iterations) */
 int sbg_l2_flush(sbg_ctx* ctx);

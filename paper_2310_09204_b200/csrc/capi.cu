@@ -1124,6 +1124,17 @@ int sbg_matvec_device(sbg_ctx* ctx, const sbg_matrix* W, const double* d_x, doub
         SBG_CUDA(cudaStreamSynchronize(ctx->c.stream));
     });
 }
+int sbg_matvec_bytes(sbg_ctx* ctx, const sbg_matrix* W, double* bytes)
+{
+    return guard([&] {
+        need(W, "W");
+        need(bytes, "bytes");
+        bind_ctx(ctx);
+        GemvPlan plan;
+        gemv_plan(&ctx->c, W->M.n, W->M.ld, plan);
+        *bytes = gemv_bytes(plan);
+    });
+}
 int sbg_apply_preconditioner_device(sbg_ctx* ctx, sbg_prec* p, const double* d_r, double* d_z, int reps)
 {
     return guard([&] {

@@ -74,6 +74,7 @@ struct GemvPlan {
 };
 // form: 0 = the symmetric form where it pays (Ctx::matvec_form default), 1 = full-matrix forms
 void gemv_plan(Ctx* ctx, int n, int ld, GemvPlan& plan);
+double gemv_bytes(const GemvPlan& plan);  // algorithmic DRAM bytes of one matvec
 // y[0:n] = W x ; x,y device vectors of length >= ld (padding zero)
 void gemv(Ctx* ctx, const DMatrix& W, GemvPlan& plan, const double* x, double* y);
 

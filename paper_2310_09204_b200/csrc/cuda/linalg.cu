@@ -404,41 +404,48 @@ __global__ void __launch_bounds__(256, 2) k_symv_tiles(const double* __restrict_
         ca[k] = make_double2(0.0, 0.0);
     }
     const double* wbase = W + c0 + 2 * lane;
+    constexpr int RP = 4;  // rows per pass: RP * KC 128-bit loads in flight per lane
+    static_assert(RW % RP == 0, "rows per warp");
 #pragma unroll 1
-    for (int j = 0; j < RW; j += 2) {
-        const int ra = r0 + warp + 8 * j, rb = ra + 8;
-        const bool va = ra < n, vb = rb < n;
-        double2 a[KC], b[KC];
+    for (int j = 0; j < RW; j += RP) {
+        double2 a[RP][KC];
+        double xr[RP];
 #pragma unroll
-        for (int k = 0; k < KC; ++k) {
-            const double2* qa = reinterpret_cast<const double2*>(wbase + (size_t)ra * ld + 64 * k);
-            const double2* qb = reinterpret_cast<const double2*>(wbase + (size_t)rb * ld + 64 * k);
-            a[k] = va && in[k] ? (KEEP ? __ldg(qa) : __ldcs(qa)) : make_double2(0.0, 0.0);
-            b[k] = vb && in[k] ? (KEEP ? __ldg(qb) : __ldcs(qb)) : make_double2(0.0, 0.0);
-        }
-        const double xa = va ? xv(ra) : 0.0, xb = vb ? xv(rb) : 0.0;
-        double sa0 = 0.0, sa1 = 0.0, sb0 = 0.0, sb1 = 0.0;
+        for (int u = 0; u < RP; ++u) {
+            const int r = r0 + warp + 8 * (j + u);
+            const bool v = r < n;
 #pragma unroll
-        for (int k = 0; k < KC; ++k) {
-            sa0 = fma(a[k].x, xj[k].x, sa0);
-            sa1 = fma(a[k].y, xj[k].y, sa1);
-            sb0 = fma(b[k].x, xj[k].x, sb0);
-            sb1 = fma(b[k].y, xj[k].y, sb1);
-            if (off[k]) {
-                ca[k].x = fma(b[k].x, xb, fma(a[k].x, xa, ca[k].x));
-                ca[k].y = fma(b[k].y, xb, fma(a[k].y, xa, ca[k].y));
+            for (int k = 0; k < KC; ++k) {
+                const double2* q = reinterpret_cast<const double2*>(wbase + (size_t)r * ld + 64 * k);
+                a[u][k] = v && in[k] ? (KEEP ? __ldg(q) : __ldcs(q)) : make_double2(0.0, 0.0);
             }
+            xr[u] = v ? xv(r) : 0.0;
         }
-        double sa = sa0 + sa1, sb = sb0 + sb1;
+        double sr[RP];
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            sa += __shfl_xor_sync(0xffffffffu, sa, o);
-            sb += __shfl_xor_sync(0xffffffffu, sb, o);
+        for (int u = 0; u < RP; ++u) {
+            double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+            for (int k = 0; k < KC; ++k) {
+                s0 = fma(a[u][k].x, xj[k].x, s0);
+                s1 = fma(a[u][k].y, xj[k].y, s1);
+                if (off[k]) {
+                    ca[k].x = fma(a[u][k].x, xr[u], ca[k].x);
+                    ca[k].y = fma(a[u][k].y, xr[u], ca[k].y);
+                }
+            }
+            sr[u] = s0 + s1;
         }
-        if (lane == 0) {
-            if (va) rowpart[(size_t)blockIdx.x * H + (ra - r0)] = sa;
-            if (vb) rowpart[(size_t)blockIdx.x * H + (rb - r0)] = sb;
-        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+            for (int u = 0; u < RP; ++u) sr[u] += __shfl_xor_sync(0xffffffffu, sr[u], o);
+        if (lane == 0)
+#pragma unroll
+            for (int u = 0; u < RP; ++u) {
+                const int r = r0 + warp + 8 * (j + u);
+                if (r < n) rowpart[(size_t)blockIdx.x * H + (r - r0)] = sr[u];
+            }
     }
 #pragma unroll
     for (int k = 0; k < KC; ++k) {
@@ -616,6 +623,22 @@ static void symv_reduce_launch(Ctx* ctx, const DMatrix& W, const GemvPlan& plan,
                (const int*)plan.tbase.p, (const double*)plan.rowpart.p, (const double*)plan.colpart.p, y, done);
     ::sbg::count_launch();
     SBG_LAUNCH_CHECK();
+}
+
+// algorithmic DRAM bytes of one matvec with this plan: the matrix entries it reads, x, y and
+// (symmetric form) its partial sums written and read back once
+double gemv_bytes(const GemvPlan& plan)
+{
+    const double n = plan.n, ld = plan.ld, e = sizeof(double);
+    if (!plan.sym) return e * n * n + 2 * e * n;  // (the zero padding of each row is not counted)
+    double w = 0.0, colp = 0.0;
+    for (int I = 0; I < plan.nstrips; ++I) {
+        const double rows = std::min(plan.H, plan.n - I * plan.H);
+        w += rows * (n - (double)I * plan.H);
+        colp += std::max(0.0, ld - (double)(I + 1) * plan.H);
+    }
+    const double rowp = (double)plan.ntiles * plan.H;
+    return e * w + 2 * e * n + 2 * e * (rowp + colp);
 }
 
 void gemv_plan(Ctx* ctx, int n, int ld, GemvPlan& plan)

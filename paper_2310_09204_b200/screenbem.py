@@ -145,6 +145,7 @@ SIGNATURES = {
     "sbg_memcpy_d2h": (C.c_int, [vp, vp, vp, C.c_longlong]),
     "sbg_pcg_device": (C.c_int, [vp, vp, vp, vp, C.c_double, C.c_int, vp, C.POINTER(PcgReportC)]),
     "sbg_matvec_device": (C.c_int, [vp, vp, vp, vp, C.c_int]),
+    "sbg_matvec_bytes": (C.c_int, [vp, vp, C.POINTER(C.c_double)]),
     "sbg_apply_preconditioner_device": (C.c_int, [vp, vp, vp, vp, C.c_int]),
     "sbg_l2_flush": (C.c_int, [vp]),
     "sbg_pool_stats": (C.c_int, [vp, C.POINTER(C.c_longlong), C.POINTER(C.c_longlong)]),
