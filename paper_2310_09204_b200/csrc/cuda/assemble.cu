@@ -71,6 +71,9 @@ RuleDims rule_dims(int far_order)
 // rules padded with zero-weight points at the centroid (their terms add exact zeros)
 __constant__ double c_far_u[NF_MAX], c_far_v[NF_MAX], c_far_w[NF_MAX];
 __constant__ double c_near_u[NN_MAX], c_near_v[NN_MAX], c_near_w[NN_MAX];
+// 1 / w^2 per rule point (0 for the zero-weight padding): the y points are staged scaled by
+// it, so rsqrt of the scaled squared distance is already w_j / |x - y| (rsqrt_acc)
+__constant__ double c_far_s[NF_MAX], c_near_s[NN_MAX];
 // composed split4 maps: for every child path of depth <= 5 (index (4^d-1)/3 + base-4 digits),
 // the barycentric weights (x32, exact dyadics) of the leaf vertices on the root vertices
 constexpr int NPATH = 1365;
@@ -208,16 +211,26 @@ __device__ __forceinline__ void far_xpoints(const double* t, const double* o, in
     }
 }
 
+// the staged y point of rule point j, scaled by s_j = 1/w_j^2: (s y, s |y|^2), so that
+// s_j |x - y|^2 = s_j |x|^2 + s |y|^2 - 2 x.(s y) costs the same four instructions
+__device__ __forceinline__ double4 scaled_ypoint(double y0, double y1, double y2, double sj)
+{
+    if (sj == 0.0) return make_double4(0.0, 0.0, 0.0, kPadR2);
+    return make_double4(sj * y0, sj * y1, sj * y2, sj * fma(y0, y0, fma(y1, y1, y2 * y2)));
+}
+
 __device__ __forceinline__ double4 far_ypoint(const double* s, const double* o, int j)
 {
     const double y0 = fma(c_far_v[j], s[6] - s[0], fma(c_far_u[j], s[3] - s[0], s[0] - o[0]));
     const double y1 = fma(c_far_v[j], s[7] - s[1], fma(c_far_u[j], s[4] - s[1], s[1] - o[1]));
     const double y2 = fma(c_far_v[j], s[8] - s[2], fma(c_far_u[j], s[5] - s[2], s[2] - o[2]));
-    return make_double4(y0, y1, y2, fma(y0, y0, fma(y1, y1, y2 * y2)));
+    return scaled_ypoint(y0, y1, y2, c_far_s[j]);
 }
 
 // sum_{q in pass} w_{4 pass + q} sum_j w_j / |x_q - y_j|  (16 y-points x 4 x-points); one
-// accumulator per x point, so the four evaluations per y point are independent chains
+// accumulator per x point, so the four evaluations per y point are independent chains;
+// w_j is folded into the staged y point (far_ypoint, rsqrt_acc): 9 FP64 instructions and one
+// MUFU per evaluation
 template <int NFP>
 __device__ __forceinline__ double far_pass_sum(const XPts& X, const double4* __restrict__ Y, int pass)
 {
@@ -227,11 +240,11 @@ __device__ __forceinline__ double far_pass_sum(const XPts& X, const double4* __r
 #pragma unroll 2
     for (int j = 0; j < NFP; ++j) {
         const double4 y = Y[j];
-        const double wj = c_far_w[j];
+        const double sj = c_far_s[j];
 #pragma unroll
         for (int q = 0; q < FAR_PASS; ++q) {
-            const double r2 = fma(X.m2x[q], y.x, fma(X.m2y[q], y.y, fma(X.m2z[q], y.z, X.x2[q] + y.w)));
-            a[q] = fma(wj, rsqrt_fast(r2), a[q]);
+            const double r2 = fma(X.m2x[q], y.x, fma(X.m2y[q], y.y, fma(X.m2z[q], y.z, fma(X.x2[q], sj, y.w))));
+            a[q] = rsqrt_acc(r2, a[q]);
         }
     }
     double acc = 0.0;
@@ -603,7 +616,7 @@ __global__ void __launch_bounds__(NEAR_LEAF_THREADS, 2) k_near_leaves(const Near
                 const double yx = fma(c_near_v[j], e2x, fma(c_near_u[j], e1x, bx));
                 const double yy = fma(c_near_v[j], e2y, fma(c_near_u[j], e1y, by));
                 const double yz = fma(c_near_v[j], e2z, fma(c_near_u[j], e1z, bz));
-                Ys[j] = make_double4(yx, yy, yz, fma(yx, yx, fma(yy, yy, yz * yz)));
+                Ys[j] = scaled_ypoint(yx, yy, yz, c_near_s[j]);
             }
             f1x = t[3] - t[0], f1y = t[4] - t[1], f1z = t[5] - t[2];
             f2x = t[6] - t[0], f2y = t[7] - t[1], f2z = t[8] - t[2];
@@ -632,11 +645,11 @@ __global__ void __launch_bounds__(NEAR_LEAF_THREADS, 2) k_near_leaves(const Near
 #pragma unroll 3
                 for (int j = j0; j < j1; ++j) {
                     const double4 y = Ys[j];
-                    const double wj = c_near_w[j];
+                    const double sj = c_near_s[j];
 #pragma unroll
                     for (int r = 0; r < NEAR_XP; ++r) {
-                        const double r2 = fma(mx[r], y.x, fma(my[r], y.y, fma(mz[r], y.z, x2[r] + y.w)));
-                        a[r] = fma(wj, rsqrt_fast(r2), a[r]);
+                        const double r2 = fma(mx[r], y.x, fma(my[r], y.y, fma(mz[r], y.z, fma(x2[r], sj, y.w))));
+                        a[r] = rsqrt_acc(r2, a[r]);
                     }
                 }
 #pragma unroll
@@ -702,7 +715,7 @@ __global__ void __launch_bounds__(NEAR_G_THREADS) k_near_leaves_g(const NearNode
                 const double yx = fma(c_near_v[j], e2x, fma(c_near_u[j], e1x, bx));
                 const double yy = fma(c_near_v[j], e2y, fma(c_near_u[j], e1y, by));
                 const double yz = fma(c_near_v[j], e2z, fma(c_near_u[j], e1z, bz));
-                Ys[j] = make_double4(yx, yy, yz, fma(yx, yx, fma(yy, yy, yz * yz)));
+                Ys[j] = scaled_ypoint(yx, yy, yz, c_near_s[j]);
             }
             f1x = t[3] - t[0], f1y = t[4] - t[1], f1z = t[5] - t[2];
             f2x = t[6] - t[0], f2y = t[7] - t[1], f2z = t[8] - t[2];
@@ -727,11 +740,11 @@ __global__ void __launch_bounds__(NEAR_G_THREADS) k_near_leaves_g(const NearNode
 #pragma unroll 2
                 for (int j = 0; j < NNP; ++j) {
                     const double4 y = Ys[j];
-                    const double wj = c_near_w[j];
+                    const double sj = c_near_s[j];
 #pragma unroll
                     for (int r = 0; r < NEAR_XP; ++r) {
-                        const double r2 = fma(mx[r], y.x, fma(my[r], y.y, fma(mz[r], y.z, x2[r] + y.w)));
-                        a[r] = fma(wj, rsqrt_fast(r2), a[r]);
+                        const double r2 = fma(mx[r], y.x, fma(my[r], y.y, fma(mz[r], y.z, fma(x2[r], sj, y.w))));
+                        a[r] = rsqrt_acc(r2, a[r]);
                     }
                 }
 #pragma unroll
@@ -1026,7 +1039,7 @@ RuleDims upload_rules(Ctx* ctx, const QuadCfg& cfg)
         std::lock_guard<std::mutex> lock(mu);
         auto& slot = cache[R.far_order];
         if (!slot) {
-            auto buf = std::make_shared<std::vector<double>>(3 * NF_MAX + 3 * NN_MAX, 0.0);
+            auto buf = std::make_shared<std::vector<double>>(4 * NF_MAX + 4 * NN_MAX, 0.0);
             const TriangleRule far = triangle_rule(R.far_order), nr = triangle_rule(R.far_order + 2);
             for (int i = 0; i < NF_MAX; ++i) {
                 const bool real = i < R.nf;
@@ -1041,6 +1054,19 @@ RuleDims upload_rules(Ctx* ctx, const QuadCfg& cfg)
                 nb[NN_MAX + i] = real ? nr.v[i] : 1.0 / 3.0;
                 nb[2 * NN_MAX + i] = real ? nr.w[i] : 0.0;
             }
+            // 1 / w^2 (0 for padding); the collapsed Gauss rules have positive weights only
+            double* fs = buf->data() + 3 * NF_MAX + 3 * NN_MAX;
+            double* ns = fs + NF_MAX;
+            for (int i = 0; i < NF_MAX; ++i) {
+                const double w = (*buf)[2 * NF_MAX + i];
+                if (i < R.nf && !(w > 0.0)) throw std::logic_error("far rule: non-positive weight");
+                fs[i] = i < R.nf ? 1.0 / (w * w) : 0.0;
+            }
+            for (int i = 0; i < NN_MAX; ++i) {
+                const double w = nb[2 * NN_MAX + i];
+                if (i < R.nn && !(w > 0.0)) throw std::logic_error("near rule: non-positive weight");
+                ns[i] = i < R.nn ? 1.0 / (w * w) : 0.0;
+            }
             slot = buf;
         }
         rules = slot;
@@ -1054,6 +1080,9 @@ RuleDims upload_rules(Ctx* ctx, const QuadCfg& cfg)
     SBG_CUDA(cudaMemcpyToSymbolAsync(c_near_u, rb, NN_MAX * sizeof(double), 0, cudaMemcpyHostToDevice, s));
     SBG_CUDA(cudaMemcpyToSymbolAsync(c_near_v, rb + NN_MAX, NN_MAX * sizeof(double), 0, cudaMemcpyHostToDevice, s));
     SBG_CUDA(cudaMemcpyToSymbolAsync(c_near_w, rb + 2 * NN_MAX, NN_MAX * sizeof(double), 0, cudaMemcpyHostToDevice, s));
+    rb += 3 * NN_MAX;
+    SBG_CUDA(cudaMemcpyToSymbolAsync(c_far_s, rb, NF_MAX * sizeof(double), 0, cudaMemcpyHostToDevice, s));
+    SBG_CUDA(cudaMemcpyToSymbolAsync(c_near_s, rb + NF_MAX, NN_MAX * sizeof(double), 0, cudaMemcpyHostToDevice, s));
     // composed split4 maps (quadrature.hpp:222-229 child order), weights x32
     static const std::vector<unsigned char> paths = [] {
         std::vector<unsigned char> paths(NPATH * 9);

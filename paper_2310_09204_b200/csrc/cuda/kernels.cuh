@@ -37,6 +37,22 @@ __device__ __forceinline__ double rsqrt_fast(double r2)
     return fma(y, e * c, y);                    // y (1 + e/2 + 3e^2/8)
 }
 
+// acc + w / |x - y| from r2s = |x - y|^2 / w^2 (the rule weight folded into the squared
+// distance, w > 0): rsqrt seed and one 3rd-order Newton step, y (1 + e (1/2 + 3e/8)) with
+// e = 1 - r2s y^2 — five FP64 instructions after the seed, the weight multiply included
+__device__ __forceinline__ double rsqrt_acc(double r2s, double acc)
+{
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(r2s));
+    const double h = r2s * y;
+    const double e = fma(-h, y, 1.0);
+    const double c = fma(0.375, e, 0.5);
+    return fma(y, fma(e, c, 1.0), acc);
+}
+// a padded (zero-weight) rule point: s = 0 and this constant term make r2s huge, so its
+// contribution (~1e-150) vanishes below the rounding of any accumulated sum
+constexpr double kPadR2 = 1e300;
+
 double fp64_peak_tflops(Ctx* ctx);
 void add_launches(long long k);  // launch bookkeeping for graph-replayed kernels
 bool pcg_graph_enabled();        // PCG loop as one graph with a device-side while node (SBG_PCG_GRAPH=0: off)
