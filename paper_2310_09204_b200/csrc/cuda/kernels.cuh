@@ -121,6 +121,8 @@ struct PcgFused {
     bool has_gate;
 };
 bool prec_apply_pcg(Ctx* ctx, Prec* p, const PcgFused& f);
+struct PrecView;
+bool prec_view(const Prec* p, PrecView& v);  // inverse mode with compact inverses only
 void prec_block_diag(Ctx* ctx, Prec* p, int which, std::vector<double>& diag);
 double prec_factor_bytes(const Prec* p);  // sum n_b^2 * 8 (roofline bookkeeping)
 void prec_materialize(Ctx* ctx, Prec* p, DMatrix& M);  // schwarz.hpp:142-148

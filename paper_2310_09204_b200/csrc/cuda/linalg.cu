@@ -1,12 +1,14 @@
 // Dense fp64 GEMV (HBM-streaming) and the device-resident PCG loop.
 // reference: inc/pcg.hpp:33-116 (the loop), :70 (W*p — the dominant cost).
 #include <algorithm>
+#include <cstdio>
 #include <cmath>
 
 #include <random>
 
 #include "kernels.cuh"
 #include "pcg_dev.cuh"
+#include "prec_dev.cuh"
 
 namespace sbg {
 
@@ -377,21 +379,16 @@ __global__ void __launch_bounds__(256) k_gemv_rows(const double* __restrict__ W,
 // PF (inside PCG): the vector is p = z + beta p_old formed on the fly (pcg.hpp:93; p itself is
 // rewritten by k_symv_alpha once every tile has read p_old), so no separate p-update launch
 template <int H, int C, bool KEEP, bool PF>
-__global__ void __launch_bounds__(256, 2) k_symv_tiles(const double* __restrict__ W, int ld, int n,
-                                                      const double* __restrict__ x, const int2* __restrict__ tiles,
-                                                      double* __restrict__ rowpart, double* __restrict__ colpart,
-                                                      const int* done, const double* __restrict__ z,
-                                                      const PcgDev* st)
+__device__ __forceinline__ void symv_tile_body(int tile, const double* __restrict__ W, int ld, int n,
+                                               const double* __restrict__ x, const int2* __restrict__ tiles,
+                                               double* __restrict__ rowpart, double* __restrict__ colpart,
+                                               const double* __restrict__ z, double beta, double (*red)[C])
 {
     static_assert(C % 64 == 0 && H % 16 == 0 && C % H == 0, "tile shape");
     constexpr int KC = C / 64, RW = H / 8;
-    __shared__ double red[8][C];
-    pdl_wait();
-    if (done && *done) return;
-    const int2 t = tiles[blockIdx.x];
+    const int2 t = tiles[tile];
     const int r0 = t.x * H, c0 = t.y * C;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const double beta = PF ? st->beta : 0.0;
     auto xv = [&](int i) { return PF ? fma(beta, __ldg(x + i), __ldg(z + i)) : __ldg(x + i); };
     double2 xj[KC], ca[KC];
     bool in[KC], off[KC];
@@ -444,7 +441,7 @@ __global__ void __launch_bounds__(256, 2) k_symv_tiles(const double* __restrict_
 #pragma unroll
             for (int u = 0; u < RP; ++u) {
                 const int r = r0 + warp + 8 * (j + u);
-                if (r < n) rowpart[(size_t)blockIdx.x * H + (r - r0)] = sr[u];
+                if (r < n) rowpart[(size_t)tile * H + (r - r0)] = sr[u];
             }
     }
 #pragma unroll
@@ -463,16 +460,29 @@ __global__ void __launch_bounds__(256, 2) k_symv_tiles(const double* __restrict_
     }
 }
 
+template <int H, int C, bool KEEP, bool PF>
+__global__ void __launch_bounds__(256, 2) k_symv_tiles(const double* __restrict__ W, int ld, int n,
+                                                      const double* __restrict__ x, const int2* __restrict__ tiles,
+                                                      double* __restrict__ rowpart, double* __restrict__ colpart,
+                                                      const int* done, const double* __restrict__ z,
+                                                      const PcgDev* st)
+{
+    __shared__ double red[8][C];
+    pdl_wait();
+    if (done && *done) return;
+    symv_tile_body<H, C, KEEP, PF>(blockIdx.x, W, ld, n, x, tiles, rowpart, colpart, z, PF ? st->beta : 0.0, red);
+}
+
 // (W x)_i for the 32 entries i = 32 blockIdx.x + lane of a 256-thread block: group g (warp g)
 // sums the strip's row partials k = g, g + 8, ... and the column partials of the strips
 // q = g, g + 8, ... above it; warp 0 adds the 8 group sums in group order (deterministic).
 // Returns the entry in warp 0 (0 elsewhere).
-__device__ __forceinline__ double symv_entry_block(int n, int H, int ld, const int* __restrict__ tbase,
+__device__ __forceinline__ double symv_entry_block(int vb, int n, int H, int ld, const int* __restrict__ tbase,
                                                    const double* __restrict__ rowpart,
                                                    const double* __restrict__ colpart, double (*sh)[33])
 {
     const int g = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int i = blockIdx.x * 32 + lane;
+    const int i = vb * 32 + lane;
     double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
     if (i < n) {
         const int I = i / H, ri = i - I * H;
@@ -506,7 +516,7 @@ __global__ void __launch_bounds__(256) k_symv_reduce(int n, int H, int ld, const
     __shared__ double sh[8][33];
     pdl_wait();
     if (done && *done) return;
-    const double v = symv_entry_block(n, H, ld, tbase, rowpart, colpart, sh);
+    const double v = symv_entry_block(blockIdx.x, n, H, ld, tbase, rowpart, colpart, sh);
     const int i = blockIdx.x * 32 + threadIdx.x;
     if (threadIdx.x < 32 && i < n) y[i] = v;
 }
@@ -523,7 +533,7 @@ __global__ void __launch_bounds__(256) k_symv_alpha(PcgDev* st, int n, int H, in
     __shared__ double red[32];
     pdl_wait();
     if (st->done) return;
-    const double y = symv_entry_block(n, H, ld, tbase, rowpart, colpart, sh);
+    const double y = symv_entry_block(blockIdx.x, n, H, ld, tbase, rowpart, colpart, sh);
     const int i = blockIdx.x * 32 + threadIdx.x;
     double v = 0.0;
     if (threadIdx.x < 32 && i < n) {
@@ -544,6 +554,221 @@ __global__ void __launch_bounds__(256) k_symv_alpha(PcgDev* st, int n, int H, in
             return;
         }
         st->alpha = st->rz / pwp;
+    }
+}
+
+// ---------------------------------------------------------------- persistent PCG
+// The whole PCG loop (pcg.hpp:69-93) as one cooperative kernel for systems whose symmetric W,
+// block inverses and vectors stay in L2 (n <= kPersistMaxN): every CTA runs the iterations,
+// with a grid barrier between the phases — (1) the symmetric-form tiles of W p (p = z + beta p
+// formed on the fly), (2) Wp, p and p.Wp, (3) the update and gather of the fused apply,
+// (4) the block-inverse GEMV, (5) the scatter and r.z — instead of five launches per iteration.
+// Every CTA sums the same per-CTA partials in the same order, so alpha, beta and the stopping
+// decision are computed identically everywhere without a further barrier (deterministic).
+constexpr int kPersistMaxN = 8000;
+constexpr int kHistPre = 256;  // history entries returned with the state (more: a second copy)
+
+// grid barrier among the co-resident CTAs of a cooperative launch: the k-th barrier waits
+// for k * gridDim.x arrivals on a counter zeroed before the launch
+__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned& target)
+{
+    __syncthreads();
+    target += gridDim.x;
+    if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(bar, 1u);
+        unsigned v;
+        do {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+        } while (v < target);
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+struct PcgPersistArgs {
+    PcgDev* st;
+    const double* W;
+    int ld, n;
+    double *x, *r, *rn, *p, *Wp, *z;
+    const int2* tiles;
+    int ntiles;
+    const int* tbase;
+    double *rowpart, *colpart;
+    PrecView V;
+    double *hist, *alphas, *betas;
+    double* part;  // 2 x gridDim.x per-CTA partial sums
+    unsigned* bar;
+    unsigned long long* trace;  // SBG_PCG_TRACE: CTA 0's phase timestamps (globaltimer, ns), 8 per iteration
+};
+
+__device__ __forceinline__ void trace_mark(unsigned long long* trace, int it, int k)
+{
+    if (trace && blockIdx.x == 0 && threadIdx.x == 0 && it < 64) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        trace[8 * it + k] = t;
+    }
+}
+
+// the fixed-order sum of the per-CTA partials, in every thread of every CTA
+__device__ __forceinline__ double grid_total(const double* part, int count, double* sred, double* bcast)
+{
+    const double t = sum_partials_block(part, count, sred);
+    if (threadIdx.x == 0) *bcast = t;
+    __syncthreads();
+    const double v = *bcast;
+    __syncthreads();
+    return v;
+}
+
+__global__ void __launch_bounds__(256, 2) k_pcg_persistent(PcgPersistArgs A)
+{
+    __shared__ double red[8][256];
+    __shared__ double sh33[8][33];
+    __shared__ double sred[32];
+    __shared__ double bcast;
+    unsigned target = 0;
+    PcgDev* st = A.st;
+    const PrecView& V = A.V;
+    const int G = gridDim.x, nvb = (A.n + 31) / 32;
+    const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
+    // loop state, identical in every CTA
+    double rz = 0.0, beta = 0.0, alpha = 0.0, r0 = 0.0;
+    const double tol = st->tol;
+    int it = st->it, done = st->done, converged = st->converged, error = st->error;
+    const int maxit = st->maxit;
+    {
+        // initial apply z = M r and r.z (pcg.hpp:45-67; k_pcg_init): the fused phases with
+        // alpha = 0 (x, p and Wp are zero: rn = r, x unchanged); p = z + 0 p forms in phase (1)
+        for (int vb = blockIdx.x; vb < V.dof_blocks + V.nc; vb += G) {
+            prec_gather_upd_body(vb, 0.0, A.x, A.r, A.rn, A.p, A.Wp, A.n, V.pos, V.loc, V.Rc_ptr, V.Rc_row, V.Rc_val,
+                                 V.nc, V.loc_c, V.dof_blocks, &red[0][0]);
+            __syncthreads();
+        }
+        grid_barrier(A.bar, target);
+        for (int t = blockIdx.x; t < V.ntasks; t += G)
+            block_gemv_body<true>(V.tasks[t], V.nbv, V.ldmv, V.locv, V.Moff, V.Mc, V.loc, V.locy);
+        grid_barrier(A.bar, target);
+        double acc = 0.0;
+        for (int vb = blockIdx.x; vb < V.dof_blocks; vb += G) {
+            double v = prec_scatter_body(vb, V.locy, V.pos, A.n, V.Rr_ptr, V.Rr_col, V.Rr_val, V.y_c, A.z, A.r, A.rn);
+            v = block_sum(v, sred);
+            if (threadIdx.x == 0) acc += v;
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) A.part[G + blockIdx.x] = acc;
+        grid_barrier(A.bar, target);
+        rz = grid_total(A.part + G, G, sred, &bcast);
+        beta = 0.0;
+        if (rz < 0) {
+            error = 2;
+            done = 1;
+        } else {
+            const double rr = sqrt(fmax(rz, 0.0));
+            if (lead) {
+                st->r0 = rr;
+                A.hist[0] = rr;
+            }
+            r0 = rr;
+            if (rr == 0.0) {
+                converged = 1;
+                done = 1;
+            }
+            if (maxit <= 0) done = 1;
+        }
+    }
+    while (!done) {
+        trace_mark(A.trace, it, 0);
+        // (1) W p from the upper triangle
+        for (int t = blockIdx.x; t < A.ntiles; t += G) {
+            symv_tile_body<64, 256, true, true>(t, A.W, A.ld, A.n, A.p, A.tiles, A.rowpart, A.colpart, A.z, beta, red);
+            __syncthreads();
+        }
+        trace_mark(A.trace, it, 1);
+        grid_barrier(A.bar, target);
+        trace_mark(A.trace, it, 2);
+        // (2) Wp, p = z + beta p, p.Wp
+        double acc = 0.0;
+        for (int vb = blockIdx.x; vb < nvb; vb += G) {
+            const double y = symv_entry_block(vb, A.n, 64, A.ld, A.tbase, A.rowpart, A.colpart, sh33);
+            const int i = vb * 32 + threadIdx.x;
+            double v = 0.0;
+            if (threadIdx.x < 32 && i < A.n) {
+                const double pn = fma(beta, A.p[i], A.z[i]);
+                A.p[i] = pn;
+                A.Wp[i] = y;
+                v = pn * y;
+            }
+            v = block_sum(v, sred);
+            if (threadIdx.x == 0) acc += v;
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) A.part[blockIdx.x] = acc;
+        grid_barrier(A.bar, target);
+        const double pwp = grid_total(A.part, G, sred, &bcast);
+        if (pwp <= 0) {  // W not positive definite (pcg.hpp:72)
+            error = 1;
+            done = 1;
+            break;
+        }
+        alpha = rz / pwp;
+        trace_mark(A.trace, it, 3);
+        // (3) x += alpha p, r - alpha Wp gathered into the blocks, coarse restriction
+        for (int vb = blockIdx.x; vb < V.dof_blocks + V.nc; vb += G) {
+            prec_gather_upd_body(vb, alpha, A.x, A.r, A.rn, A.p, A.Wp, A.n, V.pos, V.loc, V.Rc_ptr, V.Rc_row, V.Rc_val,
+                                 V.nc, V.loc_c, V.dof_blocks, &red[0][0]);
+            __syncthreads();
+        }
+        grid_barrier(A.bar, target);
+        trace_mark(A.trace, it, 4);
+        // (4) block inverses (schwarz.hpp:121-140)
+        for (int t = blockIdx.x; t < V.ntasks; t += G)
+            block_gemv_body<true>(V.tasks[t], V.nbv, V.ldmv, V.locv, V.Moff, V.Mc, V.loc, V.locy);
+        grid_barrier(A.bar, target);
+        trace_mark(A.trace, it, 5);
+        // (5) z, r, r.z
+        acc = 0.0;
+        for (int vb = blockIdx.x; vb < V.dof_blocks; vb += G) {
+            double v = prec_scatter_body(vb, V.locy, V.pos, A.n, V.Rr_ptr, V.Rr_col, V.Rr_val, V.y_c, A.z, A.r, A.rn);
+            v = block_sum(v, sred);
+            if (threadIdx.x == 0) acc += v;
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) A.part[G + blockIdx.x] = acc;
+        grid_barrier(A.bar, target);
+        const double rz_new = grid_total(A.part + G, G, sred, &bcast);
+        trace_mark(A.trace, it, 6);
+        // history, beta, stopping test (pcg_finish_rz, pcg.hpp:76-93)
+        if (rz_new < 0) {
+            error = 2;
+            done = 1;
+            break;
+        }
+        if (lead) A.alphas[it] = alpha;
+        ++it;
+        const double res = sqrt(fmax(rz_new, 0.0));
+        beta = rz_new / rz;
+        if (lead) {
+            A.hist[it] = res;
+            A.betas[it - 1] = beta;
+        }
+        rz = rz_new;
+        if (res <= tol * r0) {
+            converged = 1;
+            done = 1;
+        } else if (it >= maxit) {
+            done = 1;
+        }
+    }
+    if (lead) {
+        st->it = it;
+        st->rz = rz;
+        st->alpha = alpha;
+        st->beta = beta;
+        st->done = done;
+        st->converged = converged;
+        st->error = error;
     }
 }
 
@@ -786,7 +1011,14 @@ struct PcgWork {
     DBuf<double> ebuf, energy;  // energy history: e and exact (2 ld), per-iteration values (cap)
     DBuf<PcgDev> st;
     GemvPlan plan;
+    GemvPlan splan;             // symmetric-form plan of the persistent kernel (any n)
+    DBuf<double> ppart;         // its per-CTA partials
+    DBuf<unsigned> bar;         // its grid-barrier counter
+    DBuf<unsigned long long> trace;  // SBG_PCG_TRACE phase timestamps
     PcgDev* hs = nullptr;
+    PcgDev* hs0 = nullptr;  // page-locked initial state record
+    double* hh = nullptr;  // page-locked: the first kHistPre history, alpha and beta entries
+    double* hx = nullptr;  // page-locked right-hand side / solution staging (ld)
     // the whole iteration loop as one graph (a device-side while node), per (W, prec)
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
@@ -807,6 +1039,9 @@ struct PcgWork {
     {
         drop_graph();
         if (hs) cudaFreeHost(hs);
+        if (hh) cudaFreeHost(hh);
+        if (hs0) cudaFreeHost(hs0);
+        if (hx) cudaFreeHost(hx);
     }
 };
 
@@ -828,6 +1063,9 @@ static PcgWork& pcg_work(Ctx* ctx, const DMatrix& W, int maxit)
         SBG_CUDA(cudaMemsetAsync(fresh->xbuf.p, 0, (size_t)W.ld * sizeof(double), ctx->stream));
         gemv_plan(ctx, W.n, W.ld, fresh->plan);
         SBG_CUDA(cudaMallocHost(&fresh->hs, sizeof(PcgDev)));
+        SBG_CUDA(cudaMallocHost(&fresh->hh, 3 * kHistPre * sizeof(double)));
+        SBG_CUDA(cudaMallocHost(&fresh->hs0, sizeof(PcgDev)));
+        SBG_CUDA(cudaMallocHost(&fresh->hx, (size_t)W.ld * sizeof(double)));
         ctx->pcg_ws = fresh;
         w = fresh.get();
     }
@@ -867,6 +1105,31 @@ static bool l2_window(Ctx* ctx, const DMatrix& W, bool sym, cudaAccessPolicyWind
     return true;
 }
 
+// SBG_PCG_PERSIST=0 disables the persistent form (the graph form then runs every size)
+static bool pcg_persist_enabled()
+{
+    static const bool on = [] {
+        const char* e = getenv("SBG_PCG_PERSIST");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
+// co-resident CTAs of k_pcg_persistent on this device (0: no cooperative launch)
+static int persist_grid(Ctx* ctx)
+{
+    static int grid = -1;
+    if (grid < 0) {
+        int coop = 0, per_sm = 0;
+        SBG_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, ctx->device));
+        SBG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pcg_persistent, 256, 0));
+        grid = coop ? std::min(per_sm, 2) * ctx->sm_count : 0;
+        if (const char* e = getenv("SBG_PCG_PERSIST_GRID"))  // (tuning)
+            grid = std::max(1, std::min(grid, atoi(e)));
+    }
+    return grid;
+}
+
 // reference: inc/pcg.hpp:33-116.  All vectors and scalars stay on the device;
 // the host enqueues iterations in growing batches and reads back one small
 // state record per batch (iterations past convergence are no-op launches).
@@ -900,13 +1163,20 @@ void pcg_run(Ctx* ctx, const DMatrix& W, Prec* prec, const double* rhs, double* 
     double* rn = Wp + len;  // the fused apply's new residual (copied back into r)
     double* z = prec ? zbuf : r;  // no preconditioner: z = r (pcg.hpp:45-47)
     cudaAccessPolicyWindow keep_win{};
-    const bool keep_W = !rows && pcg_graph_enabled() && l2_window(ctx, W, w.plan.sym, keep_win);  // W held in L2 (graph form)
-    SBG_CUDA(cudaMemcpyAsync(r, rhs, n * sizeof(double), on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
+    bool keep_W = !rows && pcg_graph_enabled() && l2_window(ctx, W, w.plan.sym, keep_win);  // W held in L2 (graph form)
+    // host vectors and the state record go through page-locked staging (no driver staging copies)
+    if (on_device) {
+        SBG_CUDA(cudaMemcpyAsync(r, rhs, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    } else {
+        std::copy(rhs, rhs + n, w.hx);
+        SBG_CUDA(cudaMemcpyAsync(r, w.hx, n * sizeof(double), cudaMemcpyHostToDevice, s));
+    }
     const int nb = (n + 255) / 256;
     PcgDev h{};
     h.tol = tol;
     h.maxit = maxit;
-    SBG_CUDA(cudaMemcpyAsync(w.st.p, &h, sizeof(h), cudaMemcpyHostToDevice, s));
+    *w.hs0 = h;
+    SBG_CUDA(cudaMemcpyAsync(w.st.p, w.hs0, sizeof(h), cudaMemcpyHostToDevice, s));
     const int* done = &w.st.p->done;
     // energy error history (pcg.hpp:50-53, 59, 82): e = x - exact, sqrt(e.We) after every
     // iteration's update and for x0 = 0 — one extra matvec per iteration, as in the reference
@@ -940,13 +1210,45 @@ void pcg_run(Ctx* ctx, const DMatrix& W, Prec* prec, const double* rhs, double* 
         count_launch();
         SBG_LAUNCH_CHECK();
     };
+    // persistent form (systems that stay in L2): the whole solve in one cooperative launch
+    PrecView pv;
+    const bool persist = n > 0 && n <= kPersistMaxN && !rows && !exact && prec && ctx->matvec_form == 0 &&
+                         pcg_persist_enabled() && prec_view(prec, pv) && persist_grid(ctx) > 0;
     if (exact) enqueue_energy(0, 0);
-    if (n > 0) {
+    if (persist) {
+        const int G = persist_grid(ctx);
+        if (!w.splan.sym) symv_plan(ctx, n, W.ld, w.splan);
+        if ((int)w.ppart.n < 2 * G) w.ppart.alloc(2 * (size_t)G);
+        if (!w.bar.n) w.bar.alloc(1);
+        SBG_CUDA(cudaMemsetAsync(w.bar.p, 0, sizeof(unsigned), s));
+        static const bool tracing = getenv("SBG_PCG_TRACE") != nullptr;
+        if (tracing && !w.trace.n) w.trace.alloc(8 * 64);
+        PcgPersistArgs A{w.st.p, W.a.p, W.ld, n, x, r, rn, p, Wp, z, w.splan.tiles.p, w.splan.ntiles,
+                         w.splan.tbase.p, w.splan.rowpart.p, w.splan.colpart.p, pv, w.hist.p, w.alphas.p, w.betas.p,
+                         w.ppart.p, w.bar.p, tracing ? w.trace.p : nullptr};
+        // (no access-policy window: the upper triangle, the inverses and the vectors of these
+        // sizes stay in L2 anyway — measured equal or faster without one)
+        void* args[] = {&A};
+        SBG_CUDA(cudaLaunchCooperativeKernel((const void*)k_pcg_persistent, dim3(G), dim3(256), args, 0, s));
+        count_launch();
+        SBG_LAUNCH_CHECK();
+        if (tracing) {  // phase durations of the first iterations (us): tiles, barrier, alpha, gather+barrier, gemv+barrier, scatter+barrier+sum, next
+            std::vector<unsigned long long> tr(8 * 64);
+            SBG_CUDA(cudaMemcpyAsync(tr.data(), w.trace.p, tr.size() * 8, cudaMemcpyDeviceToHost, s));
+            SBG_CUDA(cudaStreamSynchronize(s));
+            for (int i = 1; i < 4; ++i) {
+                fprintf(stderr, "[pcg trace] it %d:", i);
+                for (int k = 1; k <= 6; ++k) fprintf(stderr, " %.2f", (tr[8 * i + k] - tr[8 * i + k - 1]) * 1e-3);
+                fprintf(stderr, " | iter %.2f us\n", (tr[8 * (i + 1)] - tr[8 * i]) * 1e-3);
+            }
+        }
+    }
+    if (n > 0 && !persist) {
         if (prec) prec_apply(ctx, prec, r, z, nullptr);
         k_pcg_init<<<nb, 256, 0, s>>>(w.st.p, r, z, p, n, w.partials.p, w.hist.p);
         count_launch();
         SBG_LAUNCH_CHECK();
-    } else {
+    } else if (!persist) {
         h.converged = 1;
         h.done = 1;
         SBG_CUDA(cudaMemcpyAsync(w.st.p, &h, sizeof(h), cudaMemcpyHostToDevice, s));
@@ -1028,7 +1330,8 @@ void pcg_run(Ctx* ctx, const DMatrix& W, Prec* prec, const double* rhs, double* 
         return gated;
     };
     // the exchange is a host call; the energy history (test path) runs host-driven too
-    const bool graph = n > 0 && pcg_graph_enabled() && !rows && !exact;
+    const bool graph = !persist && n > 0 && pcg_graph_enabled() && !rows && !exact;
+    keep_W = keep_W && graph;
     if (graph) {
         // graph form: [gate] -> while(handle) { iteration ; gate } — the loop runs on the device
         // with no host round trips and no launches past convergence
@@ -1116,12 +1419,24 @@ void pcg_run(Ctx* ctx, const DMatrix& W, Prec* prec, const double* rhs, double* 
             w.gP = prec ? prec_uid(prec) : 0;
         }
         SBG_CUDA(cudaGraphLaunch(w.exec, s));
-        SBG_CUDA(cudaMemcpyAsync(w.hs, w.st.p, sizeof(PcgDev), cudaMemcpyDeviceToHost, s));
-        SBG_CUDA(cudaStreamSynchronize(s));
-        add_launches((long long)w.kernels_per_iter * w.hs->it + 1 + (w.body_gate ? w.hs->it : 0));  // + gates
     }
-    int batch = 4, enqueued = graph ? maxit : 0;
-    while (true) {
+    // the device-looped forms (graph, persistent) come back in one round trip: the state, the
+    // first kHistPre history / alpha / beta entries (page-locked staging) and x
+    const bool device_loop = graph || persist;
+    const int pre = std::min(kHistPre, w.cap);
+    if (device_loop) {
+        SBG_CUDA(cudaMemcpyAsync(w.hs, w.st.p, sizeof(PcgDev), cudaMemcpyDeviceToHost, s));
+        SBG_CUDA(cudaMemcpyAsync(w.hh, w.hist.p, pre * sizeof(double), cudaMemcpyDeviceToHost, s));
+        SBG_CUDA(cudaMemcpyAsync(w.hh + kHistPre, w.alphas.p, pre * sizeof(double), cudaMemcpyDeviceToHost, s));
+        SBG_CUDA(cudaMemcpyAsync(w.hh + 2 * kHistPre, w.betas.p, pre * sizeof(double), cudaMemcpyDeviceToHost, s));
+        SBG_CUDA(cudaMemcpyAsync(on_device ? x_out : w.hx, x, n * sizeof(double),
+                                 on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s));
+        SBG_CUDA(cudaStreamSynchronize(s));
+        if (!on_device) std::copy(w.hx, w.hx + n, x_out);
+        if (graph) add_launches((long long)w.kernels_per_iter * w.hs->it + 1 + (w.body_gate ? w.hs->it : 0));  // + gates
+    }
+    int batch = 4, enqueued = device_loop ? maxit : 0;
+    while (!device_loop) {
         SBG_CUDA(cudaMemcpyAsync(w.hs, w.st.p, sizeof(PcgDev), cudaMemcpyDeviceToHost, s));
         SBG_CUDA(cudaStreamSynchronize(s));
         int stop = (w.hs->done || enqueued >= maxit) ? 1 : 0;
@@ -1136,10 +1451,7 @@ void pcg_run(Ctx* ctx, const DMatrix& W, Prec* prec, const double* rhs, double* 
         enqueued += todo;
         batch = std::min(batch * 2, 64);
     }
-    {
-        cudaAccessPolicyWindow win{};
-        if (l2_window(ctx, W, w.plan.sym, win)) SBG_CUDA(cudaCtxResetPersistingL2Cache());  // give L2 back to what follows
-    }
+    if (keep_W) SBG_CUDA(cudaCtxResetPersistingL2Cache());  // give L2 back to what follows
     const PcgDev fin = *w.hs;
     if (fin.error == 1) throw NumericalError("pcg: matrix is not positive definite");
     if (fin.error == 2) throw NumericalError("pcg: preconditioner is not positive definite");
@@ -1148,6 +1460,13 @@ void pcg_run(Ctx* ctx, const DMatrix& W, Prec* prec, const double* rhs, double* 
     out.history.assign(fin.it + 1, 0.0);
     out.alphas.assign(fin.it, 0.0);
     out.betas.assign(fin.it, 0.0);
+    if (device_loop && fin.it + 1 <= pre) {  // everything already on the host
+        std::copy(w.hh, w.hh + fin.it + 1, out.history.begin());
+        std::copy(w.hh + kHistPre, w.hh + kHistPre + fin.it, out.alphas.begin());
+        std::copy(w.hh + 2 * kHistPre, w.hh + 2 * kHistPre + fin.it, out.betas.begin());
+        out.kappa = lanczos_kappa(out.alphas, out.betas);
+        return;
+    }
     if (n > 0) {
         SBG_CUDA(cudaMemcpyAsync(out.history.data(), w.hist.p, (fin.it + 1) * sizeof(double), cudaMemcpyDeviceToHost, s));
         if (fin.it) {

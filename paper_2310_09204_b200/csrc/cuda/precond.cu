@@ -23,6 +23,7 @@
 
 #include "kernels.cuh"
 #include "pcg_dev.cuh"
+#include "prec_dev.cuh"
 
 namespace sbg {
 
@@ -645,45 +646,7 @@ __global__ void __launch_bounds__(256) k_block_gemv(const int2* __restrict__ tas
 {
     pdl_wait();
     if (done && *done) return;
-    const int2 t = tasks[blockIdx.x];
-    const int b = t.x, nb = nbv[b], ldm = ldmv[b];
-    const int r = t.y + (threadIdx.x >> 5), lane = threadIdx.x & 31;
-    if (r >= nb) return;
-    const double2* x2 = reinterpret_cast<const double2*>(loc + locv[b]);  // loc rows are 64-padded (zeros)
-    const double2* row = reinterpret_cast<const double2*>(Mc + Moff[b] + (size_t)r * ldm);
-    const int half = ldm >> 1;
-    double s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    if (half > 8 * 32) {  // long rows (WB): 8 x 128-bit loads in flight per lane, serial tail
-        int c = lane;
-        for (; c + 7 * 32 < half; c += 8 * 32) {
-            double2 a[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) a[u] = __ldcs(row + c + 32 * u);
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                const double2 xv = __ldg(x2 + c + 32 * u);
-                s[u] = fma(a[u].x, xv.x, fma(a[u].y, xv.y, s[u]));
-            }
-        }
-        for (; c < half; c += 32) {
-            const double2 a = __ldcs(row + c);
-            const double2 xv = __ldg(x2 + c);
-            s[0] = fma(a.x, xv.x, fma(a.y, xv.y, s[0]));
-        }
-    } else {  // short rows (faces): one predicated chunk, every load issued before the FMAs
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-            const int c = lane + 32 * u;
-            if (c < half) {
-                const double2 a = __ldcs(row + c);
-                const double2 xv = __ldg(x2 + c);
-                s[u] = fma(a.x, xv.x, fma(a.y, xv.y, s[u]));
-            }
-        }
-    }
-    double v = ((s[0] + s[1]) + (s[2] + s[3])) + ((s[4] + s[5]) + (s[6] + s[7]));
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if (lane == 0) locy[locv[b] + r] = v;
+    block_gemv_body(tasks[blockIdx.x], nbv, ldmv, locv, Moff, Mc, loc, locy);
 }
 
 // The factored apply's two passes over Mc (X below the diagonal, X^T above, X's diagonal on
@@ -873,40 +836,11 @@ __global__ void __launch_bounds__(256) k_prec_gather_upd(const PcgDev* st, doubl
                                                          const double* __restrict__ cval, int nc,
                                                          double* __restrict__ loc_c, int dof_blocks)
 {
+    __shared__ double red[8];
     pdl_wait();
     if (st->done) return;
-    const double a = st->alpha;
-    if ((int)blockIdx.x < dof_blocks) {
-        const int d = blockIdx.x * blockDim.x + threadIdx.x;
-        if (d < n) {
-            const double rv = r[d] - a * Wp[d];
-            rn[d] = rv;
-            x[d] += a * p[d];
-            if (pos[d] >= 0) loc[pos[d]] = rv;
-        }
-        return;
-    }
-    __shared__ double red[8];
-    const int c = (int)blockIdx.x - dof_blocks;
-    if (c >= nc) return;
-    const int q0 = cptr[c], q1 = cptr[c + 1];
-    double s0 = 0.0, s1 = 0.0;
-    int q = q0 + threadIdx.x;
-    for (; q + 256 < q1; q += 2 * 256) {
-        const int i0 = crow[q], i1 = crow[q + 256];
-        s0 += cval[q] * (r[i0] - a * Wp[i0]);
-        s1 += cval[q + 256] * (r[i1] - a * Wp[i1]);
-    }
-    for (; q < q1; q += 256) s0 += cval[q] * (r[crow[q]] - a * Wp[crow[q]]);
-    double v = s0 + s1;
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double t = 0.0;
-        for (int w = 0; w < 8; ++w) t += red[w];
-        loc_c[c] = t;
-    }
+    prec_gather_upd_body(blockIdx.x, st->alpha, x, r, rn, p, Wp, n, pos, loc, cptr, crow, cval, nc, loc_c, dof_blocks,
+                         red);
 }
 
 __global__ void __launch_bounds__(256) k_prec_scatter_rz(PcgDev* st, const double* __restrict__ locy,
@@ -924,20 +858,7 @@ __global__ void __launch_bounds__(256) k_prec_scatter_rz(PcgDev* st, const doubl
         return;
     }
     __shared__ double sh[32];
-    const int d = blockIdx.x * blockDim.x + threadIdx.x;
-    double v = 0.0;
-    if (d < n) {
-        double out = pos[d] >= 0 ? locy[pos[d]] : 0.0;
-        if (rptr) {
-            double y = 0.0;
-            for (int q = rptr[d]; q < rptr[d + 1]; ++q) y += rval[q] * y_c[rcol[q]];
-            out += y;
-        }
-        z[d] = out;
-        const double rv = rn[d];
-        r[d] = rv;
-        v = rv * out;
-    }
+    double v = prec_scatter_body(blockIdx.x, locy, pos, n, rptr, rcol, rval, y_c, z, r, rn);
     v = block_sum(v, sh);
     if (last_block(v, partials, &st->counter) && threadIdx.x == 0) {
         const double rz_new = sum_partials(partials, gridDim.x);
@@ -1475,6 +1396,36 @@ bool prec_apply_pcg(Ctx* ctx, Prec* P, const PcgFused& f)
                (const double*)f.rn, f.partials, f.hist, f.alphas, f.betas, f.gate, f.has_gate ? 1 : 0);
     count_launch();
     SBG_LAUNCH_CHECK();
+    return true;
+}
+
+// device pointers of an inverse-mode preconditioner with compact block inverses (not the
+// factored or TRSV forms), for the persistent PCG kernel (linalg.cu)
+bool prec_view(const Prec* P, PrecView& V)
+{
+    if (P->mode != kPrecInverse || P->factored || P->n == 0) return false;
+    const int cb = P->coarse_block;
+    V.n = P->n;
+    V.nc = P->nc;
+    V.dof_blocks = (P->n + 255) / 256;
+    V.ntasks = (int)P->sched->gemv.size();
+    V.pos = P->pos.p;
+    V.loc = P->loc.p;
+    V.locy = P->locy.p;
+    V.Rc_ptr = P->Rc_ptr.p;
+    V.Rc_row = P->Rc_row.p;
+    V.Rc_val = P->Rc_val.p;
+    V.loc_c = cb >= 0 ? P->loc.p + P->h_loc[cb] : nullptr;
+    V.Rr_ptr = P->nc > 0 ? P->Rr_ptr.p : nullptr;
+    V.Rr_col = P->Rr_col.p;
+    V.Rr_val = P->Rr_val.p;
+    V.y_c = cb >= 0 ? P->locy.p + P->h_loc[cb] : nullptr;
+    V.tasks = P->sched->d_gemv.p;
+    V.nbv = P->d_nb.p;
+    V.ldmv = P->d_ldm.p;
+    V.locv = P->d_loc.p;
+    V.Moff = P->d_Moff.p;
+    V.Mc = P->Mc.p;
     return true;
 }
 

@@ -299,6 +299,39 @@ def test_pcg_random_spd_matches_oracle_and_lanczos(ctx):
     assert rep.kappa_estimate == pytest.approx(orep.kappa_estimate, rel=1e-4)
 
 
+@pytest.mark.parametrize("cfg", [1, 2, 3])
+def test_pcg_persistent_form_matches_graph_form(ctx, cfg):
+    """n <= 8000 with an inverse-mode preconditioner: the default pcg runs as one persistent
+    cooperative kernel (symmetric matvec, grid barriers between the phases, in-kernel initial
+    apply); the full-matrix form runs the graph loop.  Same iterations (+-1), history and
+    solution to the PCG tolerances, the Lanczos estimate to 1e-8; deterministic run to run;
+    a zero right-hand side converges at iteration 0."""
+    pair = S.make_config(cfg)
+    fine, coarse = S.inflate(pair.fine), S.inflate(pair.coarse)
+    W = S.assemble_W(fine, ctx=ctx)
+    L = S.assemble_rhs(fine, S.config_g(cfg), ctx=ctx)
+    prec = S.build_preconditioner(W, S.partition_dofs(pair, fine), S.build_prolongation(pair, coarse, fine))
+    assert ctx.matvec_form == "symmetric"
+    a = S.pcg(W, prec, L, 1e-8)
+    a2 = S.pcg(W, prec, L, 1e-8)
+    assert np.array_equal(a.solution, a2.solution) and np.array_equal(a.residual_history, a2.residual_history)
+    ctx.matvec_form = "full"
+    try:
+        b = S.pcg(W, prec, L, 1e-8)
+    finally:
+        ctx.matvec_form = "symmetric"
+    assert a.converged and b.converged and abs(a.iterations - b.iterations) <= 1
+    k = min(a.iterations, b.iterations) + 1
+    np.testing.assert_allclose(a.residual_history[:k], b.residual_history[:k], rtol=1e-9)
+    assert np.linalg.norm(a.solution - b.solution) <= 1e-8 * np.linalg.norm(b.solution)
+    assert a.kappa_estimate == pytest.approx(b.kappa_estimate, rel=1e-8)
+    z = S.pcg(W, prec, np.zeros(W.n), 1e-8)
+    assert z.iterations == 0 and z.converged and not z.solution.any()
+    # an iteration cap stops it where the graph form stops (maxit, pcg.hpp:69)
+    c = S.pcg(W, prec, L, 1e-14, 3)
+    assert c.iterations == 3 and not c.converged and len(c.residual_history) == 4
+
+
 def test_pcg_energy_error_history(ctx):
     """tests/test_pcg.cpp:85-106 on the device: random_spd(60, 9), b from mt19937(10),
     exact = direct_solve; the energy error history (pcg.hpp:50-53) decreases monotonically,
