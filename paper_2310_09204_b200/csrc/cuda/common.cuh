@@ -38,6 +38,12 @@ long long launch_count();
 // cudaFree pair costs ~2-4 ms on the B200 boxes and synchronises the device).
 void* device_alloc(size_t bytes);
 void device_free(void* p);
+// frees a block of known size: blocks of >= 64 MB are parked in a process-wide exact-size
+// cache (capped) and handed to the next allocation of the same size, so repeated solves of
+// one size (a new W, a new preconditioner while the old one is alive) do not make the
+// stream-ordered pool map gigabytes again on the host thread (context.cu)
+void device_free_sized(void* p, size_t bytes);
+void device_cache_release();  // frees every parked block
 void device_pool_init(int device);
 
 template <class T>
@@ -69,7 +75,7 @@ struct DBuf {
     }
     void release()
     {
-        if (p) device_free(p);
+        if (p) device_free_sized(p, n * sizeof(T));
         p = nullptr;
         n = 0;
     }
@@ -169,22 +175,12 @@ void set_max_dynamic_smem(void (*kernel)(KArgs...), size_t bytes)
 // Row-major with a leading dimension padded to 32 doubles (256-byte rows) so
 // every row starts 16-byte aligned for 128-bit streaming loads; the padding
 // is kept at zero.
-// Parks a large dense buffer being released in a one-slot process-wide spare, so that the
-// next n x n matrix of the same size reuses it instead of having the stream-ordered pool
-// map gigabytes again on the host thread (context.cu).
-void matrix_park(DBuf<double>& a);
-void matrix_spare_release();
-
 struct DMatrix {
     Ctx* ctx = nullptr;
     int n = 0;
     int ld = 0;
     DBuf<double> a;
     static int padded_ld(int n) { return ((n + 31) / 32) * 32; }
-    DMatrix() = default;
-    DMatrix(DMatrix&&) = default;
-    DMatrix& operator=(DMatrix&&) = default;
-    ~DMatrix() { matrix_park(a); }
 };
 
 }  // namespace sbg

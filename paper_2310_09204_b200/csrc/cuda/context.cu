@@ -5,6 +5,7 @@
 #include <cstring>
 #include <sys/mman.h>
 #include <condition_variable>
+#include <list>
 #include <mutex>
 #include <set>
 #include <tuple>
@@ -37,8 +38,42 @@ void device_pool_init(int device)
     SBG_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
 }
 
+namespace {
+constexpr size_t kCacheMin = size_t(64) << 20;   // smaller blocks come from the pool quickly
+constexpr size_t kCacheCap = size_t(16) << 30;   // bytes parked at most (oldest freed first)
+struct BlockCache {
+    std::mutex mu;
+    struct Block {
+        void* p;
+        size_t bytes;
+        int device;
+    };
+    std::list<Block> blocks;  // oldest first
+    size_t total = 0;
+    cudaEvent_t mark = nullptr;
+};
+BlockCache& block_cache()
+{
+    static BlockCache* c = new BlockCache;  // never destroyed: no CUDA calls during static teardown
+    return *c;
+}
+}  // namespace
+
 void* device_alloc(size_t bytes)
 {
+    if (bytes >= kCacheMin) {
+        int dev = 0;
+        SBG_CUDA(cudaGetDevice(&dev));
+        BlockCache& C = block_cache();
+        std::lock_guard<std::mutex> lk(C.mu);
+        for (auto it = C.blocks.begin(); it != C.blocks.end(); ++it)
+            if (it->bytes == bytes && it->device == dev) {
+                void* p = it->p;
+                C.total -= bytes;
+                C.blocks.erase(it);
+                return p;
+            }
+    }
     void* p = nullptr;
     SBG_CUDA(cudaMallocAsync(&p, bytes, 0));
     return p;
@@ -47,6 +82,55 @@ void* device_alloc(size_t bytes)
 void device_free(void* p)
 {
     if (p) cudaFreeAsync(p, 0);
+}
+
+// A parked block may still be read by work in flight on a context stream.  The context
+// streams are blocking streams: an event recorded on the legacy stream at park time begins
+// only after all their earlier work, and any work issued to them later (by the block's next
+// owner) waits for it — so the next owner is ordered after every earlier use.
+void device_free_sized(void* p, size_t bytes)
+{
+    if (!p) return;
+    if (bytes < kCacheMin) {
+        cudaFreeAsync(p, 0);
+        return;
+    }
+    int dev = 0;
+    BlockCache& C = block_cache();
+    std::lock_guard<std::mutex> lk(C.mu);
+    if (cudaGetDevice(&dev) != cudaSuccess ||
+        (!C.mark && cudaEventCreateWithFlags(&C.mark, cudaEventDisableTiming) != cudaSuccess) ||
+        cudaEventRecord(C.mark, 0) != cudaSuccess) {
+        cudaFreeAsync(p, 0);
+        return;
+    }
+    C.blocks.push_back({p, bytes, dev});
+    C.total += bytes;
+    while (C.total > kCacheCap && !C.blocks.empty()) {
+        const BlockCache::Block b = C.blocks.front();
+        C.blocks.pop_front();
+        C.total -= b.bytes;
+        int cur = 0;
+        cudaGetDevice(&cur);
+        if (b.device != cur) cudaSetDevice(b.device);
+        cudaFreeAsync(b.p, 0);
+        if (b.device != cur) cudaSetDevice(cur);
+    }
+}
+
+void device_cache_release()
+{
+    BlockCache& C = block_cache();
+    std::lock_guard<std::mutex> lk(C.mu);
+    int cur = 0;
+    cudaGetDevice(&cur);
+    for (const auto& b : C.blocks) {
+        if (b.device != cur) cudaSetDevice(b.device);
+        cudaFreeAsync(b.p, 0);
+        if (b.device != cur) cudaSetDevice(cur);
+    }
+    C.blocks.clear();
+    C.total = 0;
 }
 long long launch_count() { return g_launches.load(); }
 
@@ -122,7 +206,16 @@ Timers::~Timers()
 
 Ctx::~Ctx()
 {
-    matrix_spare_release();
+    // the cached workspaces first (their large buffers go to the block cache), then the cache
+    pcg_ws.reset();
+    dl_ws.reset();
+    near_ws.reset();
+    flush_ws.reset();
+    prec_sched.reset();
+    scratch_ws.reset();
+    sauter_ws.reset();
+    stage_ws.reset();
+    device_cache_release();
     if (aux) {
         cudaStreamSynchronize(aux);
         cudaStreamDestroy(aux);
@@ -242,64 +335,12 @@ void set_max_dynamic_smem(const void* kernel, size_t bytes)
     done.insert({kernel, dev, bytes});
 }
 
-namespace {
-constexpr size_t kParkMin = size_t(256) << 20;  // bytes: smaller buffers come from the pool quickly
-struct Spare {
-    std::mutex mu;
-    DBuf<double> buf;
-    int device = -1;
-    cudaEvent_t done = nullptr;  // recorded on the legacy stream when parked
-};
-Spare& spare()
-{
-    static Spare* s = new Spare;  // never destroyed: no CUDA calls during static teardown
-    return *s;
-}
-}  // namespace
-
-void matrix_park(DBuf<double>& a)
-{
-    if (!a.p || a.n * sizeof(double) < kParkMin) return;
-    Spare& S = spare();
-    std::lock_guard<std::mutex> lk(S.mu);
-    int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess) return;
-    if (!S.done && cudaEventCreateWithFlags(&S.done, cudaEventDisableTiming) != cudaSuccess) {
-        S.done = nullptr;
-        return;
-    }
-    // the legacy stream orders after all earlier work of the (blocking) context streams
-    if (cudaEventRecord(S.done, 0) != cudaSuccess) return;
-    S.buf = std::move(a);  // frees the previous spare, if any
-    S.device = dev;
-}
-
-// a parked buffer of exactly this many elements on this device, or an empty one
-static DBuf<double> matrix_unpark(Ctx* ctx, size_t count)
-{
-    Spare& S = spare();
-    std::lock_guard<std::mutex> lk(S.mu);
-    if (!S.buf.p || S.buf.n != count || S.device != ctx->device) return {};
-    SBG_CUDA(cudaStreamWaitEvent(ctx->stream, S.done, 0));
-    return std::move(S.buf);
-}
-
-void matrix_spare_release()
-{
-    Spare& S = spare();
-    std::lock_guard<std::mutex> lk(S.mu);
-    S.buf.release();
-}
-
 void matrix_alloc(Ctx* ctx, int n, DMatrix& M)
 {
     M.ctx = ctx;
     M.n = n;
     M.ld = DMatrix::padded_ld(n);
-    const size_t count = (size_t)n * M.ld;
-    DBuf<double> reuse = matrix_unpark(ctx, count);
-    if (reuse.p) M.a = std::move(reuse);
-    else M.a.alloc(count);
+    M.a.alloc((size_t)n * M.ld);
     if (M.a.n) SBG_CUDA(cudaMemsetAsync(M.a.p, 0, M.a.n * sizeof(double), ctx->stream));
 }
 
