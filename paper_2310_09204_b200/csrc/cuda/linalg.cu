@@ -1,6 +1,7 @@
 // Dense fp64 GEMV (HBM-streaming) and the device-resident PCG loop.
 // reference: inc/pcg.hpp:33-116 (the loop), :70 (W*p — the dominant cost).
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
 #include <cmath>
 
@@ -1151,6 +1152,14 @@ void pcg_run(Ctx* ctx, const DMatrix& W, Prec* prec, const double* rhs, double* 
         return;
     }
     TimedScope tpcg(ctx, "pcg");
+    static const bool htrace = getenv("SBG_PCG_TRACE") != nullptr;
+    const auto ht0 = std::chrono::steady_clock::now();
+    auto hmark = [&](const char* what) {
+        if (htrace)
+            fprintf(stderr, " %s=%.1f", what,
+                    std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - ht0).count());
+    };
+    if (htrace) fprintf(stderr, "[pcg host]");
     cudaStream_t s = ctx->stream;
     PcgWork& w = pcg_work(ctx, W, maxit);
     const size_t len = (size_t)W.ld;
@@ -1229,7 +1238,9 @@ void pcg_run(Ctx* ctx, const DMatrix& W, Prec* prec, const double* rhs, double* 
         // (no access-policy window: the upper triangle, the inverses and the vectors of these
         // sizes stay in L2 anyway — measured equal or faster without one)
         void* args[] = {&A};
+        hmark("pre_launch");
         SBG_CUDA(cudaLaunchCooperativeKernel((const void*)k_pcg_persistent, dim3(G), dim3(256), args, 0, s));
+        hmark("launched");
         count_launch();
         SBG_LAUNCH_CHECK();
         if (tracing) {  // phase durations of the first iterations (us): tiles, barrier, alpha, gather+barrier, gemv+barrier, scatter+barrier+sum, next
@@ -1431,7 +1442,9 @@ void pcg_run(Ctx* ctx, const DMatrix& W, Prec* prec, const double* rhs, double* 
         SBG_CUDA(cudaMemcpyAsync(w.hh + 2 * kHistPre, w.betas.p, pre * sizeof(double), cudaMemcpyDeviceToHost, s));
         SBG_CUDA(cudaMemcpyAsync(on_device ? x_out : w.hx, x, n * sizeof(double),
                                  on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s));
+        hmark("copies_enqueued");
         SBG_CUDA(cudaStreamSynchronize(s));
+        hmark("synced");
         if (!on_device) std::copy(w.hx, w.hx + n, x_out);
         if (graph) add_launches((long long)w.kernels_per_iter * w.hs->it + 1 + (w.body_gate ? w.hs->it : 0));  // + gates
     }
@@ -1465,6 +1478,8 @@ void pcg_run(Ctx* ctx, const DMatrix& W, Prec* prec, const double* rhs, double* 
         std::copy(w.hh + kHistPre, w.hh + kHistPre + fin.it, out.alphas.begin());
         std::copy(w.hh + 2 * kHistPre, w.hh + 2 * kHistPre + fin.it, out.betas.begin());
         out.kappa = lanczos_kappa(out.alphas, out.betas);
+        hmark("done");
+        if (htrace) fprintf(stderr, "\n");
         return;
     }
     if (n > 0) {
