@@ -276,6 +276,35 @@ inline void dump_matrix_binary(const GalerkinMatrix& W, const std::string& path)
     check(sbg_matrix_dump_binary(W.get(), path.c_str()));
 }
 
+// ---- double-layer potential (inc/potential.hpp, 3-D)
+struct EvaluationGrid {  // reference: inc/potential.hpp:11-13
+    std::vector<Vec3> points;
+};
+// reference: inc/potential.hpp:15-25 (the point distances on the device)
+inline EvaluationGrid make_cartesian_grid(Context& ctx, const SurfaceMesh& mesh, double lo, double hi, int nx, int ny,
+                                          double mask_eps)
+{
+    std::vector<double> out(3 * (size_t)std::max(nx * ny, 1));
+    int count = 0;
+    check(sbg_make_cartesian_grid(ctx.get(), mesh.get(), lo, hi, nx, ny, mask_eps, out.data(), &count));
+    EvaluationGrid g;
+    for (int i = 0; i < count; ++i) g.points.emplace_back(out[3 * i], out[3 * i + 1], out[3 * i + 2]);
+    return g;
+}
+// reference: inc/potential.hpp:104-138 (the `workers` argument has no device counterpart)
+inline std::vector<double> eval_DL(Context& ctx, const std::vector<double>& v, const InflatedMesh& im,
+                                   const EvaluationGrid& grid, const QuadratureConfig& cfg = {})
+{
+    if ((int)v.size() != im.num_jump_dofs()) throw ValidationError("jump vector length does not match the DOF count");
+    const sbg_quad_cfg c = cfg.c();
+    std::vector<double> pts(3 * grid.points.size());
+    for (size_t i = 0; i < grid.points.size(); ++i)
+        for (int k = 0; k < 3; ++k) pts[3 * i + k] = grid.points[i][k];
+    std::vector<double> out(grid.points.size());
+    check(sbg_eval_dl(ctx.get(), im.get(), v.data(), pts.data(), (long long)grid.points.size(), &c, out.data()));
+    return out;
+}
+
 class DofPartition : public Handle<sbg_partition, sbg_partition_destroy> {  // inc/schwarz.hpp:14-17
 public:
     explicit DofPartition(sbg_partition* p) : Handle(p) {}

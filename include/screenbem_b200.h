@@ -183,6 +183,21 @@ int sbg_rhs_points(const sbg_inflated* im, const sbg_quad_cfg* cfg, double* pts)
 int sbg_assemble_rhs(sbg_ctx* ctx, const sbg_inflated* im, const sbg_quad_cfg* cfg, const double* g, int g_is_field,
                      double* L);
 
+/* ---- double-layer potential (inc/potential.hpp, 3-D) ----------------------- */
+/* U(x) = sum_t int n_t.(y-x) / (4 pi |x-y|^3) [phi](y) of jump vector v (num_jump_dofs values)
+ * at np points (np x 3, host, row-major) into out (np), potential.hpp:104-138: the rule
+ * triangle_rule(far_order + 2), split4 subdivision of a facet while the point is closer than
+ * its diameter (depth < 24).  cfg->exact_far: every facet in the reference's operation order,
+ * bitwise the CPU restatement; else the far facets take the constant-normal form.  A point
+ * within 0.5e-6 h of the screen: code 2 (ValidationError, potential.hpp:119-120). */
+int sbg_eval_dl(sbg_ctx* ctx, const sbg_inflated* im, const double* v, const double* points, long long np,
+                const sbg_quad_cfg* cfg, double* out);
+/* potential.hpp:15-25: the nx x ny grid of cell centres of [lo,hi]^2 in the z = 0 plane, points
+ * within mask_eps of the mesh dropped (mesh.hpp:121-133 distance_to); out: capacity 3 nx ny
+ * doubles, *count = points kept */
+int sbg_make_cartesian_grid(sbg_ctx* ctx, const sbg_mesh* mesh, double lo, double hi, int nx, int ny,
+                            double mask_eps, double* out, int* count);
+
 /* ---- partition / prolongation (host) ------------------------------------ */
 int sbg_partition_dofs(const sbg_level* pair, const sbg_inflated* fine, sbg_partition** out); /* schwarz.hpp:19-51 */
 int sbg_partition_create(int nfaces, const int32_t* face_ids, const int32_t* face_ptr, const int32_t* face_dofs,

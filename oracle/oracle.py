@@ -107,6 +107,11 @@ def lib():
             "orc_lanczos_kappa": (C.c_double, [f64p, f64p, C.c_int]),
             "orc_random_spd": (C.c_int, [C.c_int, C.c_uint, f64p]),
             "orc_normal_draws": (C.c_int, [C.c_uint, C.c_int, f64p]),
+            "orc_eval_dl": (C.c_int, [vp, f64p, f64p, C.c_longlong, C.c_int, C.c_int, f64p]),
+            "orc_distance_to": (C.c_int, [vp, f64p, C.c_longlong, f64p]),
+            "orc_make_cartesian_grid": (C.c_int, [vp, C.c_double, C.c_double, C.c_int, C.c_int, C.c_double, f64p,
+                                                  C.POINTER(C.c_int)]),
+            "orc_jump_coordinates": (C.c_int, [vp, f64p, f64p]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -396,6 +401,43 @@ def assemble_rhs(im: InflatedMesh, g, cfg: QuadratureConfig = QuadratureConfig()
     L = np.zeros(im.n)
     _check(lib().orc_assemble_rhs(im.h, cfg.far_order, np.ascontiguousarray(gv), L))
     return L
+
+
+# --------------------------------------------------------------------------- potential.hpp (3-D)
+def distance_to(m: Mesh, points) -> np.ndarray:
+    """reference: inc/mesh.hpp:121-133 (SurfaceMesh::distance_to), per point"""
+    pts = np.ascontiguousarray(np.asarray(points, dtype=np.float64).reshape(-1, 3))
+    out = np.zeros(len(pts))
+    _check(lib().orc_distance_to(m.h, pts.reshape(-1), len(pts), out))
+    return out
+
+
+def make_cartesian_grid(m: Mesh, lo: float, hi: float, nx: int, ny: int, mask_eps: float) -> np.ndarray:
+    """reference: inc/potential.hpp:15-25 (z = 0 grid, points within mask_eps of the screen dropped)"""
+    out = np.zeros(3 * max(nx * ny, 1))
+    cnt = C.c_int()
+    _check(lib().orc_make_cartesian_grid(m.h, lo, hi, nx, ny, mask_eps, out, C.byref(cnt)))
+    return out[:3 * cnt.value].reshape(-1, 3)
+
+
+def eval_DL(v, im: InflatedMesh, points, cfg: QuadratureConfig = QuadratureConfig(), workers: int = 0):
+    """reference: inc/potential.hpp:104-138 (3-D): the double-layer potential of jump vector v at
+    the points (n x 3); ValidationError for a point on the screen"""
+    vv = np.ascontiguousarray(np.asarray(v, dtype=np.float64))
+    if len(vv) != im.n:
+        raise ValidationError("jump vector length does not match the DOF count")
+    pts = np.ascontiguousarray(np.asarray(points, dtype=np.float64).reshape(-1, 3))
+    out = np.zeros(len(pts))
+    _check(lib().orc_eval_dl(im.h, vv, pts.reshape(-1), len(pts), cfg.far_order, workers or default_workers(), out))
+    return out
+
+
+def jump_coordinates(im: InflatedMesh, coeff) -> np.ndarray:
+    """reference: inc/jump.hpp:61-74 (trace field by gvertex coefficient -> jump coordinates)"""
+    c = np.ascontiguousarray(np.asarray(coeff, dtype=np.float64))
+    out = np.zeros(im.n)
+    _check(lib().orc_jump_coordinates(im.h, c, out))
+    return out
 
 
 # --------------------------------------------------------------------------- prolongation / partition

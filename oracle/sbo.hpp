@@ -1696,4 +1696,95 @@ inline std::vector<double> direct_solve(const Dense& W, const std::vector<double
     return x;
 }
 
+// ---------------------------------------------------------------- potential.hpp (3-D)
+// reference: inc/mesh.hpp:121-133 (SurfaceMesh::distance_to: min over facets, from 1e300)
+inline double distance_to(const SurfaceMesh& m, const Vec3& x)
+{
+    double d = 1e300;
+    for (int f = 0; f < m.num_facets(); ++f) {
+        const auto& t = m.facets[f];
+        d = std::min(d, detail::point_triangle_distance(x, m.vertices[t[0]], m.vertices[t[1]], m.vertices[t[2]]));
+    }
+    return d;
+}
+
+// reference: inc/potential.hpp:15-25 (grid in the z = 0 plane, points within mask_eps dropped)
+inline std::vector<Vec3> make_cartesian_grid(const SurfaceMesh& mesh, double lo, double hi, int nx, int ny,
+                                             double mask_eps)
+{
+    std::vector<Vec3> pts;
+    for (int i = 0; i < nx; ++i)
+        for (int j = 0; j < ny; ++j) {
+            const Vec3 p(lo + (hi - lo) * (i + 0.5) / nx, lo + (hi - lo) * (j + 0.5) / ny, 0.0);
+            if (distance_to(mesh, p) > mask_eps) pts.push_back(p);
+        }
+    return pts;
+}
+
+namespace detail {
+// reference: inc/potential.hpp:31-97 (the 3-D branch): the dipole kernel n0.(y-x)/(4 pi |y-x|^3)
+// times the side-0/side-1 value difference over one facet, split4 subdivision in barycentric
+// space (children in the reference's order) while the point is closer than the diameter
+inline double facet_dipole_integral(const Vec3& n0, const Vec3& x, const std::array<double, 3>& dvals,
+                                    const TriangleRule& tri, const std::array<Vec3, 3>& corner, int depth)
+{
+    double diam = 0;
+    for (int a = 0; a < 3; ++a)
+        for (int b = a + 1; b < 3; ++b) diam = std::max(diam, norm(corner[a] - corner[b]));
+    const double dist = point_triangle_distance(x, corner[0], corner[1], corner[2]);
+    if (dist < diam && depth < 24) {
+        const Vec3 m01 = 0.5 * (corner[0] + corner[1]);
+        const Vec3 m12 = 0.5 * (corner[1] + corner[2]);
+        const Vec3 m02 = 0.5 * (corner[0] + corner[2]);
+        const double d01 = 0.5 * (dvals[0] + dvals[1]);
+        const double d12 = 0.5 * (dvals[1] + dvals[2]);
+        const double d02 = 0.5 * (dvals[0] + dvals[2]);
+        double acc = 0;
+        acc += facet_dipole_integral(n0, x, {dvals[0], d01, d02}, tri, {corner[0], m01, m02}, depth + 1);
+        acc += facet_dipole_integral(n0, x, {d01, dvals[1], d12}, tri, {m01, corner[1], m12}, depth + 1);
+        acc += facet_dipole_integral(n0, x, {d02, d12, dvals[2]}, tri, {m02, m12, corner[2]}, depth + 1);
+        acc += facet_dipole_integral(n0, x, {d01, d12, d02}, tri, {m01, m12, m02}, depth + 1);
+        return acc;
+    }
+    const double area = 0.5 * norm(cross(corner[1] - corner[0], corner[2] - corner[0]));
+    double acc = 0;
+    for (int i = 0; i < tri.size(); ++i) {
+        const Vec3 y = corner[0] + tri.u[i] * (corner[1] - corner[0]) + tri.v[i] * (corner[2] - corner[0]);
+        const double val = (1.0 - tri.u[i] - tri.v[i]) * dvals[0] + tri.u[i] * dvals[1] + tri.v[i] * dvals[2];
+        const Vec3 r = y - x;
+        const double rn = norm(r);
+        acc += tri.w[i] * 2.0 * area * dot(n0, r) / (4.0 * M_PI * rn * rn * rn) * val;
+    }
+    return acc;
+}
+}  // namespace detail
+
+// reference: inc/potential.hpp:104-138: U(x) = sum_t int n_t.(y-x)/(4 pi |x-y|^3) [phi](y), the
+// two copies of each facet combined (side-0 minus side-1 trace), rule triangle_rule(far+2)
+inline std::vector<double> eval_DL(const std::vector<double>& v, const InflatedMesh& im,
+                                   const std::vector<Vec3>& points, const QuadratureConfig& cfg, int workers = 1)
+{
+    const SurfaceMesh& m = im.base;
+    const TraceField tf = expand(v, im);
+    const TriangleRule tri = triangle_rule(cfg.far_order + 2);
+    const double mask = 0.5 * m.max_facet_diameter() * 1e-6;
+    std::vector<double> out(points.size(), 0.0);
+    run_partitioned((std::int64_t)points.size(), workers, [&](int, std::int64_t lo, std::int64_t hi) {
+        for (std::int64_t p = lo; p < hi; ++p) {
+            const Vec3& x = points[p];
+            if (distance_to(m, x) <= mask) throw ValidationError("evaluation point lies on the screen");
+            double acc = 0;
+            for (int f = 0; f < m.num_facets(); ++f) {
+                std::array<double, 3> dv = {0, 0, 0};
+                for (int k = 0; k < 3; ++k) dv[k] = tf.at(im, 2 * f, k) - tf.at(im, 2 * f + 1, k);
+                const std::array<Vec3, 3> corner = {m.vertices[m.facets[f][0]], m.vertices[m.facets[f][1]],
+                                                    m.vertices[m.facets[f][2]]};
+                acc += detail::facet_dipole_integral(im.oriented_facets[2 * f].normal, x, dv, tri, corner, 0);
+            }
+            out[p] = acc;
+        }
+    });
+    return out;
+}
+
 }  // namespace sbo

@@ -569,4 +569,54 @@ double orc_wall_seconds()
     return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
 }
 
+// ---- potential.hpp (3-D)
+// points: np x 3 row-major; out: np values (potential.hpp:104-138)
+int orc_eval_dl(void* imh, const double* v, const double* points, long long np, int far_order, int workers,
+                double* out)
+{
+    return guard([&] {
+        const InflatedMesh& im = *static_cast<InflatedMesh*>(imh);
+        std::vector<double> vec(v, v + im.num_jump_dofs());
+        std::vector<Vec3> pts((size_t)np);
+        for (long long i = 0; i < np; ++i) pts[i] = Vec3(points[3 * i], points[3 * i + 1], points[3 * i + 2]);
+        QuadratureConfig cfg;
+        cfg.far_order = far_order;
+        const std::vector<double> u = eval_DL(vec, im, pts, cfg, workers);
+        std::copy(u.begin(), u.end(), out);
+    });
+}
+// mesh.hpp:121-133 per point
+int orc_distance_to(void* mh, const double* points, long long np, double* out)
+{
+    return guard([&] {
+        const SurfaceMesh& m = *static_cast<SurfaceMesh*>(mh);
+        for (long long i = 0; i < np; ++i)
+            out[i] = distance_to(m, Vec3(points[3 * i], points[3 * i + 1], points[3 * i + 2]));
+    });
+}
+// potential.hpp:15-25; out: capacity 3 nx ny; *count = points kept
+int orc_make_cartesian_grid(void* mh, double lo, double hi, int nx, int ny, double mask_eps, double* out, int* count)
+{
+    return guard([&] {
+        const std::vector<Vec3> pts = make_cartesian_grid(*static_cast<SurfaceMesh*>(mh), lo, hi, nx, ny, mask_eps);
+        for (size_t i = 0; i < pts.size(); ++i) {
+            out[3 * i] = pts[i].x;
+            out[3 * i + 1] = pts[i].y;
+            out[3 * i + 2] = pts[i].z;
+        }
+        *count = (int)pts.size();
+    });
+}
+// jump.hpp:61-74 from a trace field given by its gvertex coefficients
+int orc_jump_coordinates(void* imh, const double* coeff, double* out)
+{
+    return guard([&] {
+        const InflatedMesh& im = *static_cast<InflatedMesh*>(imh);
+        TraceField tf;
+        tf.coeff.assign(coeff, coeff + im.num_gvertices());
+        const std::vector<double> v = jump_coordinates(tf, im);
+        std::copy(v.begin(), v.end(), out);
+    });
+}
+
 }  // extern "C"

@@ -733,6 +733,37 @@ int sbg_assemble_rhs(sbg_ctx* ctx, const sbg_inflated* im, const sbg_quad_cfg* c
     });
 }
 
+// ---------------------------------------------------------------- potential (3-D)
+// reference: inc/potential.hpp:104-138
+int sbg_eval_dl(sbg_ctx* ctx, const sbg_inflated* im, const double* v, const double* points, long long np,
+                const sbg_quad_cfg* cfg, double* out)
+{
+    return guard([&] {
+        need(im, "im");
+        bind_ctx(ctx);
+        if (np > 0) {
+            need(points, "points");
+            need(out, "out");
+        }
+        if (im->im.num_jump_dofs() > 0) need(v, "v");
+        eval_dl(&ctx->c, im->im, v, points, np, qcfg(cfg), out);
+    });
+}
+// reference: inc/potential.hpp:15-25
+int sbg_make_cartesian_grid(sbg_ctx* ctx, const sbg_mesh* mesh, double lo, double hi, int nx, int ny,
+                            double mask_eps, double* out, int* count)
+{
+    return guard([&] {
+        need(mesh, "mesh");
+        need(count, "count");
+        bind_ctx(ctx);
+        const std::vector<double> pts = make_cartesian_grid(&ctx->c, mesh->m, lo, hi, nx, ny, mask_eps);
+        if (!pts.empty()) need(out, "out");
+        std::copy(pts.begin(), pts.end(), out);
+        *count = (int)(pts.size() / 3);
+    });
+}
+
 // ---------------------------------------------------------------- partition / prolongation
 int sbg_partition_dofs(const sbg_level* pair, const sbg_inflated* fine, sbg_partition** out)
 {

@@ -196,6 +196,12 @@ void assemble_W(Ctx* ctx, const InflatedMesh& im, const QuadCfg& cfg, DMatrix& W
 void pair_integrals(Ctx* ctx, const SurfaceMesh& m, const QuadCfg& cfg, const int* f, const int* g, long long np,
                     double* out);
 std::vector<double> rhs_points(const InflatedMesh& im, const QuadCfg& cfg);
+// potential.hpp:104-138 (3-D): double-layer potential of jump vector v at np points (host
+// arrays, points np x 3) into out; potential.hpp:15-25: the z = 0 evaluation grid (potential.cu)
+void eval_dl(Ctx* ctx, const InflatedMesh& im, const double* v, const double* points, long long np,
+             const QuadCfg& cfg, double* out);
+std::vector<double> make_cartesian_grid(Ctx* ctx, const SurfaceMesh& m, double lo, double hi, int nx, int ny,
+                                        double mask_eps);
 void assemble_rhs(Ctx* ctx, const InflatedMesh& im, const QuadCfg& cfg, const double* g, bool g_is_field,
                   double* L_host);
 

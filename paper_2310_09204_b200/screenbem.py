@@ -106,6 +106,9 @@ SIGNATURES = {
     "sbg_pair_integrals": (C.c_int, [vp, vp, C.POINTER(QuadCfgC), i32p, i32p, C.c_longlong, f64p]),
     "sbg_rhs_points": (C.c_int, [vp, C.POINTER(QuadCfgC), f64p]),
     "sbg_assemble_rhs": (C.c_int, [vp, vp, C.POINTER(QuadCfgC), f64p, C.c_int, f64p]),
+    "sbg_eval_dl": (C.c_int, [vp, vp, C.c_void_p, C.c_void_p, C.c_longlong, C.POINTER(QuadCfgC), C.c_void_p]),
+    "sbg_make_cartesian_grid": (C.c_int, [vp, vp, C.c_double, C.c_double, C.c_int, C.c_int, C.c_double, C.c_void_p,
+                                          C.POINTER(C.c_int)]),
     "sbg_partition_dofs": (C.c_int, [vp, vp, C.POINTER(vp)]),
     "sbg_partition_create": (C.c_int, [C.c_int, i32p, i32p, i32p, C.c_int, i32p, C.POINTER(vp)]),
     "sbg_partition_sizes": (C.c_int, [vp] + [C.POINTER(C.c_int)] * 3),
@@ -622,6 +625,54 @@ def assemble_rhs(im: InflatedMesh, g, cfg: QuadratureConfig = None, ctx: Context
     L = np.zeros(im.n)
     _check(lib().sbg_assemble_rhs(ctx.h, im.h, C.byref(c), gv, field_flag, L))
     return L
+
+
+# --------------------------------------------------------------------------- potential (3-D)
+@dataclass
+class EvaluationGrid:
+    """reference: inc/potential.hpp:11-13 — off-screen evaluation points (n x 3)"""
+    points: np.ndarray
+
+    def __post_init__(self):
+        self.points = np.ascontiguousarray(np.asarray(self.points, dtype=np.float64).reshape(-1, 3))
+
+    def __len__(self):
+        return len(self.points)
+
+
+def make_cartesian_grid(mesh: SurfaceMesh, lo: float, hi: float, nx: int, ny: int, mask_eps: float,
+                        ctx: Context = None) -> EvaluationGrid:
+    """reference: inc/potential.hpp:15-25 — cell centres of [lo, hi]^2 in the z = 0 plane (x-major),
+    points within mask_eps of the mesh dropped (the distances on the device)"""
+    ctx = ctx or default_context()
+    out = np.zeros(3 * max(nx * ny, 1))
+    cnt = C.c_int()
+    _check(lib().sbg_make_cartesian_grid(ctx.h, mesh.h, lo, hi, nx, ny, mask_eps, out.ctypes.data, C.byref(cnt)))
+    return EvaluationGrid(out[:3 * cnt.value].reshape(-1, 3))
+
+
+def eval_DL(v, im: InflatedMesh, grid, cfg: QuadratureConfig = None, ctx: Context = None) -> np.ndarray:
+    """reference: inc/potential.hpp:104-138 (3-D) — the double-layer potential of jump vector v at
+    the grid's points; ValidationError for a point on the screen.  cfg.exact_far: bitwise the
+    CPU restatement (every facet in the reference's operation order)."""
+    ctx = ctx or default_context()
+    cfg = cfg or QuadratureConfig()
+    vv = np.ascontiguousarray(np.asarray(v, dtype=np.float64).reshape(-1))
+    if len(vv) != im.n:
+        raise ValidationError("jump vector length does not match the DOF count")
+    pts = grid.points if isinstance(grid, EvaluationGrid) else EvaluationGrid(grid).points
+    out = np.zeros(len(pts))
+    c = cfg.c()
+    _check(lib().sbg_eval_dl(ctx.h, im.h, vv.ctypes.data, pts.ctypes.data, len(pts), C.byref(c), out.ctypes.data))
+    return out
+
+
+def grid_error(computed, exact) -> float:
+    """reference: inc/potential.hpp:188-195 — discrete l2 distance of two grid samplings"""
+    a, b = np.asarray(computed, dtype=np.float64), np.asarray(exact, dtype=np.float64)
+    if a.shape != b.shape:
+        raise ValidationError("grid error: length mismatch")
+    return 0.0 if a.size == 0 else float(np.sqrt(np.mean((a - b) ** 2)))
 
 
 # --------------------------------------------------------------------------- partition / prolongation

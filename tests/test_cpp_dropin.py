@@ -47,6 +47,12 @@ def test_cpp_dropin_runs_cfg1(tmp_path):
     assert f"rows_iterations {res.report.iterations}" in r.stdout
     assert float(r.stdout.split("rows_max_dx_rel")[1].split()[0]) <= 1e-8
     assert float(r.stdout.split("rows_max_dx_full")[1].split()[0]) == 0.0
+    # eval_DL / make_cartesian_grid through the header, against the Python path
+    import numpy as np
+    g = S.make_cartesian_grid(S.make_config(1).fine, -2.0, 2.0, 9, 9, 0.05)
+    U = S.eval_DL(res.report.solution, S.inflate(S.make_config(1).fine), g)
+    assert f"dl_points {len(g)}" in r.stdout
+    assert float(r.stdout.split("dl_sum")[1].split()[0]) == pytest.approx(float(np.sum(U)), rel=1e-9, abs=1e-14)
 
 
 @pytest.mark.gpu

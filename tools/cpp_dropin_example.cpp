@@ -102,6 +102,12 @@ int main(int argc, char** argv)
             xn = std::max(xn, std::fabs(rep.solution[k]));
         }
         std::printf("rows_iterations %d rows_max_dx_rel %.3e rows_max_dx_full %.3e\n", rr.iterations, xd / xn, xf);
+        // the solution's double-layer potential on the reference's evaluation grid (potential.hpp)
+        const sb::EvaluationGrid grid = sb::make_cartesian_grid(ctx, pair.fine(), -2.0, 2.0, 9, 9, 0.05);
+        const std::vector<double> U = sb::eval_DL(ctx, rep.solution, fine, grid);
+        double us = 0.0;
+        for (double u : U) us += u;
+        std::printf("dl_points %d dl_sum %.17g\n", (int)grid.points.size(), us);
         return rep.converged ? 0 : 3;
     } catch (const screenbem::ValidationError& e) {
         std::fprintf(stderr, "validation error: %s\n", e.what());
