@@ -64,6 +64,8 @@ def parse():
                          "assembled across the ranks")
     ap.add_argument("--shard", action="store_true", help="(default for N>1) one W across the ranks")
     ap.add_argument("--tts-runs", type=int, default=3, help="time-to-solution runs (median reported)")
+    ap.add_argument("--dl-grid", type=int, default=64,
+                    help="eval_DL of the solution on an n x n grid of [-2,2]^2 (z = 0 and z = 0.05); 0: skip")
     return ap.parse_args()
 
 
@@ -627,9 +629,48 @@ def run_ours(args):
             if it:  # the first run warms the host paths
                 tts.append(dt * 1e3)
             tts_iters = res.report.iterations
+            xsol = x
             del res, x
         tts_runs = [round(t, 2) for t in tts]
         tts.sort()
+    # ---- the next adjacent compute: eval_DL (potential.hpp:104-138) of the
+    # solution on the reference's evaluation grid, device-timed; the CPU restatement beside it on
+    # a point sample (the cpu_baseline leg)
+    dl = None
+    if not shard and args.dl_grid > 0:
+        fm = S.SurfaceMesh(pair.fine.vertices, pair.fine.facets)
+        gpts = S.make_cartesian_grid(fm, -2.0, 2.0, args.dl_grid, args.dl_grid, 1e-3, ctx=ctx).points
+        lift = gpts.copy()
+        lift[:, 2] = 0.05
+        dpts = np.concatenate([gpts, lift])
+        S.eval_DL(xsol, im2, dpts[:128], qcfg, ctx=ctx)
+        dl_ms = []
+        for _ in range(3):
+            ctx.reset_timers()
+            S.eval_DL(xsol, im2, dpts, qcfg, ctx=ctx)
+            dl_ms.append(ctx.timer("eval_dl")[0])
+        dl_ms.sort()
+        nfac = len(pair.fine.facets)
+        nrule = (qcfg.far_order + 2) ** 2
+        dpairs = len(dpts) * nfac
+        dl = {"points": len(dpts), "facets": nfac, "ms": dl_ms[1], "ms_runs": [round(t, 3) for t in dl_ms],
+              "point_facet_pairs_per_s": dpairs / (dl_ms[1] * 1e-3),
+              "rule_evaluations_per_s": dpairs * nrule / (dl_ms[1] * 1e-3),
+              "what": f"eval_DL of the PCG solution on the {args.dl_grid}x{args.dl_grid} grid of [-2,2]^2 in z = 0 "
+                      "(points within 1e-3 of the screen masked) and the same points at z = 0.05; device time of "
+                      "sbg_eval_dl (H2D of points and density, the on-screen check, the kernels, D2H), median of 3"}
+        if rank == 0 and world == 1 and not args.no_cpu_baseline:
+            try:
+                from oracle import oracle as O
+                oim = O.inflate(O.Mesh(pair.fine.vertices, pair.fine.facets), validate=False)
+                sel = np.linspace(0, len(dpts) - 1, 64).astype(int)
+                t0 = time.perf_counter()
+                O.eval_DL(xsol, oim, dpts[sel], O.QuadratureConfig(far_order=qcfg.far_order))
+                tc = time.perf_counter() - t0
+                dl["cpu_baseline"] = {"point_facet_pairs_per_s": len(sel) * nfac / tc, "cores": os.cpu_count() or 1,
+                                      "kind": "port", "sample": f"{len(sel)} of the points, oracle eval_DL"}
+            except Exception as e:  # pragma: no cover - reported, not fatal
+                dl["cpu_baseline"] = {"failed": str(e)}
     gc.enable()
     # one assembly into a fresh pageable numpy array, for the record (last: the 5 GB of fresh
     # pageable memory it faults in and frees does not run beside the timed e2e/tts runs)
@@ -694,6 +735,7 @@ def run_ours(args):
                     "precond_applies_per_s": 1e3 / (am / ac) if ac else None, "precond_apply_us": 1e3 * am / ac if ac else None,
                     "precond_factor_bytes": prec.factor_bytes()},
             "time_to_solution_ms": step_ms,
+            "eval_dl": dl,
             "tts_e2e_ms": tts[len(tts) // 2] if tts else None,
             "tts_e2e": ({"ms_median": tts[len(tts) // 2], "ms_min": tts[0], "runs": len(tts), "pcg_iterations": tts_iters,
                          "ms_runs": tts_runs,
