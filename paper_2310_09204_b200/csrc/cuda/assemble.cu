@@ -150,12 +150,65 @@ struct TileInfo {
     int fb, gb, certain_far, pad;
 };
 
-// contraction of the I tile with the curl lists, flushed to W's upper triangle
+// flush of one contracted W entry into W's upper triangle (W(j,i) = W(i,j) after the mirror)
+__device__ __forceinline__ void flush_entry(double* __restrict__ W, int ld, bool diag, int da, int db, double s)
+{
+    if (s == 0.0) return;
+    if (diag) {
+        atomicAdd(W + (size_t)da * ld + db, s);
+    } else if (da < db) {
+        atomicAdd(W + (size_t)da * ld + db, s);
+    } else if (da > db) {
+        atomicAdd(W + (size_t)db * ld + da, s);
+    } else {
+        atomicAdd(W + (size_t)da * ld + da, 2.0 * s);
+    }
+}
+
+// contraction of the I tile with the curl lists, flushed to W's upper triangle.  stage:
+// shared memory no longer needed by the caller (stage_bytes of it): both blocks' curl-list
+// entries are staged there once (u vectors + the I-tile row / column offsets as integers)
+// instead of being re-read from global memory inside the double loop; blocks whose entries do
+// not fit take the global path.
 __device__ void tile_contract_flush(const double* __restrict__ It, int fb, int gb, bool diag, const BlockPtrs& B,
-                                    double* __restrict__ W, int ld)
+                                    double* __restrict__ W, int ld, unsigned char* stage, size_t stage_bytes)
 {
     const int fa0 = B.dof_ptr[fb], na = B.dof_ptr[fb + 1] - fa0;
     const int gb0 = B.dof_ptr[gb], nbd = B.dof_ptr[gb + 1] - gb0;
+    const int ef0 = B.ent_ptr[fa0], nef = B.ent_ptr[fa0 + na] - ef0;
+    const int eg0 = B.ent_ptr[gb0], neg = B.ent_ptr[gb0 + nbd] - eg0;
+    const size_t need = (size_t)(nef + neg) * (sizeof(double) * 3 + sizeof(int));
+    if (stage && need <= stage_bytes) {
+        double* uf = reinterpret_cast<double*>(stage);  // nef x 3
+        double* ug = uf + 3 * nef;                       // neg x 3
+        int* of = reinterpret_cast<int*>(ug + 3 * neg);  // nef: I-tile row offset f_local (BS + 1)
+        int* og = of + nef;                              // neg: I-tile column g_local
+        for (int i = threadIdx.x; i < nef + neg; i += blockDim.x) {
+            const bool isf = i < nef;
+            const double4 e = B.ents[isf ? ef0 + i : eg0 + (i - nef)];
+            double* u = isf ? uf + 3 * i : ug + 3 * (i - nef);
+            u[0] = e.x, u[1] = e.y, u[2] = e.z;
+            if (isf) of[i] = (int)e.w * (BS + 1);
+            else og[i - nef] = (int)e.w;
+        }
+        __syncthreads();
+        for (int e = threadIdx.x; e < na * nbd; e += blockDim.x) {
+            const int a = e / nbd, b = e % nbd;
+            const int da = B.dofs[fa0 + a], db = B.dofs[gb0 + b];
+            if (diag && da > db) continue;
+            const int p0 = B.ent_ptr[fa0 + a] - ef0, p1 = B.ent_ptr[fa0 + a + 1] - ef0;
+            const int q0 = B.ent_ptr[gb0 + b] - eg0, q1 = B.ent_ptr[gb0 + b + 1] - eg0;
+            double s = 0.0;
+            for (int p = p0; p < p1; ++p) {
+                const double ax = uf[3 * p], ay = uf[3 * p + 1], az = uf[3 * p + 2];
+                const double* Irow = It + of[p];
+                for (int q = q0; q < q1; ++q)
+                    s = fma(Irow[og[q]], fma(ax, ug[3 * q], fma(ay, ug[3 * q + 1], az * ug[3 * q + 2])), s);
+            }
+            flush_entry(W, ld, diag, da, db, s);
+        }
+        return;
+    }
     for (int e = threadIdx.x; e < na * nbd; e += blockDim.x) {
         const int a = e / nbd, b = e % nbd;
         const int da = B.dofs[fa0 + a], db = B.dofs[gb0 + b];
@@ -169,16 +222,7 @@ __device__ void tile_contract_flush(const double* __restrict__ It, int fb, int g
                 s = fma(Irow[(int)eb.w], fma(ea.x, eb.x, fma(ea.y, eb.y, ea.z * eb.z)), s);
             }
         }
-        if (s == 0.0) continue;
-        if (diag) {
-            atomicAdd(W + (size_t)da * ld + db, s);
-        } else if (da < db) {
-            atomicAdd(W + (size_t)da * ld + db, s);
-        } else if (da > db) {
-            atomicAdd(W + (size_t)db * ld + da, s);
-        } else {
-            atomicAdd(W + (size_t)da * ld + da, 2.0 * s);
-        }
+        flush_entry(W, ld, diag, da, db, s);
     }
 }
 
@@ -374,7 +418,9 @@ __global__ void __launch_bounds__(FAR_THREADS, 3)
         }
         __syncthreads();
     }
-    tile_contract_flush(It, T.fb, T.gb, diag, B, W, ld);
+    // the staged y points are dead: their shared memory takes the curl-list entries
+    tile_contract_flush(It, T.fb, T.gb, diag, B, W, ld, EXACT ? nullptr : reinterpret_cast<unsigned char*>(Ys),
+                        EXACT ? 0 : (size_t)BS * NFP * sizeof(double4));
 }
 
 // Warp-aggregated append to a global list: every lane of the (converged) warp calls it;
