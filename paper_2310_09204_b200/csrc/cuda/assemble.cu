@@ -237,11 +237,14 @@ struct XPts {
     double m2x[FAR_PASS], m2y[FAR_PASS], m2z[FAR_PASS], x2[FAR_PASS];  // -2x, -2y, -2z, |x|^2
 };
 
-__device__ __forceinline__ void far_xpoints(const double* t, const double* o, int pass, XPts& X)
+// coordinate order (P.x, P.y, P.z): the identity, or a flat tile's two in-plane axes first and
+// its flat axis last (far_flat_axis)
+__device__ __forceinline__ void far_xpoints(const double* t, const double* o, int pass, XPts& X,
+                                            int3 P = make_int3(0, 1, 2))
 {
-    const double e1x = t[3] - t[0], e1y = t[4] - t[1], e1z = t[5] - t[2];
-    const double e2x = t[6] - t[0], e2y = t[7] - t[1], e2z = t[8] - t[2];
-    const double bx = t[0] - o[0], by = t[1] - o[1], bz = t[2] - o[2];
+    const double e1x = t[3 + P.x] - t[P.x], e1y = t[3 + P.y] - t[P.y], e1z = t[3 + P.z] - t[P.z];
+    const double e2x = t[6 + P.x] - t[P.x], e2y = t[6 + P.y] - t[P.y], e2z = t[6 + P.z] - t[P.z];
+    const double bx = t[P.x] - o[P.x], by = t[P.y] - o[P.y], bz = t[P.z] - o[P.z];
 #pragma unroll
     for (int q = 0; q < FAR_PASS; ++q) {
         const int i = FAR_PASS * pass + q;
@@ -263,19 +266,21 @@ __device__ __forceinline__ double4 scaled_ypoint(double y0, double y1, double y2
     return make_double4(sj * y0, sj * y1, sj * y2, sj * fma(y0, y0, fma(y1, y1, y2 * y2)));
 }
 
-__device__ __forceinline__ double4 far_ypoint(const double* s, const double* o, int j)
+__device__ __forceinline__ double4 far_ypoint(const double* s, const double* o, int j, int3 P = make_int3(0, 1, 2))
 {
-    const double y0 = fma(c_far_v[j], s[6] - s[0], fma(c_far_u[j], s[3] - s[0], s[0] - o[0]));
-    const double y1 = fma(c_far_v[j], s[7] - s[1], fma(c_far_u[j], s[4] - s[1], s[1] - o[1]));
-    const double y2 = fma(c_far_v[j], s[8] - s[2], fma(c_far_u[j], s[5] - s[2], s[2] - o[2]));
+    const double y0 = fma(c_far_v[j], s[6 + P.x] - s[P.x], fma(c_far_u[j], s[3 + P.x] - s[P.x], s[P.x] - o[P.x]));
+    const double y1 = fma(c_far_v[j], s[6 + P.y] - s[P.y], fma(c_far_u[j], s[3 + P.y] - s[P.y], s[P.y] - o[P.y]));
+    const double y2 = fma(c_far_v[j], s[6 + P.z] - s[P.z], fma(c_far_u[j], s[3 + P.z] - s[P.z], s[P.z] - o[P.z]));
     return scaled_ypoint(y0, y1, y2, c_far_s[j]);
 }
 
 // sum_{q in pass} w_{4 pass + q} sum_j w_j / |x_q - y_j|  (16 y-points x 4 x-points); one
 // accumulator per x point, so the four evaluations per y point are independent chains;
 // w_j is folded into the staged y point (far_ypoint, rsqrt_acc): 9 FP64 instructions and one
-// MUFU per evaluation
-template <int NFP>
+// MUFU per evaluation.  FLAT: every point of the tile has a zero last coordinate (a tile lying
+// in one coordinate plane, far_flat_axis), whose product term -2 x_z y_z = -0 adds nothing:
+// it is left out, 8 FP64 instructions per evaluation, the same value
+template <int NFP, bool FLAT = false>
 __device__ __forceinline__ double far_pass_sum(const XPts& X, const double4* __restrict__ Y, int pass)
 {
     double a[FAR_PASS];
@@ -287,7 +292,8 @@ __device__ __forceinline__ double far_pass_sum(const XPts& X, const double4* __r
         const double sj = c_far_s[j];
 #pragma unroll
         for (int q = 0; q < FAR_PASS; ++q) {
-            const double r2 = fma(X.m2x[q], y.x, fma(X.m2y[q], y.y, fma(X.m2z[q], y.z, fma(X.x2[q], sj, y.w))));
+            const double r2 = FLAT ? fma(X.m2x[q], y.x, fma(X.m2y[q], y.y, fma(X.x2[q], sj, y.w)))
+                                   : fma(X.m2x[q], y.x, fma(X.m2y[q], y.y, fma(X.m2z[q], y.z, fma(X.x2[q], sj, y.w))));
             a[q] = rsqrt_acc(r2, a[q]);
         }
     }
@@ -342,9 +348,11 @@ __global__ void __launch_bounds__(FAR_THREADS, 3)
     int* gid = reinterpret_cast<int*>(gcr + BS * 6);
     int* gvid = gid + BS;
     __shared__ double o[3];
+    __shared__ int nzax;  // bit a: some vertex of the tile differs from o in coordinate a
     const TileInfo T = tiles[(size_t)blockIdx.x * tstride];  // tstride > 1: one shard of the tile list
     const bool diag = T.fb == T.gb;
     if (threadIdx.x < 3) o[threadIdx.x] = G.v[9 * B.facets[T.fb * BS] + threadIdx.x];
+    if (threadIdx.x == 0) nzax = 0;
     for (int e = threadIdx.x; e < BS; e += blockDim.x) {
         const int g = B.facets[T.gb * BS + e];
         gid[e] = g;
@@ -360,11 +368,31 @@ __global__ void __launch_bounds__(FAR_THREADS, 3)
     }
     for (int e = threadIdx.x; e < BS * (BS + 1); e += blockDim.x) It[e] = 0.0;
     __syncthreads();
-    if (!EXACT)
+    // a tile whose 128 facets all lie in one coordinate plane (a flat screen panel: every
+    // config-5 tile, most of configs 3-4) has that coordinate equal to o's at every vertex, so
+    // it is exactly zero in tile-local coordinates: it goes last and the evaluation skips it
+    int3 P = make_int3(0, 1, 2);
+    bool flat = false;
+    if (!EXACT) {
+        if (threadIdx.x < 2 * BS) {
+            const int h = threadIdx.x < BS ? B.facets[T.fb * BS + threadIdx.x] : gid[threadIdx.x - BS];
+            int m = 0;
+            if (h >= 0)
+                for (int k = 0; k < 9; ++k)
+                    if (G.v[9 * h + k] != o[k % 3]) m |= 1 << (k % 3);
+            if (m) atomicOr(&nzax, m);
+        }
+        __syncthreads();
+        const int nz = nzax;
+        flat = (nz & 7) != 7;
+        if (!(nz & 4) || nz == 7) P = make_int3(0, 1, 2);
+        else if (!(nz & 2)) P = make_int3(0, 2, 1);
+        else P = make_int3(1, 2, 0);
         for (int e = threadIdx.x; e < BS * NFP; e += blockDim.x) {
             const int g = gid[e / NFP];
-            Ys[e] = g >= 0 ? far_ypoint(G.v + 9 * g, o, e % NFP) : make_double4(0, 0, 0, 1);
+            Ys[e] = g >= 0 ? far_ypoint(G.v + 9 * g, o, e % NFP, P) : make_double4(0, 0, 0, 1);
         }
+    }
     __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int fl = (warp & 1) * 32 + lane;
@@ -403,10 +431,17 @@ __global__ void __launch_bounds__(FAR_THREADS, 3)
         const double sf = G.area[f] * inv_pi;
         for (int pass = 0; !EXACT && pass < NFP / FAR_PASS; ++pass) {
             XPts X;
-            far_xpoints(G.v + 9 * f, o, pass, X);
-            for (int m = 0, gl = warp >> 1; gl < BS; gl += FAR_THREADS / 64, ++m) {
-                if (!(mask >> m & 1)) continue;
-                It[fl * (BS + 1) + gl] += far_pass_sum<NFP>(X, Ys + gl * NFP, pass) * sf * gcr[gl * 6 + 5];
+            far_xpoints(G.v + 9 * f, o, pass, X, P);
+            if (flat) {
+                for (int m = 0, gl = warp >> 1; gl < BS; gl += FAR_THREADS / 64, ++m) {
+                    if (!(mask >> m & 1)) continue;
+                    It[fl * (BS + 1) + gl] += far_pass_sum<NFP, true>(X, Ys + gl * NFP, pass) * sf * gcr[gl * 6 + 5];
+                }
+            } else {
+                for (int m = 0, gl = warp >> 1; gl < BS; gl += FAR_THREADS / 64, ++m) {
+                    if (!(mask >> m & 1)) continue;
+                    It[fl * (BS + 1) + gl] += far_pass_sum<NFP>(X, Ys + gl * NFP, pass) * sf * gcr[gl * 6 + 5];
+                }
             }
         }
     }
@@ -611,6 +646,25 @@ __device__ __forceinline__ void path_triangle(const double* __restrict__ root, i
 // r^2, MUFU.RSQ64H + 4 FP64 for the refined 1/r and 1 FMA, and the four
 // evaluations per loaded y point are independent chains (tools/micro_eval.cu:
 // this 4-point block is the fastest register blocking of the pattern).
+// coordinate a of vertex k (0-2) of a triangle held in registers, for a runtime axis a
+__device__ __forceinline__ double vcoord(const double* v, int k, int a)
+{
+    return a == 0 ? v[3 * k] : (a == 1 ? v[3 * k + 1] : v[3 * k + 2]);
+}
+// the axis in which every vertex of both triangles has one and the same coordinate (z first),
+// or -1; the axis order puts it last (identity when there is none)
+__device__ __forceinline__ int3 flat_axes(const double* t, const double* s, bool& flat)
+{
+    int fa = -1;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        const double c = t[a];
+        if (t[3 + a] == c && t[6 + a] == c && s[a] == c && s[3 + a] == c && s[6 + a] == c) fa = a;
+    }
+    flat = fa >= 0;
+    return fa == 1 ? make_int3(0, 2, 1) : (fa == 0 ? make_int3(1, 2, 0) : make_int3(0, 1, 2));
+}
+
 constexpr int NEAR_LEAF_THREADS = 256;
 constexpr int NEAR_XP = 4;  // x points per pass (register block)
 constexpr int NEAR_LEAF_WARPS = NEAR_LEAF_THREADS / 32;
@@ -634,6 +688,7 @@ __global__ void __launch_bounds__(NEAR_LEAF_THREADS, 2) k_near_leaves(const Near
         double acc = 0.0, scale = 0.0;
         double f1x = 0, f1y = 0, f1z = 0, f2x = 0, f2y = 0, f2z = 0;
         int pair = 0;
+        bool flat = false;
         __syncwarp();  // the previous iteration's reads of Ys are done
         if (active) {
             const NearNode nd = leaves[q];
@@ -655,19 +710,28 @@ __global__ void __launch_bounds__(NEAR_LEAF_THREADS, 2) k_near_leaves(const Near
             path_triangle(GV + 9 * pr.x, ((1 << 2 * dt) - 1) / 3 + it, t);
             path_triangle(GV + 9 * pr.y, ((1 << 2 * ds) - 1) / 3 + is, s);
             scale = __ldg(GA + pr.x) * __ldg(GA + pr.y) * ldexp(inv_pi, -2 * (dt + ds));
-            const double e1x = s[3] - s[0], e1y = s[4] - s[1], e1z = s[5] - s[2];
-            const double e2x = s[6] - s[0], e2y = s[7] - s[1], e2z = s[8] - s[2];
-            const double bx = s[0] - t[0], by = s[1] - t[1], bz = s[2] - t[2];
+            // a leaf pair in one coordinate plane: that axis goes last, all its leaf-local
+            // coordinates are exact zeros and the evaluation leaves its term out (far_pass_sum)
+            const int3 P = flat_axes(t, s, flat);
+            const double e1x = vcoord(s, 1, P.x) - vcoord(s, 0, P.x), e1y = vcoord(s, 1, P.y) - vcoord(s, 0, P.y),
+                         e1z = vcoord(s, 1, P.z) - vcoord(s, 0, P.z);
+            const double e2x = vcoord(s, 2, P.x) - vcoord(s, 0, P.x), e2y = vcoord(s, 2, P.y) - vcoord(s, 0, P.y),
+                         e2z = vcoord(s, 2, P.z) - vcoord(s, 0, P.z);
+            const double bx = vcoord(s, 0, P.x) - vcoord(t, 0, P.x), by = vcoord(s, 0, P.y) - vcoord(t, 0, P.y),
+                         bz = vcoord(s, 0, P.z) - vcoord(t, 0, P.z);
             for (int j = xg; j < NN; j += 4) {
                 const double yx = fma(c_near_v[j], e2x, fma(c_near_u[j], e1x, bx));
                 const double yy = fma(c_near_v[j], e2y, fma(c_near_u[j], e1y, by));
                 const double yz = fma(c_near_v[j], e2z, fma(c_near_u[j], e1z, bz));
                 Ys[j] = scaled_ypoint(yx, yy, yz, c_near_s[j]);
             }
-            f1x = t[3] - t[0], f1y = t[4] - t[1], f1z = t[5] - t[2];
-            f2x = t[6] - t[0], f2y = t[7] - t[1], f2z = t[8] - t[2];
+            f1x = vcoord(t, 1, P.x) - vcoord(t, 0, P.x), f1y = vcoord(t, 1, P.y) - vcoord(t, 0, P.y),
+            f1z = vcoord(t, 1, P.z) - vcoord(t, 0, P.z);
+            f2x = vcoord(t, 2, P.x) - vcoord(t, 0, P.x), f2y = vcoord(t, 2, P.y) - vcoord(t, 0, P.y),
+            f2z = vcoord(t, 2, P.z) - vcoord(t, 0, P.z);
         }
         __syncwarp();
+        flat = __all_sync(0xffffffffu, flat || !active);
         if (active) {
             // x groups of 4 consecutive points: lane xg takes groups xg and xg + 4 against all
             // 36 y points, and group 8 against y in [9 xg, 9 xg + 9)
@@ -688,14 +752,27 @@ __global__ void __launch_bounds__(NEAR_LEAF_THREADS, 2) k_near_leaves(const Near
                     mz[r] = -2.0 * xz;
                     a[r] = 0.0;
                 }
+                if (flat) {
 #pragma unroll 3
-                for (int j = j0; j < j1; ++j) {
-                    const double4 y = Ys[j];
-                    const double sj = c_near_s[j];
+                    for (int j = j0; j < j1; ++j) {
+                        const double4 y = Ys[j];
+                        const double sj = c_near_s[j];
 #pragma unroll
-                    for (int r = 0; r < NEAR_XP; ++r) {
-                        const double r2 = fma(mx[r], y.x, fma(my[r], y.y, fma(mz[r], y.z, fma(x2[r], sj, y.w))));
-                        a[r] = rsqrt_acc(r2, a[r]);
+                        for (int r = 0; r < NEAR_XP; ++r) {
+                            const double r2 = fma(mx[r], y.x, fma(my[r], y.y, fma(x2[r], sj, y.w)));
+                            a[r] = rsqrt_acc(r2, a[r]);
+                        }
+                    }
+                } else {
+#pragma unroll 3
+                    for (int j = j0; j < j1; ++j) {
+                        const double4 y = Ys[j];
+                        const double sj = c_near_s[j];
+#pragma unroll
+                        for (int r = 0; r < NEAR_XP; ++r) {
+                            const double r2 = fma(mx[r], y.x, fma(my[r], y.y, fma(mz[r], y.z, fma(x2[r], sj, y.w))));
+                            a[r] = rsqrt_acc(r2, a[r]);
+                        }
                     }
                 }
 #pragma unroll

@@ -198,3 +198,24 @@ def test_assemble_W_into_host_buffer(cfg):
         assert np.array_equal(Wd, Wd.T)
     with pytest.raises(S.ValidationError):
         S.assemble_W(im, ctx=ctx, out=np.zeros((n, n - 1)))
+
+
+@pytest.mark.parametrize("axis,offset", [(2, 0.0), (2, 0.3), (1, -0.7), (0, 1.1)])
+def test_coordinate_plane_screens_match_oracle(ctx, axis, offset):
+    """Far tiles and near leaves whose facets all lie in one coordinate plane skip the
+    evaluation's zero coordinate (assemble.cu far_flat / flat_axes): config 1 moved into the
+    planes z = 0, z = 0.3, y = -0.7 and x = 1.1 (the permuted axis orders of the flat path)
+    matches the oracle per entry, and the four placements agree with each other to the
+    reorder bound (the same screen up to a rigid motion)."""
+    m = S.make_config(1).fine
+    v0 = np.array(m.vertices, dtype=float)
+    # in-plane coordinates (u, w) -> the two axes other than `axis`; the flat coordinate = offset
+    others = [a for a in range(3) if a != axis]
+    v = np.empty_like(v0)
+    v[:, others[0]], v[:, others[1]], v[:, axis] = v0[:, 0], v0[:, 1], offset
+    f = np.array(m.facets)
+    Wg = S.assemble_W(S.inflate(S.SurfaceMesh(v, f)), ctx=ctx).download()
+    Wo = O.assemble_W(O.inflate(O.Mesh(v, f)), workers=WORKERS)
+    check_W(Wg, Wo)
+    Wz = S.assemble_W(S.inflate(S.SurfaceMesh(v0, f)), ctx=ctx).download()
+    assert np.abs(Wg - Wz).max() <= 1e-13 * np.abs(Wz).max()
