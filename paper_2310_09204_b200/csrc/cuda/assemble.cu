@@ -233,6 +233,9 @@ __device__ void tile_contract_flush(const double* __restrict__ It, int fb, int g
 // satisfy dist >= 2 diam, so (|x|^2+|y|^2)/|x-y|^2 stays O(10) inside a tile and
 // ~1 between distant tiles: the rounding stays at the 1e-15 level.
 constexpr int FAR_PASS = 4;            // rule points of f held in registers per pass
+#ifndef FAR_FLAT_UNROLL
+#define FAR_FLAT_UNROLL 2
+#endif
 struct XPts {
     double m2x[FAR_PASS], m2y[FAR_PASS], m2z[FAR_PASS], x2[FAR_PASS];  // -2x, -2y, -2z, |x|^2
 };
@@ -280,13 +283,13 @@ __device__ __forceinline__ double4 far_ypoint(const double* s, const double* o, 
 // MUFU per evaluation.  FLAT: every point of the tile has a zero last coordinate (a tile lying
 // in one coordinate plane, far_flat_axis), whose product term -2 x_z y_z = -0 adds nothing:
 // it is left out, 8 FP64 instructions per evaluation, the same value
-template <int NFP, bool FLAT = false>
+template <int NFP, bool FLAT = false, int UNROLL = 2>
 __device__ __forceinline__ double far_pass_sum(const XPts& X, const double4* __restrict__ Y, int pass)
 {
     double a[FAR_PASS];
 #pragma unroll
     for (int q = 0; q < FAR_PASS; ++q) a[q] = 0.0;
-#pragma unroll 2
+#pragma unroll UNROLL
     for (int j = 0; j < NFP; ++j) {
         const double4 y = Y[j];
         const double sj = c_far_s[j];
@@ -435,7 +438,7 @@ __global__ void __launch_bounds__(FAR_THREADS, 3)
             if (flat) {
                 for (int m = 0, gl = warp >> 1; gl < BS; gl += FAR_THREADS / 64, ++m) {
                     if (!(mask >> m & 1)) continue;
-                    It[fl * (BS + 1) + gl] += far_pass_sum<NFP, true>(X, Ys + gl * NFP, pass) * sf * gcr[gl * 6 + 5];
+                    It[fl * (BS + 1) + gl] += far_pass_sum<NFP, true, FAR_FLAT_UNROLL>(X, Ys + gl * NFP, pass) * sf * gcr[gl * 6 + 5];
                 }
             } else {
                 for (int m = 0, gl = warp >> 1; gl < BS; gl += FAR_THREADS / 64, ++m) {
@@ -666,6 +669,10 @@ __device__ __forceinline__ int3 flat_axes(const double* t, const double* s, bool
 }
 
 constexpr int NEAR_LEAF_THREADS = 256;
+#ifndef NEAR_FLAT_UNROLL
+#define NEAR_FLAT_UNROLL 9
+#endif
+constexpr int kNearFlatUnroll = NEAR_FLAT_UNROLL;  // the flat leaf loop's unroll (A/B builds)
 constexpr int NEAR_XP = 4;  // x points per pass (register block)
 constexpr int NEAR_LEAF_WARPS = NEAR_LEAF_THREADS / 32;
 constexpr size_t NEAR_LEAF_SMEM = (size_t)NEAR_LEAF_WARPS * 8 * NN * sizeof(double4);
@@ -753,7 +760,7 @@ __global__ void __launch_bounds__(NEAR_LEAF_THREADS, 2) k_near_leaves(const Near
                     a[r] = 0.0;
                 }
                 if (flat) {
-#pragma unroll 3
+#pragma unroll kNearFlatUnroll
                     for (int j = j0; j < j1; ++j) {
                         const double4 y = Ys[j];
                         const double sj = c_near_s[j];

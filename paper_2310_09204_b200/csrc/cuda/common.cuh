@@ -109,6 +109,7 @@ struct Ctx {
     int sm_count = kNumSMs;
     cudaStream_t stream = nullptr;
     cudaStream_t aux = nullptr;  // second stream for look-ahead overlap (aux_stream(), created on first use)
+    cudaStream_t aux2 = nullptr; // third stream: the L^-1 chain beside the factorisation (aux_stream(ctx, 1))
     Timers timers;
     // matrix-vector form of gemv / pcg: 0 = symmetric (reads the upper triangle only, for
     // n >= kSymvMinN), 1 = full-matrix forms (the row kernel the row-panel PCG shares)

@@ -1,4 +1,5 @@
 // Context, timers and dense-matrix utilities.
+#include <cstdlib>
 #include "common.cuh"
 #include <atomic>
 #include <chrono>
@@ -228,14 +229,15 @@ Ctx::~Ctx()
 
 // a blocking stream too, so the stream-ordered pool's legacy-stream allocations order
 // against it (common.cuh)
-cudaStream_t aux_stream(Ctx* ctx)
+cudaStream_t aux_stream(Ctx* ctx, int which)
 {
-    if (!ctx->aux) {
+    cudaStream_t& st = which == 0 ? ctx->aux : ctx->aux2;
+    if (!st) {
         int least = 0, greatest = 0;
         SBG_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
-        SBG_CUDA(cudaStreamCreateWithPriority(&ctx->aux, cudaStreamDefault, least));
+        SBG_CUDA(cudaStreamCreateWithPriority(&st, cudaStreamDefault, least));
     }
-    return ctx->aux;
+    return st;
 }
 
 TimedScope::TimedScope(Ctx* c, const char* n) : ctx(c), name(n)

@@ -61,7 +61,7 @@ void l2_flush(Ctx* ctx);  // write 256 MiB then read 256 MiB: cold, clean L2
 // context (large per-call temporaries: no pool growth or fragmentation between calls)
 enum { kScratchInverse = 0, kScratchCoarseWR = 1, kScratchCoarsePart = 2, kScratchMatvecX = 3, kScratchSlots = 4 };
 double* scratch(Ctx* ctx, int slot, size_t count);
-cudaStream_t aux_stream(Ctx* ctx);  // the context's second stream (look-ahead overlap)
+cudaStream_t aux_stream(Ctx* ctx, int which = 0);  // the context's second (0) / third (1) stream
 
 // ---------------------------------------------------------------- matrices
 void matrix_alloc(Ctx* ctx, int n, DMatrix& M);

@@ -290,86 +290,7 @@ __device__ __forceinline__ void for_acc(const double (&acc)[4][4][2], F f)
             for (int h = 0; h < 2; ++h) f(wm + 8 * x + gid, wn + 8 * y + 2 * tig + h, acc[x][y][h]);
 }
 
-// ---------------------------------------------------------------- Cholesky: fused panel step
-// Factor the 64x64 SPD tile a[] (lower part valid, row stride AS) and form its inverse:
-// right-looking elimination in LDL^T form — multipliers m_rj = a_rj / a_jj, Schur update
-// a_rc -= m_rj a_cj for j < c <= r — fused with the same eliminations applied to [L | I],
-// whose rows Y_r = L_rr (L^-1)_r obey Y_r = e_r - sum_{j<r} m_rj Y_j (the multipliers are
-// L_rj / L_jj).  256 threads, each owning a 4x4 register block of the tile: element (r,c)
-// holds a_rc until column c is eliminated and Y_rc from then on, so every step is the same
-// rank-1 update x -= m_r o_c of the whole block, with o = column j of a (c > j) or row j of
-// Y (c <= j).  Column j (zero above the diagonal, the pivot kept apart) and row j of Y are
-// published at the end of step j-1 into double-buffered shared vectors: ONE barrier per
-// column.  On exit a[r][c] (r >= c) holds the eliminated columns (a[j][j] = pivot p_j,
-// L_jj = sqrt(p_j), L_rc = a_rc / L_cc) and x[][] the thread's 4x4 block of Y; returns
-// false (all threads) if a pivot is not positive and finite.
-constexpr int AS = TB + 1;  // row stride of the tile in shared memory
-constexpr int kFactorThreads = 256;
-struct FactorBufs {
-    double col[2][TB], yrow[2][TB], piv[2], inv[2];
-};
-// 4x4 block of thread t: column block t >> 4 (so a column's 16 owners are one half warp,
-// and only that warp takes the publishing branch), row block t & 15
-__device__ __forceinline__ int blk_r0() { return (threadIdx.x & 15) * 4; }
-__device__ __forceinline__ int blk_c0() { return (threadIdx.x >> 4) * 4; }
-__device__ bool tile_ldl_inverse(double* __restrict__ a, FactorBufs& fb, double (&x)[4][4])
-{
-    const int r0 = blk_r0(), c0 = blk_c0();
-#pragma unroll
-    for (int u = 0; u < 4; ++u)
-#pragma unroll
-        for (int v = 0; v < 4; ++v) x[u][v] = a[(r0 + u) * AS + c0 + v];
-    // publish column 0 (pivot apart, rows <= 0 zero) and row 0 of Y for step 0
-    auto publish = [&](int jn, int buf) {
-        if (c0 <= jn && jn < c0 + 4) {
-#pragma unroll
-            for (int v = 0; v < 4; ++v)
-                if (c0 + v == jn) {
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        const int r = r0 + u;
-                        fb.col[buf][r] = r > jn ? x[u][v] : 0.0;
-                        if (r >= jn) a[r * AS + jn] = x[u][v];
-                        if (r == jn) {
-                            fb.piv[buf] = x[u][v];
-                            fb.inv[buf] = 1.0 / x[u][v];
-                        }
-                        x[u][v] = r == jn ? 1.0 : 0.0;  // element (r, jn) becomes Y_{r,jn}: delta
-                    }
-                }
-        }
-        if (r0 <= jn && jn < r0 + 4) {
-#pragma unroll
-            for (int u = 0; u < 4; ++u)
-                if (r0 + u == jn)
-#pragma unroll
-                    for (int v = 0; v < 4; ++v) fb.yrow[buf][c0 + v] = x[u][v];
-        }
-    };
-    publish(0, 0);
-    __syncthreads();
-    bool ok = true;
-    for (int j = 0; j < TB; ++j) {
-        const int cur = j & 1;
-        const double p = fb.piv[cur];
-        ok = ok && p > 0.0 && isfinite(p);
-        if (r0 + 3 > j) {  // some row r > j of this block is still active (m_r = 0 otherwise)
-            const double inv = fb.inv[cur];
-            double m[4], o[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) m[u] = fb.col[cur][r0 + u] * inv;
-#pragma unroll
-            for (int v = 0; v < 4; ++v) o[v] = c0 + v > j ? fb.col[cur][c0 + v] : fb.yrow[cur][c0 + v];
-#pragma unroll
-            for (int u = 0; u < 4; ++u)
-#pragma unroll
-                for (int v = 0; v < 4; ++v) x[u][v] = fma(-m[u], o[v], x[u][v]);
-        }
-        if (j + 1 < TB) publish(j + 1, cur ^ 1);
-        __syncthreads();
-    }
-    return ok;
-}
+#include "tile_factor.cuh"
 
 // One step k of the panel-blocked Cholesky (panel [p0, p0 + kPanel)), all blocks and all
 // tile rows i >= k of column k in one launch, task (block, i):
@@ -1080,25 +1001,35 @@ std::shared_ptr<PrecSchedule> prec_schedule(Ctx* ctx, const Prec* P)
 // W_bb^-1 = L^-T L^-1 for every block from the tiled factor in Lwork (overwritten):
 // X = L^-1 by panels (K_XSTEP per row of tiles, K_XUPD at panel ends), then M = X^T X over Lwork, then
 // the compact row-major inverses (row stride ldm_b) into Mc.
-void form_inverses(Ctx* ctx, Prec* P, DBuf<double>& Lwork, DBuf<double>& Mc, bool factored = false)
+// X = L^-1 scratch (zeroed, enqueued on the main stream)
+double* inverse_scratch(Ctx* ctx, size_t n)
+{
+    double* Xp = scratch(ctx, kScratchInverse, std::max<size_t>(n, 1));
+    TimedScope t0(ctx, "inv_alloc");
+    SBG_CUDA(cudaMemsetAsync(Xp, 0, std::max<size_t>(n, 1) * sizeof(double), ctx->stream));
+    return Xp;
+}
+// row k of X = L^-1 (K_XSTEP) and, at a panel end, its update of the rows below (K_XUPD):
+// needs rows < k of X and the tiles L(k, q <= k), final once factorisation step k is done
+void enqueue_inverse_row(Ctx* ctx, Prec* P, const PrecSchedule& S, int k, double* Lp, double* Xp, cudaStream_t st)
+{
+    launch_gemm<K_XSTEP>(ctx, P, k, S.d_xd.p + S.xd.off[k], S.xd.count(k), Lp, Xp, st);
+    launch_gemm<K_XUPD>(ctx, P, k, S.d_xu.p + S.xu.off[k], S.xu.count(k), Lp, Xp, st);
+}
+
+// lower_done: X = L^-1 was already formed into the inverse scratch beside the factorisation
+// (prec_build), so only the product / compaction remain
+void form_inverses(Ctx* ctx, Prec* P, DBuf<double>& Lwork, DBuf<double>& Mc, bool factored = false,
+                   bool lower_done = false)
 {
     cudaStream_t s = ctx->stream;
     const PrecSchedule& S = *P->sched;
-    double* Xp_p = scratch(ctx, kScratchInverse, std::max<size_t>(Lwork.n, 1));
-    {
-        TimedScope t0(ctx, "inv_alloc");
-        SBG_CUDA(cudaMemsetAsync(Xp_p, 0, std::max<size_t>(Lwork.n, 1) * sizeof(double), s));
-    }
     struct {
         double* p;
-    } Xp{Xp_p};
-    {
+    } Xp{lower_done ? scratch(ctx, kScratchInverse, std::max<size_t>(Lwork.n, 1)) : inverse_scratch(ctx, Lwork.n)};
+    if (!lower_done) {
         TimedScope t1(ctx, "inv_lower");
-        // (the factorisation's two-stream look-ahead measured no faster here)
-        for (int k = 0; k < P->Tmax; ++k) {
-            launch_gemm<K_XSTEP>(ctx, P, k, S.d_xd.p + S.xd.off[k], S.xd.count(k), Lwork.p, Xp.p);
-            launch_gemm<K_XUPD>(ctx, P, k, S.d_xu.p + S.xu.off[k], S.xu.count(k), Lwork.p, Xp.p);
-        }
+        for (int k = 0; k < P->Tmax; ++k) enqueue_inverse_row(ctx, P, S, k, Lwork.p, Xp.p, s);
     }
     if (!factored) {
         TimedScope t2(ctx, "inv_lauum");
@@ -1235,6 +1166,17 @@ Prec* prec_build(Ctx* ctx, const DMatrix& W, const DofPartition& part, const Pro
         // ---- batched tiled Cholesky: per step k, potrf of tile (k,k), trsm of column k, trailing update
         DBuf<int> fail(std::max(P->nblocks, 1));
         SBG_CUDA(cudaMemsetAsync(fail.p, 0, fail.n * sizeof(int), s));
+        // the inverse modes form X = L^-1 row by row on a third stream right behind the
+        // factorisation (row k needs only factorisation step k and the rows above), so the
+        // two latency-bound chains of Tmax steps run side by side instead of one after the other
+        const bool need_inv = mode == kPrecInverse || mode == kPrecFactored;
+        double* Xp = need_inv ? inverse_scratch(ctx, P->Lp.n) : nullptr;
+        cudaStream_t xs = need_inv ? aux_stream(ctx, 1) : nullptr;
+        cudaEvent_t step_ev = nullptr, x_ev = nullptr;
+        if (need_inv) {
+            SBG_CUDA(cudaEventCreateWithFlags(&step_ev, cudaEventDisableTiming));
+            SBG_CUDA(cudaEventCreateWithFlags(&x_ev, cudaEventDisableTiming));
+        }
         {
             TimedScope ts(ctx, "cholesky");
             set_max_dynamic_smem(k_panel_step, STEP_SMEM);
@@ -1248,6 +1190,11 @@ Prec* prec_build(Ctx* ctx, const DMatrix& W, const DofPartition& part, const Pro
                                                                       P->D.p, Ld.p, fail.p);
                     count_launch();
                     SBG_LAUNCH_CHECK();
+                }
+                if (need_inv) {
+                    SBG_CUDA(cudaEventRecord(step_ev, s));
+                    SBG_CUDA(cudaStreamWaitEvent(xs, step_ev, 0));
+                    enqueue_inverse_row(ctx, P, S, k, P->Lp.p, Xp, xs);
                 }
                 if (S.upd.count(k) + S.upd_far.count(k) > 0)
                     la.panel_end(
@@ -1265,6 +1212,14 @@ Prec* prec_build(Ctx* ctx, const DMatrix& W, const DofPartition& part, const Pro
             count_launch();
             SBG_LAUNCH_CHECK();
             SBG_CUDA(cudaStreamSynchronize(s));
+        }
+        if (need_inv) {  // the L^-1 chain's tail (its rows only read off-diagonal L tiles and D)
+            TimedScope ts(ctx, "inv_lower");
+            SBG_CUDA(cudaEventRecord(x_ev, xs));
+            SBG_CUDA(cudaStreamWaitEvent(s, x_ev, 0));
+            SBG_CUDA(cudaEventSynchronize(x_ev));
+            cudaEventDestroy(step_ev);
+            cudaEventDestroy(x_ev);
         }
         std::vector<int> hfail(fail.n);
         SBG_CUDA(cudaMemcpy(hfail.data(), fail.p, hfail.size() * sizeof(int), cudaMemcpyDeviceToHost));
@@ -1287,7 +1242,7 @@ Prec* prec_build(Ctx* ctx, const DMatrix& W, const DofPartition& part, const Pro
             if (P->factored) P->loct.alloc(P->loc.n);
             {
                 TimedScope ts(ctx, "block_inverse");
-                form_inverses(ctx, P, P->Lp, P->Mc, P->factored);
+                form_inverses(ctx, P, P->Lp, P->Mc, P->factored, true);
             }
             P->Lp.release();
             P->D.release();

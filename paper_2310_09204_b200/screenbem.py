@@ -15,7 +15,8 @@ from dataclasses import dataclass, field
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libscreenbem_b200.so")
+# SBG_LIB_PATH: an alternative build of the same library (A/B measurements of kernel variants)
+LIB_PATH = os.environ.get("SBG_LIB_PATH") or os.path.join(_HERE, "_lib", "libscreenbem_b200.so")
 
 
 class ValidationError(RuntimeError):

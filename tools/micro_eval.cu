@@ -28,6 +28,17 @@ __device__ __forceinline__ double rsqrt_poly_acc(double r2, double acc)
     return fma(y, p, acc);
 }
 
+// the library's form (kernels.cuh rsqrt_acc): y (1 + e (1/2 + 3e/8)) accumulated, 5 FP64 after the seed
+__device__ __forceinline__ double rsqrt_acc(double r2s, double acc)
+{
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(r2s));
+    const double h = r2s * y;
+    const double e = fma(-h, y, 1.0);
+    const double c = fma(0.375, e, 0.5);
+    return fma(y, fma(e, c, 1.0), acc);
+}
+
 template <int P, int UNROLL, int MODE = 0>
 __global__ void k_eval(double* out, int reps)
 {
@@ -64,6 +75,12 @@ __global__ void k_eval(double* out, int reps)
                     const double e = fma(-hh, y0, 1.0);
                     const double c = fma(0.375, e, 0.5);
                     a[r] = fma(wj, fma(y0, e * c, y0), a[r]);
+                } else if (MODE == 3) {  // library form, 3-D: 9 FP64 per evaluation
+                    const double r2 = fma(mx[r], y.x, fma(my[r], y.y, fma(mz[r], y.z, fma(x2[r], wj, y.w))));
+                    a[r] = rsqrt_acc(r2, a[r]);
+                } else if (MODE == 4) {  // library form, flat (one coordinate plane): 8 FP64
+                    const double r2 = fma(mx[r], y.x, fma(my[r], y.y, fma(x2[r], wj, y.w)));
+                    a[r] = rsqrt_acc(r2, a[r]);
                 } else {  // y = (y / w^2, |y|^2 / w^2), wj = 1 / w^2
                     const double r2 = fma(mx[r], y.x, fma(my[r], y.y, fma(mz[r], y.z, fma(x2[r], wj, y.w))));
                     a[r] = rsqrt_poly_acc(r2, a[r]);
@@ -192,6 +209,13 @@ int main()
     run<6, 2, 1>(256, 2, d, ghz);
     run<8, 2, 1>(256, 2, d, ghz);
     run<4, 2, 2>(256, 3, d, ghz);
+    run<4, 2, 3>(256, 3, d, ghz);
+    run<4, 2, 4>(256, 3, d, ghz);
+    run<4, 4, 4>(256, 3, d, ghz);
+    run<4, 2, 4>(256, 4, d, ghz);
+    run<6, 2, 4>(256, 2, d, ghz);
+    run<8, 2, 4>(256, 2, d, ghz);
+    run<4, 2, 4>(128, 8, d, ghz);
     run<8, 2, 2>(256, 2, d, ghz);
     mufu_rate(ghz);
     poly_error();
