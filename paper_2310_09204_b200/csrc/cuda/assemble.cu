@@ -726,11 +726,21 @@ __global__ void __launch_bounds__(NEAR_LEAF_THREADS, 2) k_near_leaves(const Near
                          e2z = vcoord(s, 2, P.z) - vcoord(s, 0, P.z);
             const double bx = vcoord(s, 0, P.x) - vcoord(t, 0, P.x), by = vcoord(s, 0, P.y) - vcoord(t, 0, P.y),
                          bz = vcoord(s, 0, P.z) - vcoord(t, 0, P.z);
-            for (int j = xg; j < NN; j += 4) {
-                const double yx = fma(c_near_v[j], e2x, fma(c_near_u[j], e1x, bx));
-                const double yy = fma(c_near_v[j], e2y, fma(c_near_u[j], e1y, by));
-                const double yz = fma(c_near_v[j], e2z, fma(c_near_u[j], e1z, bz));
-                Ys[j] = scaled_ypoint(yx, yy, yz, c_near_s[j]);
+            if (flat) {  // the same values with the zero coordinate left out
+                for (int j = xg; j < NN; j += 4) {
+                    const double yx = fma(c_near_v[j], e2x, fma(c_near_u[j], e1x, bx));
+                    const double yy = fma(c_near_v[j], e2y, fma(c_near_u[j], e1y, by));
+                    const double sj = c_near_s[j];
+                    Ys[j] = sj == 0.0 ? make_double4(0.0, 0.0, 0.0, kPadR2)
+                                      : make_double4(sj * yx, sj * yy, 0.0, sj * fma(yx, yx, yy * yy));
+                }
+            } else {
+                for (int j = xg; j < NN; j += 4) {
+                    const double yx = fma(c_near_v[j], e2x, fma(c_near_u[j], e1x, bx));
+                    const double yy = fma(c_near_v[j], e2y, fma(c_near_u[j], e1y, by));
+                    const double yz = fma(c_near_v[j], e2z, fma(c_near_u[j], e1z, bz));
+                    Ys[j] = scaled_ypoint(yx, yy, yz, c_near_s[j]);
+                }
             }
             f1x = vcoord(t, 1, P.x) - vcoord(t, 0, P.x), f1y = vcoord(t, 1, P.y) - vcoord(t, 0, P.y),
             f1z = vcoord(t, 1, P.z) - vcoord(t, 0, P.z);
@@ -752,11 +762,16 @@ __global__ void __launch_bounds__(NEAR_LEAF_THREADS, 2) k_near_leaves(const Near
                     const int i = NEAR_XP * g + r;
                     const double xx = fma(c_near_v[i], f2x, c_near_u[i] * f1x);
                     const double xy = fma(c_near_v[i], f2y, c_near_u[i] * f1y);
-                    const double xz = fma(c_near_v[i], f2z, c_near_u[i] * f1z);
-                    x2[r] = fma(xx, xx, fma(xy, xy, xz * xz));
+                    if (flat) {
+                        x2[r] = fma(xx, xx, xy * xy);
+                        mz[r] = 0.0;
+                    } else {
+                        const double xz = fma(c_near_v[i], f2z, c_near_u[i] * f1z);
+                        x2[r] = fma(xx, xx, fma(xy, xy, xz * xz));
+                        mz[r] = -2.0 * xz;
+                    }
                     mx[r] = -2.0 * xx;
                     my[r] = -2.0 * xy;
-                    mz[r] = -2.0 * xz;
                     a[r] = 0.0;
                 }
                 if (flat) {
@@ -915,7 +930,9 @@ struct SauterStride {
     static constexpr int value = CLS == 3 ? 4 : (CLS == 2 ? 8 : 5);  // 4, 8: 32-byte rows (LDS.128)
 };
 
-template <int CLS>
+// FLAT (vertex class): the four edge vectors have a zero last component (the pair lies in a
+// coordinate plane, axes ordered so that one is last): dz = 0 is left out, 10 FMA per point
+template <int CLS, bool FLAT = false>
 __device__ __forceinline__ double sauter_r2(const double* a, const double (&g)[12])
 {
     if (CLS == 3) return fma(a[0], g[0], fma(a[1], g[1], a[2] * g[2]));
@@ -923,8 +940,27 @@ __device__ __forceinline__ double sauter_r2(const double* a, const double (&g)[1
         return fma(a[0], g[0], fma(a[1], g[1], fma(a[2], g[2], fma(a[3], g[3], fma(a[4], g[4], a[5] * g[5])))));
     const double dx = fma(-a[3], g[9], fma(-a[2], g[6], fma(a[1], g[3], a[0] * g[0])));
     const double dy = fma(-a[3], g[10], fma(-a[2], g[7], fma(a[1], g[4], a[0] * g[1])));
+    if (FLAT) return fma(dx, dx, dy * dy);
     const double dz = fma(-a[3], g[11], fma(-a[2], g[8], fma(a[1], g[5], a[0] * g[2])));
     return fma(dx, dx, fma(dy, dy, dz * dz));
+}
+
+// one stage of rule points, four independent evaluations per step
+template <int CLS, bool FLAT, int ST>
+__device__ __forceinline__ void sauter_stage(const double* __restrict__ R, int cnt, const double (&g)[12],
+                                             double& acc0, double& acc1, double& acc2, double& acc3)
+{
+    int i = 0;
+    for (; i + 4 <= cnt; i += 4) {
+        double r2[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) r2[u] = sauter_r2<CLS, FLAT>(R + ST * (i + u), g);
+        acc0 = fma(R[ST * i + ST - 1], rsqrt_fast(r2[0]), acc0);
+        acc1 = fma(R[ST * (i + 1) + ST - 1], rsqrt_fast(r2[1]), acc1);
+        acc2 = fma(R[ST * (i + 2) + ST - 1], rsqrt_fast(r2[2]), acc2);
+        acc3 = fma(R[ST * (i + 3) + ST - 1], rsqrt_fast(r2[3]), acc3);
+    }
+    for (; i < cnt; ++i) acc0 = fma(R[ST * i + ST - 1], rsqrt_fast(sauter_r2<CLS, FLAT>(R + ST * i, g)), acc0);
 }
 
 template <int CLS>
@@ -938,6 +974,7 @@ __global__ void __launch_bounds__(SAUTER_THREADS)
     const int p = blockIdx.x * blockDim.x + threadIdx.x;
     const bool active = p < npairs;
     double g[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};  // vertex: e1t, e2t, e1s, e2s; else Gram entries
+    bool flat = false;
     if (active) {
         const int* q = pv + 6 * p;
         const double* t0 = X + 3 * q[0];
@@ -967,10 +1004,23 @@ __global__ void __launch_bounds__(SAUTER_THREADS)
             g[4] = dot(0, 9);
             g[5] = dot(3, 9);
         } else {
+            // a pair in a coordinate plane: that axis last, its components all exact zeros
+            int fa = -1;
 #pragma unroll
-            for (int k = 0; k < 12; ++k) g[k] = e[k];
+            for (int c = 0; c < 3; ++c)
+                if (e[c] == 0.0 && e[3 + c] == 0.0 && e[6 + c] == 0.0 && e[9 + c] == 0.0) fa = c;
+            flat = fa >= 0;
+            const int px = fa == 0 ? 1 : 0, py = fa == 2 || fa < 0 ? 1 : 2, pz = fa < 0 ? 2 : fa;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const double v[3] = {e[3 * k], e[3 * k + 1], e[3 * k + 2]};
+                g[3 * k] = px == 0 ? v[0] : v[1];
+                g[3 * k + 1] = py == 1 ? v[1] : v[2];
+                g[3 * k + 2] = pz == 0 ? v[0] : (pz == 1 ? v[1] : v[2]);
+            }
         }
     }
+    if (CLS == 1) flat = __syncthreads_and(flat || !active);  // CTA-uniform loop form
     const int q0 = blockIdx.y * chunk, q1 = min(npts, q0 + chunk);
     double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
     for (int base = q0; base < q1; base += STAGE) {
@@ -979,18 +1029,10 @@ __global__ void __launch_bounds__(SAUTER_THREADS)
         for (int k = threadIdx.x; k < cnt * ST; k += blockDim.x) R[k] = rule[(size_t)base * ST + k];
         __syncthreads();
         if (active) {
-            int i = 0;
-            // four independent evaluations per step
-            for (; i + 4 <= cnt; i += 4) {
-                double r2[4];
-#pragma unroll
-                for (int u = 0; u < 4; ++u) r2[u] = sauter_r2<CLS>(R + ST * (i + u), g);
-                acc0 = fma(R[ST * i + ST - 1], rsqrt_fast(r2[0]), acc0);
-                acc1 = fma(R[ST * (i + 1) + ST - 1], rsqrt_fast(r2[1]), acc1);
-                acc2 = fma(R[ST * (i + 2) + ST - 1], rsqrt_fast(r2[2]), acc2);
-                acc3 = fma(R[ST * (i + 3) + ST - 1], rsqrt_fast(r2[3]), acc3);
-            }
-            for (; i < cnt; ++i) acc0 = fma(R[ST * i + ST - 1], rsqrt_fast(sauter_r2<CLS>(R + ST * i, g)), acc0);
+            if (CLS == 1 && flat)
+                sauter_stage<CLS, true, ST>(R, cnt, g, acc0, acc1, acc2, acc3);
+            else
+                sauter_stage<CLS, false, ST>(R, cnt, g, acc0, acc1, acc2, acc3);
         }
     }
     if (active) part[(size_t)blockIdx.y * npairs + p] = (acc0 + acc1) + (acc2 + acc3);
