@@ -675,7 +675,11 @@ constexpr int NEAR_LEAF_THREADS = 256;
 constexpr int kNearFlatUnroll = NEAR_FLAT_UNROLL;  // the flat leaf loop's unroll (A/B builds)
 constexpr int NEAR_XP = 4;  // x points per pass (register block)
 constexpr int NEAR_LEAF_WARPS = NEAR_LEAF_THREADS / 32;
-constexpr size_t NEAR_LEAF_SMEM = (size_t)NEAR_LEAF_WARPS * 8 * NN * sizeof(double4);
+// one leaf's staged y points: npts double4 plus 16 bytes, so the eight leaves of a warp,
+// read together by one LDS.128, start in eight different 16-byte bank groups (a plain
+// 36 x 32-byte stride is a multiple of 128 bytes: an 8-way bank conflict on every load)
+__host__ __device__ constexpr size_t leaf_stage_bytes(int npts) { return (size_t)npts * sizeof(double4) + 16; }
+constexpr size_t NEAR_LEAF_SMEM = (size_t)NEAR_LEAF_WARPS * 8 * leaf_stage_bytes(NN);
 __global__ void __launch_bounds__(NEAR_LEAF_THREADS, 2) k_near_leaves(const NearNode* __restrict__ leaves,
                                                                        const unsigned long long* __restrict__ nleaves_dev,
                                                                        long long cap, const int2* __restrict__ pairs,
@@ -686,7 +690,7 @@ __global__ void __launch_bounds__(NEAR_LEAF_THREADS, 2) k_near_leaves(const Near
     extern __shared__ __align__(16) unsigned char near_smem[];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int h = lane >> 2, xg = lane & 3;
-    double4* Ys = reinterpret_cast<double4*>(near_smem) + ((size_t)wib * 8 + h) * NN;
+    double4* Ys = reinterpret_cast<double4*>(near_smem + ((size_t)wib * 8 + h) * leaf_stage_bytes(NN));
     const long long nl = min((long long)*nleaves_dev, cap);
     const long long warps = (long long)gridDim.x * NEAR_LEAF_WARPS;
     for (long long w = (long long)blockIdx.x * NEAR_LEAF_WARPS + wib; 8 * w < nl; w += warps) {
@@ -823,7 +827,7 @@ __global__ void __launch_bounds__(NEAR_G_THREADS) k_near_leaves_g(const NearNode
     constexpr int WARPS = NEAR_G_THREADS / 32;
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int h = lane >> 2, xg = lane & 3;
-    double4* Ys = reinterpret_cast<double4*>(near_g_smem) + ((size_t)wib * 8 + h) * NNP;
+    double4* Ys = reinterpret_cast<double4*>(near_g_smem + ((size_t)wib * 8 + h) * leaf_stage_bytes(NNP));
     const long long nl = min((long long)*nleaves_dev, cap);
     const long long warps = (long long)gridDim.x * WARPS;
     for (long long w = (long long)blockIdx.x * WARPS + wib; 8 * w < nl; w += warps) {
@@ -905,7 +909,7 @@ template <int NNP>
 void launch_near_leaves_g(Ctx* ctx, const NearNode* leaves, const unsigned long long* cnt, long long ncur,
                           const int2* pairs, const double* GV, const double* GA, double* out)
 {
-    const size_t smem = (size_t)(NEAR_G_THREADS / 32) * 8 * NNP * sizeof(double4);
+    const size_t smem = (size_t)(NEAR_G_THREADS / 32) * 8 * leaf_stage_bytes(NNP);
     set_max_dynamic_smem(k_near_leaves_g<NNP>, smem);
     const long long warps = (ncur + 7) / 8;
     const int grid = (int)std::min<long long>((warps + NEAR_G_THREADS / 32 - 1) / (NEAR_G_THREADS / 32),
