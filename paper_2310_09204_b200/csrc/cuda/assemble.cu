@@ -226,6 +226,74 @@ __device__ void tile_contract_flush(const double* __restrict__ It, int fb, int g
     }
 }
 
+// Two-stage contraction of the I tile (the default far path): W(a,b) = sum_k sum_{p in a}
+// u_pk V_k(f_p, b)... computed as V_k(a, g) = sum_{p in E_a} u_pk I(f_p, g) (stage A, into
+// shared memory, 32 DOFs of the f block at a time) and W(a,b) += sum_{q in E_b} V_k(a, g_q)
+// u_qk (stage B, register accumulators kept over the three components k), ~2.3x fewer
+// FP64 operations and no per-(p,q) dot products against the direct double loop; W(a,b)
+// is the same sum up to the association of its terms.  Needs nbd <= 64 DOFs in the g block
+// and 32 x 64 doubles of dead shared memory (vbuf); returns false (nothing done) otherwise.
+constexpr int CT_CH = 32;  // f-block DOFs per stage-A round
+__device__ bool tile_contract_flush_2stage(const double* __restrict__ It, int fb, int gb, bool diag,
+                                           const BlockPtrs& B, double* __restrict__ W, int ld,
+                                           double* __restrict__ vbuf, size_t vbuf_bytes)
+{
+    const int fa0 = B.dof_ptr[fb], na = B.dof_ptr[fb + 1] - fa0;
+    const int gb0 = B.dof_ptr[gb], nbd = B.dof_ptr[gb + 1] - gb0;
+    if (nbd > BS || vbuf_bytes < (size_t)CT_CH * BS * sizeof(double)) return false;
+    const int t = threadIdx.x;
+    const int col = t & (BS - 1), row0 = t >> 6;  // 256 threads: 4 rows x 64 columns per sweep
+    constexpr int RPT = CT_CH / 4;                // rows of a round per thread
+    for (int a0 = 0; a0 < na; a0 += CT_CH) {
+        const int ca = min(CT_CH, na - a0);
+        double acc[RPT];
+#pragma unroll
+        for (int i = 0; i < RPT; ++i) acc[i] = 0.0;
+        // E_b of this thread's column b (its g-block entries)
+        const int q0 = col < nbd ? B.ent_ptr[gb0 + col] : 0, q1 = col < nbd ? B.ent_ptr[gb0 + col + 1] : 0;
+#pragma unroll 1
+        for (int k = 0; k < 3; ++k) {
+            // stage A: vbuf[al][g] = sum_{p in E_(a0+al)} u_pk I(f_p, g), g = col
+#pragma unroll
+            for (int i = 0; i < RPT; ++i) {
+                const int al = row0 + 4 * i;
+                double v = 0.0;
+                if (al < ca) {
+                    const int p0 = B.ent_ptr[fa0 + a0 + al], p1 = B.ent_ptr[fa0 + a0 + al + 1];
+                    for (int p = p0; p < p1; ++p) {
+                        const double4 e = B.ents[p];  // uniform over the 64 threads of the row
+                        const double u = k == 0 ? e.x : (k == 1 ? e.y : e.z);
+                        v = fma(u, It[(int)e.w * (BS + 1) + col], v);
+                    }
+                }
+                vbuf[al * BS + col] = v;
+            }
+            __syncthreads();
+            // stage B: acc[i] += sum_{q in E_b} vbuf[al][g_q] u_qk, b = col
+            for (int q = q0; q < q1; ++q) {
+                const double4 e = B.ents[q];
+                const double u = k == 0 ? e.x : (k == 1 ? e.y : e.z);
+                const double* vc = vbuf + (int)e.w;
+#pragma unroll
+                for (int i = 0; i < RPT; ++i) acc[i] = fma(vc[(row0 + 4 * i) * BS], u, acc[i]);
+            }
+            __syncthreads();
+        }
+        if (col < nbd) {
+            const int db = B.dofs[gb0 + col];
+#pragma unroll
+            for (int i = 0; i < RPT; ++i) {
+                const int al = row0 + 4 * i;
+                if (al >= ca) continue;
+                const int da = B.dofs[fa0 + a0 + al];
+                if (diag && da > db) continue;
+                flush_entry(W, ld, diag, da, db, acc[i]);
+            }
+        }
+    }
+    return true;
+}
+
 // Far pairs with the distance expansion |x-y|^2 = |x|^2 + |y|^2 - 2 x.y in
 // tile-local coordinates (origin o = first vertex of the tile's first f-facet):
 // per evaluation DADD + 3 DFMA instead of 3 DADD + DMUL + 2 DFMA.  Each lane keeps
@@ -456,7 +524,10 @@ __global__ void __launch_bounds__(FAR_THREADS, 3)
         }
         __syncthreads();
     }
-    // the staged y points are dead: their shared memory takes the curl-list entries
+    // the staged y points are dead: their shared memory takes the contraction's buffers
+    if (!EXACT && tile_contract_flush_2stage(It, T.fb, T.gb, diag, B, W, ld, reinterpret_cast<double*>(Ys),
+                                             (size_t)BS * NFP * sizeof(double4)))
+        return;
     tile_contract_flush(It, T.fb, T.gb, diag, B, W, ld, EXACT ? nullptr : reinterpret_cast<unsigned char*>(Ys),
                         EXACT ? 0 : (size_t)BS * NFP * sizeof(double4));
 }
