@@ -78,6 +78,18 @@ __constant__ double c_far_s[NF_MAX], c_near_s[NN_MAX];
 // the barycentric weights (x32, exact dyadics) of the leaf vertices on the root vertices
 constexpr int NPATH = 1365;
 __constant__ unsigned char c_paths[NPATH * 9];
+// the same near rule and path tables in global memory: read through L1 (__ldg) where the lanes
+// of a warp index them divergently (the constant cache serialises distinct addresses)
+__device__ double g_near_u[NN_MAX], g_near_v[NN_MAX], g_near_s[NN_MAX], g_near_w[NN_MAX];
+__device__ unsigned char g_paths[NPATH * 9];
+#ifndef NEAR_GLOBAL_TABLES
+#define NEAR_GLOBAL_TABLES 1
+#endif
+#if NEAR_GLOBAL_TABLES
+#define NEAR_TAB(name, i) __ldg(&g_##name[i])
+#else
+#define NEAR_TAB(name, i) c_##name[i]
+#endif
 
 // ---------------------------------------------------------------- facet geometry
 struct GeoPtrs {
@@ -698,12 +710,15 @@ __global__ void k_near_level(const NearNode* __restrict__ nodes, const unsigned 
 }
 
 // leaf vertices from the root triangle and the composed barycentric map of a path
+template <bool GLOBAL_TAB = false>
 __device__ __forceinline__ void path_triangle(const double* __restrict__ root, int path, double* out)
 {
-    const unsigned char* B = c_paths + 9 * path;
+    const unsigned char* B = (GLOBAL_TAB ? g_paths : c_paths) + 9 * path;
 #pragma unroll
     for (int r = 0; r < 3; ++r) {
-        const double w0 = B[3 * r] * (1.0 / 32), w1 = B[3 * r + 1] * (1.0 / 32), w2 = B[3 * r + 2] * (1.0 / 32);
+        const double w0 = (GLOBAL_TAB ? __ldg(B + 3 * r) : B[3 * r]) * (1.0 / 32),
+                     w1 = (GLOBAL_TAB ? __ldg(B + 3 * r + 1) : B[3 * r + 1]) * (1.0 / 32),
+                     w2 = (GLOBAL_TAB ? __ldg(B + 3 * r + 2) : B[3 * r + 2]) * (1.0 / 32);
 #pragma unroll
         for (int c = 0; c < 3; ++c) out[3 * r + c] = fma(w2, root[6 + c], fma(w1, root[3 + c], w0 * root[c]));
     }
@@ -789,8 +804,8 @@ __global__ void __launch_bounds__(NEAR_LEAF_THREADS, 2) k_near_leaves(const Near
                 }
             }
             double t[9], s[9];
-            path_triangle(GV + 9 * pr.x, ((1 << 2 * dt) - 1) / 3 + it, t);
-            path_triangle(GV + 9 * pr.y, ((1 << 2 * ds) - 1) / 3 + is, s);
+            path_triangle<NEAR_GLOBAL_TABLES>(GV + 9 * pr.x, ((1 << 2 * dt) - 1) / 3 + it, t);
+            path_triangle<NEAR_GLOBAL_TABLES>(GV + 9 * pr.y, ((1 << 2 * ds) - 1) / 3 + is, s);
             scale = __ldg(GA + pr.x) * __ldg(GA + pr.y) * ldexp(inv_pi, -2 * (dt + ds));
             // a leaf pair in one coordinate plane: that axis goes last, all its leaf-local
             // coordinates are exact zeros and the evaluation leaves its term out (far_pass_sum)
@@ -803,18 +818,18 @@ __global__ void __launch_bounds__(NEAR_LEAF_THREADS, 2) k_near_leaves(const Near
                          bz = vcoord(s, 0, P.z) - vcoord(t, 0, P.z);
             if (flat) {  // the same values with the zero coordinate left out
                 for (int j = xg; j < NN; j += 4) {
-                    const double yx = fma(c_near_v[j], e2x, fma(c_near_u[j], e1x, bx));
-                    const double yy = fma(c_near_v[j], e2y, fma(c_near_u[j], e1y, by));
-                    const double sj = c_near_s[j];
+                    const double yx = fma(NEAR_TAB(near_v, j), e2x, fma(NEAR_TAB(near_u, j), e1x, bx));
+                    const double yy = fma(NEAR_TAB(near_v, j), e2y, fma(NEAR_TAB(near_u, j), e1y, by));
+                    const double sj = NEAR_TAB(near_s, j);
                     Ys[j] = sj == 0.0 ? make_double4(0.0, 0.0, 0.0, kPadR2)
                                       : make_double4(sj * yx, sj * yy, 0.0, sj * fma(yx, yx, yy * yy));
                 }
             } else {
                 for (int j = xg; j < NN; j += 4) {
-                    const double yx = fma(c_near_v[j], e2x, fma(c_near_u[j], e1x, bx));
-                    const double yy = fma(c_near_v[j], e2y, fma(c_near_u[j], e1y, by));
-                    const double yz = fma(c_near_v[j], e2z, fma(c_near_u[j], e1z, bz));
-                    Ys[j] = scaled_ypoint(yx, yy, yz, c_near_s[j]);
+                    const double yx = fma(NEAR_TAB(near_v, j), e2x, fma(NEAR_TAB(near_u, j), e1x, bx));
+                    const double yy = fma(NEAR_TAB(near_v, j), e2y, fma(NEAR_TAB(near_u, j), e1y, by));
+                    const double yz = fma(NEAR_TAB(near_v, j), e2z, fma(NEAR_TAB(near_u, j), e1z, bz));
+                    Ys[j] = scaled_ypoint(yx, yy, yz, NEAR_TAB(near_s, j));
                 }
             }
             f1x = vcoord(t, 1, P.x) - vcoord(t, 0, P.x), f1y = vcoord(t, 1, P.y) - vcoord(t, 0, P.y),
@@ -835,13 +850,13 @@ __global__ void __launch_bounds__(NEAR_LEAF_THREADS, 2) k_near_leaves(const Near
 #pragma unroll
                 for (int r = 0; r < NEAR_XP; ++r) {
                     const int i = NEAR_XP * g + r;
-                    const double xx = fma(c_near_v[i], f2x, c_near_u[i] * f1x);
-                    const double xy = fma(c_near_v[i], f2y, c_near_u[i] * f1y);
+                    const double xx = fma(NEAR_TAB(near_v, i), f2x, NEAR_TAB(near_u, i) * f1x);
+                    const double xy = fma(NEAR_TAB(near_v, i), f2y, NEAR_TAB(near_u, i) * f1y);
                     if (flat) {
                         x2[r] = fma(xx, xx, xy * xy);
                         mz[r] = 0.0;
                     } else {
-                        const double xz = fma(c_near_v[i], f2z, c_near_u[i] * f1z);
+                        const double xz = fma(NEAR_TAB(near_v, i), f2z, NEAR_TAB(near_u, i) * f1z);
                         x2[r] = fma(xx, xx, fma(xy, xy, xz * xz));
                         mz[r] = -2.0 * xz;
                     }
@@ -873,7 +888,7 @@ __global__ void __launch_bounds__(NEAR_LEAF_THREADS, 2) k_near_leaves(const Near
                     }
                 }
 #pragma unroll
-                for (int r = 0; r < NEAR_XP; ++r) acc = fma(c_near_w[NEAR_XP * g + r], a[r], acc);
+                for (int r = 0; r < NEAR_XP; ++r) acc = fma(NEAR_TAB(near_w, NEAR_XP * g + r), a[r], acc);
             }
         }
         for (int o = 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
@@ -1330,6 +1345,10 @@ RuleDims upload_rules(Ctx* ctx, const QuadCfg& cfg)
     rb += 3 * NN_MAX;
     SBG_CUDA(cudaMemcpyToSymbolAsync(c_far_s, rb, NF_MAX * sizeof(double), 0, cudaMemcpyHostToDevice, s));
     SBG_CUDA(cudaMemcpyToSymbolAsync(c_near_s, rb + NF_MAX, NN_MAX * sizeof(double), 0, cudaMemcpyHostToDevice, s));
+    SBG_CUDA(cudaMemcpyToSymbolAsync(g_near_u, rb - 3 * NN_MAX, NN_MAX * sizeof(double), 0, cudaMemcpyHostToDevice, s));
+    SBG_CUDA(cudaMemcpyToSymbolAsync(g_near_v, rb - 2 * NN_MAX, NN_MAX * sizeof(double), 0, cudaMemcpyHostToDevice, s));
+    SBG_CUDA(cudaMemcpyToSymbolAsync(g_near_w, rb - NN_MAX, NN_MAX * sizeof(double), 0, cudaMemcpyHostToDevice, s));
+    SBG_CUDA(cudaMemcpyToSymbolAsync(g_near_s, rb + NF_MAX, NN_MAX * sizeof(double), 0, cudaMemcpyHostToDevice, s));
     // composed split4 maps (quadrature.hpp:222-229 child order), weights x32
     static const std::vector<unsigned char> paths = [] {
         std::vector<unsigned char> paths(NPATH * 9);
@@ -1366,6 +1385,7 @@ RuleDims upload_rules(Ctx* ctx, const QuadCfg& cfg)
         return paths;
     }();
     SBG_CUDA(cudaMemcpyToSymbolAsync(c_paths, paths.data(), paths.size(), 0, cudaMemcpyHostToDevice, s));
+    SBG_CUDA(cudaMemcpyToSymbolAsync(g_paths, paths.data(), paths.size(), 0, cudaMemcpyHostToDevice, s));
     return R;
 }
 

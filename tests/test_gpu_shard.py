@@ -90,3 +90,45 @@ def test_packed_upper_triangle_roundtrip_and_shard_sum():
     Wsum = W2.download()
     assert np.abs(Wsum - Wh).max() <= 1e-13 * np.abs(Wh).max()
     assert np.array_equal(Wsum, Wsum.T)
+
+
+def _shard_worker(rank, world, port, spec, out):
+    """one rank of a sharded assembly: its share of the pair work on the (shared) GPU, the
+    partial W reduced over the ranks with gloo through host memory (bench.allreduce_sum_)"""
+    import os
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch
+    import torch.distributed as dist
+    import bench
+    from paper_2310_09204_b200 import screenbem as S2
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    ctx = S2.Context(0)
+    m = S2.make_config(1).fine if spec == "config1" else S2.make_builtin(spec)
+    plan = S2.AssemblyPlan(S2.inflate(m), ctx=ctx)
+    W = plan.run(shard=(rank, world))
+    t = torch.from_numpy(W.download())
+    bench.allreduce_sum_(t, dist, "cpu")
+    out[rank] = t.numpy()
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.timeout(600)
+@pytest.mark.parametrize("spec", ["config1", "bowtie:3"])
+def test_two_process_sharded_assembly_gloo(ctx, spec):
+    """Two processes (gloo, world size 2, both on this GPU) each assemble their shard and
+    sum the partial W over the ranks: every rank ends with the single-process W within
+    the reference's worker-reorder bound (tests/test_assemble.cpp:271-279)."""
+    import socket
+    import torch.multiprocessing as mp
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    m = S.make_config(1).fine if spec == "config1" else S.make_builtin(spec)
+    Wf = S.AssemblyPlan(S.inflate(m), ctx=ctx).run().download()
+    out = mp.Manager().dict()
+    mp.spawn(_shard_worker, args=(2, port, spec, out), nprocs=2, join=True)
+    for rank in range(2):
+        Wr = out[rank]
+        assert np.abs(Wr - Wf).max() <= 1e-13 * np.abs(Wf).max(), (rank, np.abs(Wr - Wf).max())
+        assert np.array_equal(Wr, Wr.T)
