@@ -790,9 +790,10 @@ __global__ void __launch_bounds__(256) k_prec_scatter_rz(PcgDev* st, const doubl
 }
 
 // H = R^T W R (schwarz.hpp:110-116 with the sparse R) into a padded ldh x ldh block
+// sync: wait for the kernels on the host (the build enqueues them and goes on)
 void coarse_galerkin_device(Ctx* ctx, const DMatrix& W, const std::vector<int>& col_ptr,
                             const std::vector<int>& row_idx, const int* cptr, const int* crow, const double* cval,
-                            int nc, int ldh, double* H)
+                            int nc, int ldh, double* H, bool sync = true)
 {
     const int n = W.n;
     cudaStream_t s = ctx->stream;
@@ -822,14 +823,14 @@ void coarse_galerkin_device(Ctx* ctx, const DMatrix& W, const std::vector<int>& 
         k_coarse_WR_reduce<<<dim3((n + 255) / 256, nc), 256, 0, s>>>(part, d_cfirst.p, n, WRt);
         count_launch();
         SBG_LAUNCH_CHECK();
-        SBG_CUDA(cudaStreamSynchronize(s));
+        if (sync) SBG_CUDA(cudaStreamSynchronize(s));  // (the task lists' frees are stream-ordered)
     } else {
         SBG_CUDA(cudaMemsetAsync(WRt, 0, (size_t)n * std::max(nc, 1) * sizeof(double), s));
     }
     k_coarse_Ht<<<ldh, 256, 0, s>>>(WRt, n, cptr, crow, cval, nc, ldh, H);
     count_launch();
     SBG_LAUNCH_CHECK();
-    SBG_CUDA(cudaStreamSynchronize(s));
+    if (sync) SBG_CUDA(cudaStreamSynchronize(s));
 }
 
 // far = a look-ahead far update: its CTAs reserve FAR_SMEM of shared memory, so at most one
@@ -1136,7 +1137,6 @@ Prec* prec_build(Ctx* ctx, const DMatrix& W, const DofPartition& part, const Pro
                                                                  P->d_Poff.p, S.d_gather.p, P->Lp.p);
             count_launch();
             SBG_LAUNCH_CHECK();
-            SBG_CUDA(cudaStreamSynchronize(s));
         }
         if (P->nc > 0) {  // R^T W R with the sparse R (schwarz.hpp:110-116)
             P->Rc_ptr.upload(R.col_ptr, s);
@@ -1161,7 +1161,7 @@ Prec* prec_build(Ctx* ctx, const DMatrix& W, const DofPartition& part, const Pro
             TimedScope ts(ctx, "coarse_galerkin");
             const int ldh = P->h_T[P->coarse_block] * TB;
             coarse_galerkin_device(ctx, W, R.col_ptr, R.row_idx, P->Rc_ptr.p, P->Rc_row.p, P->Rc_val.p, P->nc, ldh,
-                                   P->Lp.p + P->h_Poff[P->coarse_block]);
+                                   P->Lp.p + P->h_Poff[P->coarse_block], /*sync=*/false);
         }
         // ---- batched tiled Cholesky: per step k, potrf of tile (k,k), trsm of column k, trailing update
         DBuf<int> fail(std::max(P->nblocks, 1));
