@@ -18,6 +18,7 @@
 //   Near and singular pair integrals are scattered per pair; W is accumulated
 //   in its upper triangle and mirrored at the end (assemble.hpp:136-137).
 #include <algorithm>
+#include <array>
 #include <cstring>
 #include <optional>
 #include <cmath>
@@ -1489,7 +1490,9 @@ struct SingularLists {
 // vertex-adjacent (f, g <= f) pairs with the permutation of pair_integral
 // (quadrature.hpp:297-322): t = facet f (the larger index), shared vertices first in f's
 // order, the rest ascending.
-void singular_pairs(const SurfaceMesh& m, SingularLists& S)
+// returns the lists of consecutive facet ranges (built on up to 8 threads); their
+// concatenation in range order is the single-pass list of every class
+std::vector<SingularLists> singular_pairs(const SurfaceMesh& m)
 {
     const int nf = m.num_facets(), nv = m.num_vertices();
     std::vector<int> sptr(nv + 1, 0), sfac(3 * (size_t)nf);  // vertex -> facets (CSR, ascending)
@@ -1546,26 +1549,13 @@ void singular_pairs(const SurfaceMesh& m, SingularLists& S)
     // runs beside the plan's main thread (assembly_plan_create); facet ranges on a few
     // threads, each class list concatenated in range order (= the single-pass lists)
     const int nt = std::max(1, std::min(8, nf / 1024));
-    if (nt == 1) {
-        range(0, nf, S);
-        return;
-    }
     std::vector<SingularLists> parts(nt);
     std::vector<std::thread> th;
     for (int t = 1; t < nt; ++t)
         th.emplace_back(range, (int)((long long)nf * t / nt), (int)((long long)nf * (t + 1) / nt), std::ref(parts[t]));
     range(0, (int)((long long)nf / nt), parts[0]);
     for (auto& t : th) t.join();
-    for (int c = 1; c <= 3; ++c) {
-        size_t np = 0;
-        for (const auto& q : parts) np += q.pairs[c].size();
-        S.pairs[c].reserve(np);
-        S.pv[c].reserve(6 * np);
-        for (const auto& q : parts) {
-            S.pairs[c].insert(S.pairs[c].end(), q.pairs[c].begin(), q.pairs[c].end());
-            S.pv[c].insert(S.pv[c].end(), q.pv[c].begin(), q.pv[c].end());
-        }
-    }
+    return parts;  // (no concatenation: the plan uploads the parts at their offsets)
 }
 
 struct SauterRulesDev {
@@ -1989,9 +1979,7 @@ AssemblyPlan* assembly_plan_create(Ctx* ctx, const InflatedMesh& im, const QuadC
         // host preparation that depends only on the mesh runs beside the main thread:
         // the singular lists (vertex adjacency) and the curl lists
         auto sing_fut = std::async(std::launch::async, [&m] {
-            SingularLists S;
-            singular_pairs(m, S);
-            return S;
+            return singular_pairs(m);
         });
         auto curl_fut = std::async(std::launch::async, [&im] { return facet_curls(im); });
         P->st = std::make_unique<Stager>(ctx);
@@ -2058,30 +2046,42 @@ AssemblyPlan* assembly_plan_create(Ctx* ctx, const InflatedMesh& im, const QuadC
         HostScope hs2(ctx, "plan_tiles");
         // ---- tiles (fb >= gb); certainly-far tiles skip per-pair classification
         const double thr = cfg.near_threshold;
-        std::vector<TileInfo> tiles, cand;
-        tiles.reserve((size_t)nblk * (nblk + 1) / 2);
         const double margin = 1e-9 * std::max(1.0, dmax);
-        for (int fb = 0; fb < nblk; ++fb)
-            for (int gb = 0; gb <= fb; ++gb) {
-                const double dx = bcx[fb] - bcx[gb], dy = bcy[fb] - bcy[gb], dz = bcz[fb] - bcz[gb];
-                // any pair: dist_estimate >= D - R_f - R_g - 2 rmax >= thr * dmax (and no shared vertex)
-                const double lower = std::sqrt(dx * dx + dy * dy + dz * dz) - brad[fb] - brad[gb] - 2.0 * rmax;
-                const bool certain =
-                    fb != gb && lower > margin && lower >= std::max(0.0, thr) * dmax * (1.0 + 1e-9) + margin;
-                tiles.push_back({fb, gb, certain ? 1 : 0, 0});
-                if (!certain) cand.push_back({fb, gb, 0, 0});
-            }
         // launch order: full-cost tiles first (certain-far, off-diagonal), then the tiles with
         // per-pair tests and near pairs skipped, diagonal (half) tiles last, so the grid's
-        // last wave holds the cheapest tiles (stable: fb-major within each class)
-        {  // = stable_sort by class: three buckets filled in generation order
-            std::vector<TileInfo> sorted;
-            sorted.reserve(tiles.size());
-            for (int r = 0; r < 3; ++r)
-                for (const TileInfo& t : tiles)
-                    if ((t.fb == t.gb ? 2 : (t.certain_far ? 0 : 1)) == r) sorted.push_back(t);
-            tiles.swap(sorted);
+        // last wave holds the cheapest tiles (stable: fb-major within each class).  Generated
+        // on host threads by fb ranges of equal pair counts into per-range class buckets,
+        // concatenated in range order: the stable sort's order, and the candidate list's.
+        const int nth = (int)std::min<long long>(8, std::max<long long>(1, (long long)nblk * nblk / 20000));
+        std::vector<int> fb_cut(nth + 1, nblk);
+        fb_cut[0] = 0;
+        for (int t = 1; t < nth; ++t)  // fb^2 / 2 pairs below fb: equal-work cuts
+            fb_cut[t] = std::min(nblk, (int)std::lround(nblk * std::sqrt((double)t / nth)));
+        std::vector<std::array<std::vector<TileInfo>, 4>> part(nth);  // classes 0-2, candidates
+        auto gen = [&](int t) {
+            auto& B = part[t];
+            for (int fb = fb_cut[t]; fb < fb_cut[t + 1]; ++fb)
+                for (int gb = 0; gb <= fb; ++gb) {
+                    const double dx = bcx[fb] - bcx[gb], dy = bcy[fb] - bcy[gb], dz = bcz[fb] - bcz[gb];
+                    // any pair: dist_estimate >= D - R_f - R_g - 2 rmax >= thr * dmax (and no shared vertex)
+                    const double lower = std::sqrt(dx * dx + dy * dy + dz * dz) - brad[fb] - brad[gb] - 2.0 * rmax;
+                    const bool certain =
+                        fb != gb && lower > margin && lower >= std::max(0.0, thr) * dmax * (1.0 + 1e-9) + margin;
+                    B[fb == gb ? 2 : (certain ? 0 : 1)].push_back({fb, gb, certain ? 1 : 0, 0});
+                    if (!certain) B[3].push_back({fb, gb, 0, 0});
+                }
+        };
+        {
+            std::vector<std::thread> th;
+            for (int t = 1; t < nth; ++t) th.emplace_back(gen, t);
+            gen(0);
+            for (auto& x : th) x.join();
         }
+        std::vector<TileInfo> tiles, cand;
+        tiles.reserve((size_t)nblk * (nblk + 1) / 2);
+        for (int r = 0; r < 3; ++r)
+            for (int t = 0; t < nth; ++t) tiles.insert(tiles.end(), part[t][r].begin(), part[t][r].end());
+        for (int t = 0; t < nth; ++t) cand.insert(cand.end(), part[t][3].begin(), part[t][3].end());
         st.upload(P->bfac, bfac);
         st.upload(P->tiles, tiles);
         st.upload(P->cand, cand);
@@ -2090,14 +2090,15 @@ AssemblyPlan* assembly_plan_create(Ctx* ctx, const InflatedMesh& im, const QuadC
         HostScope hs3(ctx, "plan_singular");
         // ---- singular lists (host adjacency, deterministic order) and Sauter workspaces
         std::optional<HostScope> hs_sw(std::in_place, ctx, "plan_singular_wait");
-        SingularLists S = sing_fut.get();
+        const std::vector<SingularLists> SP = sing_fut.get();
         hs_sw.reset();
         P->SR = device_sauter(ctx, cfg);
         P->near_cap = std::max<long long>(1024, 64LL * nf);
         long long off = 0;
         for (int cls = 1; cls <= 3; ++cls) {
             P->cls_off[cls] = off;
-            P->cls_cnt[cls] = (long long)S.pairs[cls].size();
+            P->cls_cnt[cls] = 0;
+            for (const auto& q : SP) P->cls_cnt[cls] += (long long)q.pairs[cls].size();
             off += P->cls_cnt[cls];
         }
         P->nsing = off;
@@ -2106,8 +2107,14 @@ AssemblyPlan* assembly_plan_create(Ctx* ctx, const InflatedMesh& im, const QuadC
         for (int cls = 1; cls <= 3; ++cls) {
             const long long np = P->cls_cnt[cls];
             if (!np) continue;
-            st.raw(P->loc_pairs.p + P->cls_off[cls], S.pairs[cls].data(), np * sizeof(int2));
-            st.upload(P->pv[cls], S.pv[cls]);
+            if ((long long)P->pv[cls].n < 6 * np) P->pv[cls].alloc(6 * np);
+            long long o = 0;
+            for (const auto& q : SP) {  // the facet ranges' lists at their offsets (range order)
+                const long long k = (long long)q.pairs[cls].size();
+                st.raw(P->loc_pairs.p + P->cls_off[cls] + o, q.pairs[cls].data(), k * sizeof(int2));
+                st.raw(P->pv[cls].p + 6 * o, q.pv[cls].data(), 6 * k * sizeof(int));
+                o += k;
+            }
             sauter_chunking(ctx, cls, (int)np, P->SR->npts[cls], P->schunk[cls], P->schunks[cls]);
             P->spart[cls].alloc((size_t)P->schunks[cls] * np);
         }
