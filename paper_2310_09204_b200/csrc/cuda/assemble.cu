@@ -1193,13 +1193,15 @@ __global__ void k_sauter_finish(const double* __restrict__ part, int npairs, int
 // ---------------------------------------------------------------- per-pair scatter (near + singular)
 // pairs [0, nsing) are the singular pairs, then min(*nnear, near_cap) near pairs (device count)
 // band (optional): max |da - db| over the entries written, for the host copy's band patch
+// pairs [lo, nsing + near count) — or [lo, nsing) when nnear is null (the singular pairs alone)
 __global__ void k_local_scatter(const int2* __restrict__ pairs, const double* __restrict__ I, long long nsing,
                                 const unsigned long long* __restrict__ nnear, long long near_cap,
                                 const int* __restrict__ uptr, const int* __restrict__ udof,
-                                const double* __restrict__ uval, double* __restrict__ W, int ld, int* __restrict__ band)
+                                const double* __restrict__ uval, double* __restrict__ W, int ld, int* __restrict__ band,
+                                long long lo = 0)
 {
-    const long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= nsing + min((long long)*nnear, near_cap)) return;
+    const long long k = lo + (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= nsing + (nnear ? min((long long)*nnear, near_cap) : 0LL)) return;
     const int f = pairs[k].x, g = pairs[k].y;
     const double val = I[k];
     for (int p = uptr[f]; p < uptr[f + 1]; ++p) {
@@ -1242,6 +1244,29 @@ __global__ void k_mirror(double* __restrict__ W, int n, int ld, int* __restrict_
     __syncthreads();
     for (int r = ty; r < 32; r += blockDim.y) {
         const int i = bj * 32 + r, j = bi * 32 + tx;  // destination (lower) element (i, j) = source (j, i)
+        if (i < n && j < n && i > j) W[(size_t)i * ld + j] = tile[tx][r];
+    }
+}
+
+// the mirror restricted to the tiles that meet the band |i - j| <= *K (K measured on the
+// device by the scatter): after a scatter only those entries changed
+__global__ void k_mirror_band(double* __restrict__ W, int n, int ld, const int* __restrict__ Kdev, int* __restrict__ bad)
+{
+    __shared__ double tile[32][33];
+    const int bi = blockIdx.y, bj = blockIdx.x;
+    if (bi > bj || (bj - bi - 1) * 32 > *Kdev) return;  // every |i - j| in the tile exceeds K
+    const int tx = threadIdx.x, ty = threadIdx.y;
+    bool finite = true;
+    for (int r = ty; r < 32; r += blockDim.y) {
+        const int i = bi * 32 + r, j = bj * 32 + tx;
+        const double v = (i < n && j < n) ? W[(size_t)i * ld + j] : 0.0;
+        finite &= isfinite(v);
+        tile[r][tx] = v;
+    }
+    if (__any_sync(0xffffffffu, !finite) && tx == 0) *bad = 1;
+    __syncthreads();
+    for (int r = ty; r < 32; r += blockDim.y) {
+        const int i = bj * 32 + r, j = bi * 32 + tx;
         if (i < n && j < n && i > j) W[(size_t)i * ld + j] = tile[tx][r];
     }
 }
@@ -1667,7 +1692,7 @@ constexpr int kNearCnt = 10;
 // count and the mirror's non-finite flag of the assembly (read after its one synchronisation)
 unsigned long long* near_host_counters(NearWork& NW)
 {
-    if (!NW.hcnt) SBG_CUDA(cudaMallocHost(&NW.hcnt, (kNearCnt + 2) * sizeof(unsigned long long)));
+    if (!NW.hcnt) SBG_CUDA(cudaMallocHost(&NW.hcnt, (kNearCnt + 3) * sizeof(unsigned long long)));
     return NW.hcnt;
 }
 
@@ -1870,7 +1895,7 @@ struct AssemblyPlan {
     DBuf<double> loc_I;
     DBuf<unsigned long long> near_cnt;
     DBuf<int> bad;  // non-finite flag of the mirror pass
-    DBuf<int> band;  // max |i - j| of the near/singular entries (the host copy's band patch)
+    DBuf<int> band;  // max |i - j| of the near [0] and singular [1] entries (the host copy's band patches)
     // deferred curl-dependent half (plan_finish)
     std::unique_ptr<Stager> st;
     std::future<FacetCurls> curl_fut;
@@ -2223,7 +2248,7 @@ void assembly_run(AssemblyPlan* P, DMatrix& W, AssemblyStats* stats, int rank, i
             if (b) cudaEventDestroy(b);
         }
     } evg{ev_far, ev_copy};
-    if (to_host && !P->band.n) P->band.alloc(1);
+    if (to_host && P->band.n < 2) P->band.alloc(2);
     auto enqueue_far = [&]() {
         {
             TimedScope ts(ctx, "far_tiles");
@@ -2239,12 +2264,55 @@ void assembly_run(AssemblyPlan* P, DMatrix& W, AssemblyStats* stats, int rank, i
         count_launch();
         SBG_LAUNCH_CHECK();
     };
+    // the rows' band |i - j| <= K of W into host_dst on stream st: the diagonal band of the
+    // interior rows, and the fixed 2K + 1-column window at the matrix edge for the first and
+    // last K rows (a few more final entries copied is harmless) — three pitched DMAs; a band
+    // wider than n/4 (junction numberings) copies the whole W
+    const int nW = P->n;
+    auto band_wide = [&](int K) { return !(nW > 2 * K + 1 && (size_t)(2 * K + 1) * 4 < (size_t)nW); };
+    auto band_copy = [&](cudaStream_t st, int K) {
+        const size_t es = sizeof(double);
+        const int n = nW;
+        K = std::min(K, n - 1);
+        if (!band_wide(K)) {
+            const size_t w = es * (2 * (size_t)K + 1);
+            SBG_CUDA(cudaMemcpy2DAsync(host_dst + (size_t)K * (n + 1) - K, es * ((size_t)n + 1),
+                                       W.a.p + (size_t)K * (W.ld + 1) - K, es * ((size_t)W.ld + 1), w, n - 2 * K,
+                                       cudaMemcpyDeviceToHost, st));
+            if (K > 0) {
+                SBG_CUDA(cudaMemcpy2DAsync(host_dst, es * n, W.a.p, es * W.ld, w, K, cudaMemcpyDeviceToHost, st));
+                const size_t c0 = (size_t)n - (2 * (size_t)K + 1), r0 = (size_t)n - K;
+                SBG_CUDA(cudaMemcpy2DAsync(host_dst + r0 * n + c0, es * n, W.a.p + r0 * W.ld + c0, es * W.ld, w, K,
+                                           cudaMemcpyDeviceToHost, st));
+            }
+        } else {
+            SBG_CUDA(cudaMemcpy2DAsync(host_dst, es * n, W.a.p, es * W.ld, es * n, n, cudaMemcpyDeviceToHost, st));
+        }
+    };
+    auto enqueue_mirror_band = [&](const int* Kdev) {
+        TimedScope ts(ctx, "mirror");
+        const int nt = (P->n + 31) / 32;
+        k_mirror_band<<<dim3(nt, nt), dim3(32, 8), 0, s>>>(W.a.p, P->n, W.ld, Kdev, P->bad.p);
+        count_launch();
+        SBG_LAUNCH_CHECK();
+    };
+    // to_host: the band the near pairs touched is copied on the second stream while the Sauter
+    // classes run (its width is read from the device mid-assembly); only the narrower band
+    // of the singular pairs is copied after the end
+    int* hband = reinterpret_cast<int*>(hnear + 1) + 1;  // [0] near band, [1] singular band (hcnt has a spare word)
+    bool near_patched = false;
+    cudaEvent_t ev_near = nullptr, ev_patch = nullptr;
+    if (to_host) {
+        SBG_CUDA(cudaEventCreateWithFlags(&ev_near, cudaEventDisableTiming));
+        SBG_CUDA(cudaEventCreateWithFlags(&ev_patch, cudaEventDisableTiming));
+    }
+    EvGuard evg2{ev_near, ev_patch};
     for (int attempt = 0;; ++attempt) {
-        std::fill(NW.hcnt, NW.hcnt + kNearCnt + 2, 0ull);  // the previous run has synchronised
+        std::fill(NW.hcnt, NW.hcnt + kNearCnt + 3, 0ull);  // the previous run has synchronised
         if (attempt) SBG_CUDA(cudaMemsetAsync(W.a.p, 0, W.a.n * sizeof(double), s));
         SBG_CUDA(cudaMemsetAsync(P->near_cnt.p, 0, sizeof(unsigned long long), s));
         SBG_CUDA(cudaMemsetAsync(P->bad.p, 0, sizeof(int), s));
-        if (to_host) SBG_CUDA(cudaMemsetAsync(P->band.p, 0, sizeof(int), s));
+        if (to_host) SBG_CUDA(cudaMemsetAsync(P->band.p, 0, 2 * sizeof(int), s));
         tr.mark("memsets");
         if (my_cand) {  // near list: classification of the non-certainly-far tiles
             TimedScope ts(ctx, "classify");
@@ -2281,6 +2349,17 @@ void assembly_run(AssemblyPlan* P, DMatrix& W, AssemblyStats* stats, int rank, i
             tr.mark("far_copy");
             run_near_leaves(ctx, R, P->G.v.p, P->G.area.p, P->loc_pairs.p + P->nsing, P->loc_I.p + P->nsing, NW);
             tr.mark("leaves");
+            if (P->near_cap > 0) {  // the near pairs' scatter (band[0]) and its band's mirror now
+                TimedScope ts(ctx, "local_scatter");
+                k_local_scatter<<<(int)((P->near_cap + 127) / 128), 128, 0, s>>>(
+                    P->loc_pairs.p, P->loc_I.p, P->nsing, P->near_cnt.p, P->near_cap, P->uptr.p, P->udof.p, P->uval.p,
+                    W.a.p, W.ld, P->band.p, P->nsing);
+                count_launch();
+                SBG_LAUNCH_CHECK();
+            }
+            enqueue_mirror_band(P->band.p);
+            SBG_CUDA(cudaMemcpyAsync(hband, P->band.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+            SBG_CUDA(cudaEventRecord(ev_near, s));
         }
         // singular pairs (Sauter rules); a shard zeroes the integrals it does not own
         if (world > 1 && P->nsing) SBG_CUDA(cudaMemsetAsync(P->loc_I.p, 0, P->nsing * sizeof(double), s));
@@ -2298,23 +2377,41 @@ void assembly_run(AssemblyPlan* P, DMatrix& W, AssemblyStats* stats, int rank, i
             SBG_LAUNCH_CHECK();
         }
         if (!to_host) enqueue_far();
-        // per-pair scatter of singular + near integrals (near count read on the device)
-        if (P->nsing + P->near_cap > 0) {
-            TimedScope ts(ctx, "local_scatter");
-            const long long nmax = P->nsing + P->near_cap;
-            k_local_scatter<<<(int)((nmax + 127) / 128), 128, 0, s>>>(P->loc_pairs.p, P->loc_I.p, P->nsing,
-                                                                      P->near_cnt.p, P->near_cap, P->uptr.p,
-                                                                      P->udof.p, P->uval.p, W.a.p, W.ld,
-                                                                      to_host ? P->band.p : nullptr);
-            count_launch();
-            SBG_LAUNCH_CHECK();
+        if (to_host) {  // the singular pairs' scatter (band[1]) and its band's mirror
+            if (P->nsing > 0) {
+                TimedScope ts(ctx, "local_scatter");
+                k_local_scatter<<<(int)((P->nsing + 127) / 128), 128, 0, s>>>(
+                    P->loc_pairs.p, P->loc_I.p, P->nsing, nullptr, 0, P->uptr.p, P->udof.p, P->uval.p, W.a.p, W.ld,
+                    P->band.p + 1);
+                count_launch();
+                SBG_LAUNCH_CHECK();
+            }
+            enqueue_mirror_band(P->band.p + 1);
+        } else {  // per-pair scatter of singular + near integrals (near count read on the device)
+            if (P->nsing + P->near_cap > 0) {
+                TimedScope ts(ctx, "local_scatter");
+                const long long nmax = P->nsing + P->near_cap;
+                k_local_scatter<<<(int)((nmax + 127) / 128), 128, 0, s>>>(P->loc_pairs.p, P->loc_I.p, P->nsing,
+                                                                          P->near_cnt.p, P->near_cap, P->uptr.p,
+                                                                          P->udof.p, P->uval.p, W.a.p, W.ld, nullptr);
+                count_launch();
+                SBG_LAUNCH_CHECK();
+            }
+            enqueue_mirror();
         }
-        enqueue_mirror();  // (to_host: again — only the entries of the near band change)
         SBG_CUDA(cudaMemcpyAsync(hnear, P->near_cnt.p, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
         SBG_CUDA(cudaMemcpyAsync(hnear + 1, P->bad.p, sizeof(int), cudaMemcpyDeviceToHost, s));
-        if (to_host)
-            SBG_CUDA(cudaMemcpyAsync(reinterpret_cast<int*>(hnear + 1) + 1, P->band.p, sizeof(int),
-                                     cudaMemcpyDeviceToHost, s));
+        if (to_host) {
+            SBG_CUDA(cudaMemcpyAsync(hband + 1, P->band.p + 1, sizeof(int), cudaMemcpyDeviceToHost, s));
+            // the near band's copy beside the Sauter classes, once its width has landed
+            SBG_CUDA(cudaEventSynchronize(ev_near));
+            near_patched = !band_wide(hband[0]);
+            if (near_patched) {
+                SBG_CUDA(cudaStreamWaitEvent(cs, ev_near, 0));
+                band_copy(cs, hband[0]);
+            }
+            SBG_CUDA(cudaEventRecord(ev_patch, cs));
+        }
         tr.mark("enqueued");
         SBG_CUDA(cudaStreamSynchronize(s));
         tr.mark("sync");
@@ -2334,29 +2431,12 @@ void assembly_run(AssemblyPlan* P, DMatrix& W, AssemblyStats* stats, int rank, i
         }
     }
     if (to_host) {
-        // the band patch, after the whole-W copy has landed
-        const int n = P->n;
-        const int K = std::min(reinterpret_cast<const int*>(hnear + 1)[1], n - 1);
+        // the last patch, after the whole-W copy and the near band's patch have landed: the
+        // singular pairs' band (or, when the near band was too wide to patch, the larger band)
         TimedScope ts(ctx, "band_patch");
         SBG_CUDA(cudaStreamWaitEvent(s, ev_copy, 0));
-        const size_t es = sizeof(double);
-        if (n > 2 * K + 1 && (size_t)(2 * K + 1) * 4 < (size_t)n) {
-            // interior rows: the diagonal band; the first and last K rows: the fixed window of
-            // 2K + 1 columns at the matrix edge that contains their clipped band (copying a
-            // few more final entries is harmless) — three DMAs in all
-            const size_t w = es * (2 * (size_t)K + 1);
-            SBG_CUDA(cudaMemcpy2DAsync(host_dst + (size_t)K * (n + 1) - K, es * ((size_t)n + 1),
-                                       W.a.p + (size_t)K * (W.ld + 1) - K, es * ((size_t)W.ld + 1), w, n - 2 * K,
-                                       cudaMemcpyDeviceToHost, s));
-            if (K > 0) {
-                SBG_CUDA(cudaMemcpy2DAsync(host_dst, es * n, W.a.p, es * W.ld, w, K, cudaMemcpyDeviceToHost, s));
-                const size_t c0 = (size_t)n - (2 * (size_t)K + 1), r0 = (size_t)n - K;
-                SBG_CUDA(cudaMemcpy2DAsync(host_dst + r0 * n + c0, es * n, W.a.p + r0 * W.ld + c0, es * W.ld, w, K,
-                                           cudaMemcpyDeviceToHost, s));
-            }
-        } else {  // a wide band (junction numberings): copy the whole W again
-            SBG_CUDA(cudaMemcpy2DAsync(host_dst, es * n, W.a.p, es * W.ld, es * n, n, cudaMemcpyDeviceToHost, s));
-        }
+        SBG_CUDA(cudaStreamWaitEvent(s, ev_patch, 0));
+        band_copy(s, near_patched ? hband[1] : std::max(hband[0], hband[1]));
         tr.mark("band_enq");
         SBG_CUDA(cudaStreamSynchronize(s));
         tr.mark("band_sync");
