@@ -756,6 +756,9 @@ __device__ __forceinline__ int3 flat_axes(const double* t, const double* s, bool
 }
 
 constexpr int NEAR_LEAF_THREADS = 256;
+#ifndef NEAR_LEAF_CTAS
+#define NEAR_LEAF_CTAS 2  // resident CTAs per SM (launch bounds and the persistent grid)
+#endif
 #ifndef NEAR_FLAT_UNROLL
 #define NEAR_FLAT_UNROLL 9
 #endif
@@ -767,7 +770,7 @@ constexpr int NEAR_LEAF_WARPS = NEAR_LEAF_THREADS / 32;
 // 36 x 32-byte stride is a multiple of 128 bytes: an 8-way bank conflict on every load)
 __host__ __device__ constexpr size_t leaf_stage_bytes(int npts) { return (size_t)npts * sizeof(double4) + 16; }
 constexpr size_t NEAR_LEAF_SMEM = (size_t)NEAR_LEAF_WARPS * 8 * leaf_stage_bytes(NN);
-__global__ void __launch_bounds__(NEAR_LEAF_THREADS, 2) k_near_leaves(const NearNode* __restrict__ leaves,
+__global__ void __launch_bounds__(NEAR_LEAF_THREADS, NEAR_LEAF_CTAS) k_near_leaves(const NearNode* __restrict__ leaves,
                                                                        const unsigned long long* __restrict__ nleaves_dev,
                                                                        long long cap, const int2* __restrict__ pairs,
                                                                        const double* __restrict__ GV,
@@ -1269,16 +1272,6 @@ __global__ void k_mirror_band(double* __restrict__ W, int n, int ld, const int* 
         const int i = bj * 32 + r, j = bi * 32 + tx;
         if (i < n && j < n && i > j) W[(size_t)i * ld + j] = tile[tx][r];
     }
-}
-
-// rows' band [max(0, i - K), min(n, i + K + 1)) of W packed contiguously (row i at i * (2K + 1))
-__global__ void k_pack_band(const double* __restrict__ W, int n, int ld, int K, double* __restrict__ out)
-{
-    const int i = blockIdx.y;
-    const int lo = max(0, i - K), hi = min(n, i + K + 1);
-    double* dst = out + (size_t)i * (2 * K + 1);
-    for (int j = lo + blockIdx.x * blockDim.x + threadIdx.x; j < hi; j += gridDim.x * blockDim.x)
-        dst[j - lo] = W[(size_t)i * ld + j];
 }
 
 // ---------------------------------------------------------------- RHS (assemble.hpp:143-184)
@@ -1789,7 +1782,7 @@ void run_near_leaves(Ctx* ctx, const RuleDims& R, const double* GV, const double
     const long long Lcap = (long long)NW.leaves.n;
     {
         TimedScope tl_scope(ctx, "near_leaves");
-        const int lgrid = 2 * ctx->sm_count;  // persistent: the leaf count is read on the device
+        const int lgrid = NEAR_LEAF_CTAS * ctx->sm_count;  // persistent: the leaf count is read on the device
         if (R.nnp == NN) {
             k_near_leaves<<<lgrid, NEAR_LEAF_THREADS, NEAR_LEAF_SMEM, s>>>(NW.leaves.p, NW.cnt.p + 2, Lcap, pairs, GV,
                                                                            GA, 1.0 / M_PI, out);
