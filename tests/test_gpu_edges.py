@@ -219,3 +219,28 @@ def test_coordinate_plane_screens_match_oracle(ctx, axis, offset):
     check_W(Wg, Wo)
     Wz = S.assemble_W(S.inflate(S.SurfaceMesh(v0, f)), ctx=ctx).download()
     assert np.abs(Wg - Wz).max() <= 1e-13 * np.abs(Wz).max()
+
+
+def test_solve_on_an_invalid_mesh_raises_the_validation_error(ctx):
+    """S.solve validates the fine mesh beside the inflation and the assembly (screenbem.solve):
+    an invalid fine mesh still raises the reference's ValidationError with validate_mesh's
+    message, whatever the invalid data produced meanwhile (inflate.hpp validates first)."""
+    pair = S.make_config(1)
+    v = np.array(pair.fine.vertices, dtype=float)
+    f = np.array(pair.fine.facets)
+    f_dup = np.vstack([f, f[:1]])  # a duplicate facet
+    for fine in (S.SurfaceMesh(v, f_dup),):
+        with pytest.raises(S.ValidationError) as want:
+            S.validate_mesh(fine)
+        try:
+            bad = S.MeshLevelPair(pair.coarse, fine, np.append(pair.parent, pair.parent[0]))
+        except S.ValidationError:
+            continue  # rejected when the level pair is made: nothing reaches solve
+        with pytest.raises(S.ValidationError) as got:
+            S.solve(bad, [0.0, 0.0, 1.0], ctx=ctx)
+        assert str(got.value) == str(want.value)
+    # vertex ids out of range are caught before the inflation (the cheap checks)
+    with pytest.raises(S.ValidationError):
+        fine = S.SurfaceMesh(v, np.vstack([f, [[0, 1, len(v) + 5]]]))
+        S.solve(S.MeshLevelPair(pair.coarse, fine, np.append(pair.parent, pair.parent[0])), [0.0, 0.0, 1.0],
+                ctx=ctx)
