@@ -313,7 +313,13 @@ __device__ bool tile_contract_flush_2stage(const double* __restrict__ It, int fb
 // 4 of its facet's 16 rule points in registers per pass (3 CTAs of 256 per SM).  Far pairs
 // satisfy dist >= 2 diam, so (|x|^2+|y|^2)/|x-y|^2 stays O(10) inside a tile and
 // ~1 between distant tiles: the rounding stays at the 1e-15 level.
-constexpr int FAR_PASS = 4;            // rule points of f held in registers per pass
+#ifndef FAR_PASS_PTS
+#define FAR_PASS_PTS 4
+#endif
+#ifndef FAR_CTAS
+#define FAR_CTAS 3
+#endif
+constexpr int FAR_PASS = FAR_PASS_PTS;  // rule points of f held in registers per pass
 #ifndef FAR_FLAT_UNROLL
 #define FAR_FLAT_UNROLL 2
 #endif
@@ -421,7 +427,7 @@ constexpr size_t far_smem_bytes(int nfp)
 
 // NFP: far rule size padded to a multiple of FAR_PASS (16 at the default far_order 4)
 template <int NFP, bool EXACT>
-__global__ void __launch_bounds__(FAR_THREADS, 3)
+__global__ void __launch_bounds__(FAR_THREADS, FAR_CTAS)
     k_far_tiles(const TileInfo* __restrict__ tiles, int tstride, GeoPtrs G, BlockPtrs B, double thr,
                 double* __restrict__ W, int ld, double inv_pi, int nr)
 {

@@ -181,7 +181,7 @@ def test_jittered_nonplanar_mesh_matches_oracle(ctx):
     np.testing.assert_allclose(L, Lo, rtol=1e-12, atol=1e-15 * np.abs(Lo).max())
 
 
-@pytest.mark.parametrize("cfg", [1, 2, 4])
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4])
 def test_assemble_W_into_host_buffer(cfg):
     """assemble_W(im, out=buf) (C ABI sbg_assemble_w_host): the host copy equals the device W
     bit for bit — page-locked buffers get the copy overlapped with the near field plus the
