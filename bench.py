@@ -399,6 +399,19 @@ def kernel_traffic(kernel: str, cfg: int):
         return None
 
 
+def kernel_pipe(kernel: str, cfg: int):
+    """ncu's FP64-pipe activity of an assembly kernel (fraction of active cycles) and its FP64
+    instructions per evaluation, from the committed capture for this config (or None)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r02_traffic.json")) as f:
+            e = json.load(f)[kernel].get(str(cfg))
+        return None if e is None or "fp64_pipe_active" not in e else {
+            "fp64_pipe_active_ncu": e["fp64_pipe_active"], "fp64_instr_per_eval": e.get("fp64_instr_per_eval"),
+            "source": e.get("source")}
+    except Exception:
+        return None
+
+
 def load_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -717,7 +730,10 @@ def run_ours(args):
                                          "profiles/r02_traffic.json; the kernel is FP64-bound, so the bytes only "
                                          "show it re-reads nothing (leaf list, geometry and W updates)",
                          "peak_source": "DFMA loop measured by bench.py on this GPU (MEASURED_PEAKS.json has no fp64)",
-                         "flop_convention": "20 flop per tensor-rule kernel evaluation (SURVEY.md §8d)",
+                         "flop_convention": "20 flop per tensor-rule kernel evaluation (SURVEY.md §8d); an "
+                                            "evaluation issues 8 FP64 instructions on flat panels, 9 otherwise, so "
+                                            "frac can exceed the FP64-pipe activity (pipe below)",
+                         "pipe": kernel_pipe(dom[0], cfg),
                          "ms_per_step": dom[2], "launches_per_step": launches_per_step[dom[0]],
                          "achieved_other": {"kernel": ("near_leaves" if dom[0] == "far_tiles" else "far_tiles"),
                                             "tflops": (near_flop / (near_ms * 1e-3) / 1e12 if dom[0] == "far_tiles"
