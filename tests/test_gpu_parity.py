@@ -388,3 +388,26 @@ def test_pipeline_matches_oracle(ctx, cfg, g):
     rep = S.pcg(res.W, None, res.rhs, 1e-8)
     orep0 = O.pcg(Wo, None, Lo, 1e-8)
     assert abs(rep.iterations - orep0.iterations) <= 1
+
+
+@pytest.mark.parametrize("n", [8191, 9000])
+def test_sbemw_round_trip_at_size(ctx, tmp_path, n):
+    """The SBEMW dump/load streams W in 64 MB row chunks (DESIGN.md §1 row f): a matrix whose
+    rows span several chunks (n = 8191: a ragged last chunk; 9000: 648 MB) round-trips bit
+    for bit, the header holds n, and the file size is the header plus n^2 doubles."""
+    rng = np.random.default_rng(n)
+    A = rng.standard_normal((n, n))
+    W0 = A + A.T
+    del A
+    W = S.GalerkinMatrix.from_host(W0, ctx)
+    path = tmp_path / "w.bin"
+    W.dump_binary(path)
+    head = open(path, "rb").read(16)
+    assert head[:6] == b"SBEMW\0" and int.from_bytes(head[8:12], "little") == n
+    assert path.stat().st_size == 16 + 8 * n * n
+    R = S.GalerkinMatrix.load_binary(path, ctx)
+    assert np.array_equal(R.download(), W0)
+    with open(path, "r+b") as f:  # a truncated dump is a ValidationError (assemble.hpp:207-226)
+        f.truncate(16 + 8 * n * n - 8)
+    with pytest.raises(S.ValidationError, match="truncated"):
+        S.GalerkinMatrix.load_binary(path, ctx)
