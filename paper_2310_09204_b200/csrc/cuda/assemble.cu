@@ -1202,12 +1202,14 @@ __global__ void k_sauter_finish(const double* __restrict__ part, int npairs, int
 // ---------------------------------------------------------------- per-pair scatter (near + singular)
 // pairs [0, nsing) are the singular pairs, then min(*nnear, near_cap) near pairs (device count)
 // band (optional): max |da - db| over the entries written, for the host copy's band patch
+// offs: marks |i - j| (<= kOffsMax) of every entry written (the host copy's diagonal patch)
+constexpr int kOffsMax = 4095;
 // pairs [lo, nsing + near count) — or [lo, nsing) when nnear is null (the singular pairs alone)
 __global__ void k_local_scatter(const int2* __restrict__ pairs, const double* __restrict__ I, long long nsing,
                                 const unsigned long long* __restrict__ nnear, long long near_cap,
                                 const int* __restrict__ uptr, const int* __restrict__ udof,
                                 const double* __restrict__ uval, double* __restrict__ W, int ld, int* __restrict__ band,
-                                long long lo = 0)
+                                long long lo = 0, int* __restrict__ offs = nullptr)
 {
     const long long k = lo + (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= nsing + (nnear ? min((long long)*nnear, near_cap) : 0LL)) return;
@@ -1220,6 +1222,7 @@ __global__ void k_local_scatter(const int2* __restrict__ pairs, const double* __
             const int db = udof[q];
             const double v = val * fma(ax, uval[3 * q], fma(ay, uval[3 * q + 1], az * uval[3 * q + 2]));
             if (band) atomicMax(band, abs(da - db));
+            if (offs && abs(da - db) <= kOffsMax) offs[abs(da - db)] = 1;  // the entry's diagonal
             if (f == g) {
                 if (da <= db) atomicAdd(W + (size_t)da * ld + db, v);
             } else if (da < db) {
@@ -1255,6 +1258,16 @@ __global__ void k_mirror(double* __restrict__ W, int n, int ld, int* __restrict_
         const int i = bj * 32 + r, j = bi * 32 + tx;  // destination (lower) element (i, j) = source (j, i)
         if (i < n && j < n && i > j) W[(size_t)i * ld + j] = tile[tx][r];
     }
+}
+
+// entries W(i, i + d_k) of the listed diagonals (d_k may be negative), row-major by i
+__global__ void k_pack_diagonals(const double* __restrict__ W, int n, int ld, const int* __restrict__ d, int nd,
+                                 double* __restrict__ out)
+{
+    const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= (long long)n * nd) return;
+    const int i = (int)(e / nd), j = i + d[e % nd];
+    out[e] = (j >= 0 && j < n) ? W[(size_t)i * ld + j] : 0.0;
 }
 
 // the mirror restricted to the tiles that meet the band |i - j| <= *K (K measured on the
@@ -2183,6 +2196,32 @@ struct HostTrace {
 };
 }  // namespace
 
+// the host copy's diagonal patch (cached on the context: one-shot assemble_W plans are rebuilt
+// every call): the singular entries' diagonals |i - j| (marks, kOffsMax + 1), the offset list,
+// and the packed diagonals on the device and in page-locked memory
+struct DiagPatchWork {
+    DBuf<int> offs, dlist;
+    DBuf<double> dpack;
+    int* hoffs = nullptr;
+    double* hpack = nullptr;
+    size_t hpack_n = 0;
+    ~DiagPatchWork()
+    {
+        if (hoffs) cudaFreeHost(hoffs);
+        if (hpack) cudaFreeHost(hpack);
+    }
+};
+DiagPatchWork& diag_work(Ctx* ctx)
+{
+    if (!ctx->diag_ws) {
+        auto w = std::make_shared<DiagPatchWork>();
+        w->offs.alloc(kOffsMax + 1);
+        SBG_CUDA(cudaMallocHost(&w->hoffs, (kOffsMax + 1) * sizeof(int)));
+        ctx->diag_ws = w;
+    }
+    return *static_cast<DiagPatchWork*>(ctx->diag_ws.get());
+}
+
 void assembly_run(AssemblyPlan* P, DMatrix& W, AssemblyStats* stats, int rank, int world, double* host_dst)
 {
     HostTrace tr;
@@ -2248,6 +2287,7 @@ void assembly_run(AssemblyPlan* P, DMatrix& W, AssemblyStats* stats, int rank, i
         }
     } evg{ev_far, ev_copy};
     if (to_host && P->band.n < 2) P->band.alloc(2);
+    DiagPatchWork* DW = to_host ? &diag_work(ctx) : nullptr;
     auto enqueue_far = [&]() {
         {
             TimedScope ts(ctx, "far_tiles");
@@ -2379,9 +2419,10 @@ void assembly_run(AssemblyPlan* P, DMatrix& W, AssemblyStats* stats, int rank, i
         if (to_host) {  // the singular pairs' scatter (band[1]) and its band's mirror
             if (P->nsing > 0) {
                 TimedScope ts(ctx, "local_scatter");
+                SBG_CUDA(cudaMemsetAsync(DW->offs.p, 0, DW->offs.n * sizeof(int), s));
                 k_local_scatter<<<(int)((P->nsing + 127) / 128), 128, 0, s>>>(
                     P->loc_pairs.p, P->loc_I.p, P->nsing, nullptr, 0, P->uptr.p, P->udof.p, P->uval.p, W.a.p, W.ld,
-                    P->band.p + 1);
+                    P->band.p + 1, 0, DW->offs.p);
                 count_launch();
                 SBG_LAUNCH_CHECK();
             }
@@ -2402,6 +2443,10 @@ void assembly_run(AssemblyPlan* P, DMatrix& W, AssemblyStats* stats, int rank, i
         SBG_CUDA(cudaMemcpyAsync(hnear + 1, P->bad.p, sizeof(int), cudaMemcpyDeviceToHost, s));
         if (to_host) {
             SBG_CUDA(cudaMemcpyAsync(hband + 1, P->band.p + 1, sizeof(int), cudaMemcpyDeviceToHost, s));
+            if (P->nsing > 0)
+                SBG_CUDA(cudaMemcpyAsync(DW->hoffs, DW->offs.p, DW->offs.n * sizeof(int), cudaMemcpyDeviceToHost, s));
+            else
+                std::fill(DW->hoffs, DW->hoffs + DW->offs.n, 0);
             // the near band's copy beside the Sauter classes, once its width has landed
             SBG_CUDA(cudaEventSynchronize(ev_near));
             near_patched = !band_wide(hband[0]);
@@ -2435,7 +2480,55 @@ void assembly_run(AssemblyPlan* P, DMatrix& W, AssemblyStats* stats, int rank, i
         TimedScope ts(ctx, "band_patch");
         SBG_CUDA(cudaStreamWaitEvent(s, ev_copy, 0));
         SBG_CUDA(cudaStreamWaitEvent(s, ev_patch, 0));
-        band_copy(s, near_patched ? hband[1] : std::max(hband[0], hband[1]));
+        // the singular entries lie on a few diagonals (a regular grid numbering: |i - j| in a
+        // handful of short runs): when those diagonals are fewer than a quarter of the band,
+        // they are packed on the device, copied in one piece and unpacked on host threads
+        std::vector<int> dl;
+        if (near_patched && hband[1] <= kOffsMax) {
+            const int* mk = DW->hoffs;
+            for (int d = 0; d <= hband[1]; ++d)
+                if (mk[d]) {
+                    dl.push_back(d);
+                    if (d) dl.push_back(-d);
+                }
+        }
+        const int nd = (int)dl.size();
+        if (near_patched && hband[1] <= kOffsMax && (size_t)nd * 4 <= 2 * (size_t)hband[1] + 1) {
+            const size_t cnt = (size_t)nW * std::max(nd, 1);
+            if (DW->dlist.n < (size_t)std::max(nd, 1)) DW->dlist.alloc(std::max(nd, 1));
+            if (DW->dpack.n < cnt) DW->dpack.alloc(cnt);
+            if (DW->hpack_n < cnt) {
+                if (DW->hpack) SBG_CUDA(cudaFreeHost(DW->hpack));
+                DW->hpack = nullptr;
+                DW->hpack_n = 0;
+                SBG_CUDA(cudaMallocHost(&DW->hpack, cnt * sizeof(double)));
+                DW->hpack_n = cnt;
+            }
+            if (nd) {  // dl is read by the copy engine before the synchronisation below
+                SBG_CUDA(cudaMemcpyAsync(DW->dlist.p, dl.data(), nd * sizeof(int), cudaMemcpyHostToDevice, s));
+                k_pack_diagonals<<<(unsigned)((cnt + 255) / 256), 256, 0, s>>>(W.a.p, nW, W.ld, DW->dlist.p, nd,
+                                                                               DW->dpack.p);
+                count_launch();
+                SBG_LAUNCH_CHECK();
+                SBG_CUDA(cudaMemcpyAsync(DW->hpack, DW->dpack.p, cnt * sizeof(double), cudaMemcpyDeviceToHost, s));
+            }
+            SBG_CUDA(cudaStreamSynchronize(s));  // (also: the W copy and the near band patch have landed)
+            const double* hp = DW->hpack;
+            const int nth = nd ? std::max(1, std::min(16, nW / 2048)) : 0;
+            auto unpack = [&](int t) {
+                for (int i = (int)((long long)nW * t / nth); i < (int)((long long)nW * (t + 1) / nth); ++i)
+                    for (int k = 0; k < nd; ++k) {
+                        const int j = i + dl[k];
+                        if (j >= 0 && j < nW) host_dst[(size_t)i * nW + j] = hp[(size_t)i * nd + k];
+                    }
+            };
+            std::vector<std::thread> th;
+            for (int t = 1; t < nth; ++t) th.emplace_back(unpack, t);
+            if (nth) unpack(0);
+            for (auto& x : th) x.join();
+        } else {
+            band_copy(s, near_patched ? hband[1] : std::max(hband[0], hband[1]));
+        }
         tr.mark("band_enq");
         SBG_CUDA(cudaStreamSynchronize(s));
         tr.mark("band_sync");

@@ -119,6 +119,7 @@ struct Ctx {
     std::shared_ptr<void> near_ws; // cached near-field frontier buffers (assemble.cu)
     std::shared_ptr<void> flush_ws; // L2 flush buffers (context.cu)
     std::shared_ptr<void> prec_sched; // last preconditioner task schedule (precond.cu)
+    std::shared_ptr<void> diag_ws;    // host-copy diagonal patch buffers (assemble.cu)
     std::shared_ptr<void> scratch_ws; // grow-only scratch buffers (context.cu: scratch())
     std::shared_ptr<void> sauter_ws;  // device Sauter rules per singular order (assemble.cu)
     std::shared_ptr<void> stage_ws;   // page-locked staging arena of the plan uploads (assemble.cu)
