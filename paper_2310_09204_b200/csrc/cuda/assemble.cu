@@ -1055,12 +1055,13 @@ __device__ __forceinline__ void sauter_stage(const double* __restrict__ R, int c
         double r2[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) r2[u] = sauter_r2<CLS, FLAT>(R + ST * (i + u), g);
-        acc0 = fma(R[ST * i + ST - 1], rsqrt_fast(r2[0]), acc0);
-        acc1 = fma(R[ST * (i + 1) + ST - 1], rsqrt_fast(r2[1]), acc1);
-        acc2 = fma(R[ST * (i + 2) + ST - 1], rsqrt_fast(r2[2]), acc2);
-        acc3 = fma(R[ST * (i + 3) + ST - 1], rsqrt_fast(r2[3]), acc3);
+        // the table's coefficients carry 1 / w^2 in r^2: rsqrt of it is w / r (rsqrt_acc)
+        acc0 = rsqrt_acc(r2[0], acc0);
+        acc1 = rsqrt_acc(r2[1], acc1);
+        acc2 = rsqrt_acc(r2[2], acc2);
+        acc3 = rsqrt_acc(r2[3], acc3);
     }
-    for (; i < cnt; ++i) acc0 = fma(R[ST * i + ST - 1], rsqrt_fast(sauter_r2<CLS, FLAT>(R + ST * i, g)), acc0);
+    for (; i < cnt; ++i) acc0 = rsqrt_acc(sauter_r2<CLS, FLAT>(R + ST * i, g), acc0);
 }
 
 template <int CLS>
@@ -1627,28 +1628,40 @@ void upload_sauter(Ctx* ctx, const QuadCfg& cfg, SauterRulesDev& R)
         const double* a = id.pts.data() + 5 * i;
         const double c1 = a[0] - a[2], c2 = a[1] - a[3];
         double* o = idp.data() + 4 * i;
-        o[0] = c1 * c1;
-        o[1] = 2.0 * c1 * c2;
-        o[2] = c2 * c2;
+        const double sw = 1.0 / (a[4] * a[4]);  // the weight folded into r^2 (rsqrt_acc)
+        o[0] = c1 * c1 * sw;
+        o[1] = 2.0 * c1 * c2 * sw;
+        o[2] = c2 * c2 * sw;
         o[3] = a[4];
     }
     for (int i = 0; i < ed.size(); ++i) {
         const double* a = ed.pts.data() + 5 * i;
         const double c1 = a[0] - a[2], c2 = a[1], c3 = a[3];
         double* o = edp.data() + 8 * i;
-        o[0] = c1 * c1;
-        o[1] = c2 * c2;
-        o[2] = c3 * c3;
-        o[3] = 2.0 * c1 * c2;
-        o[4] = -2.0 * c1 * c3;
-        o[5] = -2.0 * c2 * c3;
+        const double sw = 1.0 / (a[4] * a[4]);
+        o[0] = c1 * c1 * sw;
+        o[1] = c2 * c2 * sw;
+        o[2] = c3 * c3 * sw;
+        o[3] = 2.0 * c1 * c2 * sw;
+        o[4] = -2.0 * c1 * c3 * sw;
+        o[5] = -2.0 * c2 * c3 * sw;
         o[7] = a[4];  // o[6] = 0: padding to 32-byte rows
     }
+    // vertex class: the four coefficients scaled by 1 / w (r^2 then carries 1 / w^2)
+    std::vector<double> vxp(vx.pts);
+    for (int i = 0; i < vx.size(); ++i) {
+        double* o = vxp.data() + 5 * i;
+        const double iw = 1.0 / o[4];
+        for (int k = 0; k < 4; ++k) o[k] *= iw;
+    }
+    for (const SauterRule* r : {&id, &ed, &vx})
+        for (int i = 0; i < r->size(); ++i)
+            if (!(r->pts[5 * i + 4] > 0.0)) throw std::logic_error("Sauter rule weight not positive: cannot fold");
     R.r[3].upload(idp, ctx->stream);
     R.npts[3] = id.size();
     R.r[2].upload(edp, ctx->stream);
     R.npts[2] = ed.size();
-    R.r[1].upload(vx.pts, ctx->stream);
+    R.r[1].upload(vxp, ctx->stream);
     R.npts[1] = vx.size();
 }
 
