@@ -321,7 +321,10 @@ __device__ bool tile_contract_flush_2stage(const double* __restrict__ It, int fb
 #endif
 constexpr int FAR_PASS = FAR_PASS_PTS;  // rule points of f held in registers per pass
 #ifndef FAR_FLAT_UNROLL
-#define FAR_FLAT_UNROLL 2
+#define FAR_FLAT_UNROLL 16  // the whole default rule (A/B: 2 -> 16 took config 5 from 213 to 205 ms)
+#endif
+#ifndef FAR_GEN_UNROLL
+#define FAR_GEN_UNROLL 2
 #endif
 struct XPts {
     double m2x[FAR_PASS], m2y[FAR_PASS], m2z[FAR_PASS], x2[FAR_PASS];  // -2x, -2y, -2z, |x|^2
@@ -530,7 +533,7 @@ __global__ void __launch_bounds__(FAR_THREADS, FAR_CTAS)
             } else {
                 for (int m = 0, gl = warp >> 1; gl < BS; gl += FAR_THREADS / 64, ++m) {
                     if (!(mask >> m & 1)) continue;
-                    It[fl * (BS + 1) + gl] += far_pass_sum<NFP>(X, Ys + gl * NFP, pass) * sf * gcr[gl * 6 + 5];
+                    It[fl * (BS + 1) + gl] += far_pass_sum<NFP, false, FAR_GEN_UNROLL>(X, Ys + gl * NFP, pass) * sf * gcr[gl * 6 + 5];
                 }
             }
         }
@@ -766,10 +769,21 @@ constexpr int NEAR_LEAF_THREADS = 256;
 #define NEAR_LEAF_CTAS 2  // resident CTAs per SM (launch bounds and the persistent grid)
 #endif
 #ifndef NEAR_FLAT_UNROLL
-#define NEAR_FLAT_UNROLL 9
+#define NEAR_FLAT_UNROLL 36
 #endif
 constexpr int kNearFlatUnroll = NEAR_FLAT_UNROLL;  // the flat leaf loop's unroll (A/B builds)
+#ifndef NEAR_GEN_UNROLL
+#define NEAR_GEN_UNROLL 3
+#endif
+constexpr int kNearGenUnroll = NEAR_GEN_UNROLL;  // the 3-D leaf loop's unroll
 constexpr int NEAR_XP = 4;  // x points per pass (register block)
+#ifndef NEAR_LEAF_XP
+#define NEAR_LEAF_XP 3
+#endif
+// the default-rule leaf kernel: 4 x points per pass (groups xg, xg + 4, then group 8 split by
+// y over the 4 lanes) or 3 (groups xg, xg + 4, xg + 8: three uniform passes of 36 y points)
+constexpr int NLX = NEAR_LEAF_XP;
+static_assert(NLX == 3 || NLX == 4, "near-leaf x block: 3 or 4 points");
 constexpr int NEAR_LEAF_WARPS = NEAR_LEAF_THREADS / 32;
 // one leaf's staged y points: npts double4 plus 16 bytes, so the eight leaves of a warp,
 // read together by one LDS.128, start in eight different 16-byte bank groups (a plain
@@ -854,12 +868,12 @@ __global__ void __launch_bounds__(NEAR_LEAF_THREADS, NEAR_LEAF_CTAS) k_near_leav
             // 36 y points, and group 8 against y in [9 xg, 9 xg + 9)
 #pragma unroll 1
             for (int pass = 0; pass < 3; ++pass) {
-                const int g = pass < 2 ? xg + 4 * pass : 8;
-                const int j0 = pass < 2 ? 0 : 9 * xg, j1 = pass < 2 ? NN : 9 * xg + 9;
-                double mx[NEAR_XP], my[NEAR_XP], mz[NEAR_XP], x2[NEAR_XP], a[NEAR_XP];
+                const int g = (NLX == 3 || pass < 2) ? xg + 4 * pass : 8;
+                const int j0 = (NLX == 3 || pass < 2) ? 0 : 9 * xg, j1 = (NLX == 3 || pass < 2) ? NN : 9 * xg + 9;
+                double mx[NLX], my[NLX], mz[NLX], x2[NLX], a[NLX];
 #pragma unroll
-                for (int r = 0; r < NEAR_XP; ++r) {
-                    const int i = NEAR_XP * g + r;
+                for (int r = 0; r < NLX; ++r) {
+                    const int i = NLX * g + r;
                     const double xx = fma(NEAR_TAB(near_v, i), f2x, NEAR_TAB(near_u, i) * f1x);
                     const double xy = fma(NEAR_TAB(near_v, i), f2y, NEAR_TAB(near_u, i) * f1y);
                     if (flat) {
@@ -880,25 +894,25 @@ __global__ void __launch_bounds__(NEAR_LEAF_THREADS, NEAR_LEAF_CTAS) k_near_leav
                         const double4 y = Ys[j];
                         const double sj = c_near_s[j];
 #pragma unroll
-                        for (int r = 0; r < NEAR_XP; ++r) {
+                        for (int r = 0; r < NLX; ++r) {
                             const double r2 = fma(mx[r], y.x, fma(my[r], y.y, fma(x2[r], sj, y.w)));
                             a[r] = rsqrt_acc(r2, a[r]);
                         }
                     }
                 } else {
-#pragma unroll 3
+#pragma unroll kNearGenUnroll
                     for (int j = j0; j < j1; ++j) {
                         const double4 y = Ys[j];
                         const double sj = c_near_s[j];
 #pragma unroll
-                        for (int r = 0; r < NEAR_XP; ++r) {
+                        for (int r = 0; r < NLX; ++r) {
                             const double r2 = fma(mx[r], y.x, fma(my[r], y.y, fma(mz[r], y.z, fma(x2[r], sj, y.w))));
                             a[r] = rsqrt_acc(r2, a[r]);
                         }
                     }
                 }
 #pragma unroll
-                for (int r = 0; r < NEAR_XP; ++r) acc = fma(NEAR_TAB(near_w, NEAR_XP * g + r), a[r], acc);
+                for (int r = 0; r < NLX; ++r) acc = fma(NEAR_TAB(near_w, NLX * g + r), a[r], acc);
             }
         }
         for (int o = 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);

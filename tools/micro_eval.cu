@@ -216,6 +216,13 @@ int main()
     run<6, 2, 4>(256, 2, d, ghz);
     run<8, 2, 4>(256, 2, d, ghz);
     run<4, 2, 4>(128, 8, d, ghz);
+    // near-leaf shapes (2 CTAs of 256 per SM): 4 points unroll 3/9, 3 points unroll 3/6/12
+    run<4, 3, 4>(256, 2, d, ghz);
+    run<4, 9, 4>(256, 2, d, ghz);
+    run<3, 3, 4>(256, 2, d, ghz);
+    run<3, 6, 4>(256, 2, d, ghz);
+    run<3, 12, 4>(256, 2, d, ghz);
+    run<6, 3, 4>(256, 2, d, ghz);
     run<8, 2, 2>(256, 2, d, ghz);
     mufu_rate(ghz);
     poly_error();
