@@ -1059,12 +1059,17 @@ __device__ __forceinline__ double sauter_r2(const double* a, const double (&g)[1
     return fma(dx, dx, fma(dy, dy, dz * dz));
 }
 
+#ifndef SAUTER_UNROLL
+#define SAUTER_UNROLL 2
+#endif
+constexpr int kSauterUnroll = SAUTER_UNROLL;  // 4-point steps per unrolled iteration (A/B builds)
 // one stage of rule points, four independent evaluations per step
 template <int CLS, bool FLAT, int ST>
 __device__ __forceinline__ void sauter_stage(const double* __restrict__ R, int cnt, const double (&g)[12],
                                              double& acc0, double& acc1, double& acc2, double& acc3)
 {
     int i = 0;
+#pragma unroll kSauterUnroll
     for (; i + 4 <= cnt; i += 4) {
         double r2[4];
 #pragma unroll
