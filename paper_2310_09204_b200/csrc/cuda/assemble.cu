@@ -314,33 +314,39 @@ __device__ bool tile_contract_flush_2stage(const double* __restrict__ It, int fb
 // satisfy dist >= 2 diam, so (|x|^2+|y|^2)/|x-y|^2 stays O(10) inside a tile and
 // ~1 between distant tiles: the rounding stays at the 1e-15 level.
 #ifndef FAR_PASS_PTS
-#define FAR_PASS_PTS 4
+#define FAR_PASS_PTS 8  // rule points of f per pass where the padded rule allows (else 4)
 #endif
 #ifndef FAR_CTAS
-#define FAR_CTAS 3
+#define FAR_CTAS 2
 #endif
-constexpr int FAR_PASS = FAR_PASS_PTS;  // rule points of f held in registers per pass
+constexpr int FAR_PASS = 4;  // the pass width every padded rule admits (nfp is a multiple of 4)
+// the far kernel's pass width for a rule of NFP (padded) points: FAR_PASS_PTS (8: the default
+// rule's 16 points in two passes, 2 CTAs/SM with 128 registers) when it divides NFP
+template <int NFP>
+constexpr int far_pass_for() { return NFP % FAR_PASS_PTS == 0 ? FAR_PASS_PTS : FAR_PASS; }
 #ifndef FAR_FLAT_UNROLL
 #define FAR_FLAT_UNROLL 16  // the whole default rule (A/B: 2 -> 16 took config 5 from 213 to 205 ms)
 #endif
 #ifndef FAR_GEN_UNROLL
 #define FAR_GEN_UNROLL 2
 #endif
+template <int PW = FAR_PASS>
 struct XPts {
-    double m2x[FAR_PASS], m2y[FAR_PASS], m2z[FAR_PASS], x2[FAR_PASS];  // -2x, -2y, -2z, |x|^2
+    double m2x[PW], m2y[PW], m2z[PW], x2[PW];  // -2x, -2y, -2z, |x|^2
 };
 
 // coordinate order (P.x, P.y, P.z): the identity, or a flat tile's two in-plane axes first and
 // its flat axis last (far_flat_axis)
-__device__ __forceinline__ void far_xpoints(const double* t, const double* o, int pass, XPts& X,
+template <int PW>
+__device__ __forceinline__ void far_xpoints(const double* t, const double* o, int pass, XPts<PW>& X,
                                             int3 P = make_int3(0, 1, 2))
 {
     const double e1x = t[3 + P.x] - t[P.x], e1y = t[3 + P.y] - t[P.y], e1z = t[3 + P.z] - t[P.z];
     const double e2x = t[6 + P.x] - t[P.x], e2y = t[6 + P.y] - t[P.y], e2z = t[6 + P.z] - t[P.z];
     const double bx = t[P.x] - o[P.x], by = t[P.y] - o[P.y], bz = t[P.z] - o[P.z];
 #pragma unroll
-    for (int q = 0; q < FAR_PASS; ++q) {
-        const int i = FAR_PASS * pass + q;
+    for (int q = 0; q < PW; ++q) {
+        const int i = PW * pass + q;
         const double x = fma(c_far_v[i], e2x, fma(c_far_u[i], e1x, bx));
         const double y = fma(c_far_v[i], e2y, fma(c_far_u[i], e1y, by));
         const double z = fma(c_far_v[i], e2z, fma(c_far_u[i], e1z, bz));
@@ -373,18 +379,18 @@ __device__ __forceinline__ double4 far_ypoint(const double* s, const double* o, 
 // MUFU per evaluation.  FLAT: every point of the tile has a zero last coordinate (a tile lying
 // in one coordinate plane, far_flat_axis), whose product term -2 x_z y_z = -0 adds nothing:
 // it is left out, 8 FP64 instructions per evaluation, the same value
-template <int NFP, bool FLAT = false, int UNROLL = 2>
-__device__ __forceinline__ double far_pass_sum(const XPts& X, const double4* __restrict__ Y, int pass)
+template <int NFP, bool FLAT = false, int UNROLL = 2, int PW = FAR_PASS>
+__device__ __forceinline__ double far_pass_sum(const XPts<PW>& X, const double4* __restrict__ Y, int pass)
 {
-    double a[FAR_PASS];
+    double a[PW];
 #pragma unroll
-    for (int q = 0; q < FAR_PASS; ++q) a[q] = 0.0;
+    for (int q = 0; q < PW; ++q) a[q] = 0.0;
 #pragma unroll UNROLL
     for (int j = 0; j < NFP; ++j) {
         const double4 y = Y[j];
         const double sj = c_far_s[j];
 #pragma unroll
-        for (int q = 0; q < FAR_PASS; ++q) {
+        for (int q = 0; q < PW; ++q) {
             const double r2 = FLAT ? fma(X.m2x[q], y.x, fma(X.m2y[q], y.y, fma(X.x2[q], sj, y.w)))
                                    : fma(X.m2x[q], y.x, fma(X.m2y[q], y.y, fma(X.m2z[q], y.z, fma(X.x2[q], sj, y.w))));
             a[q] = rsqrt_acc(r2, a[q]);
@@ -392,7 +398,7 @@ __device__ __forceinline__ double far_pass_sum(const XPts& X, const double4* __r
     }
     double acc = 0.0;
 #pragma unroll
-    for (int q = 0; q < FAR_PASS; ++q) acc = fma(c_far_w[FAR_PASS * pass + q], a[q], acc);
+    for (int q = 0; q < PW; ++q) acc = fma(c_far_w[PW * pass + q], a[q], acc);
     return acc;
 }
 
@@ -522,18 +528,19 @@ __global__ void __launch_bounds__(FAR_THREADS, FAR_CTAS)
             }
         }
         const double sf = G.area[f] * inv_pi;
-        for (int pass = 0; !EXACT && pass < NFP / FAR_PASS; ++pass) {
-            XPts X;
+        constexpr int PW = far_pass_for<NFP>();
+        for (int pass = 0; !EXACT && pass < NFP / PW; ++pass) {
+            XPts<PW> X;
             far_xpoints(G.v + 9 * f, o, pass, X, P);
             if (flat) {
                 for (int m = 0, gl = warp >> 1; gl < BS; gl += FAR_THREADS / 64, ++m) {
                     if (!(mask >> m & 1)) continue;
-                    It[fl * (BS + 1) + gl] += far_pass_sum<NFP, true, FAR_FLAT_UNROLL>(X, Ys + gl * NFP, pass) * sf * gcr[gl * 6 + 5];
+                    It[fl * (BS + 1) + gl] += far_pass_sum<NFP, true, FAR_FLAT_UNROLL, PW>(X, Ys + gl * NFP, pass) * sf * gcr[gl * 6 + 5];
                 }
             } else {
                 for (int m = 0, gl = warp >> 1; gl < BS; gl += FAR_THREADS / 64, ++m) {
                     if (!(mask >> m & 1)) continue;
-                    It[fl * (BS + 1) + gl] += far_pass_sum<NFP, false, FAR_GEN_UNROLL>(X, Ys + gl * NFP, pass) * sf * gcr[gl * 6 + 5];
+                    It[fl * (BS + 1) + gl] += far_pass_sum<NFP, false, FAR_GEN_UNROLL, PW>(X, Ys + gl * NFP, pass) * sf * gcr[gl * 6 + 5];
                 }
             }
         }
@@ -2620,7 +2627,7 @@ __global__ void k_far_pair_list(GeoPtrs G, const int2* __restrict__ pairs, long 
     for (int j = 0; j < NFP; ++j) Y[j] = far_ypoint(sv, t, j);
     double acc = 0.0;
     for (int pass = 0; pass < NFP / FAR_PASS; ++pass) {
-        XPts X;
+        XPts<> X;
         far_xpoints(t, t, pass, X);
         acc += far_pass_sum<NFP>(X, Y, pass) * (G.area[f] * inv_pi) * G.area[g];
     }
