@@ -584,8 +584,6 @@ def run_ours(args):
         S._check(S.lib().sbg_apply_preconditioner_device(ctx.h, prec.h, dx, dy, 1))
     gm, gc = ctx.timer("gemv_f64")
     am, ac = ctx.timer("precond_apply")
-    S.lib().sbg_device_free(dx)
-    S.lib().sbg_device_free(dy)
     matvec_s = gm / gc * 1e-3
     # algorithmic bytes of the context's matvec form (symmetric: the upper triangle, x, y and
     # the partial sums; linalg.cu gemv_bytes)
@@ -595,6 +593,25 @@ def run_ours(args):
     matvec_gbs = matvec_bytes / matvec_s / 1e9
     peaks = load_peaks()
     hbm_peak = peaks.get("hbm_gbs") or 6650.0
+    # the full-matrix form beside it (every stored entry of the dense W read once,
+    # 8 n^2 + 16 n bytes; the symmetric form above reads half of them and is reported separately)
+    form0 = ctx.matvec_form
+    full_s = full_bytes = None
+    if form0 == "symmetric":
+        ctx.matvec_form = "full"
+        for _ in range(3):
+            S._check(S.lib().sbg_matvec_device(ctx.h, W.h, dx, dy, 1))
+        ctx.reset_timers()
+        for _ in range(reps):
+            ctx.l2_flush()
+            S._check(S.lib().sbg_matvec_device(ctx.h, W.h, dx, dy, 1))
+        fm, fc = ctx.timer("gemv_f64")
+        full_s = fm / fc * 1e-3
+        S._check(S.lib().sbg_matvec_bytes(ctx.h, W.h, C.byref(mb)))
+        full_bytes = mb.value
+        ctx.matvec_form = form0
+    S.lib().sbg_device_free(dx)
+    S.lib().sbg_device_free(dy)
     # ---- e2e: public assemble_W with host mesh in, host W out
     e2e_times, e2e_parts = [], []
     h2d = 0
@@ -745,7 +762,13 @@ def run_ours(args):
                                 "bytes_full_matrix": 8.0 * n * n + 16.0 * n, "us_per_launch": matvec_s * 1e6,
                                 "peak_source": ("of measured: MEASURED_PEAKS.json hbm_gbs (a copy; a read-only "
                                                 "stream can exceed it)") if peaks.get("hbm_gbs") else "of fallback",
-                                "peak_nominal": 7700.0, "frac_nominal": matvec_gbs / 7700.0},
+                                "peak_nominal": 7700.0, "frac_nominal": matvec_gbs / 7700.0,
+                                "full_form": None if full_s is None else {
+                                    "bytes_per_launch": full_bytes, "us_per_launch": full_s * 1e6,
+                                    "achieved": full_bytes / full_s / 1e9, "unit": "GB/s",
+                                    "frac": full_bytes / full_s / 1e9 / hbm_peak,
+                                    "frac_nominal": full_bytes / full_s / 1e9 / 7700.0,
+                                    "what": "every entry of the dense W read once (8 n^2 + 16 n bytes), L2 flushed"}},
             "pcg": {"iterations": iters[-1], "iters_per_s": iters[-1] / (ms["pcg"] * 1e-3) if ms["pcg"] else None,
                     "ms": ms["pcg"], "kappa_lanczos": rep.kappa_estimate,
                     "precond_applies_per_s": 1e3 / (am / ac) if ac else None, "precond_apply_us": 1e3 * am / ac if ac else None,
