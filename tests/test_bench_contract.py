@@ -73,6 +73,11 @@ def test_our_arm_json_line():
     assert d["gpu_launches"] > 0
     assert "workload" in d["config"]
     assert d["tts_e2e_ms"] > 0 and d["e2e"]["statistic"] == "median" and d["e2e"]["ms_min"] <= d["e2e"]["ms"]
+    # the full-matrix matvec is reported beside the context's (symmetric) form: 8 n^2 + 16 n bytes
+    mv = d["roofline_matvec"]
+    n = d["config"]["dofs"]
+    assert mv["bound"] == "hbm" and mv["full_form"]["bytes_per_launch"] == 8.0 * n * n + 16.0 * n
+    assert mv["full_form"]["us_per_launch"] > 0 and mv["full_form"]["achieved"] > 0
 
 
 @pytest.mark.gpu
