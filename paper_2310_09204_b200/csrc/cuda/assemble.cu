@@ -393,13 +393,13 @@ __device__ __forceinline__ double far_pass_sum(const XPts<PW>& X, const double4*
         for (int q = 0; q < PW; ++q) {
             const double r2 = FLAT ? fma(X.m2x[q], y.x, fma(X.m2y[q], y.y, fma(X.x2[q], sj, y.w)))
                                    : fma(X.m2x[q], y.x, fma(X.m2y[q], y.y, fma(X.m2z[q], y.z, fma(X.x2[q], sj, y.w))));
-            a[q] = rsqrt_acc(r2, a[q]);
+            a[q] = rsqrt_acc_s(r2, a[q]);
         }
     }
     double acc = 0.0;
 #pragma unroll
     for (int q = 0; q < PW; ++q) acc = fma(c_far_w[PW * pass + q], a[q], acc);
-    return acc;
+    return acc * kRsqrtAccScale;
 }
 
 // SURVEY Appendix B switch: the oracle's triangle_pair_rule (quadrature.hpp:208-220) in its
@@ -903,7 +903,7 @@ __global__ void __launch_bounds__(NEAR_LEAF_THREADS, NEAR_LEAF_CTAS) k_near_leav
 #pragma unroll
                         for (int r = 0; r < NLX; ++r) {
                             const double r2 = fma(mx[r], y.x, fma(my[r], y.y, fma(x2[r], sj, y.w)));
-                            a[r] = rsqrt_acc(r2, a[r]);
+                            a[r] = rsqrt_acc_s(r2, a[r]);
                         }
                     }
                 } else {
@@ -914,7 +914,7 @@ __global__ void __launch_bounds__(NEAR_LEAF_THREADS, NEAR_LEAF_CTAS) k_near_leav
 #pragma unroll
                         for (int r = 0; r < NLX; ++r) {
                             const double r2 = fma(mx[r], y.x, fma(my[r], y.y, fma(mz[r], y.z, fma(x2[r], sj, y.w))));
-                            a[r] = rsqrt_acc(r2, a[r]);
+                            a[r] = rsqrt_acc_s(r2, a[r]);
                         }
                     }
                 }
@@ -923,7 +923,7 @@ __global__ void __launch_bounds__(NEAR_LEAF_THREADS, NEAR_LEAF_CTAS) k_near_leav
             }
         }
         for (int o = 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if (active && xg == 0) atomicAdd(out + pair, acc * scale);
+        if (active && xg == 0) atomicAdd(out + pair, acc * (scale * kRsqrtAccScale));
     }
 }
 
@@ -1010,7 +1010,7 @@ __global__ void __launch_bounds__(NEAR_G_THREADS) k_near_leaves_g(const NearNode
 #pragma unroll
                     for (int r = 0; r < NEAR_XP; ++r) {
                         const double r2 = fma(mx[r], y.x, fma(my[r], y.y, fma(mz[r], y.z, fma(x2[r], sj, y.w))));
-                        a[r] = rsqrt_acc(r2, a[r]);
+                        a[r] = rsqrt_acc_s(r2, a[r]);
                     }
                 }
 #pragma unroll
@@ -1018,7 +1018,7 @@ __global__ void __launch_bounds__(NEAR_G_THREADS) k_near_leaves_g(const NearNode
             }
         }
         for (int o = 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if (active && xg == 0) atomicAdd(out + pair, acc * scale);
+        if (active && xg == 0) atomicAdd(out + pair, acc * (scale * kRsqrtAccScale));
     }
 }
 

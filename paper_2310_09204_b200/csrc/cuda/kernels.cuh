@@ -39,16 +39,39 @@ __device__ __forceinline__ double rsqrt_fast(double r2)
 
 // acc + w / |x - y| from r2s = |x - y|^2 / w^2 (the rule weight folded into the squared
 // distance, w > 0): rsqrt seed and one 3rd-order Newton step, y (1 + e (1/2 + 3e/8)) with
-// e = 1 - r2s y^2 — five FP64 instructions after the seed, the weight multiply included
+// e = 1 - r2s y^2 — five FP64 instructions after the seed, the weight multiply included.
+// e comes from the seed's square: y has a zero low word (<= 21 significant bits), so y * y is
+// exact, and the square reads one register where r2s * y would read two — on sm_100a the FP64
+// pipe is bound by its register operands (profiles/r02b_micro_operand.md): config 5 far tiles
+// 202.1 -> 197.7 ms, near leaves 103.6 -> 100.1 ms for the same instruction count
 __device__ __forceinline__ double rsqrt_acc(double r2s, double acc)
 {
     double y;
     asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(r2s));
-    const double h = r2s * y;
-    const double e = fma(-h, y, 1.0);
+    const double e = fma(-r2s, y * y, 1.0);
     const double c = fma(0.375, e, 0.5);
     return fma(y, fma(e, c, 1.0), acc);
 }
+// the same step accumulated with the factor 8/3: y (8/3 + e (4/3 + e)) — the polynomial's
+// constants enter as immediates of a DADD and a DFMA (0.375 above lives in a register: one
+// operand read more per evaluation); the caller multiplies its sum by kRsqrtAccScale once
+#ifndef RSQRT_ACC_SCALED
+#define RSQRT_ACC_SCALED 1
+#endif
+#if RSQRT_ACC_SCALED
+constexpr double kRsqrtAccScale = 0.375;
+__device__ __forceinline__ double rsqrt_acc_s(double r2s, double acc)
+{
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(r2s));
+    const double e = fma(-r2s, y * y, 1.0);
+    const double c = e + 4.0 / 3.0;
+    return fma(y, fma(e, c, 8.0 / 3.0), acc);
+}
+#else
+constexpr double kRsqrtAccScale = 1.0;
+__device__ __forceinline__ double rsqrt_acc_s(double r2s, double acc) { return rsqrt_acc(r2s, acc); }
+#endif
 // a padded (zero-weight) rule point: s = 0 and this constant term make r2s huge, so its
 // contribution (~1e-150) vanishes below the rounding of any accumulated sum
 constexpr double kPadR2 = 1e300;

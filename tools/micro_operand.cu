@@ -15,6 +15,8 @@ constexpr int CH = 8;  // independent chains per thread
 // MODE 2: a_i = fma(a_i, b, c): b, c shared by all chains (reuse across consecutive instructions)
 // MODE 3: a_i = fma(b_i, c_i, a_i): three distinct registers per instruction, nothing shared
 // MODE 4: a_i = fma(b_i, c, a_i): two distinct registers + one shared
+// MODE 5: a_i = fma(b_i, b_i, a_i): two distinct registers, one of them in two slots
+// MODE 6: a_i = fma(b_i, K, a_i): two distinct registers + an immediate
 template <int MODE>
 __global__ void __launch_bounds__(256) k_dfma(double* out, const double* in, int reps)
 {
@@ -33,7 +35,9 @@ __global__ void __launch_bounds__(256) k_dfma(double* out, const double* in, int
                 if (MODE == 1) a[i] = fma(a[i], 0.999999, 1e-7);
                 else if (MODE == 2) a[i] = fma(a[i], b[0], c[0]);
                 else if (MODE == 3) a[i] = fma(b[i], c[i], a[i]);
-                else a[i] = fma(b[i], c[0], a[i]);
+                else if (MODE == 4) a[i] = fma(b[i], c[0], a[i]);
+                else if (MODE == 5) a[i] = fma(b[i], b[i], a[i]);
+                else a[i] = fma(b[i], 0.999999, a[i]);
             }
         }
     }
@@ -81,6 +85,8 @@ int main()
         run<1>("1 register + 2 immediates", d, in, ghz, ctas);
         run<2>("1 register + 2 shared registers", d, in, ghz, ctas);
         run<4>("2 registers + 1 shared register", d, in, ghz, ctas);
+        run<6>("2 registers + 1 immediate", d, in, ghz, ctas);
+        run<5>("2 registers, one in two slots", d, in, ghz, ctas);
         run<3>("3 distinct registers", d, in, ghz, ctas);
     }
     cudaError_t e = cudaDeviceSynchronize();
