@@ -564,6 +564,7 @@ def run_ours(args):
     near_flop = 20.0 * 1296 * stats["near_leaves"]
     dom = ("far_tiles", far_flop, far_ms) if far_ms >= near_ms else ("near_leaves", near_flop, near_ms)
     achieved = dom[1] / (dom[2] * 1e-3) / 1e12 if dom[2] > 0 else 0.0
+    pipe = kernel_pipe(dom[0], cfg)
     # ---- matvec (HBM) and preconditioner applies, L2 flushed between launches
     ctx.reset_timers()
     import ctypes as C
@@ -747,10 +748,16 @@ def run_ours(args):
                                          "profiles/r02_traffic.json; the kernel is FP64-bound, so the bytes only "
                                          "show it re-reads nothing (leaf list, geometry and W updates)",
                          "peak_source": "DFMA loop measured by bench.py on this GPU (MEASURED_PEAKS.json has no fp64)",
-                         "flop_convention": "20 flop per tensor-rule kernel evaluation (SURVEY.md §8d); an "
-                                            "evaluation issues 8 FP64 instructions on flat panels, 9 otherwise, so "
-                                            "frac can exceed the FP64-pipe activity (pipe below)",
-                         "pipe": kernel_pipe(dom[0], cfg),
+                         "flop_convention": "20 flop per tensor-rule kernel evaluation (SURVEY.md §8d), fixed "
+                                            "regardless of the implementation; an evaluation issues 7 FP64 "
+                                            "instructions (14 flop) on flat panels, 8 otherwise, so frac exceeds the "
+                                            "FP64-pipe activity and can exceed 1: frac_issued counts the issued "
+                                            "instructions (2 flop each) against the same DFMA peak",
+                         "pipe": pipe,
+                         "achieved_issued": achieved * 2.0 * pipe["fp64_instr_per_eval"] / 20.0
+                         if pipe and pipe.get("fp64_instr_per_eval") else None,
+                         "frac_issued": achieved * 2.0 * pipe["fp64_instr_per_eval"] / 20.0 / fp64_peak
+                         if pipe and pipe.get("fp64_instr_per_eval") and fp64_peak else None,
                          "ms_per_step": dom[2], "launches_per_step": launches_per_step[dom[0]],
                          "achieved_other": {"kernel": ("near_leaves" if dom[0] == "far_tiles" else "far_tiles"),
                                             "tflops": (near_flop / (near_ms * 1e-3) / 1e12 if dom[0] == "far_tiles"

@@ -56,7 +56,7 @@ __device__ __forceinline__ double rsqrt_acc(double r2s, double acc)
 // constants enter as immediates of a DADD and a DFMA (0.375 above lives in a register: one
 // operand read more per evaluation); the caller multiplies its sum by kRsqrtAccScale once
 #ifndef RSQRT_ACC_SCALED
-#define RSQRT_ACC_SCALED 1
+#define RSQRT_ACC_SCALED 3
 #endif
 #if RSQRT_ACC_SCALED
 constexpr double kRsqrtAccScale = 0.375;
@@ -64,9 +64,22 @@ __device__ __forceinline__ double rsqrt_acc_s(double r2s, double acc)
 {
     double y;
     asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(r2s));
+#if RSQRT_ACC_SCALED == 3
+    // 8/3 + 4e/3 + e^2 = (e + 2/3)^2 + 20/9 with d = e + 2/3 = 5/3 - r2s y^2 formed by the
+    // residual's own FMA: four FP64 instructions after the seed (d carries an absolute error
+    // of 2^-54, i.e. 2^-55 relative in the polynomial: below its own rounding)
+    const double d = fma(-r2s, y * y, 5.0 / 3.0);
+    return fma(y, fma(d, d, 20.0 / 9.0), acc);
+#elif RSQRT_ACC_SCALED == 2
+    // 8/3 + 4e/3 + e^2 = (e + 2/3)^2 + 20/9: the square reads one register
+    const double e = fma(-r2s, y * y, 1.0);
+    const double d = e + 2.0 / 3.0;
+    return fma(y, fma(d, d, 20.0 / 9.0), acc);
+#else
     const double e = fma(-r2s, y * y, 1.0);
     const double c = e + 4.0 / 3.0;
     return fma(y, fma(e, c, 8.0 / 3.0), acc);
+#endif
 }
 #else
 constexpr double kRsqrtAccScale = 1.0;

@@ -1,7 +1,7 @@
-"""Summaries for profiles/ from the outputs of tools/profile_r02b.sh and the per-config bench
+"""Summaries for profiles/ from the outputs of tools/profile_r02b.sh (the same command list serves the later capture sets) and the per-config bench
 runs brought back in gpurun_out/ (run here, on the CPU side):
 
-    python tools/write_r02b_profiles.py
+    python tools/write_r02b_profiles.py [tag]   (default tag r02c)
 """
 import csv
 import json
@@ -12,6 +12,7 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 G = os.path.join(ROOT, "gpurun_out")
 P = os.path.join(ROOT, "profiles")
+TAG = sys.argv[1] if len(sys.argv) > 1 else "r02c"  # the capture set's name in profiles/
 
 
 def last_json(path):
@@ -23,8 +24,8 @@ def main():
     for c in (1, 2, 3, 4, 5):
         src = os.path.join(G, "final_bench_cfg5.json" if c == 5 else f"bench_cfg{c}.json")
         if os.path.exists(src):
-            json.dump(last_json(src), open(os.path.join(P, f"r02b_bench_cfg{c}.json"), "w"), indent=1)
-    d5 = json.load(open(os.path.join(P, "r02b_bench_cfg5.json")))
+            json.dump(last_json(src), open(os.path.join(P, f"{TAG}_bench_cfg{c}.json"), "w"), indent=1)
+    d5 = json.load(open(os.path.join(P, f"{TAG}_bench_cfg5.json")))
     stats = d5["assembly_stats"]
     evals = {"far": stats["far_pairs"] * 256.0, "near": stats["near_leaves"] * 1296.0}
     # config-5 far/near metrics
@@ -44,8 +45,8 @@ def main():
              ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum", "shared-load bank conflicts"),
              ("launch__registers_per_thread", "registers/thread"), ("launch__grid_size", "grid"),
              ("launch__block_size", "block")]
-    out = ["# Config-5 assembly kernels — ncu metrics capture (r02b final: flat-plane evaluation, two-stage "
-           "contraction, padded leaf staging)", "",
+    out = [f"# Config-5 assembly kernels — ncu metrics capture ({TAG}: flat-plane evaluation, two-stage contraction, "
+           "padded leaf staging, 7-instruction evaluation)", "",
            "`ncu --metrics <list below> --clock-control none -k regex:'k_far_tiles|k_near_leaves' --launch-skip 2 "
            "-c 2 --csv python tools/asm_once.py 5` (`tools/profile_r02b.sh`; the second assembly's launches). ncu "
            "serialises launches and starts them cold; the pipe utilisations, instruction counts and DRAM bytes are "
@@ -56,10 +57,10 @@ def main():
     ipe = {k: float(m[k]["smsp__inst_executed.sum"][0]) * 32 / evals[k] for k in ("far", "near")}
     out += ["", f"Thread instructions per kernel evaluation: far tiles {ipe['far']:.2f}, near leaves {ipe['near']:.2f} "
             f"(evaluations: far {evals['far']:.4g} = 256 per far pair, near {evals['near']:.4g} = 1296 per leaf). "
-            "The flat evaluation is 8 FP64 instructions + MUFU.RSQ64H + its zero low word + a share of the "
+            "The flat evaluation is 7 FP64 instructions + MUFU.RSQ64H + its zero low word + a share of the "
             "shared-memory loads and loop overhead; the rest is per-tile / per-leaf setup, classification, the "
             "contraction and the flush."]
-    open(os.path.join(P, "r02b_ncu_cfg5_asm.md"), "w").write("\n".join(out) + "\n")
+    open(os.path.join(P, f"{TAG}_ncu_cfg5_asm.md"), "w").write("\n".join(out) + "\n")
     # traffic / pipe json
     tj = os.path.join(P, "r02_traffic.json")
     t = json.load(open(tj))
@@ -69,23 +70,23 @@ def main():
                                                     float(m[k]["dram__bytes_write.sum"][0]))],
                         "fp64_pipe_active": round(float(
                             m[k]["sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"][0]) / 100, 4),
-                        "fp64_instr_per_eval": 8, "source": "profiles/r02b_ncu_cfg5_asm.md"}
+                        "fp64_instr_per_eval": 7, "source": "profiles/" + TAG + "_ncu_cfg5_asm.md"}
     json.dump(t, open(tj, "w"), indent=1)
     # launch list, config-2 full capture, SASS
     tools = os.path.join(ROOT, "tools")
     subprocess.run([sys.executable, os.path.join(tools, "ncu_summary.py"), "launches",
-                    os.path.join(G, "launches_cfg5.csv"), os.path.join(P, "r02b_launches_bench_cfg5.md")],
+                    os.path.join(G, "launches_cfg5.csv"), os.path.join(P, f"{TAG}_launches_bench_cfg5.md")],
                    check=True, capture_output=True)
-    lp = os.path.join(P, "r02b_launches_bench_cfg5.md")
+    lp = os.path.join(P, f"{TAG}_launches_bench_cfg5.md")
     lines = open(lp).read().splitlines()
     lines[0] = ("# ncu launch list summary: `SBG_PCG_GRAPH=0 ncu --metrics gpu__time_duration.sum --clock-control "
                 "none python bench.py --steps 2 --warmup 1 --no-cpu-baseline --tts-runs 1 --dl-grid 0` (config 5, "
-                "r02b final code; the PCG loop on the stream so its kernels are listed)")
+                "final r02 code; the PCG loop on the stream so its kernels are listed)")
     open(lp, "w").write("\n".join(lines) + "\n")
     subprocess.run([sys.executable, os.path.join(tools, "ncu_summary.py"), "report",
-                    os.path.join(G, "asm2_full.ncu-rep"), os.path.join(P, "r02b_ncu_full_cfg2_asm.md")],
+                    os.path.join(G, "asm2_full.ncu-rep"), os.path.join(P, f"{TAG}_ncu_full_cfg2_asm.md")],
                    check=True, capture_output=True)
-    with open(os.path.join(P, "r02b_sass.md"), "w") as f:
+    with open(os.path.join(P, f"{TAG}_sass.md"), "w") as f:
         subprocess.run([sys.executable, os.path.join(tools, "sass_summary.py")], check=True, stdout=f,
                        stderr=subprocess.DEVNULL)
     print("written")
