@@ -1082,12 +1082,12 @@ __device__ __forceinline__ void sauter_stage(const double* __restrict__ R, int c
 #pragma unroll
         for (int u = 0; u < 4; ++u) r2[u] = sauter_r2<CLS, FLAT>(R + ST * (i + u), g);
         // the table's coefficients carry 1 / w^2 in r^2: rsqrt of it is w / r (rsqrt_acc)
-        acc0 = rsqrt_acc(r2[0], acc0);
-        acc1 = rsqrt_acc(r2[1], acc1);
-        acc2 = rsqrt_acc(r2[2], acc2);
-        acc3 = rsqrt_acc(r2[3], acc3);
+        acc0 = rsqrt_acc_s(r2[0], acc0);
+        acc1 = rsqrt_acc_s(r2[1], acc1);
+        acc2 = rsqrt_acc_s(r2[2], acc2);
+        acc3 = rsqrt_acc_s(r2[3], acc3);
     }
-    for (; i < cnt; ++i) acc0 = rsqrt_acc(sauter_r2<CLS, FLAT>(R + ST * i, g), acc0);
+    for (; i < cnt; ++i) acc0 = rsqrt_acc_s(sauter_r2<CLS, FLAT>(R + ST * i, g), acc0);
 }
 
 template <int CLS>
@@ -1162,7 +1162,8 @@ __global__ void __launch_bounds__(SAUTER_THREADS)
                 sauter_stage<CLS, false, ST>(R, cnt, g, acc0, acc1, acc2, acc3);
         }
     }
-    if (active) part[(size_t)blockIdx.y * npairs + p] = (acc0 + acc1) + (acc2 + acc3);
+    // (rsqrt_acc_s accumulates with the factor 8/3)
+    if (active) part[(size_t)blockIdx.y * npairs + p] = ((acc0 + acc1) + (acc2 + acc3)) * kRsqrtAccScale;
 }
 
 // launch of one class: chunk count chosen (sauter_chunking) so the grid fills whole waves

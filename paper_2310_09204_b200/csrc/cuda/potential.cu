@@ -167,8 +167,7 @@ __device__ __forceinline__ double rsqrt_refined(double r2)
 {
     double y;
     asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(r2));
-    const double h = r2 * y;
-    const double e = fma(-h, y, 1.0);
+    const double e = fma(-r2, y * y, 1.0);  // the seed's square is exact (kernels.cuh rsqrt_acc)
     return fma(y, e * fma(0.375, e, 0.5), y);
 }
 
